@@ -1,0 +1,209 @@
+/* apl.h — C-ABI of the B200 layout-conversion runtime ("autoplan layout").
+ *
+ * Plain C: fixed-size POD structs, pointers and sizes, int status codes.
+ * No exceptions cross this boundary and no CUDA / NCCL / torch types appear
+ * in it (streams travel as `void*` = cudaStream_t).
+ *
+ * What each group replaces in the reference (/root/reference/proj):
+ *   spec / path functions  -> ShardingSpec::parse / to_string / valid_for
+ *                             (src/layout.cpp:79-160), one_step_transforms
+ *                             (layout.cpp:162-221), find_transform_path
+ *                             (layout.cpp:253-316), conversion_cost
+ *                             (layout.cpp:318-329), PathCache (layout.cpp:331-362),
+ *                             collective_cost (src/cluster.cpp:374-400).
+ *   runtime functions      -> NEW. The reference only *records* conversions
+ *                             (planner.cpp:218-352 CommInsertion / kCommunication
+ *                             nodes with name/mesh_axes/axes/bytes attrs); these
+ *                             execute them on device data: shard-slice, all-gather,
+ *                             all-to-all (CollectiveKind, include/autoplan/
+ *                             cluster.hpp:46-52) and the partial-sum all-reduce of
+ *                             sharded matmul strategies (intraop.cpp:141-234,
+ *                             544-551).
+ *
+ * Status codes mirror the reference exception hierarchy (errors.hpp:25-108).
+ *
+ * Data placement: a device at mesh coordinate c holds,
+ * for every tensor dim d sharded over axes (a_1..a_m), block index
+ * s_d = mixed radix of (c_{a_1}, .., c_{a_m}) with a_1 most significant,
+ * stored dense row-major. Mesh coordinates map to device index row-major.
+ */
+#ifndef APL_H_
+#define APL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APL_MAX_DIMS 8  /* tensor rank limit */
+#define APL_MAX_MESH 8  /* mesh rank limit */
+#define APL_MAX_LOCAL 64 /* simulated devices per local mesh */
+
+typedef enum {
+  APL_OK = 0,
+  APL_ERR_SCHEMA = 1,     /* SchemaError: malformed spec / mesh text */
+  APL_ERR_AXIS = 2,       /* AxisError: mesh axis out of range / reused */
+  APL_ERR_SHAPE = 3,      /* ShapeError: spec invalid for tensor/mesh */
+  APL_ERR_RANK = 4,       /* RankMismatchError */
+  APL_ERR_INFEASIBLE = 5, /* InfeasibleError: no conversion path */
+  APL_ERR_CUDA = 6,       /* CUDA runtime failure / no device / no kernel image */
+  APL_ERR_NCCL = 7,       /* NCCL failure */
+  APL_ERR_ARG = 8,        /* bad argument (null, capacity too small, limits) */
+  APL_ERR_PLAN = 9,       /* any other PlanError */
+  APL_ERR_INTERNAL = 10   /* anything else */
+} apl_status;
+
+/* Same order as autoplan::CollectiveKind (cluster.hpp:46-52). */
+typedef enum {
+  APL_ALL_GATHER = 0,
+  APL_ALL_REDUCE = 1,
+  APL_REDUCE_SCATTER = 2,
+  APL_ALL_TO_ALL = 3,
+  APL_SHARD_SLICE = 4
+} apl_kind;
+
+typedef enum { APL_F32 = 0, APL_BF16 = 1, APL_F16 = 2 } apl_dtype;
+
+/* Execution flags for apl_run_path. */
+#define APL_STEPWISE 0u   /* run the reference's steps one by one */
+#define APL_FUSE_CHAIN 1u /* collapse the whole chain into one exchange pass */
+
+typedef struct {
+  int32_t rank;                            /* tensor rank */
+  int32_t mesh_rank;
+  int32_t naxes[APL_MAX_DIMS];             /* axes per dim (0 = replicated) */
+  int32_t axes[APL_MAX_DIMS][APL_MAX_MESH];
+} apl_spec;
+
+typedef struct {
+  int32_t rank;
+  int32_t dtype_bytes; /* 1, 2, 4 or 8 */
+  int64_t shape[APL_MAX_DIMS];
+} apl_meta;
+
+typedef struct {
+  int32_t kind; /* apl_kind */
+  int32_t tensor_dim;
+  int32_t target_dim; /* all-to-all destination dim, -1 otherwise */
+  int32_t mesh_axis;
+  apl_spec result;
+} apl_step;
+
+/* Per-axis alpha-beta model; NULL alpha/beta arrays select the reference's
+ * DeviceMesh::uniform defaults (alpha 1e-5 s, beta_inv 1e-9 s/B). */
+typedef struct {
+  int32_t ndim;
+  int64_t shape[APL_MAX_MESH];
+  double alpha[APL_MAX_MESH];
+  double beta_inv[APL_MAX_MESH];
+} apl_mesh_desc;
+
+/* One exchange piece of a conversion: the box `ext` at `src_lo` of the
+ * sender's source shard lands at `dst_lo` of the receiver's target shard
+ * (local element coordinates). */
+typedef struct {
+  int32_t sender;   /* mesh device index (row-major) */
+  int32_t receiver; /* mesh device index (row-major) */
+  int64_t src_lo[APL_MAX_DIMS];
+  int64_t dst_lo[APL_MAX_DIMS];
+  int64_t ext[APL_MAX_DIMS];
+} apl_piece;
+
+/* ---- diagnostics ---------------------------------------------------- */
+int apl_version(void); /* 100 * major + minor */
+const char* apl_last_error(void); /* thread-local message of the last failure */
+
+/* ---- spec algebra + path search (host only; no GPU needed) ------------ */
+int apl_mesh_desc_uniform(const int64_t* shape, int ndim, apl_mesh_desc* out);
+int apl_parse_mesh_shape(const char* text, int64_t* shape, int cap, int* ndim);
+int apl_spec_parse(const char* text, int mesh_rank, apl_spec* out);
+int apl_spec_to_string(const apl_spec* spec, char* buf, size_t cap);
+int apl_spec_valid(const apl_spec* spec, const apl_mesh_desc* mesh, const apl_meta* meta,
+                   int* valid);
+int apl_spec_per_device_bytes(const apl_spec* spec, const apl_mesh_desc* mesh,
+                              const apl_meta* meta, int64_t* bytes);
+int apl_one_step_transforms(const apl_spec* spec, const apl_mesh_desc* mesh,
+                            const apl_meta* meta, apl_step* out, int cap, int* count);
+int apl_dim_diff(const int32_t* src_axes, int nsrc, const int32_t* tgt_axes, int ntgt,
+                 const double* weights4 /* NULL = defaults {2,1,2,2} */, double* out);
+int apl_heuristic_diff(const apl_spec* src, const apl_spec* tgt,
+                       const double* weights4, double* out);
+int apl_find_transform_path(const apl_mesh_desc* mesh, const apl_spec* src,
+                            const apl_spec* tgt, const apl_meta* meta, apl_step* steps,
+                            int cap, int* nsteps, double* comm_cost_s);
+int apl_collective_cost(const apl_mesh_desc* mesh, const int32_t* axes, int naxes,
+                        int kind, double bytes, double* out);
+
+/* PathCache (reference layout.hpp:120-132). Thread safe. */
+typedef struct apl_path_cache apl_path_cache;
+int apl_path_cache_create(apl_path_cache** out);
+int apl_path_cache_destroy(apl_path_cache* cache);
+int apl_path_cache_get(apl_path_cache* cache, const apl_mesh_desc* mesh, const apl_spec* src,
+                       const apl_spec* tgt, const apl_meta* meta, apl_step* steps, int cap,
+                       int* nsteps, double* comm_cost_s);
+int apl_path_cache_stats(const apl_path_cache* cache, size_t* searches, size_t* size);
+int apl_path_cache_clear(apl_path_cache* cache);
+
+/* Exchange plan of a direct src->tgt redistribution (host only). role 0:
+ * pieces `device` receives; role 1: pieces `device` sends. Each target
+ * element is sourced exactly once; the sender of a piece is the source
+ * replica that agrees with the receiver on every axis the source spec does
+ * not use, so traffic stays inside the source's axis groups and a device
+ * never receives bytes it already holds. */
+int apl_plan_pieces(const apl_mesh_desc* mesh, const apl_spec* src, const apl_spec* tgt,
+                    const apl_meta* meta, int device, int role, apl_piece* out, int cap,
+                    int* count);
+
+/* ---- runtime (CUDA) --------------------------------------------------- */
+typedef struct apl_mesh apl_mesh;
+
+/* Simulated mesh: every mesh device is a separate buffer on one GPU (the
+ * 1-GPU parity / HBM-roofline mode). Buffer arrays passed to the run
+ * functions then hold num_devices pointers in row-major device order. */
+int apl_mesh_create_local(const apl_mesh_desc* mesh, int cuda_device, apl_mesh** out);
+
+/* Distributed mesh: one process per GPU. `nccl_id` is 128 bytes made by
+ * apl_nccl_unique_id on rank 0 and broadcast by the caller. Buffer arrays
+ * then hold exactly one pointer (this rank's shard). Builds one NCCL
+ * sub-communicator per non-empty mesh-axis subset (ncclCommSplit, color =
+ * coordinates off the subset, key = coordinates on it). */
+int apl_nccl_unique_id(uint8_t* out128);
+int apl_mesh_create_nccl(const apl_mesh_desc* mesh, int rank, const uint8_t* nccl_id,
+                         int cuda_device, apl_mesh** out);
+int apl_mesh_destroy(apl_mesh* mesh);
+int apl_mesh_info(const apl_mesh* mesh, int* num_devices, int* first_local, int* num_local,
+                  int* is_distributed);
+
+/* Workspace needed by apl_run_path / apl_run_step for these arguments. */
+int apl_path_workspace_bytes(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                             const apl_step* steps, int nsteps, const apl_meta* meta,
+                             unsigned flags, size_t* bytes);
+
+/* Execute one reference TransformStep: out = step applied to in. */
+int apl_run_step(apl_mesh* mesh, const apl_spec* src, const apl_step* step,
+                 const apl_meta* meta, const void* const* in, void* const* out, void* ws,
+                 size_t ws_bytes, void* stream);
+
+/* Execute a TransformPath: stepwise, or collapsed into one exchange when
+ * flags has APL_FUSE_CHAIN. Stream ordered; in/out must not alias. */
+int apl_run_path(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                 const apl_step* steps, int nsteps, const apl_meta* meta,
+                 const void* const* in, void* const* out, void* ws, size_t ws_bytes,
+                 unsigned flags, void* stream);
+
+/* Sum partial results over the mesh axes `axes` (partial_sum strategies,
+ * intraop.cpp:544-551; planner.cpp:263-282). In place; every member of an
+ * axis group ends with identical bytes. */
+int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* bufs,
+                   size_t count, int dtype, void* stream);
+
+/* Kernel launches this process issued through the library (evidence). */
+int apl_launch_count(uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* APL_H_ */

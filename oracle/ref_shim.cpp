@@ -1,0 +1,195 @@
+// ref_shim.cpp — C entry points over the REFERENCE autoplan library
+// (test infrastructure only; see oracle/Makefile).
+//
+// Linked against the reference's own translation units compiled straight
+// from /root/reference/proj/src (never copied into this repo) into
+// oracle/_ref/libautoplan_ref.so. Used by tests/ to check the drop-in host
+// API step-for-step against the real reference, by tests/golden/make_golden.py
+// to write the committed golden paths, and by bench.py --impl reference to
+// time the reference planner on the GPU box's host.
+//
+// Calls wrapped (reference file:line):
+//   ShardingSpec::parse / to_string / valid_for  src/layout.cpp:79-160
+//   one_step_transforms                          src/layout.cpp:162-221
+//   dim_diff / heuristic_diff                    src/layout.cpp:223-251
+//   find_transform_path / conversion_cost        src/layout.cpp:253-329
+//   PathCache::get                               src/layout.cpp:331-346
+//   collective_cost                              src/cluster.cpp:374-400
+//   testutil::all_valid_specs / bfs_min_steps /
+//   replay_path_error                            tests/helpers.hpp:245-363
+//   matmul strategy catalog (generate_strategies) src/intraop.cpp:141-234,497-555,719-767
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "autoplan/cluster.hpp"
+#include "autoplan/errors.hpp"
+#include "autoplan/graph_ir.hpp"
+#include "autoplan/intraop.hpp"
+#include "autoplan/layout.hpp"
+#include "helpers.hpp"
+
+using namespace autoplan;
+
+namespace {
+
+int code_of(const std::exception& e) {
+  if (dynamic_cast<const SchemaError*>(&e)) return 1;
+  if (dynamic_cast<const AxisError*>(&e)) return 2;
+  if (dynamic_cast<const ShapeError*>(&e)) return 3;
+  if (dynamic_cast<const RankMismatchError*>(&e)) return 4;
+  if (dynamic_cast<const InfeasibleError*>(&e)) return 5;
+  if (dynamic_cast<const PlanError*>(&e)) return 9;
+  return 10;
+}
+
+int put(const std::string& s, char* out, size_t cap) {
+  if (s.size() + 1 > cap) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+DeviceMesh mesh_of(const int64_t* m, int mr) {
+  return DeviceMesh::uniform(std::vector<int64_t>(m, m + mr), 1e-5, 1e-9, 1e12);
+}
+
+TensorMeta meta_of(const int64_t* shape, int rank, int dtype_bytes) {
+  TensorMeta t;
+  t.shape.assign(shape, shape + rank);
+  t.dtype_bytes = dtype_bytes;
+  return t;
+}
+
+std::string render_path(const TransformPath& p) {
+  std::ostringstream os;
+  for (const TransformStep& s : p.steps)
+    os << static_cast<int>(s.kind) << " " << s.tensor_dim << " " << s.target_dim << " "
+       << s.mesh_axis << " " << s.result.to_string() << "\n";
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "cost %.17g\n", p.comm_cost_s);
+  os << buf;
+  return os.str();
+}
+
+}  // namespace
+
+extern "C" {
+
+// Path as text: one "kind tensor_dim target_dim mesh_axis result" line per
+// step, then "cost <%.17g>". Returns 0, a PlanError class code, or -1
+// (buffer too small).
+int ref_find_path(const int64_t* mesh, int mr, const int64_t* shape, int rank, int eb,
+                  const char* src, const char* tgt, char* out, size_t cap) {
+  try {
+    DeviceMesh m = mesh_of(mesh, mr);
+    TensorMeta t = meta_of(shape, rank, eb);
+    TransformPath p = find_transform_path(ShardingSpec::parse(src, mr), ShardingSpec::parse(tgt, mr), m, t);
+    conversion_cost(p, m, t);
+    return put(render_path(p), out, cap);
+  } catch (const std::exception& e) {
+    put(e.what(), out, cap);
+    return code_of(e);
+  }
+}
+
+int ref_one_step(const int64_t* mesh, int mr, const int64_t* shape, int rank, int eb,
+                 const char* spec, char* out, size_t cap) {
+  try {
+    auto r = one_step_transforms(ShardingSpec::parse(spec, mr), mesh_of(mesh, mr), meta_of(shape, rank, eb));
+    std::ostringstream os;
+    for (auto& [next, s] : r)
+      os << static_cast<int>(s.kind) << " " << s.tensor_dim << " " << s.target_dim << " "
+         << s.mesh_axis << " " << next.to_string() << "\n";
+    return put(os.str(), out, cap);
+  } catch (const std::exception& e) {
+    put(e.what(), out, cap);
+    return code_of(e);
+  }
+}
+
+int ref_all_valid_specs(const int64_t* mesh, int mr, const int64_t* shape, int rank, int eb,
+                        char* out, size_t cap) {
+  try {
+    std::ostringstream os;
+    for (const ShardingSpec& s : testutil::all_valid_specs(meta_of(shape, rank, eb), mesh_of(mesh, mr)))
+      os << s.to_string() << "\n";
+    return put(os.str(), out, cap);
+  } catch (const std::exception& e) {
+    put(e.what(), out, cap);
+    return code_of(e);
+  }
+}
+
+int ref_bfs_min_steps(const int64_t* mesh, int mr, const int64_t* shape, int rank, int eb,
+                      const char* src, const char* tgt) {
+  try {
+    return testutil::bfs_min_steps(ShardingSpec::parse(src, mr), ShardingSpec::parse(tgt, mr),
+                                   mesh_of(mesh, mr), meta_of(shape, rank, eb));
+  } catch (const std::exception&) {
+    return -2;
+  }
+}
+
+int ref_dim_diff(const int* a, int na, const int* b, int nb, double* out) {
+  DimSpec x, y;
+  x.axes.assign(a, a + na);
+  y.axes.assign(b, b + nb);
+  *out = dim_diff(x, y);
+  return 0;
+}
+
+int ref_heuristic_diff(int mr, const char* a, const char* b, double* out) {
+  try {
+    *out = heuristic_diff(ShardingSpec::parse(a, mr), ShardingSpec::parse(b, mr));
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+int ref_collective_cost(const int64_t* mesh, int mr, const int* axes, int naxes, int kind,
+                        double bytes, double* out) {
+  try {
+    *out = collective_cost(mesh_of(mesh, mr), std::vector<int>(axes, axes + naxes),
+                           static_cast<CollectiveKind>(kind), bytes);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+int ref_spec_valid(const int64_t* mesh, int mr, const int64_t* shape, int rank, int eb,
+                   const char* spec) {
+  try {
+    return ShardingSpec::parse(spec, mr).valid_for(meta_of(shape, rank, eb), mesh_of(mesh, mr)) ? 1 : 0;
+  } catch (const std::exception& e) {
+    return -code_of(e);
+  }
+}
+
+// Mean seconds per uncached find_transform_path + conversion_cost call
+// (`hits` = 0) or per cached PathCache::get (`hits` = 1), over `iters` calls.
+double ref_time_paths(const int64_t* mesh, int mr, const int64_t* shape, int rank, int eb,
+                      const char* src, const char* tgt, int iters, int hits) {
+  DeviceMesh m = mesh_of(mesh, mr);
+  TensorMeta t = meta_of(shape, rank, eb);
+  ShardingSpec a = ShardingSpec::parse(src, mr), b = ShardingSpec::parse(tgt, mr);
+  PathCache cache;
+  cache.get(a, b, m, t);
+  volatile double sink = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < iters; ++i) {
+    if (hits) {
+      sink = sink + cache.get(a, b, m, t).comm_cost_s;
+    } else {
+      TransformPath p = find_transform_path(a, b, m, t);
+      sink = sink + conversion_cost(p, m, t);
+    }
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double>(t1 - t0).count() / iters;
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+"""ctypes declaration of the C-ABI in include/apl.h.
+
+This module only loads libapl.so and declares its signatures; it never
+substitutes anything for a missing library: if libapl.so is absent or was
+built without sm_100a kernels the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+MAX_DIMS = 8
+MAX_MESH = 8
+MAX_LOCAL = 64
+
+OK, ERR_SCHEMA, ERR_AXIS, ERR_SHAPE, ERR_RANK, ERR_INFEASIBLE, ERR_CUDA, ERR_NCCL, ERR_ARG, \
+    ERR_PLAN, ERR_INTERNAL = range(11)
+FUSE_CHAIN = 1
+STEPWISE = 0
+F32, BF16, F16 = 0, 1, 2
+
+
+class Spec(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("mesh_rank", C.c_int32),
+                ("naxes", C.c_int32 * MAX_DIMS), ("axes", (C.c_int32 * MAX_MESH) * MAX_DIMS)]
+
+
+class Meta(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("dtype_bytes", C.c_int32), ("shape", C.c_int64 * MAX_DIMS)]
+
+
+class Step(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("tensor_dim", C.c_int32), ("target_dim", C.c_int32),
+                ("mesh_axis", C.c_int32), ("result", Spec)]
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("ndim", C.c_int32), ("shape", C.c_int64 * MAX_MESH),
+                ("alpha", C.c_double * MAX_MESH), ("beta_inv", C.c_double * MAX_MESH)]
+
+
+class PieceC(C.Structure):
+    _fields_ = [("sender", C.c_int32), ("receiver", C.c_int32),
+                ("src_lo", C.c_int64 * MAX_DIMS), ("dst_lo", C.c_int64 * MAX_DIMS),
+                ("ext", C.c_int64 * MAX_DIMS)]
+
+
+LIB_PATH = Path(__file__).resolve().parent / "libapl.so"
+_lib = None
+
+P = C.POINTER
+_SIGS = {
+    "apl_version": (C.c_int, []),
+    "apl_last_error": (C.c_char_p, []),
+    "apl_mesh_desc_uniform": (C.c_int, [P(C.c_int64), C.c_int, P(MeshDesc)]),
+    "apl_parse_mesh_shape": (C.c_int, [C.c_char_p, P(C.c_int64), C.c_int, P(C.c_int)]),
+    "apl_spec_parse": (C.c_int, [C.c_char_p, C.c_int, P(Spec)]),
+    "apl_spec_to_string": (C.c_int, [P(Spec), C.c_char_p, C.c_size_t]),
+    "apl_spec_valid": (C.c_int, [P(Spec), P(MeshDesc), P(Meta), P(C.c_int)]),
+    "apl_spec_per_device_bytes": (C.c_int, [P(Spec), P(MeshDesc), P(Meta), P(C.c_int64)]),
+    "apl_one_step_transforms": (C.c_int, [P(Spec), P(MeshDesc), P(Meta), P(Step), C.c_int,
+                                          P(C.c_int)]),
+    "apl_dim_diff": (C.c_int, [P(C.c_int32), C.c_int, P(C.c_int32), C.c_int, P(C.c_double),
+                               P(C.c_double)]),
+    "apl_heuristic_diff": (C.c_int, [P(Spec), P(Spec), P(C.c_double), P(C.c_double)]),
+    "apl_find_transform_path": (C.c_int, [P(MeshDesc), P(Spec), P(Spec), P(Meta), P(Step),
+                                          C.c_int, P(C.c_int), P(C.c_double)]),
+    "apl_collective_cost": (C.c_int, [P(MeshDesc), P(C.c_int32), C.c_int, C.c_int, C.c_double,
+                                      P(C.c_double)]),
+    "apl_path_cache_create": (C.c_int, [P(C.c_void_p)]),
+    "apl_path_cache_destroy": (C.c_int, [C.c_void_p]),
+    "apl_path_cache_get": (C.c_int, [C.c_void_p, P(MeshDesc), P(Spec), P(Spec), P(Meta),
+                                     P(Step), C.c_int, P(C.c_int), P(C.c_double)]),
+    "apl_path_cache_stats": (C.c_int, [C.c_void_p, P(C.c_size_t), P(C.c_size_t)]),
+    "apl_path_cache_clear": (C.c_int, [C.c_void_p]),
+    "apl_plan_pieces": (C.c_int, [P(MeshDesc), P(Spec), P(Spec), P(Meta), C.c_int, C.c_int,
+                                  P(PieceC), C.c_int, P(C.c_int)]),
+    "apl_mesh_create_local": (C.c_int, [P(MeshDesc), C.c_int, P(C.c_void_p)]),
+    "apl_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
+    "apl_mesh_create_nccl": (C.c_int, [P(MeshDesc), C.c_int, P(C.c_uint8), C.c_int,
+                                       P(C.c_void_p)]),
+    "apl_mesh_destroy": (C.c_int, [C.c_void_p]),
+    "apl_mesh_info": (C.c_int, [C.c_void_p, P(C.c_int), P(C.c_int), P(C.c_int), P(C.c_int)]),
+    "apl_path_workspace_bytes": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Step), C.c_int,
+                                           P(Meta), C.c_uint, P(C.c_size_t)]),
+    "apl_run_step": (C.c_int, [C.c_void_p, P(Spec), P(Step), P(Meta), P(C.c_void_p),
+                               P(C.c_void_p), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "apl_run_path": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Step), C.c_int, P(Meta),
+                               P(C.c_void_p), P(C.c_void_p), C.c_void_p, C.c_size_t, C.c_uint,
+                               C.c_void_p]),
+    "apl_all_reduce": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_int, P(C.c_void_p), C.c_size_t,
+                                 C.c_int, C.c_void_p]),
+    "apl_launch_count": (C.c_int, [P(C.c_uint64)]),
+}
+
+# Symbols every build must export (tests check the .so against include/apl.h).
+EXPORTED = tuple(_SIGS)
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build the native library first "
+                "(python -c 'import __graft_entry__ as g; g.build()'); there is no fallback")
+        handle = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib

@@ -1,0 +1,486 @@
+// C-ABI (include/apl.h) over the autoplan host API and the device runtime.
+// Exceptions never cross: each entry point maps the PlanError hierarchy
+// (reference errors.hpp:25-108) and runtime failures onto apl_status codes.
+#include "apl.h"
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "autoplan/layout.hpp"
+#include "runtime/runtime.hpp"
+
+using autoplan::CollectiveKind;
+using autoplan::DeviceMesh;
+using autoplan::ShardingSpec;
+using autoplan::TensorMeta;
+using autoplan::TransformPath;
+using autoplan::TransformStep;
+
+struct apl_path_cache {
+  autoplan::PathCache cache;
+};
+struct apl_mesh {
+  apl::Mesh impl;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct ArgError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <typename F>
+int guarded(F&& body) {
+  try {
+    body();
+    g_last_error.clear();
+    return APL_OK;
+  } catch (const autoplan::SchemaError& e) {
+    g_last_error = e.what();
+    return APL_ERR_SCHEMA;
+  } catch (const autoplan::AxisError& e) {
+    g_last_error = e.what();
+    return APL_ERR_AXIS;
+  } catch (const autoplan::ShapeError& e) {
+    g_last_error = e.what();
+    return APL_ERR_SHAPE;
+  } catch (const autoplan::RankMismatchError& e) {
+    g_last_error = e.what();
+    return APL_ERR_RANK;
+  } catch (const autoplan::InfeasibleError& e) {
+    g_last_error = e.what();
+    return APL_ERR_INFEASIBLE;
+  } catch (const autoplan::PlanError& e) {
+    g_last_error = e.what();
+    return APL_ERR_PLAN;
+  } catch (const apl::RuntimeError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const ArgError& e) {
+    g_last_error = e.what();
+    return APL_ERR_ARG;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return APL_ERR_INTERNAL;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) throw ArgError(what);
+}
+
+ShardingSpec to_spec(const apl_spec* s) {
+  need(s != nullptr, "null spec");
+  need(s->rank >= 1 && s->rank <= APL_MAX_DIMS, "spec rank outside [1, APL_MAX_DIMS]");
+  need(s->mesh_rank >= 0 && s->mesh_rank <= APL_MAX_MESH, "spec mesh rank outside [0, APL_MAX_MESH]");
+  ShardingSpec out;
+  out.mesh_rank = s->mesh_rank;
+  out.dims.resize(static_cast<size_t>(s->rank));
+  for (int d = 0; d < s->rank; ++d) {
+    need(s->naxes[d] >= 0 && s->naxes[d] <= APL_MAX_MESH, "axis count out of range");
+    for (int i = 0; i < s->naxes[d]; ++i) out.dims[static_cast<size_t>(d)].axes.push_back(s->axes[d][i]);
+  }
+  return out;
+}
+
+void from_spec(const ShardingSpec& s, apl_spec* out) {
+  need(s.tensor_rank() <= APL_MAX_DIMS, "tensor rank above APL_MAX_DIMS");
+  std::memset(out, 0, sizeof(*out));
+  out->rank = s.tensor_rank();
+  out->mesh_rank = s.mesh_rank;
+  for (int d = 0; d < s.tensor_rank(); ++d) {
+    const auto& axes = s.dims[static_cast<size_t>(d)].axes;
+    need(axes.size() <= APL_MAX_MESH, "too many axes on one dim");
+    out->naxes[d] = static_cast<int32_t>(axes.size());
+    for (size_t i = 0; i < axes.size(); ++i) out->axes[d][i] = axes[i];
+  }
+}
+
+TensorMeta to_meta(const apl_meta* m) {
+  need(m != nullptr, "null meta");
+  need(m->rank >= 1 && m->rank <= APL_MAX_DIMS, "meta rank outside [1, APL_MAX_DIMS]");
+  need(m->dtype_bytes == 1 || m->dtype_bytes == 2 || m->dtype_bytes == 4 || m->dtype_bytes == 8,
+       "dtype_bytes must be one of {1,2,4,8}");
+  TensorMeta t;
+  t.dtype_bytes = m->dtype_bytes;
+  for (int i = 0; i < m->rank; ++i) {
+    need(m->shape[i] >= 1, "tensor extents must be positive");
+    t.shape.push_back(m->shape[i]);
+  }
+  return t;
+}
+
+DeviceMesh to_mesh(const apl_mesh_desc* m) {
+  need(m != nullptr, "null mesh");
+  need(m->ndim >= 1 && m->ndim <= APL_MAX_MESH, "mesh rank outside [1, APL_MAX_MESH]");
+  DeviceMesh mesh = DeviceMesh::uniform(std::vector<int64_t>(m->shape, m->shape + m->ndim));
+  for (int i = 0; i < m->ndim; ++i) {
+    need(m->shape[i] >= 1, "mesh extents must be positive");
+    mesh.axis_alpha[static_cast<size_t>(i)] = m->alpha[i];
+    mesh.axis_beta_inv[static_cast<size_t>(i)] = m->beta_inv[i];
+  }
+  return mesh;
+}
+
+void from_step(const TransformStep& s, apl_step* out) {
+  out->kind = static_cast<int32_t>(s.kind);
+  out->tensor_dim = s.tensor_dim;
+  out->target_dim = s.target_dim;
+  out->mesh_axis = s.mesh_axis;
+  from_spec(s.result, &out->result);
+}
+
+TransformStep to_step(const apl_step* s) {
+  need(s->kind >= 0 && s->kind <= APL_SHARD_SLICE, "bad step kind");
+  TransformStep t;
+  t.kind = static_cast<CollectiveKind>(s->kind);
+  t.tensor_dim = s->tensor_dim;
+  t.target_dim = s->target_dim;
+  t.mesh_axis = s->mesh_axis;
+  t.result = to_spec(&s->result);
+  return t;
+}
+
+std::vector<TransformStep> to_steps(const apl_step* steps, int n) {
+  need(n >= 0 && (n == 0 || steps != nullptr), "bad step array");
+  std::vector<TransformStep> out;
+  for (int i = 0; i < n; ++i) out.push_back(to_step(&steps[i]));
+  return out;
+}
+
+void emit_path(const TransformPath& p, apl_step* steps, int cap, int* nsteps, double* cost) {
+  need(nsteps != nullptr, "null nsteps");
+  *nsteps = static_cast<int>(p.steps.size());
+  if (cost) *cost = p.comm_cost_s;
+  need(static_cast<int>(p.steps.size()) <= cap, "step capacity too small");
+  for (size_t i = 0; i < p.steps.size(); ++i) from_step(p.steps[i], &steps[i]);
+}
+
+autoplan::DimDiffWeights weights_of(const double* w) {
+  autoplan::DimDiffWeights out;
+  if (w) {
+    out.all_gather = w[0];
+    out.shard = w[1];
+    out.all_to_all = w[2];
+    out.step_penalty = w[3];
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+int apl_version(void) { return 100; }
+
+const char* apl_last_error(void) { return g_last_error.c_str(); }
+
+int apl_mesh_desc_uniform(const int64_t* shape, int ndim, apl_mesh_desc* out) {
+  return guarded([&] {
+    need(shape && out && ndim >= 1 && ndim <= APL_MAX_MESH, "bad mesh shape");
+    std::memset(out, 0, sizeof(*out));
+    out->ndim = ndim;
+    for (int i = 0; i < ndim; ++i) {
+      need(shape[i] >= 1, "mesh extents must be positive");
+      out->shape[i] = shape[i];
+      out->alpha[i] = 1e-5;
+      out->beta_inv[i] = 1e-9;
+    }
+  });
+}
+
+int apl_parse_mesh_shape(const char* text, int64_t* shape, int cap, int* ndim) {
+  return guarded([&] {
+    need(text && shape && ndim, "null argument");
+    auto v = autoplan::parse_mesh_shape(text);
+    *ndim = static_cast<int>(v.size());
+    need(static_cast<int>(v.size()) <= cap, "mesh shape capacity too small");
+    for (size_t i = 0; i < v.size(); ++i) shape[i] = v[i];
+  });
+}
+
+int apl_spec_parse(const char* text, int mesh_rank, apl_spec* out) {
+  return guarded([&] {
+    need(text && out, "null argument");
+    from_spec(ShardingSpec::parse(text, mesh_rank), out);
+  });
+}
+
+int apl_spec_to_string(const apl_spec* spec, char* buf, size_t cap) {
+  return guarded([&] {
+    const std::string s = to_spec(spec).to_string();
+    need(buf && cap > s.size(), "string buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+int apl_spec_valid(const apl_spec* spec, const apl_mesh_desc* mesh, const apl_meta* meta,
+                   int* valid) {
+  return guarded([&] {
+    need(valid, "null out");
+    *valid = to_spec(spec).valid_for(to_meta(meta), to_mesh(mesh)) ? 1 : 0;
+  });
+}
+
+int apl_spec_per_device_bytes(const apl_spec* spec, const apl_mesh_desc* mesh,
+                              const apl_meta* meta, int64_t* bytes) {
+  return guarded([&] {
+    need(bytes, "null out");
+    *bytes = to_spec(spec).per_device_bytes(to_meta(meta), to_mesh(mesh));
+  });
+}
+
+int apl_one_step_transforms(const apl_spec* spec, const apl_mesh_desc* mesh,
+                            const apl_meta* meta, apl_step* out, int cap, int* count) {
+  return guarded([&] {
+    need(count, "null count");
+    auto r = autoplan::one_step_transforms(to_spec(spec), to_mesh(mesh), to_meta(meta));
+    *count = static_cast<int>(r.size());
+    need(static_cast<int>(r.size()) <= cap && (r.empty() || out), "step capacity too small");
+    for (size_t i = 0; i < r.size(); ++i) from_step(r[i].second, &out[i]);
+  });
+}
+
+int apl_dim_diff(const int32_t* src_axes, int nsrc, const int32_t* tgt_axes, int ntgt,
+                 const double* weights4, double* out) {
+  return guarded([&] {
+    need(out && nsrc >= 0 && ntgt >= 0, "bad argument");
+    autoplan::DimSpec a, b;
+    for (int i = 0; i < nsrc; ++i) a.axes.push_back(src_axes[i]);
+    for (int i = 0; i < ntgt; ++i) b.axes.push_back(tgt_axes[i]);
+    *out = autoplan::dim_diff(a, b, weights_of(weights4));
+  });
+}
+
+int apl_heuristic_diff(const apl_spec* src, const apl_spec* tgt, const double* weights4,
+                       double* out) {
+  return guarded([&] {
+    need(out, "null out");
+    *out = autoplan::heuristic_diff(to_spec(src), to_spec(tgt), weights_of(weights4));
+  });
+}
+
+int apl_find_transform_path(const apl_mesh_desc* mesh, const apl_spec* src, const apl_spec* tgt,
+                            const apl_meta* meta, apl_step* steps, int cap, int* nsteps,
+                            double* comm_cost_s) {
+  return guarded([&] {
+    const DeviceMesh m = to_mesh(mesh);
+    const TensorMeta t = to_meta(meta);
+    TransformPath p = autoplan::find_transform_path(to_spec(src), to_spec(tgt), m, t);
+    autoplan::conversion_cost(p, m, t);
+    emit_path(p, steps, cap, nsteps, comm_cost_s);
+  });
+}
+
+int apl_collective_cost(const apl_mesh_desc* mesh, const int32_t* axes, int naxes, int kind,
+                        double bytes, double* out) {
+  return guarded([&] {
+    need(out && naxes >= 0 && kind >= 0 && kind <= APL_SHARD_SLICE, "bad argument");
+    std::vector<int> ax(axes, axes + naxes);
+    *out = autoplan::collective_cost(to_mesh(mesh), ax, static_cast<CollectiveKind>(kind), bytes);
+  });
+}
+
+int apl_path_cache_create(apl_path_cache** out) {
+  return guarded([&] {
+    need(out, "null out");
+    *out = new apl_path_cache();
+  });
+}
+
+int apl_path_cache_destroy(apl_path_cache* cache) {
+  return guarded([&] { delete cache; });
+}
+
+int apl_path_cache_get(apl_path_cache* cache, const apl_mesh_desc* mesh, const apl_spec* src,
+                       const apl_spec* tgt, const apl_meta* meta, apl_step* steps, int cap,
+                       int* nsteps, double* comm_cost_s) {
+  return guarded([&] {
+    need(cache, "null cache");
+    TransformPath p = cache->cache.get(to_spec(src), to_spec(tgt), to_mesh(mesh), to_meta(meta));
+    emit_path(p, steps, cap, nsteps, comm_cost_s);
+  });
+}
+
+int apl_path_cache_stats(const apl_path_cache* cache, size_t* searches, size_t* size) {
+  return guarded([&] {
+    need(cache, "null cache");
+    if (searches) *searches = cache->cache.searches();
+    if (size) *size = cache->cache.size();
+  });
+}
+
+int apl_path_cache_clear(apl_path_cache* cache) {
+  return guarded([&] {
+    need(cache, "null cache");
+    cache->cache.clear();
+  });
+}
+
+int apl_plan_pieces(const apl_mesh_desc* mesh, const apl_spec* src, const apl_spec* tgt,
+                    const apl_meta* meta, int device, int role, apl_piece* out, int cap,
+                    int* count) {
+  return guarded([&] {
+    need(count, "null count");
+    const DeviceMesh m = to_mesh(mesh);
+    const TensorMeta t = to_meta(meta);
+    const ShardingSpec s = to_spec(src), g = to_spec(tgt);
+    if (!s.valid_for(t, m)) throw autoplan::ShapeError("source spec invalid for tensor/mesh");
+    if (!g.valid_for(t, m)) throw autoplan::ShapeError("target spec invalid for tensor/mesh");
+    need(device >= 0 && device < m.num_devices(), "device index out of range");
+    auto pieces = role == 0 ? apl::pieces_for_receiver(s, g, m, t, device)
+                            : apl::pieces_for_sender(s, g, m, t, device);
+    *count = static_cast<int>(pieces.size());
+    need(static_cast<int>(pieces.size()) <= cap && (pieces.empty() || out), "piece capacity too small");
+    for (size_t i = 0; i < pieces.size(); ++i) {
+      apl_piece& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      o.sender = static_cast<int32_t>(pieces[i].sender);
+      o.receiver = static_cast<int32_t>(pieces[i].receiver);
+      for (size_t d = 0; d < pieces[i].ext.size(); ++d) {
+        o.src_lo[d] = pieces[i].src_lo[d];
+        o.dst_lo[d] = pieces[i].dst_lo[d];
+        o.ext[d] = pieces[i].ext[d];
+      }
+    }
+  });
+}
+
+int apl_mesh_create_local(const apl_mesh_desc* mesh, int cuda_device, apl_mesh** out) {
+  return guarded([&] {
+    need(out, "null out");
+    DeviceMesh m = to_mesh(mesh);
+    need(m.num_devices() <= APL_MAX_LOCAL, "simulated meshes hold at most APL_MAX_LOCAL devices");
+    int n = 0;
+    apl::check_cuda(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    need(cuda_device >= 0 && cuda_device < n, "cuda device index out of range");
+    auto* h = new apl_mesh();
+    h->impl.geo = std::move(m);
+    h->impl.device = cuda_device;
+    *out = h;
+  });
+}
+
+int apl_nccl_unique_id(uint8_t* out128) {
+  return guarded([&] {
+    need(out128, "null out");
+    static_assert(sizeof(ncclUniqueId) == 128, "unexpected ncclUniqueId size");
+    ncclUniqueId id;
+    apl::check_nccl(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int apl_mesh_create_nccl(const apl_mesh_desc* mesh, int rank, const uint8_t* nccl_id,
+                         int cuda_device, apl_mesh** out) {
+  apl_mesh* h = nullptr;
+  int rc = guarded([&] {
+    need(out && nccl_id, "null argument");
+    DeviceMesh m = to_mesh(mesh);
+    const int64_t world = m.num_devices();
+    need(rank >= 0 && rank < world, "rank out of range");
+    apl::check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    h = new apl_mesh();
+    apl::Mesh& x = h->impl;
+    x.geo = std::move(m);
+    x.device = cuda_device;
+    x.distributed = true;
+    x.rank = rank;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    apl::check_nccl(ncclCommInitRank(&x.world, static_cast<int>(world), id, rank), "ncclCommInitRank");
+    // One communicator per non-empty axis subset: color = coordinates off the
+    // subset, key = mixed-radix coordinate on it (axis order).
+    const int r = x.geo.rank();
+    const auto coord = x.geo.coord_of(rank);
+    for (uint32_t mask = 1; mask < (1u << r); ++mask) {
+      int64_t color = 0, key = 0;
+      for (int a = 0; a < r; ++a) {
+        const int64_t n = x.geo.shape[static_cast<size_t>(a)];
+        if (mask & (1u << a)) key = key * n + coord[static_cast<size_t>(a)];
+        else color = color * n + coord[static_cast<size_t>(a)];
+      }
+      ncclComm_t c = nullptr;
+      apl::check_nccl(ncclCommSplit(x.world, static_cast<int>(color), static_cast<int>(key), &c, nullptr),
+                      "ncclCommSplit");
+      x.sub[mask] = c;
+    }
+    *out = h;
+  });
+  if (rc != APL_OK) delete h;
+  return rc;
+}
+
+int apl_mesh_destroy(apl_mesh* mesh) {
+  return guarded([&] { delete mesh; });
+}
+
+int apl_mesh_info(const apl_mesh* mesh, int* num_devices, int* first_local, int* num_local,
+                  int* is_distributed) {
+  return guarded([&] {
+    need(mesh, "null mesh");
+    const apl::Mesh& m = mesh->impl;
+    if (num_devices) *num_devices = static_cast<int>(m.geo.num_devices());
+    if (first_local) *first_local = m.distributed ? m.rank : 0;
+    if (num_local) *num_local = m.num_local();
+    if (is_distributed) *is_distributed = m.distributed ? 1 : 0;
+  });
+}
+
+int apl_path_workspace_bytes(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                             const apl_step* steps, int nsteps, const apl_meta* meta,
+                             unsigned flags, size_t* bytes) {
+  return guarded([&] {
+    need(mesh && bytes, "null argument");
+    const ShardingSpec s = to_spec(src), g = to_spec(tgt);
+    const TensorMeta t = to_meta(meta);
+    if (!s.valid_for(t, mesh->impl.geo) || !g.valid_for(t, mesh->impl.geo))
+      throw autoplan::ShapeError("spec is not valid for the tensor/mesh");
+    *bytes = apl::path_workspace(mesh->impl, s, g, to_steps(steps, nsteps), t,
+                                 (flags & APL_FUSE_CHAIN) != 0);
+  });
+}
+
+int apl_run_step(apl_mesh* mesh, const apl_spec* src, const apl_step* step, const apl_meta* meta,
+                 const void* const* in, void* const* out, void* ws, size_t ws_bytes,
+                 void* stream) {
+  return guarded([&] {
+    need(mesh && step && in && out, "null argument");
+    const TransformStep s = to_step(step);
+    apl::run_path(mesh->impl, to_spec(src), s.result, {s}, to_meta(meta), in, out, ws, ws_bytes,
+                  false, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int apl_run_path(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt, const apl_step* steps,
+                 int nsteps, const apl_meta* meta, const void* const* in, void* const* out,
+                 void* ws, size_t ws_bytes, unsigned flags, void* stream) {
+  return guarded([&] {
+    need(mesh && in && out, "null argument");
+    apl::run_path(mesh->impl, to_spec(src), to_spec(tgt), to_steps(steps, nsteps), to_meta(meta),
+                  in, out, ws, ws_bytes, (flags & APL_FUSE_CHAIN) != 0,
+                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* bufs,
+                   size_t count, int dtype, void* stream) {
+  return guarded([&] {
+    need(mesh && bufs && (naxes == 0 || axes), "null argument");
+    need(dtype >= APL_F32 && dtype <= APL_F16, "bad dtype");
+    apl::all_reduce(mesh->impl, std::vector<int>(axes, axes + naxes), bufs, count, dtype,
+                    static_cast<cudaStream_t>(stream));
+  });
+}
+
+int apl_launch_count(uint64_t* launches) {
+  return guarded([&] {
+    need(launches, "null out");
+    *launches = apl::launch_count();
+  });
+}
+
+}  // extern "C"

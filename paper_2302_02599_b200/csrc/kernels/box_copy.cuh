@@ -1,0 +1,40 @@
+// Batched N-D box copy: the one data-moving kernel behind shard-slice,
+// all-gather unpack, all-to-all pack/unpack, collapsed-chain redistribution
+// and the simulated-mesh exchange.
+//
+// A launch executes a table of copy descriptors. Each descriptor moves
+// rows x run bytes, where a row is addressed by up to 7 outer indices
+// (strides in bytes on both sides) and the run is contiguous on both sides.
+// The work is flattened into "units" of V bytes (V = 16 whenever every run,
+// stride, offset and base pointer allows it), so one persistent grid sweeps
+// all descriptors with coalesced 128-bit loads/stores regardless of how the
+// pieces are shaped.
+#pragma once
+
+#include <cstdint>
+
+namespace apl {
+
+constexpr int kCopyMaxOuter = 7;
+constexpr int kCopyMaxPtrs = 66;  // 64 simulated devices + 2 staging buffers
+
+// Division by a runtime-invariant uint32 via multiply-high (n < 2^31).
+struct FastDiv {
+  uint32_t div = 1, mul = 0, shr = 0;
+};
+
+struct DevCopy {
+  int64_t unit_begin;  // prefix sum of units over the table
+  int64_t src_off, dst_off;
+  int64_t src_stride[kCopyMaxOuter], dst_stride[kCopyMaxOuter];
+  FastDiv ext[kCopyMaxOuter];
+  FastDiv units_per_run;
+  int32_t src_buf, dst_buf, nouter, pad_;
+};
+
+struct PtrTable {
+  const char* src[kCopyMaxPtrs];
+  char* dst[kCopyMaxPtrs];
+};
+
+}  // namespace apl

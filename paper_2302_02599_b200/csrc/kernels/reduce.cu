@@ -1,0 +1,120 @@
+// Partial-sum all-reduce on a simulated (single-GPU) mesh.
+//
+// Each axis group of the mesh holds `group_size` partial buffers; every
+// member ends with the same sum, accumulated in fp32 in member order and
+// rounded once (so results are identical across members and independent of
+// thread scheduling). HBM-bound: reads group_size x count and writes
+// group_size x count elements per group.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+namespace apl {
+
+extern std::atomic<uint64_t> g_launches;
+
+namespace {
+
+constexpr int kMaxMembers = 64;
+
+struct ReduceArgs {
+  void* bufs[kMaxMembers];
+  int members[kMaxMembers];
+  int groups;
+  int group_size;
+};
+
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ float to_f(__half x) { return __half2float(x); }
+template <typename T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <>
+__device__ __forceinline__ __half from_f<__half>(float x) { return __float2half_rn(x); }
+
+// VEC elements per thread per iteration, moved as one 16-byte access when
+// VEC * sizeof(T) == 16.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) reduce_groups(const __grid_constant__ ReduceArgs a,
+                                                     int64_t nvec) {
+  struct alignas(sizeof(T) * VEC) Pack {
+    T v[VEC];
+  };
+  const int g = blockIdx.y;
+  const int* mem = a.members + g * a.group_size;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nvec;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
+    for (int j = 0; j < a.group_size; ++j) {
+      const Pack p = reinterpret_cast<const Pack*>(a.bufs[mem[j]])[i];
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) acc[k] += to_f(p.v[k]);
+    }
+    Pack o;
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) o.v[k] = from_f<T>(acc[k]);
+    for (int j = 0; j < a.group_size; ++j) reinterpret_cast<Pack*>(a.bufs[mem[j]])[i] = o;
+  }
+}
+
+template <typename T>
+cudaError_t launch_typed(const ReduceArgs& a, size_t count, bool aligned, cudaStream_t stream) {
+  constexpr int kVec = 16 / sizeof(T);
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_group = std::max(1, (sms * 8) / std::max(1, a.groups));
+  if (aligned && count % kVec == 0) {
+    const int64_t nvec = static_cast<int64_t>(count / kVec);
+    const int64_t want = (nvec + 255) / 256;
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>(want, per_group)), a.groups);
+    reduce_groups<T, kVec><<<grid, 256, 0, stream>>>(a, nvec);
+  } else {
+    const int64_t nvec = static_cast<int64_t>(count);
+    const int64_t want = (nvec + 255) / 256;
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>(want, per_group)), a.groups);
+    reduce_groups<T, 1><<<grid, 256, 0, stream>>>(a, nvec);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int groups,
+                                   int group_size, size_t count, int dtype,
+                                   cudaStream_t stream) {
+  if (groups * group_size > kMaxMembers) return cudaErrorInvalidValue;
+  ReduceArgs a{};
+  bool aligned = true;
+  for (int i = 0; i < groups * group_size; ++i) {
+    a.members[i] = i;
+    a.bufs[i] = bufs[members[i]];
+    aligned = aligned && (reinterpret_cast<uintptr_t>(a.bufs[i]) % 16 == 0);
+  }
+  a.groups = groups;
+  a.group_size = group_size;
+  switch (dtype) {
+    case 0:
+      return launch_typed<float>(a, count, aligned, stream);
+    case 1:
+      return launch_typed<__nv_bfloat16>(a, count, aligned, stream);
+    case 2:
+      return launch_typed<__half>(a, count, aligned, stream);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+uint64_t launch_count() { return g_launches.load(); }
+
+}  // namespace apl

@@ -1,0 +1,481 @@
+// Device runtime: exchange compilation and execution on simulated (1 GPU)
+// and distributed (NCCL, one process per GPU) meshes.
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <numeric>
+#include <cstring>
+
+#include "apl.h"
+
+namespace apl {
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+constexpr int64_t kMaxUnitsPerDesc = int64_t{1} << 30;  // keeps kernel indices in uint32
+
+int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+int pow2_vec(int64_t g) {
+  for (int v = 16; v > 1; v >>= 1)
+    if (g % v == 0) return v;
+  return 1;
+}
+
+int ptr_align(const void* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  for (int v = 16; v > 1; v >>= 1)
+    if (a % static_cast<uintptr_t>(v) == 0) return v;
+  return 1;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Splits descriptors whose unit count would overflow the kernel's 32-bit
+// per-descriptor index.
+void split_large(const CopyDesc& d, int vec, std::vector<CopyDesc>& out) {
+  const int64_t upr = d.run_bytes / vec;
+  int64_t rows = 1;
+  for (int i = 0; i < d.nouter; ++i) rows *= d.ext[i];
+  if (upr * rows <= kMaxUnitsPerDesc) {
+    out.push_back(d);
+    return;
+  }
+  if (upr > kMaxUnitsPerDesc / 4) {
+    // One very long run: cut it into 2^24-unit runs (+ a remainder).
+    const int64_t piece = (int64_t{1} << 24) * vec;
+    const int64_t whole = d.run_bytes / piece;
+    const int64_t rest = d.run_bytes - whole * piece;
+    if (d.nouter == 0) {
+      CopyDesc a = d;
+      a.run_bytes = piece;
+      a.nouter = 1;
+      a.ext[0] = whole;
+      a.src_stride[0] = piece;
+      a.dst_stride[0] = piece;
+      split_large(a, vec, out);
+      if (rest > 0) {
+        CopyDesc b = d;
+        b.src_off += whole * piece;
+        b.dst_off += whole * piece;
+        b.run_bytes = rest;
+        out.push_back(b);
+      }
+      return;
+    }
+    // Peel the outermost index and recurse on each row.
+    for (int64_t i = 0; i < d.ext[0]; ++i) {
+      CopyDesc r = d;
+      r.src_off += i * d.src_stride[0];
+      r.dst_off += i * d.dst_stride[0];
+      r.nouter = d.nouter - 1;
+      for (int j = 0; j < r.nouter; ++j) {
+        r.ext[j] = d.ext[j + 1];
+        r.src_stride[j] = d.src_stride[j + 1];
+        r.dst_stride[j] = d.dst_stride[j + 1];
+      }
+      split_large(r, vec, out);
+    }
+    return;
+  }
+  // Split the outermost dim into slabs small enough.
+  const int64_t inner = upr * rows / d.ext[0];
+  const int64_t slab = std::max<int64_t>(1, kMaxUnitsPerDesc / inner);
+  for (int64_t i = 0; i < d.ext[0]; i += slab) {
+    CopyDesc r = d;
+    r.ext[0] = std::min(slab, d.ext[0] - i);
+    r.src_off += i * d.src_stride[0];
+    r.dst_off += i * d.dst_stride[0];
+    split_large(r, vec, out);
+  }
+}
+
+}  // namespace
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw RuntimeError(APL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void check_nccl(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw RuntimeError(APL_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+int natural_vec(const std::vector<CopyDesc>& descs) {
+  int64_t g = 16;
+  for (const CopyDesc& d : descs) {
+    g = std::gcd(g, d.run_bytes);
+    g = std::gcd(g, d.src_off);
+    g = std::gcd(g, d.dst_off);
+    for (int i = 0; i < d.nouter; ++i) {
+      g = std::gcd(g, d.src_stride[i]);
+      g = std::gcd(g, d.dst_stride[i]);
+    }
+  }
+  return pow2_vec(g);
+}
+
+CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec) {
+  CompiledCopies cc;
+  cc.vec = vec;
+  std::vector<CopyDesc> flat;
+  for (const CopyDesc& d : descs)
+    if (d.bytes() > 0) split_large(d, vec, flat);
+  if (flat.empty()) return cc;
+  std::vector<DevCopy> host(flat.size());
+  int64_t units = 0;
+  for (size_t i = 0; i < flat.size(); ++i) {
+    const CopyDesc& d = flat[i];
+    DevCopy& h = host[i];
+    std::memset(&h, 0, sizeof(h));
+    h.unit_begin = units;
+    h.src_off = d.src_off;
+    h.dst_off = d.dst_off;
+    h.src_buf = d.src_buf;
+    h.dst_buf = d.dst_buf;
+    h.nouter = d.nouter;
+    const int64_t upr = d.run_bytes / vec;
+    h.units_per_run = make_fastdiv(static_cast<uint32_t>(upr));
+    int64_t rows = 1;
+    for (int j = 0; j < d.nouter; ++j) {
+      h.ext[j] = make_fastdiv(static_cast<uint32_t>(d.ext[j]));
+      h.src_stride[j] = d.src_stride[j];
+      h.dst_stride[j] = d.dst_stride[j];
+      rows *= d.ext[j];
+    }
+    units += upr * rows;
+    cc.bytes += d.bytes();
+  }
+  cc.ntasks = static_cast<int>(host.size());
+  cc.total_units = units;
+  check_cuda(cudaMalloc(&cc.table, host.size() * sizeof(DevCopy)), "cudaMalloc(copy table)");
+  check_cuda(cudaMemcpy(cc.table, host.data(), host.size() * sizeof(DevCopy),
+                        cudaMemcpyHostToDevice),
+             "cudaMemcpy(copy table)");
+  return cc;
+}
+
+void free_copies(CompiledCopies& c) {
+  if (c.table != nullptr) cudaFree(c.table);
+  c = CompiledCopies{};
+}
+
+void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream) {
+  if (c.empty()) return;
+  check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, ptrs, stream),
+             "box_copy launch");
+}
+
+Mesh::~Mesh() {
+  for (auto& [key, ex] : exchanges) {
+    for (auto* m : {&ex->copies, &ex->pre, &ex->post})
+      for (auto& [v, c] : *m) free_copies(c);
+  }
+  for (auto& [mask, comm] : sub) ncclCommDestroy(comm);
+  if (world != nullptr) ncclCommDestroy(world);
+}
+
+std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec& src,
+                                       const autoplan::ShardingSpec& tgt,
+                                       const autoplan::TensorMeta& meta) {
+  std::string key = src.to_string() + ">" + tgt.to_string() + "|";
+  for (int64_t e : meta.shape) key += std::to_string(e) + ",";
+  key += "|" + std::to_string(meta.dtype_bytes);
+  {
+    std::lock_guard<std::mutex> hold(mesh.mu);
+    auto it = mesh.exchanges.find(key);
+    if (it != mesh.exchanges.end()) return it->second;
+  }
+  auto ex = std::make_shared<Exchange>();
+  const int eb = meta.dtype_bytes;
+  const std::vector<int64_t> ls = local_shape(src, mesh.geo, meta);
+  const std::vector<int64_t> lt = local_shape(tgt, mesh.geo, meta);
+  ex->in_bytes = src.per_device_bytes(meta, mesh.geo);
+  ex->out_bytes = tgt.per_device_bytes(meta, mesh.geo);
+
+  if (!mesh.distributed) {
+    for (int64_t q = 0; q < mesh.geo.num_devices(); ++q) {
+      for (const Piece& p : pieces_for_receiver(src, tgt, mesh.geo, meta, q)) {
+        ex->host_copies.push_back(make_copy(static_cast<int>(p.sender), ls, p.src_lo,
+                                            static_cast<int>(q), lt, p.dst_lo, p.ext, eb));
+        if (p.sender != q) ex->wire_bytes_in += p.elements() * eb;
+      }
+    }
+  } else {
+    const int64_t me = mesh.rank;
+    // Source buffer ids: 0 = in, 1 = recv staging. Destination: 0 = out, 1 = send staging.
+    for (const Piece& p : pieces_for_receiver(src, tgt, mesh.geo, meta, me)) {
+      const int64_t bytes = p.elements() * eb;
+      if (p.sender == me) {
+        ex->host_pre.push_back(make_copy(0, ls, p.src_lo, 0, lt, p.dst_lo, p.ext, eb));
+        continue;
+      }
+      ex->wire_bytes_in += bytes;
+      if (box_contiguous(lt, p.ext)) {
+        ex->recvs.push_back({static_cast<int>(p.sender), true, box_offset(lt, p.dst_lo) * eb, bytes});
+      } else {
+        const int64_t off = ex->recv_staging;
+        std::vector<int64_t> zero(p.ext.size(), 0);
+        CopyDesc c = make_copy(1, p.ext, zero, 0, lt, p.dst_lo, p.ext, eb);
+        c.src_off += off;
+        ex->host_post.push_back(c);
+        ex->recvs.push_back({static_cast<int>(p.sender), false, off, bytes});
+        ex->recv_staging = align_up(off + bytes);
+      }
+    }
+    for (const Piece& p : pieces_for_sender(src, tgt, mesh.geo, meta, me)) {
+      if (p.receiver == me) continue;
+      const int64_t bytes = p.elements() * eb;
+      ex->wire_bytes_out += bytes;
+      if (box_contiguous(ls, p.ext)) {
+        ex->sends.push_back({static_cast<int>(p.receiver), true, box_offset(ls, p.src_lo) * eb, bytes});
+      } else {
+        const int64_t off = ex->send_staging;
+        std::vector<int64_t> zero(p.ext.size(), 0);
+        CopyDesc c = make_copy(0, ls, p.src_lo, 1, p.ext, zero, p.ext, eb);
+        c.dst_off += off;
+        ex->host_pre.push_back(c);
+        ex->sends.push_back({static_cast<int>(p.receiver), false, off, bytes});
+        ex->send_staging = align_up(off + bytes);
+      }
+    }
+  }
+  std::lock_guard<std::mutex> hold(mesh.mu);
+  auto [it, fresh] = mesh.exchanges.emplace(key, ex);
+  return it->second;
+}
+
+size_t exchange_workspace(const Exchange& ex) {
+  return static_cast<size_t>(align_up(ex.send_staging) + align_up(ex.recv_staging));
+}
+
+namespace {
+
+const CompiledCopies& compiled_for(std::map<int, CompiledCopies>& cache,
+                                   const std::vector<CopyDesc>& host, int vec) {
+  auto it = cache.find(vec);
+  if (it == cache.end()) it = cache.emplace(vec, compile_copies(host, vec)).first;
+  return it->second;
+}
+
+}  // namespace
+
+void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* out, void* ws,
+                  size_t ws_bytes, cudaStream_t stream) {
+  DeviceGuard guard(mesh.device);
+  const int nl = mesh.num_local();
+  if (!mesh.distributed) {
+    PtrTable t{};
+    int align = natural_vec(ex.host_copies);
+    for (int i = 0; i < nl; ++i) {
+      t.src[i] = static_cast<const char*>(in[i]);
+      t.dst[i] = static_cast<char*>(out[i]);
+      align = std::min({align, ptr_align(in[i]), ptr_align(out[i])});
+    }
+    std::lock_guard<std::mutex> hold(mesh.mu);
+    run_copies(compiled_for(ex.copies, ex.host_copies, align), t, stream);
+    return;
+  }
+  if (ws_bytes < exchange_workspace(ex))
+    throw RuntimeError(APL_ERR_ARG, "workspace smaller than apl_path_workspace_bytes");
+  char* send = static_cast<char*>(ws);
+  char* recv = send + align_up(ex.send_staging);
+  PtrTable t{};
+  t.src[0] = static_cast<const char*>(in[0]);
+  t.src[1] = recv;
+  t.dst[0] = static_cast<char*>(out[0]);
+  t.dst[1] = send;
+  const int palign = std::min({ptr_align(in[0]), ptr_align(out[0]), ptr_align(ws)});
+  {
+    std::lock_guard<std::mutex> hold(mesh.mu);
+    run_copies(compiled_for(ex.pre, ex.host_pre, std::min(palign, natural_vec(ex.host_pre))), t,
+               stream);
+  }
+  if (!ex.sends.empty() || !ex.recvs.empty()) {
+    check_nccl(ncclGroupStart(), "ncclGroupStart");
+    for (const auto& s : ex.sends) {
+      const char* p = s.direct ? static_cast<const char*>(in[0]) + s.offset : send + s.offset;
+      check_nccl(ncclSend(p, static_cast<size_t>(s.bytes), ncclInt8, s.peer, mesh.world, stream),
+                 "ncclSend");
+    }
+    for (const auto& r : ex.recvs) {
+      char* p = r.direct ? static_cast<char*>(out[0]) + r.offset : recv + r.offset;
+      check_nccl(ncclRecv(p, static_cast<size_t>(r.bytes), ncclInt8, r.peer, mesh.world, stream),
+                 "ncclRecv");
+    }
+    check_nccl(ncclGroupEnd(), "ncclGroupEnd");
+  }
+  {
+    std::lock_guard<std::mutex> hold(mesh.mu);
+    run_copies(compiled_for(ex.post, ex.host_post, std::min(palign, natural_vec(ex.host_post))),
+               t, stream);
+  }
+}
+
+namespace {
+
+// Checks the steps replay src -> tgt with the reference step semantics
+// (the same contract as reference tests/helpers.hpp:282-339).
+void validate_steps(const autoplan::ShardingSpec& src, const autoplan::ShardingSpec& tgt,
+                    const std::vector<autoplan::TransformStep>& steps,
+                    const autoplan::DeviceMesh& geo, const autoplan::TensorMeta& meta) {
+  using autoplan::CollectiveKind;
+  autoplan::ShardingSpec cur = src;
+  for (size_t i = 0; i < steps.size(); ++i) {
+    const auto& s = steps[i];
+    const int r = cur.tensor_rank();
+    bool ok = s.tensor_dim >= 0 && s.tensor_dim < r;
+    if (ok) {
+      auto& axes = cur.dims[static_cast<size_t>(s.tensor_dim)].axes;
+      switch (s.kind) {
+        case CollectiveKind::kAllGather:
+          ok = !axes.empty() && axes.back() == s.mesh_axis;
+          if (ok) axes.pop_back();
+          break;
+        case CollectiveKind::kShardSlice: {
+          const auto used = cur.used_axes();
+          ok = s.mesh_axis >= 0 && s.mesh_axis < cur.mesh_rank &&
+               std::find(used.begin(), used.end(), s.mesh_axis) == used.end();
+          if (ok) axes.push_back(s.mesh_axis);
+          break;
+        }
+        case CollectiveKind::kAllToAll:
+          ok = s.target_dim >= 0 && s.target_dim < r && s.target_dim != s.tensor_dim &&
+               !axes.empty() && axes.back() == s.mesh_axis;
+          if (ok) {
+            axes.pop_back();
+            cur.dims[static_cast<size_t>(s.target_dim)].axes.push_back(s.mesh_axis);
+          }
+          break;
+        default:
+          ok = false;
+      }
+    }
+    if (!ok || !(cur == s.result) || !cur.valid_for(meta, geo))
+      throw RuntimeError(APL_ERR_ARG, "step " + std::to_string(i) +
+                                          " does not replay from " + src.to_string());
+  }
+  if (!(cur == tgt))
+    throw RuntimeError(APL_ERR_ARG, "steps end at " + cur.to_string() + ", not " +
+                                        tgt.to_string());
+}
+
+struct StepPlan {
+  std::vector<std::shared_ptr<Exchange>> hops;
+  int64_t inter_bytes = 0;  // per ping-pong region
+  int64_t staging = 0;
+};
+
+StepPlan plan_steps(Mesh& mesh, const autoplan::ShardingSpec& src,
+                    const std::vector<autoplan::TransformStep>& steps,
+                    const autoplan::TensorMeta& meta) {
+  StepPlan sp;
+  const autoplan::ShardingSpec* cur = &src;
+  for (size_t i = 0; i < steps.size(); ++i) {
+    auto ex = get_exchange(mesh, *cur, steps[i].result, meta);
+    sp.staging = std::max<int64_t>(sp.staging, static_cast<int64_t>(exchange_workspace(*ex)));
+    if (i + 1 < steps.size())
+      sp.inter_bytes = std::max(sp.inter_bytes, align_up(ex->out_bytes) * mesh.num_local());
+    sp.hops.push_back(std::move(ex));
+    cur = &steps[i].result;
+  }
+  return sp;
+}
+
+}  // namespace
+
+size_t path_workspace(Mesh& mesh, const autoplan::ShardingSpec& src,
+                      const autoplan::ShardingSpec& tgt,
+                      const std::vector<autoplan::TransformStep>& steps,
+                      const autoplan::TensorMeta& meta, bool fuse) {
+  if (fuse || steps.empty()) return exchange_workspace(*get_exchange(mesh, src, tgt, meta));
+  StepPlan sp = plan_steps(mesh, src, steps, meta);
+  return static_cast<size_t>(2 * sp.inter_bytes + sp.staging);
+}
+
+void run_path(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::ShardingSpec& tgt,
+              const std::vector<autoplan::TransformStep>& steps,
+              const autoplan::TensorMeta& meta, const void* const* in, void* const* out,
+              void* ws, size_t ws_bytes, bool fuse, cudaStream_t stream) {
+  if (!src.valid_for(meta, mesh.geo) || !tgt.valid_for(meta, mesh.geo))
+    throw RuntimeError(APL_ERR_SHAPE, "spec is not valid for the tensor/mesh");
+  validate_steps(src, tgt, steps, mesh.geo, meta);
+  if (fuse || steps.size() <= 1) {
+    auto ex = get_exchange(mesh, src, tgt, meta);
+    run_exchange(mesh, *ex, in, out, ws, ws_bytes, stream);
+    return;
+  }
+  StepPlan sp = plan_steps(mesh, src, steps, meta);
+  if (ws_bytes < static_cast<size_t>(2 * sp.inter_bytes + sp.staging))
+    throw RuntimeError(APL_ERR_ARG, "workspace smaller than apl_path_workspace_bytes");
+  const int nl = mesh.num_local();
+  char* region[2] = {static_cast<char*>(ws), static_cast<char*>(ws) + sp.inter_bytes};
+  char* staging = static_cast<char*>(ws) + 2 * sp.inter_bytes;
+  std::vector<const void*> cur_in(in, in + nl);
+  std::vector<void*> next(static_cast<size_t>(nl));
+  for (size_t i = 0; i < sp.hops.size(); ++i) {
+    const bool last = i + 1 == sp.hops.size();
+    if (last) {
+      for (int j = 0; j < nl; ++j) next[static_cast<size_t>(j)] = out[j];
+    } else {
+      const int64_t stride = align_up(sp.hops[i]->out_bytes);
+      for (int j = 0; j < nl; ++j) next[static_cast<size_t>(j)] = region[i % 2] + j * stride;
+    }
+    run_exchange(mesh, *sp.hops[i], cur_in.data(), next.data(), staging,
+                 static_cast<size_t>(sp.staging), stream);
+    for (int j = 0; j < nl; ++j) cur_in[static_cast<size_t>(j)] = next[static_cast<size_t>(j)];
+  }
+}
+
+void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, size_t count,
+                int dtype, cudaStream_t stream) {
+  DeviceGuard guard(mesh.device);
+  uint32_t mask = 0;
+  for (int a : axes) {
+    if (a < 0 || a >= mesh.geo.rank()) throw RuntimeError(APL_ERR_AXIS, "reduce axis out of range");
+    mask |= 1u << a;
+  }
+  if (mask == 0 || count == 0) return;
+  if (mesh.distributed) {
+    ncclDataType_t t = dtype == APL_F32 ? ncclFloat32 : dtype == APL_BF16 ? ncclBfloat16 : ncclFloat16;
+    check_nccl(ncclAllReduce(bufs[0], bufs[0], count, t, ncclSum, mesh.sub.at(mask), stream),
+               "ncclAllReduce");
+    return;
+  }
+  // Groups: devices sharing every coordinate off `axes`, members ordered by
+  // their mixed-radix coordinate on `axes`.
+  const int64_t p = mesh.geo.num_devices();
+  int64_t gsize = 1;
+  for (int a = 0; a < mesh.geo.rank(); ++a)
+    if (mask & (1u << a)) gsize *= mesh.geo.shape[static_cast<size_t>(a)];
+  const int64_t ngroups = p / gsize;
+  std::vector<int> members;
+  std::vector<std::vector<int>> by_group(static_cast<size_t>(ngroups));
+  std::map<int64_t, int> group_id;
+  for (int64_t d = 0; d < p; ++d) {
+    const auto c = mesh.geo.coord_of(d);
+    int64_t off = 0;
+    for (int a = 0; a < mesh.geo.rank(); ++a)
+      if (!(mask & (1u << a))) off = off * mesh.geo.shape[static_cast<size_t>(a)] + c[static_cast<size_t>(a)];
+    by_group[static_cast<size_t>(off)].push_back(static_cast<int>(d));  // row-major => on-axes order
+  }
+  for (auto& g : by_group) members.insert(members.end(), g.begin(), g.end());
+  check_cuda(launch_allreduce_local(bufs, members.data(), static_cast<int>(ngroups),
+                                    static_cast<int>(gsize), count, dtype, stream),
+             "all-reduce launch");
+}
+
+}  // namespace apl

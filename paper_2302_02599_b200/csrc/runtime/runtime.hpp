@@ -1,0 +1,113 @@
+// Device runtime: meshes (simulated on one GPU, or one process per GPU over
+// NCCL), compiled exchanges and their execution.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../kernels/box_copy.cuh"
+#include "plan.hpp"
+
+namespace apl {
+
+// Error raised by the runtime; `code` is an apl_status value.
+struct RuntimeError : std::runtime_error {
+  int code;
+  RuntimeError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void check_cuda(cudaError_t e, const char* what);
+void check_nccl(ncclResult_t r, const char* what);
+
+FastDiv make_fastdiv(uint32_t d);
+int sm_count();
+cudaError_t launch_box_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
+                            int vec_bytes, const PtrTable& ptrs, cudaStream_t stream);
+cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int groups,
+                                   int group_size, size_t count, int dtype,
+                                   cudaStream_t stream);
+uint64_t launch_count();
+
+// A descriptor table resident on the device.
+struct CompiledCopies {
+  DevCopy* table = nullptr;
+  int ntasks = 0;
+  int64_t total_units = 0;
+  int vec = 16;
+  int64_t bytes = 0;  // payload bytes (each read once, written once)
+  bool empty() const { return ntasks == 0; }
+};
+
+// Largest vector width (16/8/4/2/1) dividing every run, stride and offset.
+int natural_vec(const std::vector<CopyDesc>& descs);
+CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec);
+void free_copies(CompiledCopies& c);
+void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream);
+
+// One direct src -> tgt redistribution, compiled for the local devices.
+struct Exchange {
+  int64_t in_bytes = 0;   // per-device source shard bytes
+  int64_t out_bytes = 0;  // per-device target shard bytes
+  std::vector<CopyDesc> host_copies;  // simulated mesh: everything
+  std::vector<CopyDesc> host_pre;     // distributed: pack + self
+  std::vector<CopyDesc> host_post;    // distributed: unpack
+  std::map<int, CompiledCopies> copies, pre, post;  // keyed by vector width
+  struct Xfer {
+    int peer;
+    bool direct;  // straight from `in` / into `out` (contiguous box)
+    int64_t offset;
+    int64_t bytes;
+  };
+  std::vector<Xfer> sends, recvs;
+  int64_t send_staging = 0, recv_staging = 0;
+  int64_t wire_bytes_in = 0;   // bytes this rank receives from peers
+  int64_t wire_bytes_out = 0;  // bytes this rank sends to peers
+};
+
+struct Mesh {
+  autoplan::DeviceMesh geo;
+  int device = 0;
+  bool distributed = false;
+  int rank = 0;  // distributed: this process's mesh device index
+  ncclComm_t world = nullptr;
+  std::map<uint32_t, ncclComm_t> sub;  // axis-subset mask -> communicator
+  std::mutex mu;
+  std::unordered_map<std::string, std::shared_ptr<Exchange>> exchanges;
+
+  int num_local() const { return distributed ? 1 : static_cast<int>(geo.num_devices()); }
+  ~Mesh();
+};
+
+std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec& src,
+                                       const autoplan::ShardingSpec& tgt,
+                                       const autoplan::TensorMeta& meta);
+
+// Workspace a src -> tgt exchange needs (distributed staging; 0 if simulated).
+size_t exchange_workspace(const Exchange& ex);
+
+// Runs `ex` moving in[] -> out[] (num_local pointers each).
+void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* out,
+                  void* ws, size_t ws_bytes, cudaStream_t stream);
+
+size_t path_workspace(Mesh& mesh, const autoplan::ShardingSpec& src,
+                      const autoplan::ShardingSpec& tgt,
+                      const std::vector<autoplan::TransformStep>& steps,
+                      const autoplan::TensorMeta& meta, bool fuse);
+
+void run_path(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::ShardingSpec& tgt,
+              const std::vector<autoplan::TransformStep>& steps,
+              const autoplan::TensorMeta& meta, const void* const* in, void* const* out,
+              void* ws, size_t ws_bytes, bool fuse, cudaStream_t stream);
+
+void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, size_t count,
+                int dtype, cudaStream_t stream);
+
+}  // namespace apl

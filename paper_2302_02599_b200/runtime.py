@@ -1,0 +1,166 @@
+"""Torch-facing runtime over the C-ABI: meshes, conversion execution,
+partial-sum all-reduce.
+
+Device memory, streams and process groups come from torch; every byte is
+moved by libapl.so kernels / NCCL calls issued from C++. There is no CPU or
+eager-torch fallback: without a GPU or without libapl.so these calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import torch
+
+from . import _capi as A
+from .layout import (DeviceMesh, ShardingSpec, TensorMeta, TransformPath, TransformStep,
+                     check, find_transform_path)
+
+_DTYPE_CODE = {torch.float32: A.F32, torch.bfloat16: A.BF16, torch.float16: A.F16}
+
+
+def _ptrs(tensors: Sequence[torch.Tensor]):
+    arr = (C.c_void_p * max(1, len(tensors)))()
+    for i, t in enumerate(tensors):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+def _stream_handle(stream) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def launch_count() -> int:
+    n = C.c_uint64()
+    check(A.lib().apl_launch_count(C.byref(n)))
+    return n.value
+
+
+class Mesh:
+    """An executing DeviceMesh.
+
+    Mesh.local(shape)  — all mesh devices simulated as buffers on one GPU;
+                         buffer lists carry num_devices tensors.
+    Mesh.nccl(shape, rank, uid) — one process per GPU over NCCL; buffer
+                         lists carry this rank's single shard.
+    """
+
+    def __init__(self, handle: C.c_void_p, geo: DeviceMesh, device: int):
+        self._h = handle
+        self.geo = geo
+        self.device = device
+        n, first, nl, dist = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        check(A.lib().apl_mesh_info(handle, C.byref(n), C.byref(first), C.byref(nl),
+                                    C.byref(dist)))
+        self.num_devices, self.first_local, self.num_local = n.value, first.value, nl.value
+        self.distributed = bool(dist.value)
+        self._ws = None
+
+    @staticmethod
+    def local(shape: Sequence[int], device: int = 0) -> "Mesh":
+        geo = DeviceMesh.uniform(shape)
+        h = C.c_void_p()
+        check(A.lib().apl_mesh_create_local(C.byref(geo.c()), device, C.byref(h)))
+        return Mesh(h, geo, device)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(A.lib().apl_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def nccl(shape: Sequence[int], rank: int, uid: bytes, device: int) -> "Mesh":
+        geo = DeviceMesh.uniform(shape)
+        h = C.c_void_p()
+        ub = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(A.lib().apl_mesh_create_nccl(C.byref(geo.c()), rank, ub, device, C.byref(h)))
+        return Mesh(h, geo, device)
+
+    @staticmethod
+    def from_process_group(shape: Sequence[int]) -> "Mesh":
+        """Distributed mesh over the default torch.distributed group (rank =
+        mesh device index, row-major; NCCL id broadcast through the group)."""
+        import torch.distributed as dist
+
+        rank = dist.get_rank()
+        obj = [Mesh.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return Mesh.nccl(shape, rank, obj[0], torch.cuda.current_device())
+
+    def close(self) -> None:
+        if self._h:
+            A.lib().apl_mesh_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- conversions ---------------------------------------------------------
+    def workspace_bytes(self, path: TransformPath, meta: TensorMeta, fuse: bool = False) -> int:
+        out = C.c_size_t()
+        steps = path.steps_c()
+        check(A.lib().apl_path_workspace_bytes(
+            self._h, C.byref(path.source.c()), C.byref(path.target.c()), steps,
+            len(path.steps), C.byref(meta.c()), A.FUSE_CHAIN if fuse else A.STEPWISE,
+            C.byref(out)))
+        return out.value
+
+    def _workspace(self, nbytes: int) -> torch.Tensor:
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8,
+                                   device=f"cuda:{self.device}")
+        return self._ws
+
+    def _check_bufs(self, bufs, nbytes: int, what: str) -> None:
+        if len(bufs) != self.num_local:
+            raise ValueError(f"{what}: expected {self.num_local} buffers, got {len(bufs)}")
+        for t in bufs:
+            if not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{what}: buffers must be contiguous CUDA tensors")
+            if t.numel() * t.element_size() < nbytes:
+                raise ValueError(f"{what}: buffer holds {t.numel() * t.element_size()} bytes, "
+                                 f"needs {nbytes}")
+
+    def run_path(self, path: TransformPath, meta: TensorMeta, inputs, outputs,
+                 fuse: bool = False, stream=None) -> None:
+        """Execute `path` (stepwise, or collapsed into one exchange)."""
+        self._check_bufs(inputs, path.source.per_device_bytes(meta, self.geo), "inputs")
+        self._check_bufs(outputs, path.target.per_device_bytes(meta, self.geo), "outputs")
+        nbytes = self.workspace_bytes(path, meta, fuse)
+        ws = self._workspace(nbytes)
+        steps = path.steps_c()
+        check(A.lib().apl_run_path(
+            self._h, C.byref(path.source.c()), C.byref(path.target.c()), steps,
+            len(path.steps), C.byref(meta.c()), _ptrs(inputs), _ptrs(outputs),
+            C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()),
+            A.FUSE_CHAIN if fuse else A.STEPWISE, _stream_handle(stream)))
+
+    def run_step(self, src: ShardingSpec, step: TransformStep, meta: TensorMeta, inputs,
+                 outputs, stream=None) -> None:
+        path = TransformPath(src, step.result, [step])
+        self.run_path(path, meta, inputs, outputs, False, stream)
+
+    def convert(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta, inputs,
+                fuse: bool = True, stream=None) -> list:
+        """Allocate target shards and convert `inputs` (src) into them."""
+        path = find_transform_path(src, tgt, self.geo, meta)
+        shape = tgt.local_shape(meta, self.geo)
+        outs = [torch.empty(shape, dtype=inputs[0].dtype, device=inputs[0].device)
+                for _ in range(self.num_local)]
+        self.run_path(path, meta, inputs, outs, fuse, stream)
+        return outs
+
+    def all_reduce(self, axes: Sequence[int], tensors, stream=None) -> None:
+        if not tensors:
+            return
+        dt = _DTYPE_CODE[tensors[0].dtype]
+        if len(tensors) != self.num_local:
+            raise ValueError(f"expected {self.num_local} buffers")
+        ax = (C.c_int32 * max(1, len(axes)))(*axes)
+        check(A.lib().apl_all_reduce(self._h, ax, len(axes), _ptrs(tensors),
+                                     tensors[0].numel(), dt, _stream_handle(stream)))
