@@ -1,0 +1,419 @@
+"""Benchmark of the layout-conversion hot path (driver contract; one JSON line).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "1D mesh of 8: all-gather S0 -> R and
+all-to-all S0R -> RS0"): one step converts a [65536, 8192] bf16 tensor
+(1 GiB) S0R -> RR (all-gather) and S0R -> RS0 (all-to-all) on a mesh of 8.
+
+  N = 1 : the 8 mesh devices are simulated as buffers on one B200, so each
+          conversion is one collapsed exchange = one box-copy kernel over HBM
+          (the "pack/unpack only" point of the north star). value = pack HBM
+          GB/s: algorithmic bytes (every output byte read once from a source
+          shard and written once) / device time.
+  N > 1 : one process per GPU over NCCL (mesh [N]), weak scaling with a
+          128 MiB shard per GPU; value = bus bytes received by all ranks /
+          max-over-ranks device time (aggregate bus GB/s).
+
+Inputs are 1 GiB (> 126 MB L2), so no L2 flush is needed between steps.
+The reference arm (--impl reference) runs the reference's own planner
+(oracle/_ref: find_transform_path + conversion_cost compiled from
+/root/reference) and the C oracle executing the returned steps in host RAM
+with all host threads, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "layout-conversion bus GB/s per GPU vs 900 GB/s at 2/4/8 B200; pack HBM GB/s"
+SHAPE_1GPU = (65536, 8192)   # bf16, 1 GiB
+SHARD_ROWS_NGPU = 8192       # per-GPU shard rows of [*, 8192] bf16 = 128 MiB
+EB = 2
+CONVERSIONS = [("S0R", "RR"), ("S0R", "RS0")]
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2302_02599_b200 import ShardingSpec, TensorMeta, find_transform_path
+    from paper_2302_02599_b200.runtime import Mesh, launch_count
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        mesh = Mesh.from_process_group([ws])
+        shape = (SHARD_ROWS_NGPU * ws, 8192)
+        ndev = ws
+    else:
+        mesh = Mesh.local([8], device=local)
+        shape = SHAPE_1GPU
+        ndev = 8
+    meta = TensorMeta(shape, EB)
+    geo = mesh.geo
+    stream = torch.cuda.current_stream()
+
+    convs = []
+    for a, b in CONVERSIONS:
+        s, t = ShardingSpec.parse(a, 1), ShardingSpec.parse(b, 1)
+        path = find_transform_path(s, t, geo, meta)
+        ins = [torch.empty(s.local_shape(meta, geo), dtype=torch.bfloat16, device=dev)
+               for _ in range(mesh.num_local)]
+        gen = torch.Generator(device=dev).manual_seed(2302 + rank)
+        for x in ins:  # synthetic payload, generated on device (bytes are moved, not interpreted)
+            x.view(torch.int16).random_(-32768, 32767, generator=gen)
+        outs = [torch.empty(t.local_shape(meta, geo), dtype=torch.bfloat16, device=dev)
+                for _ in range(mesh.num_local)]
+        out_bytes = t.per_device_bytes(meta, geo)
+        in_bytes = s.per_device_bytes(meta, geo)
+        # algorithmic bytes per launch (all local devices)
+        hbm = 2 * out_bytes * mesh.num_local
+        # bus bytes each rank must receive (NCCL busBW convention)
+        if (a, b) == ("S0R", "RR"):
+            bus = (ndev - 1) * in_bytes
+        else:
+            bus = (ndev - 1) * in_bytes // ndev
+        convs.append(dict(name=f"{a}->{b}", path=path, ins=ins, outs=outs, hbm=hbm, bus=bus,
+                          in_bytes=in_bytes, out_bytes=out_bytes))
+
+    def step():
+        for c in convs:
+            mesh.run_path(c["path"], meta, c["ins"], c["outs"], fuse=True, stream=stream)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # per-conversion kernel timing (events on the launching stream)
+    n_ev = args.steps * len(convs)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n_ev)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        t0.record(stream)
+        k = 0
+        for _ in range(args.steps):
+            for c in convs:
+                evs[k][0].record(stream)
+                mesh.run_path(c["path"], meta, c["ins"], c["outs"], fuse=True, stream=stream)
+                evs[k][1].record(stream)
+                k += 1
+        t1.record(stream)
+        barrier()
+    launches = launch_count() - launches0
+    total_ms = t0.elapsed_time(t1)
+    per_conv_ms = {c["name"]: [] for c in convs}
+    for i in range(n_ev):
+        per_conv_ms[convs[i % len(convs)]["name"]].append(evs[i][0].elapsed_time(evs[i][1]))
+    if ws > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+
+    ms_per_step = total_ms / args.steps
+    hbm_peak, peak_kind = peaks()
+    if ws == 1:
+        step_bytes = sum(c["hbm"] for c in convs)
+        value = step_bytes / (ms_per_step * 1e-3) / 1e9
+        unit = "GB/s"
+    else:
+        step_bytes = sum(c["bus"] for c in convs) * ws
+        value = step_bytes / (ms_per_step * 1e-3) / 1e9
+        unit = "GB/s"
+
+    # roofline of the dominant kernel (the box-copy of S0R->RR, largest share)
+    dom = max(convs, key=lambda c: statistics.mean(per_conv_ms[c["name"]]))
+    dom_ms = statistics.mean(per_conv_ms[dom["name"]])
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(f"n{ws}:{dom['name']}")
+    if ws == 1:
+        achieved = dom["hbm"] / (dom_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": f"box_copy_kernel<16,4> ({dom['name']}, 8 simulated devices)",
+                "achieved": round(achieved, 1), "peak": hbm_peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": dom["hbm"],
+                "launch_ms": round(dom_ms, 4)}
+    else:
+        achieved = dom["bus"] / (dom_ms * 1e-3) / 1e9
+        roof = {"bound": "nvlink", "kernel": f"{dom['name']} exchange (NCCL p2p + box_copy)",
+                "achieved": round(achieved, 1), "peak": 770.0, "peak_kind": "measured peer copy (B200_PROFILING.md)",
+                "unit": "GB/s", "frac": round(achieved / 770.0, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": dom["bus"], "launch_ms": round(dom_ms, 4)}
+
+    result = {
+        "metric": METRIC, "value": round(value, 1), "unit": unit, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (index-hashed bf16 bit patterns generated on device)",
+        "config": {"workload": "configs[1]: mesh of 8, S0R->RR all-gather + S0R->RS0 all-to-all",
+                   "tensor": list(shape), "mesh": [8] if ws == 1 else [ws],
+                   "mode": "simulated 8-device mesh on 1 GPU (pack/unpack only)" if ws == 1
+                   else "one process per GPU, NCCL",
+                   "path": "collapsed exchange (APL_FUSE_CHAIN)",
+                   "l2": "inputs 1 GiB > 126 MB L2, no flush needed" if ws == 1 else
+                   "per-GPU shard 128 MiB > L2",
+                   "parallelism": f"mesh[{8 if ws == 1 else ws}]"},
+        "per_conversion_ms": {k: round(statistics.mean(v), 4) for k, v in per_conv_ms.items()},
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if ws == 1:
+        result["e2e"] = run_e2e(args, mesh, meta, convs, stream)
+        result["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0:
+        print(json.dumps(result))
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_e2e(args, mesh, meta, convs, stream):
+    """Same metric through the public API with HOST buffers: pinned H2D of
+    the step's input shards, the conversions, D2H of the converted shards."""
+    import torch
+
+    host_in = [[torch.empty_like(x, device="cpu").pin_memory() for x in c["ins"]] for c in convs]
+    host_out = [[torch.empty_like(x, device="cpu").pin_memory() for x in c["outs"]] for c in convs]
+    for c, hi in zip(convs, host_in):
+        for h, x in zip(hi, c["ins"]):
+            h.copy_(x)
+    h2d = sum(x.numel() * x.element_size() for hi in host_in for x in hi)
+    d2h = sum(x.numel() * x.element_size() for ho in host_out for x in ho)
+    steps = max(2, min(args.steps, 5))
+
+    def e2e_step():
+        for c, hi, ho in zip(convs, host_in, host_out):
+            for x, h in zip(c["ins"], hi):
+                x.copy_(h, non_blocking=True)
+            mesh.run_path(c["path"], meta, c["ins"], c["outs"], fuse=True, stream=stream)
+            for h, x in zip(ho, c["outs"]):
+                h.copy_(x, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    step_bytes = sum(c["hbm"] for c in convs)
+    return {"value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3),
+            "steps": steps}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def _cpu_sample_shape():
+    # bounded sample of the same workload: 1/16 of the rows (64 MiB global)
+    return (SHAPE_1GPU[0] // 16, SHAPE_1GPU[1])
+
+
+def cpu_convert_once(shape, threads):
+    """Reference planner path + oracle step execution in host RAM, all 8
+    simulated devices; returns (seconds, algorithmic bytes)."""
+    import numpy as np
+
+    from oracle import data as O
+    from oracle import ref as R
+
+    O.set_threads(threads)
+    g = O.fill_global(shape, EB)
+    total_s, total_b = 0.0, 0
+    for a, b in CONVERSIONS:
+        ins = O.shards(g, O.parse_spec(a, 1), [8])
+        t0 = time.perf_counter()
+        if R.available():
+            rc, steps, _ = R.find_path([8], list(shape), EB, a, b)
+            assert rc == 0
+        else:
+            steps = [(0, 0, -1, 0, "R")] if b == "RR" else [(3, 0, 1, 0, "RS0")]
+        outs = O.replay(shape, O.parse_spec(a, 1), [8], steps, ins)
+        total_s += time.perf_counter() - t0
+        total_b += 2 * sum(o.nbytes for o in outs)
+    return total_s, total_b
+
+
+def cpu_baseline(args):
+    threads = os.cpu_count() or 1
+    shape = _cpu_sample_shape()
+    secs, nbytes, reps = 0.0, 0, 0
+    while secs < 10.0 and reps < 50:
+        s, b = cpu_convert_once(shape, threads)
+        secs += s
+        nbytes += b
+        reps += 1
+    return {"value": round(nbytes / secs / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "kind": "port" if not _ref_available() else "reference",
+            "sample": f"{reps} x (S0R->RR + S0R->RS0) on [{shape[0]},{shape[1]}] bf16, mesh [8] "
+                      f"simulated in host RAM; path from the reference planner "
+                      f"({'oracle/_ref' if _ref_available() else 'n/a'}), bytes moved by the C "
+                      f"oracle with {threads} threads"}
+
+
+def _ref_available():
+    from oracle import ref as R
+
+    return R.available()
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    shape = _cpu_sample_shape()
+    for _ in range(args.warmup):
+        cpu_convert_once(shape, threads)
+    secs, nbytes = 0.0, 0
+    for _ in range(args.steps):
+        s, b = cpu_convert_once(shape, threads)
+        secs += s
+        nbytes += b
+    value = nbytes / secs / 1e9
+    planner_us = None
+    if _ref_available():
+        from oracle import ref as R
+
+        planner_us = round(1e6 * R.time_paths([8], list(SHAPE_1GPU), EB, "S0R", "RS0", 2000), 3)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * secs / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "configs[1]: mesh of 8, S0R->RR all-gather + S0R->RS0 all-to-all",
+                   "tensor": list(shape), "mesh": [8], "mode": "host RAM, all host threads",
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
+                         "kind": "reference" if _ref_available() else "port",
+                         "sample": f"per step: S0R->RR + S0R->RS0 of a [{shape[0]},{shape[1]}] "
+                                   "bf16 tensor on 8 simulated devices (1/16 of the GPU "
+                                   "workload); reference planner (oracle/_ref) picks the path, "
+                                   "the C oracle moves the bytes"},
+        "reference_planner_us_per_path": planner_us,
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

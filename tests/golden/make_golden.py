@@ -32,6 +32,8 @@ CASES = [
     ("mesh22_1024sq", [2, 2], [1024, 1024], 4, True),  # config 1
     ("mesh24_8192sq_bf16", [2, 4], [8192, 8192], 2, True),  # config 3
     ("mesh222_rank2", [2, 2, 2], [8192, 8192], 2, True),    # config 4 (rank 2)
+    ("mesh222_rank2_small", [2, 2, 2], [8, 8], 4, True),
+    ("mesh222_rank3_444", [2, 2, 2], [4, 4, 4], 4, True),   # SURVEY Appendix A replay case
     ("mesh222_rank3_small", [2, 2, 2], [8, 4, 2], 4, True),  # test_layout.cpp:264-280
     ("mesh222_rank3", [2, 2, 2], [512, 512, 256], 2, True),  # config 4 (rank 3)
     ("mesh42_1024sq", [4, 2], [1024, 1024], 4, True),
