@@ -193,11 +193,52 @@ int apl_run_path(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
                  const void* const* in, void* const* out, void* ws, size_t ws_bytes,
                  unsigned flags, void* stream);
 
+/* Algorithmic traffic of the collapsed src->tgt exchange for this mesh's
+ * local devices: bytes the copy kernels read (each source byte once) and
+ * write (every destination), and bytes received from other mesh devices
+ * (what crosses NVLink on a distributed mesh). */
+int apl_exchange_traffic(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                         const apl_meta* meta, int64_t* hbm_read, int64_t* hbm_write,
+                         int64_t* wire_in);
+
 /* Sum partial results over the mesh axes `axes` (partial_sum strategies,
  * intraop.cpp:544-551; planner.cpp:263-282). In place; every member of an
  * axis group ends with identical bytes. */
 int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* bufs,
                    size_t count, int dtype, void* stream);
+
+/* ---- sharded matmul strategies (reference intraop.cpp:141-234) -------- */
+#define APL_EPI_NONE 0
+#define APL_EPI_GELU 1 /* exact erf GELU, applied after any partial-sum reduction */
+
+/* One SPMD matmul strategy of the reference catalog: C[..m.., n] = A[..m.., k]
+ * . B[k, n]; specs are on the LOGICAL tensors exactly as the reference writes
+ * them (OpStrategy, intraop.hpp:34-49). partial_sum strategies (split-k
+ * forms) all-reduce C over reduce_axes. */
+typedef struct {
+  apl_spec a;
+  apl_spec b;
+  apl_spec c;
+  int32_t partial_sum;
+  int32_t nreduce;
+  int32_t reduce_axes[APL_MAX_MESH];
+} apl_matmul_strategy;
+
+/* Local dense contraction on the tcgen05 tensor cores:
+ * C[M,N] = epi(A[M,K] . Bt[N,K]^T); A, Bt bf16 with unit stride along K
+ * (Bt = nn.Linear weight layout), fp32 accumulation, C bf16 or f32. */
+int apl_gemm_bf16(const void* A, const void* Bt, void* C, int64_t M, int64_t N, int64_t K,
+                  int64_t lda, int64_t ldb, int64_t ldc, int out_dtype, int epilogue,
+                  void* stream);
+
+/* Execute a strategy on the mesh: per local device one tcgen05 GEMM on its
+ * shards (A: local shard of A; Bt: local shard of B stored transposed,
+ * [n_local, k_local]; C: local shard of C), then the partial-sum all-reduce
+ * over reduce_axes, then the epilogue if it could not be fused. */
+int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
+                       const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
+                       const void* const* Bt, void* const* C, int out_dtype, int epilogue,
+                       void* stream);
 
 /* Kernel launches this process issued through the library (evidence). */
 int apl_launch_count(uint64_t* launches);

@@ -18,6 +18,7 @@ OK, ERR_SCHEMA, ERR_AXIS, ERR_SHAPE, ERR_RANK, ERR_INFEASIBLE, ERR_CUDA, ERR_NCC
 FUSE_CHAIN = 1
 STEPWISE = 0
 F32, BF16, F16 = 0, 1, 2
+EPI_NONE, EPI_GELU = 0, 1
 
 
 class Spec(C.Structure):
@@ -37,6 +38,11 @@ class Step(C.Structure):
 class MeshDesc(C.Structure):
     _fields_ = [("ndim", C.c_int32), ("shape", C.c_int64 * MAX_MESH),
                 ("alpha", C.c_double * MAX_MESH), ("beta_inv", C.c_double * MAX_MESH)]
+
+
+class MatmulStrategyC(C.Structure):
+    _fields_ = [("a", Spec), ("b", Spec), ("c", Spec), ("partial_sum", C.c_int32),
+                ("nreduce", C.c_int32), ("reduce_axes", C.c_int32 * MAX_MESH)]
 
 
 class PieceC(C.Structure):
@@ -88,8 +94,16 @@ _SIGS = {
     "apl_run_path": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Step), C.c_int, P(Meta),
                                P(C.c_void_p), P(C.c_void_p), C.c_void_p, C.c_size_t, C.c_uint,
                                C.c_void_p]),
+    "apl_exchange_traffic": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_int64),
+                                       P(C.c_int64), P(C.c_int64)]),
     "apl_all_reduce": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_int, P(C.c_void_p), C.c_size_t,
                                  C.c_int, C.c_void_p]),
+    "apl_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                C.c_void_p]),
+    "apl_sharded_matmul": (C.c_int, [C.c_void_p, P(MatmulStrategyC), P(Meta), P(Meta),
+                                     P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
+                                     C.c_int, C.c_void_p]),
     "apl_launch_count": (C.c_int, [P(C.c_uint64)]),
 }
 

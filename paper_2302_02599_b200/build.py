@@ -44,6 +44,7 @@ HOST_SRCS = [
     CSRC / "host" / "search.cpp",
     CSRC / "runtime" / "plan.cpp",
     CSRC / "runtime" / "runtime.cpp",
+    CSRC / "runtime" / "matmul.cpp",
     CSRC / "capi.cpp",
 ]
 CUDA_SRCS = [

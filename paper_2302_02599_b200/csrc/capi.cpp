@@ -3,6 +3,7 @@
 // (reference errors.hpp:25-108) and runtime failures onto apl_status codes.
 #include "apl.h"
 
+#include <climits>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -466,6 +467,28 @@ int apl_run_path(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt, const
   });
 }
 
+int apl_exchange_traffic(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                         const apl_meta* meta, int64_t* hbm_read, int64_t* hbm_write,
+                         int64_t* wire_in) {
+  return guarded([&] {
+    need(mesh, "null mesh");
+    const ShardingSpec s = to_spec(src), g = to_spec(tgt);
+    const TensorMeta t = to_meta(meta);
+    if (!s.valid_for(t, mesh->impl.geo) || !g.valid_for(t, mesh->impl.geo))
+      throw autoplan::ShapeError("spec is not valid for the tensor/mesh");
+    auto ex = apl::get_exchange(mesh->impl, s, g, t);
+    int64_t r = 0, w = 0;
+    for (const auto* list : {&ex->host_copies, &ex->host_pre, &ex->host_post})
+      for (const apl::CopyDesc& c : *list) {
+        r += c.bytes();
+        w += c.bytes() * c.ndst;
+      }
+    if (hbm_read) *hbm_read = r;
+    if (hbm_write) *hbm_write = w;
+    if (wire_in) *wire_in = ex->wire_bytes_in;
+  });
+}
+
 int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* bufs,
                    size_t count, int dtype, void* stream) {
   return guarded([&] {
@@ -473,6 +496,46 @@ int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* 
     need(dtype >= APL_F32 && dtype <= APL_F16, "bad dtype");
     apl::all_reduce(mesh->impl, std::vector<int>(axes, axes + naxes), bufs, count, dtype,
                     static_cast<cudaStream_t>(stream));
+  });
+}
+
+int apl_gemm_bf16(const void* A, const void* Bt, void* C, int64_t M, int64_t N, int64_t K,
+                  int64_t lda, int64_t ldb, int64_t ldc, int out_dtype, int epilogue,
+                  void* stream) {
+  return guarded([&] {
+    need(A && Bt && C, "null operand");
+    need(M >= 0 && N >= 0 && K >= 0 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX,
+         "extents out of range");
+    need(lda >= K && ldb >= K && ldc >= N, "leading dimensions too small");
+    need(out_dtype == APL_F32 || out_dtype == APL_BF16, "output dtype must be f32 or bf16");
+    need(epilogue == APL_EPI_NONE || epilogue == APL_EPI_GELU, "unknown epilogue");
+    apl::check_cuda(apl::gemm_bf16_tn(A, Bt, C, static_cast<int>(M), static_cast<int>(N),
+                                      static_cast<int>(K), static_cast<int>(lda),
+                                      static_cast<int>(ldb), static_cast<int>(ldc),
+                                      out_dtype == APL_F32, epilogue == APL_EPI_GELU,
+                                      static_cast<cudaStream_t>(stream)),
+                    "apl_gemm_bf16");
+  });
+}
+
+int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
+                       const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
+                       const void* const* Bt, void* const* C, int out_dtype, int epilogue,
+                       void* stream) {
+  return guarded([&] {
+    need(mesh && strategy && A && Bt && C, "null argument");
+    need(out_dtype == APL_F32 || out_dtype == APL_BF16, "output dtype must be f32 or bf16");
+    need(epilogue == APL_EPI_NONE || epilogue == APL_EPI_GELU, "unknown epilogue");
+    need(strategy->nreduce >= 0 && strategy->nreduce <= APL_MAX_MESH, "bad reduce axis count");
+    apl::MatmulStrategy s;
+    s.a = to_spec(&strategy->a);
+    s.b = to_spec(&strategy->b);
+    s.c = to_spec(&strategy->c);
+    s.partial_sum = strategy->partial_sum != 0;
+    for (int i = 0; i < strategy->nreduce; ++i) s.reduce_axes.push_back(strategy->reduce_axes[i]);
+    need(s.partial_sum == !s.reduce_axes.empty(), "partial_sum iff reduce axes are given");
+    apl::sharded_matmul(mesh->impl, s, to_meta(a_meta), to_meta(b_meta), A, Bt, C, out_dtype,
+                        epilogue, static_cast<cudaStream_t>(stream));
   });
 }
 

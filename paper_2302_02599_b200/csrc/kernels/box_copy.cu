@@ -1,14 +1,16 @@
 // Batched N-D box copy kernel (sm_100a). See box_copy.cuh for the model.
 //
-// Roofline: HBM. Algorithmic bytes per launch = 2 x sum of descriptor bytes
-// (every byte is read once and written once). Design points:
+// Roofline: HBM. Algorithmic bytes per launch = sum over descriptors of
+// (bytes read once + bytes written to each destination). Design points:
 //  * persistent grid (a multiple of the SM count), each CTA sweeping chunks
 //    of blockDim * U units; U independent 128-bit loads are issued before
 //    any store so every thread keeps U x 16 B in flight;
-//  * the chunk's descriptor is staged in shared memory once per chunk, so
-//    the per-unit address math is two multiply-high divisions per outer dim
-//    against smem-resident constants (no per-unit global descriptor loads
-//    unless a chunk straddles two descriptors);
+//  * the chunk's descriptor is staged in shared memory once per chunk and
+//    then held in registers (the kernel is specialised on the largest outer
+//    rank NO of the table), so the per-unit address math is one multiply-
+//    high division per outer dim plus the run division;
+//  * fan-out descriptors: one load, up to 8 stores (replicated targets on a
+//    simulated mesh read their source bytes once);
 //  * loads use the non-coherent streaming path (ld.global.nc.L1::no_allocate),
 //    stores are plain 128-bit st.global (data is consumed by the next kernel
 //    or a collective, so it should stay in L2 when it fits).
@@ -16,6 +18,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -72,7 +76,7 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
   return f.div == 1 ? n : (__umulhi(n, f.mul) >> f.shr);
 }
 
-// Resolves unit `local` of descriptor `c` into (src, dst) byte offsets.
+// Generic resolution straight from a (global or shared) descriptor.
 template <int V>
 __device__ __forceinline__ void resolve(const DevCopy& c, uint32_t local, int64_t& so,
                                         int64_t& dd) {
@@ -89,11 +93,12 @@ __device__ __forceinline__ void resolve(const DevCopy& c, uint32_t local, int64_
   }
 }
 
-template <int V, int U>
-__global__ void __launch_bounds__(256, 4)
+template <int V, int U, int NO, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     box_copy_kernel(const DevCopy* __restrict__ table, int ntasks, int64_t total,
                     const __grid_constant__ PtrTable ptrs) {
   using T = typename Vec<V>::T;
+  constexpr int NR = NO > 0 ? NO : 1;
   __shared__ DevCopy s_desc;
   __shared__ int s_task;
   __shared__ int64_t s_next_begin;
@@ -120,42 +125,134 @@ __global__ void __launch_bounds__(256, 4)
         s[w] = g[w];
     }
     __syncthreads();
+    // Register copy of the chunk's descriptor.
     const int64_t next_begin = s_next_begin;
+    const int64_t begin = s_desc.unit_begin;
+    const FastDiv upr = s_desc.units_per_run;
+    const int64_t soff = s_desc.src_off, doff = s_desc.dst_off;
+    const int nout = s_desc.nouter;
+    const int ndst = s_desc.ndst;
+    FastDiv ext[NR];
+    int64_t sst[NR], dst_[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      ext[i] = s_desc.ext[i];
+      sst[i] = s_desc.src_stride[i];
+      dst_[i] = s_desc.dst_stride[i];
+    }
+    const char* sp0 = ptrs.src[s_desc.src_buf];
+    // destination buffer ids, 4 per register; pointers come from the param bank at store time
+    uint32_t dbuf[2];
+    std::memcpy(dbuf, s_desc.dst_bufs, sizeof(dbuf));
 
     T v[U];
-    char* dst[U];
+    int64_t dd[U];
+    int slow_task[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t g = base + static_cast<int64_t>(u) * blockDim.x + threadIdx.x;
-      dst[u] = nullptr;
+      slow_task[u] = -2;  // -2: nothing, -1: fast path, >= 0: descriptor index
       if (g < total) {
-        int64_t so, dd;
+        int64_t so;
         const char* sp;
-        char* dp;
         if (g < next_begin) {
-          resolve<V>(s_desc, static_cast<uint32_t>(g - s_desc.unit_begin), so, dd);
-          sp = ptrs.src[s_desc.src_buf];
-          dp = ptrs.dst[s_desc.dst_buf];
+          uint32_t row = fdiv(static_cast<uint32_t>(g - begin), upr);
+          const uint32_t col = static_cast<uint32_t>(g - begin) - row * upr.div;
+          so = soff + static_cast<int64_t>(col) * V;
+          dd[u] = doff + static_cast<int64_t>(col) * V;
+          if constexpr (NO > 0) {
+#pragma unroll
+            for (int i = NO - 1; i >= 0; --i) {
+              if (i < nout) {
+                const uint32_t q = fdiv(row, ext[i]);
+                const uint32_t r = row - q * ext[i].div;
+                so += static_cast<int64_t>(r) * sst[i];
+                dd[u] += static_cast<int64_t>(r) * dst_[i];
+                row = q;
+              }
+            }
+          }
+          sp = sp0;
+          slow_task[u] = -1;
         } else {  // chunk straddles descriptors: walk forward in global
           int t = t0 + 1;
           while (t + 1 < ntasks && table[t + 1].unit_begin <= g) ++t;
           const DevCopy& c = table[t];
-          resolve<V>(c, static_cast<uint32_t>(g - c.unit_begin), so, dd);
+          resolve<V>(c, static_cast<uint32_t>(g - c.unit_begin), so, dd[u]);
           sp = ptrs.src[c.src_buf];
-          dp = ptrs.dst[c.dst_buf];
+          slow_task[u] = t;
         }
         v[u] = load_stream(reinterpret_cast<const T*>(sp + so));
-        dst[u] = dp + dd;
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (dst[u] != nullptr) *reinterpret_cast<T*>(dst[u]) = v[u];
+    for (int u = 0; u < U; ++u) {
+      if (slow_task[u] == -1) {
+#pragma unroll
+        for (int j = 0; j < kCopyMaxFan; ++j)
+          if (j < ndst)
+            *reinterpret_cast<T*>(ptrs.dst[(dbuf[j >> 2] >> (8 * (j & 3))) & 0xFF] + dd[u]) = v[u];
+      } else if (slow_task[u] >= 0) {
+        const DevCopy& c = table[slow_task[u]];
+        for (int j = 0; j < c.ndst; ++j)
+          *reinterpret_cast<T*>(ptrs.dst[c.dst_bufs[j]] + dd[u]) = v[u];
+      }
+    }
     __syncthreads();  // s_desc is rewritten by the next chunk
   }
 }
 
 int g_num_sms = 0;
+
+}  // namespace
+int sm_count();
+namespace {
+
+// Tiling variants: (U units in flight per thread, min resident CTAs per SM).
+// 0: U=8 @ 2 CTAs/SM (128 regs, no spills; default); 1: U=4 @ 4 CTAs/SM.
+int copy_variant() {
+  static int v = [] {
+    const char* e = std::getenv("APL_COPY_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int V, int U, int MINB>
+void launch_vu(int no, int grid, const DevCopy* t, int n, int64_t total, const PtrTable& p,
+               cudaStream_t s) {
+  constexpr int kThreads = 256;
+  switch (no) {
+    case 0:
+      box_copy_kernel<V, U, 0, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      break;
+    case 1:
+      box_copy_kernel<V, U, 1, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      break;
+    case 2:
+      box_copy_kernel<V, U, 2, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      break;
+    case 3:
+      box_copy_kernel<V, U, 3, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      break;
+    default:
+      box_copy_kernel<V, U, kCopyMaxOuter, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      break;
+  }
+}
+
+template <int V>
+void launch_v(int no, int64_t total_units, const DevCopy* t, int n, const PtrTable& p,
+              cudaStream_t s) {
+  const int variant = copy_variant();
+  const int u = variant == 1 ? 4 : 8;
+  const int minb = variant == 1 ? 4 : 2;
+  const int64_t chunk = 256 * u;
+  const int64_t chunks = (total_units + chunk - 1) / chunk;
+  const int grid = static_cast<int>(std::min<int64_t>(chunks, static_cast<int64_t>(sm_count()) * minb));
+  if (variant == 1) launch_vu<V, 4, 4>(no, grid, t, n, total_units, p, s);
+  else launch_vu<V, 8, 2>(no, grid, t, n, total_units, p, s);
+}
 
 }  // namespace
 
@@ -185,29 +282,24 @@ int sm_count() {
 }
 
 cudaError_t launch_box_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
-                            int vec_bytes, const PtrTable& ptrs, cudaStream_t stream) {
+                            int vec_bytes, int max_outer, const PtrTable& ptrs,
+                            cudaStream_t stream) {
   if (ntasks <= 0 || total_units <= 0) return cudaSuccess;
-  constexpr int kThreads = 256;
-  constexpr int kUnroll = 4;
-  const int64_t chunk = static_cast<int64_t>(kThreads) * kUnroll;
-  const int64_t chunks = (total_units + chunk - 1) / chunk;
-  const int64_t cap = static_cast<int64_t>(sm_count()) * 4;  // 4 resident CTAs per SM
-  const int grid = static_cast<int>(std::min(chunks, cap));
   switch (vec_bytes) {
     case 16:
-      box_copy_kernel<16, kUnroll><<<grid, kThreads, 0, stream>>>(d_table, ntasks, total_units, ptrs);
+      launch_v<16>(max_outer, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 8:
-      box_copy_kernel<8, kUnroll><<<grid, kThreads, 0, stream>>>(d_table, ntasks, total_units, ptrs);
+      launch_v<8>(max_outer, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 4:
-      box_copy_kernel<4, kUnroll><<<grid, kThreads, 0, stream>>>(d_table, ntasks, total_units, ptrs);
+      launch_v<4>(max_outer, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 2:
-      box_copy_kernel<2, kUnroll><<<grid, kThreads, 0, stream>>>(d_table, ntasks, total_units, ptrs);
+      launch_v<2>(max_outer, total_units, d_table, ntasks, ptrs, stream);
       break;
     default:
-      box_copy_kernel<1, kUnroll><<<grid, kThreads, 0, stream>>>(d_table, ntasks, total_units, ptrs);
+      launch_v<1>(max_outer, total_units, d_table, ntasks, ptrs, stream);
       break;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -5,6 +5,9 @@
 // A launch executes a table of copy descriptors. Each descriptor moves
 // rows x run bytes, where a row is addressed by up to 7 outer indices
 // (strides in bytes on both sides) and the run is contiguous on both sides.
+// A descriptor may fan out to several destination buffers at the same
+// offset (one read, `ndst` writes): on a simulated mesh every receiver of a
+// replicated block takes the same bytes, so they are read from HBM once.
 // The work is flattened into "units" of V bytes (V = 16 whenever every run,
 // stride, offset and base pointer allows it), so one persistent grid sweeps
 // all descriptors with coalesced 128-bit loads/stores regardless of how the
@@ -17,6 +20,7 @@ namespace apl {
 
 constexpr int kCopyMaxOuter = 7;
 constexpr int kCopyMaxPtrs = 66;  // 64 simulated devices + 2 staging buffers
+constexpr int kCopyMaxFan = 8;    // destinations per descriptor
 
 // Division by a runtime-invariant uint32 via multiply-high (n < 2^31).
 struct FastDiv {
@@ -29,7 +33,9 @@ struct DevCopy {
   int64_t src_stride[kCopyMaxOuter], dst_stride[kCopyMaxOuter];
   FastDiv ext[kCopyMaxOuter];
   FastDiv units_per_run;
-  int32_t src_buf, dst_buf, nouter, pad_;
+  int32_t src_buf, nouter, ndst;
+  uint8_t dst_bufs[kCopyMaxFan];
+  int32_t pad_;
 };
 
 struct PtrTable {

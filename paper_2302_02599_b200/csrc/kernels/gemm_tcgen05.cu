@@ -1,0 +1,347 @@
+// Dense bf16 GEMM on the 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+//   C[M,N] = epilogue( A[M,K] . Bt[N,K]^T ),  A, Bt bf16 K-contiguous
+//   (Bt is the nn.Linear weight layout [out_features, in_features]),
+//   fp32 accumulation in TMEM, output bf16 or fp32, optional exact-erf GELU.
+//
+// This is the local contraction of every sharded-matmul strategy of the
+// reference catalog (proj/src/intraop.cpp:141-234): each device multiplies
+// its shards; the strategy's layout conversions and partial-sum all-reduce
+// run around it in the runtime.
+//
+// Kernel shape (one CTA per 128 x BN output tile, 6 warps, warp-specialized):
+//   warp 0       TMA producer: 64-wide K slabs of A (128 rows) and Bt (BN
+//                rows) into a kStages-deep smem ring, 128B swizzle,
+//                mbarrier complete_tx;
+//   warp 1       owns the TMEM allocation; lane 0 issues tcgen05.mma
+//                (M=128, N=BN, K=16 per instruction, cta_group::1) and
+//                tcgen05.commit's each ring slot back to the producer;
+//   warps 2..5   epilogue: tcgen05.ld 32x32b.x16 from TMEM (warp w reads
+//                lanes 32*(w%4)..+31), GELU / convert, 16-column stores.
+// Tails in M, N and K are handled by TMA zero fill plus masked stores.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+namespace apl {
+
+extern std::atomic<uint64_t> g_launches;
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // one 128-byte swizzle row of bf16
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// K-major, 128B-swizzled operand tile: rows of 128 B, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc(const void* tile) {
+  const uint64_t addr = smem_addr(tile);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;          // start address
+  d |= uint64_t(1) << 16;                // leading byte offset (unused for swizzled K-major)
+  d |= uint64_t(1024 >> 4) << 32;        // stride byte offset: 8 rows x 128 B
+  d |= uint64_t(1) << 46;                // descriptor version (sm_100)
+  d |= uint64_t(2) << 61;                // SWIZZLE_128B
+  return d;
+}
+
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t instr_desc() {
+  return (1u << 4)                     // D = f32
+         | (1u << 7)                   // A = bf16
+         | (1u << 10)                  // B = bf16
+         | (uint32_t(BN >> 3) << 17)   // N
+         | (uint32_t(kBM >> 4) << 24); // M
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float gelu_erf(float x) {
+  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+
+template <int BN>
+struct Smem {
+  static constexpr int kStageA = kBM * kBK * 2;
+  static constexpr int kStageB = BN * kBK * 2;
+  static constexpr int kStages = (BN >= 256) ? 4 : 6;
+  static constexpr int kData = kStages * (kStageA + kStageB);
+  static constexpr int kBytes = kData + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool kGelu, bool kOutF32>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b, void* __restrict__ out, int M,
+                      int N, int K, int ldc) {
+  using S = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* tiles_a = base;
+  uint8_t* tiles_b = base + S::kStages * S::kStageA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + S::kData);
+  uint64_t* empty = full + S::kStages;
+  uint64_t* done = empty + S::kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * kBM;
+  const int n0 = blockIdx.x * BN;
+  const int kblocks = (K + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 1) {  // whole warp allocates BN fp32 columns of TMEM
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % S::kStages;
+        const uint32_t phase = (kb / S::kStages) & 1;
+        mbar_wait(&empty[s], phase ^ 1);
+        mbar_expect_tx(&full[s], S::kStageA + S::kStageB);
+        tma_load_2d(tiles_a + s * S::kStageA, &map_a, &full[s], kb * kBK, m0);
+        tma_load_2d(tiles_b + s * S::kStageB, &map_b, &full[s], kb * kBK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc<BN>();
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % S::kStages;
+        const uint32_t phase = (kb / S::kStages) & 1;
+        mbar_wait(&full[s], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = smem_desc(tiles_a + s * S::kStageA);
+        const uint64_t db = smem_desc(tiles_b + s * S::kStageB);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          // advance 16 bf16 = 32 B along K inside the swizzle row
+          mma_bf16(tmem, da + uint64_t(2 * k), db + uint64_t(2 * k), idesc,
+                   (kb > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
+      }
+      mma_commit(done);  // accumulator complete
+    }
+  } else {
+    // Epilogue warps 2..5 -> TMEM lane quarter (warp % 4).
+    const int quarter = warp % 4;
+    const int row = m0 + quarter * 32 + lane;
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t r[16];
+      tmem_ld16(lane_addr + uint32_t(c), r);
+      const int col = n0 + c;
+      if (row >= M || col >= N) continue;
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        v[i] = __uint_as_float(r[i]);
+        if (kGelu) v[i] = gelu_erf(v[i]);
+      }
+      if constexpr (kOutF32) {
+        float* dst = static_cast<float*>(out) + static_cast<size_t>(row) * ldc + col;
+        if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+          for (int i = 0; i < 16 && col + i < N; ++i) dst[i] = v[i];
+        }
+      } else {
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(row) * ldc + col;
+        if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          uint32_t p[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            std::memcpy(&p[i], &h, 4);
+          }
+          reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+          reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        } else {
+          for (int i = 0; i < 16 && col + i < N; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+        }
+      }
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---- host side ---------------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeFn>(nullptr);
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int box_rows) {
+  EncodeFn enc = encode_fn();
+  if (enc == nullptr) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t elem[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+             elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool G, bool F>
+cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, void* c, int M, int N, int K,
+                        int ldc, cudaStream_t stream) {
+  auto kernel = gemm_bf16_tcgen05<BN, G, F>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Smem<BN>::kBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((N + BN - 1) / BN, (M + kBM - 1) / kBM);
+  kernel<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(a, b, c, M, N, K, ldc);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// C[M,N] = A[M,K] . Bt[N,K]^T (bf16 in, fp32 accumulate). out_f32 selects the
+// output type; gelu applies exact-erf GELU in the epilogue.
+cudaError_t gemm_bf16_tn(const void* A, const void* Bt, void* C, int M, int N, int K, int lda,
+                         int ldb, int ldc, bool out_f32, bool gelu, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(Bt) & 15) ||
+      (lda * 2) % 16 || (ldb * 2) % 16)
+    return cudaErrorInvalidValue;  // TMA needs 16-byte aligned rows
+  const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, lda, kBM) || !make_map(&mb, Bt, N, K, ldb, bn))
+    return cudaErrorInvalidValue;
+#define APL_GEMM_CASE(BN_, G_, F_) \
+  if (bn == BN_ && gelu == G_ && out_f32 == F_) return launch_gemm<BN_, G_, F_>(ma, mb, C, M, N, K, ldc, stream);
+  APL_GEMM_CASE(256, false, false)
+  APL_GEMM_CASE(256, true, false)
+  APL_GEMM_CASE(256, false, true)
+  APL_GEMM_CASE(256, true, true)
+  APL_GEMM_CASE(128, false, false)
+  APL_GEMM_CASE(128, true, false)
+  APL_GEMM_CASE(128, false, true)
+  APL_GEMM_CASE(128, true, true)
+#undef APL_GEMM_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace apl

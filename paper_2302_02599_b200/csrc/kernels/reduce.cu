@@ -9,6 +9,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 
@@ -113,6 +114,41 @@ cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int gr
     default:
       return cudaErrorInvalidValue;
   }
+}
+
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) gelu_inplace(T* __restrict__ buf, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float x = to_f(buf[i]);
+    buf[i] = from_f<T>(0.5f * x * (1.f + erff(x * 0.70710678118654752f)));
+  }
+}
+
+}  // namespace
+
+// Exact-erf GELU over a buffer (the epilogue of partial-sum strategies,
+// applied once the all-reduce has produced the full sums).
+cudaError_t launch_gelu_inplace(void* buf, size_t count, int dtype, cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 16));
+  switch (dtype) {
+    case 0:
+      gelu_inplace<float><<<grid, 256, 0, stream>>>(static_cast<float*>(buf), count);
+      break;
+    case 1:
+      gelu_inplace<__nv_bfloat16><<<grid, 256, 0, stream>>>(static_cast<__nv_bfloat16*>(buf), count);
+      break;
+    case 2:
+      gelu_inplace<__half><<<grid, 256, 0, stream>>>(static_cast<__half*>(buf), count);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
 }
 
 uint64_t launch_count() { return g_launches.load(); }

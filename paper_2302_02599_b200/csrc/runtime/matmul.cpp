@@ -1,0 +1,63 @@
+// Sharded-matmul strategy execution: local tcgen05 GEMM on each device's
+// shards, partial-sum all-reduce over the strategy's reduce axes, epilogue.
+//
+// Strategy semantics follow the reference catalog (proj/src/intraop.cpp:
+// 141-234): C[..m.., n] = A[..m.., k] . B[k, n] with the input/output specs
+// of the strategy; partial_sum strategies (split-k and the k-containing
+// pairs) leave per-device partial sums that are reduced over reduce_axes
+// (priced at intraop.cpp:544-551, inserted as <host>.ar nodes at
+// planner.cpp:263-282).
+#include <algorithm>
+
+#include "apl.h"
+#include "runtime.hpp"
+
+namespace apl {
+
+void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorMeta& a_meta,
+                    const autoplan::TensorMeta& b_meta, const void* const* A,
+                    const void* const* Bt, void* const* C, int out_dtype, int epilogue,
+                    cudaStream_t stream) {
+  const auto& geo = mesh.geo;
+  if (b_meta.rank() != 2 || a_meta.rank() < 2)
+    throw RuntimeError(APL_ERR_SHAPE, "matmul wants A[..m.., k] and B[k, n]");
+  if (a_meta.dtype_bytes != 2 || b_meta.dtype_bytes != 2)
+    throw RuntimeError(APL_ERR_ARG, "matmul operands must be bf16");
+  if (a_meta.shape.back() != b_meta.shape[0])
+    throw RuntimeError(APL_ERR_SHAPE, "contraction extents differ");
+  autoplan::TensorMeta c_meta = a_meta;
+  c_meta.shape.back() = b_meta.shape[1];
+  c_meta.dtype_bytes = out_dtype == APL_F32 ? 4 : 2;
+  if (!s.a.valid_for(a_meta, geo) || !s.b.valid_for(b_meta, geo) || !s.c.valid_for(c_meta, geo))
+    throw RuntimeError(APL_ERR_SHAPE, "strategy specs are not valid for these tensors");
+  const auto la = local_shape(s.a, geo, a_meta);
+  const auto lb = local_shape(s.b, geo, b_meta);
+  const auto lc = local_shape(s.c, geo, c_meta);
+  int64_t m = 1;
+  for (size_t i = 0; i + 1 < la.size(); ++i) {
+    m *= la[i];
+    if (la[i] != lc[i]) throw RuntimeError(APL_ERR_SHAPE, "A and C shards disagree on m dims");
+  }
+  const int64_t k = la.back(), n = lb[1];
+  if (lb[0] != k || lc.back() != n)
+    throw RuntimeError(APL_ERR_SHAPE, "local shards do not form a matmul");
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+    throw RuntimeError(APL_ERR_ARG, "local GEMM extents exceed int32");
+  const bool fuse_gelu = epilogue == APL_EPI_GELU && !s.partial_sum;
+  const int nl = mesh.num_local();
+  for (int d = 0; d < nl; ++d) {
+    check_cuda(gemm_bf16_tn(A[d], Bt[d], C[d], static_cast<int>(m), static_cast<int>(n),
+                            static_cast<int>(k), static_cast<int>(k), static_cast<int>(k),
+                            static_cast<int>(n), out_dtype == APL_F32, fuse_gelu, stream),
+               "tcgen05 GEMM launch");
+  }
+  if (s.partial_sum) {
+    all_reduce(mesh, s.reduce_axes, C, static_cast<size_t>(m * n), out_dtype, stream);
+    if (epilogue == APL_EPI_GELU)
+      for (int d = 0; d < nl; ++d)
+        check_cuda(launch_gelu_inplace(C[d], static_cast<size_t>(m * n), out_dtype, stream),
+                   "gelu launch");
+  }
+}
+
+}  // namespace apl

@@ -57,8 +57,11 @@ std::vector<Piece> pieces_for_sender(const ShardingSpec& src, const ShardingSpec
 // A strided byte copy: `rows` (outer dims, up to kMaxDims-1, innermost last)
 // of `run_bytes` contiguous bytes each.
 struct CopyDesc {
+  static constexpr int kMaxFan = 8;
   int src_buf = 0;  // index into the launch's source pointer table
   int dst_buf = 0;  // index into the launch's destination pointer table
+  int ndst = 1;     // fan-out: the same bytes also land in extra_dst[0..ndst-2]
+  int extra_dst[kMaxFan - 1] = {};
   int64_t src_off = 0, dst_off = 0;  // bytes
   int64_t run_bytes = 0;
   int nouter = 0;

@@ -145,8 +145,11 @@ CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec) {
     h.src_off = d.src_off;
     h.dst_off = d.dst_off;
     h.src_buf = d.src_buf;
-    h.dst_buf = d.dst_buf;
+    h.ndst = d.ndst;
+    h.dst_bufs[0] = static_cast<uint8_t>(d.dst_buf);
+    for (int j = 1; j < d.ndst; ++j) h.dst_bufs[j] = static_cast<uint8_t>(d.extra_dst[j - 1]);
     h.nouter = d.nouter;
+    cc.max_outer = std::max(cc.max_outer, d.nouter);
     const int64_t upr = d.run_bytes / vec;
     h.units_per_run = make_fastdiv(static_cast<uint32_t>(upr));
     int64_t rows = 1;
@@ -158,6 +161,7 @@ CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec) {
     }
     units += upr * rows;
     cc.bytes += d.bytes();
+    cc.write_bytes += d.bytes() * d.ndst;
   }
   cc.ntasks = static_cast<int>(host.size());
   cc.total_units = units;
@@ -175,7 +179,7 @@ void free_copies(CompiledCopies& c) {
 
 void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream) {
   if (c.empty()) return;
-  check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, ptrs, stream),
+  check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, c.max_outer, ptrs, stream),
              "box_copy launch");
 }
 
@@ -207,11 +211,27 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
   ex->out_bytes = tgt.per_device_bytes(meta, mesh.geo);
 
   if (!mesh.distributed) {
+    // Receivers taking the identical box from the same sender at the same
+    // local offset (replicated targets) share one fan-out descriptor, so the
+    // source bytes are read from HBM once.
+    std::map<std::vector<int64_t>, size_t> group;
     for (int64_t q = 0; q < mesh.geo.num_devices(); ++q) {
       for (const Piece& p : pieces_for_receiver(src, tgt, mesh.geo, meta, q)) {
+        if (p.sender != q) ex->wire_bytes_in += p.elements() * eb;
+        std::vector<int64_t> key{p.sender};
+        key.insert(key.end(), p.src_lo.begin(), p.src_lo.end());
+        key.insert(key.end(), p.dst_lo.begin(), p.dst_lo.end());
+        key.insert(key.end(), p.ext.begin(), p.ext.end());
+        auto it = group.find(key);
+        if (it != group.end() && ex->host_copies[it->second].ndst < CopyDesc::kMaxFan) {
+          CopyDesc& c = ex->host_copies[it->second];
+          c.extra_dst[c.ndst - 1] = static_cast<int>(q);
+          ++c.ndst;
+          continue;
+        }
+        group[key] = ex->host_copies.size();
         ex->host_copies.push_back(make_copy(static_cast<int>(p.sender), ls, p.src_lo,
                                             static_cast<int>(q), lt, p.dst_lo, p.ext, eb));
-        if (p.sender != q) ex->wire_bytes_in += p.elements() * eb;
       }
     }
   } else {

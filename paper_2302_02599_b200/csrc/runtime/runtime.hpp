@@ -30,11 +30,23 @@ void check_nccl(ncclResult_t r, const char* what);
 FastDiv make_fastdiv(uint32_t d);
 int sm_count();
 cudaError_t launch_box_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
-                            int vec_bytes, const PtrTable& ptrs, cudaStream_t stream);
+                            int vec_bytes, int max_outer, const PtrTable& ptrs,
+                            cudaStream_t stream);
 cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int groups,
                                    int group_size, size_t count, int dtype,
                                    cudaStream_t stream);
 uint64_t launch_count();
+cudaError_t launch_gelu_inplace(void* buf, size_t count, int dtype, cudaStream_t stream);
+cudaError_t gemm_bf16_tn(const void* A, const void* Bt, void* C, int M, int N, int K, int lda,
+                         int ldb, int ldc, bool out_f32, bool gelu, cudaStream_t stream);
+
+// One sharded-matmul strategy (reference OpStrategy, intraop.hpp:34-49).
+struct MatmulStrategy {
+  autoplan::ShardingSpec a, b, c;  // on logical A[..m.., k], B[k, n], C[..m.., n]
+  bool partial_sum = false;
+  std::vector<int> reduce_axes;
+};
+
 
 // A descriptor table resident on the device.
 struct CompiledCopies {
@@ -42,7 +54,9 @@ struct CompiledCopies {
   int ntasks = 0;
   int64_t total_units = 0;
   int vec = 16;
-  int64_t bytes = 0;  // payload bytes (each read once, written once)
+  int max_outer = 0;
+  int64_t bytes = 0;        // bytes read (each source byte once)
+  int64_t write_bytes = 0;  // bytes written (fan-out counted per destination)
   bool empty() const { return ntasks == 0; }
 };
 
@@ -109,5 +123,10 @@ void run_path(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::Sha
 
 void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, size_t count,
                 int dtype, cudaStream_t stream);
+
+void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorMeta& a_meta,
+                    const autoplan::TensorMeta& b_meta, const void* const* A,
+                    const void* const* Bt, void* const* C, int out_dtype, int epilogue,
+                    cudaStream_t stream);
 
 }  // namespace apl

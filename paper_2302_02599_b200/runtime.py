@@ -37,6 +37,55 @@ def launch_count() -> int:
     return n.value
 
 
+def gemm(a: torch.Tensor, bt: torch.Tensor, out: torch.Tensor | None = None,
+         gelu: bool = False, out_dtype=torch.bfloat16, stream=None) -> torch.Tensor:
+    """out[M,N] = epi(a[M,K] . bt[N,K]^T) on the tcgen05 tensor cores (bf16 in,
+    fp32 accumulate)."""
+    if a.dtype != torch.bfloat16 or bt.dtype != torch.bfloat16:
+        raise TypeError("gemm operands must be bf16")
+    if a.dim() != 2 or bt.dim() != 2 or a.shape[1] != bt.shape[1]:
+        raise ValueError("gemm wants a[M,K], bt[N,K]")
+    if a.stride(1) != 1 or bt.stride(1) != 1:
+        raise ValueError("operands need unit stride along K")
+    m, k = a.shape
+    n = bt.shape[0]
+    if out is None:
+        out = torch.empty(m, n, dtype=out_dtype, device=a.device)
+    code = _DTYPE_CODE[out.dtype]
+    check(A.lib().apl_gemm_bf16(C.c_void_p(a.data_ptr()), C.c_void_p(bt.data_ptr()),
+                                C.c_void_p(out.data_ptr()), m, n, k, a.stride(0), bt.stride(0),
+                                out.stride(0), code, A.EPI_GELU if gelu else A.EPI_NONE,
+                                _stream_handle(stream)))
+    return out
+
+
+class MatmulStrategy:
+    """A reference-catalog strategy (OpStrategy, intraop.hpp:34-49) with specs
+    on the logical A[..m.., k], B[k, n], C[..m.., n]."""
+
+    def __init__(self, name: str, a: ShardingSpec, b: ShardingSpec, c: ShardingSpec,
+                 reduce_axes: Sequence[int] = ()):
+        self.name, self.a, self.b, self.c = name, a, b, c
+        self.reduce_axes = tuple(reduce_axes)
+
+    @property
+    def partial_sum(self) -> bool:
+        return bool(self.reduce_axes)
+
+    def c_struct(self) -> A.MatmulStrategyC:
+        s = A.MatmulStrategyC()
+        s.a, s.b, s.c = self.a.c(), self.b.c(), self.c.c()
+        s.partial_sum = 1 if self.reduce_axes else 0
+        s.nreduce = len(self.reduce_axes)
+        for i, ax in enumerate(self.reduce_axes):
+            s.reduce_axes[i] = ax
+        return s
+
+    def __repr__(self) -> str:
+        return (f"MatmulStrategy({self.name}: {self.a} x {self.b} -> {self.c}"
+                f"{' partial over ' + str(self.reduce_axes) if self.reduce_axes else ''})")
+
+
 class Mesh:
     """An executing DeviceMesh.
 
@@ -154,6 +203,26 @@ class Mesh:
                 for _ in range(self.num_local)]
         self.run_path(path, meta, inputs, outs, fuse, stream)
         return outs
+
+    def exchange_traffic(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta) -> dict:
+        """Algorithmic bytes of the collapsed src->tgt exchange (local devices)."""
+        r, w, wire = C.c_int64(), C.c_int64(), C.c_int64()
+        check(A.lib().apl_exchange_traffic(self._h, C.byref(src.c()), C.byref(tgt.c()),
+                                           C.byref(meta.c()), C.byref(r), C.byref(w),
+                                           C.byref(wire)))
+        return {"hbm_read": r.value, "hbm_write": w.value, "wire_in": wire.value}
+
+    def sharded_matmul(self, strategy: "MatmulStrategy", a_meta: TensorMeta, b_meta: TensorMeta,
+                       a_shards, bt_shards, c_shards, gelu: bool = False, stream=None) -> None:
+        """Local tcgen05 GEMM per device + partial-sum all-reduce (+ epilogue).
+        bt_shards hold each device's B shard transposed: [n_local, k_local]."""
+        for what, bufs in (("A", a_shards), ("Bt", bt_shards), ("C", c_shards)):
+            if len(bufs) != self.num_local:
+                raise ValueError(f"{what}: expected {self.num_local} shards")
+        check(A.lib().apl_sharded_matmul(
+            self._h, C.byref(strategy.c_struct()), C.byref(a_meta.c()), C.byref(b_meta.c()),
+            _ptrs(a_shards), _ptrs(bt_shards), _ptrs(c_shards), _DTYPE_CODE[c_shards[0].dtype],
+            A.EPI_GELU if gelu else A.EPI_NONE, _stream_handle(stream)))
 
     def all_reduce(self, axes: Sequence[int], tensors, stream=None) -> None:
         if not tensors:

@@ -109,7 +109,7 @@ def test_config2_mesh8_gather_and_all_to_all(cuda, eb):
 
 def test_edge_shapes_and_unaligned_runs(cuda):
     cases = [
-        ([2, 3], (6, 9), 1, "S0S1", "S1S0"),     # 3-byte runs, 1-byte vectors
+        ([2, 3], (12, 9), 1, "S0S1", "S10R"),    # 3-byte runs, 1-byte vectors
         ([2, 3], (6, 9), 2, "RS1", "S10R"),
         ([4], (4,), 8, "S0", "R"),               # rank-1, one element per shard
         ([2, 2, 2, 2], (2, 2, 2, 2), 4, "S0S1S2S3", "S3S2S1S0"),  # rank-4, 16 devices

@@ -1,0 +1,73 @@
+"""Times the tcgen05 GEMM (libapl.so) on the config-5 shapes against
+torch.matmul (cuBLAS) and the measured bf16 peak; prints one JSON object.
+
+    python tools/gemm_bench.py [--quick]
+"""
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from paper_2302_02599_b200.runtime import gemm  # noqa: E402
+
+# (name, M, N, K): GPT-2-medium MLP (x[16384,1024], W1[1024,4096], W2[4096,1024])
+SHAPES = [
+    ("fc1 full", 16384, 4096, 1024),
+    ("fc2 full", 16384, 1024, 4096),
+    ("fc1 split-m/8", 2048, 4096, 1024),
+    ("fc2 split-m/8", 2048, 1024, 4096),
+    ("fc1 split-n/8", 16384, 512, 1024),
+    ("fc2 split-k/8", 16384, 1024, 512),
+    ("square 8192", 8192, 8192, 8192),
+]
+
+
+def peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    return json.loads(p.read_text())["bf16_tflops"] if p.exists() else 1590.0
+
+
+def time_fn(fn, iters):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def main():
+    quick = "--quick" in sys.argv
+    shapes = SHAPES[:1] if quick else SHAPES
+    out = {"peak_tflops": peak(), "rows": []}
+    for name, m, n, k in shapes:
+        a = torch.randn(m, k, device="cuda").bfloat16()
+        bt = torch.randn(n, k, device="cuda").bfloat16()
+        c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        flops = 2.0 * m * n * k
+        iters = 3 if quick else 20
+        ms = time_fn(lambda: gemm(a, bt, out=c), iters)
+        ms_g = time_fn(lambda: gemm(a, bt, out=c, gelu=True), iters)
+        ms_cublas = time_fn(lambda: torch.matmul(a, bt.t(), out=c), iters)
+        ref = (a.float() @ bt.float().t())
+        err = ((gemm(a, bt).float() - ref).abs().max() / ref.abs().max()).item()
+        out["rows"].append({
+            "shape": name, "m": m, "n": n, "k": k,
+            "ours_ms": round(ms, 4), "ours_tflops": round(flops / ms / 1e9, 1),
+            "ours_gelu_tflops": round(flops / ms_g / 1e9, 1),
+            "cublas_ms": round(ms_cublas, 4), "cublas_tflops": round(flops / ms_cublas / 1e9, 1),
+            "frac_of_peak": round(flops / ms / 1e9 / out["peak_tflops"], 3),
+            "max_rel_err": err})
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
