@@ -229,7 +229,8 @@ def run_ours(args):
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(f"n{ws}:{dom['name']}")
+        entry = json.loads(tf.read_text()).get(f"n{ws}:{dom['name']}")
+        traffic = entry["dram_bytes"] if entry else None
     if ws == 1:
         achieved = dom["hbm"] / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": f"box_copy_kernel<16,4> ({dom['name']}, 8 simulated devices)",
@@ -410,7 +411,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     args = ap.parse_args()

@@ -201,6 +201,14 @@ int apl_exchange_traffic(apl_mesh* mesh, const apl_spec* src, const apl_spec* tg
                          const apl_meta* meta, int64_t* hbm_read, int64_t* hbm_write,
                          int64_t* wire_in);
 
+/* Host-only dry run of the distributed executor: the exact schedule rank
+ * `rank` would run for the collapsed src->tgt exchange (pack/self copies,
+ * NCCL sends/recvs with their staging offsets, unpack copies) as JSON.
+ * Used to check the N>1 path on CPU (tests/test_distributed_gloo.py). */
+int apl_exchange_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_spec* src,
+                               const apl_spec* tgt, const apl_meta* meta, char* out, size_t cap,
+                               size_t* len);
+
 /* Sum partial results over the mesh axes `axes` (partial_sum strategies,
  * intraop.cpp:544-551; planner.cpp:263-282). In place; every member of an
  * axis group ends with identical bytes. */

@@ -489,6 +489,61 @@ int apl_exchange_traffic(apl_mesh* mesh, const apl_spec* src, const apl_spec* tg
   });
 }
 
+int apl_exchange_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_spec* src,
+                               const apl_spec* tgt, const apl_meta* meta, char* out, size_t cap,
+                               size_t* len) {
+  return guarded([&] {
+    need(len, "null len");
+    apl::Mesh dry;  // no communicators: schedule compilation is host-only
+    dry.geo = to_mesh(mesh);
+    dry.distributed = true;
+    need(rank >= 0 && rank < dry.geo.num_devices(), "rank out of range");
+    dry.rank = rank;
+    const ShardingSpec s = to_spec(src), g = to_spec(tgt);
+    const TensorMeta t = to_meta(meta);
+    if (!s.valid_for(t, dry.geo) || !g.valid_for(t, dry.geo))
+      throw autoplan::ShapeError("spec is not valid for the tensor/mesh");
+    auto ex = apl::get_exchange(dry, s, g, t);
+    std::string j = "{";
+    auto copies = [&](const char* name, const std::vector<apl::CopyDesc>& v) {
+      j += std::string("\"") + name + "\":[";
+      for (size_t i = 0; i < v.size(); ++i) {
+        const apl::CopyDesc& c = v[i];
+        if (i) j += ",";
+        j += "{\"src_buf\":" + std::to_string(c.src_buf) + ",\"dst_buf\":" + std::to_string(c.dst_buf) +
+             ",\"src_off\":" + std::to_string(c.src_off) + ",\"dst_off\":" + std::to_string(c.dst_off) +
+             ",\"run_bytes\":" + std::to_string(c.run_bytes) + ",\"ext\":[";
+        for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.ext[d]);
+        j += "],\"src_stride\":[";
+        for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.src_stride[d]);
+        j += "],\"dst_stride\":[";
+        for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.dst_stride[d]);
+        j += "]}";
+      }
+      j += "],";
+    };
+    auto xfers = [&](const char* name, const std::vector<apl::Exchange::Xfer>& v) {
+      j += std::string("\"") + name + "\":[";
+      for (size_t i = 0; i < v.size(); ++i) {
+        if (i) j += ",";
+        j += "[" + std::to_string(v[i].peer) + "," + (v[i].direct ? "1" : "0") + "," +
+             std::to_string(v[i].offset) + "," + std::to_string(v[i].bytes) + "]";
+      }
+      j += "],";
+    };
+    copies("pre", ex->host_pre);
+    copies("post", ex->host_post);
+    xfers("sends", ex->sends);
+    xfers("recvs", ex->recvs);
+    j += "\"send_staging\":" + std::to_string(ex->send_staging) +
+         ",\"recv_staging\":" + std::to_string(ex->recv_staging) +
+         ",\"workspace\":" + std::to_string(apl::exchange_workspace(*ex)) + "}";
+    *len = j.size() + 1;
+    need(out != nullptr && cap >= j.size() + 1, "output buffer too small");
+    std::memcpy(out, j.c_str(), j.size() + 1);
+  });
+}
+
 int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* bufs,
                    size_t count, int dtype, void* stream) {
   return guarded([&] {

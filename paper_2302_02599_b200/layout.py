@@ -444,3 +444,22 @@ def plan_pieces(mesh: DeviceMesh, src: ShardingSpec, tgt: ShardingSpec, meta: Te
         k = len(meta.shape)
         return [Piece(arr[i].sender, arr[i].receiver, tuple(arr[i].src_lo[:k]),
                       tuple(arr[i].dst_lo[:k]), tuple(arr[i].ext[:k])) for i in range(n.value)]
+
+
+def exchange_schedule(mesh: DeviceMesh, rank: int, src: ShardingSpec, tgt: ShardingSpec,
+                      meta: TensorMeta) -> dict:
+    """Dry run of the distributed executor's schedule for `rank` (host only)."""
+    import json
+
+    n = C.c_size_t()
+    cap = 1 << 16
+    while True:
+        buf = C.create_string_buffer(cap)
+        rc = A.lib().apl_exchange_schedule_json(C.byref(mesh.c()), rank, C.byref(src.c()),
+                                                C.byref(tgt.c()), C.byref(meta.c()), buf, cap,
+                                                C.byref(n))
+        if rc == A.ERR_ARG and n.value > cap:
+            cap = n.value
+            continue
+        check(rc)
+        return json.loads(buf.value.decode())

@@ -113,7 +113,7 @@ def test_edge_shapes_and_unaligned_runs(cuda):
         ([2, 3], (6, 9), 2, "RS1", "S10R"),
         ([4], (4,), 8, "S0", "R"),               # rank-1, one element per shard
         ([2, 2, 2, 2], (2, 2, 2, 2), 4, "S0S1S2S3", "S3S2S1S0"),  # rank-4, 16 devices
-        ([2, 2], (2, 4, 6, 8), 2, "RS0RS1", "S10RRR"),
+        ([2, 2], (4, 4, 6, 8), 2, "RS0RS1", "S10RRR"),
         ([3], (3, 5), 4, "S0R", "RR"),
         ([1, 4], (4, 4), 4, "S1R", "RS01"),      # unit mesh axis
         ([2, 2], (1, 16), 4, "RS01", "RS10"),    # leading unit dim
