@@ -208,20 +208,31 @@ int g_num_sms = 0;
 int sm_count();
 namespace {
 
-// Tiling variants: (U units in flight per thread, min resident CTAs per SM).
-// 0: U=8 @ 2 CTAs/SM (128 regs, no spills; default); 1: U=4 @ 4 CTAs/SM.
+// Tiling variants (16-byte path; narrower vectors always use variant 0):
+//   0: U=8  @ 2 CTAs/SM (128 regs, no spills; default)
+//   1: U=4  @ 4 CTAs/SM
+//   2: U=16 @ 1 CTA/SM
+//   3: U=8  @ 3 CTAs/SM
+// APL_COPY_VARIANT selects one, APL_COPY_CTAS_PER_SM overrides the grid.
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 int copy_variant() {
-  static int v = [] {
-    const char* e = std::getenv("APL_COPY_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
+  static int v = env_int("APL_COPY_VARIANT", 0);
   return v;
 }
 
 template <int V, int U, int MINB>
-void launch_vu(int no, int grid, const DevCopy* t, int n, int64_t total, const PtrTable& p,
+void launch_vu(int no, int64_t total, const DevCopy* t, int n, const PtrTable& p,
                cudaStream_t s) {
   constexpr int kThreads = 256;
+  static int ctas_per_sm = env_int("APL_COPY_CTAS_PER_SM", MINB);
+  const int64_t chunk = int64_t{kThreads} * U;
+  const int64_t chunks = (total + chunk - 1) / chunk;
+  const int grid =
+      static_cast<int>(std::min<int64_t>(chunks, static_cast<int64_t>(sm_count()) * ctas_per_sm));
   switch (no) {
     case 0:
       box_copy_kernel<V, U, 0, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
@@ -244,14 +255,19 @@ void launch_vu(int no, int grid, const DevCopy* t, int n, int64_t total, const P
 template <int V>
 void launch_v(int no, int64_t total_units, const DevCopy* t, int n, const PtrTable& p,
               cudaStream_t s) {
-  const int variant = copy_variant();
-  const int u = variant == 1 ? 4 : 8;
-  const int minb = variant == 1 ? 4 : 2;
-  const int64_t chunk = 256 * u;
-  const int64_t chunks = (total_units + chunk - 1) / chunk;
-  const int grid = static_cast<int>(std::min<int64_t>(chunks, static_cast<int64_t>(sm_count()) * minb));
-  if (variant == 1) launch_vu<V, 4, 4>(no, grid, t, n, total_units, p, s);
-  else launch_vu<V, 8, 2>(no, grid, t, n, total_units, p, s);
+  if constexpr (V == 16) {
+    switch (copy_variant()) {
+      case 1:
+        return launch_vu<V, 4, 4>(no, total_units, t, n, p, s);
+      case 2:
+        return launch_vu<V, 16, 1>(no, total_units, t, n, p, s);
+      case 3:
+        return launch_vu<V, 8, 3>(no, total_units, t, n, p, s);
+      default:
+        break;
+    }
+  }
+  launch_vu<V, 8, 2>(no, total_units, t, n, p, s);
 }
 
 }  // namespace
