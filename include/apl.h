@@ -232,6 +232,20 @@ typedef struct {
   int32_t reduce_axes[APL_MAX_MESH];
 } apl_matmul_strategy;
 
+/* Strategy catalog entry (reference OpStrategy, intraop.hpp:34-49). */
+typedef struct {
+  char name[64];
+  apl_matmul_strategy strategy;
+  double compute_time_s, comm_time_s, bwd_compute_time_s, bwd_comm_time_s;
+  int64_t comm_buffer_bytes, memory_bytes;
+} apl_strategy_info;
+
+/* Every valid strategy of a matmul (batched = 0) or batched matmul on the
+ * mesh, in the reference catalog's order (intraop.cpp:141-234, 497-555). */
+int apl_matmul_strategies(const apl_mesh_desc* mesh, const apl_meta* a_meta,
+                          const apl_meta* b_meta, int batched, double device_flops_per_s,
+                          apl_strategy_info* out, int cap, int* count);
+
 /* Local dense contraction on the tcgen05 tensor cores:
  * C[M,N] = epi(A[M,K] . Bt[N,K]^T); A, Bt bf16 with unit stride along K
  * (Bt = nn.Linear weight layout), fp32 accumulation, C bf16 or f32. */

@@ -193,3 +193,52 @@ double ref_time_paths(const int64_t* mesh, int mr, const int64_t* shape, int ran
 }
 
 }  // extern "C"
+
+// ---- strategy catalog and planner (config 5) -------------------------------
+#include "autoplan/planner.hpp"
+
+extern "C" {
+
+// generate_strategies for one node of a graph document (intraop.cpp:719-767):
+// one line per strategy "name|in0|in1|out|partial|reduce axes|compute|comm|mem".
+int ref_node_strategies(const char* graph_json, const char* node_id, const int64_t* mesh,
+                        int mr, double flops, char* out, size_t cap) {
+  try {
+    ComputationGraph g = parse_graph_text(graph_json);
+    infer_meta(g);
+    DeviceMesh m = DeviceMesh::uniform(std::vector<int64_t>(mesh, mesh + mr), 1e-5, 1e-9, flops);
+    std::ostringstream os;
+    char buf[128];
+    for (const OpStrategy& s : generate_strategies(g, g.node(node_id), m)) {
+      os << s.name << "|";
+      for (const ShardingSpec& in : s.input_specs) os << in.to_string() << "|";
+      os << s.output_spec.to_string() << "|" << (s.partial_sum ? 1 : 0) << "|";
+      for (size_t i = 0; i < s.reduce_axes.size(); ++i) os << (i ? "," : "") << s.reduce_axes[i];
+      std::snprintf(buf, sizeof(buf), "|%.17g|%.17g|%lld\n", s.compute_time_s, s.comm_time_s,
+                    static_cast<long long>(s.memory_bytes));
+      os << buf;
+    }
+    return put(os.str(), out, cap);
+  } catch (const std::exception& e) {
+    put(e.what(), out, cap);
+    return code_of(e);
+  }
+}
+
+// Full planner run (sweep, planner.cpp:91-212) on a uniform mesh; writes the
+// version-1 plan document (plan_to_json, planner.cpp:455-600).
+int ref_plan(const char* graph_json, const int64_t* mesh, int mr, double alpha, double beta_inv,
+             double flops, int64_t device_budget_bytes, char* out, size_t cap) {
+  try {
+    ComputationGraph g = parse_graph_text(graph_json);
+    infer_meta(g);
+    DeviceMesh m = DeviceMesh::uniform(std::vector<int64_t>(mesh, mesh + mr), alpha, beta_inv, flops);
+    ExecutionPlan plan = sweep(g, m, device_budget_bytes);
+    return put(plan_to_json(plan).dump(1), out, cap);
+  } catch (const std::exception& e) {
+    put(e.what(), out, cap);
+    return code_of(e);
+  }
+}
+
+}  // extern "C"

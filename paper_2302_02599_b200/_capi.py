@@ -45,6 +45,13 @@ class MatmulStrategyC(C.Structure):
                 ("nreduce", C.c_int32), ("reduce_axes", C.c_int32 * MAX_MESH)]
 
 
+class StrategyInfoC(C.Structure):
+    _fields_ = [("name", C.c_char * 64), ("strategy", MatmulStrategyC),
+                ("compute_time_s", C.c_double), ("comm_time_s", C.c_double),
+                ("bwd_compute_time_s", C.c_double), ("bwd_comm_time_s", C.c_double),
+                ("comm_buffer_bytes", C.c_int64), ("memory_bytes", C.c_int64)]
+
+
 class PieceC(C.Structure):
     _fields_ = [("sender", C.c_int32), ("receiver", C.c_int32),
                 ("src_lo", C.c_int64 * MAX_DIMS), ("dst_lo", C.c_int64 * MAX_DIMS),
@@ -100,6 +107,8 @@ _SIGS = {
                                              C.c_char_p, C.c_size_t, P(C.c_size_t)]),
     "apl_all_reduce": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_int, P(C.c_void_p), C.c_size_t,
                                  C.c_int, C.c_void_p]),
+    "apl_matmul_strategies": (C.c_int, [P(MeshDesc), P(Meta), P(Meta), C.c_int, C.c_double,
+                                        P(StrategyInfoC), C.c_int, P(C.c_int)]),
     "apl_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                 C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
                                 C.c_void_p]),

@@ -42,6 +42,7 @@ HOST_SRCS = [
     CSRC / "host" / "mesh.cpp",
     CSRC / "host" / "spec.cpp",
     CSRC / "host" / "search.cpp",
+    CSRC / "host" / "strategies.cpp",
     CSRC / "runtime" / "plan.cpp",
     CSRC / "runtime" / "runtime.cpp",
     CSRC / "runtime" / "matmul.cpp",

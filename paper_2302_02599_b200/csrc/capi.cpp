@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "autoplan/layout.hpp"
+#include "autoplan/matmul_strategies.hpp"
 #include "runtime/runtime.hpp"
 
 using autoplan::CollectiveKind;
@@ -551,6 +552,41 @@ int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* 
     need(dtype >= APL_F32 && dtype <= APL_F16, "bad dtype");
     apl::all_reduce(mesh->impl, std::vector<int>(axes, axes + naxes), bufs, count, dtype,
                     static_cast<cudaStream_t>(stream));
+  });
+}
+
+int apl_matmul_strategies(const apl_mesh_desc* mesh, const apl_meta* a_meta,
+                          const apl_meta* b_meta, int batched, double device_flops_per_s,
+                          apl_strategy_info* out, int cap, int* count) {
+  return guarded([&] {
+    need(count, "null count");
+    DeviceMesh m = to_mesh(mesh);
+    m.device_flops_per_s = device_flops_per_s;
+    const TensorMeta a = to_meta(a_meta), b = to_meta(b_meta);
+    need(batched ? (a.rank() == 3 && b.rank() == 3) : (a.rank() >= 2 && b.rank() == 2),
+         "matmul wants A[..m.., k] . B[k, n] (or rank-3 batched operands)");
+    const auto all = autoplan::matmul_strategies(a, b, m, batched != 0);
+    *count = static_cast<int>(all.size());
+    need(static_cast<int>(all.size()) <= cap && (all.empty() || out), "capacity too small");
+    for (size_t i = 0; i < all.size(); ++i) {
+      const autoplan::OpStrategy& s = all[i];
+      apl_strategy_info& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      need(s.name.size() < sizeof(o.name), "strategy name too long");
+      std::memcpy(o.name, s.name.c_str(), s.name.size() + 1);
+      from_spec(s.input_specs[0], &o.strategy.a);
+      from_spec(s.input_specs[1], &o.strategy.b);
+      from_spec(s.output_spec, &o.strategy.c);
+      o.strategy.partial_sum = s.partial_sum ? 1 : 0;
+      o.strategy.nreduce = static_cast<int32_t>(s.reduce_axes.size());
+      for (size_t j = 0; j < s.reduce_axes.size(); ++j) o.strategy.reduce_axes[j] = s.reduce_axes[j];
+      o.compute_time_s = s.compute_time_s;
+      o.comm_time_s = s.comm_time_s;
+      o.bwd_compute_time_s = s.bwd_compute_time_s;
+      o.bwd_comm_time_s = s.bwd_comm_time_s;
+      o.comm_buffer_bytes = s.comm_buffer_bytes;
+      o.memory_bytes = s.memory_bytes;
+    }
   });
 }
 

@@ -209,19 +209,23 @@ int sm_count();
 namespace {
 
 // Tiling variants (16-byte path; narrower vectors always use variant 0):
-//   0: U=8  @ 2 CTAs/SM (128 regs, no spills; default)
-//   1: U=4  @ 4 CTAs/SM
-//   2: U=16 @ 1 CTA/SM
-//   3: U=8  @ 3 CTAs/SM
-// APL_COPY_VARIANT selects one, APL_COPY_CTAS_PER_SM overrides the grid.
+//   0: U=8  @ 2 CTAs/SM (128 regs, no spills)
+//   1: U=4  @ 4 CTAs/SM   -- plain contiguous runs (r01 sweep: 96% of copy peak)
+//   2: U=16 @ 1 CTA/SM    -- fan-out tables (one load, many stores: 92%)
+//   3: U=8  @ 3 CTAs/SM   -- strided boxes (all-to-all packs: 80%)
+// The launch picks by table shape (profiles/r01_copy_sweep.md);
+// APL_COPY_VARIANT forces one, APL_COPY_CTAS_PER_SM overrides the grid.
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
 }
 
-int copy_variant() {
-  static int v = env_int("APL_COPY_VARIANT", 0);
-  return v;
+int copy_variant(int max_outer, int max_fan) {
+  static int forced = env_int("APL_COPY_VARIANT", -1);
+  if (forced >= 0) return forced;
+  if (max_fan > 1) return 2;
+  if (max_outer == 0) return 1;
+  return 3;
 }
 
 template <int V, int U, int MINB>
@@ -253,10 +257,10 @@ void launch_vu(int no, int64_t total, const DevCopy* t, int n, const PtrTable& p
 }
 
 template <int V>
-void launch_v(int no, int64_t total_units, const DevCopy* t, int n, const PtrTable& p,
+void launch_v(int no, int fan, int64_t total_units, const DevCopy* t, int n, const PtrTable& p,
               cudaStream_t s) {
   if constexpr (V == 16) {
-    switch (copy_variant()) {
+    switch (copy_variant(no, fan)) {
       case 1:
         return launch_vu<V, 4, 4>(no, total_units, t, n, p, s);
       case 2:
@@ -298,24 +302,24 @@ int sm_count() {
 }
 
 cudaError_t launch_box_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
-                            int vec_bytes, int max_outer, const PtrTable& ptrs,
+                            int vec_bytes, int max_outer, int max_fan, const PtrTable& ptrs,
                             cudaStream_t stream) {
   if (ntasks <= 0 || total_units <= 0) return cudaSuccess;
   switch (vec_bytes) {
     case 16:
-      launch_v<16>(max_outer, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<16>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 8:
-      launch_v<8>(max_outer, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<8>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 4:
-      launch_v<4>(max_outer, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<4>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 2:
-      launch_v<2>(max_outer, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<2>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
       break;
     default:
-      launch_v<1>(max_outer, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<1>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
       break;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -137,8 +137,15 @@ struct Smem {
   static constexpr int kStages = (BN >= 256) ? 4 : 6;
   static constexpr int kData = kStages * (kStageA + kStageB);
   static constexpr int kBytes = kData + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
 };
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Persistent: CTA b handles tiles b, b + grid, ... (n fastest). The MMA of
+// tile i+1 overlaps the epilogue of tile i through two TMEM accumulators.
 template <int BN, bool kGelu, bool kOutF32>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
@@ -152,29 +159,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* tiles_b = base + S::kStages * S::kStageA;
   uint64_t* full = reinterpret_cast<uint64_t*>(base + S::kData);
   uint64_t* empty = full + S::kStages;
-  uint64_t* done = empty + S::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + S::kStages;  // [2] MMA -> epilogue
+  uint64_t* acc_empty = acc_full + 2;       // [2] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int m0 = blockIdx.y * kBM;
-  const int n0 = blockIdx.x * BN;
   const int kblocks = (K + kBK - 1) / kBK;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int tiles = ((M + kBM - 1) / kBM) * n_tiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
-  if (warp == 1) {  // whole warp allocates BN fp32 columns of TMEM
+  if (warp == 1) {  // whole warp allocates 2 x BN fp32 columns of TMEM
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(tmem_slot)),
-                 "r"(BN));
+                 "r"(S::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -184,78 +195,102 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % S::kStages;
-        const uint32_t phase = (kb / S::kStages) & 1;
-        mbar_wait(&empty[s], phase ^ 1);
-        mbar_expect_tx(&full[s], S::kStageA + S::kStageB);
-        tma_load_2d(tiles_a + s * S::kStageA, &map_a, &full[s], kb * kBK, m0);
-        tma_load_2d(tiles_b + s * S::kStageB, &map_b, &full[s], kb * kBK, n0);
+      int it = 0;  // ring position across tiles
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / n_tiles) * kBM, n0 = (t % n_tiles) * BN;
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % S::kStages;
+          const uint32_t phase = (it / S::kStages) & 1;
+          mbar_wait(&empty[s], phase ^ 1);
+          mbar_expect_tx(&full[s], S::kStageA + S::kStageB);
+          tma_load_2d(tiles_a + s * S::kStageA, &map_a, &full[s], kb * kBK, m0);
+          tma_load_2d(tiles_b + s * S::kStageB, &map_b, &full[s], kb * kBK, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc<BN>();
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % S::kStages;
-        const uint32_t phase = (kb / S::kStages) & 1;
-        mbar_wait(&full[s], phase);
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = smem_desc(tiles_a + s * S::kStageA);
-        const uint64_t db = smem_desc(tiles_b + s * S::kStageB);
+        const uint32_t d = tmem + uint32_t(acc * BN);
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % S::kStages;
+          const uint32_t phase = (it / S::kStages) & 1;
+          mbar_wait(&full[s], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = smem_desc(tiles_a + s * S::kStageA);
+          const uint64_t db = smem_desc(tiles_b + s * S::kStageB);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          // advance 16 bf16 = 32 B along K inside the swizzle row
-          mma_bf16(tmem, da + uint64_t(2 * k), db + uint64_t(2 * k), idesc,
-                   (kb > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < kBK / 16; ++k) {
+            // advance 16 bf16 = 32 B along K inside the swizzle row
+            mma_bf16(d, da + uint64_t(2 * k), db + uint64_t(2 * k), idesc,
+                     (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
         }
-        mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
+        mma_commit(&acc_full[acc]);  // accumulator complete
       }
-      mma_commit(done);  // accumulator complete
     }
   } else {
     // Epilogue warps 2..5 -> TMEM lane quarter (warp % 4).
     const int quarter = warp % 4;
-    const int row = m0 + quarter * 32 + lane;
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16);
+    int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int m0 = (t / n_tiles) * kBM, n0 = (t % n_tiles) * BN;
+      const int row = m0 + quarter * 32 + lane;
+      mbar_wait(&acc_full[acc], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t r[16];
-      tmem_ld16(lane_addr + uint32_t(c), r);
-      const int col = n0 + c;
-      if (row >= M || col >= N) continue;
-      float v[16];
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(lane_addr + uint32_t(c), r);
+        const int col = n0 + c;
+        if (row >= M || col >= N) continue;
+        float v[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        v[i] = __uint_as_float(r[i]);
-        if (kGelu) v[i] = gelu_erf(v[i]);
-      }
-      if constexpr (kOutF32) {
-        float* dst = static_cast<float*>(out) + static_cast<size_t>(row) * ldc + col;
-        if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-          for (int i = 0; i < 16 && col + i < N; ++i) dst[i] = v[i];
+        for (int i = 0; i < 16; ++i) {
+          v[i] = __uint_as_float(r[i]);
+          if (kGelu) v[i] = gelu_erf(v[i]);
         }
-      } else {
-        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(row) * ldc + col;
-        if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-          uint32_t p[8];
+        if constexpr (kOutF32) {
+          float* dst = static_cast<float*>(out) + static_cast<size_t>(row) * ldc + col;
+          if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-            std::memcpy(&p[i], &h, 4);
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (col + i < N) dst[i] = v[i];
           }
-          reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
-          reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
         } else {
-          for (int i = 0; i < 16 && col + i < N; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(row) * ldc + col;
+          if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            uint32_t p[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              std::memcpy(&p[i], &h, 4);
+            }
+            reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+            reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (col + i < N) dst[i] = __float2bfloat16_rn(v[i]);
+          }
         }
       }
+      // All TMEM reads of this buffer are done: hand it back to the MMA warp.
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
   }
 
@@ -263,7 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(S::kTmemCols));
   }
 }
 
@@ -310,7 +346,14 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, void* c, int
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((N + BN - 1) / BN, (M + kBM - 1) / kBM);
+  static int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  const int tiles = ((N + BN - 1) / BN) * ((M + kBM - 1) / kBM);
+  const int grid = tiles < sms ? tiles : sms;
   kernel<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(a, b, c, M, N, K, ldc);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();

@@ -150,6 +150,7 @@ CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec) {
     for (int j = 1; j < d.ndst; ++j) h.dst_bufs[j] = static_cast<uint8_t>(d.extra_dst[j - 1]);
     h.nouter = d.nouter;
     cc.max_outer = std::max(cc.max_outer, d.nouter);
+    cc.max_fan = std::max(cc.max_fan, d.ndst);
     const int64_t upr = d.run_bytes / vec;
     h.units_per_run = make_fastdiv(static_cast<uint32_t>(upr));
     int64_t rows = 1;
@@ -179,7 +180,8 @@ void free_copies(CompiledCopies& c) {
 
 void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream) {
   if (c.empty()) return;
-  check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, c.max_outer, ptrs, stream),
+  check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, c.max_outer, c.max_fan, ptrs,
+                             stream),
              "box_copy launch");
 }
 

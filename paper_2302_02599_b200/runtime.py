@@ -15,6 +15,7 @@ import torch
 from . import _capi as A
 from .layout import (DeviceMesh, ShardingSpec, TensorMeta, TransformPath, TransformStep,
                      check, find_transform_path)
+from .strategies import MatmulStrategy  # noqa: F401  (re-exported)
 
 _DTYPE_CODE = {torch.float32: A.F32, torch.bfloat16: A.BF16, torch.float16: A.F16}
 
@@ -57,33 +58,6 @@ def gemm(a: torch.Tensor, bt: torch.Tensor, out: torch.Tensor | None = None,
                                 out.stride(0), code, A.EPI_GELU if gelu else A.EPI_NONE,
                                 _stream_handle(stream)))
     return out
-
-
-class MatmulStrategy:
-    """A reference-catalog strategy (OpStrategy, intraop.hpp:34-49) with specs
-    on the logical A[..m.., k], B[k, n], C[..m.., n]."""
-
-    def __init__(self, name: str, a: ShardingSpec, b: ShardingSpec, c: ShardingSpec,
-                 reduce_axes: Sequence[int] = ()):
-        self.name, self.a, self.b, self.c = name, a, b, c
-        self.reduce_axes = tuple(reduce_axes)
-
-    @property
-    def partial_sum(self) -> bool:
-        return bool(self.reduce_axes)
-
-    def c_struct(self) -> A.MatmulStrategyC:
-        s = A.MatmulStrategyC()
-        s.a, s.b, s.c = self.a.c(), self.b.c(), self.c.c()
-        s.partial_sum = 1 if self.reduce_axes else 0
-        s.nreduce = len(self.reduce_axes)
-        for i, ax in enumerate(self.reduce_axes):
-            s.reduce_axes[i] = ax
-        return s
-
-    def __repr__(self) -> str:
-        return (f"MatmulStrategy({self.name}: {self.a} x {self.b} -> {self.c}"
-                f"{' partial over ' + str(self.reduce_axes) if self.reduce_axes else ''})")
 
 
 class Mesh:

@@ -1,0 +1,120 @@
+"""Regenerate tests/golden/{strategies,plans}/ from the REFERENCE planner
+(oracle/_ref). Run in the build container:
+
+    make -C oracle && python tests/golden/make_plans.py
+
+strategies.json : the reference catalog (generate_strategies,
+                  proj/src/intraop.cpp:141-234, 497-555, 719-767) for the
+                  GPT-2-medium MLP matmuls and a rank-3 batched case.
+plans/*.json    : version-1 plan documents (plan_to_json, planner.cpp:455-600)
+                  of the reference's full sweep (planner.cpp:91-212) for
+                  BASELINE config 5 on an 8-GPU uniform NVSwitch mesh
+                  (alpha 3 us, 900 GB/s, 1.65 PFLOP/s per device), with the
+                  graph document they were planned from.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent.parent))
+
+from oracle import ref  # noqa: E402
+
+ALPHA, BETA_INV, FLOPS = 3e-6, 1.0 / 900e9, 1.65e15
+
+
+def mlp_graph(tokens=16384, d=1024, hidden=4096, dtype_bytes=2):
+    def node(id_, kind, inputs, shape=None, grad=False):
+        n = {"id": id_, "kind": kind, "inputs": [[i, 0] for i in inputs], "outputs": []}
+        if shape is not None:
+            n["outputs"] = [{"shape": list(shape), "dtype_bytes": dtype_bytes,
+                             "requires_grad": grad}]
+        return n
+
+    return {"version": 1, "placeholders": ["x"], "output": "out", "nodes": [
+        node("x", "placeholder", [], (tokens, d)),
+        node("w1", "parameter", [], (d, hidden), True),
+        node("w2", "parameter", [], (hidden, d), True),
+        node("fc1", "matmul", ["x", "w1"]),
+        node("gelu", "elementwise-unary", ["fc1"]),
+        node("fc2", "matmul", ["gelu", "w2"]),
+        node("out", "output", ["fc2"]),
+    ]}
+
+
+def bmm_graph():
+    def node(id_, kind, inputs, shape=None, grad=False):
+        n = {"id": id_, "kind": kind, "inputs": [[i, 0] for i in inputs], "outputs": []}
+        if shape is not None:
+            n["outputs"] = [{"shape": list(shape), "dtype_bytes": 2, "requires_grad": grad}]
+        return n
+
+    return {"version": 1, "placeholders": ["a", "b"], "output": "out", "nodes": [
+        node("a", "placeholder", [], (16, 64, 32)), node("b", "placeholder", [], (16, 32, 48)),
+        node("bmm", "batched-matmul", ["a", "b"]), node("out", "output", ["bmm"])]}
+
+
+def node_strategies(graph, node_id, mesh):
+    lib = ref.lib()
+    lib.ref_node_strategies.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_int64), C.c_int,
+                                        C.c_double, C.c_char_p, C.c_size_t]
+    buf = C.create_string_buffer(1 << 20)
+    rc = lib.ref_node_strategies(json.dumps(graph).encode(), node_id.encode(),
+                                 (C.c_int64 * len(mesh))(*mesh), len(mesh), FLOPS, buf, len(buf))
+    assert rc == 0, buf.value
+    rows = []
+    for line in buf.value.decode().splitlines():
+        name, a, b, c, partial, red, comp, comm, mem = line.split("|")
+        rows.append({"name": name, "a": a, "b": b, "c": c, "partial_sum": partial == "1",
+                     "reduce_axes": [int(x) for x in red.split(",") if x],
+                     "compute_time_s": comp, "comm_time_s": comm, "memory_bytes": int(mem)})
+    return rows
+
+
+def plan(graph, mesh, budget):
+    lib = ref.lib()
+    lib.ref_plan.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.c_int, C.c_double, C.c_double,
+                             C.c_double, C.c_int64, C.c_char_p, C.c_size_t]
+    buf = C.create_string_buffer(1 << 24)
+    rc = lib.ref_plan(json.dumps(graph).encode(), (C.c_int64 * len(mesh))(*mesh), len(mesh),
+                      ALPHA, BETA_INV, FLOPS, budget, buf, len(buf))
+    assert rc == 0, buf.value[:500]
+    return json.loads(buf.value.decode())
+
+
+def main():
+    assert ref.available(), "build oracle/_ref first: make -C oracle"
+    g = mlp_graph()
+    strategies = []
+    for mesh in ([8], [2, 4], [2, 2, 2]):
+        for nid in ("fc1", "fc2"):
+            strategies.append({"graph": "gpt2_mlp", "node": nid, "mesh": mesh,
+                               "flops": FLOPS, "strategies": node_strategies(g, nid, mesh)})
+    strategies.append({"graph": "bmm", "node": "bmm", "mesh": [2, 2], "flops": FLOPS,
+                       "strategies": node_strategies(bmm_graph(), "bmm", [2, 2])})
+    (HERE / "strategies.json").write_text(json.dumps({"graphs": {"gpt2_mlp": g, "bmm": bmm_graph()},
+                                                      "cases": strategies}, indent=0))
+    out = HERE / "plans"
+    out.mkdir(exist_ok=True)
+    (out / "gpt2_mlp_graph.json").write_text(json.dumps(g, indent=1))
+    for mesh in ([8], [2, 4], [2, 2, 2]):
+        for budget_mib in (0, 96, 192):
+            budget = (budget_mib << 20) if budget_mib else (1 << 40)
+            name = f"gpt2_mlp_mesh{'x'.join(map(str, mesh))}_{budget_mib or 'unlimited'}"
+            try:
+                doc = plan(g, mesh, budget)
+            except AssertionError as e:
+                print(f"{name}: infeasible ({e})", file=sys.stderr)
+                continue
+            (out / f"{name}.json").write_text(json.dumps(doc, indent=1))
+            sel = {k: v["strategy"] for k, v in doc["nodes"].items()}
+            comm = [(c["node"], c["collective"], c["axes"]) for c in doc["inserted_comm_nodes"]]
+            print(name, sel, comm, file=sys.stderr)
+
+
+if __name__ == "__main__":
+    main()
