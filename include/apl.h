@@ -246,21 +246,30 @@ int apl_matmul_strategies(const apl_mesh_desc* mesh, const apl_meta* a_meta,
                           const apl_meta* b_meta, int batched, double device_flops_per_s,
                           apl_strategy_info* out, int cap, int* count);
 
+/* Physical layout of the B operand. */
+#define APL_B_NK 0 /* Bt [N, K], K contiguous (nn.Linear weight layout) */
+#define APL_B_KN 1 /* B [K, N], N contiguous (the logical reference layout) */
+
 /* Local dense contraction on the tcgen05 tensor cores:
- * C[M,N] = epi(A[M,K] . Bt[N,K]^T); A, Bt bf16 with unit stride along K
- * (Bt = nn.Linear weight layout), fp32 accumulation, C bf16 or f32. */
-int apl_gemm_bf16(const void* A, const void* Bt, void* C, int64_t M, int64_t N, int64_t K,
-                  int64_t lda, int64_t ldb, int64_t ldc, int out_dtype, int epilogue,
-                  void* stream);
+ * C[M,N] = epi(A[M,K] . B[K,N]); A bf16 with unit stride along K, B bf16 in
+ * either layout (b_layout), fp32 accumulation in TMEM, C bf16 or f32. */
+int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                  int64_t lda, int64_t ldb, int64_t ldc, int b_layout, int out_dtype,
+                  int epilogue, void* stream);
 
 /* Execute a strategy on the mesh: per local device one tcgen05 GEMM on its
- * shards (A: local shard of A; Bt: local shard of B stored transposed,
- * [n_local, k_local]; C: local shard of C), then the partial-sum all-reduce
- * over reduce_axes, then the epilogue if it could not be fused. */
+ * shards (A: local shard of A; B: local shard of B, [k_local, n_local] for
+ * APL_B_KN or transposed [n_local, k_local] for APL_B_NK; C: local shard of
+ * C), then the partial-sum all-reduce over reduce_axes, then the epilogue if
+ * it could not be fused. */
 int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
                        const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
-                       const void* const* Bt, void* const* C, int out_dtype, int epilogue,
-                       void* stream);
+                       const void* const* B, void* const* C, int b_layout, int out_dtype,
+                       int epilogue, void* stream);
+
+/* Exact-erf GELU in place over `count` elements (elementwise-unary nodes of
+ * a plan that could not be fused into a GEMM epilogue). */
+int apl_gelu_inplace(void* buf, size_t count, int dtype, void* stream);
 
 /* Kernel launches this process issued through the library (evidence). */
 int apl_launch_count(uint64_t* launches);

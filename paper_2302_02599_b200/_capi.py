@@ -19,6 +19,7 @@ FUSE_CHAIN = 1
 STEPWISE = 0
 F32, BF16, F16 = 0, 1, 2
 EPI_NONE, EPI_GELU = 0, 1
+B_NK, B_KN = 0, 1
 
 
 class Spec(C.Structure):
@@ -111,10 +112,11 @@ _SIGS = {
                                         P(StrategyInfoC), C.c_int, P(C.c_int)]),
     "apl_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                 C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
-                                C.c_void_p]),
+                                C.c_int, C.c_void_p]),
     "apl_sharded_matmul": (C.c_int, [C.c_void_p, P(MatmulStrategyC), P(Meta), P(Meta),
                                      P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
-                                     C.c_int, C.c_void_p]),
+                                     C.c_int, C.c_int, C.c_void_p]),
+    "apl_gelu_inplace": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "apl_launch_count": (C.c_int, [P(C.c_uint64)]),
 }
 

@@ -590,31 +590,34 @@ int apl_matmul_strategies(const apl_mesh_desc* mesh, const apl_meta* a_meta,
   });
 }
 
-int apl_gemm_bf16(const void* A, const void* Bt, void* C, int64_t M, int64_t N, int64_t K,
-                  int64_t lda, int64_t ldb, int64_t ldc, int out_dtype, int epilogue,
-                  void* stream) {
+int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                  int64_t lda, int64_t ldb, int64_t ldc, int b_layout, int out_dtype,
+                  int epilogue, void* stream) {
   return guarded([&] {
-    need(A && Bt && C, "null operand");
+    need(A && B && C, "null operand");
     need(M >= 0 && N >= 0 && K >= 0 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX,
          "extents out of range");
-    need(lda >= K && ldb >= K && ldc >= N, "leading dimensions too small");
+    need(b_layout == APL_B_NK || b_layout == APL_B_KN, "unknown B layout");
+    const bool kn = b_layout == APL_B_KN;
+    need(lda >= K && ldb >= (kn ? N : K) && ldc >= N, "leading dimensions too small");
     need(out_dtype == APL_F32 || out_dtype == APL_BF16, "output dtype must be f32 or bf16");
     need(epilogue == APL_EPI_NONE || epilogue == APL_EPI_GELU, "unknown epilogue");
-    apl::check_cuda(apl::gemm_bf16_tn(A, Bt, C, static_cast<int>(M), static_cast<int>(N),
-                                      static_cast<int>(K), static_cast<int>(lda),
-                                      static_cast<int>(ldb), static_cast<int>(ldc),
-                                      out_dtype == APL_F32, epilogue == APL_EPI_GELU,
-                                      static_cast<cudaStream_t>(stream)),
+    apl::check_cuda(apl::gemm_bf16(A, B, C, static_cast<int>(M), static_cast<int>(N),
+                                   static_cast<int>(K), static_cast<int>(lda),
+                                   static_cast<int>(ldb), static_cast<int>(ldc), kn,
+                                   out_dtype == APL_F32, epilogue == APL_EPI_GELU,
+                                   static_cast<cudaStream_t>(stream)),
                     "apl_gemm_bf16");
   });
 }
 
 int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
                        const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
-                       const void* const* Bt, void* const* C, int out_dtype, int epilogue,
-                       void* stream) {
+                       const void* const* B, void* const* C, int b_layout, int out_dtype,
+                       int epilogue, void* stream) {
   return guarded([&] {
-    need(mesh && strategy && A && Bt && C, "null argument");
+    need(mesh && strategy && A && B && C, "null argument");
+    need(b_layout == APL_B_NK || b_layout == APL_B_KN, "unknown B layout");
     need(out_dtype == APL_F32 || out_dtype == APL_BF16, "output dtype must be f32 or bf16");
     need(epilogue == APL_EPI_NONE || epilogue == APL_EPI_GELU, "unknown epilogue");
     need(strategy->nreduce >= 0 && strategy->nreduce <= APL_MAX_MESH, "bad reduce axis count");
@@ -625,8 +628,18 @@ int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
     s.partial_sum = strategy->partial_sum != 0;
     for (int i = 0; i < strategy->nreduce; ++i) s.reduce_axes.push_back(strategy->reduce_axes[i]);
     need(s.partial_sum == !s.reduce_axes.empty(), "partial_sum iff reduce axes are given");
-    apl::sharded_matmul(mesh->impl, s, to_meta(a_meta), to_meta(b_meta), A, Bt, C, out_dtype,
-                        epilogue, static_cast<cudaStream_t>(stream));
+    apl::sharded_matmul(mesh->impl, s, to_meta(a_meta), to_meta(b_meta), A, B, C,
+                        b_layout == APL_B_KN, out_dtype, epilogue,
+                        static_cast<cudaStream_t>(stream));
+  });
+}
+
+int apl_gelu_inplace(void* buf, size_t count, int dtype, void* stream) {
+  return guarded([&] {
+    need(buf || count == 0, "null buffer");
+    need(dtype >= APL_F32 && dtype <= APL_F16, "bad dtype");
+    apl::check_cuda(apl::launch_gelu_inplace(buf, count, dtype, static_cast<cudaStream_t>(stream)),
+                    "gelu launch");
   });
 }
 

@@ -88,11 +88,27 @@ __device__ __forceinline__ uint64_t smem_desc(const void* tile) {
   return d;
 }
 
-template <int BN>
+// MN-major (N-contiguous), 128B-swizzled B tile built from [64 k][64 n]
+// TMA boxes: 64-element MN atoms 8 KiB apart (leading byte offset), 8-row K
+// groups 1 KiB apart (stride byte offset) — the canonical
+// ((8,n),(8,k)):((1,LBO),(8,SBO)) UMMA layout in 16-byte units.
+__device__ __forceinline__ uint64_t smem_desc_mn(const void* tile) {
+  const uint64_t addr = smem_addr(tile);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= uint64_t(8192 >> 4) << 16;  // LBO: next 64 columns of N
+  d |= uint64_t(1024 >> 4) << 32;  // SBO: next 8 rows of K
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+
+template <int BN, bool kBMN>
 __device__ __forceinline__ constexpr uint32_t instr_desc() {
   return (1u << 4)                     // D = f32
          | (1u << 7)                   // A = bf16
          | (1u << 10)                  // B = bf16
+         | (uint32_t(kBMN ? 1 : 0) << 16)  // B major: 0 = K, 1 = MN
          | (uint32_t(BN >> 3) << 17)   // N
          | (uint32_t(kBM >> 4) << 24); // M
 }
@@ -146,7 +162,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // Persistent: CTA b handles tiles b, b + grid, ... (n fastest). The MMA of
 // tile i+1 overlaps the epilogue of tile i through two TMEM accumulators.
-template <int BN, bool kGelu, bool kOutF32>
+// kBMN: B is the logical row-major [K, N] (N contiguous, MN-major operand)
+// instead of Bt [N, K].
+template <int BN, bool kGelu, bool kOutF32, bool kBMN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, void* __restrict__ out, int M,
@@ -204,13 +222,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], phase ^ 1);
           mbar_expect_tx(&full[s], S::kStageA + S::kStageB);
           tma_load_2d(tiles_a + s * S::kStageA, &map_a, &full[s], kb * kBK, m0);
-          tma_load_2d(tiles_b + s * S::kStageB, &map_b, &full[s], kb * kBK, n0);
+          if constexpr (kBMN) {
+            // BN/64 boxes of [64 k][64 n], one MN swizzle atom column each
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(tiles_b + s * S::kStageB + j * 8192, &map_b, &full[s], n0 + j * 64,
+                          kb * kBK);
+          } else {
+            tma_load_2d(tiles_b + s * S::kStageB, &map_b, &full[s], kb * kBK, n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc<BN>();
+      constexpr uint32_t idesc = instr_desc<BN, kBMN>();
       int it = 0, local = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
         const int acc = local & 1;
@@ -223,11 +249,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[s], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t da = smem_desc(tiles_a + s * S::kStageA);
-          const uint64_t db = smem_desc(tiles_b + s * S::kStageB);
+          const uint64_t db = kBMN ? smem_desc_mn(tiles_b + s * S::kStageB)
+                                   : smem_desc(tiles_b + s * S::kStageB);
+          // K advance per instruction: K-major = 32 B inside the swizzle row;
+          // MN-major = 16 rows of 128 B.
+          constexpr uint64_t kAdvB = kBMN ? (16 * 128) >> 4 : 2;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            // advance 16 bf16 = 32 B along K inside the swizzle row
-            mma_bf16(d, da + uint64_t(2 * k), db + uint64_t(2 * k), idesc,
+            mma_bf16(d, da + uint64_t(2 * k), db + kAdvB * k, idesc,
                      (kb > 0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
@@ -323,22 +352,25 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int box_rows) {
+// 2-D bf16 tensor map, 128B swizzle, box = [box_rows][box_cols] (box_cols
+// x 2 B = one 128-byte swizzle row).
+bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int box_rows,
+              int box_cols = kBK) {
   EncodeFn enc = encode_fn();
   if (enc == nullptr) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t elem[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
              elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool G, bool F>
+template <int BN, bool G, bool F, bool BMN>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, void* c, int M, int N, int K,
                         int ldc, cudaStream_t stream) {
-  auto kernel = gemm_bf16_tcgen05<BN, G, F>;
+  auto kernel = gemm_bf16_tcgen05<BN, G, F, BMN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -359,32 +391,43 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, void* c, int
   return cudaGetLastError();
 }
 
+template <int BN, bool BMN>
+cudaError_t dispatch(const CUtensorMap& a, const CUtensorMap& b, void* c, int M, int N, int K,
+                     int ldc, bool out_f32, bool gelu, cudaStream_t stream) {
+  if (gelu)
+    return out_f32 ? launch_gemm<BN, true, true, BMN>(a, b, c, M, N, K, ldc, stream)
+                   : launch_gemm<BN, true, false, BMN>(a, b, c, M, N, K, ldc, stream);
+  return out_f32 ? launch_gemm<BN, false, true, BMN>(a, b, c, M, N, K, ldc, stream)
+                 : launch_gemm<BN, false, false, BMN>(a, b, c, M, N, K, ldc, stream);
+}
+
 }  // namespace
 
-// C[M,N] = A[M,K] . Bt[N,K]^T (bf16 in, fp32 accumulate). out_f32 selects the
-// output type; gelu applies exact-erf GELU in the epilogue.
-cudaError_t gemm_bf16_tn(const void* A, const void* Bt, void* C, int M, int N, int K, int lda,
-                         int ldb, int ldc, bool out_f32, bool gelu, cudaStream_t stream) {
+// C[M,N] = A[M,K] . B with B given as Bt [N,K] (b_kn = false, nn.Linear
+// layout) or as row-major [K,N] (b_kn = true); bf16 in, fp32 accumulate.
+// out_f32 selects the output type; gelu applies exact-erf GELU in the epilogue.
+cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
+                      int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
-  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(Bt) & 15) ||
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
       (lda * 2) % 16 || (ldb * 2) % 16)
     return cudaErrorInvalidValue;  // TMA needs 16-byte aligned rows
   const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K, lda, kBM) || !make_map(&mb, Bt, N, K, ldb, bn))
-    return cudaErrorInvalidValue;
-#define APL_GEMM_CASE(BN_, G_, F_) \
-  if (bn == BN_ && gelu == G_ && out_f32 == F_) return launch_gemm<BN_, G_, F_>(ma, mb, C, M, N, K, ldc, stream);
-  APL_GEMM_CASE(256, false, false)
-  APL_GEMM_CASE(256, true, false)
-  APL_GEMM_CASE(256, false, true)
-  APL_GEMM_CASE(256, true, true)
-  APL_GEMM_CASE(128, false, false)
-  APL_GEMM_CASE(128, true, false)
-  APL_GEMM_CASE(128, false, true)
-  APL_GEMM_CASE(128, true, true)
-#undef APL_GEMM_CASE
-  return cudaErrorInvalidValue;
+  if (!make_map(&ma, A, M, K, lda, kBM)) return cudaErrorInvalidValue;
+  if (b_kn) {
+    if (!make_map(&mb, B, K, N, ldb, kBK, 64)) return cudaErrorInvalidValue;
+    return bn == 256 ? dispatch<256, true>(ma, mb, C, M, N, K, ldc, out_f32, gelu, stream)
+                     : dispatch<128, true>(ma, mb, C, M, N, K, ldc, out_f32, gelu, stream);
+  }
+  if (!make_map(&mb, B, N, K, ldb, bn)) return cudaErrorInvalidValue;
+  return bn == 256 ? dispatch<256, false>(ma, mb, C, M, N, K, ldc, out_f32, gelu, stream)
+                   : dispatch<128, false>(ma, mb, C, M, N, K, ldc, out_f32, gelu, stream);
+}
+
+cudaError_t gemm_bf16_tn(const void* A, const void* Bt, void* C, int M, int N, int K, int lda,
+                         int ldb, int ldc, bool out_f32, bool gelu, cudaStream_t stream) {
+  return gemm_bf16(A, Bt, C, M, N, K, lda, ldb, ldc, false, out_f32, gelu, stream);
 }
 
 }  // namespace apl

@@ -16,7 +16,7 @@ namespace apl {
 
 void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorMeta& a_meta,
                     const autoplan::TensorMeta& b_meta, const void* const* A,
-                    const void* const* Bt, void* const* C, int out_dtype, int epilogue,
+                    const void* const* B, void* const* C, bool b_kn, int out_dtype, int epilogue,
                     cudaStream_t stream) {
   const auto& geo = mesh.geo;
   if (b_meta.rank() != 2 || a_meta.rank() < 2)
@@ -46,9 +46,10 @@ void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorM
   const bool fuse_gelu = epilogue == APL_EPI_GELU && !s.partial_sum;
   const int nl = mesh.num_local();
   for (int d = 0; d < nl; ++d) {
-    check_cuda(gemm_bf16_tn(A[d], Bt[d], C[d], static_cast<int>(m), static_cast<int>(n),
-                            static_cast<int>(k), static_cast<int>(k), static_cast<int>(k),
-                            static_cast<int>(n), out_dtype == APL_F32, fuse_gelu, stream),
+    check_cuda(gemm_bf16(A[d], B[d], C[d], static_cast<int>(m), static_cast<int>(n),
+                         static_cast<int>(k), static_cast<int>(k),
+                         static_cast<int>(b_kn ? n : k), static_cast<int>(n), b_kn,
+                         out_dtype == APL_F32, fuse_gelu, stream),
                "tcgen05 GEMM launch");
   }
   if (s.partial_sum) {

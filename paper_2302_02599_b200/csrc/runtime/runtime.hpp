@@ -37,8 +37,8 @@ cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int gr
                                    cudaStream_t stream);
 uint64_t launch_count();
 cudaError_t launch_gelu_inplace(void* buf, size_t count, int dtype, cudaStream_t stream);
-cudaError_t gemm_bf16_tn(const void* A, const void* Bt, void* C, int M, int N, int K, int lda,
-                         int ldb, int ldc, bool out_f32, bool gelu, cudaStream_t stream);
+cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
+                      int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream);
 
 // One sharded-matmul strategy (reference OpStrategy, intraop.hpp:34-49).
 struct MatmulStrategy {
@@ -125,9 +125,11 @@ void run_path(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::Sha
 void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, size_t count,
                 int dtype, cudaStream_t stream);
 
+// B shards are row-major [k_local, n_local] when b_kn, else transposed
+// [n_local, k_local] (nn.Linear layout).
 void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorMeta& a_meta,
                     const autoplan::TensorMeta& b_meta, const void* const* A,
-                    const void* const* Bt, void* const* C, int out_dtype, int epilogue,
-                    cudaStream_t stream);
+                    const void* const* B, void* const* C, bool b_kn, int out_dtype,
+                    int epilogue, cudaStream_t stream);
 
 }  // namespace apl

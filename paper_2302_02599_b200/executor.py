@@ -1,0 +1,269 @@
+"""Plan executor: runs a reference execution plan on device data.
+
+Consumes the reference's two wire formats unchanged:
+  * graph document v1   (proj/src/graph_ir.cpp:449-573): nodes in topological
+    order with kind / inputs / output metadata;
+  * plan document v1    (proj/src/planner.cpp:455-600, plan_to_json): per node
+    the selected strategy name and output spec (+ partial_sum / reduce_axes),
+    and the inserted communication (all-reduce after partial sums,
+    per-step conversion chains on mismatched edges).
+
+and executes the forward pass on a `runtime.Mesh` (simulated or distributed):
+  * placeholders / parameters are sharded by their plan spec;
+  * every mismatched edge is converted with the reference's own path
+    (find_transform_path, identical to proj/src/layout.cpp:253-316) — either
+    step by step, exactly like the plan's `<producer>.cvN` nodes
+    (insert_comm_nodes, planner.cpp:284-347), or collapsed into one exchange;
+    chains are shared between consumers of the same (producer, target spec),
+    as in planner.cpp:299-305;
+  * matmul nodes run their strategy (catalog decode of the strategy name,
+    intraop.cpp:141-234) as tcgen05 GEMMs on the shards, with the partial-sum
+    all-reduce of `<host>.ar` (planner.cpp:263-282);
+  * an elementwise-unary GELU consuming a non-partial matmul output in the
+    same layout is fused into the GEMM epilogue;
+  * the output node collects to RR (intraop.cpp:469-482).
+
+The executor also cross-checks its own communication against the plan's
+`inserted_comm_nodes` (same producers/consumers, same step kinds and axes),
+so a plan this runtime would execute differently is rejected up front.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from .layout import DeviceMesh, ShardingSpec, TensorMeta, find_transform_path
+from .strategies import MatmulStrategy, find_matmul_strategy
+
+_DTYPES = {2: torch.bfloat16, 4: torch.float32}
+
+
+def infer_shapes(graph: dict) -> dict:
+    """Output shape + dtype bytes per node (shape rules of graph_ir.cpp:189-373
+    for the kinds the MLP/block graphs use)."""
+    out = {}
+    for n in graph["nodes"]:
+        if n["outputs"]:
+            o = n["outputs"][0]
+            out[n["id"]] = (tuple(o["shape"]), o["dtype_bytes"])
+            continue
+        ins = [out[i[0]] for i in n["inputs"]]
+        k = n["kind"]
+        if k == "matmul":
+            (a, ea), (b, _) = ins
+            out[n["id"]] = (a[:-1] + (b[-1],), ea)
+        elif k == "batched-matmul":
+            (a, ea), (b, _) = ins
+            out[n["id"]] = ((a[0], a[1], b[2]), ea)
+        elif k in ("elementwise-unary", "output"):
+            out[n["id"]] = ins[0]
+        else:
+            raise NotImplementedError(f"node kind {k!r} is not executable yet")
+    return out
+
+
+@dataclass
+class CommRecord:
+    """One communication the executor performs (mirrors CommInsertion)."""
+    producer: str
+    consumer: str
+    collective: str
+    axes: tuple
+    bytes: int
+
+
+@dataclass
+class PlanExecutor:
+    mesh: "object"  # runtime.Mesh
+    graph: dict
+    plan: dict
+    fuse: bool = True
+    comm: list = field(default_factory=list)
+
+    def __post_init__(self):
+        self.geo: DeviceMesh = self.mesh.geo
+        mr = self.geo.rank()
+        self.shapes = infer_shapes(self.graph)
+        self.nodes = {n["id"]: n for n in self.graph["nodes"]}
+        self.spec = {nid: ShardingSpec.parse(p["spec"], mr) for nid, p in self.plan["nodes"].items()}
+        self.partial = {nid: tuple(p.get("reduce_axes", ())) for nid, p in self.plan["nodes"].items()
+                        if p.get("partial_sum")}
+        self.strategy: dict[str, MatmulStrategy] = {}
+        for n in self.graph["nodes"]:
+            if n["kind"] == "matmul":
+                a_meta = self._meta(n["inputs"][0][0])
+                b_meta = self._meta(n["inputs"][1][0])
+                st = find_matmul_strategy(self.plan["nodes"][n["id"]]["strategy"], self.geo,
+                                          a_meta, b_meta)
+                if st.c != self.spec[n["id"]]:
+                    raise ValueError(f"{n['id']}: plan spec {self.spec[n['id']]} != strategy "
+                                     f"output {st.c}")
+                self.strategy[n["id"]] = st
+        self._consumers = {}
+        for n in self.graph["nodes"]:
+            for slot, (src, _) in enumerate(n["inputs"]):
+                self._consumers.setdefault(src, []).append((n["id"], slot))
+        self._paths = {}
+
+    # ---- layout bookkeeping ------------------------------------------------
+    def _meta(self, nid: str) -> TensorMeta:
+        shape, eb = self.shapes[nid]
+        return TensorMeta(shape, eb)
+
+    def required_spec(self, consumer: str, slot: int) -> ShardingSpec:
+        n = self.nodes[consumer]
+        if n["kind"] == "matmul":
+            st = self.strategy[consumer]
+            return st.a if slot == 0 else st.b
+        if n["kind"] == "output":
+            return ShardingSpec.replicated(len(self.shapes[consumer][0]), self.geo.rank())
+        return self.spec[consumer]  # elementwise: layout mirrored onto the input
+
+    def _fusable_gelu(self, mm: str):
+        """The GELU node fused into matmul `mm`'s epilogue, if any."""
+        cons = self._consumers.get(mm, [])
+        if len(cons) != 1 or mm in self.partial:
+            return None
+        gid, _ = cons[0]
+        g = self.nodes[gid]
+        if g["kind"] == "elementwise-unary" and self.spec[gid] == self.spec[mm]:
+            return gid
+        return None
+
+    def planned_communication(self) -> list:
+        """The communication this executor will issue, in graph walk order:
+        one record per reference step (fuse=False semantics) so it can be
+        compared with the plan's inserted_comm_nodes."""
+        recs = []
+        for n in self.graph["nodes"]:
+            nid = n["id"]
+            if nid in self.partial:
+                recs.append(CommRecord(nid, "", "all-reduce", self.partial[nid], 0))
+            seen = set()
+            for consumer, slot in self._consumers.get(nid, []):
+                src, tgt = self.spec[nid], self.required_spec(consumer, slot)
+                if src == tgt or (str(src), str(tgt)) in seen:
+                    continue
+                seen.add((str(src), str(tgt)))
+                for s in self._path(nid, src, tgt).steps:
+                    recs.append(CommRecord(nid, consumer, str(s.kind), (s.mesh_axis,), 0))
+        return recs
+
+    def check_against_plan(self) -> None:
+        mine = [(r.producer, r.collective, tuple(r.axes)) for r in self.planned_communication()]
+        theirs = [(c["producer"], c["collective"], tuple(c["axes"]))
+                  for c in self.plan["inserted_comm_nodes"]]
+        if mine != theirs:
+            raise ValueError(f"plan communication differs from the executor's:\n{theirs}\n{mine}")
+
+    def _path(self, nid, src, tgt):
+        key = (nid, str(src), str(tgt))
+        if key not in self._paths:
+            self._paths[key] = find_transform_path(src, tgt, self.geo, self._meta(nid))
+        return self._paths[key]
+
+    # ---- execution ---------------------------------------------------------
+    def shard(self, nid: str, full: torch.Tensor) -> list:
+        """Local shards of a global tensor under node `nid`'s plan spec."""
+        spec = self.spec[nid]
+        devs = range(self.mesh.num_devices) if not self.mesh.distributed else [self.mesh.first_local]
+        out = []
+        for d in devs:
+            coord = self.geo.coord_of(d)
+            sl = []
+            for k, dim in enumerate(spec.dims):
+                s, split = 0, 1
+                for a in dim.axes:
+                    s = s * self.geo.shape[a] + coord[a]
+                    split *= self.geo.shape[a]
+                L = full.shape[k] // split
+                sl.append(slice(s * L, (s + 1) * L))
+            out.append(full[tuple(sl)].contiguous())
+        return out
+
+    def _alloc(self, nid: str, spec: ShardingSpec, like: torch.Tensor) -> list:
+        shape = spec.local_shape(self._meta(nid), self.geo)
+        return [torch.empty(shape, dtype=like.dtype, device=like.device)
+                for _ in range(self.mesh.num_local)]
+
+    def _convert(self, nid, shards, src, tgt, stream):
+        path = self._path(nid, src, tgt)
+        outs = self._alloc(nid, tgt, shards[0])
+        self.mesh.run_path(path, self._meta(nid), shards, outs, fuse=self.fuse, stream=stream)
+        return outs
+
+    def forward(self, feeds: dict, stream=None) -> list:
+        """feeds: global tensors for every placeholder and parameter, or
+        already-sharded lists (node id -> list of local shards)."""
+        from . import _capi as A
+        from .layout import check
+        import ctypes as C
+
+        values, converted, fused = {}, {}, set()
+        for n in self.graph["nodes"]:
+            nid, kind = n["id"], n["kind"]
+            if kind in ("placeholder", "parameter"):
+                v = feeds[nid]
+                values[nid] = v if isinstance(v, list) else self.shard(nid, v)
+                continue
+            ins = []
+            for slot, (src, _) in enumerate(n["inputs"]):
+                have, want = self.spec[src], self.required_spec(nid, slot)
+                if have == want:
+                    ins.append(values[src])
+                    continue
+                key = (src, str(want))
+                if key not in converted:
+                    converted[key] = self._convert(src, values[src], have, want, stream)
+                ins.append(converted[key])
+            if kind == "matmul":
+                st = self.strategy[nid]
+                out_spec = self.spec[nid]
+                outs = self._alloc(nid, out_spec, ins[0][0])
+                gelu_node = self._fusable_gelu(nid)
+                self.mesh.sharded_matmul(st, self._meta(n["inputs"][0][0]),
+                                         self._meta(n["inputs"][1][0]), ins[0], ins[1], outs,
+                                         gelu=gelu_node is not None, b_layout="kn",
+                                         stream=stream)
+                if gelu_node:
+                    fused.add(gelu_node)
+                values[nid] = outs
+            elif kind == "elementwise-unary":
+                if nid in fused:
+                    values[nid] = ins[0]
+                else:
+                    outs = [t.clone() for t in ins[0]]
+                    code = {torch.float32: A.F32, torch.bfloat16: A.BF16}[outs[0].dtype]
+                    s = stream if stream is not None else torch.cuda.current_stream()
+                    for t in outs:
+                        check(A.lib().apl_gelu_inplace(C.c_void_p(t.data_ptr()), t.numel(), code,
+                                                       C.c_void_p(s.cuda_stream)))
+                    values[nid] = outs
+            elif kind == "output":
+                values[nid] = ins[0]
+            else:
+                raise NotImplementedError(kind)
+        return values[self.graph["output"]]
+
+
+def megatron_mlp_plan(mesh_rank: int = 1, axis: int = 0) -> dict:
+    """BASELINE config 5 pinned selection on a mesh axis: fc1 split-n (RR x RS
+    -> RS, GELU fused), fc2 split-k (RS x SR -> RR partial, all-reduce).
+    Same document shape as plan_to_json (nodes + inserted_comm_nodes)."""
+    r = "R" * 1
+    s = f"S{axis}"
+    rr = "RR" if mesh_rank >= 1 else r
+    nodes = {
+        "x": {"strategy": f"src:{rr}", "spec": rr, "partial_sum": False},
+        "w1": {"strategy": f"src:R{s}", "spec": f"R{s}", "partial_sum": False},
+        "w2": {"strategy": f"src:{s}R", "spec": f"{s}R", "partial_sum": False},
+        "fc1": {"strategy": f"split-n:{axis}", "spec": f"R{s}", "partial_sum": False},
+        "gelu": {"strategy": f"split-n:{axis}", "spec": f"R{s}", "partial_sum": False},
+        "fc2": {"strategy": f"split-k:{axis}", "spec": rr, "partial_sum": True,
+                "reduce_axes": [axis]},
+        "out": {"strategy": "collect", "spec": rr, "partial_sum": False},
+    }
+    return {"version": 1, "nodes": nodes,
+            "inserted_comm_nodes": [{"node": "fc2.ar", "producer": "fc2", "producer_out": 0,
+                                     "collective": "all-reduce", "axes": [axis], "bytes": 0}]}

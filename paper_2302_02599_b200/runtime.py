@@ -38,25 +38,28 @@ def launch_count() -> int:
     return n.value
 
 
-def gemm(a: torch.Tensor, bt: torch.Tensor, out: torch.Tensor | None = None,
-         gelu: bool = False, out_dtype=torch.bfloat16, stream=None) -> torch.Tensor:
-    """out[M,N] = epi(a[M,K] . bt[N,K]^T) on the tcgen05 tensor cores (bf16 in,
-    fp32 accumulate)."""
-    if a.dtype != torch.bfloat16 or bt.dtype != torch.bfloat16:
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
+         gelu: bool = False, out_dtype=torch.bfloat16, b_layout: str = "nk",
+         stream=None) -> torch.Tensor:
+    """out[M,N] = epi(a[M,K] . B) on the tcgen05 tensor cores (bf16 in, fp32
+    accumulate). b_layout "nk": b is Bt [N,K] (nn.Linear weight); "kn": b is
+    the row-major [K,N] matrix itself."""
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
         raise TypeError("gemm operands must be bf16")
-    if a.dim() != 2 or bt.dim() != 2 or a.shape[1] != bt.shape[1]:
-        raise ValueError("gemm wants a[M,K], bt[N,K]")
-    if a.stride(1) != 1 or bt.stride(1) != 1:
-        raise ValueError("operands need unit stride along K")
+    kn = b_layout == "kn"
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != (b.shape[0] if kn else b.shape[1]):
+        raise ValueError("gemm wants a[M,K] and b[N,K] ('nk') or b[K,N] ('kn')")
+    if a.stride(1) != 1 or b.stride(1) != 1:
+        raise ValueError("operands need a unit inner stride")
     m, k = a.shape
-    n = bt.shape[0]
+    n = b.shape[1] if kn else b.shape[0]
     if out is None:
         out = torch.empty(m, n, dtype=out_dtype, device=a.device)
     code = _DTYPE_CODE[out.dtype]
-    check(A.lib().apl_gemm_bf16(C.c_void_p(a.data_ptr()), C.c_void_p(bt.data_ptr()),
-                                C.c_void_p(out.data_ptr()), m, n, k, a.stride(0), bt.stride(0),
-                                out.stride(0), code, A.EPI_GELU if gelu else A.EPI_NONE,
-                                _stream_handle(stream)))
+    check(A.lib().apl_gemm_bf16(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                C.c_void_p(out.data_ptr()), m, n, k, a.stride(0), b.stride(0),
+                                out.stride(0), A.B_KN if kn else A.B_NK, code,
+                                A.EPI_GELU if gelu else A.EPI_NONE, _stream_handle(stream)))
     return out
 
 
@@ -187,15 +190,18 @@ class Mesh:
         return {"hbm_read": r.value, "hbm_write": w.value, "wire_in": wire.value}
 
     def sharded_matmul(self, strategy: "MatmulStrategy", a_meta: TensorMeta, b_meta: TensorMeta,
-                       a_shards, bt_shards, c_shards, gelu: bool = False, stream=None) -> None:
+                       a_shards, b_shards, c_shards, gelu: bool = False, b_layout: str = "nk",
+                       stream=None) -> None:
         """Local tcgen05 GEMM per device + partial-sum all-reduce (+ epilogue).
-        bt_shards hold each device's B shard transposed: [n_local, k_local]."""
-        for what, bufs in (("A", a_shards), ("Bt", bt_shards), ("C", c_shards)):
+        b_layout "nk": each B shard stored transposed [n_local, k_local];
+        "kn": the logical row-major shard [k_local, n_local]."""
+        for what, bufs in (("A", a_shards), ("B", b_shards), ("C", c_shards)):
             if len(bufs) != self.num_local:
                 raise ValueError(f"{what}: expected {self.num_local} shards")
         check(A.lib().apl_sharded_matmul(
             self._h, C.byref(strategy.c_struct()), C.byref(a_meta.c()), C.byref(b_meta.c()),
-            _ptrs(a_shards), _ptrs(bt_shards), _ptrs(c_shards), _DTYPE_CODE[c_shards[0].dtype],
+            _ptrs(a_shards), _ptrs(b_shards), _ptrs(c_shards),
+            A.B_KN if b_layout == "kn" else A.B_NK, _DTYPE_CODE[c_shards[0].dtype],
             A.EPI_GELU if gelu else A.EPI_NONE, _stream_handle(stream)))
 
     def all_reduce(self, axes: Sequence[int], tensors, stream=None) -> None:

@@ -27,11 +27,15 @@ def ref_mm(a, bt, gelu=False):
                                    (2048, 1024, 4096), (16384, 512, 1024), (200, 136, 72),
                                    (1, 16, 16), (130, 260, 520)])
 @pytest.mark.parametrize("gelu", [False, True])
-def test_gemm_bf16_out(cuda, m, n, k, gelu):
+@pytest.mark.parametrize("b_layout", ["nk", "kn"])
+def test_gemm_bf16_out(cuda, m, n, k, gelu, b_layout):
     torch.manual_seed(m + n + k)
     a = torch.randn(m, k, device="cuda").bfloat16()
     bt = (torch.randn(n, k, device="cuda") / k ** 0.5).bfloat16()
-    out = gemm(a, bt, gelu=gelu)
+    if b_layout == "kn" and (n * 2) % 16:
+        pytest.skip("TMA needs 16-byte rows of B[K,N]")
+    b = bt.t().contiguous() if b_layout == "kn" else bt
+    out = gemm(a, b, gelu=gelu, b_layout=b_layout)
     torch.cuda.synchronize()
     assert rel_err(out, ref_mm(a, bt, gelu)) <= TOL_BF16
 
@@ -71,7 +75,7 @@ def shard(t, spec: ShardingSpec, geo: DeviceMesh, dev: int):
 
 
 def run_strategy(mesh_shape, name, a_spec, b_spec, c_spec, reduce_axes, m=512, k=256, n=384,
-                 gelu=False, out_dtype=torch.bfloat16):
+                 gelu=False, out_dtype=torch.bfloat16, b_layout="nk"):
     mesh = Mesh.local(mesh_shape)
     geo, mr = mesh.geo, len(mesh_shape)
     torch.manual_seed(3)
@@ -80,12 +84,15 @@ def run_strategy(mesh_shape, name, a_spec, b_spec, c_spec, reduce_axes, m=512, k
     st = MatmulStrategy(name, ShardingSpec.parse(a_spec, mr), ShardingSpec.parse(b_spec, mr),
                         ShardingSpec.parse(c_spec, mr), reduce_axes)
     a_sh = [shard(a, st.a, geo, d) for d in range(mesh.num_devices)]
-    bt_sh = [shard(b, st.b, geo, d).t().contiguous() for d in range(mesh.num_devices)]
+    if b_layout == "kn":
+        bt_sh = [shard(b, st.b, geo, d) for d in range(mesh.num_devices)]
+    else:
+        bt_sh = [shard(b, st.b, geo, d).t().contiguous() for d in range(mesh.num_devices)]
     c_meta = TensorMeta((m, n), 4 if out_dtype == torch.float32 else 2)
     c_sh = [torch.empty(st.c.local_shape(c_meta, geo), dtype=out_dtype, device="cuda")
             for _ in range(mesh.num_devices)]
     mesh.sharded_matmul(st, TensorMeta((m, k), 2), TensorMeta((k, n), 2), a_sh, bt_sh, c_sh,
-                        gelu=gelu)
+                        gelu=gelu, b_layout=b_layout)
     torch.cuda.synchronize()
     ref = a.double() @ b.double()
     if gelu:
@@ -109,9 +116,10 @@ def run_strategy(mesh_shape, name, a_spec, b_spec, c_spec, reduce_axes, m=512, k
     ([2, 4], "split-mk@0:1,0", "S1S0", "S0R", "S1R", [0]),
 ])
 @pytest.mark.parametrize("gelu", [False, True])
-def test_sharded_matmul_strategies(cuda, case, gelu):
+@pytest.mark.parametrize("b_layout", ["nk", "kn"])
+def test_sharded_matmul_strategies(cuda, case, gelu, b_layout):
     mesh_shape, name, a, b, c, red = case
-    run_strategy(mesh_shape, name, a, b, c, red, gelu=gelu)
+    run_strategy(mesh_shape, name, a, b, c, red, gelu=gelu, b_layout=b_layout)
 
 
 def test_split_k_fp32_partials(cuda):
@@ -136,9 +144,15 @@ def test_megatron_mlp_on_mesh8(cuda):
     y = [torch.empty(2048, 1024, dtype=torch.bfloat16, device="cuda") for _ in range(8)]
     mesh.sharded_matmul(fc1, TensorMeta((2048, 1024), 2), TensorMeta((1024, 4096), 2), xs, w1t, h,
                         gelu=True)
+    # same fc1 with the weight kept in its logical [k, n] layout (MN-major B)
+    w1s = [shard(w1, fc1.b, geo, d) for d in range(8)]
+    h_kn = [torch.empty_like(t) for t in h]
+    mesh.sharded_matmul(fc1, TensorMeta((2048, 1024), 2), TensorMeta((1024, 4096), 2), xs, w1s,
+                        h_kn, gelu=True, b_layout="kn")
     mesh.sharded_matmul(fc2, TensorMeta((2048, 4096), 2), TensorMeta((4096, 1024), 2), h, w2t, y)
     torch.cuda.synchronize()
     ref = torch.nn.functional.gelu(x.float() @ w1.float()) @ w2.float()
     for d in range(8):
         assert rel_err(y[d], ref.double()) <= TOL_BF16
         assert torch.equal(y[d], y[0])  # all-reduce leaves identical replicas
+        assert rel_err(h_kn[d], h[d].double()) <= 1e-2

@@ -56,6 +56,8 @@ def main():
         iters = 3 if quick else 20
         ms = time_fn(lambda: gemm(a, bt, out=c), iters)
         ms_g = time_fn(lambda: gemm(a, bt, out=c, gelu=True), iters)
+        b_kn = bt.t().contiguous()
+        ms_kn = time_fn(lambda: gemm(a, b_kn, out=c, b_layout="kn"), iters)
         ms_cublas = time_fn(lambda: torch.matmul(a, bt.t(), out=c), iters)
         ref = (a.float() @ bt.float().t())
         err = ((gemm(a, bt).float() - ref).abs().max() / ref.abs().max()).item()
@@ -63,6 +65,7 @@ def main():
             "shape": name, "m": m, "n": n, "k": k,
             "ours_ms": round(ms, 4), "ours_tflops": round(flops / ms / 1e9, 1),
             "ours_gelu_tflops": round(flops / ms_g / 1e9, 1),
+            "ours_b_kn_tflops": round(flops / ms_kn / 1e9, 1),
             "cublas_ms": round(ms_cublas, 4), "cublas_tflops": round(flops / ms_cublas / 1e9, 1),
             "frac_of_peak": round(flops / ms / 1e9 / out["peak_tflops"], 3),
             "max_rel_err": err})
