@@ -36,7 +36,13 @@ struct DevCopy {
   int32_t src_buf, nouter, ndst;
   uint8_t dst_bufs[kCopyMaxFan];
   int32_t pad_;
+  int64_t run_bytes;  // bulk (TMA) tables: run length, units are kBulkSeg segments
 };
+
+// TMA bulk engine (bulk_copy.cu): rows of >= kBulkMinRun contiguous bytes
+// move as cp.async.bulk global->smem->global segments of <= kBulkSeg bytes.
+constexpr int kBulkSeg = 2048;
+constexpr int kBulkMinRun = 512;
 
 struct PtrTable {
   const char* src[kCopyMaxPtrs];

@@ -25,6 +25,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -164,11 +165,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // tile i+1 overlaps the epilogue of tile i through two TMEM accumulators.
 // kBMN: B is the logical row-major [K, N] (N contiguous, MN-major operand)
 // instead of Bt [N, K].
+// A batch of equally shaped problems (one per simulated device of a mesh)
+// shares one persistent launch: tiles of all problems form one work list,
+// so small per-device GEMMs do not each pay a partial last wave.
+constexpr int kMaxBatch = 8;
+struct GemmArgs {
+  CUtensorMap a[kMaxBatch];
+  CUtensorMap b[kMaxBatch];
+  void* c[kMaxBatch];
+  int count, M, N, K, ldc;
+};
+
 template <int BN, bool kGelu, bool kOutF32, bool kBMN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b, void* __restrict__ out, int M,
-                      int N, int K, int ldc) {
+    gemm_bf16_tcgen05(const __grid_constant__ GemmArgs args) {
+  const int M = args.M, N = args.N, K = args.K, ldc = args.ldc;
   using S = Smem<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -185,7 +196,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x % 32;
   const int kblocks = (K + kBK - 1) / kBK;
   const int n_tiles = (N + BN - 1) / BN;
-  const int tiles = ((M + kBM - 1) / kBM) * n_tiles;
+  const int per_problem = ((M + kBM - 1) / kBM) * n_tiles;
+  const int tiles = per_problem * args.count;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
@@ -197,8 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_empty[a], 4);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    for (int g = 0; g < args.count; ++g) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.a[g])) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.b[g])) : "memory");
+    }
   }
   if (warp == 1) {  // whole warp allocates 2 x BN fp32 columns of TMEM
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -215,21 +229,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int it = 0;  // ring position across tiles
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t / n_tiles) * kBM, n0 = (t % n_tiles) * BN;
+        const int g = t / per_problem, lt = t % per_problem;
+        const int m0 = (lt / n_tiles) * kBM, n0 = (lt % n_tiles) * BN;
+        const CUtensorMap* map_a = &args.a[g];
+        const CUtensorMap* map_b = &args.b[g];
         for (int kb = 0; kb < kblocks; ++kb, ++it) {
           const int s = it % S::kStages;
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
           mbar_expect_tx(&full[s], S::kStageA + S::kStageB);
-          tma_load_2d(tiles_a + s * S::kStageA, &map_a, &full[s], kb * kBK, m0);
+          tma_load_2d(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
           if constexpr (kBMN) {
             // BN/64 boxes of [64 k][64 n], one MN swizzle atom column each
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(tiles_b + s * S::kStageB + j * 8192, &map_b, &full[s], n0 + j * 64,
+              tma_load_2d(tiles_b + s * S::kStageB + j * 8192, map_b, &full[s], n0 + j * 64,
                           kb * kBK);
           } else {
-            tma_load_2d(tiles_b + s * S::kStageB, &map_b, &full[s], kb * kBK, n0);
+            tma_load_2d(tiles_b + s * S::kStageB, map_b, &full[s], kb * kBK, n0);
           }
         }
       }
@@ -270,7 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
       const int acc = local & 1;
-      const int m0 = (t / n_tiles) * kBM, n0 = (t % n_tiles) * BN;
+      const int g = t / per_problem, lt = t % per_problem;
+      const int m0 = (lt / n_tiles) * kBM, n0 = (lt % n_tiles) * BN;
+      void* const out = args.c[g];
       const int row = m0 + quarter * 32 + lane;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -368,8 +387,7 @@ bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int
 }
 
 template <int BN, bool G, bool F, bool BMN>
-cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, void* c, int M, int N, int K,
-                        int ldc, cudaStream_t stream) {
+cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
   auto kernel = gemm_bf16_tcgen05<BN, G, F, BMN>;
   static bool configured = false;
   if (!configured) {
@@ -384,45 +402,69 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, void* c, int
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
   }();
-  const int tiles = ((N + BN - 1) / BN) * ((M + kBM - 1) / kBM);
+  const int tiles = ((args.N + BN - 1) / BN) * ((args.M + kBM - 1) / kBM) * args.count;
   const int grid = tiles < sms ? tiles : sms;
-  kernel<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(a, b, c, M, N, K, ldc);
+  kernel<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
 template <int BN, bool BMN>
-cudaError_t dispatch(const CUtensorMap& a, const CUtensorMap& b, void* c, int M, int N, int K,
-                     int ldc, bool out_f32, bool gelu, cudaStream_t stream) {
+cudaError_t dispatch(const GemmArgs& args, bool out_f32, bool gelu, cudaStream_t stream) {
   if (gelu)
-    return out_f32 ? launch_gemm<BN, true, true, BMN>(a, b, c, M, N, K, ldc, stream)
-                   : launch_gemm<BN, true, false, BMN>(a, b, c, M, N, K, ldc, stream);
-  return out_f32 ? launch_gemm<BN, false, true, BMN>(a, b, c, M, N, K, ldc, stream)
-                 : launch_gemm<BN, false, false, BMN>(a, b, c, M, N, K, ldc, stream);
+    return out_f32 ? launch_gemm<BN, true, true, BMN>(args, stream)
+                   : launch_gemm<BN, true, false, BMN>(args, stream);
+  return out_f32 ? launch_gemm<BN, false, true, BMN>(args, stream)
+                 : launch_gemm<BN, false, false, BMN>(args, stream);
 }
 
 }  // namespace
 
-// C[M,N] = A[M,K] . B with B given as Bt [N,K] (b_kn = false, nn.Linear
-// layout) or as row-major [K,N] (b_kn = true); bf16 in, fp32 accumulate.
-// out_f32 selects the output type; gelu applies exact-erf GELU in the epilogue.
+// count equally shaped problems C_i[M,N] = A_i[M,K] . B_i, B_i given as Bt
+// [N,K] (b_kn = false, nn.Linear layout) or as row-major [K,N] (b_kn = true);
+// bf16 in, fp32 accumulate. out_f32 selects the output type; gelu applies
+// exact-erf GELU in the epilogue. All problems share one persistent launch
+// (chunks of kMaxBatch).
+cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,
+                              int count, int M, int N, int K, int lda, int ldb, int ldc,
+                              bool b_kn, bool out_f32, bool gelu, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || count <= 0) return cudaSuccess;
+  if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;  // TMA row alignment
+  const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
+  for (int first = 0; first < count; first += kMaxBatch) {
+    GemmArgs args;
+    std::memset(&args, 0, sizeof(args));
+    args.count = std::min(kMaxBatch, count - first);
+    args.M = M;
+    args.N = N;
+    args.K = K;
+    args.ldc = ldc;
+    for (int i = 0; i < args.count; ++i) {
+      const void* a = A[first + i];
+      const void* b = B[first + i];
+      if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
+        return cudaErrorInvalidValue;
+      if (!make_map(&args.a[i], a, M, K, lda, kBM)) return cudaErrorInvalidValue;
+      const bool ok = b_kn ? make_map(&args.b[i], b, K, N, ldb, kBK, 64)
+                           : make_map(&args.b[i], b, N, K, ldb, bn);
+      if (!ok) return cudaErrorInvalidValue;
+      args.c[i] = C[first + i];
+    }
+    cudaError_t e;
+    if (b_kn)
+      e = bn == 256 ? dispatch<256, true>(args, out_f32, gelu, stream)
+                    : dispatch<128, true>(args, out_f32, gelu, stream);
+    else
+      e = bn == 256 ? dispatch<256, false>(args, out_f32, gelu, stream)
+                    : dispatch<128, false>(args, out_f32, gelu, stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                       int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream) {
-  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
-  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
-      (lda * 2) % 16 || (ldb * 2) % 16)
-    return cudaErrorInvalidValue;  // TMA needs 16-byte aligned rows
-  const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K, lda, kBM)) return cudaErrorInvalidValue;
-  if (b_kn) {
-    if (!make_map(&mb, B, K, N, ldb, kBK, 64)) return cudaErrorInvalidValue;
-    return bn == 256 ? dispatch<256, true>(ma, mb, C, M, N, K, ldc, out_f32, gelu, stream)
-                     : dispatch<128, true>(ma, mb, C, M, N, K, ldc, out_f32, gelu, stream);
-  }
-  if (!make_map(&mb, B, N, K, ldb, bn)) return cudaErrorInvalidValue;
-  return bn == 256 ? dispatch<256, false>(ma, mb, C, M, N, K, ldc, out_f32, gelu, stream)
-                   : dispatch<128, false>(ma, mb, C, M, N, K, ldc, out_f32, gelu, stream);
+  return gemm_bf16_batched(&A, &B, &C, 1, M, N, K, lda, ldb, ldc, b_kn, out_f32, gelu, stream);
 }
 
 cudaError_t gemm_bf16_tn(const void* A, const void* Bt, void* C, int M, int N, int K, int lda,

@@ -45,13 +45,13 @@ void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorM
     throw RuntimeError(APL_ERR_ARG, "local GEMM extents exceed int32");
   const bool fuse_gelu = epilogue == APL_EPI_GELU && !s.partial_sum;
   const int nl = mesh.num_local();
-  for (int d = 0; d < nl; ++d) {
-    check_cuda(gemm_bf16(A[d], B[d], C[d], static_cast<int>(m), static_cast<int>(n),
-                         static_cast<int>(k), static_cast<int>(k),
-                         static_cast<int>(b_kn ? n : k), static_cast<int>(n), b_kn,
-                         out_dtype == APL_F32, fuse_gelu, stream),
-               "tcgen05 GEMM launch");
-  }
+  // Every local device has the same shard shapes: one persistent batched
+  // launch covers all of them (a simulated mesh runs 8 GEMMs as one).
+  check_cuda(gemm_bf16_batched(A, B, C, nl, static_cast<int>(m), static_cast<int>(n),
+                               static_cast<int>(k), static_cast<int>(k),
+                               static_cast<int>(b_kn ? n : k), static_cast<int>(n), b_kn,
+                               out_dtype == APL_F32, fuse_gelu, stream),
+             "tcgen05 GEMM launch");
   if (s.partial_sum) {
     all_reduce(mesh, s.reduce_axes, C, static_cast<size_t>(m * n), out_dtype, stream);
     if (epilogue == APL_EPI_GELU)

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <numeric>
+#include <cstdlib>
 #include <cstring>
 
 #include "apl.h"
@@ -128,9 +129,23 @@ int natural_vec(const std::vector<CopyDesc>& descs) {
   return pow2_vec(g);
 }
 
-CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec) {
+bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec) {
+  static const int forced = [] {
+    const char* e = std::getenv("APL_COPY_ENGINE");  // "ldg" | "bulk" | unset (auto)
+    if (e == nullptr) return -1;
+    return std::string(e) == "bulk" ? 1 : std::string(e) == "ldg" ? 0 : -1;
+  }();
+  if (vec != 16 || descs.empty() || forced == 0) return false;
+  for (const CopyDesc& d : descs)
+    if (d.bytes() > 0 && (d.run_bytes < (forced == 1 ? 16 : kBulkMinRun) || d.run_bytes % 16))
+      return false;
+  return true;
+}
+
+CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool bulk) {
   CompiledCopies cc;
   cc.vec = vec;
+  cc.bulk = bulk;
   std::vector<CopyDesc> flat;
   for (const CopyDesc& d : descs)
     if (d.bytes() > 0) split_large(d, vec, flat);
@@ -151,8 +166,9 @@ CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec) {
     h.nouter = d.nouter;
     cc.max_outer = std::max(cc.max_outer, d.nouter);
     cc.max_fan = std::max(cc.max_fan, d.ndst);
-    const int64_t upr = d.run_bytes / vec;
+    const int64_t upr = bulk ? (d.run_bytes + kBulkSeg - 1) / kBulkSeg : d.run_bytes / vec;
     h.units_per_run = make_fastdiv(static_cast<uint32_t>(upr));
+    h.run_bytes = d.run_bytes;
     int64_t rows = 1;
     for (int j = 0; j < d.nouter; ++j) {
       h.ext[j] = make_fastdiv(static_cast<uint32_t>(d.ext[j]));
@@ -180,6 +196,10 @@ void free_copies(CompiledCopies& c) {
 
 void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream) {
   if (c.empty()) return;
+  if (c.bulk) {
+    check_cuda(launch_bulk_copy(c.table, c.ntasks, c.total_units, ptrs, stream), "bulk copy launch");
+    return;
+  }
   check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, c.max_outer, c.max_fan, ptrs,
                              stream),
              "box_copy launch");
@@ -288,8 +308,10 @@ namespace {
 
 const CompiledCopies& compiled_for(std::map<int, CompiledCopies>& cache,
                                    const std::vector<CopyDesc>& host, int vec) {
-  auto it = cache.find(vec);
-  if (it == cache.end()) it = cache.emplace(vec, compile_copies(host, vec)).first;
+  const bool bulk = bulk_eligible(host, vec);
+  const int key = vec + (bulk ? 1000 : 0);
+  auto it = cache.find(key);
+  if (it == cache.end()) it = cache.emplace(key, compile_copies(host, vec, bulk)).first;
   return it->second;
 }
 

@@ -39,6 +39,9 @@ uint64_t launch_count();
 cudaError_t launch_gelu_inplace(void* buf, size_t count, int dtype, cudaStream_t stream);
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                       int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream);
+cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,
+                              int count, int M, int N, int K, int lda, int ldb, int ldc,
+                              bool b_kn, bool out_f32, bool gelu, cudaStream_t stream);
 
 // One sharded-matmul strategy (reference OpStrategy, intraop.hpp:34-49).
 struct MatmulStrategy {
@@ -58,12 +61,18 @@ struct CompiledCopies {
   int max_fan = 1;
   int64_t bytes = 0;        // bytes read (each source byte once)
   int64_t write_bytes = 0;  // bytes written (fan-out counted per destination)
+  bool bulk = false;        // TMA bulk engine (units = kBulkSeg segments)
   bool empty() const { return ntasks == 0; }
 };
 
+cudaError_t launch_bulk_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
+                             const PtrTable& ptrs, cudaStream_t stream);
+// True when every run of the table suits the TMA bulk engine.
+bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec);
+
 // Largest vector width (16/8/4/2/1) dividing every run, stride and offset.
 int natural_vec(const std::vector<CopyDesc>& descs);
-CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec);
+CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool bulk = false);
 void free_copies(CompiledCopies& c);
 void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream);
 

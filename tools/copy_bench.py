@@ -45,7 +45,43 @@ def ev_time(fn, iters):
     return a.elapsed_time(b) / iters
 
 
+def sweep():
+    """BASELINE config 2: mesh [8], S0R->RR and S0R->RS0, global 1 MiB .. 4 GiB,
+    shape [T/(e*8192), 8192], fp32 and bf16 (collapsed exchange, one launch)."""
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    mesh = Mesh.local([8])
+    for eb, dt in ((4, torch.int32), (2, torch.int16)):
+        for k in range(20, 33):
+            total = 1 << k
+            rows = total // (eb * 8192)
+            if rows < 8:
+                continue
+            meta = TensorMeta((rows, 8192), eb)
+            s = ShardingSpec.parse("S0R", 1)
+            ins = [torch.randint(-100, 100, s.local_shape(meta, mesh.geo), dtype=dt, device="cuda")
+                   for _ in range(8)]
+            for tgt in ("RR", "RS0"):
+                t = ShardingSpec.parse(tgt, 1)
+                path = find_transform_path(s, t, mesh.geo, meta)
+                outs = [torch.empty(t.local_shape(meta, mesh.geo), dtype=dt, device="cuda")
+                        for _ in range(8)]
+                tr = mesh.exchange_traffic(s, t, meta)
+                nbytes = tr["hbm_read"] + tr["hbm_write"]
+                iters = max(3, min(200, int(2e9 // max(nbytes, 1))))
+                ms = ev_time(lambda: mesh.run_path(path, meta, ins, outs, fuse=True), iters)
+                print(json.dumps({"case": f"[8] S0R->{tgt}", "global_bytes": total, "eb": eb,
+                                  "alg_bytes": nbytes, "ms": round(ms, 5),
+                                  "gbs": round(nbytes / ms / 1e6, 1),
+                                  "frac": round(nbytes / ms / 1e6 / peak, 3)}), flush=True)
+                del outs
+            del ins
+            torch.cuda.empty_cache()
+
+
 def main():
+    if "--sweep" in sys.argv:
+        return sweep()
     quick = "--quick" in sys.argv
     variant = os.environ.get("APL_COPY_VARIANT", "0")
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
