@@ -164,8 +164,11 @@ def run_ours(args):
             bus = (ndev - 1) * in_bytes
         else:
             bus = (ndev - 1) * in_bytes // ndev
+        engine = mesh.exchange_engine(s, t, meta)
         convs.append(dict(name=f"{a}->{b}", path=path, ins=ins, outs=outs, hbm=hbm, bus=bus,
-                          in_bytes=in_bytes, out_bytes=out_bytes))
+                          in_bytes=in_bytes, out_bytes=out_bytes,
+                          kernel="bulk_copy_kernel (TMA cp.async.bulk ring)" if engine == "bulk"
+                          else "box_copy_kernel<16,U,NO,MINB> (LDG/STG.128)"))
 
     def step():
         for c in convs:
@@ -233,7 +236,7 @@ def run_ours(args):
         traffic = entry["dram_bytes"] if entry else None
     if ws == 1:
         achieved = dom["hbm"] / (dom_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": f"box_copy_kernel<16,4> ({dom['name']}, 8 simulated devices)",
+        roof = {"bound": "hbm", "kernel": f"{dom['kernel']} ({dom['name']}, 8 simulated devices)",
                 "achieved": round(achieved, 1), "peak": hbm_peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_launch": dom["hbm"],

@@ -201,6 +201,11 @@ int apl_exchange_traffic(apl_mesh* mesh, const apl_spec* src, const apl_spec* tg
                          const apl_meta* meta, int64_t* hbm_read, int64_t* hbm_write,
                          int64_t* wire_in);
 
+/* Copy engine the collapsed src->tgt exchange runs on (16-byte aligned
+ * buffers): 0 = vectorised LDG/STG box copy, 1 = TMA bulk engine. */
+int apl_exchange_engine(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                        const apl_meta* meta, int* engine);
+
 /* Host-only dry run of the distributed executor: the exact schedule rank
  * `rank` would run for the collapsed src->tgt exchange (pack/self copies,
  * NCCL sends/recvs with their staging offsets, unpack copies) as JSON.

@@ -490,6 +490,20 @@ int apl_exchange_traffic(apl_mesh* mesh, const apl_spec* src, const apl_spec* tg
   });
 }
 
+int apl_exchange_engine(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                        const apl_meta* meta, int* engine) {
+  return guarded([&] {
+    need(mesh && engine, "null argument");
+    const ShardingSpec s = to_spec(src), g = to_spec(tgt);
+    const TensorMeta t = to_meta(meta);
+    if (!s.valid_for(t, mesh->impl.geo) || !g.valid_for(t, mesh->impl.geo))
+      throw autoplan::ShapeError("spec is not valid for the tensor/mesh");
+    auto ex = apl::get_exchange(mesh->impl, s, g, t);
+    const auto& host = mesh->impl.distributed ? ex->host_pre : ex->host_copies;
+    *engine = apl::bulk_eligible(host, apl::natural_vec(host)) ? 1 : 0;
+  });
+}
+
 int apl_exchange_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_spec* src,
                                const apl_spec* tgt, const apl_meta* meta, char* out, size_t cap,
                                size_t* len) {
