@@ -165,14 +165,15 @@ def run_ours(args):
         else:
             bus = (ndev - 1) * in_bytes // ndev
         engine = mesh.exchange_engine(s, t, meta)
-        convs.append(dict(name=f"{a}->{b}", path=path, ins=ins, outs=outs, hbm=hbm, bus=bus,
+        conv = mesh.prepare(path, meta, fuse=True)  # public API: compiled once, launched per step
+        convs.append(dict(name=f"{a}->{b}", path=path, conv=conv, ins=ins, outs=outs, hbm=hbm, bus=bus,
                           in_bytes=in_bytes, out_bytes=out_bytes,
                           kernel="bulk_copy_kernel (TMA cp.async.bulk ring)" if engine == "bulk"
                           else "box_copy_kernel<16,U,NO,MINB> (LDG/STG.128)"))
 
     def step():
         for c in convs:
-            mesh.run_path(c["path"], meta, c["ins"], c["outs"], fuse=True, stream=stream)
+            c["conv"](c["ins"], c["outs"], stream=stream)
 
     def barrier():
         if ws > 1:
@@ -198,7 +199,7 @@ def run_ours(args):
         for _ in range(args.steps):
             for c in convs:
                 evs[k][0].record(stream)
-                mesh.run_path(c["path"], meta, c["ins"], c["outs"], fuse=True, stream=stream)
+                c["conv"](c["ins"], c["outs"], stream=stream)
                 evs[k][1].record(stream)
                 k += 1
         t1.record(stream)
@@ -296,7 +297,7 @@ def run_e2e(args, mesh, meta, convs, stream):
         for c, hi, ho in zip(convs, host_in, host_out):
             for x, h in zip(c["ins"], hi):
                 x.copy_(h, non_blocking=True)
-            mesh.run_path(c["path"], meta, c["ins"], c["outs"], fuse=True, stream=stream)
+            c["conv"](c["ins"], c["outs"], stream=stream)
             for h, x in zip(ho, c["outs"]):
                 h.copy_(x, non_blocking=True)
 

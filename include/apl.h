@@ -214,6 +214,19 @@ int apl_exchange_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_sp
                                const apl_spec* tgt, const apl_meta* meta, char* out, size_t cap,
                                size_t* len);
 
+/* Prepared conversion: validates the path and compiles its exchanges once,
+ * so the per-call cost is one lookup-free launch sequence (and the calls can
+ * be captured into a CUDA graph after the first run). Same semantics as
+ * apl_run_path. */
+typedef struct apl_conversion apl_conversion;
+int apl_conversion_create(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                          const apl_step* steps, int nsteps, const apl_meta* meta,
+                          unsigned flags, apl_conversion** out);
+int apl_conversion_workspace(const apl_conversion* conv, size_t* bytes);
+int apl_conversion_run(apl_conversion* conv, const void* const* in, void* const* out, void* ws,
+                       size_t ws_bytes, void* stream);
+int apl_conversion_destroy(apl_conversion* conv);
+
 /* Sum partial results over the mesh axes `axes` (partial_sum strategies,
  * intraop.cpp:544-551; planner.cpp:263-282). In place; every member of an
  * axis group ends with identical bytes. */

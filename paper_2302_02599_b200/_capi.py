@@ -104,6 +104,12 @@ _SIGS = {
                                C.c_void_p]),
     "apl_exchange_traffic": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_int64),
                                        P(C.c_int64), P(C.c_int64)]),
+    "apl_conversion_create": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Step), C.c_int, P(Meta),
+                                        C.c_uint, P(C.c_void_p)]),
+    "apl_conversion_workspace": (C.c_int, [C.c_void_p, P(C.c_size_t)]),
+    "apl_conversion_run": (C.c_int, [C.c_void_p, P(C.c_void_p), P(C.c_void_p), C.c_void_p,
+                                     C.c_size_t, C.c_void_p]),
+    "apl_conversion_destroy": (C.c_int, [C.c_void_p]),
     "apl_exchange_engine": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_int)]),
     "apl_exchange_schedule_json": (C.c_int, [P(MeshDesc), C.c_int, P(Spec), P(Spec), P(Meta),
                                              C.c_char_p, C.c_size_t, P(C.c_size_t)]),

@@ -25,6 +25,9 @@ struct apl_path_cache {
 struct apl_mesh {
   apl::Mesh impl;
 };
+struct apl_conversion {
+  apl::Conversion impl;  // holds a pointer to its mesh: destroy before the mesh
+};
 
 namespace {
 
@@ -488,6 +491,43 @@ int apl_exchange_traffic(apl_mesh* mesh, const apl_spec* src, const apl_spec* tg
     if (hbm_write) *hbm_write = w;
     if (wire_in) *wire_in = ex->wire_bytes_in;
   });
+}
+
+int apl_conversion_create(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                          const apl_step* steps, int nsteps, const apl_meta* meta,
+                          unsigned flags, apl_conversion** out) {
+  return guarded([&] {
+    need(mesh && out, "null argument");
+    auto* c = new apl_conversion();
+    try {
+      c->impl = apl::prepare_conversion(mesh->impl, to_spec(src), to_spec(tgt),
+                                        to_steps(steps, nsteps), to_meta(meta),
+                                        (flags & APL_FUSE_CHAIN) != 0);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int apl_conversion_workspace(const apl_conversion* conv, size_t* bytes) {
+  return guarded([&] {
+    need(conv && bytes, "null argument");
+    *bytes = apl::conversion_workspace(conv->impl);
+  });
+}
+
+int apl_conversion_run(apl_conversion* conv, const void* const* in, void* const* out, void* ws,
+                       size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    need(conv && in && out, "null argument");
+    apl::run_conversion(conv->impl, in, out, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int apl_conversion_destroy(apl_conversion* conv) {
+  return guarded([&] { delete conv; });
 }
 
 int apl_exchange_engine(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,

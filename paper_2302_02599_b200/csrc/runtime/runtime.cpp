@@ -425,71 +425,79 @@ void validate_steps(const autoplan::ShardingSpec& src, const autoplan::ShardingS
                                         tgt.to_string());
 }
 
-struct StepPlan {
-  std::vector<std::shared_ptr<Exchange>> hops;
-  int64_t inter_bytes = 0;  // per ping-pong region
-  int64_t staging = 0;
-};
+}  // namespace
 
-StepPlan plan_steps(Mesh& mesh, const autoplan::ShardingSpec& src,
-                    const std::vector<autoplan::TransformStep>& steps,
-                    const autoplan::TensorMeta& meta) {
-  StepPlan sp;
+Conversion prepare_conversion(Mesh& mesh, const autoplan::ShardingSpec& src,
+                              const autoplan::ShardingSpec& tgt,
+                              const std::vector<autoplan::TransformStep>& steps,
+                              const autoplan::TensorMeta& meta, bool fuse) {
+  if (!src.valid_for(meta, mesh.geo) || !tgt.valid_for(meta, mesh.geo))
+    throw RuntimeError(APL_ERR_SHAPE, "spec is not valid for the tensor/mesh");
+  validate_steps(src, tgt, steps, mesh.geo, meta);
+  Conversion cv;
+  cv.mesh = &mesh;
+  if (fuse || steps.size() <= 1) {
+    cv.hops.push_back(get_exchange(mesh, src, tgt, meta));
+    cv.staging = static_cast<int64_t>(exchange_workspace(*cv.hops[0]));
+    return cv;
+  }
   const autoplan::ShardingSpec* cur = &src;
   for (size_t i = 0; i < steps.size(); ++i) {
     auto ex = get_exchange(mesh, *cur, steps[i].result, meta);
-    sp.staging = std::max<int64_t>(sp.staging, static_cast<int64_t>(exchange_workspace(*ex)));
+    cv.staging = std::max<int64_t>(cv.staging, static_cast<int64_t>(exchange_workspace(*ex)));
     if (i + 1 < steps.size())
-      sp.inter_bytes = std::max(sp.inter_bytes, align_up(ex->out_bytes) * mesh.num_local());
-    sp.hops.push_back(std::move(ex));
+      cv.inter_bytes = std::max(cv.inter_bytes, align_up(ex->out_bytes) * mesh.num_local());
+    cv.hops.push_back(std::move(ex));
     cur = &steps[i].result;
   }
-  return sp;
+  return cv;
 }
 
-}  // namespace
+size_t conversion_workspace(const Conversion& cv) {
+  return static_cast<size_t>(2 * cv.inter_bytes + cv.staging);
+}
+
+void run_conversion(Conversion& cv, const void* const* in, void* const* out, void* ws,
+                    size_t ws_bytes, cudaStream_t stream) {
+  Mesh& mesh = *cv.mesh;
+  if (ws_bytes < conversion_workspace(cv))
+    throw RuntimeError(APL_ERR_ARG, "workspace smaller than apl_path_workspace_bytes");
+  if (cv.hops.size() == 1) {
+    run_exchange(mesh, *cv.hops[0], in, out, ws, ws_bytes, stream);
+    return;
+  }
+  const int nl = mesh.num_local();
+  char* region[2] = {static_cast<char*>(ws), static_cast<char*>(ws) + cv.inter_bytes};
+  char* staging = static_cast<char*>(ws) + 2 * cv.inter_bytes;
+  std::vector<const void*> cur_in(in, in + nl);
+  std::vector<void*> next(static_cast<size_t>(nl));
+  for (size_t i = 0; i < cv.hops.size(); ++i) {
+    const bool last = i + 1 == cv.hops.size();
+    if (last) {
+      for (int j = 0; j < nl; ++j) next[static_cast<size_t>(j)] = out[j];
+    } else {
+      const int64_t stride = align_up(cv.hops[i]->out_bytes);
+      for (int j = 0; j < nl; ++j) next[static_cast<size_t>(j)] = region[i % 2] + j * stride;
+    }
+    run_exchange(mesh, *cv.hops[i], cur_in.data(), next.data(), staging,
+                 static_cast<size_t>(cv.staging), stream);
+    for (int j = 0; j < nl; ++j) cur_in[static_cast<size_t>(j)] = next[static_cast<size_t>(j)];
+  }
+}
 
 size_t path_workspace(Mesh& mesh, const autoplan::ShardingSpec& src,
                       const autoplan::ShardingSpec& tgt,
                       const std::vector<autoplan::TransformStep>& steps,
                       const autoplan::TensorMeta& meta, bool fuse) {
-  if (fuse || steps.empty()) return exchange_workspace(*get_exchange(mesh, src, tgt, meta));
-  StepPlan sp = plan_steps(mesh, src, steps, meta);
-  return static_cast<size_t>(2 * sp.inter_bytes + sp.staging);
+  return conversion_workspace(prepare_conversion(mesh, src, tgt, steps, meta, fuse));
 }
 
 void run_path(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::ShardingSpec& tgt,
               const std::vector<autoplan::TransformStep>& steps,
               const autoplan::TensorMeta& meta, const void* const* in, void* const* out,
               void* ws, size_t ws_bytes, bool fuse, cudaStream_t stream) {
-  if (!src.valid_for(meta, mesh.geo) || !tgt.valid_for(meta, mesh.geo))
-    throw RuntimeError(APL_ERR_SHAPE, "spec is not valid for the tensor/mesh");
-  validate_steps(src, tgt, steps, mesh.geo, meta);
-  if (fuse || steps.size() <= 1) {
-    auto ex = get_exchange(mesh, src, tgt, meta);
-    run_exchange(mesh, *ex, in, out, ws, ws_bytes, stream);
-    return;
-  }
-  StepPlan sp = plan_steps(mesh, src, steps, meta);
-  if (ws_bytes < static_cast<size_t>(2 * sp.inter_bytes + sp.staging))
-    throw RuntimeError(APL_ERR_ARG, "workspace smaller than apl_path_workspace_bytes");
-  const int nl = mesh.num_local();
-  char* region[2] = {static_cast<char*>(ws), static_cast<char*>(ws) + sp.inter_bytes};
-  char* staging = static_cast<char*>(ws) + 2 * sp.inter_bytes;
-  std::vector<const void*> cur_in(in, in + nl);
-  std::vector<void*> next(static_cast<size_t>(nl));
-  for (size_t i = 0; i < sp.hops.size(); ++i) {
-    const bool last = i + 1 == sp.hops.size();
-    if (last) {
-      for (int j = 0; j < nl; ++j) next[static_cast<size_t>(j)] = out[j];
-    } else {
-      const int64_t stride = align_up(sp.hops[i]->out_bytes);
-      for (int j = 0; j < nl; ++j) next[static_cast<size_t>(j)] = region[i % 2] + j * stride;
-    }
-    run_exchange(mesh, *sp.hops[i], cur_in.data(), next.data(), staging,
-                 static_cast<size_t>(sp.staging), stream);
-    for (int j = 0; j < nl; ++j) cur_in[static_cast<size_t>(j)] = next[static_cast<size_t>(j)];
-  }
+  Conversion cv = prepare_conversion(mesh, src, tgt, steps, meta, fuse);
+  run_conversion(cv, in, out, ws, ws_bytes, stream);
 }
 
 void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, size_t count,

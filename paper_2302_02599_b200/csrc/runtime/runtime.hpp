@@ -121,6 +121,24 @@ size_t exchange_workspace(const Exchange& ex);
 void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* out,
                   void* ws, size_t ws_bytes, cudaStream_t stream);
 
+// A validated path with its exchanges compiled: one hop when collapsed (or a
+// single step), one hop per reference step otherwise (intermediates ping-pong
+// through the workspace).
+struct Conversion {
+  Mesh* mesh = nullptr;
+  std::vector<std::shared_ptr<Exchange>> hops;
+  int64_t inter_bytes = 0;  // per ping-pong region
+  int64_t staging = 0;      // distributed pack/unpack staging
+};
+
+Conversion prepare_conversion(Mesh& mesh, const autoplan::ShardingSpec& src,
+                              const autoplan::ShardingSpec& tgt,
+                              const std::vector<autoplan::TransformStep>& steps,
+                              const autoplan::TensorMeta& meta, bool fuse);
+size_t conversion_workspace(const Conversion& cv);
+void run_conversion(Conversion& cv, const void* const* in, void* const* out, void* ws,
+                    size_t ws_bytes, cudaStream_t stream);
+
 size_t path_workspace(Mesh& mesh, const autoplan::ShardingSpec& src,
                       const autoplan::ShardingSpec& tgt,
                       const std::vector<autoplan::TransformStep>& steps,

@@ -105,6 +105,7 @@ class PlanExecutor:
             for slot, (src, _) in enumerate(n["inputs"]):
                 self._consumers.setdefault(src, []).append((n["id"], slot))
         self._paths = {}
+        self._convs = {}
 
     # ---- layout bookkeeping ------------------------------------------------
     def _meta(self, nid: str) -> TensorMeta:
@@ -188,9 +189,13 @@ class PlanExecutor:
                 for _ in range(self.mesh.num_local)]
 
     def _convert(self, nid, shards, src, tgt, stream):
-        path = self._path(nid, src, tgt)
+        key = (nid, str(src), str(tgt))
+        conv = self._convs.get(key)
+        if conv is None:  # compiled once per edge, reused every forward
+            conv = self.mesh.prepare(self._path(nid, src, tgt), self._meta(nid), fuse=self.fuse)
+            self._convs[key] = conv
         outs = self._alloc(nid, tgt, shards[0])
-        self.mesh.run_path(path, self._meta(nid), shards, outs, fuse=self.fuse, stream=stream)
+        conv(shards, outs, stream=stream)
         return outs
 
     def forward(self, feeds: dict, stream=None) -> list:

@@ -166,6 +166,12 @@ class Mesh:
             C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()),
             A.FUSE_CHAIN if fuse else A.STEPWISE, _stream_handle(stream)))
 
+    def prepare(self, path: TransformPath, meta: TensorMeta, fuse: bool = True) -> "Conversion":
+        """Validate + compile `path` once; the returned callable runs it with
+        no per-call planning (and can be captured into a CUDA graph after
+        its first run)."""
+        return Conversion(self, path, meta, fuse)
+
     def run_step(self, src: ShardingSpec, step: TransformStep, meta: TensorMeta, inputs,
                  outputs, stream=None) -> None:
         path = TransformPath(src, step.result, [step])
@@ -220,3 +226,54 @@ class Mesh:
         ax = (C.c_int32 * max(1, len(axes)))(*axes)
         check(A.lib().apl_all_reduce(self._h, ax, len(axes), _ptrs(tensors),
                                      tensors[0].numel(), dt, _stream_handle(stream)))
+
+
+class Conversion:
+    """A prepared conversion (apl_conversion_*): the path is validated and its
+    exchanges compiled at construction; calling it only launches kernels /
+    collectives. Keeps its Mesh alive."""
+
+    def __init__(self, mesh: Mesh, path: TransformPath, meta: TensorMeta, fuse: bool = True):
+        self.mesh, self.path, self.meta, self.fuse = mesh, path, meta, fuse
+        h = C.c_void_p()
+        steps = path.steps_c()
+        check(A.lib().apl_conversion_create(mesh._h, C.byref(path.source.c()),
+                                            C.byref(path.target.c()), steps, len(path.steps),
+                                            C.byref(meta.c()),
+                                            A.FUSE_CHAIN if fuse else A.STEPWISE, C.byref(h)))
+        self._h = h
+        n = C.c_size_t()
+        check(A.lib().apl_conversion_workspace(h, C.byref(n)))
+        self.workspace_bytes = n.value
+        self._ws = torch.empty(max(n.value, 256), dtype=torch.uint8, device=f"cuda:{mesh.device}")
+        self._in_bytes = path.source.per_device_bytes(meta, mesh.geo)
+        self._out_bytes = path.target.per_device_bytes(meta, mesh.geo)
+        self._ptr_cache = {}
+
+    def _ptrs(self, ins, outs):
+        key = tuple(t.data_ptr() for t in ins) + tuple(t.data_ptr() for t in outs)
+        hit = self._ptr_cache.get(key)
+        if hit is None:
+            self.mesh._check_bufs(ins, self._in_bytes, "inputs")
+            self.mesh._check_bufs(outs, self._out_bytes, "outputs")
+            hit = (_ptrs(ins), _ptrs(outs))
+            if len(self._ptr_cache) > 64:
+                self._ptr_cache.clear()
+            self._ptr_cache[key] = hit
+        return hit
+
+    def __call__(self, inputs, outputs, stream=None) -> None:
+        pin, pout = self._ptrs(inputs, outputs)
+        check(A.lib().apl_conversion_run(self._h, pin, pout, C.c_void_p(self._ws.data_ptr()),
+                                         C.c_size_t(self._ws.numel()), _stream_handle(stream)))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            A.lib().apl_conversion_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
