@@ -8,6 +8,7 @@
 // (priced at intraop.cpp:544-551, inserted as <host>.ar nodes at
 // planner.cpp:263-282).
 #include <algorithm>
+#include <vector>
 
 #include "apl.h"
 #include "runtime.hpp"
@@ -19,45 +20,65 @@ void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorM
                     const void* const* B, void* const* C, bool b_kn, int out_dtype, int epilogue,
                     cudaStream_t stream) {
   const auto& geo = mesh.geo;
-  if (b_meta.rank() != 2 || a_meta.rank() < 2)
-    throw RuntimeError(APL_ERR_SHAPE, "matmul wants A[..m.., k] and B[k, n]");
+  // matmul: A[..m.., k] . B[k, n];  batched matmul: A[b, m, k] . B[b, k, n]
+  const bool batched = b_meta.rank() == 3;
+  if (batched ? a_meta.rank() != 3 : (b_meta.rank() != 2 || a_meta.rank() < 2))
+    throw RuntimeError(APL_ERR_SHAPE, "matmul wants A[..m.., k] . B[k, n] or A[b,m,k] . B[b,k,n]");
   if (a_meta.dtype_bytes != 2 || b_meta.dtype_bytes != 2)
     throw RuntimeError(APL_ERR_ARG, "matmul operands must be bf16");
-  if (a_meta.shape.back() != b_meta.shape[0])
-    throw RuntimeError(APL_ERR_SHAPE, "contraction extents differ");
+  const size_t kb = batched ? 1 : 0;  // contraction dim of B
+  if (a_meta.shape.back() != b_meta.shape[kb] || (batched && a_meta.shape[0] != b_meta.shape[0]))
+    throw RuntimeError(APL_ERR_SHAPE, "contraction / batch extents differ");
   autoplan::TensorMeta c_meta = a_meta;
-  c_meta.shape.back() = b_meta.shape[1];
+  c_meta.shape.back() = b_meta.shape.back();
   c_meta.dtype_bytes = out_dtype == APL_F32 ? 4 : 2;
   if (!s.a.valid_for(a_meta, geo) || !s.b.valid_for(b_meta, geo) || !s.c.valid_for(c_meta, geo))
     throw RuntimeError(APL_ERR_SHAPE, "strategy specs are not valid for these tensors");
   const auto la = local_shape(s.a, geo, a_meta);
   const auto lb = local_shape(s.b, geo, b_meta);
   const auto lc = local_shape(s.c, geo, c_meta);
-  int64_t m = 1;
-  for (size_t i = 0; i + 1 < la.size(); ++i) {
-    m *= la[i];
-    if (la[i] != lc[i]) throw RuntimeError(APL_ERR_SHAPE, "A and C shards disagree on m dims");
+  int64_t batch = 1, m = 1;
+  if (batched) {
+    batch = la[0];
+    m = la[1];
+    if (lb[0] != batch || lc[0] != batch || lc[1] != m)
+      throw RuntimeError(APL_ERR_SHAPE, "A, B and C shards disagree on b / m");
+  } else {
+    for (size_t i = 0; i + 1 < la.size(); ++i) {
+      m *= la[i];
+      if (la[i] != lc[i]) throw RuntimeError(APL_ERR_SHAPE, "A and C shards disagree on m dims");
+    }
   }
-  const int64_t k = la.back(), n = lb[1];
-  if (lb[0] != k || lc.back() != n)
+  const int64_t k = la.back(), n = lb.back();
+  if (lb[kb] != k || lc.back() != n)
     throw RuntimeError(APL_ERR_SHAPE, "local shards do not form a matmul");
   if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
     throw RuntimeError(APL_ERR_ARG, "local GEMM extents exceed int32");
   const bool fuse_gelu = epilogue == APL_EPI_GELU && !s.partial_sum;
   const int nl = mesh.num_local();
-  // Every local device has the same shard shapes: one persistent batched
-  // launch covers all of them (a simulated mesh runs 8 GEMMs as one).
-  check_cuda(gemm_bf16_batched(A, B, C, nl, static_cast<int>(m), static_cast<int>(n),
-                               static_cast<int>(k), static_cast<int>(k),
-                               static_cast<int>(b_kn ? n : k), static_cast<int>(n), b_kn,
-                               out_dtype == APL_F32, fuse_gelu, stream),
+  const int eb_c = out_dtype == APL_F32 ? 4 : 2;
+  // Every local device (and every batch element) has the same shard shapes:
+  // all problems go through the persistent batched launcher together (a
+  // simulated mesh runs its 8 GEMMs as one launch).
+  std::vector<const void*> pa, pb;
+  std::vector<void*> pc;
+  for (int d = 0; d < nl; ++d)
+    for (int64_t i = 0; i < batch; ++i) {
+      pa.push_back(static_cast<const char*>(A[d]) + i * m * k * 2);
+      pb.push_back(static_cast<const char*>(B[d]) + i * k * n * 2);
+      pc.push_back(static_cast<char*>(C[d]) + i * m * n * eb_c);
+    }
+  check_cuda(gemm_bf16_batched(pa.data(), pb.data(), pc.data(), static_cast<int>(pa.size()),
+                               static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+                               static_cast<int>(k), static_cast<int>(b_kn ? n : k),
+                               static_cast<int>(n), b_kn, out_dtype == APL_F32, fuse_gelu, stream),
              "tcgen05 GEMM launch");
+  const size_t count = static_cast<size_t>(batch * m * n);
   if (s.partial_sum) {
-    all_reduce(mesh, s.reduce_axes, C, static_cast<size_t>(m * n), out_dtype, stream);
+    all_reduce(mesh, s.reduce_axes, C, count, out_dtype, stream);
     if (epilogue == APL_EPI_GELU)
       for (int d = 0; d < nl; ++d)
-        check_cuda(launch_gelu_inplace(C[d], static_cast<size_t>(m * n), out_dtype, stream),
-                   "gelu launch");
+        check_cuda(launch_gelu_inplace(C[d], count, out_dtype, stream), "gelu launch");
   }
 }
 

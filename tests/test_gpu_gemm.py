@@ -122,6 +122,58 @@ def test_sharded_matmul_strategies(cuda, case, gelu, b_layout):
     run_strategy(mesh_shape, name, a, b, c, red, gelu=gelu, b_layout=b_layout)
 
 
+def test_every_catalog_strategy_on_2x2(cuda):
+    """All reference-catalog matmul strategies on mesh [2,2] (decoded by
+    matmul_strategies, intraop.cpp:141-234) execute to the same product."""
+    from paper_2302_02599_b200.strategies import matmul_strategies
+
+    mesh = Mesh.local([2, 2])
+    geo = mesh.geo
+    m, k, n = 256, 128, 192
+    torch.manual_seed(9)
+    a = torch.randn(m, k, device="cuda").bfloat16()
+    b = (torch.randn(k, n, device="cuda") / k ** 0.5).bfloat16()
+    ref = a.double() @ b.double()
+    cat = matmul_strategies(geo, TensorMeta((m, k), 2), TensorMeta((k, n), 2))
+    assert len(cat) == 16
+    for st in cat:
+        a_sh = [shard(a, st.a, geo, d) for d in range(4)]
+        b_sh = [shard(b, st.b, geo, d) for d in range(4)]
+        c_sh = [torch.empty(st.c.local_shape(TensorMeta((m, n), 2), geo), dtype=torch.bfloat16,
+                            device="cuda") for _ in range(4)]
+        mesh.sharded_matmul(st, TensorMeta((m, k), 2), TensorMeta((k, n), 2), a_sh, b_sh, c_sh,
+                            b_layout="kn")
+        torch.cuda.synchronize()
+        for d in range(4):
+            assert rel_err(c_sh[d], shard(ref, st.c, geo, d)) <= TOL_BF16, st.name
+
+
+def test_batched_matmul_catalog_on_2x2(cuda):
+    """Batched-matmul strategies (split-b/m/n/k and pairs, intraop.cpp:208-231)
+    run as batched tcgen05 GEMMs on the shards."""
+    from paper_2302_02599_b200.strategies import matmul_strategies
+
+    mesh = Mesh.local([2, 2])
+    geo = mesh.geo
+    bsz, m, k, n = 16, 128, 64, 96
+    torch.manual_seed(10)
+    a = torch.randn(bsz, m, k, device="cuda").bfloat16()
+    b = (torch.randn(bsz, k, n, device="cuda") / k ** 0.5).bfloat16()
+    ref = torch.bmm(a.double(), b.double())
+    am, bm, cm = TensorMeta((bsz, m, k), 2), TensorMeta((bsz, k, n), 2), TensorMeta((bsz, m, n), 2)
+    cat = matmul_strategies(geo, am, bm, batched=True)
+    assert any(s.name.startswith("split-bk") for s in cat)
+    for st in cat:
+        a_sh = [shard(a, st.a, geo, d) for d in range(4)]
+        b_sh = [shard(b, st.b, geo, d) for d in range(4)]
+        c_sh = [torch.empty(st.c.local_shape(cm, geo), dtype=torch.bfloat16, device="cuda")
+                for _ in range(4)]
+        mesh.sharded_matmul(st, am, bm, a_sh, b_sh, c_sh, b_layout="kn")
+        torch.cuda.synchronize()
+        for d in range(4):
+            assert rel_err(c_sh[d], shard(ref, st.c, geo, d)) <= TOL_BF16, st.name
+
+
 def test_split_k_fp32_partials(cuda):
     run_strategy([4], "split-k:0", "RS0", "S0R", "RR", [0], out_dtype=torch.float32)
 
