@@ -173,6 +173,26 @@ int apl_nccl_unique_id(uint8_t* out128);
 int apl_mesh_create_nccl(const apl_mesh_desc* mesh, int rank, const uint8_t* nccl_id,
                          int cuda_device, apl_mesh** out);
 int apl_mesh_destroy(apl_mesh* mesh);
+
+/* Distributed mesh over peer memory only (no NCCL): the transport is CUDA
+ * IPC-mapped peer pointers (NVLink through NVSwitch between GPUs; also valid
+ * between processes sharing one GPU). Used by apl_run_pull. */
+int apl_mesh_create_peer(const apl_mesh_desc* mesh, int rank, int cuda_device, apl_mesh** out);
+
+/* Device buffer exported to the other ranks: cudaMalloc'd (an allocation
+ * base, as IPC requires) plus its 64-byte IPC handle. Freed with the mesh. */
+int apl_peer_alloc(apl_mesh* mesh, size_t bytes, void** ptr, uint8_t* handle64);
+/* Maps another process's exported buffer; closed with the mesh. */
+int apl_peer_open(apl_mesh* mesh, const uint8_t* handle64, void** ptr);
+
+/* Fused collapsed exchange over peer memory: ONE kernel pulls every piece of
+ * this rank's target shard straight out of the senders' source shards
+ * (peer_in[r] = rank r's source shard mapped into this process, this rank's
+ * own shard at index rank) and writes it in place — no pack, no staging, no
+ * separate collective. The caller orders it after all ranks' writes to their
+ * source shards and keeps them unchanged until every rank has pulled. */
+int apl_run_pull(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt, const apl_meta* meta,
+                 const void* const* peer_in, void* out, void* stream);
 int apl_mesh_info(const apl_mesh* mesh, int* num_devices, int* first_local, int* num_local,
                   int* is_distributed);
 

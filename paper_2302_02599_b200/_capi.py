@@ -94,6 +94,11 @@ _SIGS = {
     "apl_mesh_create_nccl": (C.c_int, [P(MeshDesc), C.c_int, P(C.c_uint8), C.c_int,
                                        P(C.c_void_p)]),
     "apl_mesh_destroy": (C.c_int, [C.c_void_p]),
+    "apl_mesh_create_peer": (C.c_int, [P(MeshDesc), C.c_int, C.c_int, P(C.c_void_p)]),
+    "apl_peer_alloc": (C.c_int, [C.c_void_p, C.c_size_t, P(C.c_void_p), P(C.c_uint8)]),
+    "apl_peer_open": (C.c_int, [C.c_void_p, P(C.c_uint8), P(C.c_void_p)]),
+    "apl_run_pull": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_void_p), C.c_void_p,
+                               C.c_void_p]),
     "apl_mesh_info": (C.c_int, [C.c_void_p, P(C.c_int), P(C.c_int), P(C.c_int), P(C.c_int)]),
     "apl_path_workspace_bytes": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Step), C.c_int,
                                            P(Meta), C.c_uint, P(C.c_size_t)]),

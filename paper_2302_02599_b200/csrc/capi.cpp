@@ -419,6 +419,66 @@ int apl_mesh_create_nccl(const apl_mesh_desc* mesh, int rank, const uint8_t* ncc
   return rc;
 }
 
+int apl_mesh_create_peer(const apl_mesh_desc* mesh, int rank, int cuda_device, apl_mesh** out) {
+  return guarded([&] {
+    need(out, "null out");
+    DeviceMesh m = to_mesh(mesh);
+    need(rank >= 0 && rank < m.num_devices(), "rank out of range");
+    need(m.num_devices() <= APL_MAX_LOCAL, "peer meshes hold at most APL_MAX_LOCAL ranks");
+    apl::check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    auto* h = new apl_mesh();
+    h->impl.geo = std::move(m);
+    h->impl.device = cuda_device;
+    h->impl.distributed = true;
+    h->impl.rank = rank;
+    *out = h;
+  });
+}
+
+int apl_peer_alloc(apl_mesh* mesh, size_t bytes, void** ptr, uint8_t* handle64) {
+  return guarded([&] {
+    need(mesh && ptr && handle64 && bytes > 0, "bad argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "unexpected IPC handle size");
+    apl::check_cuda(cudaSetDevice(mesh->impl.device), "cudaSetDevice");
+    void* p = nullptr;
+    apl::check_cuda(cudaMalloc(&p, bytes), "cudaMalloc(peer buffer)");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      apl::check_cuda(e, "cudaIpcGetMemHandle");
+    }
+    std::lock_guard<std::mutex> hold(mesh->impl.mu);
+    mesh->impl.peer_buffers[p] = true;
+    std::memcpy(handle64, &h, sizeof(h));
+    *ptr = p;
+  });
+}
+
+int apl_peer_open(apl_mesh* mesh, const uint8_t* handle64, void** ptr) {
+  return guarded([&] {
+    need(mesh && ptr && handle64, "bad argument");
+    apl::check_cuda(cudaSetDevice(mesh->impl.device), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    void* p = nullptr;
+    apl::check_cuda(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess),
+                    "cudaIpcOpenMemHandle");
+    std::lock_guard<std::mutex> hold(mesh->impl.mu);
+    mesh->impl.peer_buffers[p] = false;
+    *ptr = p;
+  });
+}
+
+int apl_run_pull(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt, const apl_meta* meta,
+                 const void* const* peer_in, void* out, void* stream) {
+  return guarded([&] {
+    need(mesh && peer_in && out, "null argument");
+    apl::run_pull(mesh->impl, to_spec(src), to_spec(tgt), to_meta(meta), peer_in, out,
+                  static_cast<cudaStream_t>(stream));
+  });
+}
+
 int apl_mesh_destroy(apl_mesh* mesh) {
   return guarded([&] { delete mesh; });
 }

@@ -215,9 +215,12 @@ void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stre
 
 Mesh::~Mesh() {
   for (auto& [key, ex] : exchanges) {
-    for (auto* m : {&ex->copies, &ex->pre, &ex->post})
+    for (auto* m : {&ex->copies, &ex->pre, &ex->post, &ex->pull})
       for (auto& [v, c] : *m) free_copies(c);
   }
+  for (auto& [ptr, owned] : peer_buffers)
+    if (owned) cudaFree(ptr);
+    else cudaIpcCloseMemHandle(ptr);
   for (auto& [mask, comm] : sub) ncclCommDestroy(comm);
   if (world != nullptr) ncclCommDestroy(world);
 }
@@ -268,6 +271,10 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
     const int64_t me = mesh.rank;
     // Source buffer ids: 0 = in, 1 = recv staging. Destination: 0 = out, 1 = send staging.
     for (const Piece& p : pieces_for_receiver(src, tgt, mesh.geo, meta, me)) {
+      // Peer-pull form of the same piece: source buffer id = sender rank in
+      // the table of peer-mapped source shards.
+      ex->host_pull.push_back(make_copy(static_cast<int>(p.sender), ls, p.src_lo, 0, lt, p.dst_lo,
+                                        p.ext, eb));
       const int64_t bytes = p.elements() * eb;
       if (p.sender == me) {
         ex->host_pre.push_back(make_copy(0, ls, p.src_lo, 0, lt, p.dst_lo, p.ext, eb));
@@ -375,6 +382,31 @@ void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* 
     run_copies(compiled_for(ex.post, ex.host_post, std::min(palign, natural_vec(ex.host_post))),
                t, stream);
   }
+}
+
+void run_pull(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::ShardingSpec& tgt,
+              const autoplan::TensorMeta& meta, const void* const* peer_in, void* out,
+              cudaStream_t stream) {
+  if (!mesh.distributed) throw RuntimeError(APL_ERR_ARG, "peer pull needs a distributed mesh");
+  if (!src.valid_for(meta, mesh.geo) || !tgt.valid_for(meta, mesh.geo))
+    throw RuntimeError(APL_ERR_SHAPE, "spec is not valid for the tensor/mesh");
+  const int64_t p = mesh.geo.num_devices();
+  if (p > kCopyMaxPtrs) throw RuntimeError(APL_ERR_ARG, "mesh too large for one pull launch");
+  DeviceGuard guard(mesh.device);
+  auto ex = get_exchange(mesh, src, tgt, meta);
+  PtrTable t{};
+  int align = std::min(natural_vec(ex->host_pull), ptr_align(out));
+  for (int64_t i = 0; i < p; ++i) {
+    t.src[i] = static_cast<const char*>(peer_in[i]);
+    align = std::min(align, ptr_align(peer_in[i]));
+  }
+  t.dst[0] = static_cast<char*>(out);
+  std::lock_guard<std::mutex> hold(mesh.mu);
+  // Peer loads stay on the LDG/STG engine (plain ld.global through the
+  // peer aperture, L2-bypassing over NVLink).
+  auto it = ex->pull.find(align);
+  if (it == ex->pull.end()) it = ex->pull.emplace(align, compile_copies(ex->host_pull, align, false)).first;
+  run_copies(it->second, t, stream);
 }
 
 namespace {

@@ -83,7 +83,9 @@ struct Exchange {
   std::vector<CopyDesc> host_copies;  // simulated mesh: everything
   std::vector<CopyDesc> host_pre;     // distributed: pack + self
   std::vector<CopyDesc> host_post;    // distributed: unpack
-  std::map<int, CompiledCopies> copies, pre, post;  // keyed by vector width
+  std::vector<CopyDesc> host_pull;    // distributed, peer mode: one kernel pulls every
+                                      // piece straight from the senders' shards
+  std::map<int, CompiledCopies> copies, pre, post, pull;  // keyed by vector width
   struct Xfer {
     int peer;
     bool direct;  // straight from `in` / into `out` (contiguous box)
@@ -105,6 +107,9 @@ struct Mesh {
   std::map<uint32_t, ncclComm_t> sub;  // axis-subset mask -> communicator
   std::mutex mu;
   std::unordered_map<std::string, std::shared_ptr<Exchange>> exchanges;
+  // Peer memory: buffers this process allocated for export (true) or opened
+  // from another process's IPC handle (false).
+  std::map<void*, bool> peer_buffers;
 
   int num_local() const { return distributed ? 1 : static_cast<int>(geo.num_devices()); }
   ~Mesh();
@@ -138,6 +143,15 @@ Conversion prepare_conversion(Mesh& mesh, const autoplan::ShardingSpec& src,
 size_t conversion_workspace(const Conversion& cv);
 void run_conversion(Conversion& cv, const void* const* in, void* const* out, void* ws,
                     size_t ws_bytes, cudaStream_t stream);
+
+// Distributed mesh, peer mode: one box-copy launch pulls every piece of this
+// rank's target shard straight from the senders' source shards.
+// `peer_in[p]` is rank p's source shard mapped into this process (own shard
+// at index rank). The caller orders it after every rank's writes to its
+// source shard and keeps the sources unchanged until every rank finished.
+void run_pull(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::ShardingSpec& tgt,
+              const autoplan::TensorMeta& meta, const void* const* peer_in, void* out,
+              cudaStream_t stream);
 
 size_t path_workspace(Mesh& mesh, const autoplan::ShardingSpec& src,
                       const autoplan::ShardingSpec& tgt,

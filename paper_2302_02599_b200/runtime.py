@@ -277,3 +277,86 @@ class Conversion:
             self.close()
         except Exception:
             pass
+
+
+# ---- peer memory (fused single-kernel pull exchange) ---------------------------
+class _CudaArray:
+    """Zero-copy view of a raw device allocation for torch.as_tensor."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class PeerMesh:
+    """Distributed mesh whose transport is peer memory (CUDA IPC mapped
+    pointers): every rank exports its source shard buffer, maps every other
+    rank's, and a conversion is ONE kernel per rank pulling its target shard
+    straight out of the peers' shards (apl_run_pull). Works between GPUs
+    over NVLink/NVSwitch and between processes sharing one GPU.
+
+    `group` is any torch.distributed process group (gloo is enough): it only
+    carries the 64-byte IPC handles and the host barriers of `exchange`."""
+
+    def __init__(self, shape: Sequence[int], rank: int, device: int, shard_bytes: int,
+                 group=None):
+        import torch.distributed as dist
+
+        self.geo = DeviceMesh.uniform(shape)
+        self.rank, self.device, self.group = rank, device, group
+        h = C.c_void_p()
+        check(A.lib().apl_mesh_create_peer(C.byref(self.geo.c()), rank, device, C.byref(h)))
+        self._h = h
+        ptr, handle = C.c_void_p(), (C.c_uint8 * 64)()
+        check(A.lib().apl_peer_alloc(h, max(shard_bytes, 16), C.byref(ptr), handle))
+        self.shard_bytes = shard_bytes
+        self.local_ptr = ptr.value
+        self.local = torch.as_tensor(_CudaArray(ptr.value, shard_bytes), device=f"cuda:{device}")
+        handles = [None] * self.geo.num_devices()
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.peer_ptrs = []
+        for r, hb in enumerate(handles):
+            if r == rank:
+                self.peer_ptrs.append(ptr.value)
+                continue
+            p = C.c_void_p()
+            check(A.lib().apl_peer_open(h, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
+            self.peer_ptrs.append(p.value)
+        self._table = (C.c_void_p * len(self.peer_ptrs))(*self.peer_ptrs)
+
+    def shard(self, shape, dtype) -> torch.Tensor:
+        """This rank's exported source shard as a typed tensor view."""
+        n = 1
+        for e in shape:
+            n *= e
+        nbytes = n * torch.empty((), dtype=dtype).element_size()
+        if nbytes > self.shard_bytes:
+            raise ValueError("shard larger than the exported buffer")
+        return self.local[:nbytes].view(dtype).view(*shape)
+
+    def pull(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta, out: torch.Tensor,
+             stream=None) -> None:
+        """Stream-ordered fused exchange into `out` (no host synchronisation)."""
+        if src.per_device_bytes(meta, self.geo) > self.shard_bytes:
+            raise ValueError("source shard larger than the exported buffer")
+        if out.numel() * out.element_size() < tgt.per_device_bytes(meta, self.geo):
+            raise ValueError("output too small")
+        check(A.lib().apl_run_pull(self._h, C.byref(src.c()), C.byref(tgt.c()), C.byref(meta.c()),
+                                   self._table, C.c_void_p(out.data_ptr()), _stream_handle(stream)))
+
+    def exchange(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta,
+                 out: torch.Tensor) -> None:
+        """pull() bracketed by host barriers: every rank's source is complete
+        before anyone reads it and stays untouched until everyone has read."""
+        import torch.distributed as dist
+
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        self.pull(src, tgt, meta, out)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            A.lib().apl_mesh_destroy(self._h)
+            self._h = None

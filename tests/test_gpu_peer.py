@@ -1,0 +1,81 @@
+"""The fused peer-memory exchange on real hardware: one process per mesh
+rank (4 and 8 ranks sharing cuda:0 through CUDA IPC), each rank pulling its
+target shard out of the other ranks' exported source shards with ONE kernel
+(apl_run_pull). Bytes must equal the CPU oracle on every rank. Handles and
+barriers travel over gloo."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    4: [([2, 2], (1024, 512), 2, "S0R", "RS0"), ([2, 2], (256, 384), 4, "S01R", "RS10"),
+        ([2, 2], (64, 96, 32), 2, "S0S1R", "RS1S0"), ([4], (4096, 256), 2, "S0R", "RR"),
+        ([2, 2], (128, 128), 1, "S1S0", "S0S1")],
+    8: [([2, 4], (2048, 2048), 2, "S01R", "S1S0"), ([2, 4], (2048, 2048), 2, "S0S1", "RS01"),
+        ([2, 4], (2048, 2048), 2, "RS01", "RR"), ([2, 2, 2], (2048, 2048), 2, "S012R", "RS012"),
+        ([2, 2, 2], (128, 128, 64), 2, "S0S1R", "RS1S0"), ([8], (8192, 1024), 2, "S0R", "RS0")],
+}
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cases, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from oracle import data as O
+    from paper_2302_02599_b200 import ShardingSpec, TensorMeta
+    from paper_2302_02599_b200.runtime import PeerMesh
+
+    dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}
+    try:
+        biggest = max(int(np.prod(s)) * eb for _, s, eb, _, _ in cases)
+        for mesh_shape, shape, eb, a, b in cases:
+            pm = PeerMesh(mesh_shape, rank, 0, biggest)
+            mr = len(mesh_shape)
+            meta = TensorMeta(shape, eb)
+            g = O.fill_global(shape, eb)
+            mine = O.local(g, O.parse_spec(a, mr), mesh_shape, rank)
+            want = O.local(g, O.parse_spec(b, mr), mesh_shape, rank)
+            src = pm.shard(mine.shape, dt[eb])
+            src.copy_(torch.from_numpy(mine.view(np.dtype(f"i{eb}") if eb > 1 else np.uint8)))
+            out = torch.full(want.shape, -1, dtype=dt[eb], device="cuda:0")
+            pm.exchange(ShardingSpec.parse(a, mr), ShardingSpec.parse(b, mr), meta, out)
+            q.put((rank, a, b, out.cpu().numpy().tobytes() == want.tobytes()))
+            pm.close()
+            dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_peer_pull_exchange_multiprocess(cuda, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES[world], q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    res = []
+    while not q.empty():
+        res.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert len(res) == world * len(CASES[world])
+    assert all(ok for *_, ok in res), [r for r in res if not r[-1]]
