@@ -26,6 +26,7 @@
 #include <atomic>
 #include <cstdint>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -145,6 +146,48 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 
 __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+
+// Epilogue of one accumulator row chunk: 16 fp32 columns of row `row`
+// starting at `col` -> (GELU) -> bf16 / fp32, vectorised when aligned.
+template <bool kGelu, bool kOutF32>
+__device__ __forceinline__ void store_chunk(void* out, int ldc, int M, int N, int row, int col,
+                                            const uint32_t (&r)[16]) {
+  if (row >= M || col >= N) return;
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v[i] = __uint_as_float(r[i]);
+    if (kGelu) v[i] = gelu_erf(v[i]);
+  }
+  if constexpr (kOutF32) {
+    float* dst = static_cast<float*>(out) + static_cast<size_t>(row) * ldc + col;
+    if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 4)
+        *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col + i < N) dst[i] = v[i];
+    }
+  } else {
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(row) * ldc + col;
+    if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      uint32_t p[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        std::memcpy(&p[i], &h, 4);
+      }
+      reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+      reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col + i < N) dst[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
 }
 
 template <int BN>
@@ -299,41 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[16];
         tmem_ld16(lane_addr + uint32_t(c), r);
         const int col = n0 + c;
-        if (row >= M || col >= N) continue;
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          v[i] = __uint_as_float(r[i]);
-          if (kGelu) v[i] = gelu_erf(v[i]);
-        }
-        if constexpr (kOutF32) {
-          float* dst = static_cast<float*>(out) + static_cast<size_t>(row) * ldc + col;
-          if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (col + i < N) dst[i] = v[i];
-          }
-        } else {
-          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(row) * ldc + col;
-          if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-            uint32_t p[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-              std::memcpy(&p[i], &h, 4);
-            }
-            reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
-            reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (col + i < N) dst[i] = __float2bfloat16_rn(v[i]);
-          }
-        }
+        store_chunk<kGelu, kOutF32>(out, ldc, M, N, row, col, r);
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -350,6 +359,232 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "r"(S::kTmemCols));
   }
 }
+
+// ---- 2-CTA (CTA pair) variant: tcgen05.mma.cta_group::2, M = 256 ----------
+//
+// A cluster of two CTAs on one TPC computes a 256 x 256 tile: CTA r loads
+// rows [r*128, r*128+128) of A and rows/columns [r*128, r*128+128) of B
+// into the same shared-memory offsets, the leader (rank 0) issues
+// M=256,N=256 MMAs that read both CTAs' operand halves, and each CTA's
+// TMEM receives its own 128 accumulator rows. Per SM this halves the B
+// operand traffic of the 1-CTA 128 x 256 tile (32 KiB instead of 48 KiB of
+// shared-memory fill per 64-deep K block), which is what limits it.
+//
+// Barrier protocol (same shared-memory offsets in both CTAs):
+//   full[s]      leader only, count 2: leader arrive.expect_tx(both CTAs'
+//                bytes) + peer's remote arrive; both CTAs' TMA loads
+//                complete_tx on the leader's barrier (peer bit cleared).
+//   empty[s]     per CTA, count 1: leader's tcgen05.commit multicast (0b11).
+//   acc_full[a]  per CTA, count 1: leader's commit multicast after the tile.
+//   acc_empty[a] leader only, count 8: 4 epilogue warps x 2 CTAs arrive
+//                (peer through mapa) once their TMEM rows are read.
+namespace pair {
+
+constexpr int kBM = 128;  // rows per CTA (M = 256 per pair)
+constexpr int kBN = 256;  // pair tile N; each CTA stages 128 rows/cols of B
+constexpr int kStageA = kBM * kBK * 2;         // 16 KiB
+constexpr int kStageB = (kBN / 2) * kBK * 2;   // 16 KiB
+constexpr int kStages = 6;
+constexpr int kData = kStages * (kStageA + kStageB);
+constexpr int kBytes = kData + 1024 + 256;
+constexpr int kTmemCols = 512;  // 2 x 256 fp32 accumulator columns
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr_local, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(saddr_local), "r"(rank));
+  return out;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void remote_arrive(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// TMA load whose completion is counted on the leader CTA's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
+                                                 uint64_t* bar_local, int x, int y) {
+  const uint32_t bar = smem_addr(bar_local) & 0xFEFFFFFFu;  // peer bit -> rank 0
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void commit_pair(uint64_t* bar_local) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_addr(bar_local)),
+      "h"(static_cast<uint16_t>(0b11))
+      : "memory");
+}
+
+template <bool kBMN>
+__device__ __forceinline__ constexpr uint32_t instr_desc_pair() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kBMN ? 1 : 0) << 16) |
+         (uint32_t(kBN >> 3) << 17) | (uint32_t((2 * kBM) >> 4) << 24);
+}
+
+template <bool kGelu, bool kOutF32, bool kBMN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_tcgen05_pair(const __grid_constant__ GemmArgs args) {
+  const int M = args.M, N = args.N, K = args.K, ldc = args.ldc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* tiles_a = base;
+  uint8_t* tiles_b = base + kStages * kStageA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + kData);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int kblocks = (K + kBK - 1) / kBK;
+  const int n_tiles = (N + kBN - 1) / kBN;
+  const int per_problem = ((M + 2 * kBM - 1) / (2 * kBM)) * n_tiles;
+  const int tiles = per_problem * args.count;
+  const int cluster = blockIdx.x / 2, clusters = gridDim.x / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int g = 0; g < args.count; ++g) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.a[g])) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.b[g])) : "memory");
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();  // barriers initialised in both CTAs before any remote use
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full_leader0 = map_to_rank(smem_addr(&full[0]), 0);
+      int it = 0;
+      for (int t = cluster; t < tiles; t += clusters) {
+        const int g = t / per_problem, lt = t % per_problem;
+        const int m0 = (lt / n_tiles) * 2 * kBM + static_cast<int>(rank) * kBM;
+        const int n0 = (lt % n_tiles) * kBN + static_cast<int>(rank) * (kBN / 2);
+        const CUtensorMap* map_a = &args.a[g];
+        const CUtensorMap* map_b = &args.b[g];
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % kStages;
+          const uint32_t phase = (it / kStages) & 1;
+          mbar_wait(&empty[s], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[s], 2 * (kStageA + kStageB));
+          tma_load_2d_pair(tiles_a + s * kStageA, map_a, &full[s], kb * kBK, m0);
+          if constexpr (kBMN) {
+#pragma unroll
+            for (int j = 0; j < (kBN / 2) / 64; ++j)
+              tma_load_2d_pair(tiles_b + s * kStageB + j * 8192, map_b, &full[s], n0 + j * 64,
+                               kb * kBK);
+          } else {
+            tma_load_2d_pair(tiles_b + s * kStageB, map_b, &full[s], kb * kBK, n0);
+          }
+          if (!leader) remote_arrive(full_leader0 + s * 8);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = instr_desc_pair<kBMN>();
+      int it = 0, local = 0;
+      for (int t = cluster; t < tiles; t += clusters, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + uint32_t(acc * kBN);
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = smem_desc(tiles_a + s * kStageA);
+          const uint64_t db = kBMN ? smem_desc_mn(tiles_b + s * kStageB)
+                                   : smem_desc(tiles_b + s * kStageB);
+          constexpr uint64_t kAdvB = kBMN ? (16 * 128) >> 4 : 2;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_pair(d, da + uint64_t(2 * k), db + kAdvB * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          commit_pair(&empty[s]);
+        }
+        commit_pair(&acc_full[acc]);
+      }
+    }
+  } else {
+    const int quarter = warp % 4;
+    const uint32_t acc_empty_leader = map_to_rank(smem_addr(&acc_empty[0]), 0);
+    int local = 0;
+    for (int t = cluster; t < tiles; t += clusters, ++local) {
+      const int acc = local & 1;
+      const int g = t / per_problem, lt = t % per_problem;
+      const int m0 = (lt / n_tiles) * 2 * kBM + static_cast<int>(rank) * kBM;
+      const int n0 = (lt % n_tiles) * kBN;
+      void* const out = args.c[g];
+      const int row = m0 + quarter * 32 + lane;
+      mbar_wait(&acc_full[acc], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN);
+#pragma unroll 1
+      for (int c = 0; c < kBN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(lane_addr + uint32_t(c), r);
+        store_chunk<kGelu, kOutF32>(out, ldc, M, N, row, n0 + c, r);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) remote_arrive(acc_empty_leader + acc * 8);
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();  // peer done with our barriers / TMEM before teardown
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+}  // namespace pair
 
 // ---- host side ---------------------------------------------------------------
 
@@ -418,19 +653,69 @@ cudaError_t dispatch(const GemmArgs& args, bool out_f32, bool gelu, cudaStream_t
                  : launch_gemm<BN, false, false, BMN>(args, stream);
 }
 
+// 2-CTA pair kernel launch (cluster dims are compiled into the kernel).
+template <bool G, bool F, bool BMN>
+cudaError_t launch_pair(const GemmArgs& args, cudaStream_t stream) {
+  auto kernel = pair::gemm_bf16_tcgen05_pair<G, F, BMN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         pair::kBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  static int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  const int tiles = ((args.N + pair::kBN - 1) / pair::kBN) *
+                    ((args.M + 2 * pair::kBM - 1) / (2 * pair::kBM)) * args.count;
+  const int clusters = std::min(tiles, sms / 2);
+  kernel<<<2 * clusters, kThreads, pair::kBytes, stream>>>(args);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <bool BMN>
+cudaError_t dispatch_pair(const GemmArgs& args, bool out_f32, bool gelu, cudaStream_t stream) {
+  if (gelu)
+    return out_f32 ? launch_pair<true, true, BMN>(args, stream)
+                   : launch_pair<true, false, BMN>(args, stream);
+  return out_f32 ? launch_pair<false, true, BMN>(args, stream)
+                 : launch_pair<false, false, BMN>(args, stream);
+}
+
+// CTA-pair kernel for problems big enough to fill 256 x 256 tiles;
+// APL_GEMM_PAIR=0/1 forces the choice.
+bool use_pair(int M, int N) {
+  static const int forced = [] {
+    const char* e = std::getenv("APL_GEMM_PAIR");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (forced >= 0) return forced == 1;
+  return M >= 256 && N >= 256;
+}
+
 }  // namespace
 
 // count equally shaped problems C_i[M,N] = A_i[M,K] . B_i, B_i given as Bt
 // [N,K] (b_kn = false, nn.Linear layout) or as row-major [K,N] (b_kn = true);
 // bf16 in, fp32 accumulate. out_f32 selects the output type; gelu applies
 // exact-erf GELU in the epilogue. All problems share one persistent launch
-// (chunks of kMaxBatch).
+// (chunks of kMaxBatch): the CTA-pair kernel (M=256 x N=256 tiles) for
+// large problems, the single-CTA kernel (128 x BN) otherwise.
 cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,
                               int count, int M, int N, int K, int lda, int ldb, int ldc,
                               bool b_kn, bool out_f32, bool gelu, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || count <= 0) return cudaSuccess;
   if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;  // TMA row alignment
+  const bool paired = use_pair(M, N);
   const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
+  // B box rows for the K-major layout: the pair kernel stages half of its
+  // 256-wide N tile per CTA.
+  const int b_rows = paired ? pair::kBN / 2 : bn;
   for (int first = 0; first < count; first += kMaxBatch) {
     GemmArgs args;
     std::memset(&args, 0, sizeof(args));
@@ -446,12 +731,15 @@ cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* 
         return cudaErrorInvalidValue;
       if (!make_map(&args.a[i], a, M, K, lda, kBM)) return cudaErrorInvalidValue;
       const bool ok = b_kn ? make_map(&args.b[i], b, K, N, ldb, kBK, 64)
-                           : make_map(&args.b[i], b, N, K, ldb, bn);
+                           : make_map(&args.b[i], b, N, K, ldb, b_rows);
       if (!ok) return cudaErrorInvalidValue;
       args.c[i] = C[first + i];
     }
     cudaError_t e;
-    if (b_kn)
+    if (paired)
+      e = b_kn ? dispatch_pair<true>(args, out_f32, gelu, stream)
+               : dispatch_pair<false>(args, out_f32, gelu, stream);
+    else if (b_kn)
       e = bn == 256 ? dispatch<256, true>(args, out_f32, gelu, stream)
                     : dispatch<128, true>(args, out_f32, gelu, stream);
     else
