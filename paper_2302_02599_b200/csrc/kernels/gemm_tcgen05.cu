@@ -40,7 +40,8 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle row of bf16
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;  // 2 per TMEM lane quarter, each taking half the columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&acc_empty[a], kEpiWarps);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int g = 0; g < args.count; ++g) {
@@ -326,7 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // Epilogue warps 2..5 -> TMEM lane quarter (warp % 4).
-    const int quarter = warp % 4;
+    const int quarter = warp % 4;          // TMEM lanes this warp may access
+    const int half = (warp - 2) / 4;       // which half of the tile's columns
     int local = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
         uint32_t r[16];
         tmem_ld16(lane_addr + uint32_t(c), r);
         const int col = n0 + c;
@@ -477,7 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 8);
+      mbar_init(&acc_empty[a], 2 * kEpiWarps);  // epilogue warps of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int g = 0; g < args.count; ++g) {
@@ -551,6 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp % 4;
+    const int half = (warp - 2) / 4;
     const uint32_t acc_empty_leader = map_to_rank(smem_addr(&acc_empty[0]), 0);
     int local = 0;
     for (int t = cluster; t < tiles; t += clusters, ++local) {
@@ -564,7 +567,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN);
 #pragma unroll 1
-      for (int c = 0; c < kBN; c += 16) {
+      for (int c = half * (kBN / 2); c < (half + 1) * (kBN / 2); c += 16) {
         uint32_t r[16];
         tmem_ld16(lane_addr + uint32_t(c), r);
         store_chunk<kGelu, kOutF32>(out, ldc, M, N, row, n0 + c, r);
@@ -689,13 +692,17 @@ cudaError_t dispatch_pair(const GemmArgs& args, bool out_f32, bool gelu, cudaStr
 
 // CTA-pair kernel for problems big enough to fill 256 x 256 tiles;
 // APL_GEMM_PAIR=0/1 forces the choice.
-bool use_pair(int M, int N) {
+bool use_pair(int M, int N, int count) {
   static const int forced = [] {
     const char* e = std::getenv("APL_GEMM_PAIR");
     return e ? std::atoi(e) : -1;
   }();
   if (forced >= 0) return forced == 1;
-  return M >= 256 && N >= 256;
+  // r01 gemm_bench: pairs win once there are at least ~half an SM-count of
+  // 256 x 256 tiles (fc1 1331 vs 1145 TFLOP/s); with fewer the single-CTA
+  // 128 x 256 tiles fill the machine better (fc2 split-m/8: 673 vs 626).
+  const int pair_tiles = ((M + 255) / 256) * ((N + 255) / 256) * count;
+  return M >= 256 && N >= 256 && pair_tiles >= 72;
 }
 
 }  // namespace
@@ -711,7 +718,7 @@ cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* 
                               bool b_kn, bool out_f32, bool gelu, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || count <= 0) return cudaSuccess;
   if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;  // TMA row alignment
-  const bool paired = use_pair(M, N);
+  const bool paired = use_pair(M, N, std::min(count, kMaxBatch));
   const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
   // B box rows for the K-major layout: the pair kernel stages half of its
   // 256-wide N tile per CTA.
