@@ -213,11 +213,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // shares one persistent launch: tiles of all problems form one work list,
 // so small per-device GEMMs do not each pay a partial last wave.
 constexpr int kMaxBatch = 8;
+//
+// Fused reduction (simulated-mesh partial sums): output problem g sums
+// `reduce` inputs (maps a/b[g*reduce + r]) into one TMEM accumulator — the
+// k-loop simply runs over every input's K blocks — and the epilogue writes
+// the finished tile to `fan` outputs (c[g*fan + j]). With reduce = fan =
+// group size this is the split-k GEMM and its all-reduce in one kernel:
+// no partial buffers, no reduction pass, every replica bit-identical.
 struct GemmArgs {
   CUtensorMap a[kMaxBatch];
   CUtensorMap b[kMaxBatch];
   void* c[kMaxBatch];
   int count, M, N, K, ldc;
+  int reduce, fan;
 };
 
 template <int BN, bool kGelu, bool kOutF32, bool kBMN>
@@ -253,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_empty[a], kEpiWarps);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int g = 0; g < args.count; ++g) {
+    for (int g = 0; g < args.count * args.reduce; ++g) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.a[g])) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.b[g])) : "memory");
     }
@@ -275,9 +283,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int g = t / per_problem, lt = t % per_problem;
         const int m0 = (lt / n_tiles) * kBM, n0 = (lt % n_tiles) * BN;
-        const CUtensorMap* map_a = &args.a[g];
-        const CUtensorMap* map_b = &args.b[g];
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        for (int kk = 0; kk < kblocks * args.reduce; ++kk, ++it) {
+          const int kb = kk % kblocks;
+          const CUtensorMap* map_a = &args.a[g * args.reduce + kk / kblocks];
+          const CUtensorMap* map_b = &args.b[g * args.reduce + kk / kblocks];
           const int s = it % S::kStages;
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + uint32_t(acc * BN);
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        for (int kk = 0; kk < kblocks * args.reduce; ++kk, ++it) {
           const int s = it % S::kStages;
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&full[s], phase);
@@ -318,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             mma_bf16(d, da + uint64_t(2 * k), db + kAdvB * k, idesc,
-                     (kb > 0 || k > 0) ? 1u : 0u);
+                     (kk > 0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
         }
@@ -334,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = local & 1;
       const int g = t / per_problem, lt = t % per_problem;
       const int m0 = (lt / n_tiles) * kBM, n0 = (lt % n_tiles) * BN;
-      void* const out = args.c[g];
+      void* const* const outs = args.c + g * args.fan;
       const int row = m0 + quarter * 32 + lane;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -344,7 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[16];
         tmem_ld16(lane_addr + uint32_t(c), r);
         const int col = n0 + c;
-        store_chunk<kGelu, kOutF32>(out, ldc, M, N, row, col, r);
+        for (int j = 0; j < args.fan; ++j)
+          store_chunk<kGelu, kOutF32>(outs[j], ldc, M, N, row, col, r);
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -482,7 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&acc_empty[a], 2 * kEpiWarps);  // epilogue warps of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int g = 0; g < args.count; ++g) {
+    for (int g = 0; g < args.count * args.reduce; ++g) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.a[g])) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.b[g])) : "memory");
     }
@@ -506,9 +516,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int g = t / per_problem, lt = t % per_problem;
         const int m0 = (lt / n_tiles) * 2 * kBM + static_cast<int>(rank) * kBM;
         const int n0 = (lt % n_tiles) * kBN + static_cast<int>(rank) * (kBN / 2);
-        const CUtensorMap* map_a = &args.a[g];
-        const CUtensorMap* map_b = &args.b[g];
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        for (int kk = 0; kk < kblocks * args.reduce; ++kk, ++it) {
+          const int kb = kk % kblocks;
+          const CUtensorMap* map_a = &args.a[g * args.reduce + kk / kblocks];
+          const CUtensorMap* map_b = &args.b[g * args.reduce + kk / kblocks];
           const int s = it % kStages;
           const uint32_t phase = (it / kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
@@ -535,7 +546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + uint32_t(acc * kBN);
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        for (int kk = 0; kk < kblocks * args.reduce; ++kk, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -545,7 +556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           constexpr uint64_t kAdvB = kBMN ? (16 * 128) >> 4 : 2;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            mma_pair(d, da + uint64_t(2 * k), db + kAdvB * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            mma_pair(d, da + uint64_t(2 * k), db + kAdvB * k, idesc, (kk > 0 || k > 0) ? 1u : 0u);
           commit_pair(&empty[s]);
         }
         commit_pair(&acc_full[acc]);
@@ -561,7 +572,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int g = t / per_problem, lt = t % per_problem;
       const int m0 = (lt / n_tiles) * 2 * kBM + static_cast<int>(rank) * kBM;
       const int n0 = (lt % n_tiles) * kBN;
-      void* const out = args.c[g];
+      void* const* const outs = args.c + g * args.fan;
       const int row = m0 + quarter * 32 + lane;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -570,7 +581,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int c = half * (kBN / 2); c < (half + 1) * (kBN / 2); c += 16) {
         uint32_t r[16];
         tmem_ld16(lane_addr + uint32_t(c), r);
-        store_chunk<kGelu, kOutF32>(out, ldc, M, N, row, n0 + c, r);
+        for (int j = 0; j < args.fan; ++j)
+          store_chunk<kGelu, kOutF32>(outs[j], ldc, M, N, row, n0 + c, r);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -713,35 +725,40 @@ bool use_pair(int M, int N, int count) {
 // exact-erf GELU in the epilogue. All problems share one persistent launch
 // (chunks of kMaxBatch): the CTA-pair kernel (M=256 x N=256 tiles) for
 // large problems, the single-CTA kernel (128 x BN) otherwise.
-cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,
-                              int count, int M, int N, int K, int lda, int ldb, int ldc,
-                              bool b_kn, bool out_f32, bool gelu, cudaStream_t stream) {
-  if (M <= 0 || N <= 0 || K <= 0 || count <= 0) return cudaSuccess;
+cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* const* C,
+                              int groups, int reduce, int fan, int M, int N, int K, int lda,
+                              int ldb, int ldc, bool b_kn, bool out_f32, bool gelu,
+                              cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || groups <= 0) return cudaSuccess;
+  if (reduce < 1 || fan < 1 || reduce > kMaxBatch || fan > kMaxBatch) return cudaErrorInvalidValue;
   if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;  // TMA row alignment
-  const bool paired = use_pair(M, N, std::min(count, kMaxBatch));
+  const int per_launch = std::max(1, std::min(kMaxBatch / reduce, kMaxBatch / fan));
+  const bool paired = use_pair(M, N, std::min(groups, per_launch));
   const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
   // B box rows for the K-major layout: the pair kernel stages half of its
   // 256-wide N tile per CTA.
   const int b_rows = paired ? pair::kBN / 2 : bn;
-  for (int first = 0; first < count; first += kMaxBatch) {
+  for (int first = 0; first < groups; first += per_launch) {
     GemmArgs args;
     std::memset(&args, 0, sizeof(args));
-    args.count = std::min(kMaxBatch, count - first);
+    args.count = std::min(per_launch, groups - first);
+    args.reduce = reduce;
+    args.fan = fan;
     args.M = M;
     args.N = N;
     args.K = K;
     args.ldc = ldc;
-    for (int i = 0; i < args.count; ++i) {
-      const void* a = A[first + i];
-      const void* b = B[first + i];
+    for (int i = 0; i < args.count * reduce; ++i) {
+      const void* a = A[first * reduce + i];
+      const void* b = B[first * reduce + i];
       if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
         return cudaErrorInvalidValue;
       if (!make_map(&args.a[i], a, M, K, lda, kBM)) return cudaErrorInvalidValue;
       const bool ok = b_kn ? make_map(&args.b[i], b, K, N, ldb, kBK, 64)
                            : make_map(&args.b[i], b, N, K, ldb, b_rows);
       if (!ok) return cudaErrorInvalidValue;
-      args.c[i] = C[first + i];
     }
+    for (int i = 0; i < args.count * fan; ++i) args.c[i] = C[first * fan + i];
     cudaError_t e;
     if (paired)
       e = b_kn ? dispatch_pair<true>(args, out_f32, gelu, stream)
@@ -755,6 +772,13 @@ cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* 
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,
+                              int count, int M, int N, int K, int lda, int ldb, int ldc,
+                              bool b_kn, bool out_f32, bool gelu, cudaStream_t stream) {
+  return gemm_bf16_grouped(A, B, C, count, 1, 1, M, N, K, lda, ldb, ldc, b_kn, out_f32, gelu,
+                           stream);
 }
 
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,

@@ -54,9 +54,40 @@ void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorM
     throw RuntimeError(APL_ERR_SHAPE, "local shards do not form a matmul");
   if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
     throw RuntimeError(APL_ERR_ARG, "local GEMM extents exceed int32");
-  const bool fuse_gelu = epilogue == APL_EPI_GELU && !s.partial_sum;
   const int nl = mesh.num_local();
   const int eb_c = out_dtype == APL_F32 ? 4 : 2;
+  // Simulated mesh + partial sums: the GEMM and its all-reduce are ONE
+  // kernel — each reduction group's tile accumulates every member's K slice
+  // in TMEM (fp32, member order) and the epilogue writes the finished tile
+  // (GELU applied to the full sum) to every member. APL_FUSED_AR=0 keeps the
+  // two-pass form (GEMM writes partials, reduce_groups sums them).
+  static const bool fused_ar_enabled = [] {
+    const char* e = std::getenv("APL_FUSED_AR");
+    return e == nullptr || std::string(e) != "0";
+  }();
+  if (s.partial_sum && !mesh.distributed && batch == 1 && fused_ar_enabled) {
+    const auto groups = axis_groups(geo, s.reduce_axes);
+    const int gsize = static_cast<int>(groups[0].size());
+    if (gsize <= 8) {
+      std::vector<const void*> pa, pb;
+      std::vector<void*> pc;
+      for (const auto& g : groups)
+        for (int d : g) {
+          pa.push_back(A[d]);
+          pb.push_back(B[d]);
+          pc.push_back(C[d]);
+        }
+      check_cuda(gemm_bf16_grouped(pa.data(), pb.data(), pc.data(),
+                                   static_cast<int>(groups.size()), gsize, gsize,
+                                   static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+                                   static_cast<int>(k), static_cast<int>(b_kn ? n : k),
+                                   static_cast<int>(n), b_kn, out_dtype == APL_F32,
+                                   epilogue == APL_EPI_GELU, stream),
+                 "fused GEMM + all-reduce launch");
+      return;
+    }
+  }
+  const bool fuse_gelu = epilogue == APL_EPI_GELU && !s.partial_sum;
   // Every local device (and every batch element) has the same shard shapes:
   // all problems go through the persistent batched launcher together (a
   // simulated mesh runs its 8 GEMMs as one launch).

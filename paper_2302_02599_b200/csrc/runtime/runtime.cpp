@@ -547,27 +547,33 @@ void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, siz
                "ncclAllReduce");
     return;
   }
-  // Groups: devices sharing every coordinate off `axes`, members ordered by
-  // their mixed-radix coordinate on `axes`.
-  const int64_t p = mesh.geo.num_devices();
-  int64_t gsize = 1;
-  for (int a = 0; a < mesh.geo.rank(); ++a)
-    if (mask & (1u << a)) gsize *= mesh.geo.shape[static_cast<size_t>(a)];
-  const int64_t ngroups = p / gsize;
+  const auto groups = axis_groups(mesh.geo, axes);
   std::vector<int> members;
-  std::vector<std::vector<int>> by_group(static_cast<size_t>(ngroups));
-  std::map<int64_t, int> group_id;
-  for (int64_t d = 0; d < p; ++d) {
-    const auto c = mesh.geo.coord_of(d);
-    int64_t off = 0;
-    for (int a = 0; a < mesh.geo.rank(); ++a)
-      if (!(mask & (1u << a))) off = off * mesh.geo.shape[static_cast<size_t>(a)] + c[static_cast<size_t>(a)];
-    by_group[static_cast<size_t>(off)].push_back(static_cast<int>(d));  // row-major => on-axes order
-  }
-  for (auto& g : by_group) members.insert(members.end(), g.begin(), g.end());
-  check_cuda(launch_allreduce_local(bufs, members.data(), static_cast<int>(ngroups),
-                                    static_cast<int>(gsize), count, dtype, stream),
+  for (const auto& g : groups) members.insert(members.end(), g.begin(), g.end());
+  check_cuda(launch_allreduce_local(bufs, members.data(), static_cast<int>(groups.size()),
+                                    static_cast<int>(groups[0].size()), count, dtype, stream),
              "all-reduce launch");
+}
+
+std::vector<std::vector<int>> axis_groups(const autoplan::DeviceMesh& geo,
+                                          const std::vector<int>& axes) {
+  // Devices sharing every coordinate off `axes`; members ordered by their
+  // mixed-radix coordinate on `axes` (row-major order preserves it).
+  uint32_t mask = 0;
+  for (int a : axes) mask |= 1u << a;
+  const int64_t p = geo.num_devices();
+  int64_t gsize = 1;
+  for (int a = 0; a < geo.rank(); ++a)
+    if (mask & (1u << a)) gsize *= geo.shape[static_cast<size_t>(a)];
+  std::vector<std::vector<int>> groups(static_cast<size_t>(p / gsize));
+  for (int64_t d = 0; d < p; ++d) {
+    const auto c = geo.coord_of(d);
+    int64_t off = 0;
+    for (int a = 0; a < geo.rank(); ++a)
+      if (!(mask & (1u << a))) off = off * geo.shape[static_cast<size_t>(a)] + c[static_cast<size_t>(a)];
+    groups[static_cast<size_t>(off)].push_back(static_cast<int>(d));
+  }
+  return groups;
 }
 
 }  // namespace apl

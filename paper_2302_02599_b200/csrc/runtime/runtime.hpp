@@ -166,6 +166,15 @@ void run_path(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::Sha
 void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, size_t count,
                 int dtype, cudaStream_t stream);
 
+// Axis groups of `axes` (reduction groups), members in mixed-radix order.
+std::vector<std::vector<int>> axis_groups(const autoplan::DeviceMesh& geo,
+                                          const std::vector<int>& axes);
+
+cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* const* C,
+                              int groups, int reduce, int fan, int M, int N, int K, int lda,
+                              int ldb, int ldc, bool b_kn, bool out_f32, bool gelu,
+                              cudaStream_t stream);
+
 // B shards are row-major [k_local, n_local] when b_kn, else transposed
 // [n_local, k_local] (nn.Linear layout).
 void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorMeta& a_meta,
