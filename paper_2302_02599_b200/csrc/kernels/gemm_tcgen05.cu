@@ -9,16 +9,21 @@
 // its shards; the strategy's layout conversions and partial-sum all-reduce
 // run around it in the runtime.
 //
-// Kernel shape (one CTA per 128 x BN output tile, 6 warps, warp-specialized):
-//   warp 0       TMA producer: 64-wide K slabs of A (128 rows) and Bt (BN
-//                rows) into a kStages-deep smem ring, 128B swizzle,
-//                mbarrier complete_tx;
-//   warp 1       owns the TMEM allocation; lane 0 issues tcgen05.mma
-//                (M=128, N=BN, K=16 per instruction, cta_group::1) and
-//                tcgen05.commit's each ring slot back to the producer;
-//   warps 2..5   epilogue: tcgen05.ld 32x32b.x16 from TMEM (warp w reads
-//                lanes 32*(w%4)..+31), GELU / convert, 16-column stores.
-// Tails in M, N and K are handled by TMA zero fill plus masked stores.
+// Two persistent, warp-specialized kernels (10 warps each):
+//   warp 0       TMA producer: 64-wide K slabs of A and B into a kStages-
+//                deep smem ring, 128B swizzle, mbarrier complete_tx;
+//   warp 1       owns the TMEM allocation (2 accumulators, so the epilogue
+//                of tile i overlaps the MMAs of tile i+1); lane 0 issues
+//                tcgen05.mma and tcgen05.commit's each ring slot back;
+//   warps 2..9   epilogue: tcgen05.ld 32x32b.x16 from TMEM (warp w reads
+//                lanes 32*(w%4)..+31, half the columns each), GELU /
+//                convert, 16-column stores.
+// gemm_bf16_tcgen05       cta_group::1, 128 x BN tiles (BN 128 / 256);
+// gemm_bf16_tcgen05_pair  cta_group::2 on a 2-CTA cluster, 256 x 256 tiles
+//                         (each SM stages half of B: less smem fill per MMA).
+// Both take a batch of problems in one launch and can fuse a reduction
+// across problems (GemmArgs.reduce / .fan). Tails in M, N and K are handled
+// by TMA zero fill plus masked stores.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
