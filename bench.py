@@ -268,8 +268,8 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    result["e2e"] = run_e2e(args, mesh, meta, convs, stream, ws)
     if ws == 1:
-        result["e2e"] = run_e2e(args, mesh, meta, convs, stream)
         result["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
         print(json.dumps(result))
@@ -297,7 +297,7 @@ def _distinct_shards(spec, geo, meta):
     return keep
 
 
-def run_e2e(args, mesh, meta, convs, stream):
+def run_e2e(args, mesh, meta, convs, stream, ws=1):
     """Same metric through the public API with HOST buffers. Every step:
     pinned H2D of the step's input shards, the conversions (prepared
     conversions, the public API), D2H of the converted result (each distinct
@@ -321,7 +321,10 @@ def run_e2e(args, mesh, meta, convs, stream):
     keep = []
     for c in convs:
         a, b = c["name"].split("->")
-        keep.append(_distinct_shards(ShardingSpec.parse(b, mesh.geo.rank()), mesh.geo, meta))
+        if mesh.distributed:  # every rank reads back its own converted shard
+            keep.append([0])
+        else:
+            keep.append(_distinct_shards(ShardingSpec.parse(b, mesh.geo.rank()), mesh.geo, meta))
     host_out = [[torch.empty_like(c["outs"][d], device="cpu").pin_memory() for d in k]
                 for c, k in zip(convs, keep)]
     h2d = sum(x.numel() * x.element_size() for hi in host_in for x in hi)
@@ -365,7 +368,15 @@ def run_e2e(args, mesh, meta, convs, stream):
     z.record(s_out)
     torch.cuda.synchronize()
     ms = a.elapsed_time(z) / steps
-    step_bytes = sum(c["hbm"] for c in convs)
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=f"cuda:{mesh.device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        step_bytes = sum(c["bus"] for c in convs) * ws  # same metric as `value`
+    else:
+        step_bytes = sum(c["hbm"] for c in convs)
     return {"value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3),
             "steps": steps,
