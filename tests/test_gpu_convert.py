@@ -123,6 +123,28 @@ def test_edge_shapes_and_unaligned_runs(cuda):
             check_conversion(mesh, shape, eb, a, b, fuse)
 
 
+def test_random_meshes_shapes_and_specs(cuda):
+    """300 random conversions: mesh rank 1-3 (non-power-of-two extents
+    included), tensor rank 1-4, dtype 1/2/4/8 bytes, random valid specs,
+    stepwise and collapsed, bytewise vs the oracle."""
+    from test_layout_api import all_valid_specs
+
+    rng = random.Random(20230205)
+    meshes = [[2], [3], [4], [8], [2, 2], [2, 3], [3, 2], [2, 4], [4, 2], [2, 2, 2], [1, 4]]
+    done = 0
+    while done < 300:
+        mesh_shape = rng.choice(meshes)
+        rank = rng.choice([1, 2, 3, 4])
+        shape = tuple(rng.choice([2, 4, 6, 8, 12, 16, 24]) for _ in range(rank))
+        eb = rng.choice([1, 2, 4, 8])
+        specs = all_valid_specs(TensorMeta(shape, eb), DeviceMesh.uniform(mesh_shape))
+        if len(specs) < 2:
+            continue
+        a, b = rng.choice(specs), rng.choice(specs)
+        check_conversion(mesh_shape, shape, eb, str(a), str(b), rng.random() < 0.5)
+        done += 1
+
+
 def test_run_step_for_each_kind(cuda):
     mesh = Mesh.local([2, 4])
     meta = TensorMeta((64, 96), 4)
