@@ -633,6 +633,13 @@ int apl_exchange_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_sp
         for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.src_stride[d]);
         j += "],\"dst_stride\":[";
         for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.dst_stride[d]);
+        j += "],\"ksplit\":" + std::to_string(c.ksplit) +
+             ",\"split_src_step\":" + std::to_string(c.split_src_step) + ",\"split_dst\":[";
+        for (int d = 0; d < c.ksplit && c.ksplit > 1; ++d)
+          j += (d ? "," : "") + std::to_string(c.split_dst[d]);
+        j += "],\"split_dst_off\":[";
+        for (int d = 0; d < c.ksplit && c.ksplit > 1; ++d)
+          j += (d ? "," : "") + std::to_string(c.split_dst_off[d]);
         j += "]}";
       }
       j += "],";

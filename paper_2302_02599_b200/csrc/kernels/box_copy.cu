@@ -76,14 +76,25 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
   return f.div == 1 ? n : (__umulhi(n, f.mul) >> f.shr);
 }
 
-// Generic resolution straight from a (global or shared) descriptor.
-template <int V>
-__device__ __forceinline__ void resolve(const DevCopy& c, uint32_t local, int64_t& so,
-                                        int64_t& dd) {
+// Generic resolution straight from a (global or shared) descriptor: source
+// offset and destination offset relative to the descriptor's first
+// destination buffer (a split unit's chunk lands in its own buffer, folded
+// in as the difference of the two base addresses).
+template <int V, bool SPLIT>
+__device__ __forceinline__ void resolve(const DevCopy& c, uint32_t local, const PtrTable& ptrs,
+                                        int64_t& so, int64_t& dd) {
   uint32_t row = fdiv(local, c.units_per_run);
-  const uint32_t col = local - row * c.units_per_run.div;
-  so = c.src_off + static_cast<int64_t>(col) * V;
-  dd = c.dst_off + static_cast<int64_t>(col) * V;
+  uint32_t col = local - row * c.units_per_run.div;
+  if (SPLIT && c.ksplit > 1) {
+    const uint32_t j = fdiv(col, c.split_div);
+    col -= j * c.split_div.div;
+    so = c.src_off + static_cast<int64_t>(j) * c.split_src_step + static_cast<int64_t>(col) * V;
+    dd = c.dst_offs[j] + (ptrs.dst[c.dst_bufs[j]] - ptrs.dst[c.dst_bufs[0]]) +
+         static_cast<int64_t>(col) * V;
+  } else {
+    so = c.src_off + static_cast<int64_t>(col) * V;
+    dd = c.dst_off + static_cast<int64_t>(col) * V;
+  }
   for (int i = c.nouter - 1; i >= 0; --i) {
     const uint32_t q = fdiv(row, c.ext[i]);
     const uint32_t r = row - q * c.ext[i].div;
@@ -93,7 +104,7 @@ __device__ __forceinline__ void resolve(const DevCopy& c, uint32_t local, int64_
   }
 }
 
-template <int V, int U, int NO, int MINB>
+template <int V, int U, int NO, int MINB, bool SPLIT>
 __global__ void __launch_bounds__(256, MINB)
     box_copy_kernel(const DevCopy* __restrict__ table, int ntasks, int64_t total,
                     const __grid_constant__ PtrTable ptrs) {
@@ -132,6 +143,9 @@ __global__ void __launch_bounds__(256, MINB)
     const int64_t soff = s_desc.src_off, doff = s_desc.dst_off;
     const int nout = s_desc.nouter;
     const int ndst = s_desc.ndst;
+    const int ks = s_desc.ksplit;  // uniform per chunk
+    const FastDiv sdiv = s_desc.split_div;
+    const int64_t sstep = s_desc.split_src_step;
     FastDiv ext[NR];
     int64_t sst[NR], dst_[NR];
 #pragma unroll
@@ -146,7 +160,7 @@ __global__ void __launch_bounds__(256, MINB)
     std::memcpy(dbuf, s_desc.dst_bufs, sizeof(dbuf));
 
     T v[U];
-    int64_t dd[U];
+    int64_t dd[U];  // offset from the first destination buffer's base
     int slow_task[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -157,9 +171,18 @@ __global__ void __launch_bounds__(256, MINB)
         const char* sp;
         if (g < next_begin) {
           uint32_t row = fdiv(static_cast<uint32_t>(g - begin), upr);
-          const uint32_t col = static_cast<uint32_t>(g - begin) - row * upr.div;
-          so = soff + static_cast<int64_t>(col) * V;
-          dd[u] = doff + static_cast<int64_t>(col) * V;
+          uint32_t col = static_cast<uint32_t>(g - begin) - row * upr.div;
+          if (SPLIT && ks > 1) {
+            const uint32_t j = fdiv(col, sdiv);
+            col -= j * sdiv.div;
+            so = soff + static_cast<int64_t>(j) * sstep + static_cast<int64_t>(col) * V;
+            dd[u] = s_desc.dst_offs[j] +
+                    (ptrs.dst[s_desc.dst_bufs[j]] - ptrs.dst[s_desc.dst_bufs[0]]) +
+                    static_cast<int64_t>(col) * V;
+          } else {
+            so = soff + static_cast<int64_t>(col) * V;
+            dd[u] = doff + static_cast<int64_t>(col) * V;
+          }
           if constexpr (NO > 0) {
 #pragma unroll
             for (int i = NO - 1; i >= 0; --i) {
@@ -178,7 +201,7 @@ __global__ void __launch_bounds__(256, MINB)
           int t = t0 + 1;
           while (t + 1 < ntasks && table[t + 1].unit_begin <= g) ++t;
           const DevCopy& c = table[t];
-          resolve<V>(c, static_cast<uint32_t>(g - c.unit_begin), so, dd[u]);
+          resolve<V, SPLIT>(c, static_cast<uint32_t>(g - c.unit_begin), ptrs, so, dd[u]);
           sp = ptrs.src[c.src_buf];
           slow_task[u] = t;
         }
@@ -188,6 +211,7 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (slow_task[u] == -1) {
+        // split descriptors have ndst == 1 (their chunks are folded into dd)
 #pragma unroll
         for (int j = 0; j < kCopyMaxFan; ++j)
           if (j < ndst)
@@ -228,7 +252,7 @@ int copy_variant(int max_outer, int max_fan) {
   return 3;
 }
 
-template <int V, int U, int MINB>
+template <int V, int U, int MINB, bool SPLIT = false>
 void launch_vu(int no, int64_t total, const DevCopy* t, int n, const PtrTable& p,
                cudaStream_t s) {
   constexpr int kThreads = 256;
@@ -239,26 +263,29 @@ void launch_vu(int no, int64_t total, const DevCopy* t, int n, const PtrTable& p
       static_cast<int>(std::min<int64_t>(chunks, static_cast<int64_t>(sm_count()) * ctas_per_sm));
   switch (no) {
     case 0:
-      box_copy_kernel<V, U, 0, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      box_copy_kernel<V, U, 0, MINB, SPLIT><<<grid, kThreads, 0, s>>>(t, n, total, p);
       break;
     case 1:
-      box_copy_kernel<V, U, 1, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      box_copy_kernel<V, U, 1, MINB, SPLIT><<<grid, kThreads, 0, s>>>(t, n, total, p);
       break;
     case 2:
-      box_copy_kernel<V, U, 2, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      box_copy_kernel<V, U, 2, MINB, SPLIT><<<grid, kThreads, 0, s>>>(t, n, total, p);
       break;
     case 3:
-      box_copy_kernel<V, U, 3, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      box_copy_kernel<V, U, 3, MINB, SPLIT><<<grid, kThreads, 0, s>>>(t, n, total, p);
       break;
     default:
-      box_copy_kernel<V, U, kCopyMaxOuter, MINB><<<grid, kThreads, 0, s>>>(t, n, total, p);
+      box_copy_kernel<V, U, kCopyMaxOuter, MINB, SPLIT><<<grid, kThreads, 0, s>>>(t, n, total, p);
       break;
   }
 }
 
 template <int V>
-void launch_v(int no, int fan, int64_t total_units, const DevCopy* t, int n, const PtrTable& p,
-              cudaStream_t s) {
+void launch_v(int no, int fan, bool split, int64_t total_units, const DevCopy* t, int n,
+              const PtrTable& p, cudaStream_t s) {
+  // Split tables get their own instantiation so the chunk arithmetic does
+  // not cost the common kernels registers (U=8 @ 2 CTAs/SM: no spills).
+  if (split) return launch_vu<V, 8, 2, true>(no, total_units, t, n, p, s);
   if constexpr (V == 16) {
     switch (copy_variant(no, fan)) {
       case 1:
@@ -302,24 +329,24 @@ int sm_count() {
 }
 
 cudaError_t launch_box_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
-                            int vec_bytes, int max_outer, int max_fan, const PtrTable& ptrs,
-                            cudaStream_t stream) {
+                            int vec_bytes, int max_outer, int max_fan, bool split,
+                            const PtrTable& ptrs, cudaStream_t stream) {
   if (ntasks <= 0 || total_units <= 0) return cudaSuccess;
   switch (vec_bytes) {
     case 16:
-      launch_v<16>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<16>(max_outer, max_fan, split, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 8:
-      launch_v<8>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<8>(max_outer, max_fan, split, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 4:
-      launch_v<4>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<4>(max_outer, max_fan, split, total_units, d_table, ntasks, ptrs, stream);
       break;
     case 2:
-      launch_v<2>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<2>(max_outer, max_fan, split, total_units, d_table, ntasks, ptrs, stream);
       break;
     default:
-      launch_v<1>(max_outer, max_fan, total_units, d_table, ntasks, ptrs, stream);
+      launch_v<1>(max_outer, max_fan, split, total_units, d_table, ntasks, ptrs, stream);
       break;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);

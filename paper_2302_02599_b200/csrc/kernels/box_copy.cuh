@@ -35,8 +35,18 @@ struct DevCopy {
   FastDiv units_per_run;
   int32_t src_buf, nouter, ndst;
   uint8_t dst_bufs[kCopyMaxFan];
-  int32_t pad_;
+  int32_t ksplit;     // > 1: split descriptor (see below)
   int64_t run_bytes;  // bulk (TMA) tables: run length, units are kBulkSeg segments
+  // Split descriptor (short-run transposes): one source row holds ksplit
+  // adjacent chunks of run bytes (split_src_step apart); chunk j goes to
+  // destination buffer dst_bufs[j] at dst_offs[j]. Units enumerate
+  // (row, chunk, column) row-major, so consecutive lanes read one whole
+  // source row (ksplit * run bytes, contiguous) and every destination still
+  // receives its contiguous run — the smem-free form of a tile transpose for
+  // rows of a few bytes per receiver.
+  FastDiv split_div;  // units per chunk (the run's unit count)
+  int64_t split_src_step;
+  int64_t dst_offs[kCopyMaxFan];
 };
 
 // TMA bulk engine (bulk_copy.cu): rows of >= kBulkMinRun contiguous bytes

@@ -7,6 +7,9 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <string>
 #include <stdexcept>
 
 namespace apl {
@@ -227,6 +230,60 @@ CopyDesc make_copy(int src_buf, const std::vector<int64_t>& src_shape,
     c.dst_stride[i] = merged[i].d * elem_bytes;
   }
   return c;
+}
+
+void merge_splits(std::vector<CopyDesc>& descs) {
+  constexpr int64_t kShortRun = 64;
+  static const bool enabled = [] {
+    const char* e = std::getenv("APL_SPLIT");  // "0" disables (A/B measurements)
+    return e == nullptr || std::string(e) != "0";
+  }();
+  if (!enabled) return;
+  // Bucket candidates by everything but the source offset / destination.
+  std::map<std::vector<int64_t>, std::vector<size_t>> buckets;
+  for (size_t i = 0; i < descs.size(); ++i) {
+    const CopyDesc& d = descs[i];
+    if (d.run_bytes >= kShortRun || d.ndst != 1 || d.ksplit != 1 || d.nouter == 0) continue;
+    std::vector<int64_t> key{d.src_buf, d.run_bytes, d.nouter};
+    for (int j = 0; j < d.nouter; ++j) {
+      key.push_back(d.ext[j]);
+      key.push_back(d.src_stride[j]);
+      key.push_back(d.dst_stride[j]);
+    }
+    buckets[key].push_back(i);
+  }
+  std::vector<char> gone(descs.size(), 0);
+  std::vector<CopyDesc> merged;
+  for (auto& [key, idx] : buckets) {
+    std::sort(idx.begin(), idx.end(),
+              [&](size_t a, size_t b) { return descs[a].src_off < descs[b].src_off; });
+    size_t i = 0;
+    while (i < idx.size()) {
+      // Longest run of chunks exactly run_bytes apart, at most kMaxFan.
+      size_t j = i + 1;
+      while (j < idx.size() && j - i < static_cast<size_t>(CopyDesc::kMaxFan) &&
+             descs[idx[j]].src_off == descs[idx[j - 1]].src_off + descs[idx[i]].run_bytes)
+        ++j;
+      if (j - i >= 2) {
+        CopyDesc s = descs[idx[i]];
+        s.ksplit = static_cast<int>(j - i);
+        s.split_src_step = s.run_bytes;
+        for (size_t t = i; t < j; ++t) {
+          s.split_dst[t - i] = descs[idx[t]].dst_buf;
+          s.split_dst_off[t - i] = descs[idx[t]].dst_off;
+          gone[idx[t]] = 1;
+        }
+        merged.push_back(s);
+      }
+      i = j;
+    }
+  }
+  if (merged.empty()) return;
+  std::vector<CopyDesc> out;
+  for (size_t i = 0; i < descs.size(); ++i)
+    if (!gone[i]) out.push_back(descs[i]);
+  out.insert(out.end(), merged.begin(), merged.end());
+  descs.swap(out);
 }
 
 std::vector<int> active_axes(const ShardingSpec& src, const ShardingSpec& tgt,

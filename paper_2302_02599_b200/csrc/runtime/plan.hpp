@@ -62,14 +62,20 @@ struct CopyDesc {
   int dst_buf = 0;  // index into the launch's destination pointer table
   int ndst = 1;     // fan-out: the same bytes also land in extra_dst[0..ndst-2]
   int extra_dst[kMaxFan - 1] = {};
+  // Split form (ksplit > 1): chunk j of each source row (src_off + j *
+  // split_src_step) goes to buffer split_dst[j] at split_dst_off[j].
+  int ksplit = 1;
+  int64_t split_src_step = 0;
+  int split_dst[kMaxFan] = {};
+  int64_t split_dst_off[kMaxFan] = {};
   int64_t src_off = 0, dst_off = 0;  // bytes
   int64_t run_bytes = 0;
   int nouter = 0;
   int64_t ext[kMaxDims - 1] = {};
   int64_t src_stride[kMaxDims - 1] = {};  // bytes
   int64_t dst_stride[kMaxDims - 1] = {};  // bytes
-  int64_t bytes() const {
-    int64_t n = run_bytes;
+  int64_t bytes() const {  // bytes read (= written per destination)
+    int64_t n = run_bytes * ksplit;
     for (int i = 0; i < nouter; ++i) n *= ext[i];
     return n;
   }
@@ -81,6 +87,11 @@ CopyDesc make_copy(int src_buf, const std::vector<int64_t>& src_shape,
                    const std::vector<int64_t>& src_lo, int dst_buf,
                    const std::vector<int64_t>& dst_shape, const std::vector<int64_t>& dst_lo,
                    const std::vector<int64_t>& ext, int elem_bytes);
+
+// Merges descriptors with short runs (< 64 B) that read adjacent chunks of
+// the same source rows (same buffer, outer extents and strides, source
+// offsets run_bytes apart) into split descriptors of up to 8 chunks.
+void merge_splits(std::vector<CopyDesc>& descs);
 
 // True when the box is one contiguous run inside an array of `shape`.
 bool box_contiguous(const std::vector<int64_t>& shape, const std::vector<int64_t>& ext);

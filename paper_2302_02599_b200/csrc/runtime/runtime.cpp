@@ -47,7 +47,7 @@ struct DeviceGuard {
 // Splits descriptors whose unit count would overflow the kernel's 32-bit
 // per-descriptor index.
 void split_large(const CopyDesc& d, int vec, std::vector<CopyDesc>& out) {
-  const int64_t upr = d.run_bytes / vec;
+  const int64_t upr = d.run_bytes / vec * d.ksplit;
   int64_t rows = 1;
   for (int i = 0; i < d.nouter; ++i) rows *= d.ext[i];
   if (upr * rows <= kMaxUnitsPerDesc) {
@@ -125,6 +125,10 @@ int natural_vec(const std::vector<CopyDesc>& descs) {
       g = std::gcd(g, d.src_stride[i]);
       g = std::gcd(g, d.dst_stride[i]);
     }
+    if (d.ksplit > 1) {
+      g = std::gcd(g, d.split_src_step);
+      for (int j = 0; j < d.ksplit; ++j) g = std::gcd(g, d.split_dst_off[j]);
+    }
   }
   return pow2_vec(g);
 }
@@ -139,7 +143,8 @@ bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec) {
   bool strided = false, fan = false;
   for (const CopyDesc& d : descs) {
     if (d.bytes() == 0) continue;
-    if (d.run_bytes < (forced == 1 ? 16 : kBulkMinRun) || d.run_bytes % 16) return false;
+    if (d.run_bytes < (forced == 1 ? 16 : kBulkMinRun) || d.run_bytes % 16 || d.ksplit > 1)
+      return false;
     strided = strided || d.nouter > 0;
     fan = fan || d.ndst > 1;
   }
@@ -174,7 +179,18 @@ CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool 
     h.nouter = d.nouter;
     cc.max_outer = std::max(cc.max_outer, d.nouter);
     cc.max_fan = std::max(cc.max_fan, d.ndst);
-    const int64_t upr = bulk ? (d.run_bytes + kBulkSeg - 1) / kBulkSeg : d.run_bytes / vec;
+    int64_t upr = bulk ? (d.run_bytes + kBulkSeg - 1) / kBulkSeg : d.run_bytes / vec;
+    h.ksplit = d.ksplit;
+    cc.split = cc.split || d.ksplit > 1;
+    if (d.ksplit > 1) {  // units of one row: ksplit chunks of upr units
+      h.split_div = make_fastdiv(static_cast<uint32_t>(upr));
+      h.split_src_step = d.split_src_step;
+      for (int j = 0; j < d.ksplit; ++j) {
+        h.dst_bufs[j] = static_cast<uint8_t>(d.split_dst[j]);
+        h.dst_offs[j] = d.split_dst_off[j];
+      }
+      upr *= d.ksplit;
+    }
     h.units_per_run = make_fastdiv(static_cast<uint32_t>(upr));
     h.run_bytes = d.run_bytes;
     int64_t rows = 1;
@@ -208,7 +224,7 @@ void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stre
     check_cuda(launch_bulk_copy(c.table, c.ntasks, c.total_units, ptrs, stream), "bulk copy launch");
     return;
   }
-  check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, c.max_outer, c.max_fan, ptrs,
+  check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, c.max_outer, c.max_fan, c.split, ptrs,
                              stream),
              "box_copy launch");
 }
@@ -267,6 +283,7 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
                                             static_cast<int>(q), lt, p.dst_lo, p.ext, eb));
       }
     }
+    merge_splits(ex->host_copies);
   } else {
     const int64_t me = mesh.rank;
     // Source buffer ids: 0 = in, 1 = recv staging. Destination: 0 = out, 1 = send staging.
@@ -309,6 +326,7 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
         ex->send_staging = align_up(off + bytes);
       }
     }
+    merge_splits(ex->host_pre);
   }
   std::lock_guard<std::mutex> hold(mesh.mu);
   auto [it, fresh] = mesh.exchanges.emplace(key, ex);

@@ -30,8 +30,8 @@ void check_nccl(ncclResult_t r, const char* what);
 FastDiv make_fastdiv(uint32_t d);
 int sm_count();
 cudaError_t launch_box_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
-                            int vec_bytes, int max_outer, int max_fan, const PtrTable& ptrs,
-                            cudaStream_t stream);
+                            int vec_bytes, int max_outer, int max_fan, bool split,
+                            const PtrTable& ptrs, cudaStream_t stream);
 cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int groups,
                                    int group_size, size_t count, int dtype,
                                    cudaStream_t stream);
@@ -59,6 +59,7 @@ struct CompiledCopies {
   int vec = 16;
   int max_outer = 0;
   int max_fan = 1;
+  bool split = false;       // some descriptor has ksplit > 1
   int64_t bytes = 0;        // bytes read (each source byte once)
   int64_t write_bytes = 0;  // bytes written (fan-out counted per destination)
   bool bulk = false;        // TMA bulk engine (units = kBulkSeg segments)

@@ -31,15 +31,22 @@ def _free_port():
 
 
 def _copy(desc, srcs, dsts):
-    """Emulates one CopyDesc of the box-copy kernel on byte buffers."""
+    """Emulates one CopyDesc of the box-copy kernel on byte buffers. A split
+    descriptor (ksplit > 1) sends chunk j of every source row (src_off + j *
+    split_src_step) to buffer split_dst[j] at split_dst_off[j]."""
     ext = tuple(desc["ext"]) + (desc["run_bytes"],)
+    if desc.get("ksplit", 1) > 1:
+        chunks = [(desc["src_off"] + j * desc["split_src_step"], b, off)
+                  for j, (b, off) in enumerate(zip(desc["split_dst"], desc["split_dst_off"]))]
+    else:
+        chunks = [(desc["src_off"], desc["dst_buf"], desc["dst_off"])]
     src = srcs[desc["src_buf"]]
-    dst = dsts[desc["dst_buf"]]
-    sv = np.lib.stride_tricks.as_strided(src[desc["src_off"]:], shape=ext,
-                                         strides=tuple(desc["src_stride"]) + (1,))
-    dv = np.lib.stride_tricks.as_strided(dst[desc["dst_off"]:], shape=ext,
-                                         strides=tuple(desc["dst_stride"]) + (1,))
-    dv[...] = sv
+    for src_off, dst_buf, dst_off in chunks:
+        sv = np.lib.stride_tricks.as_strided(src[src_off:], shape=ext,
+                                             strides=tuple(desc["src_stride"]) + (1,))
+        dv = np.lib.stride_tricks.as_strided(dsts[dst_buf][dst_off:], shape=ext,
+                                             strides=tuple(desc["dst_stride"]) + (1,))
+        dv[...] = sv
 
 
 def _worker(rank, world, port, cases, q):

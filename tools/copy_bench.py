@@ -29,6 +29,9 @@ CASES = [
     ([2, 2, 2], (8192, 8192), 2, "S012R", "RS012"),  # config 4
     ([2, 2, 2], (512, 512, 256), 2, "S0S1R", "RS1S0"),
     ([2, 2, 2], (4096, 4096, 32), 2, "RS012R", "RRS012"),  # innermost-dim A2A (64 B runs)
+    ([8], (1 << 21, 64), 2, "S0R", "RS0"),     # 16 B runs per receiver (split rows)
+    ([8], (1 << 22, 32), 4, "S0R", "RS0"),     # 16 B runs, fp32
+    ([2, 4], (1 << 20, 128), 2, "S01R", "RS01"),  # 32 B runs
 ]
 
 
