@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include "box_copy.cuh"
 
@@ -30,7 +31,9 @@ namespace {
 
 constexpr int kStages = 3;
 constexpr int kStageBytes = 32 * kBulkSeg;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024;
+constexpr int kBulkSmemTasks = 64;  // descriptors per launch, staged in smem
+constexpr int kTableBytes = kBulkSmemTasks * static_cast<int>(sizeof(DevCopy));
+constexpr int kSmemBytes = kTableBytes + kStages * kStageBytes + 128;
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -55,17 +58,25 @@ struct Unit {
   uint32_t bytes;
 };
 
-// Unit u -> descriptor, source/destination byte offsets, segment length.
-__device__ __forceinline__ bool resolve_unit(const DevCopy* __restrict__ table, int ntasks,
-                                             int64_t total, int64_t u, Unit& out) {
-  if (u >= total) return false;
+__device__ __forceinline__ int find_task(const DevCopy* table, int ntasks, int64_t u) {
   int lo = 0, hi = ntasks - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (table[mid].unit_begin <= u) lo = mid;
     else hi = mid - 1;
   }
-  const DevCopy& c = table[lo];
+  return lo;
+}
+
+// Unit u -> descriptor, source/destination byte offsets, segment length.
+// `cur` is the lane's descriptor cursor: units only move forward, so only
+// the entries after it are searched.
+__device__ __forceinline__ bool resolve_unit(const DevCopy* table, int ntasks, int64_t total,
+                                             int64_t u, int& cur, Unit& out) {
+  if (u >= total) return false;
+  if (cur + 1 < ntasks && table[cur + 1].unit_begin <= u)
+    cur = cur + 1 + find_task(table + cur + 1, ntasks - cur - 1, u);
+  const DevCopy& c = table[cur];
   const uint32_t local = static_cast<uint32_t>(u - c.unit_begin);
   uint32_t row = fdiv(local, c.units_per_run);
   const uint32_t seg = local - row * c.units_per_run.div;
@@ -87,13 +98,19 @@ __device__ __forceinline__ bool resolve_unit(const DevCopy* __restrict__ table, 
 }
 
 __global__ void __launch_bounds__(64, 1)
-    bulk_copy_kernel(const DevCopy* __restrict__ table, int ntasks, int64_t total,
+    bulk_copy_kernel(const DevCopy* __restrict__ table, int ntasks, int64_t first, int64_t total,
                      const __grid_constant__ PtrTable ptrs) {
-  extern __shared__ uint8_t raw[];
-  uint8_t* stage = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 127) &
-                                              ~uintptr_t(127));
+  // Shared memory: [descriptor table (this launch's <= kBulkSmemTasks)] [ring].
+  // The table is staged once per CTA so unit resolution is a broadcast smem
+  // search, not a chain of dependent global loads per batch.
+  extern __shared__ __align__(128) uint8_t raw[];
+  const DevCopy* tab = reinterpret_cast<const DevCopy*>(raw);
+  uint8_t* stage = raw + kTableBytes;
   __shared__ uint64_t full[kStages], empty[kStages];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  {
+    stage_table(table, ntasks, raw);
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&full[s])));
@@ -103,14 +120,17 @@ __global__ void __launch_bounds__(64, 1)
   }
   __syncthreads();
 
-  const int64_t batches = (total + 31) / 32;
+  const int64_t batches = (total - first + 31) / 32;
+  // Batches go round-robin over the CTAs; a lane's units only move forward,
+  // so its descriptor cursor is advanced by a search over later entries.
+  int cur = 0;
   if (warp == 0) {  // loader
     int i = 0;
     for (int64_t b = blockIdx.x; b < batches; b += gridDim.x, ++i) {
       const int s = i % kStages;
       bar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
       Unit u;
-      const bool ok = resolve_unit(table, ntasks, total, b * 32 + lane, u);
+      const bool ok = resolve_unit(tab, ntasks, total, first + b * 32 + lane, cur, u);
       uint32_t bytes = ok ? u.bytes : 0;
       uint32_t sum = bytes;
 #pragma unroll
@@ -136,7 +156,7 @@ __global__ void __launch_bounds__(64, 1)
       const int s = i % kStages;
       bar_wait(&full[s], (i / kStages) & 1);
       Unit u;
-      if (resolve_unit(table, ntasks, total, b * 32 + lane, u)) {
+      if (resolve_unit(tab, ntasks, total, first + b * 32 + lane, cur, u)) {
         const uint32_t from = saddr(stage + s * kStageBytes + lane * kBulkSeg);
         for (int j = 0; j < u.d->ndst; ++j) {
           char* dst = ptrs.dst[u.d->dst_bufs[j]] + u.dd;
@@ -163,8 +183,8 @@ __global__ void __launch_bounds__(64, 1)
 
 int bulk_smem_bytes() { return kSmemBytes; }
 
-cudaError_t launch_bulk_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
-                             const PtrTable& ptrs, cudaStream_t stream) {
+cudaError_t launch_bulk_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,
+                             int64_t total_units, const PtrTable& ptrs, cudaStream_t stream) {
   if (ntasks <= 0 || total_units <= 0) return cudaSuccess;
   static bool configured = false;
   if (!configured) {
@@ -173,9 +193,14 @@ cudaError_t launch_bulk_copy(const DevCopy* d_table, int ntasks, int64_t total_u
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int64_t batches = (total_units + 31) / 32;
-  const int grid = static_cast<int>(std::min<int64_t>(batches, sm_count()));
-  bulk_copy_kernel<<<grid, 64, kSmemBytes, stream>>>(d_table, ntasks, total_units, ptrs);
+  for (int k = 0; k < ntasks; k += kBulkSmemTasks) {
+    const int m = std::min(kBulkSmemTasks, ntasks - k);
+    const int64_t first = begins[k];
+    const int64_t end = k + m < ntasks ? begins[k + m] : total_units;
+    const int64_t batches = (end - first + 31) / 32;
+    const int grid = static_cast<int>(std::min<int64_t>(batches, sm_count()));
+    bulk_copy_kernel<<<grid, 64, kSmemBytes, stream>>>(d_table + k, m, first, end, ptrs);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -233,7 +233,10 @@ CopyDesc make_copy(int src_buf, const std::vector<int64_t>& src_shape,
 }
 
 void merge_splits(std::vector<CopyDesc>& descs) {
-  constexpr int64_t kShortRun = 64;
+  static const int64_t kShortRun = [] {  // APL_SPLIT_RUN: experiment knob
+    const char* e = std::getenv("APL_SPLIT_RUN");
+    return e ? std::atoll(e) : int64_t{64};
+  }();
   static const bool enabled = [] {
     const char* e = std::getenv("APL_SPLIT");  // "0" disables (A/B measurements)
     return e == nullptr || std::string(e) != "0";

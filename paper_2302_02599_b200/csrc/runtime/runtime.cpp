@@ -163,6 +163,28 @@ CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool 
   for (const CopyDesc& d : descs)
     if (d.bytes() > 0) split_large(d, vec, flat);
   if (flat.empty()) return cc;
+  static const int slabs = [] {  // experiment knob: cut every descriptor into row slabs
+    const char* e = std::getenv("APL_SLABS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (slabs > 1) {
+    std::vector<CopyDesc> cut;
+    for (const CopyDesc& d : flat) {
+      if (d.nouter == 0 || d.ext[0] < slabs) {
+        cut.push_back(d);
+        continue;
+      }
+      const int64_t per = (d.ext[0] + slabs - 1) / slabs;
+      for (int64_t i = 0; i < d.ext[0]; i += per) {
+        CopyDesc r = d;
+        r.ext[0] = std::min(per, d.ext[0] - i);
+        r.src_off += i * d.src_stride[0];
+        r.dst_off += i * d.dst_stride[0];
+        cut.push_back(r);
+      }
+    }
+    flat.swap(cut);
+  }
   std::vector<DevCopy> host(flat.size());
   int64_t units = 0;
   for (size_t i = 0; i < flat.size(); ++i) {
@@ -206,6 +228,7 @@ CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool 
   }
   cc.ntasks = static_cast<int>(host.size());
   cc.total_units = units;
+  for (const DevCopy& h : host) cc.begins.push_back(h.unit_begin);
   check_cuda(cudaMalloc(&cc.table, host.size() * sizeof(DevCopy)), "cudaMalloc(copy table)");
   check_cuda(cudaMemcpy(cc.table, host.data(), host.size() * sizeof(DevCopy),
                         cudaMemcpyHostToDevice),
@@ -221,10 +244,10 @@ void free_copies(CompiledCopies& c) {
 void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream) {
   if (c.empty()) return;
   if (c.bulk) {
-    check_cuda(launch_bulk_copy(c.table, c.ntasks, c.total_units, ptrs, stream), "bulk copy launch");
+    check_cuda(launch_bulk_copy(c.table, c.begins.data(), c.ntasks, c.total_units, ptrs, stream), "bulk copy launch");
     return;
   }
-  check_cuda(launch_box_copy(c.table, c.ntasks, c.total_units, c.vec, c.max_outer, c.max_fan, c.split, ptrs,
+  check_cuda(launch_box_copy(c.table, c.begins.data(), c.ntasks, c.total_units, c.vec, c.max_outer, c.max_fan, c.split, ptrs,
                              stream),
              "box_copy launch");
 }

@@ -29,8 +29,9 @@ void check_nccl(ncclResult_t r, const char* what);
 
 FastDiv make_fastdiv(uint32_t d);
 int sm_count();
-cudaError_t launch_box_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
-                            int vec_bytes, int max_outer, int max_fan, bool split,
+// begins: host copy of the table's unit_begin column (slicing into launches).
+cudaError_t launch_box_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,
+                            int64_t total_units, int vec_bytes, int max_outer, int max_fan, bool split,
                             const PtrTable& ptrs, cudaStream_t stream);
 cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int groups,
                                    int group_size, size_t count, int dtype,
@@ -54,6 +55,7 @@ struct MatmulStrategy {
 // A descriptor table resident on the device.
 struct CompiledCopies {
   DevCopy* table = nullptr;
+  std::vector<int64_t> begins;  // host copy of table[i].unit_begin
   int ntasks = 0;
   int64_t total_units = 0;
   int vec = 16;
@@ -66,8 +68,8 @@ struct CompiledCopies {
   bool empty() const { return ntasks == 0; }
 };
 
-cudaError_t launch_bulk_copy(const DevCopy* d_table, int ntasks, int64_t total_units,
-                             const PtrTable& ptrs, cudaStream_t stream);
+cudaError_t launch_bulk_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,
+                             int64_t total_units, const PtrTable& ptrs, cudaStream_t stream);
 // True when every run of the table suits the TMA bulk engine.
 bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec);
 
