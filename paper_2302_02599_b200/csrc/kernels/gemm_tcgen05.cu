@@ -111,11 +111,12 @@ __device__ __forceinline__ uint64_t smem_desc_mn(const void* tile) {
   return d;
 }
 
-template <int BN, bool kBMN>
+template <int BN, bool kBMN, bool kAMN>
 __device__ __forceinline__ constexpr uint32_t instr_desc() {
   return (1u << 4)                     // D = f32
          | (1u << 7)                   // A = bf16
          | (1u << 10)                  // B = bf16
+         | (uint32_t(kAMN ? 1 : 0) << 15)  // A major: 0 = K, 1 = MN
          | (uint32_t(kBMN ? 1 : 0) << 16)  // B major: 0 = K, 1 = MN
          | (uint32_t(BN >> 3) << 17)   // N
          | (uint32_t(kBM >> 4) << 24); // M
@@ -168,17 +169,58 @@ __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.f + erf_v);
 }
 
+// d/dx GELU(x) = Phi(x) + x phi(x), with the same A&S erf as gelu_erf.
+__device__ __forceinline__ float gelu_grad(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __frcp_rn(1.f + 0.3275911f * z);
+  float poly = fmaf(1.061405429f, t, -1.453152027f);
+  poly = fmaf(poly, t, 1.421413741f);
+  poly = fmaf(poly, t, -0.284496736f);
+  poly = fmaf(poly, t, 0.254829592f);
+  poly *= t;
+  const float e = exp2f(-z * z * 1.4426950408889634f);  // exp(-x^2 / 2)
+  const float erf_v = copysignf(fmaf(-poly, e, 1.f), x);
+  return 0.5f * (1.f + erf_v) + x * e * 0.3989422804014327f;
+}
+
+// Epilogues: 0 = none, 1 = GELU, 2 = GELU backward (C = acc * GELU'(aux),
+// aux bf16 [M, N] with leading dimension ldaux: the saved pre-activation).
+constexpr int kEpiNone = 0, kEpiGelu = 1, kEpiDGelu = 2;
+
 // Epilogue of one accumulator row chunk: 16 fp32 columns of row `row`
-// starting at `col` -> (GELU) -> bf16 / fp32, vectorised when aligned.
-template <bool kGelu, bool kOutF32>
+// starting at `col` -> epilogue -> bf16 / fp32, vectorised when aligned.
+template <int kEpi, bool kOutF32>
 __device__ __forceinline__ void store_chunk(void* out, int ldc, int M, int N, int row, int col,
-                                            const uint32_t (&r)[16]) {
+                                            const uint32_t (&r)[16], const void* aux = nullptr,
+                                            int ldaux = 0) {
   if (row >= M || col >= N) return;
   float v[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     v[i] = __uint_as_float(r[i]);
-    if (kGelu) v[i] = gelu_erf(v[i]);
+    if (kEpi == kEpiGelu) v[i] = gelu_erf(v[i]);
+  }
+  if constexpr (kEpi == kEpiDGelu) {
+    const __nv_bfloat16* a =
+        static_cast<const __nv_bfloat16*>(aux) + static_cast<size_t>(row) * ldaux + col;
+    float x[16];
+    if (col + 16 <= N && (reinterpret_cast<uintptr_t>(a) & 15) == 0) {
+      uint4 q[2];
+      q[0] = reinterpret_cast<const uint4*>(a)[0];
+      q[1] = reinterpret_cast<const uint4*>(a)[1];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(q);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        x[2 * i] = f.x;
+        x[2 * i + 1] = f.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = col + i < N ? __bfloat162float(a[i]) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] *= gelu_grad(x[i]);
   }
   if constexpr (kOutF32) {
     float* dst = static_cast<float*>(out) + static_cast<size_t>(row) * ldc + col;
@@ -239,15 +281,20 @@ constexpr int kMaxBatch = 8;
 // the finished tile to `fan` outputs (c[g*fan + j]). With reduce = fan =
 // group size this is the split-k GEMM and its all-reduce in one kernel:
 // no partial buffers, no reduction pass, every replica bit-identical.
+//
+// kAMN: A is given transposed, as the row-major [K, M] (M contiguous, an
+// MN-major UMMA operand) -- the weight-gradient GEMM dW = X^T . dY reads the
+// saved activation X [tokens, features] as is, with no transpose pass.
 struct GemmArgs {
   CUtensorMap a[kMaxBatch];
   CUtensorMap b[kMaxBatch];
   void* c[kMaxBatch];
-  int count, M, N, K, ldc;
+  const void* aux[kMaxBatch];  // kEpiDGelu: pre-activation per output problem
+  int count, M, N, K, ldc, ldaux;
   int reduce, fan;
 };
 
-template <int BN, bool kGelu, bool kOutF32, bool kBMN>
+template <int BN, int kEpi, bool kOutF32, bool kBMN, bool kAMN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ GemmArgs args) {
   const int M = args.M, N = args.N, K = args.K, ldc = args.ldc;
@@ -310,7 +357,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
           mbar_expect_tx(&full[s], S::kStageA + S::kStageB);
-          tma_load_2d(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
+          if constexpr (kAMN) {
+            // two boxes of [64 k][64 m], one MN swizzle atom column each
+            tma_load_2d(tiles_a + s * S::kStageA, map_a, &full[s], m0, kb * kBK);
+            tma_load_2d(tiles_a + s * S::kStageA + 8192, map_a, &full[s], m0 + 64, kb * kBK);
+          } else {
+            tma_load_2d(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
+          }
           if constexpr (kBMN) {
             // BN/64 boxes of [64 k][64 n], one MN swizzle atom column each
 #pragma unroll
@@ -325,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc<BN, kBMN>();
+      constexpr uint32_t idesc = instr_desc<BN, kBMN, kAMN>();
       int it = 0, local = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
         const int acc = local & 1;
@@ -337,15 +390,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&full[s], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t da = smem_desc(tiles_a + s * S::kStageA);
+          const uint64_t da = kAMN ? smem_desc_mn(tiles_a + s * S::kStageA)
+                                   : smem_desc(tiles_a + s * S::kStageA);
           const uint64_t db = kBMN ? smem_desc_mn(tiles_b + s * S::kStageB)
                                    : smem_desc(tiles_b + s * S::kStageB);
           // K advance per instruction: K-major = 32 B inside the swizzle row;
           // MN-major = 16 rows of 128 B.
+          constexpr uint64_t kAdvA = kAMN ? (16 * 128) >> 4 : 2;
           constexpr uint64_t kAdvB = kBMN ? (16 * 128) >> 4 : 2;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            mma_bf16(d, da + uint64_t(2 * k), db + kAdvB * k, idesc,
+            mma_bf16(d, da + kAdvA * k, db + kAdvB * k, idesc,
                      (kk > 0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
@@ -373,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld16(lane_addr + uint32_t(c), r);
         const int col = n0 + c;
         for (int j = 0; j < args.fan; ++j)
-          store_chunk<kGelu, kOutF32>(outs[j], ldc, M, N, row, col, r);
+          store_chunk<kEpi, kOutF32>(outs[j], ldc, M, N, row, col, r, args.aux[g], args.ldaux);
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -601,7 +656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t r[16];
         tmem_ld16(lane_addr + uint32_t(c), r);
         for (int j = 0; j < args.fan; ++j)
-          store_chunk<kGelu, kOutF32>(outs[j], ldc, M, N, row, n0 + c, r);
+          store_chunk<kGelu ? kEpiGelu : kEpiNone, kOutF32>(outs[j], ldc, M, N, row, n0 + c, r);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -655,9 +710,9 @@ bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool G, bool F, bool BMN>
+template <int BN, int E, bool F, bool BMN, bool AMN = false>
 cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
-  auto kernel = gemm_bf16_tcgen05<BN, G, F, BMN>;
+  auto kernel = gemm_bf16_tcgen05<BN, E, F, BMN, AMN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -679,12 +734,21 @@ cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
 }
 
 template <int BN, bool BMN>
-cudaError_t dispatch(const GemmArgs& args, bool out_f32, bool gelu, cudaStream_t stream) {
-  if (gelu)
-    return out_f32 ? launch_gemm<BN, true, true, BMN>(args, stream)
-                   : launch_gemm<BN, true, false, BMN>(args, stream);
-  return out_f32 ? launch_gemm<BN, false, true, BMN>(args, stream)
-                 : launch_gemm<BN, false, false, BMN>(args, stream);
+cudaError_t dispatch(const GemmArgs& args, bool out_f32, int epi, bool a_km,
+                     cudaStream_t stream) {
+  if (a_km) {  // weight-gradient GEMMs: no activation epilogue
+    if (epi != kEpiNone) return cudaErrorInvalidValue;
+    return out_f32 ? launch_gemm<BN, kEpiNone, true, BMN, true>(args, stream)
+                   : launch_gemm<BN, kEpiNone, false, BMN, true>(args, stream);
+  }
+  if (epi == kEpiDGelu)
+    return out_f32 ? launch_gemm<BN, kEpiDGelu, true, BMN>(args, stream)
+                   : launch_gemm<BN, kEpiDGelu, false, BMN>(args, stream);
+  if (epi == kEpiGelu)
+    return out_f32 ? launch_gemm<BN, kEpiGelu, true, BMN>(args, stream)
+                   : launch_gemm<BN, kEpiGelu, false, BMN>(args, stream);
+  return out_f32 ? launch_gemm<BN, kEpiNone, true, BMN>(args, stream)
+                 : launch_gemm<BN, kEpiNone, false, BMN>(args, stream);
 }
 
 // 2-CTA pair kernel launch (cluster dims are compiled into the kernel).
@@ -738,21 +802,26 @@ bool use_pair(int M, int N, int count) {
 
 }  // namespace
 
-// count equally shaped problems C_i[M,N] = A_i[M,K] . B_i, B_i given as Bt
-// [N,K] (b_kn = false, nn.Linear layout) or as row-major [K,N] (b_kn = true);
-// bf16 in, fp32 accumulate. out_f32 selects the output type; gelu applies
-// exact-erf GELU in the epilogue. All problems share one persistent launch
-// (chunks of kMaxBatch): the CTA-pair kernel (M=256 x N=256 tiles) for
-// large problems, the single-CTA kernel (128 x BN) otherwise.
+// count equally shaped problems C_i[M,N] = epi(A_i . B_i); A_i given as
+// [M,K] (K contiguous) or, with a_km, as row-major [K,M] (M contiguous);
+// B_i as Bt [N,K] (b_kn = false, nn.Linear layout) or row-major [K,N]
+// (b_kn = true); bf16 in, fp32 accumulate. out_f32 selects the output type;
+// epi: 0 none, 1 exact-erf GELU, 2 GELU backward against aux_i (bf16 [M,N],
+// leading dimension ldaux, one per output problem). All problems share one
+// persistent launch (chunks of kMaxBatch): the CTA-pair kernel (M=256 x
+// N=256 tiles) for large forward problems, the single-CTA kernel (128 x BN)
+// otherwise.
 cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* const* C,
                               int groups, int reduce, int fan, int M, int N, int K, int lda,
-                              int ldb, int ldc, bool b_kn, bool out_f32, bool gelu,
-                              cudaStream_t stream) {
+                              int ldb, int ldc, bool b_kn, bool out_f32, int epi, bool a_km,
+                              const void* const* aux, int ldaux, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || groups <= 0) return cudaSuccess;
   if (reduce < 1 || fan < 1 || reduce > kMaxBatch || fan > kMaxBatch) return cudaErrorInvalidValue;
   if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;  // TMA row alignment
+  if (epi < kEpiNone || epi > kEpiDGelu || (epi == kEpiDGelu && aux == nullptr))
+    return cudaErrorInvalidValue;
   const int per_launch = std::max(1, std::min(kMaxBatch / reduce, kMaxBatch / fan));
-  const bool paired = use_pair(M, N, std::min(groups, per_launch));
+  const bool paired = !a_km && epi != kEpiDGelu && use_pair(M, N, std::min(groups, per_launch));
   const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
   // B box rows for the K-major layout: the pair kernel stages half of its
   // 256-wide N tile per CTA.
@@ -767,30 +836,42 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
     args.N = N;
     args.K = K;
     args.ldc = ldc;
+    args.ldaux = ldaux;
     for (int i = 0; i < args.count * reduce; ++i) {
       const void* a = A[first * reduce + i];
       const void* b = B[first * reduce + i];
       if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
         return cudaErrorInvalidValue;
-      if (!make_map(&args.a[i], a, M, K, lda, kBM)) return cudaErrorInvalidValue;
-      const bool ok = b_kn ? make_map(&args.b[i], b, K, N, ldb, kBK, 64)
-                           : make_map(&args.b[i], b, N, K, ldb, b_rows);
-      if (!ok) return cudaErrorInvalidValue;
+      const bool oka = a_km ? make_map(&args.a[i], a, K, M, lda, kBK, 64)
+                            : make_map(&args.a[i], a, M, K, lda, kBM);
+      const bool okb = b_kn ? make_map(&args.b[i], b, K, N, ldb, kBK, 64)
+                            : make_map(&args.b[i], b, N, K, ldb, b_rows);
+      if (!oka || !okb) return cudaErrorInvalidValue;
     }
     for (int i = 0; i < args.count * fan; ++i) args.c[i] = C[first * fan + i];
+    if (epi == kEpiDGelu)
+      for (int i = 0; i < args.count; ++i) args.aux[i] = aux[first + i];
     cudaError_t e;
     if (paired)
-      e = b_kn ? dispatch_pair<true>(args, out_f32, gelu, stream)
-               : dispatch_pair<false>(args, out_f32, gelu, stream);
+      e = b_kn ? dispatch_pair<true>(args, out_f32, epi == kEpiGelu, stream)
+               : dispatch_pair<false>(args, out_f32, epi == kEpiGelu, stream);
     else if (b_kn)
-      e = bn == 256 ? dispatch<256, true>(args, out_f32, gelu, stream)
-                    : dispatch<128, true>(args, out_f32, gelu, stream);
+      e = bn == 256 ? dispatch<256, true>(args, out_f32, epi, a_km, stream)
+                    : dispatch<128, true>(args, out_f32, epi, a_km, stream);
     else
-      e = bn == 256 ? dispatch<256, false>(args, out_f32, gelu, stream)
-                    : dispatch<128, false>(args, out_f32, gelu, stream);
+      e = bn == 256 ? dispatch<256, false>(args, out_f32, epi, a_km, stream)
+                    : dispatch<128, false>(args, out_f32, epi, a_km, stream);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* const* C,
+                              int groups, int reduce, int fan, int M, int N, int K, int lda,
+                              int ldb, int ldc, bool b_kn, bool out_f32, bool gelu,
+                              cudaStream_t stream) {
+  return gemm_bf16_grouped(A, B, C, groups, reduce, fan, M, N, K, lda, ldb, ldc, b_kn, out_f32,
+                           gelu ? kEpiGelu : kEpiNone, false, nullptr, 0, stream);
 }
 
 cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,
