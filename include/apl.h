@@ -309,6 +309,34 @@ int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
  * a plan that could not be fused into a GEMM epilogue). */
 int apl_gelu_inplace(void* buf, size_t count, int dtype, void* stream);
 
+/* ---- backward (reverse-path conversions + gradient sync) ---
+ * The reference prices the backward pass (reverse-path conversions,
+ * ckpt.cpp:348-356; gradient all-reduce over replica axes, ckpt.cpp:359-395,
+ * planner.cpp:358-385) but never runs it. These entry points execute it. */
+
+/* y = GELU(x) out of place (a training forward keeps the pre-activation). */
+int apl_gelu(const void* x, void* y, size_t count, int dtype, void* stream);
+/* dx = dy * GELU'(x). */
+int apl_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int dtype,
+                      void* stream);
+
+#define APL_EPI_DGELU 2 /* backward epilogue: dA *= GELU'(aux) */
+
+/* Backward of apl_sharded_matmul for the same strategy and shards: per local
+ * device dA = dC . B^T (bf16, [m_local, k_local]; epilogue APL_EPI_DGELU
+ * multiplies by GELU'(aux), aux = the bf16 pre-activation that produced A)
+ * and dB = A^T . dC (dB_dtype, in B's storage layout b_layout). Each is
+ * summed over the mesh axes it is partial over: dA over the axes sharding
+ * C's n dim, dB over the axes sharding C's m dims (the data-parallel
+ * gradient all-reduce). dA or dB may be NULL. dC must be the (replicated)
+ * gradient of the all-reduced C. */
+int apl_sharded_matmul_backward(apl_mesh* mesh, const apl_matmul_strategy* strategy,
+                                const apl_meta* a_meta, const apl_meta* b_meta,
+                                const void* const* A, const void* const* B,
+                                const void* const* dC, void* const* dA, void* const* dB,
+                                int b_layout, int dA_epilogue, const void* const* aux,
+                                int dB_dtype, void* stream);
+
 /* Kernel launches this process issued through the library (evidence). */
 int apl_launch_count(uint64_t* launches);
 

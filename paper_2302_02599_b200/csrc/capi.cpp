@@ -764,6 +764,53 @@ int apl_gelu_inplace(void* buf, size_t count, int dtype, void* stream) {
   });
 }
 
+int apl_gelu(const void* x, void* y, size_t count, int dtype, void* stream) {
+  return guarded([&] {
+    need((x && y) || count == 0, "null buffer");
+    need(dtype >= APL_F32 && dtype <= APL_F16, "bad dtype");
+    apl::check_cuda(apl::launch_gelu(x, y, count, dtype, static_cast<cudaStream_t>(stream)),
+                    "gelu launch");
+  });
+}
+
+int apl_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int dtype,
+                      void* stream) {
+  return guarded([&] {
+    need((dy && x && dx) || count == 0, "null buffer");
+    need(dtype >= APL_F32 && dtype <= APL_F16, "bad dtype");
+    apl::check_cuda(
+        apl::launch_gelu_backward(dy, x, dx, count, dtype, static_cast<cudaStream_t>(stream)),
+        "gelu backward launch");
+  });
+}
+
+int apl_sharded_matmul_backward(apl_mesh* mesh, const apl_matmul_strategy* strategy,
+                                const apl_meta* a_meta, const apl_meta* b_meta,
+                                const void* const* A, const void* const* B,
+                                const void* const* dC, void* const* dA, void* const* dB,
+                                int b_layout, int dA_epilogue, const void* const* aux,
+                                int dB_dtype, void* stream) {
+  return guarded([&] {
+    need(mesh && strategy && dC, "null argument");
+    need(dA == nullptr || B != nullptr, "dA needs B");
+    need(dB == nullptr || A != nullptr, "dB needs A");
+    need(b_layout == APL_B_NK || b_layout == APL_B_KN, "unknown B layout");
+    need(dA_epilogue == APL_EPI_NONE || dA_epilogue == APL_EPI_DGELU, "unknown dA epilogue");
+    need(dA_epilogue != APL_EPI_DGELU || aux != nullptr, "APL_EPI_DGELU needs aux");
+    need(dB_dtype == APL_F32 || dB_dtype == APL_BF16, "dB dtype must be f32 or bf16");
+    need(strategy->nreduce >= 0 && strategy->nreduce <= APL_MAX_MESH, "bad reduce axis count");
+    apl::MatmulStrategy s;
+    s.a = to_spec(&strategy->a);
+    s.b = to_spec(&strategy->b);
+    s.c = to_spec(&strategy->c);
+    s.partial_sum = strategy->partial_sum != 0;
+    for (int i = 0; i < strategy->nreduce; ++i) s.reduce_axes.push_back(strategy->reduce_axes[i]);
+    apl::sharded_matmul_backward(mesh->impl, s, to_meta(a_meta), to_meta(b_meta), A, B, dC, dA,
+                                 dB, b_layout == APL_B_KN, dA_epilogue == APL_EPI_DGELU, aux,
+                                 dB_dtype, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int apl_launch_count(uint64_t* launches) {
   return guarded([&] {
     need(launches, "null out");

@@ -119,12 +119,60 @@ cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int gr
 namespace {
 
 template <typename T>
-__global__ void __launch_bounds__(256) gelu_inplace(T* __restrict__ buf, int64_t n) {
+__global__ void __launch_bounds__(256) gelu_apply(const T* __restrict__ x, T* __restrict__ y,
+                                                  int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float x = to_f(buf[i]);
-    buf[i] = from_f<T>(0.5f * x * (1.f + erff(x * 0.70710678118654752f)));
+    const float v = to_f(x[i]);
+    y[i] = from_f<T>(0.5f * v * (1.f + erff(v * 0.70710678118654752f)));
   }
+}
+
+// dx = dy * GELU'(x), GELU'(x) = Phi(x) + x phi(x).
+template <typename T>
+__global__ void __launch_bounds__(256) gelu_backward(const T* __restrict__ dy,
+                                                     const T* __restrict__ x, T* __restrict__ dx,
+                                                     int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = to_f(x[i]);
+    const float g = 0.5f * (1.f + erff(v * 0.70710678118654752f)) +
+                    v * 0.3989422804014327f * __expf(-0.5f * v * v);
+    dx[i] = from_f<T>(to_f(dy[i]) * g);
+  }
+}
+
+template <typename T>
+cudaError_t gelu_typed(const void* x, void* y, const void* dy, size_t count, cudaStream_t stream) {
+  const int grid = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 16));
+  if (dy == nullptr)
+    gelu_apply<T><<<grid, 256, 0, stream>>>(static_cast<const T*>(x), static_cast<T*>(y), count);
+  else
+    gelu_backward<T><<<grid, 256, 0, stream>>>(static_cast<const T*>(dy),
+                                               static_cast<const T*>(x), static_cast<T*>(y),
+                                               count);
+  return cudaGetLastError();
+}
+
+cudaError_t gelu_dispatch(const void* x, void* y, const void* dy, size_t count, int dtype,
+                          cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  cudaError_t e;
+  switch (dtype) {
+    case 0:
+      e = gelu_typed<float>(x, y, dy, count, stream);
+      break;
+    case 1:
+      e = gelu_typed<__nv_bfloat16>(x, y, dy, count, stream);
+      break;
+    case 2:
+      e = gelu_typed<__half>(x, y, dy, count, stream);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return e;
 }
 
 }  // namespace
@@ -132,23 +180,18 @@ __global__ void __launch_bounds__(256) gelu_inplace(T* __restrict__ buf, int64_t
 // Exact-erf GELU over a buffer (the epilogue of partial-sum strategies,
 // applied once the all-reduce has produced the full sums).
 cudaError_t launch_gelu_inplace(void* buf, size_t count, int dtype, cudaStream_t stream) {
-  if (count == 0) return cudaSuccess;
-  const int grid = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 16));
-  switch (dtype) {
-    case 0:
-      gelu_inplace<float><<<grid, 256, 0, stream>>>(static_cast<float*>(buf), count);
-      break;
-    case 1:
-      gelu_inplace<__nv_bfloat16><<<grid, 256, 0, stream>>>(static_cast<__nv_bfloat16*>(buf), count);
-      break;
-    case 2:
-      gelu_inplace<__half><<<grid, 256, 0, stream>>>(static_cast<__half*>(buf), count);
-      break;
-    default:
-      return cudaErrorInvalidValue;
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return gelu_dispatch(buf, buf, nullptr, count, dtype, stream);
+}
+
+// y = GELU(x) out of place (training forward keeps the pre-activation x).
+cudaError_t launch_gelu(const void* x, void* y, size_t count, int dtype, cudaStream_t stream) {
+  return gelu_dispatch(x, y, nullptr, count, dtype, stream);
+}
+
+// dx = dy * GELU'(x) (backward of an unfused elementwise GELU node).
+cudaError_t launch_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int dtype,
+                                 cudaStream_t stream) {
+  return gelu_dispatch(x, dx, dy, count, dtype, stream);
 }
 
 uint64_t launch_count() { return g_launches.load(); }

@@ -38,6 +38,9 @@ cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int gr
                                    cudaStream_t stream);
 uint64_t launch_count();
 cudaError_t launch_gelu_inplace(void* buf, size_t count, int dtype, cudaStream_t stream);
+cudaError_t launch_gelu(const void* x, void* y, size_t count, int dtype, cudaStream_t stream);
+cudaError_t launch_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int dtype,
+                                 cudaStream_t stream);
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                       int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream);
 cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,
@@ -178,11 +181,31 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
                               int ldb, int ldc, bool b_kn, bool out_f32, bool gelu,
                               cudaStream_t stream);
 
+// Extended form: A given transposed (a_km: row-major [K, M]) and epilogue
+// 0 none / 1 GELU / 2 GELU backward against aux (bf16 [M, N], one per
+// output problem).
+cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* const* C,
+                              int groups, int reduce, int fan, int M, int N, int K, int lda,
+                              int ldb, int ldc, bool b_kn, bool out_f32, int epi, bool a_km,
+                              const void* const* aux, int ldaux, cudaStream_t stream);
+
 // B shards are row-major [k_local, n_local] when b_kn, else transposed
 // [n_local, k_local] (nn.Linear layout).
 void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorMeta& a_meta,
                     const autoplan::TensorMeta& b_meta, const void* const* A,
                     const void* const* B, void* const* C, bool b_kn, int out_dtype,
                     int epilogue, cudaStream_t stream);
+
+// Backward of one strategy: per local device dA = dC . B^T (bf16; with
+// dgelu, times GELU'(aux) -- the fused backward of a GELU feeding A) and
+// dB = A^T . dC (dB_dtype, in B's storage layout), each summed over the
+// mesh axes it is partial over (dA: the axes sharding C's n dim; dB: the
+// axes sharding C's m dims). dA / dB may be null to skip.
+void sharded_matmul_backward(Mesh& mesh, const MatmulStrategy& s,
+                             const autoplan::TensorMeta& a_meta,
+                             const autoplan::TensorMeta& b_meta, const void* const* A,
+                             const void* const* B, const void* const* dC, void* const* dA,
+                             void* const* dB, bool b_kn, bool dgelu, const void* const* aux,
+                             int dB_dtype, cudaStream_t stream);
 
 }  // namespace apl

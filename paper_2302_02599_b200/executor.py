@@ -80,6 +80,7 @@ class PlanExecutor:
     plan: dict
     fuse: bool = True
     comm: list = field(default_factory=list)
+    _saved: dict = None
 
     def __post_init__(self):
         self.geo: DeviceMesh = self.mesh.geo
@@ -198,14 +199,16 @@ class PlanExecutor:
         conv(shards, outs, stream=stream)
         return outs
 
-    def forward(self, feeds: dict, stream=None) -> list:
+    def forward(self, feeds: dict, stream=None, train: bool = False) -> list:
         """feeds: global tensors for every placeholder and parameter, or
-        already-sharded lists (node id -> list of local shards)."""
-        from . import _capi as A
-        from .layout import check
-        import ctypes as C
+        already-sharded lists (node id -> list of local shards).
+        train=True keeps what backward() needs: every matmul's operands in
+        the layouts its strategy consumed them, and every GELU's input (the
+        GELU is then not fused into the GEMM epilogue)."""
+        from .runtime import gelu
 
         values, converted, fused = {}, {}, set()
+        self._saved = {} if train else None
         for n in self.graph["nodes"]:
             nid, kind = n["id"], n["kind"]
             if kind in ("placeholder", "parameter"):
@@ -226,7 +229,9 @@ class PlanExecutor:
                 st = self.strategy[nid]
                 out_spec = self.spec[nid]
                 outs = self._alloc(nid, out_spec, ins[0][0])
-                gelu_node = self._fusable_gelu(nid)
+                gelu_node = None if train else self._fusable_gelu(nid)
+                if train:
+                    self._saved[nid] = (ins[0], ins[1])
                 self.mesh.sharded_matmul(st, self._meta(n["inputs"][0][0]),
                                          self._meta(n["inputs"][1][0]), ins[0], ins[1], outs,
                                          gelu=gelu_node is not None, b_layout="kn",
@@ -238,18 +243,125 @@ class PlanExecutor:
                 if nid in fused:
                     values[nid] = ins[0]
                 else:
-                    outs = [t.clone() for t in ins[0]]
-                    code = {torch.float32: A.F32, torch.bfloat16: A.BF16}[outs[0].dtype]
-                    s = stream if stream is not None else torch.cuda.current_stream()
-                    for t in outs:
-                        check(A.lib().apl_gelu_inplace(C.c_void_p(t.data_ptr()), t.numel(), code,
-                                                       C.c_void_p(s.cuda_stream)))
+                    outs = [torch.empty_like(t) for t in ins[0]]
+                    for x, y in zip(ins[0], outs):
+                        gelu(x, y, stream=stream)
+                    if train:
+                        self._saved[nid] = ins[0]  # the pre-activation
                     values[nid] = outs
             elif kind == "output":
                 values[nid] = ins[0]
             else:
                 raise NotImplementedError(kind)
         return values[self.graph["output"]]
+
+
+    # ---- backward ---------------------------------------------
+    def _convert_grad(self, nid, shards, have, want, stream):
+        """Gradient of node `nid`'s value, held in layout `have`, into layout
+        `want`. A layout conversion is the identity on the global tensor, so
+        its adjoint is the identity too: the gradient takes the reverse
+        conversion (the reference prices exactly this path for the backward
+        pass, ckpt.cpp:348-356). Gradients here are never partial -- every
+        partial sum is reduced where it is produced -- so the reverse path is
+        exact."""
+        if have == want:
+            return shards
+        shape, _ = self.shapes[nid]
+        meta = TensorMeta(shape, shards[0].element_size())
+        key = ("grad", nid, str(have), str(want), meta.dtype_bytes)
+        conv = self._convs.get(key)
+        if conv is None:
+            conv = self.mesh.prepare(find_transform_path(have, want, self.geo, meta), meta,
+                                     fuse=self.fuse)
+            self._convs[key] = conv
+        outs = [torch.empty(want.local_shape(meta, self.geo), dtype=shards[0].dtype,
+                            device=shards[0].device) for _ in range(self.mesh.num_local)]
+        conv(shards, outs, stream=stream)
+        return outs
+
+    def backward(self, grad_out, stream=None, input_grads: bool = False) -> dict:
+        """Backward pass of the last forward(train=True).
+
+        grad_out: gradient of the output (global tensor, or its RR shards).
+        Returns {node id: gradient shards in the node's plan spec} for every
+        parameter (fp32) and, with input_grads, every placeholder (bf16).
+
+        Per matmul (reverse graph order): dA = dC . B^T and dB = A^T . dC on
+        each device's shards (tcgen05, apl_sharded_matmul_backward), each
+        summed over the mesh axes it is partial over -- for dB that is the
+        data-parallel gradient all-reduce the reference prices over replica
+        axes (ckpt.cpp:359-395, planner.cpp:358-385); on a simulated mesh the
+        sum is fused into the GEMM. A GELU feeding A (in A's layout, single
+        consumer) has its backward fused into the dA epilogue. Gradients then
+        take the reverse conversion back to the producer's layout."""
+        if self._saved is None:
+            raise RuntimeError("backward() needs a preceding forward(train=True)")
+        out_id = self.graph["output"]
+        out_node = self.nodes[out_id]
+        src = out_node["inputs"][0][0]
+        rr = self.required_spec(out_id, 0)
+        if isinstance(grad_out, list):
+            g = grad_out
+        else:
+            g = [grad_out.to(torch.bfloat16).contiguous() for _ in range(self.mesh.num_local)]
+        grads = {src: self._convert_grad(src, g, rr, self.spec[src], stream)}
+        done = set()
+        kinds = {"parameter"} | ({"placeholder"} if input_grads else set())
+
+        def add(nid, shards):
+            if nid in grads:
+                for acc, x in zip(grads[nid], shards):
+                    acc.add_(x)
+            else:
+                grads[nid] = shards
+
+        def wants_grad(nid):
+            k = self.nodes[nid]["kind"]
+            return k not in ("placeholder", "parameter") or k in kinds
+
+        for n in reversed(self.graph["nodes"]):
+            nid, kind = n["id"], n["kind"]
+            if nid in done or nid not in grads:
+                continue
+            dy = grads[nid]
+            if kind == "matmul":
+                st = self.strategy[nid]
+                a_saved, b_saved = self._saved[nid]
+                a_src, b_src = n["inputs"][0][0], n["inputs"][1][0]
+                a_meta, b_meta = self._meta(a_src), self._meta(b_src)
+                # GELU producing A in A's layout: its backward rides the dA epilogue.
+                aux, a_target = None, a_src
+                an = self.nodes[a_src]
+                if (an["kind"] == "elementwise-unary" and self.spec[a_src] == st.a
+                        and len(self._consumers.get(a_src, [])) == 1
+                        and isinstance(self._saved.get(a_src), list)):
+                    aux, a_target = self._saved[a_src], an["inputs"][0][0]
+                    done.add(a_src)
+                need_a = wants_grad(a_target)
+                need_b = wants_grad(b_src)
+                ga = [torch.empty_like(t) for t in a_saved] if need_a else None
+                gb = [torch.empty(t.shape, dtype=torch.float32, device=t.device)
+                      for t in b_saved] if need_b else None
+                if need_a or need_b:
+                    self.mesh.sharded_matmul_backward(st, a_meta, b_meta, a_saved, b_saved, dy,
+                                                      ga, gb, b_layout="kn", gelu_aux=aux,
+                                                      stream=stream)
+                if need_a:
+                    add(a_target, self._convert_grad(a_target, ga, st.a, self.spec[a_target],
+                                                      stream))
+                if need_b:
+                    add(b_src, self._convert_grad(b_src, gb, st.b, self.spec[b_src], stream))
+            elif kind == "elementwise-unary":
+                from .runtime import gelu_backward
+                x_src = n["inputs"][0][0]
+                pre = self._saved[nid]
+                dx = [torch.empty_like(t) for t in pre]
+                for a, x, o in zip(dy, pre, dx):
+                    gelu_backward(a, x, o, stream=stream)
+                add(x_src, self._convert_grad(x_src, dx, self.spec[nid], self.spec[x_src], stream))
+        return {nid: grads[nid] for nid in grads
+                if self.nodes[nid]["kind"] in kinds}
 
 
 def megatron_mlp_plan(mesh_rank: int = 1, axis: int = 0) -> dict:

@@ -32,6 +32,19 @@ def _stream_handle(stream) -> C.c_void_p:
     return C.c_void_p(s.cuda_stream)
 
 
+def gelu(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
+    """y = GELU(x) on the device (exact erf)."""
+    check(A.lib().apl_gelu(C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), x.numel(),
+                           _DTYPE_CODE[x.dtype], _stream_handle(stream)))
+
+
+def gelu_backward(dy: torch.Tensor, x: torch.Tensor, dx: torch.Tensor, stream=None) -> None:
+    """dx = dy * GELU'(x) on the device."""
+    check(A.lib().apl_gelu_backward(C.c_void_p(dy.data_ptr()), C.c_void_p(x.data_ptr()),
+                                    C.c_void_p(dx.data_ptr()), x.numel(), _DTYPE_CODE[x.dtype],
+                                    _stream_handle(stream)))
+
+
 def launch_count() -> int:
     n = C.c_uint64()
     check(A.lib().apl_launch_count(C.byref(n)))
@@ -216,6 +229,29 @@ class Mesh:
             _ptrs(a_shards), _ptrs(b_shards), _ptrs(c_shards),
             A.B_KN if b_layout == "kn" else A.B_NK, _DTYPE_CODE[c_shards[0].dtype],
             A.EPI_GELU if gelu else A.EPI_NONE, _stream_handle(stream)))
+
+    def sharded_matmul_backward(self, strategy: "MatmulStrategy", a_meta: TensorMeta,
+                                b_meta: TensorMeta, a_shards, b_shards, dc_shards,
+                                da_shards=None, db_shards=None, b_layout: str = "nk",
+                                gelu_aux=None, stream=None) -> None:
+        """Backward of sharded_matmul: dA = dC . B^T (times GELU'(gelu_aux)
+        when given) and dB = A^T . dC in B's storage layout, each summed over
+        the mesh axes it is partial over (see apl_sharded_matmul_backward)."""
+        n = self.num_local
+        for what, bufs in (("A", a_shards), ("B", b_shards), ("dC", dc_shards),
+                           ("dA", da_shards), ("dB", db_shards), ("aux", gelu_aux)):
+            if bufs is not None and len(bufs) != n:
+                raise ValueError(f"{what}: expected {n} shards")
+        db_dtype = _DTYPE_CODE[db_shards[0].dtype] if db_shards is not None else A.F32
+        check(A.lib().apl_sharded_matmul_backward(
+            self._h, C.byref(strategy.c_struct()), C.byref(a_meta.c()), C.byref(b_meta.c()),
+            _ptrs(a_shards) if a_shards is not None else None,
+            _ptrs(b_shards) if b_shards is not None else None, _ptrs(dc_shards),
+            _ptrs(da_shards) if da_shards is not None else None,
+            _ptrs(db_shards) if db_shards is not None else None,
+            A.B_KN if b_layout == "kn" else A.B_NK,
+            A.EPI_DGELU if gelu_aux is not None else A.EPI_NONE,
+            _ptrs(gelu_aux) if gelu_aux is not None else None, db_dtype, _stream_handle(stream)))
 
     def all_reduce(self, axes: Sequence[int], tensors, stream=None) -> None:
         if not tensors:
