@@ -7,6 +7,7 @@ built without sm_100a kernels the import fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 MAX_DIMS = 8
@@ -59,7 +60,8 @@ class PieceC(C.Structure):
                 ("ext", C.c_int64 * MAX_DIMS)]
 
 
-LIB_PATH = Path(__file__).resolve().parent / "libapl.so"
+# APL_LIB: load another build (A/B timing of two builds on one box).
+LIB_PATH = Path(os.environ.get("APL_LIB", Path(__file__).resolve().parent / "libapl.so"))
 _lib = None
 
 P = C.POINTER

@@ -21,6 +21,9 @@ from paper_2302_02599_b200.runtime import Mesh  # noqa: E402
 PLANS = ROOT / "tests" / "golden" / "plans"
 GRAPH = json.loads((PLANS / "gpt2_mlp_graph.json").read_text())
 FLOPS = 2 * 2.0 * 16384 * 1024 * 4096
+# training step: forward (2 GEMMs) + backward (fc2 dA and dB, fc1 dB; the
+# input x needs no gradient) = 5 GEMMs of 2*16384*1024*4096
+TRAIN_FLOPS = 5 * 2.0 * 16384 * 1024 * 4096
 
 
 def main():
@@ -49,8 +52,25 @@ def main():
             b.record()
             torch.cuda.synchronize()
             ms = a.elapsed_time(b) / iters
+            gy = torch.randn(16384, 1024, device="cuda").bfloat16()
+
+            def step():
+                ex.forward(shards, train=True)
+                ex.backward(gy)
+
+            for _ in range(3):
+                step()
+            torch.cuda.synchronize()
+            a.record()
+            for _ in range(iters):
+                step()
+            b.record()
+            torch.cuda.synchronize()
+            tms = a.elapsed_time(b) / iters
             print(json.dumps({"plan": name, "fuse": fuse, "ms_per_forward": round(ms, 4),
                               "tflops": round(FLOPS / ms / 1e9, 1),
+                              "ms_per_train_step": round(tms, 4),
+                              "train_tflops": round(TRAIN_FLOPS / tms / 1e9, 1),
                               "strategies": {k: v.name for k, v in ex.strategy.items()}}),
                   flush=True)
 
