@@ -822,7 +822,21 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
     return cudaErrorInvalidValue;
   const int per_launch = std::max(1, std::min(kMaxBatch / reduce, kMaxBatch / fan));
   const bool paired = !a_km && epi != kEpiDGelu && use_pair(M, N, std::min(groups, per_launch));
-  const int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
+  int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
+  {
+    // Too few 128 x 256 tiles to cover the SMs once (a per-GPU shard of a
+    // split-m / split-n strategy, e.g. 2048 x 1024): 128 x 128 tiles double
+    // the CTAs that work.
+    static const int sms = [] {
+      int dev = 0, n = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      return n > 0 ? n : 148;
+    }();
+    const int count = std::min(groups, per_launch);
+    const int tiles256 = ((M + kBM - 1) / kBM) * ((N + 255) / 256) * count;
+    if (bn == 256 && tiles256 < sms) bn = 128;
+  }
   // B box rows for the K-major layout: the pair kernel stages half of its
   // 256-wide N tile per CTA.
   const int b_rows = paired ? pair::kBN / 2 : bn;
