@@ -269,6 +269,8 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     result["e2e"] = run_e2e(args, mesh, meta, convs, stream, ws)
+    if not args.no_sweep:
+        result["mesh_sweep"] = mesh_sweep(ws, rank, dev, stream, hbm_peak)
     if ws == 1:
         result["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
@@ -384,6 +386,90 @@ def run_e2e(args, mesh, meta, convs, stream, ws=1):
                     "(replicas of an RR block read once), 3 streams, double-buffered shards"}
 
 
+# ----------------------------------------------------------------------------- configs 3/4
+CONFIG3_SPECS = ["S01R", "S0S1", "S1S0", "RS01", "RR"]
+
+
+def _sweep_cases(mesh_shape):
+    """BASELINE configs 3/4 conversions for a mesh: every ordered pair among
+    the config-3 specs on [8192, 8192] bf16 (2x4; the same specs on 2x2), and
+    the config-4 chains on 2x2x2."""
+    if len(mesh_shape) == 2:
+        return [((8192, 8192), a, b) for a in CONFIG3_SPECS for b in CONFIG3_SPECS if a != b]
+    return [((8192, 8192), "S012R", "RS012"), ((8192, 8192), "RS012", "S012R"),
+            ((512, 512, 256), "S0S1R", "RS1S0"), ((512, 512, 256), "RS1S0", "S0S1R")]
+
+
+def mesh_sweep(ws, rank, dev, stream, hbm_peak, iters=20):
+    """configs 3/4 (2-D / 3-D meshes) through the same public API.
+    N = 1: 2x4 and 2x2x2 simulated on one GPU -> pack HBM GB/s vs the
+    measured copy peak. N = 4 / 8: the real meshes ([2,2]; [2,4] and [2,2,2])
+    over NCCL -> bus GB/s per GPU = max over ranks of the minimal one-shot
+    bytes a rank receives / max-over-ranks time, vs the
+    measured 770 GB/s peer copy. Collapsed exchanges, events on the launch
+    stream."""
+    import torch
+
+    from paper_2302_02599_b200 import ShardingSpec, TensorMeta, find_transform_path
+    from paper_2302_02599_b200.runtime import Mesh
+
+    meshes = {1: [[2, 4], [2, 2, 2]], 4: [[2, 2]], 8: [[2, 4], [2, 2, 2]]}.get(ws, [])
+    rows = []
+    for ms in meshes:
+        mesh = Mesh.local(ms, device=dev.index or 0) if ws == 1 else Mesh.from_process_group(ms)
+        for shape, a, b in _sweep_cases(ms):
+            meta = TensorMeta(shape, 2)
+            s, t = ShardingSpec.parse(a, len(ms)), ShardingSpec.parse(b, len(ms))
+            path = find_transform_path(s, t, mesh.geo, meta)
+            ins = [torch.empty(s.local_shape(meta, mesh.geo), dtype=torch.bfloat16, device=dev)
+                   for _ in range(mesh.num_local)]
+            outs = [torch.empty(t.local_shape(meta, mesh.geo), dtype=torch.bfloat16, device=dev)
+                    for _ in range(mesh.num_local)]
+            conv = mesh.prepare(path, meta, fuse=True)
+            tr = mesh.exchange_traffic(s, t, meta)
+            for _ in range(3):
+                conv(ins, outs, stream=stream)
+            if ws > 1:
+                import torch.distributed as dist
+
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(iters):
+                conv(ins, outs, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_t = e0.elapsed_time(e1) / iters
+            row = {"mesh": ms, "tensor": list(shape), "conversion": f"{a}->{b}",
+                   "ref_steps": len(path.steps), "us": None}
+            if ws == 1:
+                nbytes = tr["hbm_read"] + tr["hbm_write"]
+                row.update(us=round(ms_t * 1e3, 2), hbm_bytes=nbytes,
+                           gbs=round(nbytes / ms_t / 1e6, 1),
+                           frac=round(nbytes / ms_t / 1e6 / hbm_peak, 3))
+            else:
+                import torch.distributed as dist
+
+                v = torch.tensor([ms_t, float(tr["wire_in"])], device=dev, dtype=torch.float64)
+                dist.all_reduce(v, op=dist.ReduceOp.MAX)
+                ms_t, wire = float(v[0]), float(v[1])
+                row.update(us=round(ms_t * 1e3, 2), bus_bytes=int(wire),
+                           bus_gbs=round(wire / ms_t / 1e6, 1) if wire else None,
+                           frac=round(wire / ms_t / 1e6 / 770.0, 3) if wire else None)
+            rows.append(row)
+            conv.close()
+            del ins, outs
+        mesh.close()
+        torch.cuda.empty_cache()
+    fr = [r["frac"] for r in rows if r.get("frac") is not None]
+    return {"rows": rows, "frac_min": min(fr) if fr else None,
+            "frac_median": statistics.median(fr) if fr else None,
+            "peak": hbm_peak if ws == 1 else 770.0,
+            "kind": "pack HBM GB/s (simulated mesh)" if ws == 1 else
+                    "bus GB/s per GPU (minimal one-shot bytes, NCCL)"}
+
+
 # ----------------------------------------------------------------------------- CPU legs
 def _cpu_sample_shape():
     # bounded sample of the same workload: 1/16 of the rows (64 MiB global)
@@ -486,6 +572,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs 3/4 mesh sweep")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
