@@ -185,6 +185,21 @@ int apl_peer_alloc(apl_mesh* mesh, size_t bytes, void** ptr, uint8_t* handle64);
 /* Maps another process's exported buffer; closed with the mesh. */
 int apl_peer_open(apl_mesh* mesh, const uint8_t* handle64, void** ptr);
 
+/* Device-side epoch flags for peer exchanges without host barriers. Every
+ * rank owns a uint32 flag array of 2 x num_ranks entries (apl_peer_alloc +
+ * zero fill; peers map it with apl_peer_open). apl_peer_flags_store writes
+ * `epoch` into entry `slot` of each of the n mapped arrays (system-scope
+ * release after a system fence; stream-ordered after the work it announces).
+ * apl_peer_flags_wait blocks the stream until local_flags[slots[i]] >= epoch
+ * for all i (acquire; traps with a launch error after timeout_ms instead of
+ * hanging). Protocol at epoch e on rank r (see PeerMesh.exchange_async):
+ * store ready (slot r) -> wait ready of the senders -> apl_run_pull -> store
+ * done (slot P + r); before overwriting the source: wait done of the readers. */
+int apl_peer_flags_store(void* const* remote_flags, int n, int slot, uint32_t epoch,
+                         void* stream);
+int apl_peer_flags_wait(const void* local_flags, const int32_t* slots, int n, uint32_t epoch,
+                        uint32_t timeout_ms, void* stream);
+
 /* Fused collapsed exchange over peer memory: ONE kernel pulls every piece of
  * this rank's target shard straight out of the senders' source shards
  * (peer_in[r] = rank r's source shard mapped into this process, this rank's

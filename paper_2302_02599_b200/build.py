@@ -52,6 +52,7 @@ CUDA_SRCS = [
     CSRC / "kernels" / "box_copy.cu",
     CSRC / "kernels" / "bulk_copy.cu",
     CSRC / "kernels" / "reduce.cu",
+    CSRC / "kernels" / "peer_sync.cu",
     CSRC / "kernels" / "gemm_tcgen05.cu",
 ]
 

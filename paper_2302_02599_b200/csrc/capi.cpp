@@ -479,6 +479,37 @@ int apl_run_pull(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt, const
   });
 }
 
+int apl_peer_flags_store(void* const* remote_flags, int n, int slot, uint32_t epoch,
+                         void* stream) {
+  return guarded([&] {
+    need(n >= 0 && n <= 64, "at most 64 flag arrays");
+    need(remote_flags || n == 0, "null flag table");
+    need(slot >= 0, "bad slot");
+    std::vector<uint32_t*> p(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      need(remote_flags[i] != nullptr, "null flag array");
+      p[static_cast<size_t>(i)] = static_cast<uint32_t*>(remote_flags[i]);
+    }
+    apl::check_cuda(apl::launch_flag_store(p.data(), n, slot, epoch,
+                                           static_cast<cudaStream_t>(stream)),
+                    "flag store launch");
+  });
+}
+
+int apl_peer_flags_wait(const void* local_flags, const int32_t* slots, int n, uint32_t epoch,
+                        uint32_t timeout_ms, void* stream) {
+  return guarded([&] {
+    need(n >= 0 && n <= 64, "at most 64 flags");
+    need(local_flags && (slots || n == 0), "null argument");
+    std::vector<int> s(slots, slots + n);
+    for (int v : s) need(v >= 0, "bad slot");
+    apl::check_cuda(apl::launch_flag_wait(static_cast<const uint32_t*>(local_flags), s.data(), n,
+                                          epoch, uint64_t{timeout_ms} * 1000000ull,
+                                          static_cast<cudaStream_t>(stream)),
+                    "flag wait launch");
+  });
+}
+
 int apl_mesh_destroy(apl_mesh* mesh) {
   return guarded([&] { delete mesh; });
 }

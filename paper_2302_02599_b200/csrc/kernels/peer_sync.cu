@@ -1,0 +1,92 @@
+// Device-side epoch flags for the peer-memory exchange (no host barrier, no
+// NCCL): every rank owns a small IPC-exported flag array that its peers
+// write into over NVLink.
+//
+//   flags[r][slot]  slot p          : "rank p's source shard of epoch e is written"
+//                   slot P + p      : "rank p finished reading epoch e's sources"
+//
+// An exchange at epoch e on rank r is, in stream order:
+//   store(ready, e) to every peer -> wait(all ready >= e) -> pull kernel ->
+//   store(done, e) to every peer
+// and before r overwrites its source for epoch e+1: wait(all done >= e).
+// Stores are st.release.sys after a system fence (the producer's writes and
+// the pull's reads completed at the preceding kernel boundary); waits spin on
+// ld.acquire.sys with a nanosleep back-off and trap after a timeout instead of
+// hanging the GPU.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+namespace apl {
+
+extern std::atomic<uint64_t> g_launches;
+
+constexpr int kMaxFlagPeers = 64;
+
+struct FlagPtrs {
+  uint32_t* p[kMaxFlagPeers];
+};
+struct FlagSlots {
+  int s[kMaxFlagPeers];
+};
+
+namespace {
+
+__global__ void flag_store_kernel(const __grid_constant__ FlagPtrs ptrs, int n, int slot,
+                                  uint32_t epoch) {
+  __threadfence_system();
+  const int i = threadIdx.x;
+  if (i < n)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(ptrs.p[i] + slot), "r"(epoch)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void flag_wait_kernel(const uint32_t* flags, const __grid_constant__ FlagSlots slots,
+                                 int n, uint32_t epoch, uint64_t timeout_ns) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    const uint32_t* f = flags + slots.s[i];
+    const uint64_t t0 = global_ns();
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (static_cast<int32_t>(v - epoch) >= 0) break;  // wrap-safe v >= epoch
+      __nanosleep(256);
+      if (global_ns() - t0 > timeout_ns) __trap();  // a lost peer: fail, do not hang
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+cudaError_t launch_flag_store(uint32_t* const* remote, int n, int slot, uint32_t epoch,
+                              cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kMaxFlagPeers) return cudaErrorInvalidValue;
+  FlagPtrs p{};
+  for (int i = 0; i < n; ++i) p.p[i] = remote[i];
+  flag_store_kernel<<<1, 64, 0, stream>>>(p, n, slot, epoch);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flag_wait(const uint32_t* flags, const int* slots, int n, uint32_t epoch,
+                             uint64_t timeout_ns, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kMaxFlagPeers) return cudaErrorInvalidValue;
+  FlagSlots s{};
+  for (int i = 0; i < n; ++i) s.s[i] = slots[i];
+  flag_wait_kernel<<<1, 64, 0, stream>>>(flags, s, n, epoch, timeout_ns);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+}  // namespace apl

@@ -38,6 +38,11 @@ cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int gr
                                    cudaStream_t stream);
 uint64_t launch_count();
 cudaError_t launch_gelu_inplace(void* buf, size_t count, int dtype, cudaStream_t stream);
+// Peer-exchange epoch flags (peer_sync.cu).
+cudaError_t launch_flag_store(uint32_t* const* remote, int n, int slot, uint32_t epoch,
+                              cudaStream_t stream);
+cudaError_t launch_flag_wait(const uint32_t* flags, const int* slots, int n, uint32_t epoch,
+                             uint64_t timeout_ns, cudaStream_t stream);
 cudaError_t launch_gelu(const void* x, void* y, size_t count, int dtype, cudaStream_t stream);
 cudaError_t launch_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int dtype,
                                  cudaStream_t stream);

@@ -348,17 +348,35 @@ class PeerMesh:
         self.shard_bytes = shard_bytes
         self.local_ptr = ptr.value
         self.local = torch.as_tensor(_CudaArray(ptr.value, shard_bytes), device=f"cuda:{device}")
-        handles = [None] * self.geo.num_devices()
-        dist.all_gather_object(handles, bytes(handle), group=group)
-        self.peer_ptrs = []
-        for r, hb in enumerate(handles):
+        # epoch flags: [ready x P][done x P] uint32, written by the peers
+        P = self.geo.num_devices()
+        fptr, fhandle = C.c_void_p(), (C.c_uint8 * 64)()
+        check(A.lib().apl_peer_alloc(h, max(8 * P, 256), C.byref(fptr), fhandle))
+        self.flags = torch.as_tensor(_CudaArray(fptr.value, 8 * P),
+                                     device=f"cuda:{device}").view(torch.int32)
+        self.flags.zero_()
+        torch.cuda.synchronize(device)
+        self.epoch = 0
+        handles = [None] * P
+        dist.all_gather_object(handles, (bytes(handle), bytes(fhandle)), group=group)
+        self.peer_ptrs, flag_ptrs = [], []
+        for r, (hb, fb) in enumerate(handles):
             if r == rank:
                 self.peer_ptrs.append(ptr.value)
+                flag_ptrs.append(fptr.value)
                 continue
-            p = C.c_void_p()
+            p, q = C.c_void_p(), C.c_void_p()
             check(A.lib().apl_peer_open(h, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
+            check(A.lib().apl_peer_open(h, (C.c_uint8 * 64).from_buffer_copy(fb), C.byref(q)))
             self.peer_ptrs.append(p.value)
+            flag_ptrs.append(q.value)
         self._table = (C.c_void_p * len(self.peer_ptrs))(*self.peer_ptrs)
+        others = [q for q in range(P) if q != rank]
+        self._peer_flags = (C.c_void_p * len(others))(*[flag_ptrs[q] for q in others])
+        self._n_others = len(others)
+        self._ready_slots = (C.c_int32 * max(1, len(others)))(*others)
+        self._done_slots = (C.c_int32 * max(1, len(others)))(*[P + q for q in others])
+        self.timeout_ms = 60000
 
     def shard(self, shape, dtype) -> torch.Tensor:
         """This rank's exported source shard as a typed tensor view."""
@@ -391,6 +409,33 @@ class PeerMesh:
         self.pull(src, tgt, meta, out)
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)
+
+    def exchange_async(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta,
+                       out: torch.Tensor, stream=None) -> int:
+        """Stream-ordered exchange synchronised on the device, no host
+        barrier: announce this rank's source (ready flag at every peer), wait
+        until every peer announced theirs, pull (one kernel), announce that
+        this rank finished reading. Returns the epoch. Call wait_readers()
+        before overwriting the exported source for the next epoch."""
+        self.epoch += 1
+        e, r, P = self.epoch, self.rank, self.geo.num_devices()
+        sh = _stream_handle(stream)
+        lib = A.lib()
+        check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, r, e, sh))
+        check(lib.apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), self._ready_slots,
+                                      self._n_others, e, self.timeout_ms, sh))
+        self.pull(src, tgt, meta, out, stream=stream)
+        check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, P + r, e, sh))
+        return e
+
+    def wait_readers(self, stream=None) -> None:
+        """Stream-ordered: block until every peer finished reading this
+        rank's source of the last epoch (then it may be overwritten)."""
+        if self.epoch == 0:
+            return
+        check(A.lib().apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), self._done_slots,
+                                          self._n_others, self.epoch, self.timeout_ms,
+                                          _stream_handle(stream)))
 
     def close(self) -> None:
         if getattr(self, "_h", None):

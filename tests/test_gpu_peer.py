@@ -79,3 +79,77 @@ def test_peer_pull_exchange_multiprocess(cuda, world):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert len(res) == world * len(CASES[world])
     assert all(ok for *_, ok in res), [r for r in res if not r[-1]]
+
+
+EPOCH_CASES = {
+    4: [([2, 2], (1024, 512), 2, "S0R", "RS0"), ([4], (2048, 256), 4, "S0R", "RR")],
+    8: [([2, 4], (1024, 1024), 2, "S01R", "S1S0"), ([2, 2, 2], (1024, 512), 2, "S012R", "RS012")],
+}
+EPOCHS = 3
+
+
+def _epoch_worker(rank, world, port, cases, q):
+    """Repeated exchanges synchronised only on the device: each epoch the
+    rank rewrites its exported source (after wait_readers) with a different
+    tensor, then exchange_async; no host barrier between epochs."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from oracle import data as O
+    from paper_2302_02599_b200 import ShardingSpec, TensorMeta
+    from paper_2302_02599_b200.runtime import PeerMesh
+
+    dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}
+    npdt = {1: np.uint8, 2: np.int16, 4: np.int32}
+    try:
+        for mesh_shape, shape, eb, a, b in cases:
+            mr = len(mesh_shape)
+            meta = TensorMeta(shape, eb)
+            nbytes = int(np.prod(shape)) * eb
+            pm = PeerMesh(mesh_shape, rank, 0, nbytes)
+            srcs, wants = [], []
+            for e in range(EPOCHS):  # stage every epoch's source on the device up front
+                g = O.fill_global(shape, eb, seed=1000 + e)
+                mine = O.local(g, O.parse_spec(a, mr), mesh_shape, rank)
+                srcs.append(torch.from_numpy(mine.view(npdt[eb])).cuda())
+                wants.append(O.local(g, O.parse_spec(b, mr), mesh_shape, rank))
+            torch.cuda.synchronize()
+            dist.barrier()  # setup only; the epochs below never meet on the host
+            outs = []
+            for e in range(EPOCHS):
+                pm.wait_readers()
+                pm.shard(srcs[e].shape, dt[eb]).copy_(srcs[e])
+                out = torch.full(wants[e].shape, -1, dtype=dt[eb], device="cuda:0")
+                pm.exchange_async(ShardingSpec.parse(a, mr), ShardingSpec.parse(b, mr), meta, out)
+                outs.append(out)
+            pm.wait_readers()
+            torch.cuda.synchronize()
+            for e in range(EPOCHS):
+                q.put((rank, a, b, e, outs[e].cpu().numpy().tobytes() == wants[e].tobytes()))
+            dist.barrier()
+            pm.close()
+            dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_peer_exchange_device_synchronised_epochs(cuda, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_epoch_worker, args=(r, world, port, EPOCH_CASES[world], q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    res = []
+    while not q.empty():
+        res.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert len(res) == world * len(EPOCH_CASES[world]) * EPOCHS
+    assert all(ok for *_, ok in res), [r for r in res if not r[-1]]
