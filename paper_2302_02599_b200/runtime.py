@@ -428,6 +428,11 @@ class PeerMesh:
         check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, P + r, e, sh))
         return e
 
+    def exchange_traffic(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta) -> dict:
+        """This rank's bytes of the src->tgt exchange (wire_in = bytes pulled
+        from peers)."""
+        return Mesh.exchange_traffic(self, src, tgt, meta)
+
     def wait_readers(self, stream=None) -> None:
         """Stream-ordered: block until every peer finished reading this
         rank's source of the last epoch (then it may be overwritten)."""
