@@ -200,6 +200,23 @@ int apl_peer_flags_store(void* const* remote_flags, int n, int slot, uint32_t ep
 int apl_peer_flags_wait(const void* local_flags, const int32_t* slots, int n, uint32_t epoch,
                         uint32_t timeout_ms, void* stream);
 
+/* Fused split-k GEMM + all-reduce over peer memory (Megatron fc2 /
+ * split-k strategies on a peer mesh group of P <= 8 ranks), two kernels:
+ *  apl_peer_gemm_scatter: C_r = A . B (bf16 in, fp32 partial) with row block
+ *    q of the partial stored straight into owner q's staging slab for this
+ *    rank (owner_slabs[q], peer-mapped): the reduce-scatter's transfer is
+ *    the GEMM epilogue, overlapping the next tiles' MMAs. M / P must be a
+ *    multiple of 128.
+ *  apl_peer_reduce_gather: the owner sums its P received slabs (rank order)
+ *    and writes the result into every rank's output rows (outs[q], peer-
+ *    mapped): the all-gather as peer stores. Every replica is bit-identical.
+ * Ordering between the two (and across epochs) uses apl_peer_flags_*. */
+int apl_peer_gemm_scatter(const void* A, const void* B, void* const* owner_slabs, int owners,
+                          int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+                          int b_layout, void* stream);
+int apl_peer_reduce_gather(const float* staging, int P, int64_t slab_elems, void* const* outs,
+                           int nout, int out_dtype, void* stream);
+
 /* Fused collapsed exchange over peer memory: ONE kernel pulls every piece of
  * this rank's target shard straight out of the senders' source shards
  * (peer_in[r] = rank r's source shard mapped into this process, this rank's

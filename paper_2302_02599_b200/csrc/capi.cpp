@@ -510,6 +510,39 @@ int apl_peer_flags_wait(const void* local_flags, const int32_t* slots, int n, ui
   });
 }
 
+int apl_peer_gemm_scatter(const void* A, const void* B, void* const* owner_slabs, int owners,
+                          int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+                          int b_layout, void* stream) {
+  return guarded([&] {
+    need(A && B && owner_slabs, "null argument");
+    need(owners >= 1 && owners <= 8, "1..8 owners");
+    need(b_layout == APL_B_NK || b_layout == APL_B_KN, "unknown B layout");
+    need(M > 0 && N > 0 && K > 0 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX,
+         "extents out of range");
+    need(M % owners == 0 && (M / owners) % 128 == 0, "M / owners must be a multiple of 128");
+    for (int q = 0; q < owners; ++q) need(owner_slabs[q] != nullptr, "null owner slab");
+    apl::check_cuda(apl::gemm_bf16_scatter(A, B, owner_slabs, owners, static_cast<int>(M),
+                                           static_cast<int>(N), static_cast<int>(K),
+                                           static_cast<int>(lda), static_cast<int>(ldb),
+                                           b_layout == APL_B_KN, static_cast<cudaStream_t>(stream)),
+                    "GEMM scatter launch");
+  });
+}
+
+int apl_peer_reduce_gather(const float* staging, int P, int64_t slab_elems, void* const* outs,
+                           int nout, int out_dtype, void* stream) {
+  return guarded([&] {
+    need(staging && outs, "null argument");
+    need(P >= 1 && nout >= 1 && nout <= 8, "bad group size");
+    need(slab_elems > 0 && slab_elems % 4 == 0, "slab must hold a multiple of 4 elements");
+    need(out_dtype == APL_F32 || out_dtype == APL_BF16, "output dtype must be f32 or bf16");
+    apl::check_cuda(apl::launch_reduce_gather(staging, P, slab_elems, outs, nout,
+                                              out_dtype == APL_F32,
+                                              static_cast<cudaStream_t>(stream)),
+                    "reduce-gather launch");
+  });
+}
+
 int apl_mesh_destroy(apl_mesh* mesh) {
   return guarded([&] { delete mesh; });
 }

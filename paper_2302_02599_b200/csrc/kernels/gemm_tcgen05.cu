@@ -292,6 +292,11 @@ struct GemmArgs {
   const void* aux[kMaxBatch];  // kEpiDGelu: pre-activation per output problem
   int count, M, N, K, ldc, ldaux;
   int reduce, fan;
+  // > 0: fused reduce-scatter epilogue (single problem). Rows are owned in
+  // blocks of scatter_rows; a tile's rows go to c[owner] (the owner's
+  // staging slab for this rank, typically a peer-mapped pointer), so the
+  // partial tile crosses NVLink while the next tile's MMAs run.
+  int scatter_rows;
 };
 
 template <int BN, int kEpi, bool kOutF32, bool kBMN, bool kAMN>
@@ -417,8 +422,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = local & 1;
       const int g = t / per_problem, lt = t % per_problem;
       const int m0 = (lt / n_tiles) * kBM, n0 = (lt % n_tiles) * BN;
-      void* const* const outs = args.c + g * args.fan;
-      const int row = m0 + quarter * 32 + lane;
+      void* const* outs = args.c + g * args.fan;
+      int row = m0 + quarter * 32 + lane;
+      int rows = M, fan = args.fan;
+      if (args.scatter_rows > 0) {
+        const int owner = m0 / args.scatter_rows;
+        outs = args.c + owner;
+        row -= owner * args.scatter_rows;
+        rows = args.scatter_rows;
+        fan = 1;
+      }
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
@@ -427,8 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[16];
         tmem_ld16(lane_addr + uint32_t(c), r);
         const int col = n0 + c;
-        for (int j = 0; j < args.fan; ++j)
-          store_chunk<kEpi, kOutF32>(outs[j], ldc, M, N, row, col, r, args.aux[g], args.ldaux);
+        for (int j = 0; j < fan; ++j)
+          store_chunk<kEpi, kOutF32>(outs[j], ldc, rows, N, row, col, r, args.aux[g], args.ldaux);
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -886,6 +899,41 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
                               cudaStream_t stream) {
   return gemm_bf16_grouped(A, B, C, groups, reduce, fan, M, N, K, lda, ldb, ldc, b_kn, out_f32,
                            gelu ? kEpiGelu : kEpiNone, false, nullptr, 0, stream);
+}
+
+// Fused GEMM + reduce-scatter send: C = A . B (one problem) with row block
+// q (M / owners rows) of the fp32 partial written to owner_slabs[q] (the
+// owner's staging slab reserved for this rank; peer-mapped pointers on a
+// peer mesh). M / owners must be a multiple of the 128-row tile.
+cudaError_t gemm_bf16_scatter(const void* A, const void* B, void* const* owner_slabs, int owners,
+                              int M, int N, int K, int lda, int ldb, bool b_kn,
+                              cudaStream_t stream) {
+  if (owners < 1 || owners > kMaxBatch || M % owners || (M / owners) % kBM)
+    return cudaErrorInvalidValue;
+  if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
+    return cudaErrorInvalidValue;
+  GemmArgs args;
+  std::memset(&args, 0, sizeof(args));
+  args.count = 1;
+  args.reduce = 1;
+  args.fan = 1;
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.ldc = N;
+  args.scatter_rows = M / owners;
+  const int bn = (N >= 256 && N % 256 == 0) ? 256 : 128;
+  if (!make_map(&args.a[0], A, M, K, lda, kBM)) return cudaErrorInvalidValue;
+  const bool okb = b_kn ? make_map(&args.b[0], B, K, N, ldb, kBK, 64)
+                        : make_map(&args.b[0], B, N, K, ldb, bn);
+  if (!okb) return cudaErrorInvalidValue;
+  for (int q = 0; q < owners; ++q) args.c[q] = owner_slabs[q];
+  if (b_kn)
+    return bn == 256 ? dispatch<256, true>(args, true, kEpiNone, false, stream)
+                     : dispatch<128, true>(args, true, kEpiNone, false, stream);
+  return bn == 256 ? dispatch<256, false>(args, true, kEpiNone, false, stream)
+                   : dispatch<128, false>(args, true, kEpiNone, false, stream);
 }
 
 cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,

@@ -13,8 +13,10 @@
 // the pull's reads completed at the preceding kernel boundary); waits spin on
 // ld.acquire.sys with a nanosleep back-off and trap after a timeout instead of
 // hanging the GPU.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 
@@ -65,7 +67,54 @@ __global__ void flag_wait_kernel(const uint32_t* flags, const __grid_constant__ 
   __syncthreads();
 }
 
+struct OutPtrs {
+  void* p[8];
+};
+
+// Owner side of the fused all-reduce: sum the P fp32 partial slabs this rank
+// received (in rank order: deterministic, and only the owner computes its
+// rows, so every replica gets identical bytes) and write the result into
+// every rank's output at this rank's rows (peer stores = the all-gather).
+__global__ void __launch_bounds__(256) reduce_gather_kernel(const float* __restrict__ staging,
+                                                            int P, int64_t slab4,
+                                                            const __grid_constant__ OutPtrs outs,
+                                                            int nout, int out_f32) {
+  const float4* st = reinterpret_cast<const float4*>(staging);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < slab4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 a = __ldg(st + i);
+    for (int r = 1; r < P; ++r) {
+      const float4 b = __ldg(st + r * slab4 + i);
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    if (out_f32) {
+      for (int q = 0; q < nout; ++q) reinterpret_cast<float4*>(outs.p[q])[i] = a;
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+      uint2 v;
+      v.x = *reinterpret_cast<uint32_t*>(&lo);
+      v.y = *reinterpret_cast<uint32_t*>(&hi);
+      for (int q = 0; q < nout; ++q) reinterpret_cast<uint2*>(outs.p[q])[i] = v;
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_reduce_gather(const float* staging, int P, int64_t slab_elems,
+                                 void* const* outs, int nout, bool out_f32, cudaStream_t stream) {
+  if (P < 1 || nout < 1 || nout > 8 || slab_elems % 4) return cudaErrorInvalidValue;
+  OutPtrs o{};
+  for (int q = 0; q < nout; ++q) o.p[q] = outs[q];
+  const int64_t slab4 = slab_elems / 4;
+  const int grid = static_cast<int>(std::min<int64_t>((slab4 + 255) / 256, 148 * 8));
+  reduce_gather_kernel<<<grid, 256, 0, stream>>>(staging, P, slab4, o, nout, out_f32 ? 1 : 0);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_flag_store(uint32_t* const* remote, int n, int slot, uint32_t epoch,
                               cudaStream_t stream) {

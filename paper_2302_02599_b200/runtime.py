@@ -428,6 +428,78 @@ class PeerMesh:
         check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, P + r, e, sh))
         return e
 
+    def shared_buffer(self, nbytes: int):
+        """Collective: allocate and export a device buffer on every rank and
+        map every peer's. Returns (this rank's buffer as a uint8 tensor,
+        [device pointer of rank q's buffer, mapped here, for every q])."""
+        import torch.distributed as dist
+
+        ptr, handle = C.c_void_p(), (C.c_uint8 * 64)()
+        check(A.lib().apl_peer_alloc(self._h, max(nbytes, 16), C.byref(ptr), handle))
+        local = torch.as_tensor(_CudaArray(ptr.value, nbytes), device=f"cuda:{self.device}")
+        handles = [None] * self.geo.num_devices()
+        dist.all_gather_object(handles, bytes(handle), group=self.group)
+        ptrs = []
+        for q, hb in enumerate(handles):
+            if q == self.rank:
+                ptrs.append(ptr.value)
+                continue
+            p = C.c_void_p()
+            check(A.lib().apl_peer_open(self._h, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
+            ptrs.append(p.value)
+        return local, ptrs
+
+    def matmul_allreduce(self, a: torch.Tensor, b: torch.Tensor, out_dtype=torch.bfloat16,
+                         b_layout: str = "kn", stream=None) -> torch.Tensor:
+        """Split-k matmul over all ranks of this peer mesh with its all-reduce
+        fused in (Megatron fc2, reference split-k strategies, intraop.cpp:
+        141-234 with the partial-sum all-reduce of planner.cpp:263-282):
+        C = sum_r A_r . B_r on every rank, bit-identical replicas.
+
+        Two kernels instead of GEMM + a collective: the GEMM's epilogue stores
+        each row block of its fp32 partial straight into the owning rank's
+        staging slab (reduce-scatter traffic overlapping the MMAs), then each
+        owner sums its slabs and stores its rows into every rank's output
+        (the all-gather as peer stores); device-side epoch flags order them.
+        Returns this rank's exported output (valid until the next call with
+        the same shape)."""
+        P, r = self.geo.num_devices(), self.rank
+        if P > 8:
+            raise ValueError("fused peer all-reduce groups hold at most 8 ranks")
+        M, K = a.shape
+        N = b.shape[1] if b_layout == "kn" else b.shape[0]
+        eb = torch.empty((), dtype=out_dtype).element_size()
+        if M % P or (M // P) % 128:
+            raise ValueError("M / ranks must be a multiple of 128")
+        rpo = M // P
+        key = (M, N, out_dtype)
+        bufs = getattr(self, "_ar_bufs", None)
+        if bufs is None:
+            bufs = self._ar_bufs = {}
+        if key not in bufs:
+            staging, staging_peers = self.shared_buffer(P * rpo * N * 4)
+            c_local, c_peers = self.shared_buffer(M * N * eb)
+            slabs = (C.c_void_p * P)(*[sp + r * rpo * N * 4 for sp in staging_peers])
+            outs = (C.c_void_p * P)(*[cp + r * rpo * N * eb for cp in c_peers])
+            bufs[key] = (staging, c_local.view(out_dtype).view(M, N), slabs, outs)
+        staging, c_out, slabs, outs = bufs[key]
+        self.epoch += 1
+        e = self.epoch
+        sh = _stream_handle(stream)
+        lib = A.lib()
+        check(lib.apl_peer_gemm_scatter(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), slabs, P,
+                                        M, N, K, a.stride(0), b.stride(0),
+                                        A.B_KN if b_layout == "kn" else A.B_NK, sh))
+        check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, r, e, sh))
+        check(lib.apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), self._ready_slots,
+                                      self._n_others, e, self.timeout_ms, sh))
+        check(lib.apl_peer_reduce_gather(C.c_void_p(staging.data_ptr()), P, rpo * N, outs, P,
+                                         _DTYPE_CODE[out_dtype], sh))
+        check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, P + r, e, sh))
+        check(lib.apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), self._done_slots,
+                                      self._n_others, e, self.timeout_ms, sh))
+        return c_out
+
     def exchange_traffic(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta) -> dict:
         """This rank's bytes of the src->tgt exchange (wire_in = bytes pulled
         from peers)."""

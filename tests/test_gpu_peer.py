@@ -153,3 +153,60 @@ def test_peer_exchange_device_synchronised_epochs(cuda, world):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert len(res) == world * len(EPOCH_CASES[world]) * EPOCHS
     assert all(ok for *_, ok in res), [r for r in res if not r[-1]]
+
+
+def _allreduce_worker(rank, world, port, q):
+    """Megatron fc2 (split-k over all ranks) with the GEMM and its all-reduce
+    fused over peer memory, two epochs with fresh operands."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2302_02599_b200.runtime import PeerMesh
+
+    try:
+        M, Kt, N = 1024, 2048, 512
+        kr = Kt // world
+        pm = PeerMesh([world], rank, 0, 16)
+        for epoch in range(2):
+            g = torch.Generator(device="cuda").manual_seed(100 + epoch)
+            x = torch.randn(M, Kt, device="cuda", generator=g).bfloat16()
+            w = (torch.randn(Kt, N, device="cuda", generator=g) / Kt ** 0.5).bfloat16()
+            a = x[:, rank * kr:(rank + 1) * kr].contiguous()
+            b = w[rank * kr:(rank + 1) * kr].contiguous()
+            for out_dtype in (torch.bfloat16, torch.float32):
+                c = pm.matmul_allreduce(a, b, out_dtype=out_dtype)
+                torch.cuda.synchronize()
+                ref = x.double() @ w.double()
+                err = ((c.double() - ref).abs().max() / ref.abs().max()).item()
+                tol = 2e-2 if out_dtype == torch.bfloat16 else 1e-5
+                digest = c.view(torch.uint8).sum(dtype=torch.int64).item()
+                q.put((rank, epoch, str(out_dtype), err <= tol, err, digest))
+        dist.barrier()
+        pm.close()
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_fused_gemm_allreduce_over_peer_memory(cuda, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_allreduce_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    res = []
+    while not q.empty():
+        res.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert len(res) == world * 4
+    assert all(r[3] for r in res), [r for r in res if not r[3]]
+    for epoch in range(2):  # every rank holds the same bytes
+        for dt in ("torch.bfloat16", "torch.float32"):
+            assert len({r[5] for r in res if r[1] == epoch and r[2] == dt}) == 1
