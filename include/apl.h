@@ -288,6 +288,7 @@ int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* 
 /* ---- sharded matmul strategies (reference intraop.cpp:141-234) -------- */
 #define APL_EPI_NONE 0
 #define APL_EPI_GELU 1 /* exact erf GELU, applied after any partial-sum reduction */
+#define APL_EPI_GELU_SAVE 3 /* GELU, and the pre-activation kept in aux (training) */
 
 /* One SPMD matmul strategy of the reference catalog: C[..m.., n] = A[..m.., k]
  * . B[k, n]; specs are on the LOGICAL tensors exactly as the reference writes
@@ -336,6 +337,14 @@ int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
                        const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
                        const void* const* B, void* const* C, int b_layout, int out_dtype,
                        int epilogue, void* stream);
+
+/* apl_sharded_matmul with an aux buffer per local device: APL_EPI_GELU_SAVE
+ * (bf16 C) writes GELU(acc) to C and the pre-activation acc to aux -- one
+ * pass over the tile for a training forward that needs both. */
+int apl_sharded_matmul_ex(apl_mesh* mesh, const apl_matmul_strategy* strategy,
+                          const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
+                          const void* const* B, void* const* C, int b_layout, int out_dtype,
+                          int epilogue, void* const* aux, void* stream);
 
 /* Exact-erf GELU in place over `count` elements (elementwise-unary nodes of
  * a plan that could not be fused into a GEMM epilogue). */

@@ -19,7 +19,7 @@ OK, ERR_SCHEMA, ERR_AXIS, ERR_SHAPE, ERR_RANK, ERR_INFEASIBLE, ERR_CUDA, ERR_NCC
 FUSE_CHAIN = 1
 STEPWISE = 0
 F32, BF16, F16 = 0, 1, 2
-EPI_NONE, EPI_GELU, EPI_DGELU = 0, 1, 2
+EPI_NONE, EPI_GELU, EPI_DGELU, EPI_GELU_SAVE = 0, 1, 2, 3
 B_NK, B_KN = 0, 1
 
 
@@ -130,6 +130,9 @@ _SIGS = {
     "apl_sharded_matmul": (C.c_int, [C.c_void_p, P(MatmulStrategyC), P(Meta), P(Meta),
                                      P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
                                      C.c_int, C.c_int, C.c_void_p]),
+    "apl_sharded_matmul_ex": (C.c_int, [C.c_void_p, P(MatmulStrategyC), P(Meta), P(Meta),
+                                        P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
+                                        C.c_int, C.c_int, P(C.c_void_p), C.c_void_p]),
     "apl_gelu_inplace": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "apl_gelu": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "apl_gelu_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int,

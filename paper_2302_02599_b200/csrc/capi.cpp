@@ -796,15 +796,18 @@ int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, i
   });
 }
 
-int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
-                       const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
-                       const void* const* B, void* const* C, int b_layout, int out_dtype,
-                       int epilogue, void* stream) {
+int apl_sharded_matmul_ex(apl_mesh* mesh, const apl_matmul_strategy* strategy,
+                          const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
+                          const void* const* B, void* const* C, int b_layout, int out_dtype,
+                          int epilogue, void* const* aux, void* stream) {
   return guarded([&] {
     need(mesh && strategy && A && B && C, "null argument");
     need(b_layout == APL_B_NK || b_layout == APL_B_KN, "unknown B layout");
     need(out_dtype == APL_F32 || out_dtype == APL_BF16, "output dtype must be f32 or bf16");
-    need(epilogue == APL_EPI_NONE || epilogue == APL_EPI_GELU, "unknown epilogue");
+    need(epilogue == APL_EPI_NONE || epilogue == APL_EPI_GELU || epilogue == APL_EPI_GELU_SAVE,
+         "unknown epilogue");
+    need(epilogue != APL_EPI_GELU_SAVE || (aux != nullptr && out_dtype == APL_BF16),
+         "APL_EPI_GELU_SAVE needs aux buffers and bf16 output");
     need(strategy->nreduce >= 0 && strategy->nreduce <= APL_MAX_MESH, "bad reduce axis count");
     apl::MatmulStrategy s;
     s.a = to_spec(&strategy->a);
@@ -815,8 +818,20 @@ int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
     need(s.partial_sum == !s.reduce_axes.empty(), "partial_sum iff reduce axes are given");
     apl::sharded_matmul(mesh->impl, s, to_meta(a_meta), to_meta(b_meta), A, B, C,
                         b_layout == APL_B_KN, out_dtype, epilogue,
-                        static_cast<cudaStream_t>(stream));
+                        static_cast<cudaStream_t>(stream), aux);
   });
+}
+
+int apl_sharded_matmul(apl_mesh* mesh, const apl_matmul_strategy* strategy,
+                       const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
+                       const void* const* B, void* const* C, int b_layout, int out_dtype,
+                       int epilogue, void* stream) {
+  if (epilogue == APL_EPI_GELU_SAVE) {
+    g_last_error = "APL_EPI_GELU_SAVE needs apl_sharded_matmul_ex (aux buffers)";
+    return APL_ERR_ARG;
+  }
+  return apl_sharded_matmul_ex(mesh, strategy, a_meta, b_meta, A, B, C, b_layout, out_dtype,
+                               epilogue, nullptr, stream);
 }
 
 int apl_gelu_inplace(void* buf, size_t count, int dtype, void* stream) {

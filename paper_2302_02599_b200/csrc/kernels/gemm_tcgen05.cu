@@ -140,15 +140,29 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15}, [%16];"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // GELU with erf from Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7 on erf,
@@ -157,13 +171,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // keeps up with the MMAs (the GELU epilogue was the pacing stage).
 __device__ __forceinline__ float gelu_erf(float x) {
   const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = __frcp_rn(1.f + 0.3275911f * z);
+  const float t = rcp_approx(1.f + 0.3275911f * z);
   float poly = fmaf(1.061405429f, t, -1.453152027f);
   poly = fmaf(poly, t, 1.421413741f);
   poly = fmaf(poly, t, -0.284496736f);
   poly = fmaf(poly, t, 0.254829592f);
   poly *= t;
-  const float e = exp2f(-z * z * 1.4426950408889634f);
+  const float e = ex2_approx(-z * z * 1.4426950408889634f);
   const float erf_abs = fmaf(-poly, e, 1.f);
   const float erf_v = copysignf(erf_abs, x);
   return 0.5f * x * (1.f + erf_v);
@@ -172,13 +186,13 @@ __device__ __forceinline__ float gelu_erf(float x) {
 // d/dx GELU(x) = Phi(x) + x phi(x), with the same A&S erf as gelu_erf.
 __device__ __forceinline__ float gelu_grad(float x) {
   const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = __frcp_rn(1.f + 0.3275911f * z);
+  const float t = rcp_approx(1.f + 0.3275911f * z);
   float poly = fmaf(1.061405429f, t, -1.453152027f);
   poly = fmaf(poly, t, 1.421413741f);
   poly = fmaf(poly, t, -0.284496736f);
   poly = fmaf(poly, t, 0.254829592f);
   poly *= t;
-  const float e = exp2f(-z * z * 1.4426950408889634f);  // exp(-x^2 / 2)
+  const float e = ex2_approx(-z * z * 1.4426950408889634f);  // exp(-x^2 / 2)
   const float erf_v = copysignf(fmaf(-poly, e, 1.f), x);
   return 0.5f * (1.f + erf_v) + x * e * 0.3989422804014327f;
 }
@@ -187,67 +201,96 @@ __device__ __forceinline__ float gelu_grad(float x) {
 // aux bf16 [M, N] with leading dimension ldaux: the saved pre-activation).
 constexpr int kEpiNone = 0, kEpiGelu = 1, kEpiDGelu = 2;
 
-// Epilogue of one accumulator row chunk: 16 fp32 columns of row `row`
-// starting at `col` -> epilogue -> bf16 / fp32, vectorised when aligned.
+constexpr int kEpiGeluSave = 3;  // GELU, and the pre-activation stored to aux (training)
+
+// 32 accumulator columns of one row: epilogue computed once, then stored to
+// each of `fan` outputs (the fused all-reduce writes every group member).
+// Vector path when the 32 columns are in bounds and 16-byte aligned.
 template <int kEpi, bool kOutF32>
-__device__ __forceinline__ void store_chunk(void* out, int ldc, int M, int N, int row, int col,
-                                            const uint32_t (&r)[16], const void* aux = nullptr,
-                                            int ldaux = 0) {
+__device__ __forceinline__ void epi_store32(void* const* outs, int fan, int ldc, int M, int N,
+                                            int row, int col, const uint32_t (&r)[32],
+                                            const void* aux, int ldaux) {
   if (row >= M || col >= N) return;
-  float v[16];
+  float v[32];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    v[i] = __uint_as_float(r[i]);
-    if (kEpi == kEpiGelu) v[i] = gelu_erf(v[i]);
-  }
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  const bool full = col + 32 <= N;
   if constexpr (kEpi == kEpiDGelu) {
     const __nv_bfloat16* a =
         static_cast<const __nv_bfloat16*>(aux) + static_cast<size_t>(row) * ldaux + col;
-    float x[16];
-    if (col + 16 <= N && (reinterpret_cast<uintptr_t>(a) & 15) == 0) {
-      uint4 q[2];
-      q[0] = reinterpret_cast<const uint4*>(a)[0];
-      q[1] = reinterpret_cast<const uint4*>(a)[1];
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(q);
+    if (full && (reinterpret_cast<uintptr_t>(a) & 15) == 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 f = __bfloat1622float2(h[i]);
-        x[2 * i] = f.x;
-        x[2 * i + 1] = f.y;
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = reinterpret_cast<const uint4*>(a)[q];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          v[8 * q + 2 * i] *= gelu_grad(f.x);
+          v[8 * q + 2 * i + 1] *= gelu_grad(f.y);
+        }
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) x[i] = col + i < N ? __bfloat162float(a[i]) : 0.f;
+      for (int i = 0; i < 32; ++i)
+        if (col + i < N) v[i] *= gelu_grad(__bfloat162float(a[i]));
     }
+  }
+  if constexpr (kEpi == kEpiGeluSave) {  // pre-activation out (bf16), before GELU
+    __nv_bfloat16* a = const_cast<__nv_bfloat16*>(static_cast<const __nv_bfloat16*>(aux)) +
+                       static_cast<size_t>(row) * ldaux + col;
+    if (full && (reinterpret_cast<uintptr_t>(a) & 15) == 0) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] *= gelu_grad(x[i]);
+      for (int q = 0; q < 4; ++q) {
+        uint32_t p[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
+          std::memcpy(&p[i], &h, 4);
+        }
+        reinterpret_cast<uint4*>(a)[q] = make_uint4(p[0], p[1], p[2], p[3]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col + i < N) a[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
+  if constexpr (kEpi == kEpiGelu || kEpi == kEpiGeluSave) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
   }
   if constexpr (kOutF32) {
-    float* dst = static_cast<float*>(out) + static_cast<size_t>(row) * ldc + col;
-    if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    for (int j = 0; j < fan; ++j) {
+      float* dst = static_cast<float*>(outs[j]) + static_cast<size_t>(row) * ldc + col;
+      if (full && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
-      for (int i = 0; i < 16; i += 4)
-        *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (col + i < N) dst[i] = v[i];
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (col + i < N) dst[i] = v[i];
+      }
     }
   } else {
-    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(row) * ldc + col;
-    if (col + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-      uint32_t p[8];
+    uint32_t p[16];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-        std::memcpy(&p[i], &h, 4);
+    for (int i = 0; i < 16; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      std::memcpy(&p[i], &h, 4);
+    }
+    for (int j = 0; j < fan; ++j) {
+      __nv_bfloat16* dst =
+          static_cast<__nv_bfloat16*>(outs[j]) + static_cast<size_t>(row) * ldc + col;
+      if (full && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<uint4*>(dst)[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2],
+                                                        p[4 * q + 3]);
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (col + i < N) dst[i] = __float2bfloat16_rn(v[i]);
       }
-      reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
-      reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (col + i < N) dst[i] = __float2bfloat16_rn(v[i]);
     }
   }
 }
@@ -436,12 +479,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
-        uint32_t r[16];
-        tmem_ld16(lane_addr + uint32_t(c), r);
-        const int col = n0 + c;
-        for (int j = 0; j < fan; ++j)
-          store_chunk<kEpi, kOutF32>(outs[j], ldc, rows, N, row, col, r, args.aux[g], args.ldaux);
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_addr + uint32_t(c), r);
+        epi_store32<kEpi, kOutF32>(outs, fan, ldc, rows, N, row, n0 + c, r, args.aux[g],
+                                   args.ldaux);
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -665,11 +707,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN);
 #pragma unroll 1
-      for (int c = half * (kBN / 2); c < (half + 1) * (kBN / 2); c += 16) {
-        uint32_t r[16];
-        tmem_ld16(lane_addr + uint32_t(c), r);
-        for (int j = 0; j < args.fan; ++j)
-          store_chunk<kGelu ? kEpiGelu : kEpiNone, kOutF32>(outs[j], ldc, M, N, row, n0 + c, r);
+      for (int c = half * (kBN / 2); c < (half + 1) * (kBN / 2); c += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_addr + uint32_t(c), r);
+        epi_store32<kGelu ? kEpiGelu : kEpiNone, kOutF32>(outs, args.fan, ldc, M, N, row, n0 + c,
+                                                          r, nullptr, 0);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -757,6 +799,8 @@ cudaError_t dispatch(const GemmArgs& args, bool out_f32, int epi, bool a_km,
   if (epi == kEpiDGelu)
     return out_f32 ? launch_gemm<BN, kEpiDGelu, true, BMN>(args, stream)
                    : launch_gemm<BN, kEpiDGelu, false, BMN>(args, stream);
+  if (epi == kEpiGeluSave)
+    return out_f32 ? cudaErrorInvalidValue : launch_gemm<BN, kEpiGeluSave, false, BMN>(args, stream);
   if (epi == kEpiGelu)
     return out_f32 ? launch_gemm<BN, kEpiGelu, true, BMN>(args, stream)
                    : launch_gemm<BN, kEpiGelu, false, BMN>(args, stream);
@@ -831,10 +875,10 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
   if (M <= 0 || N <= 0 || K <= 0 || groups <= 0) return cudaSuccess;
   if (reduce < 1 || fan < 1 || reduce > kMaxBatch || fan > kMaxBatch) return cudaErrorInvalidValue;
   if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;  // TMA row alignment
-  if (epi < kEpiNone || epi > kEpiDGelu || (epi == kEpiDGelu && aux == nullptr))
+  if (epi < kEpiNone || epi > kEpiGeluSave || (epi >= kEpiDGelu && aux == nullptr))
     return cudaErrorInvalidValue;
   const int per_launch = std::max(1, std::min(kMaxBatch / reduce, kMaxBatch / fan));
-  const bool paired = !a_km && epi != kEpiDGelu && use_pair(M, N, std::min(groups, per_launch));
+  const bool paired = !a_km && epi <= kEpiGelu && use_pair(M, N, std::min(groups, per_launch));
   int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
   {
     // Too few 128 x 256 tiles to cover the SMs once (a per-GPU shard of a
@@ -876,7 +920,7 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
       if (!oka || !okb) return cudaErrorInvalidValue;
     }
     for (int i = 0; i < args.count * fan; ++i) args.c[i] = C[first * fan + i];
-    if (epi == kEpiDGelu)
+    if (epi >= kEpiDGelu)
       for (int i = 0; i < args.count; ++i) args.aux[i] = aux[first + i];
     cudaError_t e;
     if (paired)

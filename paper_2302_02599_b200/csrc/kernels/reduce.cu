@@ -118,39 +118,54 @@ cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int gr
 
 namespace {
 
-template <typename T>
-__global__ void __launch_bounds__(256) gelu_apply(const T* __restrict__ x, T* __restrict__ y,
-                                                  int64_t n) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float v = to_f(x[i]);
-    y[i] = from_f<T>(0.5f * v * (1.f + erff(v * 0.70710678118654752f)));
-  }
+__device__ __forceinline__ float gelu_f(float v) {
+  return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+}
+__device__ __forceinline__ float gelu_grad_f(float v) {
+  return 0.5f * (1.f + erff(v * 0.70710678118654752f)) +
+         v * 0.3989422804014327f * __expf(-0.5f * v * v);
 }
 
-// dx = dy * GELU'(x), GELU'(x) = Phi(x) + x phi(x).
+// y = GELU(x) (dy == nullptr) or y = dy * GELU'(x), 16-byte vectors of
+// 16 / sizeof(T) elements per thread per iteration (scalar tail).
 template <typename T>
-__global__ void __launch_bounds__(256) gelu_backward(const T* __restrict__ dy,
-                                                     const T* __restrict__ x, T* __restrict__ dx,
-                                                     int64_t n) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+__global__ void __launch_bounds__(256) gelu_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                   const T* __restrict__ dy, int64_t n,
+                                                   int64_t nv) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += stride) {
+    uint4 xv = reinterpret_cast<const uint4*>(x)[i], gv;
+    if (dy != nullptr) gv = reinterpret_cast<const uint4*>(dy)[i];
+    const T* xe = reinterpret_cast<const T*>(&xv);
+    const T* ge = reinterpret_cast<const T*>(&gv);
+    uint4 ov;
+    T* oe = reinterpret_cast<T*>(&ov);
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      const float v = to_f(xe[k]);
+      oe[k] = from_f<T>(dy != nullptr ? to_f(ge[k]) * gelu_grad_f(v) : gelu_f(v));
+    }
+    reinterpret_cast<uint4*>(y)[i] = ov;
+  }
+  for (int64_t i = nv * VEC + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
     const float v = to_f(x[i]);
-    const float g = 0.5f * (1.f + erff(v * 0.70710678118654752f)) +
-                    v * 0.3989422804014327f * __expf(-0.5f * v * v);
-    dx[i] = from_f<T>(to_f(dy[i]) * g);
+    y[i] = from_f<T>(dy != nullptr ? to_f(dy[i]) * gelu_grad_f(v) : gelu_f(v));
   }
 }
 
 template <typename T>
 cudaError_t gelu_typed(const void* x, void* y, const void* dy, size_t count, cudaStream_t stream) {
-  const int grid = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 16));
-  if (dy == nullptr)
-    gelu_apply<T><<<grid, 256, 0, stream>>>(static_cast<const T*>(x), static_cast<T*>(y), count);
-  else
-    gelu_backward<T><<<grid, 256, 0, stream>>>(static_cast<const T*>(dy),
-                                               static_cast<const T*>(x), static_cast<T*>(y),
-                                               count);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                         reinterpret_cast<uintptr_t>(dy)) & 15) == 0;
+  const size_t vec = 16 / sizeof(T);
+  const int64_t nv = aligned ? static_cast<int64_t>(count / vec) : 0;  // else all scalar
+  const int grid = static_cast<int>(std::min<size_t>((count / vec + 255) / 256 + 1, 148 * 8));
+  gelu_kernel<T><<<grid, 256, 0, stream>>>(static_cast<const T*>(x), static_cast<T*>(y),
+                                           static_cast<const T*>(dy), static_cast<int64_t>(count),
+                                           nv);
   return cudaGetLastError();
 }
 

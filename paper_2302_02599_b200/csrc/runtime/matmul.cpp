@@ -20,7 +20,10 @@ namespace apl {
 void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorMeta& a_meta,
                     const autoplan::TensorMeta& b_meta, const void* const* A,
                     const void* const* B, void* const* C, bool b_kn, int out_dtype, int epilogue,
-                    cudaStream_t stream) {
+                    cudaStream_t stream, void* const* aux) {
+  const bool save = epilogue == APL_EPI_GELU_SAVE;
+  if (save && (aux == nullptr || out_dtype != APL_BF16))
+    throw RuntimeError(APL_ERR_ARG, "GELU_SAVE needs bf16 output and aux buffers");
   const auto& geo = mesh.geo;
   // matmul: A[..m.., k] . B[k, n];  batched matmul: A[b, m, k] . B[b, k, n]
   const bool batched = b_meta.rank() == 3;
@@ -67,7 +70,7 @@ void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorM
     const char* e = std::getenv("APL_FUSED_AR");
     return e == nullptr || std::string(e) != "0";
   }();
-  if (s.partial_sum && !mesh.distributed && batch == 1 && fused_ar_enabled) {
+  if (s.partial_sum && !mesh.distributed && batch == 1 && fused_ar_enabled && !save) {
     const auto groups = axis_groups(geo, s.reduce_axes);
     const int gsize = static_cast<int>(groups[0].size());
     if (gsize <= 8) {
@@ -89,7 +92,7 @@ void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorM
       return;
     }
   }
-  const bool fuse_gelu = epilogue == APL_EPI_GELU && !s.partial_sum;
+  const bool fuse_gelu = (epilogue == APL_EPI_GELU || save) && !s.partial_sum;
   // Every local device (and every batch element) has the same shard shapes:
   // all problems go through the persistent batched launcher together (a
   // simulated mesh runs its 8 GEMMs as one launch).
@@ -101,17 +104,27 @@ void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorM
       pb.push_back(static_cast<const char*>(B[d]) + i * k * n * 2);
       pc.push_back(static_cast<char*>(C[d]) + i * m * n * eb_c);
     }
-  check_cuda(gemm_bf16_batched(pa.data(), pb.data(), pc.data(), static_cast<int>(pa.size()),
+  std::vector<const void*> px;
+  if (save && fuse_gelu)
+    for (int d = 0; d < nl; ++d)
+      for (int64_t i = 0; i < batch; ++i)
+        px.push_back(static_cast<const char*>(aux[d]) + i * m * n * 2);
+  check_cuda(gemm_bf16_grouped(pa.data(), pb.data(), pc.data(), static_cast<int>(pa.size()), 1, 1,
                                static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
                                static_cast<int>(k), static_cast<int>(b_kn ? n : k),
-                               static_cast<int>(n), b_kn, out_dtype == APL_F32, fuse_gelu, stream),
+                               static_cast<int>(n), b_kn, out_dtype == APL_F32,
+                               fuse_gelu ? (save ? 3 : 1) : 0, false,
+                               px.empty() ? nullptr : px.data(), static_cast<int>(n), stream),
              "tcgen05 GEMM launch");
   const size_t count = static_cast<size_t>(batch * m * n);
   if (s.partial_sum) {
     all_reduce(mesh, s.reduce_axes, C, count, out_dtype, stream);
-    if (epilogue == APL_EPI_GELU)
-      for (int d = 0; d < nl; ++d)
-        check_cuda(launch_gelu_inplace(C[d], count, out_dtype, stream), "gelu launch");
+    for (int d = 0; d < nl && (epilogue == APL_EPI_GELU || save); ++d) {
+      if (save)  // the full sum is the pre-activation
+        check_cuda(cudaMemcpyAsync(aux[d], C[d], count * 2, cudaMemcpyDeviceToDevice, stream),
+                   "save pre-activation");
+      check_cuda(launch_gelu_inplace(C[d], count, out_dtype, stream), "gelu launch");
+    }
   }
 }
 

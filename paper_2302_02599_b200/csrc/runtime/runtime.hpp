@@ -202,10 +202,11 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
 
 // B shards are row-major [k_local, n_local] when b_kn, else transposed
 // [n_local, k_local] (nn.Linear layout).
+// epilogue APL_EPI_GELU_SAVE also stores the pre-activation to aux[d].
 void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorMeta& a_meta,
                     const autoplan::TensorMeta& b_meta, const void* const* A,
                     const void* const* B, void* const* C, bool b_kn, int out_dtype,
-                    int epilogue, cudaStream_t stream);
+                    int epilogue, cudaStream_t stream, void* const* aux = nullptr);
 
 // Backward of one strategy: per local device dA = dC . B^T (bf16; with
 // dgelu, times GELU'(aux) -- the fused backward of a GELU feeding A) and

@@ -204,7 +204,7 @@ class PlanExecutor:
         already-sharded lists (node id -> list of local shards).
         train=True keeps what backward() needs: every matmul's operands in
         the layouts its strategy consumed them, and every GELU's input (the
-        GELU is then not fused into the GEMM epilogue)."""
+        fused GELU's epilogue then also stores its pre-activation)."""
         from .runtime import gelu
 
         values, converted, fused = {}, {}, set()
@@ -229,13 +229,17 @@ class PlanExecutor:
                 st = self.strategy[nid]
                 out_spec = self.spec[nid]
                 outs = self._alloc(nid, out_spec, ins[0][0])
-                gelu_node = None if train else self._fusable_gelu(nid)
+                gelu_node = self._fusable_gelu(nid)
+                pre = None
                 if train:
                     self._saved[nid] = (ins[0], ins[1])
+                    if gelu_node:  # one pass writes GELU(acc) and keeps acc for backward
+                        pre = self._alloc(nid, self.spec[nid], ins[0][0])
+                        self._saved[gelu_node] = pre
                 self.mesh.sharded_matmul(st, self._meta(n["inputs"][0][0]),
                                          self._meta(n["inputs"][1][0]), ins[0], ins[1], outs,
                                          gelu=gelu_node is not None, b_layout="kn",
-                                         stream=stream)
+                                         stream=stream, gelu_save=pre)
                 if gelu_node:
                     fused.add(gelu_node)
                 values[nid] = outs

@@ -217,18 +217,22 @@ class Mesh:
 
     def sharded_matmul(self, strategy: "MatmulStrategy", a_meta: TensorMeta, b_meta: TensorMeta,
                        a_shards, b_shards, c_shards, gelu: bool = False, b_layout: str = "nk",
-                       stream=None) -> None:
+                       stream=None, gelu_save=None) -> None:
         """Local tcgen05 GEMM per device + partial-sum all-reduce (+ epilogue).
         b_layout "nk": each B shard stored transposed [n_local, k_local];
-        "kn": the logical row-major shard [k_local, n_local]."""
-        for what, bufs in (("A", a_shards), ("B", b_shards), ("C", c_shards)):
-            if len(bufs) != self.num_local:
+        "kn": the logical row-major shard [k_local, n_local]. gelu_save: one
+        bf16 buffer per local device receiving the pre-activation while C
+        gets GELU of it (training forward, one pass)."""
+        for what, bufs in (("A", a_shards), ("B", b_shards), ("C", c_shards),
+                           ("aux", gelu_save)):
+            if bufs is not None and len(bufs) != self.num_local:
                 raise ValueError(f"{what}: expected {self.num_local} shards")
-        check(A.lib().apl_sharded_matmul(
+        epi = A.EPI_GELU_SAVE if gelu_save is not None else (A.EPI_GELU if gelu else A.EPI_NONE)
+        check(A.lib().apl_sharded_matmul_ex(
             self._h, C.byref(strategy.c_struct()), C.byref(a_meta.c()), C.byref(b_meta.c()),
             _ptrs(a_shards), _ptrs(b_shards), _ptrs(c_shards),
-            A.B_KN if b_layout == "kn" else A.B_NK, _DTYPE_CODE[c_shards[0].dtype],
-            A.EPI_GELU if gelu else A.EPI_NONE, _stream_handle(stream)))
+            A.B_KN if b_layout == "kn" else A.B_NK, _DTYPE_CODE[c_shards[0].dtype], epi,
+            _ptrs(gelu_save) if gelu_save is not None else None, _stream_handle(stream)))
 
     def sharded_matmul_backward(self, strategy: "MatmulStrategy", a_meta: TensorMeta,
                                 b_meta: TensorMeta, a_shards, b_shards, dc_shards,

@@ -67,10 +67,43 @@ def main():
             b.record()
             torch.cuda.synchronize()
             tms = a.elapsed_time(b) / iters
+            # the same steps captured in CUDA graphs (device time, no host
+            # launch overhead): every kernel of the executor is stream-ordered
+            # on the capture stream and everything is compiled by the warm-up
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            graphs = {}
+            with torch.cuda.stream(side):
+                ex.forward(shards, stream=side)
+                ex.forward(shards, stream=side, train=True)
+                ex.backward(gy, stream=side)
+                side.synchronize()
+                gf, gt = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gf, stream=side):
+                    ex.forward(shards, stream=side)
+                with torch.cuda.graph(gt, stream=side):
+                    ex.forward(shards, stream=side, train=True)
+                    ex.backward(gy, stream=side)
+                graphs = {"fwd": gf, "train": gt}
+            torch.cuda.current_stream().wait_stream(side)
+            gms = {}
+            for k, g in graphs.items():
+                g.replay()
+                torch.cuda.synchronize()
+                a.record()
+                for _ in range(iters):
+                    g.replay()
+                b.record()
+                torch.cuda.synchronize()
+                gms[k] = a.elapsed_time(b) / iters
             print(json.dumps({"plan": name, "fuse": fuse, "ms_per_forward": round(ms, 4),
                               "tflops": round(FLOPS / ms / 1e9, 1),
                               "ms_per_train_step": round(tms, 4),
                               "train_tflops": round(TRAIN_FLOPS / tms / 1e9, 1),
+                              "graph_ms_per_forward": round(gms["fwd"], 4),
+                              "graph_tflops": round(FLOPS / gms["fwd"] / 1e9, 1),
+                              "graph_ms_per_train_step": round(gms["train"], 4),
+                              "graph_train_tflops": round(TRAIN_FLOPS / gms["train"] / 1e9, 1),
                               "strategies": {k: v.name for k, v in ex.strategy.items()}}),
                   flush=True)
 
