@@ -581,13 +581,14 @@ __device__ __forceinline__ void commit_pair(uint64_t* bar_local) {
       : "memory");
 }
 
-template <bool kBMN>
+template <bool kBMN, bool kAMN>
 __device__ __forceinline__ constexpr uint32_t instr_desc_pair() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kBMN ? 1 : 0) << 16) |
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kAMN ? 1 : 0) << 15) |
+         (uint32_t(kBMN ? 1 : 0) << 16) |
          (uint32_t(kBN >> 3) << 17) | (uint32_t((2 * kBM) >> 4) << 24);
 }
 
-template <bool kGelu, bool kOutF32, bool kBMN>
+template <int kEpi, bool kOutF32, bool kBMN, bool kAMN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ GemmArgs args) {
   const int M = args.M, N = args.N, K = args.K, ldc = args.ldc;
@@ -653,7 +654,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t phase = (it / kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
           if (leader) mbar_expect_tx(&full[s], 2 * (kStageA + kStageB));
-          tma_load_2d_pair(tiles_a + s * kStageA, map_a, &full[s], kb * kBK, m0);
+          if constexpr (kAMN) {  // A^T stored [K, M]: two [64 k][64 m] MN atoms
+            tma_load_2d_pair(tiles_a + s * kStageA, map_a, &full[s], m0, kb * kBK);
+            tma_load_2d_pair(tiles_a + s * kStageA + 8192, map_a, &full[s], m0 + 64, kb * kBK);
+          } else {
+            tma_load_2d_pair(tiles_a + s * kStageA, map_a, &full[s], kb * kBK, m0);
+          }
           if constexpr (kBMN) {
 #pragma unroll
             for (int j = 0; j < (kBN / 2) / 64; ++j)
@@ -668,7 +674,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = instr_desc_pair<kBMN>();
+      constexpr uint32_t idesc = instr_desc_pair<kBMN, kAMN>();
       int it = 0, local = 0;
       for (int t = cluster; t < tiles; t += clusters, ++local) {
         const int acc = local & 1;
@@ -679,13 +685,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t da = smem_desc(tiles_a + s * kStageA);
+          const uint64_t da = kAMN ? smem_desc_mn(tiles_a + s * kStageA)
+                                   : smem_desc(tiles_a + s * kStageA);
           const uint64_t db = kBMN ? smem_desc_mn(tiles_b + s * kStageB)
                                    : smem_desc(tiles_b + s * kStageB);
+          constexpr uint64_t kAdvA = kAMN ? (16 * 128) >> 4 : 2;
           constexpr uint64_t kAdvB = kBMN ? (16 * 128) >> 4 : 2;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            mma_pair(d, da + uint64_t(2 * k), db + kAdvB * k, idesc, (kk > 0 || k > 0) ? 1u : 0u);
+            mma_pair(d, da + kAdvA * k, db + kAdvB * k, idesc, (kk > 0 || k > 0) ? 1u : 0u);
           commit_pair(&empty[s]);
         }
         commit_pair(&acc_full[acc]);
@@ -710,8 +718,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int c = half * (kBN / 2); c < (half + 1) * (kBN / 2); c += 32) {
         uint32_t r[32];
         tmem_ld32(lane_addr + uint32_t(c), r);
-        epi_store32<kGelu ? kEpiGelu : kEpiNone, kOutF32>(outs, args.fan, ldc, M, N, row, n0 + c,
-                                                          r, nullptr, 0);
+        epi_store32<kEpi, kOutF32>(outs, args.fan, ldc, M, N, row, n0 + c, r, args.aux[g],
+                                   args.ldaux);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -809,9 +817,9 @@ cudaError_t dispatch(const GemmArgs& args, bool out_f32, int epi, bool a_km,
 }
 
 // 2-CTA pair kernel launch (cluster dims are compiled into the kernel).
-template <bool G, bool F, bool BMN>
+template <int E, bool F, bool BMN, bool AMN = false>
 cudaError_t launch_pair(const GemmArgs& args, cudaStream_t stream) {
-  auto kernel = pair::gemm_bf16_tcgen05_pair<G, F, BMN>;
+  auto kernel = pair::gemm_bf16_tcgen05_pair<E, F, BMN, AMN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -834,12 +842,25 @@ cudaError_t launch_pair(const GemmArgs& args, cudaStream_t stream) {
 }
 
 template <bool BMN>
-cudaError_t dispatch_pair(const GemmArgs& args, bool out_f32, bool gelu, cudaStream_t stream) {
-  if (gelu)
-    return out_f32 ? launch_pair<true, true, BMN>(args, stream)
-                   : launch_pair<true, false, BMN>(args, stream);
-  return out_f32 ? launch_pair<false, true, BMN>(args, stream)
-                 : launch_pair<false, false, BMN>(args, stream);
+cudaError_t dispatch_pair(const GemmArgs& args, bool out_f32, int epi, bool a_km,
+                          cudaStream_t stream) {
+  if (a_km) {
+    if (epi != kEpiNone) return cudaErrorInvalidValue;
+    return out_f32 ? launch_pair<kEpiNone, true, BMN, true>(args, stream)
+                   : launch_pair<kEpiNone, false, BMN, true>(args, stream);
+  }
+  switch (epi) {
+    case kEpiGelu:
+      return out_f32 ? launch_pair<kEpiGelu, true, BMN>(args, stream)
+                     : launch_pair<kEpiGelu, false, BMN>(args, stream);
+    case kEpiDGelu:
+      return out_f32 ? cudaErrorInvalidValue : launch_pair<kEpiDGelu, false, BMN>(args, stream);
+    case kEpiGeluSave:
+      return out_f32 ? cudaErrorInvalidValue : launch_pair<kEpiGeluSave, false, BMN>(args, stream);
+    default:
+      return out_f32 ? launch_pair<kEpiNone, true, BMN>(args, stream)
+                     : launch_pair<kEpiNone, false, BMN>(args, stream);
+  }
 }
 
 // CTA-pair kernel for problems big enough to fill 256 x 256 tiles;
@@ -854,7 +875,7 @@ bool use_pair(int M, int N, int count) {
   // 256 x 256 tiles (fc1 1331 vs 1145 TFLOP/s); with fewer the single-CTA
   // 128 x 256 tiles fill the machine better (fc2 split-m/8: 673 vs 626).
   const int pair_tiles = ((M + 255) / 256) * ((N + 255) / 256) * count;
-  return M >= 256 && N >= 256 && pair_tiles >= 72;
+  return M >= 256 && N >= 256 && pair_tiles >= 56;
 }
 
 }  // namespace
@@ -878,7 +899,7 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
   if (epi < kEpiNone || epi > kEpiGeluSave || (epi >= kEpiDGelu && aux == nullptr))
     return cudaErrorInvalidValue;
   const int per_launch = std::max(1, std::min(kMaxBatch / reduce, kMaxBatch / fan));
-  const bool paired = !a_km && epi <= kEpiGelu && use_pair(M, N, std::min(groups, per_launch));
+  const bool paired = !(epi == kEpiDGelu && out_f32) && use_pair(M, N, std::min(groups, per_launch));
   int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
   {
     // Too few 128 x 256 tiles to cover the SMs once (a per-GPU shard of a
@@ -924,8 +945,8 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
       for (int i = 0; i < args.count; ++i) args.aux[i] = aux[first + i];
     cudaError_t e;
     if (paired)
-      e = b_kn ? dispatch_pair<true>(args, out_f32, epi == kEpiGelu, stream)
-               : dispatch_pair<false>(args, out_f32, epi == kEpiGelu, stream);
+      e = b_kn ? dispatch_pair<true>(args, out_f32, epi, a_km, stream)
+               : dispatch_pair<false>(args, out_f32, epi, a_km, stream);
     else if (b_kn)
       e = bn == 256 ? dispatch<256, true>(args, out_f32, epi, a_km, stream)
                     : dispatch<128, true>(args, out_f32, epi, a_km, stream);
