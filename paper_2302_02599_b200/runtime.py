@@ -504,6 +504,21 @@ class PeerMesh:
                                       self._n_others, e, self.timeout_ms, sh))
         return c_out
 
+    def sharded_matmul(self, strategy: "MatmulStrategy", a: torch.Tensor, b: torch.Tensor,
+                       gelu: bool = False, b_layout: str = "kn", stream=None) -> torch.Tensor:
+        """This rank's part of a sharded-matmul strategy on the peer mesh:
+        strategies without a partial sum are one local tcgen05 GEMM on the
+        shards (GELU fused); partial-sum strategies reducing over every mesh
+        axis (split-k on a 1-D mesh, split-k:01.. on 2-D/3-D) run as the fused
+        GEMM + all-reduce over peer memory (matmul_allreduce)."""
+        if not strategy.partial_sum:
+            return gemm(a, b, gelu=gelu, b_layout=b_layout, stream=stream)
+        if sorted(strategy.reduce_axes) != list(range(self.geo.rank())):
+            raise NotImplementedError("peer partial sums reduce over all mesh axes")
+        if gelu:
+            raise NotImplementedError("GELU after a peer all-reduce is not fused")
+        return self.matmul_allreduce(a, b, b_layout=b_layout, stream=stream)
+
     def exchange_traffic(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta) -> dict:
         """This rank's bytes of the src->tgt exchange (wire_in = bytes pulled
         from peers)."""

@@ -184,6 +184,25 @@ def _allreduce_worker(rank, world, port, q):
                 tol = 2e-2 if out_dtype == torch.bfloat16 else 1e-5
                 digest = c.view(torch.uint8).sum(dtype=torch.int64).item()
                 q.put((rank, epoch, str(out_dtype), err <= tol, err, digest))
+        # config 5, Megatron selection through PeerMesh.sharded_matmul: fc1
+        # split-n:0 (local GEMM + GELU), fc2 split-k:0 (fused GEMM + all-reduce)
+        from paper_2302_02599_b200 import ShardingSpec
+        from paper_2302_02599_b200.runtime import MatmulStrategy
+
+        g = torch.Generator(device="cuda").manual_seed(7)
+        x = torch.randn(1024, 256, device="cuda", generator=g).bfloat16()
+        w1 = (torch.randn(256, 1024, device="cuda", generator=g) / 16).bfloat16()
+        w2 = (torch.randn(1024, 256, device="cuda", generator=g) / 32).bfloat16()
+        hs = 1024 // world
+        p = lambda s: ShardingSpec.parse(s, 1)  # noqa: E731
+        h = pm.sharded_matmul(MatmulStrategy("split-n:0", p("RR"), p("RS0"), p("RS0")), x,
+                              w1[:, rank * hs:(rank + 1) * hs].contiguous(), gelu=True)
+        y = pm.sharded_matmul(MatmulStrategy("split-k:0", p("RS0"), p("S0R"), p("RR"), [0]), h,
+                              w2[rank * hs:(rank + 1) * hs].contiguous())
+        torch.cuda.synchronize()
+        ref = torch.nn.functional.gelu(x.double() @ w1.double()) @ w2.double()
+        err = ((y.double() - ref).abs().max() / ref.abs().max()).item()
+        q.put((rank, 9, "megatron", err <= 2e-2, err, y.view(torch.uint8).sum(dtype=torch.int64).item()))
         dist.barrier()
         pm.close()
         dist.barrier()
@@ -205,8 +224,9 @@ def test_fused_gemm_allreduce_over_peer_memory(cuda, world):
     while not q.empty():
         res.append(q.get())
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    assert len(res) == world * 4
+    assert len(res) == world * 5
     assert all(r[3] for r in res), [r for r in res if not r[3]]
+    assert len({r[5] for r in res if r[2] == "megatron"}) == 1
     for epoch in range(2):  # every rank holds the same bytes
         for dt in ("torch.bfloat16", "torch.float32"):
             assert len({r[5] for r in res if r[1] == epoch and r[2] == dt}) == 1
