@@ -217,6 +217,14 @@ int apl_peer_gemm_scatter(const void* A, const void* B, void* const* owner_slabs
 int apl_peer_reduce_gather(const float* staging, int P, int64_t slab_elems, void* const* outs,
                            int nout, int out_dtype, void* stream);
 
+/* In-place all-reduce over peer memory, ONE kernel per rank: members[r] =
+ * member r's buffer at this rank's block (count elements, 16-byte aligned,
+ * f32 or bf16). The owner of each block sums it over the members in member
+ * order (fp32) and writes the sum back to every member; blocks of different
+ * owners are disjoint. Bracket with apl_peer_flags_* (ready before, done
+ * after). Used for partial sums over arbitrary mesh-axis groups. */
+int apl_peer_allreduce(void* const* members, int P, size_t count, int dtype, void* stream);
+
 /* Fused collapsed exchange over peer memory: ONE kernel pulls every piece of
  * this rank's target shard straight out of the senders' source shards
  * (peer_in[r] = rank r's source shard mapped into this process, this rank's

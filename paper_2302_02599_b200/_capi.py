@@ -147,6 +147,7 @@ _SIGS = {
                                         C.c_int, C.c_void_p]),
     "apl_peer_reduce_gather": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, P(C.c_void_p), C.c_int,
                                          C.c_int, C.c_void_p]),
+    "apl_peer_allreduce": (C.c_int, [P(C.c_void_p), C.c_int, C.c_size_t, C.c_int, C.c_void_p]),
     "apl_peer_flags_store": (C.c_int, [P(C.c_void_p), C.c_int, C.c_int, C.c_uint32,
                                        C.c_void_p]),
     "apl_peer_flags_wait": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_int, C.c_uint32,

@@ -529,6 +529,17 @@ int apl_peer_gemm_scatter(const void* A, const void* B, void* const* owner_slabs
   });
 }
 
+int apl_peer_allreduce(void* const* members, int P, size_t count, int dtype, void* stream) {
+  return guarded([&] {
+    need(members && P >= 1 && P <= 8, "1..8 members");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    for (int r = 0; r < P; ++r) need(members[r] != nullptr, "null member buffer");
+    apl::check_cuda(apl::launch_peer_allreduce(members, P, static_cast<int64_t>(count), dtype,
+                                               static_cast<cudaStream_t>(stream)),
+                    "peer all-reduce launch");
+  });
+}
+
 int apl_peer_reduce_gather(const float* staging, int P, int64_t slab_elems, void* const* outs,
                            int nout, int out_dtype, void* stream) {
   return guarded([&] {

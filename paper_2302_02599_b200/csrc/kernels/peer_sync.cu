@@ -102,7 +102,63 @@ __global__ void __launch_bounds__(256) reduce_gather_kernel(const float* __restr
   }
 }
 
+// In-place all-reduce of this rank's block across the P members of a group:
+// bufs.p[r] = member r's tensor at this rank's block (peer-mapped). Each
+// rank owns one block: it reads the block from every member, sums in member
+// order in fp32 (deterministic; only the owner computes the block, so every
+// member ends with identical bytes) and writes the sum back to every member.
+// Blocks of different owners never overlap, so no two kernels race.
+template <typename T>
+__global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_constant__ OutPtrs bufs,
+                                                             int P, int64_t n) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int64_t nv = n / VEC;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (int64_t i = tid; i < nv; i += stride) {
+    float acc[VEC];
+    for (int r = 0; r < P; ++r) {
+      const uint4 u = reinterpret_cast<const uint4*>(bufs.p[r])[i];
+      const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) acc[k] = (r == 0 ? 0.f : acc[k]) + static_cast<float>(e[k]);
+    }
+    uint4 o;
+    T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) oe[k] = static_cast<T>(acc[k]);
+    for (int r = 0; r < P; ++r) reinterpret_cast<uint4*>(bufs.p[r])[i] = o;
+  }
+  for (int64_t i = nv * VEC + tid; i < n; i += stride) {
+    float acc = 0.f;
+    for (int r = 0; r < P; ++r) acc += static_cast<float>(static_cast<const T*>(bufs.p[r])[i]);
+    for (int r = 0; r < P; ++r) static_cast<T*>(bufs.p[r])[i] = static_cast<T>(acc);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_peer_allreduce(void* const* members, int P, int64_t count, int dtype,
+                                  cudaStream_t stream) {
+  if (P < 1 || P > 8 || count < 0) return cudaErrorInvalidValue;
+  if (count == 0) return cudaSuccess;
+  OutPtrs b{};
+  bool aligned = true;
+  for (int r = 0; r < P; ++r) {
+    b.p[r] = members[r];
+    aligned = aligned && (reinterpret_cast<uintptr_t>(members[r]) & 15) == 0;
+  }
+  if (!aligned) return cudaErrorMisalignedAddress;
+  const int grid = static_cast<int>(std::min<int64_t>((count / 4 + 255) / 256 + 1, 148 * 8));
+  if (dtype == 0)
+    peer_allreduce_kernel<float><<<grid, 256, 0, stream>>>(b, P, count);
+  else if (dtype == 1)
+    peer_allreduce_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>(b, P, count);
+  else
+    return cudaErrorInvalidValue;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_reduce_gather(const float* staging, int P, int64_t slab_elems,
                                  void* const* outs, int nout, bool out_f32, cudaStream_t stream) {

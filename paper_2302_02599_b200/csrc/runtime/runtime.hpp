@@ -39,6 +39,8 @@ cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int gr
 uint64_t launch_count();
 cudaError_t launch_gelu_inplace(void* buf, size_t count, int dtype, cudaStream_t stream);
 // Fused all-reduce over peer memory (peer_sync.cu / gemm_tcgen05.cu).
+cudaError_t launch_peer_allreduce(void* const* members, int P, int64_t count, int dtype,
+                                  cudaStream_t stream);
 cudaError_t launch_reduce_gather(const float* staging, int P, int64_t slab_elems,
                                  void* const* outs, int nout, bool out_f32, cudaStream_t stream);
 cudaError_t gemm_bf16_scatter(const void* A, const void* B, void* const* owner_slabs, int owners,

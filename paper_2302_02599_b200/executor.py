@@ -184,10 +184,17 @@ class PlanExecutor:
             out.append(full[tuple(sl)].contiguous())
         return out
 
+    def _empty(self, shape, dtype, device) -> torch.Tensor:
+        """Device buffer for a value; meshes with their own allocator (the
+        peer runtime's symmetric heap) provide it."""
+        alloc = getattr(self.mesh, "empty", None)
+        if alloc is not None:
+            return alloc(shape, dtype)
+        return torch.empty(shape, dtype=dtype, device=device)
+
     def _alloc(self, nid: str, spec: ShardingSpec, like: torch.Tensor) -> list:
         shape = spec.local_shape(self._meta(nid), self.geo)
-        return [torch.empty(shape, dtype=like.dtype, device=like.device)
-                for _ in range(self.mesh.num_local)]
+        return [self._empty(shape, like.dtype, like.device) for _ in range(self.mesh.num_local)]
 
     def _convert(self, nid, shards, src, tgt, stream):
         key = (nid, str(src), str(tgt))
@@ -209,6 +216,9 @@ class PlanExecutor:
 
         values, converted, fused = {}, {}, set()
         self._saved = {} if train else None
+        begin = getattr(self.mesh, "begin_step", None)
+        if begin is not None:  # recycle a per-step allocator (peer runtime heap)
+            begin(stream)
         for n in self.graph["nodes"]:
             nid, kind = n["id"], n["kind"]
             if kind in ("placeholder", "parameter"):
@@ -247,7 +257,7 @@ class PlanExecutor:
                 if nid in fused:
                     values[nid] = ins[0]
                 else:
-                    outs = [torch.empty_like(t) for t in ins[0]]
+                    outs = [self._empty(t.shape, t.dtype, t.device) for t in ins[0]]
                     for x, y in zip(ins[0], outs):
                         gelu(x, y, stream=stream)
                     if train:
@@ -279,8 +289,8 @@ class PlanExecutor:
             conv = self.mesh.prepare(find_transform_path(have, want, self.geo, meta), meta,
                                      fuse=self.fuse)
             self._convs[key] = conv
-        outs = [torch.empty(want.local_shape(meta, self.geo), dtype=shards[0].dtype,
-                            device=shards[0].device) for _ in range(self.mesh.num_local)]
+        outs = [self._empty(want.local_shape(meta, self.geo), shards[0].dtype, shards[0].device)
+                for _ in range(self.mesh.num_local)]
         conv(shards, outs, stream=stream)
         return outs
 
@@ -344,8 +354,8 @@ class PlanExecutor:
                     done.add(a_src)
                 need_a = wants_grad(a_target)
                 need_b = wants_grad(b_src)
-                ga = [torch.empty_like(t) for t in a_saved] if need_a else None
-                gb = [torch.empty(t.shape, dtype=torch.float32, device=t.device)
+                ga = [self._empty(t.shape, t.dtype, t.device) for t in a_saved] if need_a else None
+                gb = [self._empty(t.shape, torch.float32, t.device)
                       for t in b_saved] if need_b else None
                 if need_a or need_b:
                     self.mesh.sharded_matmul_backward(st, a_meta, b_meta, a_saved, b_saved, dy,
@@ -360,7 +370,7 @@ class PlanExecutor:
                 from .runtime import gelu_backward
                 x_src = n["inputs"][0][0]
                 pre = self._saved[nid]
-                dx = [torch.empty_like(t) for t in pre]
+                dx = [self._empty(t.shape, t.dtype, t.device) for t in pre]
                 for a, x, o in zip(dy, pre, dx):
                     gelu_backward(a, x, o, stream=stream)
                 add(x_src, self._convert_grad(x_src, dx, self.spec[nid], self.spec[x_src], stream))

@@ -1,0 +1,108 @@
+"""BASELINE config 5 executed distributed over peer memory: 8 processes (one
+per mesh device, sharing cuda:0 through CUDA IPC -- on an 8-GPU box the same
+code reads over NVLink) run the reference planner's GPT-2-medium MLP plans
+([8], 2x4, 2x2x2) and the Megatron plan with the PlanExecutor on a
+PeerRuntime: conversions are one pull kernel per rank, partial sums one
+in-place peer all-reduce kernel per rank, ordering by device-side flags.
+Forward output and dX/dW1/dW2 of every rank within 2e-2 of fp32 torch
+autograd on the same bf16 operands."""
+import json
+import os
+import socket
+from pathlib import Path
+
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+PLANS = Path(__file__).resolve().parent / "golden" / "plans"
+NAMES = ["megatron", "gpt2_mlp_mesh8_unlimited.json", "gpt2_mlp_mesh2x4_unlimited.json",
+         "gpt2_mlp_mesh2x2x2_unlimited.json", "gpt2_mlp_mesh2x4_96.json"]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _shard(t, spec, geo, dev):
+    coord = geo.coord_of(dev)
+    sl = []
+    for d, dim in enumerate(spec.dims):
+        s, split = 0, 1
+        for a in dim.axes:
+            s = s * geo.shape[a] + coord[a]
+            split *= geo.shape[a]
+        L = t.shape[d] // split
+        sl.append(slice(s * L, (s + 1) * L))
+    return t[tuple(sl)]
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2302_02599_b200.executor import PlanExecutor, megatron_mlp_plan
+    from paper_2302_02599_b200.peer import PeerRuntime
+
+    graph = json.loads((PLANS / "gpt2_mlp_graph.json").read_text())
+    try:
+        torch.manual_seed(2302)
+        x = torch.randn(16384, 1024, device="cuda").bfloat16()
+        w1 = (torch.randn(1024, 4096, device="cuda") / 32).bfloat16()
+        w2 = (torch.randn(4096, 1024, device="cuda") / 64).bfloat16()
+        gy = torch.randn(16384, 1024, device="cuda").bfloat16()
+        xr, w1r, w2r = (t.float().requires_grad_() for t in (x, w1, w2))
+        y_ref = torch.nn.functional.gelu(xr @ w1r) @ w2r
+        y_ref.backward(gy.float())
+        ref = {"x": xr.grad, "w1": w1r.grad, "w2": w2r.grad}
+        y_ref = y_ref.detach()
+        for name in NAMES:
+            plan = megatron_mlp_plan() if name == "megatron" else \
+                json.loads((PLANS / name).read_text())
+            shape = plan["mesh"]["shape"] if "mesh" in plan else [8]
+            rt = PeerRuntime(shape, rank, 0, heap_bytes=1 << 30)
+            ex = PlanExecutor(rt, graph, plan)
+            for step in range(2):  # the second step recycles the heap
+                out = ex.forward({"x": x, "w1": w1, "w2": w2}, train=True)
+                grads = ex.backward(gy, input_grads=True)
+            torch.cuda.synchronize()
+            err = ((out[0].double() - y_ref.double()).abs().max() / y_ref.abs().max()).item()
+            ok = err <= 2e-2
+            for nid, g in grads.items():
+                want = _shard(ref[nid], ex.spec[nid], rt.geo, rank)
+                e = ((g[0].double() - want.double()).abs().max() / want.abs().max()).item()
+                ok = ok and g[0].shape == want.shape and e <= 2e-2
+                err = max(err, e)
+            q.put((rank, name, ok, err))
+            torch.cuda.synchronize()
+            dist.barrier()
+            rt.close()
+            dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_mlp_plans_over_peer_memory(cuda):
+    world = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=900)
+    res = []
+    while not q.empty():
+        res.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert len(res) == world * len(NAMES), res
+    assert all(r[2] for r in res), [r for r in res if not r[2]]
