@@ -27,7 +27,7 @@ import torch
 
 from . import _capi as A
 from .layout import DeviceMesh, ShardingSpec, TensorMeta, check
-from .runtime import PeerMesh, Mesh, MatmulStrategy, _CudaArray, _DTYPE_CODE, _stream_handle
+from .runtime import PeerMesh, Mesh, MatmulStrategy, _DTYPE_CODE, _stream_handle
 
 
 def _group(geo: DeviceMesh, rank: int, axes: Sequence[int]) -> list:
@@ -71,7 +71,6 @@ class PeerRuntime:
         self.heap_bytes = heap_bytes
         self._off = 0
         self._local = Mesh.local([1], device=device)  # per-rank GEMMs on the local shards
-        self._epoch_of_last_read = 0
 
     # ---- symmetric heap ------------------------------------------------------
     def empty(self, shape, dtype) -> torch.Tensor:
@@ -186,13 +185,45 @@ class PeerRuntime:
                                        gelu_save=None if gelu_save is None else
                                        [gelu_save[0].view(cv.shape)])
             return
-        self._local.sharded_matmul(st, am, bm, [av], [b], [cv], b_layout=b_layout, stream=stream)
-        self.all_reduce(strategy.reduce_axes, [c], stream=stream)
+        P = self.num_devices
+        M, N = cv.shape
+        if (sorted(strategy.reduce_axes) == list(range(self.geo.rank())) and 1 < P <= 8
+                and M % (P * 128) == 0 and self._in_heap(c)):
+            self._gemm_allreduce(av, b, cv, b_layout, stream)
+        else:
+            self._local.sharded_matmul(st, am, bm, [av], [b], [cv], b_layout=b_layout,
+                                       stream=stream)
+            self.all_reduce(strategy.reduce_axes, [c], stream=stream)
         if gelu_save is not None:
             gelu_save[0].copy_(c)
         if gelu or gelu_save is not None:
             from .runtime import gelu as gelu_fn
             gelu_fn(c, c, stream=stream)
+
+    def _gemm_allreduce(self, a, b, c, b_layout, stream) -> None:
+        """Partial sum over every rank, fused: the GEMM epilogue stores each
+        fp32 row block of the partial into its owner's heap staging slab
+        (reduce-scatter traffic overlapping the MMAs); each owner sums its
+        slabs and stores its rows into every rank's `c` (heap, same offset)."""
+        P, r = self.num_devices, self.rank
+        M, N = c.shape
+        rpo = M // P
+        staging = self.empty((P, rpo, N), torch.float32)
+        slabs = (C.c_void_p * P)(*[p + r * rpo * N * 4 for p in self._peer_ptrs(staging, range(P))])
+        eb = c.element_size()
+        outs = (C.c_void_p * P)(*[p + r * rpo * N * eb for p in self._peer_ptrs(c, range(P))])
+        pm, lib, sh = self.pm, A.lib(), _stream_handle(stream)
+        check(lib.apl_peer_gemm_scatter(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), slabs,
+                                        P, M, N, a.shape[1], a.stride(0), b.stride(0),
+                                        A.B_KN if b_layout == "kn" else A.B_NK, sh))
+        pm.epoch += 1
+        e = pm.epoch
+        self._store(False, stream)
+        self._wait(self._all_others(), e, False, stream)
+        check(lib.apl_peer_reduce_gather(C.c_void_p(staging.data_ptr()), P, rpo * N, outs, P,
+                                         _DTYPE_CODE[c.dtype], sh))
+        self._store(True, stream)
+        self._wait(self._all_others(), e, True, stream)
 
     def sharded_matmul_backward(self, strategy: MatmulStrategy, a_meta, b_meta, a_shards,
                                 b_shards, dc_shards, da_shards=None, db_shards=None,

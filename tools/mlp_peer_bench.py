@@ -1,12 +1,14 @@
-"""BASELINE config 5 on N GPUs over peer memory (one process per GPU):
-the GPT-2-medium MLP with the pinned Megatron selection -- fc1 split-n:0
-(local tcgen05 GEMM + GELU on each rank's W1 column block), fc2 split-k:0
-(GEMM + all-reduce fused over peer memory: the epilogue scatters fp32 row
-blocks to their owners, owners reduce and store into every rank). Prints one
-JSON line (rank 0): ms per forward (max over ranks) and TFLOP/s of the whole
-job, plus max|err| vs an fp32 torch forward on rank 0.
+"""BASELINE config 5 on N GPUs over peer memory (one process per GPU): the
+GPT-2-medium MLP executed by the PlanExecutor on a PeerRuntime -- the pinned
+Megatron plan (fc1 split-n:0 local GEMM + GELU; fc2 split-k:0 GEMM +
+all-reduce fused over peer memory) or a reference planner plan
+(conversions as one pull kernel per rank, partial sums as one peer
+all-reduce kernel). Prints one JSON line (rank 0): ms per forward and per
+training step (max over ranks), TFLOP/s of the whole job, and the max
+relative error of the forward vs an fp32 torch forward.
 
-    python -m torch.distributed.run --nproc-per-node N tools/mlp_peer_bench.py [--tokens T]
+    python -m torch.distributed.run --nproc-per-node N tools/mlp_peer_bench.py \\
+        [--plan megatron|tests/golden/plans/gpt2_mlp_mesh2x4_unlimited.json]
 """
 import argparse
 import json
@@ -20,65 +22,72 @@ sys.path.insert(0, str(ROOT))
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from paper_2302_02599_b200 import ShardingSpec  # noqa: E402
-from paper_2302_02599_b200.runtime import MatmulStrategy, PeerMesh  # noqa: E402
+from paper_2302_02599_b200.executor import PlanExecutor, megatron_mlp_plan  # noqa: E402
+from paper_2302_02599_b200.peer import PeerRuntime  # noqa: E402
+
+GRAPH = json.loads((ROOT / "tests" / "golden" / "plans" / "gpt2_mlp_graph.json").read_text())
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--tokens", type=int, default=16384)
+    ap.add_argument("--plan", default="megatron")
     ap.add_argument("--iters", type=int, default=20)
     args = ap.parse_args()
     ws, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     dev = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
     torch.cuda.set_device(dev)
     dist.init_process_group("gloo")
-    M, D, H = args.tokens, 1024, 4096
+    plan = megatron_mlp_plan() if args.plan == "megatron" else json.loads(Path(args.plan).read_text())
+    shape = plan["mesh"]["shape"] if "mesh" in plan else [ws]
     g = torch.Generator(device="cuda").manual_seed(2302)
-    x = torch.randn(M, D, device="cuda", generator=g).bfloat16()
-    w1 = (torch.randn(D, H, device="cuda", generator=g) / 32).bfloat16()
-    w2 = (torch.randn(H, D, device="cuda", generator=g) / 64).bfloat16()
-    hs = H // ws
-    w1s = w1[:, rank * hs:(rank + 1) * hs].contiguous()   # RS0 [D, H/ws]
-    w2s = w2[rank * hs:(rank + 1) * hs].contiguous()      # S0R [H/ws, D]
-    p = lambda s: ShardingSpec.parse(s, 1)  # noqa: E731
-    fc1 = MatmulStrategy("split-n:0", p("RR"), p("RS0"), p("RS0"))
-    fc2 = MatmulStrategy("split-k:0", p("RS0"), p("S0R"), p("RR"), [0])
-    pm = PeerMesh([ws], rank, dev, 16)
+    x = torch.randn(16384, 1024, device="cuda", generator=g).bfloat16()
+    w1 = (torch.randn(1024, 4096, device="cuda", generator=g) / 32).bfloat16()
+    w2 = (torch.randn(4096, 1024, device="cuda", generator=g) / 64).bfloat16()
+    gy = torch.randn(16384, 1024, device="cuda", generator=g).bfloat16()
+    rt = PeerRuntime(shape, rank, dev, heap_bytes=2 << 30)
+    ex = PlanExecutor(rt, GRAPH, plan)
+    shards = {k: ex.shard(k, v) for k, v in {"x": x, "w1": w1, "w2": w2}.items()}
     stream = torch.cuda.current_stream()
-
-    def forward():
-        h = pm.sharded_matmul(fc1, x, w1s, gelu=True, stream=stream)
-        return pm.sharded_matmul(fc2, h, w2s, stream=stream)
-
-    y = forward()
+    y = ex.forward(shards, stream=stream)[0]
     torch.cuda.synchronize()
-    err = None
+    ref = torch.nn.functional.gelu(x.float() @ w1.float()) @ w2.float()
+    err = ((y.double() - ref.double()).abs().max() / ref.abs().max()).item()
+
+    def time_it(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.iters):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / args.iters], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    fwd = time_it(lambda: ex.forward(shards, stream=stream))
+
+    def train():
+        ex.forward(shards, stream=stream, train=True)
+        ex.backward(gy, stream=stream)
+
+    trn = time_it(train)
+    flops = 2 * 2.0 * 16384 * 1024 * 4096
     if rank == 0:
-        ref = torch.nn.functional.gelu(x.float() @ w1.float()) @ w2.float()
-        err = ((y.double() - ref.double()).abs().max() / ref.abs().max()).item()
-    for _ in range(3):
-        forward()
+        print(json.dumps({"config": "configs[4]: GPT-2-medium MLP", "plan": args.plan,
+                          "mesh": shape, "n_gpus": ws, "transport": "peer (PeerRuntime)",
+                          "strategies": {k: v.name for k, v in ex.strategy.items()},
+                          "ms_per_forward": round(fwd, 4),
+                          "tflops_forward_job": round(flops / fwd / 1e9, 1),
+                          "ms_per_train_step": round(trn, 4),
+                          "tflops_train_job": round(2.5 * flops / trn / 1e9, 1),
+                          "max_rel_err": err}), flush=True)
     torch.cuda.synchronize()
     dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(args.iters):
-        forward()
-    b.record(stream)
-    torch.cuda.synchronize()
-    t = torch.tensor([a.elapsed_time(b) / args.iters], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t[0])
-    flops = 2 * 2.0 * M * D * H
-    if rank == 0:
-        print(json.dumps({"config": "configs[4]: GPT-2-medium MLP, Megatron split-n:0 / split-k:0",
-                          "n_gpus": ws, "tokens": M, "transport": "peer (fused GEMM + all-reduce)",
-                          "ms_per_forward": round(ms, 4),
-                          "tflops_job": round(flops / ms / 1e9, 1), "max_rel_err": err}),
-              flush=True)
-    dist.barrier()
-    pm.close()
+    rt.close()
     dist.destroy_process_group()
 
 
