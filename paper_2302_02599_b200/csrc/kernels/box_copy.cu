@@ -72,6 +72,21 @@ __device__ __forceinline__ uint32_t load_stream(const uint32_t* p) { return __ld
 __device__ __forceinline__ uint16_t load_stream(const uint16_t* p) { return __ldg(p); }
 __device__ __forceinline__ uint8_t load_stream(const uint8_t* p) { return __ldg(p); }
 
+// Stores; `cs` = cache-streaming (evict-first) for outputs far larger than L2.
+template <typename T>
+__device__ __forceinline__ void store_v(T* p, const T& v, bool cs) {
+  *p = v;
+}
+template <>
+__device__ __forceinline__ void store_v<uint4>(uint4* p, const uint4& v, bool cs) {
+  if (cs)
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+  else
+    *p = v;
+}
+
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
   return f.div == 1 ? n : (__umulhi(n, f.mul) >> f.shr);
 }
@@ -143,6 +158,7 @@ __global__ void __launch_bounds__(256, MINB)
     const int t0 = lo;
     const int64_t next_begin = (lo + 1 < ntasks) ? tab[lo + 1].unit_begin : total;
     const DevCopy& D = tab[lo];
+    const bool cs = (lockstep & 2) != 0;
     // Register copy of the chunk's descriptor.
     const int64_t begin = D.unit_begin;
     const FastDiv upr = D.units_per_run;
@@ -220,14 +236,15 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
         for (int j = 0; j < kCopyMaxFan; ++j)
           if (j < ndst)
-            *reinterpret_cast<T*>(ptrs.dst[(dbuf[j >> 2] >> (8 * (j & 3))) & 0xFF] + dd[u]) = v[u];
+            store_v(reinterpret_cast<T*>(ptrs.dst[(dbuf[j >> 2] >> (8 * (j & 3))) & 0xFF] + dd[u]),
+                    v[u], cs);
       } else if (slow_task[u] >= 0) {
         const DevCopy& c = tab[slow_task[u]];
         for (int j = 0; j < c.ndst; ++j)
           *reinterpret_cast<T*>(ptrs.dst[c.dst_bufs[j]] + dd[u]) = v[u];
       }
     }
-    if (lockstep) __syncthreads();
+    if (lockstep & 1) __syncthreads();
   }
 }
 
@@ -259,7 +276,7 @@ int copy_variant(int max_outer, int max_fan) {
 
 template <int V, int U, int MINB, bool SPLIT = false>
 void launch_vu(int no, int64_t total, const DevCopy* t, const int64_t* begins, int n,
-               const PtrTable& p, cudaStream_t s, bool lock) {
+               const PtrTable& p, cudaStream_t s, bool lock, bool streaming) {
   constexpr int kThreads = 256;
   static int ctas_per_sm = env_int("APL_COPY_CTAS_PER_SM", MINB);
   // Tables larger than kCopySmemTasks run as consecutive launches over
@@ -276,7 +293,11 @@ void launch_vu(int no, int64_t total, const DevCopy* t, const int64_t* begins, i
     // Block barrier per chunk (warps write each chunk together): +7% on
     // plain and fan-out copies, -3% on strided boxes (r01 lock probe).
     static const int forced_lock = env_int("APL_COPY_LOCKSTEP", -1);
-    const int lockstep = forced_lock >= 0 ? forced_lock : (lock ? 1 : 0);
+    // Cache-streaming stores for single-destination launches writing far
+    // more than L2 holds (+2% on a 1 GiB copy; -1% on fan-out, so not there).
+    static const int cs_env = env_int("APL_COPY_CS", -1);
+    const bool cs = cs_env >= 0 ? cs_env != 0 : streaming;
+    const int lockstep = (forced_lock >= 0 ? forced_lock : (lock ? 1 : 0)) | (cs ? 2 : 0);
     const DevCopy* tk = t + k;
     switch (no) {
       case 0:
@@ -301,24 +322,25 @@ void launch_vu(int no, int64_t total, const DevCopy* t, const int64_t* begins, i
 
 template <int V>
 void launch_v(int no, int fan, bool split, int64_t total_units, const DevCopy* t,
-              const int64_t* begins, int n, const PtrTable& p, cudaStream_t s) {
+              const int64_t* begins, int n, const PtrTable& p, cudaStream_t s, int64_t wbytes) {
+  const bool streaming = fan == 1 && wbytes > (int64_t{256} << 20);
   const bool lock = fan > 1 || no == 0;
   // Split tables get their own instantiation so the chunk arithmetic does
   // not cost the common kernels registers (U=8 @ 2 CTAs/SM: no spills).
-  if (split) return launch_vu<V, 8, 2, true>(no, total_units, t, begins, n, p, s, lock);
+  if (split) return launch_vu<V, 8, 2, true>(no, total_units, t, begins, n, p, s, lock, streaming);
   if constexpr (V == 16) {
     switch (copy_variant(no, fan)) {
       case 1:
-        return launch_vu<V, 4, 4>(no, total_units, t, begins, n, p, s, lock);
+        return launch_vu<V, 4, 4>(no, total_units, t, begins, n, p, s, lock, streaming);
       case 2:
-        return launch_vu<V, 16, 1>(no, total_units, t, begins, n, p, s, lock);
+        return launch_vu<V, 16, 1>(no, total_units, t, begins, n, p, s, lock, streaming);
       case 3:
-        return launch_vu<V, 8, 3>(no, total_units, t, begins, n, p, s, lock);
+        return launch_vu<V, 8, 3>(no, total_units, t, begins, n, p, s, lock, streaming);
       default:
         break;
     }
   }
-  launch_vu<V, 8, 2>(no, total_units, t, begins, n, p, s, lock);
+  launch_vu<V, 8, 2>(no, total_units, t, begins, n, p, s, lock, streaming);
 }
 
 }  // namespace
@@ -350,23 +372,23 @@ int sm_count() {
 
 cudaError_t launch_box_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,
                             int64_t total_units, int vec_bytes, int max_outer, int max_fan, bool split,
-                            const PtrTable& ptrs, cudaStream_t stream) {
+                            const PtrTable& ptrs, cudaStream_t stream, int64_t write_bytes) {
   if (ntasks <= 0 || total_units <= 0) return cudaSuccess;
   switch (vec_bytes) {
     case 16:
-      launch_v<16>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream);
+      launch_v<16>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream, write_bytes);
       break;
     case 8:
-      launch_v<8>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream);
+      launch_v<8>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream, write_bytes);
       break;
     case 4:
-      launch_v<4>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream);
+      launch_v<4>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream, write_bytes);
       break;
     case 2:
-      launch_v<2>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream);
+      launch_v<2>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream, write_bytes);
       break;
     default:
-      launch_v<1>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream);
+      launch_v<1>(max_outer, max_fan, split, total_units, d_table, begins, ntasks, ptrs, stream, write_bytes);
       break;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -248,7 +248,7 @@ void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stre
     return;
   }
   check_cuda(launch_box_copy(c.table, c.begins.data(), c.ntasks, c.total_units, c.vec, c.max_outer, c.max_fan, c.split, ptrs,
-                             stream),
+                             stream, c.write_bytes),
              "box_copy launch");
 }
 

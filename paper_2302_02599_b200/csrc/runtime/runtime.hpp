@@ -32,7 +32,8 @@ int sm_count();
 // begins: host copy of the table's unit_begin column (slicing into launches).
 cudaError_t launch_box_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,
                             int64_t total_units, int vec_bytes, int max_outer, int max_fan, bool split,
-                            const PtrTable& ptrs, cudaStream_t stream);
+                            const PtrTable& ptrs, cudaStream_t stream,
+                            int64_t write_bytes = 0);
 cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int groups,
                                    int group_size, size_t count, int dtype,
                                    cudaStream_t stream);
