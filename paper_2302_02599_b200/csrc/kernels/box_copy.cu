@@ -294,7 +294,7 @@ void launch_vu(int no, int64_t total, const DevCopy* t, const int64_t* begins, i
     // plain and fan-out copies, -3% on strided boxes (r01 lock probe).
     static const int forced_lock = env_int("APL_COPY_LOCKSTEP", -1);
     // Cache-streaming stores for single-destination launches writing far
-    // more than L2 holds (+2% on a 1 GiB copy; -1% on fan-out, so not there).
+    // at least half of L2 (+2-3% on 64 MiB-1 GiB copies; -1% on fan-out, so not there).
     static const int cs_env = env_int("APL_COPY_CS", -1);
     const bool cs = cs_env >= 0 ? cs_env != 0 : streaming;
     const int lockstep = (forced_lock >= 0 ? forced_lock : (lock ? 1 : 0)) | (cs ? 2 : 0);
@@ -323,7 +323,7 @@ void launch_vu(int no, int64_t total, const DevCopy* t, const int64_t* begins, i
 template <int V>
 void launch_v(int no, int fan, bool split, int64_t total_units, const DevCopy* t,
               const int64_t* begins, int n, const PtrTable& p, cudaStream_t s, int64_t wbytes) {
-  const bool streaming = fan == 1 && wbytes > (int64_t{256} << 20);
+  const bool streaming = fan == 1 && wbytes >= (int64_t{64} << 20);
   const bool lock = fan > 1 || no == 0;
   // Split tables get their own instantiation so the chunk arithmetic does
   // not cost the common kernels registers (U=8 @ 2 CTAs/SM: no spills).

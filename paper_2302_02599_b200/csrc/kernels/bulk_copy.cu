@@ -99,7 +99,7 @@ __device__ __forceinline__ bool resolve_unit(const DevCopy* table, int ntasks, i
 
 __global__ void __launch_bounds__(64, 1)
     bulk_copy_kernel(const DevCopy* __restrict__ table, int ntasks, int64_t first, int64_t total,
-                     const __grid_constant__ PtrTable ptrs) {
+                     int evict_first, const __grid_constant__ PtrTable ptrs) {
   // Shared memory: [descriptor table (this launch's <= kBulkSmemTasks)] [ring].
   // The table is staged once per CTA so unit resolution is a broadcast smem
   // search, not a chain of dependent global loads per batch.
@@ -151,6 +151,10 @@ __global__ void __launch_bounds__(64, 1)
       }
     }
   } else {  // storer
+    // Outputs of >= 64 MiB: stores marked evict-first (+3-7% at 64 MiB-1 GiB).
+    uint64_t policy = 0;
+    if (evict_first)
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     int i = 0, prev = -1;
     for (int64_t b = blockIdx.x; b < batches; b += gridDim.x, ++i) {
       const int s = i % kStages;
@@ -160,9 +164,16 @@ __global__ void __launch_bounds__(64, 1)
         const uint32_t from = saddr(stage + s * kStageBytes + lane * kBulkSeg);
         for (int j = 0; j < u.d->ndst; ++j) {
           char* dst = ptrs.dst[u.d->dst_bufs[j]] + u.dd;
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                       "r"(from), "r"(u.bytes)
-                       : "memory");
+          if (evict_first)
+            asm volatile(
+                "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                    dst),
+                "r"(from), "r"(u.bytes), "l"(policy)
+                : "memory");
+          else
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                         "r"(from), "r"(u.bytes)
+                         : "memory");
         }
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -184,8 +195,14 @@ __global__ void __launch_bounds__(64, 1)
 int bulk_smem_bytes() { return kSmemBytes; }
 
 cudaError_t launch_bulk_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,
-                             int64_t total_units, const PtrTable& ptrs, cudaStream_t stream) {
+                             int64_t total_units, const PtrTable& ptrs, cudaStream_t stream,
+                             int64_t write_bytes) {
   if (ntasks <= 0 || total_units <= 0) return cudaSuccess;
+  static const int ef_env = [] {
+    const char* e = std::getenv("APL_COPY_CS");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int ef = ef_env >= 0 ? ef_env : (write_bytes >= (int64_t{64} << 20) ? 1 : 0);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(bulk_copy_kernel,
@@ -199,7 +216,7 @@ cudaError_t launch_bulk_copy(const DevCopy* d_table, const int64_t* begins, int 
     const int64_t end = k + m < ntasks ? begins[k + m] : total_units;
     const int64_t batches = (end - first + 31) / 32;
     const int grid = static_cast<int>(std::min<int64_t>(batches, sm_count()));
-    bulk_copy_kernel<<<grid, 64, kSmemBytes, stream>>>(d_table + k, m, first, end, ptrs);
+    bulk_copy_kernel<<<grid, 64, kSmemBytes, stream>>>(d_table + k, m, first, end, ef, ptrs);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();

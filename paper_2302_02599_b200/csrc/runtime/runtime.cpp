@@ -244,7 +244,8 @@ void free_copies(CompiledCopies& c) {
 void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream) {
   if (c.empty()) return;
   if (c.bulk) {
-    check_cuda(launch_bulk_copy(c.table, c.begins.data(), c.ntasks, c.total_units, ptrs, stream), "bulk copy launch");
+    check_cuda(launch_bulk_copy(c.table, c.begins.data(), c.ntasks, c.total_units, ptrs, stream,
+                                c.write_bytes), "bulk copy launch");
     return;
   }
   check_cuda(launch_box_copy(c.table, c.begins.data(), c.ntasks, c.total_units, c.vec, c.max_outer, c.max_fan, c.split, ptrs,

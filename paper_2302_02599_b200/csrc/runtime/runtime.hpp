@@ -86,7 +86,8 @@ struct CompiledCopies {
 };
 
 cudaError_t launch_bulk_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,
-                             int64_t total_units, const PtrTable& ptrs, cudaStream_t stream);
+                             int64_t total_units, const PtrTable& ptrs, cudaStream_t stream,
+                             int64_t write_bytes = 0);
 // True when every run of the table suits the TMA bulk engine.
 bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec);
 
