@@ -198,3 +198,34 @@ def test_megatron_plan_backward(cuda, mlp_reference, fuse):
     # axis 0 in the dA GEMM) is bit-identical on every device.
     for g in grads["x"][1:]:
         assert torch.equal(g, grads["x"][0])
+
+
+def test_batched_matmul_catalog_backward_on_2x2(cuda):
+    """Backward of every batched-matmul strategy (split-b/m/n/k and pairs,
+    intraop.cpp:208-231): dA = dC . B^T and dB = A^T . dC per batch element,
+    partial sums over the n / m axes reduced (batch axes never are)."""
+    from paper_2302_02599_b200.strategies import matmul_strategies
+
+    mesh = Mesh.local([2, 2])
+    geo = mesh.geo
+    bsz, m, k, n = 8, 256, 128, 192
+    torch.manual_seed(11)
+    a = torch.randn(bsz, m, k, device="cuda").bfloat16()
+    b = (torch.randn(bsz, k, n, device="cuda") / k ** 0.5).bfloat16()
+    dc = torch.randn(bsz, m, n, device="cuda").bfloat16()
+    ref_da = torch.bmm(dc.double(), b.double().transpose(1, 2))
+    ref_db = torch.bmm(a.double().transpose(1, 2), dc.double())
+    am, bm = TensorMeta((bsz, m, k), 2), TensorMeta((bsz, k, n), 2)
+    cat = matmul_strategies(geo, am, bm, batched=True)
+    assert len(cat) > 4
+    for st in cat:
+        a_sh = [shard(a, st.a, geo, d) for d in range(4)]
+        b_sh = [shard(b, st.b, geo, d) for d in range(4)]
+        dc_sh = [shard(dc, st.c, geo, d) for d in range(4)]
+        da = [torch.empty_like(t) for t in a_sh]
+        db = [torch.empty(t.shape, dtype=torch.float32, device="cuda") for t in b_sh]
+        mesh.sharded_matmul_backward(st, am, bm, a_sh, b_sh, dc_sh, da, db, b_layout="kn")
+        torch.cuda.synchronize()
+        for d in range(4):
+            assert rel_err(da[d], shard(ref_da, st.a, geo, d)) <= TOL, (st.name, d, "dA")
+            assert rel_err(db[d], shard(ref_db, st.b, geo, d)) <= 1e-4, (st.name, d, "dB")
