@@ -340,6 +340,47 @@ struct GemmArgs {
   // staging slab for this rank, typically a peer-mapped pointer), so the
   // partial tile crosses NVLink while the next tile's MMAs run.
   int scatter_rows;
+  // Stream-K (single-CTA kernel, reduce == fan == 1): CTA b owns the
+  // k-iterations [b*T/G, (b+1)*T/G) of the tile-major iteration space, so an
+  // under-filled problem keeps every SM busy. A tile split across CTAs is
+  // finished by the CTA holding its first k-block (the "head", at the end of
+  // its range); the others (at the start of theirs) write fp32 partial tiles
+  // to sk_ws[cta] and raise sk_flags[cta]; the head adds them in CTA order
+  // (deterministic) and clears the flags.
+  int streamk;
+  float* sk_ws;
+  int* sk_flags;
+};
+
+// Segments of the (tile, k-block) iteration space a CTA processes, in order.
+struct SegIter {
+  int64_t pos, end, total;
+  int t, tiles, grid, KT;
+  bool sk;
+  __device__ SegIter(bool streamk, int b, int G, int tiles_, int KT_)
+      : tiles(tiles_), grid(G), KT(KT_), sk(streamk) {
+    total = static_cast<int64_t>(tiles_) * KT_;
+    pos = sk ? total * b / G : 0;
+    end = sk ? total * (b + 1) / G : 0;
+    t = b;
+  }
+  __device__ bool next(int& tile, int& k0, int& k1) {
+    if (sk) {
+      if (pos >= end) return false;
+      tile = static_cast<int>(pos / KT);
+      k0 = static_cast<int>(pos - static_cast<int64_t>(tile) * KT);
+      const int64_t left = end - pos;
+      k1 = left < KT - k0 ? k0 + static_cast<int>(left) : KT;
+      pos += k1 - k0;
+      return true;
+    }
+    if (t >= tiles) return false;
+    tile = t;
+    k0 = 0;
+    k1 = KT;
+    t += grid;
+    return true;
+  }
 };
 
 template <int BN, int kEpi, bool kOutF32, bool kBMN, bool kAMN>
@@ -391,13 +432,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  const int KT = kblocks * args.reduce;
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;  // ring position across tiles
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      SegIter seg(args.streamk != 0, blockIdx.x, gridDim.x, tiles, KT);
+      int t, k0, k1;
+      while (seg.next(t, k0, k1)) {
         const int g = t / per_problem, lt = t % per_problem;
         const int m0 = (lt / n_tiles) * kBM, n0 = (lt % n_tiles) * BN;
-        for (int kk = 0; kk < kblocks * args.reduce; ++kk, ++it) {
+        for (int kk = k0; kk < k1; ++kk, ++it) {
           const int kb = kk % kblocks;
           const CUtensorMap* map_a = &args.a[g * args.reduce + kk / kblocks];
           const CUtensorMap* map_b = &args.b[g * args.reduce + kk / kblocks];
@@ -428,12 +472,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc<BN, kBMN, kAMN>();
       int it = 0, local = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      SegIter seg(args.streamk != 0, blockIdx.x, gridDim.x, tiles, KT);
+      int t, k0, k1;
+      for (; seg.next(t, k0, k1); ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + uint32_t(acc * BN);
-        for (int kk = 0; kk < kblocks * args.reduce; ++kk, ++it) {
+        for (int kk = k0; kk < k1; ++kk, ++it) {
           const int s = it % S::kStages;
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&full[s], phase);
@@ -449,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             mma_bf16(d, da + kAdvA * k, db + kAdvB * k, idesc,
-                     (kk > 0 || k > 0) ? 1u : 0u);
+                     (kk > k0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
         }
@@ -457,16 +503,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // Epilogue warps 2..5 -> TMEM lane quarter (warp % 4).
+    // Epilogue warps 2..9 -> TMEM lane quarter (warp % 4), half the columns each.
     const int quarter = warp % 4;          // TMEM lanes this warp may access
     const int half = (warp - 2) / 4;       // which half of the tile's columns
     int local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    SegIter seg(args.streamk != 0, blockIdx.x, gridDim.x, tiles, KT);
+    int t, k0, k1;
+    for (; seg.next(t, k0, k1); ++local) {
       const int acc = local & 1;
       const int g = t / per_problem, lt = t % per_problem;
       const int m0 = (lt / n_tiles) * kBM, n0 = (lt % n_tiles) * BN;
       void* const* outs = args.c + g * args.fan;
-      int row = m0 + quarter * 32 + lane;
+      const int trow = quarter * 32 + lane;  // row within the tile
+      int row = m0 + trow;
       int rows = M, fan = args.fan;
       if (args.scatter_rows > 0) {
         const int owner = m0 / args.scatter_rows;
@@ -475,6 +524,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         rows = args.scatter_rows;
         fan = 1;
       }
+      // stream-K roles: partial (k0 > 0: write fp32 tile for the head) or
+      // head of a split tile (k0 == 0, k1 < KT: add the later CTAs' partials)
+      const bool partial = k0 > 0;
+      const bool head = !partial && k1 < KT;
+      int c_first = 0, c_last = -1;
+      if (head) {
+        // CTAs after this one whose ranges start inside this tile
+        // (CTAs with empty ranges contribute nothing and raise no flag)
+        const int64_t tile_end = static_cast<int64_t>(t + 1) * KT;
+        const int G = gridDim.x;
+        c_first = blockIdx.x + 1;
+        c_last = blockIdx.x;
+        while (c_last + 1 < G && seg.total * (c_last + 1) / G < tile_end) ++c_last;
+        for (int c = c_first; c <= c_last; ++c) {
+          if (seg.total * c / G == seg.total * (c + 1) / G) continue;  // empty range
+          volatile int* f = args.sk_flags + c;
+          while (true) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if (v != 0) break;
+            __nanosleep(64);
+          }
+        }
+      }
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
@@ -482,6 +555,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
         uint32_t r[32];
         tmem_ld32(lane_addr + uint32_t(c), r);
+        if (partial) {
+          float4* w = reinterpret_cast<float4*>(args.sk_ws +
+                                                (static_cast<size_t>(blockIdx.x) * kBM + trow) * BN + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            w[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                               __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          continue;
+        }
+        for (int cc = c_first; cc <= c_last; ++cc) {
+          if (seg.total * cc / gridDim.x == seg.total * (cc + 1) / gridDim.x) continue;
+          const float4* w = reinterpret_cast<const float4*>(
+              args.sk_ws + (static_cast<size_t>(cc) * kBM + trow) * BN + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 p = w[i];
+            r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + p.x);
+            r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + p.y);
+            r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + p.z);
+            r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + p.w);
+          }
+        }
         epi_store32<kEpi, kOutF32>(outs, fan, ldc, rows, N, row, n0 + c, r, args.aux[g],
                                    args.ldaux);
       }
@@ -489,6 +584,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (partial || head) {
+        // all 8 epilogue warps finished writing (partial) / reading (head)
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (warp == 2 && lane == 0) {
+          if (partial) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(args.sk_flags + blockIdx.x),
+                         "r"(1)
+                         : "memory");
+          } else {
+            for (int cc = c_first; cc <= c_last; ++cc) args.sk_flags[cc] = 0;
+          }
+        }
+      }
     }
   }
 
@@ -790,7 +899,7 @@ cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
     return n > 0 ? n : 148;
   }();
   const int tiles = ((args.N + BN - 1) / BN) * ((args.M + kBM - 1) / kBM) * args.count;
-  const int grid = tiles < sms ? tiles : sms;
+  const int grid = args.streamk ? sms : (tiles < sms ? tiles : sms);
   kernel<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -863,6 +972,57 @@ cudaError_t dispatch_pair(const GemmArgs& args, bool out_f32, int epi, bool a_km
   }
 }
 
+// Stream-K for single-CTA launches whose tiles fill the SMs badly, e.g.
+// per-GPU shards of 8-way strategies (opt-in, see streamk_setup). Workspace
+// (fp32 partial tiles, one per CTA) and flags are kept per stream.
+struct StreamKWs {
+  float* ws = nullptr;
+  int* flags = nullptr;
+};
+
+int stream_k_forced() {
+  static const int forced = [] {
+    const char* e = std::getenv("APL_GEMM_STREAMK");
+    return e ? std::atoi(e) : -1;
+  }();
+  return forced;
+}
+bool stream_k_enabled() { return stream_k_forced() == 1; }
+
+bool streamk_setup(GemmArgs& args, int tiles, int kt, cudaStream_t stream) {
+  const int forced = stream_k_forced();
+  static int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  const int waves = (tiles + sms - 1) / sms;
+  const double fill = static_cast<double>(tiles) / (static_cast<double>(waves) * sms);
+  // Opt-in (APL_GEMM_STREAMK=1): on the r01 per-GPU shapes the 128 x 256
+  // stream-K tiles were L2-latency bound (2048 x 1024 x 4096: 405 vs 675
+  // TFLOP/s with plain 128 x 128 tiles), so the default keeps the tile grid.
+  (void)fill;
+  (void)waves;
+  const bool want = forced == 1 && kt >= 4 && static_cast<int64_t>(tiles) * kt >= 2 * sms;
+  if (!want || args.reduce != 1 || args.fan != 1 || args.scatter_rows > 0) return false;
+  static std::mutex mu;
+  static std::map<cudaStream_t, StreamKWs> pool;
+  std::lock_guard<std::mutex> hold(mu);
+  StreamKWs& w = pool[stream];
+  if (w.ws == nullptr) {
+    if (cudaMalloc(&w.ws, static_cast<size_t>(sms) * kBM * 256 * sizeof(float)) != cudaSuccess)
+      return false;
+    if (cudaMalloc(&w.flags, static_cast<size_t>(sms) * sizeof(int)) != cudaSuccess ||
+        cudaMemset(w.flags, 0, static_cast<size_t>(sms) * sizeof(int)) != cudaSuccess)
+      return false;
+  }
+  args.streamk = 1;
+  args.sk_ws = w.ws;
+  args.sk_flags = w.flags;
+  return true;
+}
+
 // CTA-pair kernel for problems big enough to fill 256 x 256 tiles;
 // APL_GEMM_PAIR=0/1 forces the choice.
 bool use_pair(int M, int N, int count) {
@@ -913,7 +1073,10 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
     }();
     const int count = std::min(groups, per_launch);
     const int tiles256 = ((M + kBM - 1) / kBM) * ((N + 255) / 256) * count;
-    if (bn == 256 && tiles256 < sms) bn = 128;
+    // stream-K keeps the 128 x 256 tiles (less operand traffic per FLOP) and
+    // spreads their k-iterations over every SM instead
+    const bool sk_ok = !paired && reduce == 1 && fan == 1 && stream_k_enabled();
+    if (bn == 256 && tiles256 < sms && !sk_ok) bn = 128;
   }
   // B box rows for the K-major layout: the pair kernel stages half of its
   // 256-wide N tile per CTA.
@@ -943,6 +1106,9 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
     for (int i = 0; i < args.count * fan; ++i) args.c[i] = C[first * fan + i];
     if (epi >= kEpiDGelu)
       for (int i = 0; i < args.count; ++i) args.aux[i] = aux[first + i];
+    if (!paired)
+      streamk_setup(args, ((M + kBM - 1) / kBM) * ((N + bn - 1) / bn) * args.count,
+                    (K + kBK - 1) / kBK, stream);
     cudaError_t e;
     if (paired)
       e = b_kn ? dispatch_pair<true>(args, out_f32, epi, a_km, stream)

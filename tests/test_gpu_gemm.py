@@ -208,3 +208,21 @@ def test_megatron_mlp_on_mesh8(cuda):
         assert rel_err(y[d], ref.double()) <= TOL_BF16
         assert torch.equal(y[d], y[0])  # all-reduce leaves identical replicas
         assert rel_err(h_kn[d], h[d].double()) <= 1e-2
+
+
+# Shapes that under-fill the SMs (stream-K candidates; the stream-K path itself
+# is opt-in -- run this file with APL_GEMM_STREAMK=1 to cover it).
+@pytest.mark.parametrize("m,n,k", [(2048, 1024, 4096), (1024, 512, 2048), (384, 768, 1000),
+                                   (2048, 1024, 512)])
+@pytest.mark.parametrize("gelu", [False, True])
+def test_gemm_stream_k_shapes(cuda, m, n, k, gelu):
+    torch.manual_seed(m + k)
+    a = torch.randn(m, k, device="cuda").bfloat16()
+    bt = (torch.randn(n, k, device="cuda") / k ** 0.5).bfloat16()
+    for _ in range(2):  # the second call reuses the stream's workspace and flags
+        out = gemm(a, bt, gelu=gelu)
+        torch.cuda.synchronize()
+        assert rel_err(out, ref_mm(a, bt, gelu)) <= TOL_BF16
+    out32 = gemm(a, bt, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert rel_err(out32, ref_mm(a, bt)) <= TOL_F32 * 10
