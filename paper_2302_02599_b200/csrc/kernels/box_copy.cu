@@ -143,9 +143,22 @@ __global__ void __launch_bounds__(256, MINB)
   // contiguous range per CTA measured 2-5% slower). A CTA's chunks only move
   // forward, so each lookup is a binary search over the table entries at or
   // after the previous chunk's.
+  // (lockstep bit 2: contiguous chunk range per CTA instead)
+  const int64_t nchunks = (total - first + chunk - 1) / chunk;
+  int64_t ci, cend, cstep;
+  if (lockstep & 4) {
+    const int64_t span = (nchunks + gridDim.x - 1) / gridDim.x;
+    ci = static_cast<int64_t>(blockIdx.x) * span;
+    cend = ci + span < nchunks ? ci + span : nchunks;
+    cstep = 1;
+  } else {
+    ci = blockIdx.x;
+    cend = nchunks;
+    cstep = gridDim.x;
+  }
   int lo = 0;
-  for (int64_t base = first + static_cast<int64_t>(blockIdx.x) * chunk; base < total;
-       base += static_cast<int64_t>(gridDim.x) * chunk) {
+  for (; ci < cend; ci += cstep) {
+    const int64_t base = first + ci * chunk;
     if (lo + 1 < ntasks && tab[lo + 1].unit_begin <= base) {
       int hi = ntasks - 1;
       ++lo;
@@ -276,7 +289,7 @@ int copy_variant(int max_outer, int max_fan) {
 
 template <int V, int U, int MINB, bool SPLIT = false>
 void launch_vu(int no, int64_t total, const DevCopy* t, const int64_t* begins, int n,
-               const PtrTable& p, cudaStream_t s, bool lock, bool streaming) {
+               const PtrTable& p, cudaStream_t s, bool lock, bool streaming, bool spanning) {
   constexpr int kThreads = 256;
   static int ctas_per_sm = env_int("APL_COPY_CTAS_PER_SM", MINB);
   // Tables larger than kCopySmemTasks run as consecutive launches over
@@ -297,7 +310,13 @@ void launch_vu(int no, int64_t total, const DevCopy* t, const int64_t* begins, i
     // at least half of L2 (+2-3% on 64 MiB-1 GiB copies; -1% on fan-out, so not there).
     static const int cs_env = env_int("APL_COPY_CS", -1);
     const bool cs = cs_env >= 0 ? cs_env != 0 : streaming;
-    const int lockstep = (forced_lock >= 0 ? forced_lock : (lock ? 1 : 0)) | (cs ? 2 : 0);
+    // Contiguous chunk range per CTA for strided single-destination launches
+    // of >= 512 MiB (r01 span probe: +5% at 1 GiB with 64 pieces, -1..7% at
+    // 128 MiB, where round-robin keeps the grid on shared DRAM pages).
+    static const int span_env = env_int("APL_COPY_SPAN", -1);
+    const bool span = span_env >= 0 ? span_env != 0 : (no > 0 && spanning);
+    const int lockstep =
+        (forced_lock >= 0 ? forced_lock : (lock ? 1 : 0)) | (cs ? 2 : 0) | (span ? 4 : 0);
     const DevCopy* tk = t + k;
     switch (no) {
       case 0:
@@ -324,23 +343,24 @@ template <int V>
 void launch_v(int no, int fan, bool split, int64_t total_units, const DevCopy* t,
               const int64_t* begins, int n, const PtrTable& p, cudaStream_t s, int64_t wbytes) {
   const bool streaming = fan == 1 && wbytes >= (int64_t{64} << 20);
+  const bool spanning = fan == 1 && wbytes >= (int64_t{512} << 20);
   const bool lock = fan > 1 || no == 0;
   // Split tables get their own instantiation so the chunk arithmetic does
   // not cost the common kernels registers (U=8 @ 2 CTAs/SM: no spills).
-  if (split) return launch_vu<V, 8, 2, true>(no, total_units, t, begins, n, p, s, lock, streaming);
+  if (split) return launch_vu<V, 8, 2, true>(no, total_units, t, begins, n, p, s, lock, streaming, spanning);
   if constexpr (V == 16) {
     switch (copy_variant(no, fan)) {
       case 1:
-        return launch_vu<V, 4, 4>(no, total_units, t, begins, n, p, s, lock, streaming);
+        return launch_vu<V, 4, 4>(no, total_units, t, begins, n, p, s, lock, streaming, spanning);
       case 2:
-        return launch_vu<V, 16, 1>(no, total_units, t, begins, n, p, s, lock, streaming);
+        return launch_vu<V, 16, 1>(no, total_units, t, begins, n, p, s, lock, streaming, spanning);
       case 3:
-        return launch_vu<V, 8, 3>(no, total_units, t, begins, n, p, s, lock, streaming);
+        return launch_vu<V, 8, 3>(no, total_units, t, begins, n, p, s, lock, streaming, spanning);
       default:
         break;
     }
   }
-  launch_vu<V, 8, 2>(no, total_units, t, begins, n, p, s, lock, streaming);
+  launch_vu<V, 8, 2>(no, total_units, t, begins, n, p, s, lock, streaming, spanning);
 }
 
 }  // namespace
