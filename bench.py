@@ -139,7 +139,22 @@ def run_ours_peer(args):
     meta = TensorMeta(shape, EB)
     s = ShardingSpec.parse("S0R", 1)
     pm_geo = DeviceMesh.uniform([ws])
-    pm = PeerMesh([ws], rank, dev_idx, s.per_device_bytes(meta, pm_geo))
+    # Peer mapping needs P2P between the GPUs (NVLink/NVSwitch). If any rank
+    # cannot map its peers, every rank agrees and the run uses NCCL instead.
+    pm, err = None, ""
+    try:
+        pm = PeerMesh([ws], rank, dev_idx, s.per_device_bytes(meta, pm_geo))
+    except Exception as e:  # noqa: BLE001
+        err = f"{type(e).__name__}: {e}"
+    ok = torch.tensor([0.0 if pm is None else 1.0])
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() < 1.0:
+        print(f"[bench] peer transport unavailable ({err or 'on another rank'}); using NCCL",
+              file=sys.stderr, flush=True)
+        if pm is not None:
+            pm.close()
+        dist.destroy_process_group()
+        return False
     src = pm.shard(s.local_shape(meta, pm_geo), torch.bfloat16)
     gen = torch.Generator(device=dev).manual_seed(2302 + rank)
     src.view(torch.int16).random_(-32768, 32767, generator=gen)
@@ -252,6 +267,7 @@ def run_ours_peer(args):
     if rank == 0:
         print(json.dumps(result))
     dist.destroy_process_group()
+    return True
 
 
 def peer_mesh_sweep(ws, rank, dev_idx, iters=10):
@@ -782,7 +798,8 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     elif dist_env()[0] > 1 and args.transport == "peer":
-        run_ours_peer(args)
+        if not run_ours_peer(args):
+            run_ours(args)
     else:
         run_ours(args)
 
