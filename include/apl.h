@@ -262,7 +262,8 @@ int apl_exchange_traffic(apl_mesh* mesh, const apl_spec* src, const apl_spec* tg
                          int64_t* wire_in);
 
 /* Copy engine the collapsed src->tgt exchange runs on (16-byte aligned
- * buffers): 0 = vectorised LDG/STG box copy, 1 = TMA bulk engine. */
+ * buffers): 0 = vectorised LDG/STG box copy, 1 = TMA bulk engine, 2 = TMA
+ * tensor-tile engine. */
 int apl_exchange_engine(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
                         const apl_meta* meta, int* engine);
 

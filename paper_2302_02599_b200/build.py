@@ -51,6 +51,7 @@ HOST_SRCS = [
 CUDA_SRCS = [
     CSRC / "kernels" / "box_copy.cu",
     CSRC / "kernels" / "bulk_copy.cu",
+    CSRC / "kernels" / "tile_copy.cu",
     CSRC / "kernels" / "reduce.cu",
     CSRC / "kernels" / "peer_sync.cu",
     CSRC / "kernels" / "gemm_tcgen05.cu",

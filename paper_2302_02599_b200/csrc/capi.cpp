@@ -675,7 +675,8 @@ int apl_exchange_engine(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt
       throw autoplan::ShapeError("spec is not valid for the tensor/mesh");
     auto ex = apl::get_exchange(mesh->impl, s, g, t);
     const auto& host = mesh->impl.distributed ? ex->host_pre : ex->host_copies;
-    *engine = apl::bulk_eligible(host, apl::natural_vec(host)) ? 1 : 0;
+    const int vec = apl::natural_vec(host);
+    *engine = apl::tile_eligible(host, vec) ? 2 : apl::bulk_eligible(host, vec) ? 1 : 0;
   });
 }
 

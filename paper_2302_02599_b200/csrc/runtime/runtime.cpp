@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda.h>
+
 #include "apl.h"
 
 namespace apl {
@@ -133,13 +135,33 @@ int natural_vec(const std::vector<CopyDesc>& descs) {
   return pow2_vec(g);
 }
 
-bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec) {
+namespace {
+
+int copy_engine_forced() {  // APL_COPY_ENGINE = ldg | bulk | tile, unset = auto
   static const int forced = [] {
-    const char* e = std::getenv("APL_COPY_ENGINE");  // "ldg" | "bulk" | unset (auto)
+    const char* e = std::getenv("APL_COPY_ENGINE");
     if (e == nullptr) return -1;
-    return std::string(e) == "bulk" ? 1 : std::string(e) == "ldg" ? 0 : -1;
+    const std::string v(e);
+    return v == "bulk" ? 1 : v == "ldg" ? 0 : v == "tile" ? 2 : -1;
   }();
-  if (vec != 16 || descs.empty() || forced == 0) return false;
+  return forced;
+}
+
+// The tile engine's place in the automatic policy (APL_TILE_AUTO=0 keeps
+// short strided rows on the LDG engine).
+bool tile_auto_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_TILE_AUTO");
+    return e == nullptr || std::string(e) != "0";
+  }();
+  return on;
+}
+
+}  // namespace
+
+bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec) {
+  const int forced = copy_engine_forced();
+  if (vec != 16 || descs.empty() || forced == 0 || forced == 2) return false;
   bool strided = false, fan = false;
   for (const CopyDesc& d : descs) {
     if (d.bytes() == 0) continue;
@@ -155,10 +177,140 @@ bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec) {
   return strided && !fan;
 }
 
-CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool bulk) {
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_tiled() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiled>(nullptr);
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// Tensor geometry of a descriptor for the tile engine: dim 0 = the run in
+// 8-byte elements, dims 1.. = the outer dims innermost first.
+struct TileGeo {
+  int rank;
+  cuuint64_t dim[5];
+  cuuint32_t box[5];
+  int64_t nb[5];
+};
+
+TileGeo tile_geo(const CopyDesc& d) {
+  TileGeo g{};
+  g.rank = 1 + d.nouter;
+  g.dim[0] = static_cast<cuuint64_t>(d.run_bytes / 8);
+  for (int k = 1; k < g.rank; ++k) g.dim[k] = static_cast<cuuint64_t>(d.ext[d.nouter - k]);
+  g.box[0] = static_cast<cuuint32_t>(std::min<cuuint64_t>(g.dim[0], 256));
+  const int64_t rows = kTileBoxBytes / (int64_t{g.box[0]} * 8);
+  g.box[1] = static_cast<cuuint32_t>(std::min<int64_t>({static_cast<int64_t>(g.dim[1]), 256, rows}));
+  for (int k = 2; k < g.rank; ++k) g.box[k] = 1;
+  for (int k = 0; k < 5; ++k)
+    g.nb[k] = k < g.rank ? (static_cast<int64_t>(g.dim[k]) + g.box[k] - 1) / g.box[k] : 1;
+  return g;
+}
+
+bool encode_map(CUtensorMap* map, const TileGeo& g, const char* base, const int64_t* stride_outer,
+                int nouter) {
+  EncodeTiled enc = encode_tiled();
+  if (enc == nullptr) return false;
+  cuuint64_t strides[4];
+  for (int k = 1; k < g.rank; ++k) strides[k - 1] = static_cast<cuuint64_t>(stride_outer[nouter - k]);
+  const cuuint32_t elem[5] = {1, 1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, static_cast<cuuint32_t>(g.rank),
+             const_cast<char*>(base), g.dim, strides, g.box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void build_tile_launches(const CompiledCopies& c, const PtrTable& ptrs) {
+  c.tile_launches.clear();
+  TileArgs cur;
+  std::memset(&cur, 0, sizeof(cur));
+  int nmaps = 0;
+  int64_t units = 0;
+  auto flush = [&] {
+    if (cur.ndesc == 0) return;
+    cur.total = units;
+    c.tile_launches.push_back(cur);
+    std::memset(&cur, 0, sizeof(cur));
+    nmaps = 0;
+  };
+  for (const CopyDesc& d : c.tile_descs) {
+    if (cur.ndesc == kTileMaxDesc || nmaps + 1 + d.ndst > kTileMaxMaps) flush();
+    if (cur.ndesc == 0) cur.first = units;
+    const TileGeo g = tile_geo(d);
+    TileDesc& t = cur.d[cur.ndesc++];
+    t.unit_begin = units;
+    int64_t n = 1;
+    for (int k = 0; k < 5; ++k) {
+      t.nb[k] = make_fastdiv(static_cast<uint32_t>(g.nb[k]));
+      t.box[k] = k < g.rank ? static_cast<int>(g.box[k]) : 1;
+      n *= g.nb[k];
+    }
+    t.rank = g.rank;
+    t.box_bytes = static_cast<int>(int64_t{g.box[0]} * 8 * g.box[1]);
+    t.src_map = nmaps;
+    if (!encode_map(&cur.maps[nmaps++], g, ptrs.src[d.src_buf] + d.src_off, d.src_stride,
+                    d.nouter))
+      throw RuntimeError(APL_ERR_CUDA, "cuTensorMapEncodeTiled failed (source)");
+    t.dst_map = nmaps;
+    t.ndst = d.ndst;
+    for (int j = 0; j < d.ndst; ++j) {
+      const int buf = j == 0 ? d.dst_buf : d.extra_dst[j - 1];
+      if (!encode_map(&cur.maps[nmaps++], g, ptrs.dst[buf] + d.dst_off, d.dst_stride, d.nouter))
+        throw RuntimeError(APL_ERR_CUDA, "cuTensorMapEncodeTiled failed (destination)");
+    }
+    units += n;
+  }
+  flush();
+  c.tile_ptrs = ptrs;
+  c.tile_cached = true;
+}
+
+}  // namespace
+
+bool tile_eligible(const std::vector<CopyDesc>& descs, int vec) {
+  const int forced = copy_engine_forced();
+  if (vec != 16 || descs.empty() || forced == 0 || forced == 1) return false;
+  if (encode_tiled() == nullptr) return false;
+  for (const CopyDesc& d : descs) {
+    if (d.bytes() == 0) continue;
+    if (d.ksplit > 1 || d.ndst > kTileMaxFan || d.nouter < 1 || d.nouter > 4) return false;
+    if (d.run_bytes % 16 || d.run_bytes < 64 || d.src_off % 16 || d.dst_off % 16) return false;
+    if (forced != 2 && d.run_bytes >= kBulkMinRun) return false;  // the bulk ring's regime
+    for (int i = 0; i < d.nouter; ++i) {
+      if (d.src_stride[i] % 16 || d.dst_stride[i] % 16 || d.ext[i] > (int64_t{1} << 31))
+        return false;
+    }
+  }
+  return forced == 2 || tile_auto_enabled();
+}
+
+CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool bulk, bool tile) {
   CompiledCopies cc;
   cc.vec = vec;
   cc.bulk = bulk;
+  if (tile) {
+    cc.tile = true;
+    for (const CopyDesc& d : descs)
+      if (d.bytes() > 0) {
+        cc.tile_descs.push_back(d);
+        cc.bytes += d.bytes();
+        cc.write_bytes += d.bytes() * d.ndst;
+      }
+    return cc;
+  }
   std::vector<CopyDesc> flat;
   for (const CopyDesc& d : descs)
     if (d.bytes() > 0) split_large(d, vec, flat);
@@ -243,6 +395,13 @@ void free_copies(CompiledCopies& c) {
 
 void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream) {
   if (c.empty()) return;
+  if (c.tile) {
+    if (!c.tile_cached || std::memcmp(&c.tile_ptrs, &ptrs, sizeof(PtrTable)) != 0)
+      build_tile_launches(c, ptrs);
+    for (const TileArgs& a : c.tile_launches)
+      check_cuda(launch_tile_copy(a, stream), "tile copy launch");
+    return;
+  }
   if (c.bulk) {
     check_cuda(launch_bulk_copy(c.table, c.begins.data(), c.ntasks, c.total_units, ptrs, stream,
                                 c.write_bytes), "bulk copy launch");
@@ -365,10 +524,11 @@ namespace {
 
 const CompiledCopies& compiled_for(std::map<int, CompiledCopies>& cache,
                                    const std::vector<CopyDesc>& host, int vec) {
-  const bool bulk = bulk_eligible(host, vec);
-  const int key = vec + (bulk ? 1000 : 0);
+  const bool tile = tile_eligible(host, vec);
+  const bool bulk = !tile && bulk_eligible(host, vec);
+  const int key = vec + (bulk ? 1000 : 0) + (tile ? 2000 : 0);
   auto it = cache.find(key);
-  if (it == cache.end()) it = cache.emplace(key, compile_copies(host, vec, bulk)).first;
+  if (it == cache.end()) it = cache.emplace(key, compile_copies(host, vec, bulk, tile)).first;
   return it->second;
 }
 

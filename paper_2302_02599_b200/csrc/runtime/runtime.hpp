@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../kernels/box_copy.cuh"
+#include "../kernels/tile_copy.cuh"
 #include "plan.hpp"
 
 namespace apl {
@@ -82,8 +83,20 @@ struct CompiledCopies {
   int64_t bytes = 0;        // bytes read (each source byte once)
   int64_t write_bytes = 0;  // bytes written (fan-out counted per destination)
   bool bulk = false;        // TMA bulk engine (units = kBulkSeg segments)
-  bool empty() const { return ntasks == 0; }
+  // TMA tensor-tile engine: the descriptors themselves (tensor maps embed
+  // the buffer addresses, so launch arguments are encoded per pointer table
+  // and cached for the last table seen).
+  bool tile = false;
+  std::vector<CopyDesc> tile_descs;
+  mutable std::vector<TileArgs> tile_launches;
+  mutable PtrTable tile_ptrs{};
+  mutable bool tile_cached = false;
+  bool empty() const { return ntasks == 0 && tile_descs.empty(); }
 };
+
+cudaError_t launch_tile_copy(const TileArgs& args, cudaStream_t stream);
+// True when every descriptor suits the tensor-tile engine.
+bool tile_eligible(const std::vector<CopyDesc>& descs, int vec);
 
 cudaError_t launch_bulk_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,
                              int64_t total_units, const PtrTable& ptrs, cudaStream_t stream,
@@ -93,7 +106,8 @@ bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec);
 
 // Largest vector width (16/8/4/2/1) dividing every run, stride and offset.
 int natural_vec(const std::vector<CopyDesc>& descs);
-CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool bulk = false);
+CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool bulk = false,
+                              bool tile = false);
 void free_copies(CompiledCopies& c);
 void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stream);
 

@@ -209,11 +209,12 @@ class Mesh:
         return {"hbm_read": r.value, "hbm_write": w.value, "wire_in": wire.value}
 
     def exchange_engine(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta) -> str:
-        """'bulk' (TMA engine) or 'ldg' (vectorised box copy) for this exchange."""
+        """'tile' (TMA tensor boxes), 'bulk' (TMA bulk ring) or 'ldg' (vectorised
+        box copy) for this exchange."""
         e = C.c_int()
         check(A.lib().apl_exchange_engine(self._h, C.byref(src.c()), C.byref(tgt.c()),
                                           C.byref(meta.c()), C.byref(e)))
-        return "bulk" if e.value == 1 else "ldg"
+        return {1: "bulk", 2: "tile"}.get(e.value, "ldg")
 
     def sharded_matmul(self, strategy: "MatmulStrategy", a_meta: TensorMeta, b_meta: TensorMeta,
                        a_shards, b_shards, c_shards, gelu: bool = False, b_layout: str = "nk",
