@@ -77,6 +77,9 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError(f"build step failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
 
 
+CLI = ROOT / "paper_2302_02599_b200" / "apl_convert"
+
+
 def build(verbose: bool = False, force: bool = False) -> Path:
     nccl = _nccl_root()
     incs = [f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{CUDA_HOME / 'include'}",
@@ -110,6 +113,12 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         _run([NVCC, "-shared", *ARCH, "-o", str(LIB), *map(str, objs),
               f"-L{nccl / 'lib'}", "-l:libnccl.so.2",
               "-Xlinker", f"-rpath,{nccl / 'lib'}"])
+    # the `plan convert` CLI with an execute mode (tools/apl_convert.cpp)
+    cli_src = ROOT / "tools" / "apl_convert.cpp"
+    if cli_src.exists() and (force or _stale(CLI, [cli_src, LIB] + headers)):
+        _run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", f"-I{CUDA_HOME / 'include'}",
+              str(cli_src), f"-L{LIB.parent}", "-lapl", f"-L{CUDA_HOME / 'lib64'}", "-lcudart",
+              f"-Wl,-rpath,{LIB.parent}", f"-Wl,-rpath,{CUDA_HOME / 'lib64'}", "-o", str(CLI)])
     return LIB
 
 
