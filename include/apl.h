@@ -274,6 +274,15 @@ int apl_exchange_engine(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt
 int apl_exchange_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_spec* src,
                                const apl_spec* tgt, const apl_meta* meta, char* out, size_t cap,
                                size_t* len);
+/* Host-only dry run of a whole conversion for `rank` of a distributed mesh:
+ * {"hops": [schedule of each hop, as apl_exchange_schedule_json, plus
+ * "allgather": {"axis", "direct"} for hops that are one all-gather on an axis
+ * communicator], "inter_bytes", "staging"} -- what apl_run_path executes
+ * with `flags` (APL_FUSE_CHAIN / APL_STEPWISE) on an NCCL mesh. */
+int apl_conversion_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_spec* src,
+                                 const apl_spec* tgt, const apl_step* steps, int nsteps,
+                                 const apl_meta* meta, unsigned flags, char* out, size_t cap,
+                                 size_t* len);
 
 /* Prepared conversion: validates the path and compiles its exchanges once,
  * so the per-call cost is one lookup-free launch sequence (and the calls can

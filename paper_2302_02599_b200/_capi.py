@@ -147,6 +147,9 @@ _SIGS = {
                                         C.c_int, C.c_void_p]),
     "apl_peer_reduce_gather": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, P(C.c_void_p), C.c_int,
                                          C.c_int, C.c_void_p]),
+    "apl_conversion_schedule_json": (C.c_int, [P(MeshDesc), C.c_int, P(Spec), P(Spec), P(Step),
+                                               C.c_int, P(Meta), C.c_uint, C.c_char_p, C.c_size_t,
+                                               P(C.c_size_t)]),
     "apl_peer_allreduce": (C.c_int, [P(C.c_void_p), C.c_int, C.c_size_t, C.c_int, C.c_void_p]),
     "apl_peer_flags_store": (C.c_int, [P(C.c_void_p), C.c_int, C.c_int, C.c_uint32,
                                        C.c_void_p]),

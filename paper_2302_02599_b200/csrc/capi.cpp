@@ -680,6 +680,66 @@ int apl_exchange_engine(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt
   });
 }
 
+namespace {
+
+std::string copies_json(const std::vector<apl::CopyDesc>& v) {
+  std::string j = "[";
+  for (size_t i = 0; i < v.size(); ++i) {
+    const apl::CopyDesc& c = v[i];
+    if (i) j += ",";
+    j += "{\"src_buf\":" + std::to_string(c.src_buf) + ",\"dst_buf\":" + std::to_string(c.dst_buf) +
+         ",\"src_off\":" + std::to_string(c.src_off) + ",\"dst_off\":" + std::to_string(c.dst_off) +
+         ",\"run_bytes\":" + std::to_string(c.run_bytes) + ",\"ext\":[";
+    for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.ext[d]);
+    j += "],\"src_stride\":[";
+    for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.src_stride[d]);
+    j += "],\"dst_stride\":[";
+    for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.dst_stride[d]);
+    j += "],\"ksplit\":" + std::to_string(c.ksplit) +
+         ",\"split_src_step\":" + std::to_string(c.split_src_step) + ",\"split_dst\":[";
+    for (int d = 0; d < c.ksplit && c.ksplit > 1; ++d)
+      j += (d ? "," : "") + std::to_string(c.split_dst[d]);
+    j += "],\"split_dst_off\":[";
+    for (int d = 0; d < c.ksplit && c.ksplit > 1; ++d)
+      j += (d ? "," : "") + std::to_string(c.split_dst_off[d]);
+    j += "]}";
+  }
+  return j + "]";
+}
+
+std::string xfers_json(const std::vector<apl::Exchange::Xfer>& v) {
+  std::string j = "[";
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (i) j += ",";
+    j += "[" + std::to_string(v[i].peer) + "," + (v[i].direct ? "1" : "0") + "," +
+         std::to_string(v[i].offset) + "," + std::to_string(v[i].bytes) + "]";
+  }
+  return j + "]";
+}
+
+// The distributed executor's schedule of one hop for this rank.
+std::string exchange_json(const apl::Exchange& ex) {
+  std::string j = "{\"pre\":" + copies_json(ex.host_pre) + ",\"post\":" + copies_json(ex.host_post) +
+                  ",\"sends\":" + xfers_json(ex.sends) + ",\"recvs\":" + xfers_json(ex.recvs) +
+                  ",\"send_staging\":" + std::to_string(ex.send_staging) +
+                  ",\"recv_staging\":" + std::to_string(ex.recv_staging) +
+                  ",\"workspace\":" + std::to_string(apl::exchange_workspace(ex)) +
+                  ",\"in_bytes\":" + std::to_string(ex.in_bytes) +
+                  ",\"out_bytes\":" + std::to_string(ex.out_bytes);
+  if (ex.ag_axis >= 0)
+    j += ",\"allgather\":{\"axis\":" + std::to_string(ex.ag_axis) +
+         ",\"direct\":" + (ex.ag_direct ? "1" : "0") + "}";
+  return j + "}";
+}
+
+void emit(const std::string& j, char* out, size_t cap, size_t* len) {
+  *len = j.size() + 1;
+  need(out != nullptr && cap >= j.size() + 1, "output buffer too small");
+  std::memcpy(out, j.c_str(), j.size() + 1);
+}
+
+}  // namespace
+
 int apl_exchange_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_spec* src,
                                const apl_spec* tgt, const apl_meta* meta, char* out, size_t cap,
                                size_t* len) {
@@ -694,54 +754,33 @@ int apl_exchange_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_sp
     const TensorMeta t = to_meta(meta);
     if (!s.valid_for(t, dry.geo) || !g.valid_for(t, dry.geo))
       throw autoplan::ShapeError("spec is not valid for the tensor/mesh");
-    auto ex = apl::get_exchange(dry, s, g, t);
-    std::string j = "{";
-    auto copies = [&](const char* name, const std::vector<apl::CopyDesc>& v) {
-      j += std::string("\"") + name + "\":[";
-      for (size_t i = 0; i < v.size(); ++i) {
-        const apl::CopyDesc& c = v[i];
-        if (i) j += ",";
-        j += "{\"src_buf\":" + std::to_string(c.src_buf) + ",\"dst_buf\":" + std::to_string(c.dst_buf) +
-             ",\"src_off\":" + std::to_string(c.src_off) + ",\"dst_off\":" + std::to_string(c.dst_off) +
-             ",\"run_bytes\":" + std::to_string(c.run_bytes) + ",\"ext\":[";
-        for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.ext[d]);
-        j += "],\"src_stride\":[";
-        for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.src_stride[d]);
-        j += "],\"dst_stride\":[";
-        for (int d = 0; d < c.nouter; ++d) j += (d ? "," : "") + std::to_string(c.dst_stride[d]);
-        j += "],\"ksplit\":" + std::to_string(c.ksplit) +
-             ",\"split_src_step\":" + std::to_string(c.split_src_step) + ",\"split_dst\":[";
-        for (int d = 0; d < c.ksplit && c.ksplit > 1; ++d)
-          j += (d ? "," : "") + std::to_string(c.split_dst[d]);
-        j += "],\"split_dst_off\":[";
-        for (int d = 0; d < c.ksplit && c.ksplit > 1; ++d)
-          j += (d ? "," : "") + std::to_string(c.split_dst_off[d]);
-        j += "]}";
-      }
-      j += "],";
-    };
-    auto xfers = [&](const char* name, const std::vector<apl::Exchange::Xfer>& v) {
-      j += std::string("\"") + name + "\":[";
-      for (size_t i = 0; i < v.size(); ++i) {
-        if (i) j += ",";
-        j += "[" + std::to_string(v[i].peer) + "," + (v[i].direct ? "1" : "0") + "," +
-             std::to_string(v[i].offset) + "," + std::to_string(v[i].bytes) + "]";
-      }
-      j += "],";
-    };
-    copies("pre", ex->host_pre);
-    copies("post", ex->host_post);
-    xfers("sends", ex->sends);
-    xfers("recvs", ex->recvs);
-    j += "\"send_staging\":" + std::to_string(ex->send_staging) +
-         ",\"recv_staging\":" + std::to_string(ex->recv_staging) +
-         ",\"workspace\":" + std::to_string(apl::exchange_workspace(*ex)) + "}";
-    *len = j.size() + 1;
-    need(out != nullptr && cap >= j.size() + 1, "output buffer too small");
-    std::memcpy(out, j.c_str(), j.size() + 1);
+    emit(exchange_json(*apl::get_exchange(dry, s, g, t)), out, cap, len);
   });
 }
 
+int apl_conversion_schedule_json(const apl_mesh_desc* mesh, int rank, const apl_spec* src,
+                                 const apl_spec* tgt, const apl_step* steps, int nsteps,
+                                 const apl_meta* meta, unsigned flags, char* out, size_t cap,
+                                 size_t* len) {
+  return guarded([&] {
+    need(len, "null len");
+    need(nsteps >= 0 && (steps || nsteps == 0), "bad steps");
+    apl::Mesh dry;  // host-only compilation of a distributed rank's conversion
+    dry.geo = to_mesh(mesh);
+    dry.distributed = true;
+    need(rank >= 0 && rank < dry.geo.num_devices(), "rank out of range");
+    dry.rank = rank;
+    std::vector<autoplan::TransformStep> st;
+    for (int i = 0; i < nsteps; ++i) st.push_back(to_step(&steps[i]));
+    apl::Conversion cv = apl::prepare_conversion(dry, to_spec(src), to_spec(tgt), st,
+                                                 to_meta(meta), (flags & APL_FUSE_CHAIN) != 0);
+    std::string j = "{\"hops\":[";
+    for (size_t i = 0; i < cv.hops.size(); ++i) j += (i ? "," : "") + exchange_json(*cv.hops[i]);
+    j += "],\"inter_bytes\":" + std::to_string(cv.inter_bytes) +
+         ",\"staging\":" + std::to_string(cv.staging) + "}";
+    emit(j, out, cap, len);
+  });
+}
 int apl_all_reduce(apl_mesh* mesh, const int32_t* axes, int naxes, void* const* bufs,
                    size_t count, int dtype, void* stream) {
   return guarded([&] {

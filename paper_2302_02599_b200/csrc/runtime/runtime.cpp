@@ -516,6 +516,50 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
   return it->second;
 }
 
+std::shared_ptr<Exchange> get_allgather(Mesh& mesh, const autoplan::ShardingSpec& src,
+                                        const autoplan::TransformStep& step,
+                                        const autoplan::TensorMeta& meta) {
+  std::string key = "AG|" + src.to_string() + ">" + step.result.to_string() + "|" +
+                    std::to_string(step.tensor_dim) + "," + std::to_string(step.mesh_axis) + "|";
+  for (int64_t e : meta.shape) key += std::to_string(e) + ",";
+  key += "|" + std::to_string(meta.dtype_bytes);
+  {
+    std::lock_guard<std::mutex> hold(mesh.mu);
+    auto it = mesh.exchanges.find(key);
+    if (it != mesh.exchanges.end()) return it->second;
+  }
+  auto ex = std::make_shared<Exchange>();
+  const int eb = meta.dtype_bytes;
+  const std::vector<int64_t> ls = local_shape(src, mesh.geo, meta);
+  const std::vector<int64_t> lt = local_shape(step.result, mesh.geo, meta);
+  const int d = step.tensor_dim;
+  const int64_t n = mesh.geo.shape[static_cast<size_t>(step.mesh_axis)];
+  ex->in_bytes = src.per_device_bytes(meta, mesh.geo);
+  ex->out_bytes = step.result.per_device_bytes(meta, mesh.geo);
+  ex->ag_axis = step.mesh_axis;
+  int64_t outer = 1;
+  for (int i = 0; i < d; ++i) outer *= ls[static_cast<size_t>(i)];
+  ex->ag_direct = outer == 1;  // [n][1..][L][Q] == [1..][n*L][Q]
+  ex->wire_bytes_in = (n - 1) * ex->in_bytes;
+  ex->wire_bytes_out = (n - 1) * ex->in_bytes;
+  if (!ex->ag_direct) {
+    // block j (coordinate j on the axis, the least significant digit of
+    // dims[d]) -> offset j * L along dim d of the output
+    std::vector<int64_t> zero(ls.size(), 0);
+    for (int64_t j = 0; j < n; ++j) {
+      std::vector<int64_t> lo(ls.size(), 0);
+      lo[static_cast<size_t>(d)] = j * ls[static_cast<size_t>(d)];
+      CopyDesc c = make_copy(1, ls, zero, 0, lt, lo, ls, eb);
+      c.src_off += j * ex->in_bytes;
+      ex->host_post.push_back(c);
+    }
+    ex->recv_staging = align_up(n * ex->in_bytes);
+  }
+  std::lock_guard<std::mutex> hold(mesh.mu);
+  auto [it, fresh] = mesh.exchanges.emplace(key, ex);
+  return it->second;
+}
+
 size_t exchange_workspace(const Exchange& ex) {
   return static_cast<size_t>(align_up(ex.send_staging) + align_up(ex.recv_staging));
 }
@@ -559,6 +603,22 @@ void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* 
   t.src[1] = recv;
   t.dst[0] = static_cast<char*>(out[0]);
   t.dst[1] = send;
+  if (ex.ag_axis >= 0) {  // one NCCL all-gather on the axis communicator (+ unpack)
+    auto comm = mesh.sub.find(1u << ex.ag_axis);
+    if (comm == mesh.sub.end())
+      throw RuntimeError(APL_ERR_NCCL, "no communicator for mesh axis " +
+                                           std::to_string(ex.ag_axis));
+    check_nccl(ncclAllGather(in[0], ex.ag_direct ? out[0] : static_cast<void*>(recv),
+                             static_cast<size_t>(ex.in_bytes), ncclInt8, comm->second, stream),
+               "ncclAllGather");
+    if (!ex.ag_direct) {
+      const int palign = std::min(ptr_align(out[0]), ptr_align(ws));
+      std::lock_guard<std::mutex> hold(mesh.mu);
+      run_copies(compiled_for(ex.post, ex.host_post, std::min(palign, natural_vec(ex.host_post))),
+                 t, stream);
+    }
+    return;
+  }
   const int palign = std::min({ptr_align(in[0]), ptr_align(out[0]), ptr_align(ws)});
   {
     std::lock_guard<std::mutex> hold(mesh.mu);
@@ -670,14 +730,22 @@ Conversion prepare_conversion(Mesh& mesh, const autoplan::ShardingSpec& src,
   validate_steps(src, tgt, steps, mesh.geo, meta);
   Conversion cv;
   cv.mesh = &mesh;
-  if (fuse || steps.size() <= 1) {
+  // Distributed meshes run an all-gather step as ONE ncclAllGather on the
+  // step's axis communicator (NVLS-capable), also when the path is that
+  // single step; a collapsed multi-step chain stays one point-to-point
+  // exchange.
+  const bool ag_single = mesh.distributed && steps.size() == 1 &&
+                         steps[0].kind == autoplan::CollectiveKind::kAllGather;
+  if ((fuse || steps.size() <= 1) && !ag_single) {
     cv.hops.push_back(get_exchange(mesh, src, tgt, meta));
     cv.staging = static_cast<int64_t>(exchange_workspace(*cv.hops[0]));
     return cv;
   }
   const autoplan::ShardingSpec* cur = &src;
   for (size_t i = 0; i < steps.size(); ++i) {
-    auto ex = get_exchange(mesh, *cur, steps[i].result, meta);
+    auto ex = mesh.distributed && steps[i].kind == autoplan::CollectiveKind::kAllGather
+                  ? get_allgather(mesh, *cur, steps[i], meta)
+                  : get_exchange(mesh, *cur, steps[i].result, meta);
     cv.staging = std::max<int64_t>(cv.staging, static_cast<int64_t>(exchange_workspace(*ex)));
     if (i + 1 < steps.size())
       cv.inter_bytes = std::max(cv.inter_bytes, align_up(ex->out_bytes) * mesh.num_local());

@@ -131,7 +131,15 @@ struct Exchange {
   int64_t send_staging = 0, recv_staging = 0;
   int64_t wire_bytes_in = 0;   // bytes this rank receives from peers
   int64_t wire_bytes_out = 0;  // bytes this rank sends to peers
+  // Distributed all-gather step (reference kAllGather on one mesh axis):
+  // ncclAllGather of the source shard on that axis's communicator into
+  // receive staging laid out [n_a][source shard] (group order = coordinate
+  // on the axis), then host_post unpacks it into `out`; ag_direct: the
+  // gathered layout already is `out` (nothing outside the gathered dim).
+  int ag_axis = -1;
+  bool ag_direct = false;
 };
+
 
 struct Mesh {
   autoplan::DeviceMesh geo;
@@ -164,6 +172,11 @@ void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* 
 // A validated path with its exchanges compiled: one hop when collapsed (or a
 // single step), one hop per reference step otherwise (intermediates ping-pong
 // through the workspace).
+// The all-gather form of one AG step on a distributed mesh.
+std::shared_ptr<Exchange> get_allgather(Mesh& mesh, const autoplan::ShardingSpec& src,
+                                        const autoplan::TransformStep& step,
+                                        const autoplan::TensorMeta& meta);
+
 struct Conversion {
   Mesh* mesh = nullptr;
   std::vector<std::shared_ptr<Exchange>> hops;

@@ -446,6 +446,29 @@ def plan_pieces(mesh: DeviceMesh, src: ShardingSpec, tgt: ShardingSpec, meta: Te
                       tuple(arr[i].dst_lo[:k]), tuple(arr[i].ext[:k])) for i in range(n.value)]
 
 
+def conversion_schedule(mesh: DeviceMesh, rank: int, path: "TransformPath", meta: TensorMeta,
+                        fuse: bool) -> dict:
+    """Dry run of the distributed executor for `rank`: every hop of the
+    conversion (collapsed exchange, point-to-point step exchanges, or
+    all-gathers on an axis communicator) with its copies and transfers."""
+    import json
+
+    n = C.c_size_t()
+    cap = 1 << 16
+    steps = path.steps_c()
+    while True:
+        buf = C.create_string_buffer(cap)
+        rc = A.lib().apl_conversion_schedule_json(
+            C.byref(mesh.c()), rank, C.byref(path.source.c()), C.byref(path.target.c()), steps,
+            len(path.steps), C.byref(meta.c()), A.FUSE_CHAIN if fuse else A.STEPWISE, buf, cap,
+            C.byref(n))
+        if rc == A.ERR_ARG and n.value > cap:
+            cap = n.value
+            continue
+        check(rc)
+        return json.loads(buf.value.decode())
+
+
 def exchange_schedule(mesh: DeviceMesh, rank: int, src: ShardingSpec, tgt: ShardingSpec,
                       meta: TensorMeta) -> dict:
     """Dry run of the distributed executor's schedule for `rank` (host only)."""
