@@ -729,6 +729,11 @@ std::string exchange_json(const apl::Exchange& ex) {
   if (ex.ag_axis >= 0)
     j += ",\"allgather\":{\"axis\":" + std::to_string(ex.ag_axis) +
          ",\"direct\":" + (ex.ag_direct ? "1" : "0") + "}";
+  if (ex.a2a_axis >= 0)
+    j += ",\"alltoall\":{\"axis\":" + std::to_string(ex.a2a_axis) +
+         ",\"chunk\":" + std::to_string(ex.a2a_chunk) +
+         ",\"direct_send\":" + (ex.a2a_direct_send ? "1" : "0") +
+         ",\"direct_recv\":" + (ex.a2a_direct_recv ? "1" : "0") + "}";
   return j + "}";
 }
 

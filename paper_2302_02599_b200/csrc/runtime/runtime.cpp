@@ -560,6 +560,64 @@ std::shared_ptr<Exchange> get_allgather(Mesh& mesh, const autoplan::ShardingSpec
   return it->second;
 }
 
+std::shared_ptr<Exchange> get_alltoall(Mesh& mesh, const autoplan::ShardingSpec& src,
+                                       const autoplan::TransformStep& step,
+                                       const autoplan::TensorMeta& meta) {
+  std::string key = "A2A|" + src.to_string() + ">" + step.result.to_string() + "|" +
+                    std::to_string(step.tensor_dim) + "," + std::to_string(step.target_dim) +
+                    "," + std::to_string(step.mesh_axis) + "|";
+  for (int64_t e : meta.shape) key += std::to_string(e) + ",";
+  key += "|" + std::to_string(meta.dtype_bytes);
+  {
+    std::lock_guard<std::mutex> hold(mesh.mu);
+    auto it = mesh.exchanges.find(key);
+    if (it != mesh.exchanges.end()) return it->second;
+  }
+  auto ex = std::make_shared<Exchange>();
+  const int eb = meta.dtype_bytes;
+  const std::vector<int64_t> ls = local_shape(src, mesh.geo, meta);
+  const std::vector<int64_t> lt = local_shape(step.result, mesh.geo, meta);
+  const size_t d = static_cast<size_t>(step.tensor_dim), d2 = static_cast<size_t>(step.target_dim);
+  const int64_t n = mesh.geo.shape[static_cast<size_t>(step.mesh_axis)];
+  ex->in_bytes = src.per_device_bytes(meta, mesh.geo);
+  ex->out_bytes = step.result.per_device_bytes(meta, mesh.geo);
+  ex->a2a_axis = step.mesh_axis;
+  ex->a2a_chunk = ex->in_bytes / n;
+  // chunk j = `in` with dim d2 cut to its j-th 1/n (peer j's part)
+  std::vector<int64_t> chunk = ls;
+  chunk[d2] /= n;
+  int64_t before_d2 = 1, before_d = 1;
+  for (size_t i = 0; i < d2; ++i) before_d2 *= ls[i];
+  for (size_t i = 0; i < d; ++i) before_d *= lt[i];
+  ex->a2a_direct_send = before_d2 == 1;  // `in` is [n][chunk] already
+  ex->a2a_direct_recv = before_d == 1;   // [n][chunk] lands as `out`
+  const std::vector<int64_t> zero(ls.size(), 0);
+  for (int64_t j = 0; j < n; ++j) {
+    if (!ex->a2a_direct_send) {
+      std::vector<int64_t> lo(ls.size(), 0);
+      lo[d2] = j * chunk[d2];
+      CopyDesc c = make_copy(0, ls, lo, 1, chunk, zero, chunk, eb);
+      c.dst_off += j * ex->a2a_chunk;
+      ex->host_pre.push_back(c);
+    }
+    if (!ex->a2a_direct_recv) {  // block from coordinate j -> offset j * L along d
+      std::vector<int64_t> lo(lt.size(), 0);
+      lo[d] = j * chunk[d];
+      CopyDesc c = make_copy(1, chunk, zero, 0, lt, lo, chunk, eb);
+      c.src_off += j * ex->a2a_chunk;
+      ex->host_post.push_back(c);
+    }
+  }
+  if (!ex->a2a_direct_send) ex->send_staging = align_up(ex->in_bytes);
+  if (!ex->a2a_direct_recv) ex->recv_staging = align_up(ex->out_bytes);
+  ex->wire_bytes_in = (n - 1) * ex->a2a_chunk;
+  ex->wire_bytes_out = (n - 1) * ex->a2a_chunk;
+  merge_splits(ex->host_pre);
+  std::lock_guard<std::mutex> hold(mesh.mu);
+  auto [it, fresh] = mesh.exchanges.emplace(key, ex);
+  return it->second;
+}
+
 size_t exchange_workspace(const Exchange& ex) {
   return static_cast<size_t>(align_up(ex.send_staging) + align_up(ex.recv_staging));
 }
@@ -603,6 +661,28 @@ void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* 
   t.src[1] = recv;
   t.dst[0] = static_cast<char*>(out[0]);
   t.dst[1] = send;
+  if (ex.a2a_axis >= 0) {  // pack, one ncclAlltoAll on the axis communicator, unpack
+    auto comm = mesh.sub.find(1u << ex.a2a_axis);
+    if (comm == mesh.sub.end())
+      throw RuntimeError(APL_ERR_NCCL, "no communicator for mesh axis " +
+                                           std::to_string(ex.a2a_axis));
+    const int palign = std::min({ptr_align(in[0]), ptr_align(out[0]), ptr_align(ws)});
+    if (!ex.a2a_direct_send) {
+      std::lock_guard<std::mutex> hold(mesh.mu);
+      run_copies(compiled_for(ex.pre, ex.host_pre, std::min(palign, natural_vec(ex.host_pre))), t,
+                 stream);
+    }
+    check_nccl(ncclAlltoAll(ex.a2a_direct_send ? in[0] : static_cast<const void*>(send),
+                            ex.a2a_direct_recv ? out[0] : static_cast<void*>(recv),
+                            static_cast<size_t>(ex.a2a_chunk), ncclInt8, comm->second, stream),
+               "ncclAlltoAll");
+    if (!ex.a2a_direct_recv) {
+      std::lock_guard<std::mutex> hold(mesh.mu);
+      run_copies(compiled_for(ex.post, ex.host_post, std::min(palign, natural_vec(ex.host_post))),
+                 t, stream);
+    }
+    return;
+  }
   if (ex.ag_axis >= 0) {  // one NCCL all-gather on the axis communicator (+ unpack)
     auto comm = mesh.sub.find(1u << ex.ag_axis);
     if (comm == mesh.sub.end())
@@ -730,12 +810,13 @@ Conversion prepare_conversion(Mesh& mesh, const autoplan::ShardingSpec& src,
   validate_steps(src, tgt, steps, mesh.geo, meta);
   Conversion cv;
   cv.mesh = &mesh;
-  // Distributed meshes run an all-gather step as ONE ncclAllGather on the
-  // step's axis communicator (NVLS-capable), also when the path is that
-  // single step; a collapsed multi-step chain stays one point-to-point
-  // exchange.
+  // Distributed meshes run an all-gather step as ONE ncclAllGather and an
+  // all-to-all step as ONE ncclAlltoAll on the step's mesh-axis
+  // communicator (also when the path is that single step); a collapsed
+  // multi-step chain stays one point-to-point exchange.
   const bool ag_single = mesh.distributed && steps.size() == 1 &&
-                         steps[0].kind == autoplan::CollectiveKind::kAllGather;
+                         (steps[0].kind == autoplan::CollectiveKind::kAllGather ||
+                          steps[0].kind == autoplan::CollectiveKind::kAllToAll);
   if ((fuse || steps.size() <= 1) && !ag_single) {
     cv.hops.push_back(get_exchange(mesh, src, tgt, meta));
     cv.staging = static_cast<int64_t>(exchange_workspace(*cv.hops[0]));
@@ -743,8 +824,12 @@ Conversion prepare_conversion(Mesh& mesh, const autoplan::ShardingSpec& src,
   }
   const autoplan::ShardingSpec* cur = &src;
   for (size_t i = 0; i < steps.size(); ++i) {
-    auto ex = mesh.distributed && steps[i].kind == autoplan::CollectiveKind::kAllGather
+    const auto kind = steps[i].kind;
+    auto ex = !mesh.distributed ? get_exchange(mesh, *cur, steps[i].result, meta)
+              : kind == autoplan::CollectiveKind::kAllGather
                   ? get_allgather(mesh, *cur, steps[i], meta)
+              : kind == autoplan::CollectiveKind::kAllToAll
+                  ? get_alltoall(mesh, *cur, steps[i], meta)
                   : get_exchange(mesh, *cur, steps[i].result, meta);
     cv.staging = std::max<int64_t>(cv.staging, static_cast<int64_t>(exchange_workspace(*ex)));
     if (i + 1 < steps.size())

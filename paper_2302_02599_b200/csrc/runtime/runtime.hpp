@@ -138,6 +138,14 @@ struct Exchange {
   // gathered layout already is `out` (nothing outside the gathered dim).
   int ag_axis = -1;
   bool ag_direct = false;
+  // Distributed all-to-all step (reference kAllToAll on one mesh axis):
+  // host_pre packs the n_a equal chunks along the split dim into send
+  // staging [n_a][chunk] (skipped when `in` already is that layout),
+  // ncclAlltoAll on the axis communicator, host_post unpacks receive staging
+  // [n_a][chunk] along the gathered dim (skipped when it lands in `out`).
+  int a2a_axis = -1;
+  bool a2a_direct_send = false, a2a_direct_recv = false;
+  int64_t a2a_chunk = 0;
 };
 
 
@@ -172,6 +180,10 @@ void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* 
 // A validated path with its exchanges compiled: one hop when collapsed (or a
 // single step), one hop per reference step otherwise (intermediates ping-pong
 // through the workspace).
+// The all-to-all form of one A2A step on a distributed mesh.
+std::shared_ptr<Exchange> get_alltoall(Mesh& mesh, const autoplan::ShardingSpec& src,
+                                       const autoplan::TransformStep& step,
+                                       const autoplan::TensorMeta& meta);
 // The all-gather form of one AG step on a distributed mesh.
 std::shared_ptr<Exchange> get_allgather(Mesh& mesh, const autoplan::ShardingSpec& src,
                                         const autoplan::TransformStep& step,

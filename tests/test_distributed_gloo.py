@@ -118,15 +118,19 @@ def test_distributed_schedule_over_gloo(world):
 
 
 # Stepwise conversions on the distributed executor: every reference step is
-# one hop -- an all-gather runs as ONE collective on that mesh axis's
-# communicator (emulated here with gloo all_gather on the axis group), the
-# other steps as point-to-point exchanges -- with intermediate shards between
-# hops, exactly as apl_conversion_schedule_json reports for each rank.
+# one hop -- an all-gather runs as ONE ncclAllGather and an all-to-all as ONE
+# ncclAlltoAll on that mesh axis's communicator (emulated here with gloo on
+# the axis group, members in coordinate order), a shard-slice as a local
+# copy -- with intermediate shards between hops, exactly as
+# apl_conversion_schedule_json reports for each rank.
 STEP_CASES = {
     4: [([2, 2], (64, 48), 4, "S01R", "RR"), ([2, 2], (16, 8, 12), 2, "S0S1R", "RRS1"),
-        ([4], (64, 32), 2, "S0R", "RR"), ([2, 2], (64, 48), 2, "S10R", "RS0")],
+        ([4], (64, 32), 2, "S0R", "RR"), ([2, 2], (64, 48), 2, "S10R", "RS0"),
+        ([4], (64, 32), 2, "S0R", "RS0"), ([2, 2], (8, 12, 16), 2, "S0S1R", "RS1S0"),
+        ([2, 2], (16, 16), 1, "S1S0", "S0S1")],
     8: [([2, 4], (64, 64), 2, "S01R", "S1S0"), ([2, 2, 2], (64, 64), 2, "S012R", "RS012"),
-        ([2, 4], (64, 64), 2, "RS01", "RR"), ([8], (64, 128), 4, "S0R", "RR")],
+        ([2, 4], (64, 64), 2, "RS01", "RR"), ([8], (64, 128), 4, "S0R", "RR"),
+        ([8], (64, 128), 4, "S0R", "RS0"), ([2, 4], (64, 64), 2, "RS01", "S1S0")],
 }
 
 
@@ -179,7 +183,34 @@ def _step_worker(rank, world, port, cases, q):
                 out = np.full(hop["out_bytes"], 0xAB, dtype=np.uint8)
                 send = np.zeros(max(1, hop["send_staging"]), dtype=np.uint8)
                 recv = np.zeros(max(1, hop["recv_staging"]), dtype=np.uint8)
-                if "allgather" in hop:
+                if "alltoall" in hop:
+                    n_ag += 1
+                    a2a = hop["alltoall"]
+                    members, _ = next((m, gr) for m, gr in groups[a2a["axis"]] if rank in m)
+                    ch = a2a["chunk"]
+                    for d in hop["pre"]:
+                        _copy(d, [cur, recv], [out, send])
+                    sbuf = cur if a2a["direct_send"] else send
+                    rbuf = out if a2a["direct_recv"] else recv
+                    reqs, landing = [], []
+                    for j, peer in enumerate(members):
+                        if peer == rank:
+                            me = members.index(rank)
+                            rbuf[me * ch:(me + 1) * ch] = sbuf[me * ch:(me + 1) * ch]
+                            continue
+                        reqs.append(dist.isend(torch.from_numpy(sbuf[j * ch:(j + 1) * ch].copy()),
+                                               peer))
+                        t = torch.empty(ch, dtype=torch.uint8)
+                        reqs.append(dist.irecv(t, peer))
+                        landing.append((j, t))
+                    for r in reqs:
+                        r.wait()
+                    for j, t in landing:
+                        rbuf[j * ch:(j + 1) * ch] = t.numpy()
+                    if not a2a["direct_recv"]:
+                        for d in hop["post"]:
+                            _copy(d, [cur, recv], [out, send])
+                elif "allgather" in hop:
                     n_ag += 1
                     a = hop["allgather"]["axis"]
                     members, grp = next((m, gr) for m, gr in groups[a] if rank in m)
@@ -235,4 +266,4 @@ def test_stepwise_schedule_with_axis_allgathers_over_gloo(world):
     assert len(results) == world * len(STEP_CASES[world])
     bad = [r for r in results if not r[3]]
     assert not bad, bad
-    assert all(r[4] >= 1 for r in results if r[2] in ("RR",))  # gathers ran as collectives
+    assert all(r[4] >= 1 for r in results)  # the gathers / all-to-alls ran as collectives
