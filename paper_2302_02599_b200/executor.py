@@ -378,6 +378,31 @@ class PlanExecutor:
                 if self.nodes[nid]["kind"] in kinds}
 
 
+    # ---- CUDA graphs ---------------------------------------------------------
+    def capture(self, feeds: dict, grad_out=None, warmup: int = 1):
+        """Record one step -- forward, or forward + backward when grad_out is
+        given -- into a CUDA graph and return (replay, outputs, grads): every
+        launch of the step (conversion kernels, GEMMs, all-reduces) replays
+        with no host work. The outputs / grads are the graph's own buffers,
+        rewritten by each replay; feeds must stay at the same addresses (copy
+        new data into them between replays)."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        train = grad_out is not None
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):  # compiles every exchange / tensor map
+                self.forward(feeds, stream=side, train=train)
+                if train:
+                    self.backward(grad_out, stream=side)
+            side.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=side):
+                outs = self.forward(feeds, stream=side, train=train)
+                grads = self.backward(grad_out, stream=side) if train else None
+        torch.cuda.current_stream().wait_stream(side)
+        return graph.replay, outs, grads
+
+
 def megatron_mlp_plan(mesh_rank: int = 1, axis: int = 0) -> dict:
     """BASELINE config 5 pinned selection on a mesh axis: fc1 split-n (RR x RS
     -> RS, GELU fused), fc2 split-k (RS x SR -> RR partial, all-reduce).
