@@ -346,6 +346,18 @@ int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, i
                   int64_t lda, int64_t ldb, int64_t ldc, int b_layout, int out_dtype,
                   int epilogue, void* stream);
 
+/* Grouped GEMM, one persistent launch: `groups` output problems, each the
+ * sum over `reduce` inputs C_g = epi(sum_r A[g*reduce+r] . B[g*reduce+r]),
+ * all problems [M,N] with inner dim K and the given leading dimensions.
+ * With reduce > 1 this is an all-gather of the B operand fused into the
+ * GEMM: the K-slices of a gathered weight are read straight from the
+ * buffers (or peer-mapped shards) that own them, no gathered copy. aux:
+ * APL_EPI_GELU_SAVE / APL_EPI_DGELU buffers, one per group (else NULL). */
+int apl_gemm_bf16_grouped(const void* const* A, const void* const* B, void* const* C,
+                          int groups, int reduce, int64_t M, int64_t N, int64_t K, int64_t lda,
+                          int64_t ldb, int64_t ldc, int b_layout, int out_dtype, int epilogue,
+                          const void* const* aux, void* stream);
+
 /* Execute a strategy on the mesh: per local device one tcgen05 GEMM on its
  * shards (A: local shard of A; B: local shard of B, [k_local, n_local] for
  * APL_B_KN or transposed [n_local, k_local] for APL_B_NK; C: local shard of

@@ -130,6 +130,10 @@ _SIGS = {
     "apl_sharded_matmul": (C.c_int, [C.c_void_p, P(MatmulStrategyC), P(Meta), P(Meta),
                                      P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
                                      C.c_int, C.c_int, C.c_void_p]),
+    "apl_gemm_bf16_grouped": (C.c_int, [P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
+                                        C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                        C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                        P(C.c_void_p), C.c_void_p]),
     "apl_sharded_matmul_ex": (C.c_int, [C.c_void_p, P(MatmulStrategyC), P(Meta), P(Meta),
                                         P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
                                         C.c_int, C.c_int, P(C.c_void_p), C.c_void_p]),

@@ -852,6 +852,33 @@ int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, i
   });
 }
 
+int apl_gemm_bf16_grouped(const void* const* A, const void* const* B, void* const* C,
+                          int groups, int reduce, int64_t M, int64_t N, int64_t K, int64_t lda,
+                          int64_t ldb, int64_t ldc, int b_layout, int out_dtype, int epilogue,
+                          const void* const* aux, void* stream) {
+  return guarded([&] {
+    need(A && B && C, "null operand table");
+    need(groups >= 1 && reduce >= 1 && reduce <= 8, "groups >= 1, 1 <= reduce <= 8");
+    need(M > 0 && N > 0 && K > 0 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX,
+         "extents out of range");
+    need(b_layout == APL_B_NK || b_layout == APL_B_KN, "unknown B layout");
+    const bool kn = b_layout == APL_B_KN;
+    need(lda >= K && ldb >= (kn ? N : K) && ldc >= N, "leading dimensions too small");
+    need(out_dtype == APL_F32 || out_dtype == APL_BF16, "output dtype must be f32 or bf16");
+    need(epilogue >= APL_EPI_NONE && epilogue <= APL_EPI_GELU_SAVE, "unknown epilogue");
+    need(epilogue < APL_EPI_DGELU || aux != nullptr, "epilogue needs aux buffers");
+    for (int i = 0; i < groups * reduce; ++i) need(A[i] && B[i], "null operand");
+    for (int i = 0; i < groups; ++i) need(C[i] != nullptr, "null output");
+    apl::check_cuda(apl::gemm_bf16_grouped(A, B, C, groups, reduce, 1, static_cast<int>(M),
+                                           static_cast<int>(N), static_cast<int>(K),
+                                           static_cast<int>(lda), static_cast<int>(ldb),
+                                           static_cast<int>(ldc), kn, out_dtype == APL_F32,
+                                           epilogue, false, aux, static_cast<int>(ldc),
+                                           static_cast<cudaStream_t>(stream)),
+                    "grouped GEMM launch");
+  });
+}
+
 int apl_sharded_matmul_ex(apl_mesh* mesh, const apl_matmul_strategy* strategy,
                           const apl_meta* a_meta, const apl_meta* b_meta, const void* const* A,
                           const void* const* B, void* const* C, int b_layout, int out_dtype,

@@ -139,6 +139,29 @@ class PeerRuntime:
                                    table, C.c_void_p(out.data_ptr()), _stream_handle(stream)))
         self._store(True, stream)
 
+    # ---- fused all-gather -> GEMM -------------------------------------------
+    def peer_ptr(self, t: torch.Tensor, rank: int) -> int:
+        """Device address of heap tensor `t` on `rank`, mapped here."""
+        return self.peer_base[rank] + (t.data_ptr() - self.heap_base)
+
+    def gather_begin(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """Publish this rank's block of a sharded operand for peers to read in
+        place (staged in the heap if needed; ready flags): the all-gather of
+        an all-gather -> GEMM fusion, whose GEMM then reads the owners'
+        blocks over peer memory. Pair with gather_end()."""
+        if not self._in_heap(x):
+            y = self.empty(x.shape, x.dtype)
+            y.copy_(x)
+            x = y
+        self.pm.epoch += 1
+        self._store(False, stream)
+        self._wait(self._all_others(), self.pm.epoch, False, stream)
+        return x
+
+    def gather_end(self, stream=None) -> None:
+        """This rank's readers of peer blocks are done (after the GEMM)."""
+        self._store(True, stream)
+
     # ---- partial sums ----------------------------------------------------------
     def all_reduce(self, axes: Sequence[int], tensors, stream=None) -> None:
         """In-place sum over the mesh-axis group of `axes` (one kernel)."""

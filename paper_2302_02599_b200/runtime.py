@@ -32,6 +32,22 @@ def _stream_handle(stream) -> C.c_void_p:
     return C.c_void_p(s.cuda_stream)
 
 
+def gemm_grouped(a_ptrs, b_ptrs, c_ptrs, reduce: int, M: int, N: int, K: int, lda: int,
+                 ldb: int, ldc: int, b_layout: str = "kn", out_dtype=torch.bfloat16,
+                 gelu: bool = False, stream=None) -> None:
+    """Grouped tcgen05 GEMM over raw device pointers (apl_gemm_bf16_grouped):
+    C[g] = epi(sum_r A[g*reduce+r] . B[g*reduce+r]). Used for all-gather ->
+    GEMM fusion: B[r] are the owner buffers of a sharded weight's K-slices."""
+    P = C.c_void_p
+    arr = lambda xs: (P * len(xs))(*xs)  # noqa: E731
+    check(A.lib().apl_gemm_bf16_grouped(arr(a_ptrs), arr(b_ptrs), arr(c_ptrs), len(c_ptrs), reduce,
+                                        M, N, K, lda, ldb, ldc,
+                                        A.B_KN if b_layout == "kn" else A.B_NK,
+                                        _DTYPE_CODE[out_dtype],
+                                        A.EPI_GELU if gelu else A.EPI_NONE, None,
+                                        _stream_handle(stream)))
+
+
 def gelu(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
     """y = GELU(x) on the device (exact erf)."""
     check(A.lib().apl_gelu(C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), x.numel(),

@@ -79,3 +79,19 @@ def test_captured_training_step_replays(cuda, operands):
     for k in eager_grads:
         for a, b in zip(grads[k], eager_grads[k]):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["gpt2_mlp_mesh8_96.json", "gpt2_mlp_mesh2x4_96.json",
+                                  "gpt2_mlp_mesh2x2x2_192.json"])
+def test_weight_gather_fused_into_gemm(cuda, operands, name):
+    """fuse_gather=True: the plans' weight all-gathers run inside a grouped
+    GEMM that reads each K/N block from the device holding it."""
+    feeds, ref = operands
+    plan = json.loads((PLANS / name).read_text())
+    mesh = Mesh.local(plan["mesh"]["shape"])
+    ex = PlanExecutor(mesh, GRAPH, plan, fuse_gather=True)
+    assert ex._gatherable_b("fc1") and ex._gatherable_b("fc2")
+    outs = ex.forward(feeds)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert ((o.double() - ref).abs().max() / ref.abs().max()).item() <= TOL
