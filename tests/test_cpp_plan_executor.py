@@ -1,0 +1,61 @@
+"""The native C++ PlanExecutor (include/autoplan/plan_executor.hpp) runs the
+reference planner's GPT-2-medium MLP plans and produces exactly the bytes of
+the Python PlanExecutor (same kernels, same order) -- and both match fp32
+torch within the config-5 tolerance."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+PLANS = ROOT / "tests" / "golden" / "plans"
+NLOHMANN = Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty")
+
+
+def build(tmp_path):
+    exe = tmp_path / "plan_executor_test"
+    lib = ROOT / "paper_2302_02599_b200"
+    cmd = ["g++", "-std=c++20", "-O1", f"-I{ROOT / 'include'}", f"-I{NLOHMANN}",
+           "-I/usr/local/cuda/include", str(ROOT / "tests/cpp/plan_executor_test.cpp"),
+           f"-L{lib}", "-lapl", "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}",
+           "-Wl,-rpath,/usr/local/cuda/lib64", "-o", str(exe)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+@pytest.mark.skipif(not NLOHMANN.exists(), reason="nlohmann/json headers not in this image")
+def test_plan_executor_header_compiles(tmp_path):
+    build(tmp_path)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["gpt2_mlp_mesh8_unlimited.json", "gpt2_mlp_mesh2x4_96.json",
+                                  "gpt2_mlp_mesh2x2x2_unlimited.json"])
+def test_native_executor_matches_python_executor(cuda, tmp_path, name):
+    import torch
+
+    from paper_2302_02599_b200.executor import PlanExecutor
+    from paper_2302_02599_b200.runtime import Mesh
+
+    exe = build(tmp_path)
+    torch.manual_seed(2302)
+    feeds = {"x": torch.randn(16384, 1024, device="cuda").bfloat16(),
+             "w1": (torch.randn(1024, 4096, device="cuda") / 32).bfloat16(),
+             "w2": (torch.randn(4096, 1024, device="cuda") / 64).bfloat16()}
+    for k, v in feeds.items():
+        (tmp_path / f"{k}.bin").write_bytes(v.view(torch.int16).cpu().numpy().tobytes())
+    plan = json.loads((PLANS / name).read_text())
+    mesh_arg = "x".join(map(str, plan["mesh"]["shape"]))
+    r = subprocess.run([str(exe), str(PLANS / "gpt2_mlp_graph.json"), str(PLANS / name), mesh_arg,
+                        str(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    native = (tmp_path / "out.bin").read_bytes()
+    mesh = Mesh.local(plan["mesh"]["shape"])
+    ex = PlanExecutor(mesh, json.loads((PLANS / "gpt2_mlp_graph.json").read_text()), plan)
+    out = ex.forward(feeds)[0]
+    torch.cuda.synchronize()
+    assert out.view(torch.int16).cpu().numpy().tobytes() == native
+    ref = torch.nn.functional.gelu(feeds["x"].float() @ feeds["w1"].float()) @ feeds["w2"].float()
+    assert ((out.double() - ref.double()).abs().max() / ref.abs().max()).item() <= 2e-2
