@@ -391,6 +391,36 @@ int apl_gelu(const void* x, void* y, size_t count, int dtype, void* stream);
 int apl_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int dtype,
                       void* stream);
 
+/* ---- transformer-block node kinds (gpt_block plans) -------
+ * The non-GEMM kinds of the reference's block graph (graph_ir.cpp:40-46,
+ * shape rules graph_ir.cpp:240-345) on ONE device's shard. Every strategy
+ * the reference generates for them is local (intraop.cpp:280-450), so these
+ * never communicate; the plan executor converts their inputs first. dtype:
+ * APL_F32 or APL_BF16, fp32 math. */
+
+/* embedding-lookup: out[t, :] = table[ids[t], :] for n int64 ids; table
+ * [vocab, width] of elem_bytes elements (a hidden-sharded table is just a
+ * narrower one). Ids outside [0, vocab) give zero rows. */
+int apl_embedding_lookup(const int64_t* ids, int64_t n, const void* table, int64_t vocab,
+                         int64_t width, int elem_bytes, void* out, void* stream);
+/* layernorm over the last dim: y = (x - mean) / sqrt(var + eps) * gamma + beta
+ * per row of `width`; gamma / beta may be NULL (no affine). */
+int apl_layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,
+                  int64_t width, float eps, int dtype, void* stream);
+/* softmax over the last dim (rows of `width`). */
+int apl_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype, void* stream);
+/* transpose perm [0, 2, 1]: x [batch, rows, cols] -> y [batch, cols, rows]. */
+int apl_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
+                  int elem_bytes, void* stream);
+/* elementwise-unary y = alpha * x. */
+int apl_scale(const void* x, void* y, size_t count, float alpha, int dtype, void* stream);
+/* elementwise-binary y = a + alpha * b; b has a's dtype, or with b_mask != 0
+ * is a u8 0/1 mask (alpha = -1e4: the additive attention mask). */
+int apl_add(const void* a, const void* b, int b_mask, void* y, size_t count, float alpha,
+            int dtype, void* stream);
+/* elementwise-unary on a u8 mask: y = !x. */
+int apl_mask_not(const void* x, void* y, size_t count, void* stream);
+
 #define APL_EPI_DGELU 2 /* backward epilogue: dA *= GELU'(aux) */
 
 /* Backward of apl_sharded_matmul for the same strategy and shards: per local

@@ -159,6 +159,18 @@ _SIGS = {
                                        C.c_void_p]),
     "apl_peer_flags_wait": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_int, C.c_uint32,
                                       C.c_uint32, C.c_void_p]),
+    "apl_embedding_lookup": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                                       C.c_int, C.c_void_p, C.c_void_p]),
+    "apl_layernorm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                C.c_int64, C.c_float, C.c_int, C.c_void_p]),
+    "apl_softmax": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                              C.c_void_p]),
+    "apl_transpose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
+                                C.c_void_p]),
+    "apl_scale": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_float, C.c_int, C.c_void_p]),
+    "apl_add": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_float,
+                          C.c_int, C.c_void_p]),
+    "apl_mask_not": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
 }
 
 # Symbols every build must export (tests check the .so against include/apl.h).

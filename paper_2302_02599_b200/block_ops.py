@@ -1,0 +1,71 @@
+"""Transformer-block node kinds on one shard (apl_embedding_lookup, apl_layernorm,
+apl_softmax, apl_transpose, apl_scale, apl_add, apl_mask_not; block_ops.cu).
+
+The non-GEMM kinds of the reference's gpt_block graph (graph_ir.cpp:40-46,
+shape rules graph_ir.cpp:240-345). The reference's strategies keep all of
+them local (intraop.cpp:280-450), so each call works on one device's shard
+and never communicates. Tensors in, tensors out; no torch compute, no fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _capi as A
+from .layout import check
+from .runtime import _DTYPE_CODE, _stream_handle
+
+
+def _p(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None else None)
+
+
+def embedding(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor, stream=None) -> None:
+    """out[..., :] = table[ids[...], :]; ids int64, table [vocab, width]."""
+    if ids.dtype != torch.int64:
+        raise TypeError("ids must be int64")
+    check(A.lib().apl_embedding_lookup(_p(ids), ids.numel(), _p(table), table.shape[0],
+                                       table.shape[1], table.element_size(), _p(out),
+                                       _stream_handle(stream)))
+
+
+def layernorm(x: torch.Tensor, gamma: torch.Tensor | None, beta: torch.Tensor | None,
+              y: torch.Tensor, eps: float = 1e-5, stream=None) -> None:
+    w = x.shape[-1]
+    check(A.lib().apl_layernorm(_p(x), _p(gamma), _p(beta), _p(y), x.numel() // w, w, eps,
+                                _DTYPE_CODE[x.dtype], _stream_handle(stream)))
+
+
+def softmax(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
+    """Softmax over the last dim."""
+    w = x.shape[-1]
+    check(A.lib().apl_softmax(_p(x), _p(y), x.numel() // w, w, _DTYPE_CODE[x.dtype],
+                              _stream_handle(stream)))
+
+
+def transpose_last2(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
+    """y = x with its last two dims swapped (perm [..., -1, -2])."""
+    r, c = x.shape[-2], x.shape[-1]
+    check(A.lib().apl_transpose(_p(x), _p(y), x.numel() // max(1, r * c), r, c,
+                                x.element_size(), _stream_handle(stream)))
+
+
+def scale(x: torch.Tensor, y: torch.Tensor, alpha: float, stream=None) -> None:
+    check(A.lib().apl_scale(_p(x), _p(y), x.numel(), alpha, _DTYPE_CODE[x.dtype],
+                            _stream_handle(stream)))
+
+
+def add(a: torch.Tensor, b: torch.Tensor, y: torch.Tensor, alpha: float = 1.0,
+        stream=None) -> None:
+    """y = a + alpha * b; b of a's dtype, or a uint8 0/1 mask."""
+    mask = b.dtype == torch.uint8
+    if not mask and b.dtype != a.dtype:
+        raise TypeError("b must have a's dtype or be a uint8 mask")
+    check(A.lib().apl_add(_p(a), _p(b), 1 if mask else 0, _p(y), a.numel(), alpha,
+                          _DTYPE_CODE[a.dtype], _stream_handle(stream)))
+
+
+def mask_not(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
+    """y = !x on a uint8 mask."""
+    check(A.lib().apl_mask_not(_p(x), _p(y), x.numel(), _stream_handle(stream)))

@@ -53,6 +53,7 @@ CUDA_SRCS = [
     CSRC / "kernels" / "bulk_copy.cu",
     CSRC / "kernels" / "tile_copy.cu",
     CSRC / "kernels" / "reduce.cu",
+    CSRC / "kernels" / "block_ops.cu",
     CSRC / "kernels" / "peer_sync.cu",
     CSRC / "kernels" / "gemm_tcgen05.cu",
 ]

@@ -946,6 +946,86 @@ int apl_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int
   });
 }
 
+int apl_embedding_lookup(const int64_t* ids, int64_t n, const void* table, int64_t vocab,
+                         int64_t width, int elem_bytes, void* out, void* stream) {
+  return guarded([&] {
+    need(n >= 0 && width >= 0 && vocab >= 0, "negative extent");
+    need((ids && table && out) || n == 0 || width == 0, "null buffer");
+    need(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8,
+         "elem_bytes must be 1, 2, 4 or 8");
+    apl::check_cuda(apl::launch_embedding(ids, n, table, vocab, width, elem_bytes, out,
+                                          static_cast<cudaStream_t>(stream)),
+                    "embedding launch");
+  });
+}
+
+int apl_layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,
+                  int64_t width, float eps, int dtype, void* stream) {
+  return guarded([&] {
+    need(rows >= 0 && width > 0, "bad extents");
+    need((x && y) || rows == 0, "null buffer");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    apl::check_cuda(apl::launch_layernorm(x, gamma, beta, y, rows, width, eps, dtype,
+                                          static_cast<cudaStream_t>(stream)),
+                    "layernorm launch");
+  });
+}
+
+int apl_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype, void* stream) {
+  return guarded([&] {
+    need(rows >= 0 && width > 0, "bad extents");
+    need((x && y) || rows == 0, "null buffer");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    apl::check_cuda(
+        apl::launch_softmax(x, y, rows, width, dtype, static_cast<cudaStream_t>(stream)),
+        "softmax launch");
+  });
+}
+
+int apl_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
+                  int elem_bytes, void* stream) {
+  return guarded([&] {
+    need(batch >= 0 && rows >= 0 && cols >= 0 && rows <= INT32_MAX && cols <= INT32_MAX,
+         "extents out of range");
+    need((x && y) || batch * rows * cols == 0, "null buffer");
+    need(x != y, "transpose is out of place");
+    need(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8,
+         "elem_bytes must be 1, 2, 4 or 8");
+    apl::check_cuda(apl::launch_transpose(x, y, batch, rows, cols, elem_bytes,
+                                          static_cast<cudaStream_t>(stream)),
+                    "transpose launch");
+  });
+}
+
+int apl_scale(const void* x, void* y, size_t count, float alpha, int dtype, void* stream) {
+  return guarded([&] {
+    need((x && y) || count == 0, "null buffer");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    apl::check_cuda(
+        apl::launch_scale(x, y, count, alpha, dtype, static_cast<cudaStream_t>(stream)),
+        "scale launch");
+  });
+}
+
+int apl_add(const void* a, const void* b, int b_mask, void* y, size_t count, float alpha,
+            int dtype, void* stream) {
+  return guarded([&] {
+    need((a && b && y) || count == 0, "null buffer");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    apl::check_cuda(apl::launch_add(a, b, b_mask != 0, y, count, alpha, dtype,
+                                    static_cast<cudaStream_t>(stream)),
+                    "add launch");
+  });
+}
+
+int apl_mask_not(const void* x, void* y, size_t count, void* stream) {
+  return guarded([&] {
+    need((x && y) || count == 0, "null buffer");
+    apl::check_cuda(apl::launch_mask_not(x, y, count, static_cast<cudaStream_t>(stream)),
+                    "mask launch");
+  });
+}
+
 int apl_sharded_matmul_backward(apl_mesh* mesh, const apl_matmul_strategy* strategy,
                                 const apl_meta* a_meta, const apl_meta* b_meta,
                                 const void* const* A, const void* const* B,

@@ -1,0 +1,388 @@
+// The non-GEMM node kinds of the reference's transformer-block graph
+// (proj/tests/fixtures/gpt_block.json; kinds graph_ir.cpp:40-46, shape rules
+// graph_ir.cpp:240-345), run on one device's shard. Every strategy the
+// reference generates for them keeps the op local (intraop.cpp:280-450: the
+// softmax / layernorm axis stays replicated, an embedding shards the lookup
+// batch or the table's hidden dim, a transpose permutes the spec with the
+// data), so these kernels never communicate: the plan executor converts
+// their inputs first.
+//
+// All HBM-bound; fp32 math, bf16 / f32 / u8 storage:
+//   embedding  : rows of the table gathered per id       (width x eb read + written per id)
+//   layernorm  : warp per row, mean / var / affine        (row read 3x from L1, written once)
+//   softmax    : warp per row, online max + sum, write    (row read 2x, written once)
+//   transpose  : [batch, R, C] -> [batch, C, R], 32 x 32 shared-memory tiles
+//   scale / add / not : 16-byte vectors, grid-stride
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+
+namespace apl {
+
+extern std::atomic<uint64_t> g_launches;
+
+namespace {
+
+__device__ __forceinline__ float ld(const float* p) { return *p; }
+__device__ __forceinline__ float ld(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void st(float* p, float v) { *p = v; }
+__device__ __forceinline__ void st(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// V contiguous elements per access: 16-byte vectors when the row allows, else 1.
+template <typename T, int V>
+struct Vec {
+  T v[V];
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void load_row(const T* row, int64_t i, float (&f)[V]) {
+  const Vec<T, V> x = reinterpret_cast<const Vec<T, V>*>(row)[i];
+#pragma unroll
+  for (int k = 0; k < V; ++k) f[k] = ld(&x.v[k]);
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void store_row(T* row, int64_t i, const float (&f)[V]) {
+  Vec<T, V> x;
+#pragma unroll
+  for (int k = 0; k < V; ++k) st(&x.v[k], f[k]);
+  reinterpret_cast<Vec<T, V>*>(row)[i] = x;
+}
+
+// ---- embedding lookup: out[t, :] = table[ids[t], :] ------------------------
+// Ids outside [0, vocab) produce a zero row (the reference plans the op and
+// does not define out-of-range lookups).
+template <typename W>
+__global__ void __launch_bounds__(256) embedding_kernel(const int64_t* __restrict__ ids, int64_t n,
+                                                        const W* __restrict__ table, int64_t vocab,
+                                                        int64_t words, W* __restrict__ out) {
+  const int64_t total = n * words;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += stride) {
+    const int64_t t = i / words, w = i - t * words;
+    const int64_t id = __ldg(ids + t);
+    W v{};
+    if (id >= 0 && id < vocab) v = table[id * words + w];
+    out[i] = v;
+  }
+}
+
+// ---- layernorm over the last dim ----------------------------------------
+template <typename T, int V>
+__global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
+                                                        const T* __restrict__ gamma,
+                                                        const T* __restrict__ beta,
+                                                        T* __restrict__ y, int64_t rows,
+                                                        int64_t width, float eps) {
+  const int lane = threadIdx.x % 32;
+  const int64_t nv = width / V;
+  const float inv_w = 1.f / static_cast<float>(width);
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const T* xr = x + r * width;
+    T* yr = y + r * width;
+    float s = 0.f;
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V];
+      load_row<T, V>(xr, i, f);
+#pragma unroll
+      for (int k = 0; k < V; ++k) s += f[k];
+    }
+    const float mean = warp_sum(s) * inv_w;
+    float q = 0.f;
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V];
+      load_row<T, V>(xr, i, f);
+#pragma unroll
+      for (int k = 0; k < V; ++k) q += (f[k] - mean) * (f[k] - mean);
+    }
+    const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V], g[V], b[V];
+      load_row<T, V>(xr, i, f);
+      if (gamma != nullptr) load_row<T, V>(gamma, i, g);
+      if (beta != nullptr) load_row<T, V>(beta, i, b);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        float v = (f[k] - mean) * rstd;
+        if (gamma != nullptr) v *= g[k];
+        if (beta != nullptr) v += b[k];
+        f[k] = v;
+      }
+      store_row<T, V>(yr, i, f);
+    }
+  }
+}
+
+// ---- softmax over the last dim ------------------------------------------
+template <typename T, int V>
+__global__ void __launch_bounds__(256) softmax_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                      int64_t rows, int64_t width) {
+  const int lane = threadIdx.x % 32;
+  const int64_t nv = width / V;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const T* xr = x + r * width;
+    T* yr = y + r * width;
+    float m = -INFINITY, s = 0.f;  // online max / sum per lane
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V];
+      load_row<T, V>(xr, i, f);
+      float mv = f[0];
+#pragma unroll
+      for (int k = 1; k < V; ++k) mv = fmaxf(mv, f[k]);
+      const float nm = fmaxf(m, mv);
+      s *= __expf(m - nm);
+#pragma unroll
+      for (int k = 0; k < V; ++k) s += __expf(f[k] - nm);
+      m = nm;
+    }
+    const float gm = warp_max(m);
+    const float gs = warp_sum(m == -INFINITY ? 0.f : s * __expf(m - gm));
+    const float inv = 1.f / gs;
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V];
+      load_row<T, V>(xr, i, f);
+#pragma unroll
+      for (int k = 0; k < V; ++k) f[k] = __expf(f[k] - gm) * inv;
+      store_row<T, V>(yr, i, f);
+    }
+  }
+}
+
+// ---- [batch, R, C] -> [batch, C, R] -------------------------------------
+template <typename W>
+__global__ void __launch_bounds__(256) transpose_kernel(const W* __restrict__ x, W* __restrict__ y,
+                                                        int64_t batch, int R, int C) {
+  __shared__ W tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int64_t b = blockIdx.z; b < batch; b += gridDim.z) {
+    const W* xb = x + b * R * static_cast<int64_t>(C);
+    W* yb = y + b * R * static_cast<int64_t>(C);
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int r = r0 + j, c = c0 + threadIdx.x;
+      if (r < R && c < C) tile[j][threadIdx.x] = xb[static_cast<int64_t>(r) * C + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int c = c0 + j, r = r0 + threadIdx.x;
+      if (r < R && c < C) yb[static_cast<int64_t>(c) * R + r] = tile[threadIdx.x][j];
+    }
+    __syncthreads();
+  }
+}
+
+// ---- elementwise ----------------------------------------------------------
+// y = alpha * x
+template <typename T, int V>
+__global__ void __launch_bounds__(256) scale_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                    int64_t nv, float alpha) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float f[V];
+    load_row<T, V>(x, i, f);
+#pragma unroll
+    for (int k = 0; k < V; ++k) f[k] *= alpha;
+    store_row<T, V>(y, i, f);
+  }
+}
+
+// y = a + alpha * b, b of the same type or a u8 mask (B = uint8_t)
+template <typename T, typename B, int V>
+__global__ void __launch_bounds__(256) add_kernel(const T* __restrict__ a, const B* __restrict__ b,
+                                                  T* __restrict__ y, int64_t nv, float alpha) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float f[V];
+    load_row<T, V>(a, i, f);
+    const Vec<B, V> bv = reinterpret_cast<const Vec<B, V>*>(b)[i];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float g;
+      if constexpr (sizeof(B) == 1) g = static_cast<float>(bv.v[k]);
+      else g = ld(&bv.v[k]);
+      f[k] += alpha * g;
+    }
+    store_row<T, V>(y, i, f);
+  }
+}
+
+__global__ void __launch_bounds__(256) not_kernel(const uint8_t* __restrict__ x,
+                                                  uint8_t* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = x[i] == 0 ? 1 : 0;
+}
+
+int grid_for(int64_t threads) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((threads + 255) / 256, 148 * 16)));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+cudaError_t done() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t rowwise(bool softmax, const void* x, const void* g, const void* b, void* y,
+                    int64_t rows, int64_t width, float eps, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const bool vec = width % V == 0 && aligned16(x) && aligned16(y) && (!g || aligned16(g)) &&
+                   (!b || aligned16(b));
+  const int grid = grid_for(rows * 32);
+  auto X = static_cast<const T*>(x);
+  auto Y = static_cast<T*>(y);
+  if (softmax) {
+    if (vec) softmax_kernel<T, V><<<grid, 256, 0, s>>>(X, Y, rows, width);
+    else softmax_kernel<T, 1><<<grid, 256, 0, s>>>(X, Y, rows, width);
+  } else {
+    auto G = static_cast<const T*>(g);
+    auto B = static_cast<const T*>(b);
+    if (vec) layernorm_kernel<T, V><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);
+    else layernorm_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);
+  }
+  return done();
+}
+
+template <typename T>
+cudaError_t scale_typed(const void* x, void* y, size_t count, float alpha, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t n = static_cast<int64_t>(count);
+  if (n % V == 0 && aligned16(x) && aligned16(y))
+    scale_kernel<T, V><<<grid_for(n / V), 256, 0, s>>>(static_cast<const T*>(x), static_cast<T*>(y),
+                                                       n / V, alpha);
+  else
+    scale_kernel<T, 1><<<grid_for(n), 256, 0, s>>>(static_cast<const T*>(x), static_cast<T*>(y), n,
+                                                   alpha);
+  return done();
+}
+
+template <typename T>
+cudaError_t add_typed(const void* a, const void* b, bool b_mask, void* y, size_t count, float alpha,
+                      cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t n = static_cast<int64_t>(count);
+  // a u8 operand moves V bytes per access: keep it 4-byte aligned at least
+  const bool vec = n % V == 0 && aligned16(a) && aligned16(y) &&
+                   (b_mask ? (reinterpret_cast<uintptr_t>(b) % V == 0) : aligned16(b));
+  auto A = static_cast<const T*>(a);
+  auto Y = static_cast<T*>(y);
+  if (b_mask) {
+    auto Bm = static_cast<const uint8_t*>(b);
+    if (vec) add_kernel<T, uint8_t, V><<<grid_for(n / V), 256, 0, s>>>(A, Bm, Y, n / V, alpha);
+    else add_kernel<T, uint8_t, 1><<<grid_for(n), 256, 0, s>>>(A, Bm, Y, n, alpha);
+  } else {
+    auto Bt = static_cast<const T*>(b);
+    if (vec) add_kernel<T, T, V><<<grid_for(n / V), 256, 0, s>>>(A, Bt, Y, n / V, alpha);
+    else add_kernel<T, T, 1><<<grid_for(n), 256, 0, s>>>(A, Bt, Y, n, alpha);
+  }
+  return done();
+}
+
+}  // namespace
+
+cudaError_t launch_embedding(const int64_t* ids, int64_t n, const void* table, int64_t vocab,
+                             int64_t width, int elem_bytes, void* out, cudaStream_t s) {
+  if (n == 0 || width == 0) return cudaSuccess;
+  const int64_t row = width * elem_bytes;
+  if (row % 16 == 0 && aligned16(table) && aligned16(out))
+    embedding_kernel<uint4><<<grid_for(n * row / 16), 256, 0, s>>>(
+        ids, n, static_cast<const uint4*>(table), vocab, row / 16, static_cast<uint4*>(out));
+  else if (row % 4 == 0 && reinterpret_cast<uintptr_t>(table) % 4 == 0 &&
+           reinterpret_cast<uintptr_t>(out) % 4 == 0)
+    embedding_kernel<uint32_t><<<grid_for(n * row / 4), 256, 0, s>>>(
+        ids, n, static_cast<const uint32_t*>(table), vocab, row / 4, static_cast<uint32_t*>(out));
+  else
+    embedding_kernel<uint8_t><<<grid_for(n * row), 256, 0, s>>>(
+        ids, n, static_cast<const uint8_t*>(table), vocab, row, static_cast<uint8_t*>(out));
+  return done();
+}
+
+cudaError_t launch_layernorm(const void* x, const void* gamma, const void* beta, void* y,
+                             int64_t rows, int64_t width, float eps, int dtype, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  if (dtype == 0) return rowwise<float>(false, x, gamma, beta, y, rows, width, eps, s);
+  if (dtype == 1) return rowwise<__nv_bfloat16>(false, x, gamma, beta, y, rows, width, eps, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype,
+                           cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  if (dtype == 0) return rowwise<float>(true, x, nullptr, nullptr, y, rows, width, 0.f, s);
+  if (dtype == 1) return rowwise<__nv_bfloat16>(true, x, nullptr, nullptr, y, rows, width, 0.f, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
+                             int elem_bytes, cudaStream_t s) {
+  if (batch == 0 || rows == 0 || cols == 0) return cudaSuccess;
+  const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32),
+                  static_cast<unsigned>(std::min<int64_t>(batch, 65535)));
+  const dim3 block(32, 8);
+  const int R = static_cast<int>(rows), C = static_cast<int>(cols);
+  switch (elem_bytes) {
+    case 1:
+      transpose_kernel<uint8_t><<<grid, block, 0, s>>>(static_cast<const uint8_t*>(x),
+                                                       static_cast<uint8_t*>(y), batch, R, C);
+      break;
+    case 2:
+      transpose_kernel<uint16_t><<<grid, block, 0, s>>>(static_cast<const uint16_t*>(x),
+                                                        static_cast<uint16_t*>(y), batch, R, C);
+      break;
+    case 4:
+      transpose_kernel<uint32_t><<<grid, block, 0, s>>>(static_cast<const uint32_t*>(x),
+                                                        static_cast<uint32_t*>(y), batch, R, C);
+      break;
+    case 8:
+      transpose_kernel<uint64_t><<<grid, block, 0, s>>>(static_cast<const uint64_t*>(x),
+                                                        static_cast<uint64_t*>(y), batch, R, C);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return done();
+}
+
+cudaError_t launch_scale(const void* x, void* y, size_t count, float alpha, int dtype,
+                         cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  if (dtype == 0) return scale_typed<float>(x, y, count, alpha, s);
+  if (dtype == 1) return scale_typed<__nv_bfloat16>(x, y, count, alpha, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_add(const void* a, const void* b, bool b_mask, void* y, size_t count,
+                       float alpha, int dtype, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  if (dtype == 0) return add_typed<float>(a, b, b_mask, y, count, alpha, s);
+  if (dtype == 1) return add_typed<__nv_bfloat16>(a, b, b_mask, y, count, alpha, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mask_not(const void* x, void* y, size_t count, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  const int64_t n = static_cast<int64_t>(count);
+  not_kernel<<<grid_for(n), 256, 0, s>>>(static_cast<const uint8_t*>(x), static_cast<uint8_t*>(y),
+                                         n);
+  return done();
+}
+
+}  // namespace apl

@@ -56,6 +56,20 @@ cudaError_t launch_flag_wait(const uint32_t* flags, const int* slots, int n, uin
 cudaError_t launch_gelu(const void* x, void* y, size_t count, int dtype, cudaStream_t stream);
 cudaError_t launch_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int dtype,
                                  cudaStream_t stream);
+// Transformer-block node kinds on one shard (block_ops.cu).
+cudaError_t launch_embedding(const int64_t* ids, int64_t n, const void* table, int64_t vocab,
+                             int64_t width, int elem_bytes, void* out, cudaStream_t s);
+cudaError_t launch_layernorm(const void* x, const void* gamma, const void* beta, void* y,
+                             int64_t rows, int64_t width, float eps, int dtype, cudaStream_t s);
+cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype,
+                           cudaStream_t s);
+cudaError_t launch_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
+                             int elem_bytes, cudaStream_t s);
+cudaError_t launch_scale(const void* x, void* y, size_t count, float alpha, int dtype,
+                         cudaStream_t s);
+cudaError_t launch_add(const void* a, const void* b, bool b_mask, void* y, size_t count,
+                       float alpha, int dtype, cudaStream_t s);
+cudaError_t launch_mask_not(const void* x, void* y, size_t count, cudaStream_t s);
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                       int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream);
 cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,

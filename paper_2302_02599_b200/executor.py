@@ -21,7 +21,22 @@ and executes the forward pass on a `runtime.Mesh` (simulated or distributed):
     all-reduce of `<host>.ar` (planner.cpp:263-282);
   * an elementwise-unary GELU consuming a non-partial matmul output in the
     same layout is fused into the GEMM epilogue;
+  * the transformer-block kinds (gpt_block graph: embedding-lookup, layernorm,
+    reshape, transpose, batched-matmul, softmax, elementwise-binary) run
+    their named strategy (intraop.cpp:280-450) on the local shards: reshape
+    is a view with the plan's rewritten local shape (reshape_rewrites,
+    planner.cpp:401-450), transpose permutes shard and spec together,
+    batched matmul is one grouped tcgen05 GEMM per device (+ the partial-sum
+    all-reduce of split-k strategies), the rest are block_ops.cu kernels;
   * the output node collects to RR (intraop.cpp:469-482).
+
+The graph format names the elementwise-unary function only by node id (the
+reference plans it as an opaque elementwise op), so the executor binds:
+a uint8 operand -> logical not (the block's `mask2`); an id containing
+"scale" behind a batched matmul -> x / sqrt(k) (attention scaling); anything
+else -> exact-erf GELU. A binary op with a uint8 operand adds it as an
+additive mask (a - 1e4 * m); otherwise it is a + b (residuals). `unary=`
+overrides the binding per node.
 
 The executor also cross-checks its own communication against the plan's
 `inserted_comm_nodes` (same producers/consumers, same step kinds and axes),
@@ -33,10 +48,13 @@ from dataclasses import dataclass, field
 
 import torch
 
-from .layout import DeviceMesh, ShardingSpec, TensorMeta, find_transform_path
+from .layout import DeviceMesh, DimSpec, ShardingSpec, TensorMeta, find_transform_path
 from .strategies import MatmulStrategy, find_matmul_strategy
 
-_DTYPES = {2: torch.bfloat16, 4: torch.float32}
+_DTYPES = {1: torch.uint8, 2: torch.bfloat16, 4: torch.float32, 8: torch.int64}
+_BLOCK_KINDS = ("embedding-lookup", "layernorm", "reshape", "transpose", "softmax",
+                "elementwise-binary", "batched-matmul")
+MASK_FILL = -1e4  # additive attention mask: a + MASK_FILL * m
 
 
 def infer_shapes(graph: dict) -> dict:
@@ -56,8 +74,18 @@ def infer_shapes(graph: dict) -> dict:
         elif k == "batched-matmul":
             (a, ea), (b, _) = ins
             out[n["id"]] = ((a[0], a[1], b[2]), ea)
-        elif k in ("elementwise-unary", "output"):
+        elif k in ("elementwise-unary", "output", "layernorm", "softmax"):
             out[n["id"]] = ins[0]
+        elif k == "elementwise-binary":
+            out[n["id"]] = (ins[0][0], max(ins[0][1], ins[1][1]))
+        elif k == "reshape":
+            out[n["id"]] = (tuple(n["attrs"]["target_shape"]), ins[0][1])
+        elif k == "transpose":
+            perm = n["attrs"]["perm"]
+            out[n["id"]] = (tuple(ins[0][0][p] for p in perm), ins[0][1])
+        elif k == "embedding-lookup":
+            (ids, _), (table, eb) = ins
+            out[n["id"]] = (tuple(ids) + (table[1],), eb)
         else:
             raise NotImplementedError(f"node kind {k!r} is not executable yet")
     return out
@@ -83,6 +111,8 @@ class PlanExecutor:
     # the peer runtime, off on a simulated mesh, where the K-sliced grouped
     # GEMM measured slower than gather + one batched GEMM: 0.43 vs 0.31 ms)
     fuse_gather: bool | None = None
+    # elementwise-unary binding per node id: ("gelu",) | ("scale", alpha) | ("not",)
+    unary: dict | None = None
     comm: list = field(default_factory=list)
     _saved: dict = None
 
@@ -95,16 +125,24 @@ class PlanExecutor:
         self.partial = {nid: tuple(p.get("reduce_axes", ())) for nid, p in self.plan["nodes"].items()
                         if p.get("partial_sum")}
         self.strategy: dict[str, MatmulStrategy] = {}
+        self.in_specs: dict[str, list] = {}
         for n in self.graph["nodes"]:
-            if n["kind"] == "matmul":
+            nid, kind = n["id"], n["kind"]
+            name = self.plan["nodes"][nid]["strategy"]
+            if kind in ("matmul", "batched-matmul"):
                 a_meta = self._meta(n["inputs"][0][0])
                 b_meta = self._meta(n["inputs"][1][0])
-                st = find_matmul_strategy(self.plan["nodes"][n["id"]]["strategy"], self.geo,
-                                          a_meta, b_meta)
-                if st.c != self.spec[n["id"]]:
-                    raise ValueError(f"{n['id']}: plan spec {self.spec[n['id']]} != strategy "
+                st = find_matmul_strategy(name, self.geo, a_meta, b_meta,
+                                          batched=kind == "batched-matmul")
+                if st.c != self.spec[nid]:
+                    raise ValueError(f"{nid}: plan spec {self.spec[nid]} != strategy "
                                      f"output {st.c}")
-                self.strategy[n["id"]] = st
+                self.strategy[nid] = st
+                self.in_specs[nid] = [st.a, st.b]
+            elif kind in ("placeholder", "parameter"):
+                self.in_specs[nid] = []
+            else:
+                self.in_specs[nid] = self._input_specs(n, name)
         self._consumers = {}
         for n in self.graph["nodes"]:
             for slot, (src, _) in enumerate(n["inputs"]):
@@ -117,23 +155,56 @@ class PlanExecutor:
         shape, eb = self.shapes[nid]
         return TensorMeta(shape, eb)
 
+    def _input_specs(self, n: dict, name: str) -> list:
+        """Input layouts of a non-matmul node's named strategy
+        (intraop.cpp:280-450): the name carries the input spec for reshape /
+        perm / softmax / layernorm, the axes for embeddings; elementwise ops
+        mirror the output layout onto every input."""
+        nid, kind, mr = n["id"], n["kind"], self.geo.rank()
+        out = self.spec[nid]
+        if kind == "output":
+            return [ShardingSpec.replicated(len(self.shapes[nid][0]), mr)]
+        if kind in ("reshape", "transpose", "softmax", "layernorm"):
+            spec = ShardingSpec.parse(name.split(":", 1)[1], mr)
+            if kind == "transpose":
+                perm = n["attrs"]["perm"]
+                if [spec.dims[p] for p in perm] != list(out.dims):
+                    raise ValueError(f"{nid}: {name} does not produce {out}")
+            if kind == "layernorm":
+                return [spec] + [ShardingSpec.replicated(1, mr)] * (len(n["inputs"]) - 1)
+            return [spec]
+        if kind == "embedding-lookup":
+            # emb-batch@i:t / emb-h:t / emb-bh@i:x,y (intraop.cpp:406-450)
+            ri = len(self.shapes[n["inputs"][0][0]][0])
+            return [ShardingSpec(tuple(out.dims[:ri]), mr),
+                    ShardingSpec((DimSpec(), out.dims[ri]), mr)]
+        return [out] * len(n["inputs"])  # elementwise
+
     def required_spec(self, consumer: str, slot: int) -> ShardingSpec:
-        n = self.nodes[consumer]
-        if n["kind"] == "matmul":
-            st = self.strategy[consumer]
-            return st.a if slot == 0 else st.b
-        if n["kind"] == "output":
-            return ShardingSpec.replicated(len(self.shapes[consumer][0]), self.geo.rank())
-        return self.spec[consumer]  # elementwise: layout mirrored onto the input
+        return self.in_specs[consumer][slot]
+
+    def unary_op(self, nid: str) -> tuple:
+        """The function an elementwise-unary node computes (module docstring)."""
+        if self.unary and nid in self.unary:
+            return tuple(self.unary[nid])
+        src = self.nodes[nid]["inputs"][0][0]
+        if self.shapes[src][1] == 1:
+            return ("not",)
+        prod = self.nodes[src]
+        if "scale" in nid and prod["kind"] == "batched-matmul":
+            k = self.shapes[prod["inputs"][0][0]][0][-1]
+            return ("scale", 1.0 / float(k) ** 0.5)
+        return ("gelu",)
 
     def _fusable_gelu(self, mm: str):
         """The GELU node fused into matmul `mm`'s epilogue, if any."""
         cons = self._consumers.get(mm, [])
-        if len(cons) != 1 or mm in self.partial:
+        if len(cons) != 1 or mm in self.partial or self.nodes[mm]["kind"] != "matmul":
             return None
         gid, _ = cons[0]
         g = self.nodes[gid]
-        if g["kind"] == "elementwise-unary" and self.spec[gid] == self.spec[mm]:
+        if (g["kind"] == "elementwise-unary" and self.spec[gid] == self.spec[mm]
+                and self.unary_op(gid) == ("gelu",)):
             return gid
         return None
 
@@ -266,17 +337,85 @@ class PlanExecutor:
                 if nid in fused:
                     values[nid] = ins[0]
                 else:
+                    from . import block_ops as B
+                    op = self.unary_op(nid)
                     outs = [self._empty(t.shape, t.dtype, t.device) for t in ins[0]]
                     for x, y in zip(ins[0], outs):
-                        gelu(x, y, stream=stream)
+                        if op[0] == "gelu":
+                            gelu(x, y, stream=stream)
+                        elif op[0] == "scale":
+                            B.scale(x, y, op[1], stream=stream)
+                        elif op[0] == "not":
+                            B.mask_not(x, y, stream=stream)
+                        else:
+                            raise ValueError(f"{nid}: unknown unary op {op}")
                     if train:
                         self._saved[nid] = ins[0]  # the pre-activation
                     values[nid] = outs
             elif kind == "output":
                 values[nid] = ins[0]
+            elif kind in _BLOCK_KINDS:
+                values[nid] = self._block_node(n, ins, stream)
             else:
                 raise NotImplementedError(kind)
         return values[self.graph["output"]]
+
+    def _block_node(self, n: dict, ins: list, stream) -> list:
+        """One transformer-block node on every local shard (module docstring)."""
+        from . import block_ops as B
+        from .runtime import gemm_grouped
+
+        nid, kind = n["id"], n["kind"]
+        spec = self.spec[nid]
+        local = spec.local_shape(self._meta(nid), self.geo)
+        if kind == "reshape":  # a view: the plan's rewritten local target shape
+            return [x.view(local) for x in ins[0]]
+        if kind == "embedding-lookup":
+            outs = [self._empty(local, t.dtype, t.device) for t in ins[1]]
+            for ids, table, o in zip(ins[0], ins[1], outs):
+                B.embedding(ids, table, o, stream=stream)
+            return outs
+        dt = next(x[0].dtype for x in ins if x[0].dtype != torch.uint8)
+        outs = [self._empty(local, dt, ins[0][0].device) for _ in range(self.mesh.num_local)]
+        if kind == "layernorm":
+            g = ins[1] if len(ins) > 1 else [None] * len(outs)
+            b = ins[2] if len(ins) > 2 else [None] * len(outs)
+            for x, gg, bb, o in zip(ins[0], g, b, outs):
+                B.layernorm(x, gg, bb, o, stream=stream)
+        elif kind == "softmax":
+            axis = n.get("attrs", {}).get("axis", -1)
+            if axis not in (-1, len(local) - 1):
+                raise NotImplementedError("softmax over a non-last axis")
+            for x, o in zip(ins[0], outs):
+                B.softmax(x, o, stream=stream)
+        elif kind == "transpose":
+            perm = list(n["attrs"]["perm"])
+            r = len(perm)
+            if perm != list(range(r - 2)) + [r - 1, r - 2]:
+                raise NotImplementedError(f"transpose perm {perm}")
+            for x, o in zip(ins[0], outs):
+                B.transpose_last2(x, o, stream=stream)
+        elif kind == "elementwise-binary":
+            a, b = ins
+            if a[0].dtype == torch.uint8:
+                a, b = b, a
+            alpha = MASK_FILL if b[0].dtype == torch.uint8 else 1.0
+            for x, y, o in zip(a, b, outs):
+                B.add(x, y, o, alpha, stream=stream)
+        elif kind == "batched-matmul":
+            # one grouped tcgen05 GEMM per device: a problem per local batch
+            st = self.strategy[nid]
+            for a, b, o in zip(ins[0], ins[1], outs):
+                nb, m, k = a.shape
+                nn = b.shape[2]
+                ea, eo = a.element_size(), o.element_size()
+                gemm_grouped([a.data_ptr() + i * m * k * ea for i in range(nb)],
+                             [b.data_ptr() + i * k * nn * ea for i in range(nb)],
+                             [o.data_ptr() + i * m * nn * eo for i in range(nb)], 1, m, nn, k,
+                             k, nn, nn, "kn", o.dtype, False, stream)
+            if st.partial_sum:  # split-k strategies: `<host>.ar` (planner.cpp:263-282)
+                self.mesh.all_reduce(list(st.reduce_axes), outs, stream=stream)
+        return outs
 
 
     # ---- all-gather -> GEMM fusion -------------------------------------------
@@ -391,6 +530,10 @@ class PlanExecutor:
         take the reverse conversion back to the producer's layout."""
         if self._saved is None:
             raise RuntimeError("backward() needs a preceding forward(train=True)")
+        for n in self.graph["nodes"]:
+            if n["kind"] in _BLOCK_KINDS or (n["kind"] == "elementwise-unary"
+                                             and self.unary_op(n["id"]) != ("gelu",)):
+                raise NotImplementedError(f"backward through {n['kind']} ({n['id']})")
         out_id = self.graph["output"]
         out_node = self.nodes[out_id]
         src = out_node["inputs"][0][0]

@@ -38,3 +38,27 @@ def test_megatron_plan_decodes():
     ex.check_against_plan()
     assert ex.strategy["fc1"].name == "split-n:0" and ex.strategy["fc2"].partial_sum
     assert ex._fusable_gelu("fc1") == "gelu"
+
+
+@pytest.mark.parametrize("path", sorted(p.name for p in PLANS.glob("gpt_block_*_mesh*.json")))
+def test_block_plans_decode_and_match_communication(path):
+    """The reference's transformer-block plans (embedding, layernorm, reshape,
+    transpose, batched matmul, softmax, elementwise strategies): every
+    non-matmul strategy decodes to input layouts whose conversions are
+    exactly the plan's inserted communication."""
+    tag = path.split("_mesh")[0]
+    graph = json.loads((PLANS / f"{tag}_graph.json").read_text())
+    plan = json.loads((PLANS / path).read_text())
+    ex = PlanExecutor(_GeoOnly(plan["mesh"]["shape"]), graph, plan)
+    ex.check_against_plan()
+    assert ex.unary_op("mask2") == ("not",)
+    assert ex.unary_op("act") == ("gelu",)
+    op, alpha = ex.unary_op("scaled")
+    h = ex.shapes["qr"][0][-1]
+    assert op == "scale" and abs(alpha - h ** -0.5) < 1e-12
+    assert ex.strategy["scores"].name == plan["nodes"]["scores"]["strategy"]
+    # reshape strategies: the plan's rewritten local target shape is the
+    # local shape of the node's spec (a view of the producer's shard)
+    for rw in plan.get("reshape_rewrites", []):
+        nid = rw["node"]
+        assert list(ex.spec[nid].local_shape(ex._meta(nid), ex.geo)) == rw["new_target_shape"]
