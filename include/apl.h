@@ -403,6 +403,17 @@ int apl_gelu_backward(const void* dy, const void* x, void* dx, size_t count, int
  * narrower one). Ids outside [0, vocab) give zero rows. */
 int apl_embedding_lookup(const int64_t* ids, int64_t n, const void* table, int64_t vocab,
                          int64_t width, int elem_bytes, void* out, void* stream);
+/* embedding-lookup with the table's all-gather fused in: the table
+ * [vocab, width] is given as its owners' blocks, a row-major grid of
+ * vocab_blocks x hidden_blocks (<= 64) equal contiguous blocks [vocab /
+ * vocab_blocks, width / hidden_blocks] (a simulated mesh's shards or
+ * peer-mapped shards, e.g. a vocab-sharded `src:S0R` table consumed
+ * replicated, gpt_block `wte`). out [n, cols] = table[ids, col_begin :
+ * col_begin + cols], read in place; no gathered copy of the table. */
+int apl_embedding_lookup_blocks(const int64_t* ids, int64_t n, const void* const* blocks,
+                                int vocab_blocks, int hidden_blocks, int64_t vocab, int64_t width,
+                                int64_t col_begin, int64_t cols, int elem_bytes, void* out,
+                                void* stream);
 /* layernorm over the last dim: y = (x - mean) / sqrt(var + eps) * gamma + beta
  * per row of `width`; gamma / beta may be NULL (no affine). */
 int apl_layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,

@@ -161,6 +161,9 @@ _SIGS = {
                                       C.c_uint32, C.c_void_p]),
     "apl_embedding_lookup": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
                                        C.c_int, C.c_void_p, C.c_void_p]),
+    "apl_embedding_lookup_blocks": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_void_p), C.c_int,
+                                              C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                              C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),
     "apl_layernorm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                 C.c_int64, C.c_float, C.c_int, C.c_void_p]),
     "apl_softmax": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,

@@ -30,6 +30,21 @@ def embedding(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor, stream=
                                        _stream_handle(stream)))
 
 
+def embedding_blocks(ids: torch.Tensor, block_ptrs, vocab_blocks: int, hidden_blocks: int,
+                     vocab: int, width: int, col_begin: int, out: torch.Tensor,
+                     stream=None) -> None:
+    """out = table[ids, col_begin : col_begin + out.shape[-1]] with the table
+    given as its owners' blocks (row-major [vocab_blocks x hidden_blocks]
+    device addresses): the table's all-gather fused into the lookup."""
+    if ids.dtype != torch.int64:
+        raise TypeError("ids must be int64")
+    arr = (C.c_void_p * len(block_ptrs))(*block_ptrs)
+    check(A.lib().apl_embedding_lookup_blocks(_p(ids), ids.numel(), arr, vocab_blocks,
+                                              hidden_blocks, vocab, width, col_begin,
+                                              out.shape[-1], out.element_size(), _p(out),
+                                              _stream_handle(stream)))
+
+
 def layernorm(x: torch.Tensor, gamma: torch.Tensor | None, beta: torch.Tensor | None,
               y: torch.Tensor, eps: float = 1e-5, stream=None) -> None:
     w = x.shape[-1]

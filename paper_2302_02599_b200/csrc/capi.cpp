@@ -959,6 +959,29 @@ int apl_embedding_lookup(const int64_t* ids, int64_t n, const void* table, int64
   });
 }
 
+int apl_embedding_lookup_blocks(const int64_t* ids, int64_t n, const void* const* blocks,
+                                int vocab_blocks, int hidden_blocks, int64_t vocab, int64_t width,
+                                int64_t col_begin, int64_t cols, int elem_bytes, void* out,
+                                void* stream) {
+  return guarded([&] {
+    need(n >= 0 && vocab >= 0 && width > 0 && cols >= 0, "bad extents");
+    need(vocab_blocks >= 1 && hidden_blocks >= 1 && vocab_blocks * hidden_blocks <= 64,
+         "1..64 table blocks");
+    need(vocab % vocab_blocks == 0 && width % hidden_blocks == 0,
+         "blocks must split the table evenly");
+    need(col_begin >= 0 && col_begin + cols <= width, "column slice outside the table");
+    need((ids && blocks && out) || n == 0 || cols == 0, "null buffer");
+    for (int i = 0; blocks && i < vocab_blocks * hidden_blocks; ++i)
+      need(blocks[i] != nullptr, "null table block");
+    need(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8,
+         "elem_bytes must be 1, 2, 4 or 8");
+    apl::check_cuda(apl::launch_embedding_blocks(ids, n, blocks, vocab_blocks, hidden_blocks,
+                                                 vocab, width, col_begin, cols, elem_bytes, out,
+                                                 static_cast<cudaStream_t>(stream)),
+                    "embedding launch");
+  });
+}
+
 int apl_layernorm(const void* x, const void* gamma, const void* beta, void* y, int64_t rows,
                   int64_t width, float eps, int dtype, void* stream) {
   return guarded([&] {

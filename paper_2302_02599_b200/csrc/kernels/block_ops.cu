@@ -8,9 +8,11 @@
 // their inputs first.
 //
 // All HBM-bound; fp32 math, bf16 / f32 / u8 storage:
-//   embedding  : rows of the table gathered per id       (width x eb read + written per id)
-//   layernorm  : warp per row, mean / var / affine        (row read 3x from L1, written once)
-//   softmax    : warp per row, online max + sum, write    (row read 2x, written once)
+//   embedding  : rows of the table gathered per id       (width x eb read + written per id);
+//                from a sharded table's owner blocks directly (all-gather fused)
+//   layernorm  : warp per row, mean / var / affine        (row read once into registers
+//   softmax    : warp per row, max, exp-sum, normalise     up to 256 x 16 B, else streamed
+//                                                          from L1 in 3 / 2 passes; written once)
 //   transpose  : [batch, R, C] -> [batch, C, R], 32 x 32 shared-memory tiles
 //   scale / add / not : 16-byte vectors, grid-stride
 #include <cuda_bf16.h>
@@ -78,6 +80,39 @@ __global__ void __launch_bounds__(256) embedding_kernel(const int64_t* __restric
     const int64_t id = __ldg(ids + t);
     W v{};
     if (id >= 0 && id < vocab) v = table[id * words + w];
+    out[i] = v;
+  }
+}
+
+// ---- embedding lookup from a sharded table, all-gather fused ----------------
+// The table is a grid of [vocab_blocks x hidden_blocks] equal blocks, each
+// contiguous [vb_rows, hb_words] in its owner's buffer (a simulated mesh's
+// shard, or a peer-mapped shard); out[t, :] = table[ids[t], col0 : col0 +
+// out_words] read straight from the owners: the gather of the whole table
+// every device would otherwise materialise is never written.
+constexpr int kMaxBlocks = 64;
+struct TableBlocks {
+  const void* p[kMaxBlocks];
+};
+
+template <typename W>
+__global__ void __launch_bounds__(256) embedding_blocks_kernel(
+    const int64_t* __restrict__ ids, int64_t n, const __grid_constant__ TableBlocks blocks,
+    int hidden_blocks, int64_t vb_rows, int64_t hb_words, int64_t vocab, int64_t col0,
+    int64_t out_words, W* __restrict__ out) {
+  const int64_t total = n * out_words;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += stride) {
+    const int64_t t = i / out_words, w = i - t * out_words;
+    const int64_t id = __ldg(ids + t);
+    W v{};
+    if (id >= 0 && id < vocab) {
+      const int64_t col = col0 + w;
+      const int64_t vb = id / vb_rows, hb = col / hb_words;
+      const W* blk = static_cast<const W*>(blocks.p[vb * hidden_blocks + hb]);
+      v = blk[(id - vb * vb_rows) * hb_words + (col - hb * hb_words)];
+    }
     out[i] = v;
   }
 }
@@ -187,6 +222,101 @@ __global__ void __launch_bounds__(256) transpose_kernel(const W* __restrict__ x,
   }
 }
 
+// ---- row-cached variants: rows of up to 32 x NV x V elements are loaded once
+// into registers (every load of the row in flight together), then reduced and
+// written -- one HBM round trip of latency per row instead of three.
+template <typename T, int V, int NV>
+__global__ void __launch_bounds__(256) layernorm_cached_kernel(
+    const T* __restrict__ x, const T* __restrict__ gamma, const T* __restrict__ beta,
+    T* __restrict__ y, int64_t rows, int64_t width, float eps) {
+  const int lane = threadIdx.x % 32;
+  const int nv = static_cast<int>(width / V);
+  const float inv_w = 1.f / static_cast<float>(width);
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const T* xr = x + r * width;
+    float c[NV][V];
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        load_row<T, V>(xr, i, c[j]);
+#pragma unroll
+        for (int k = 0; k < V; ++k) s += c[j][k];
+      }
+    }
+    const float mean = warp_sum(s) * inv_w;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv)
+#pragma unroll
+        for (int k = 0; k < V; ++k) q += (c[j][k] - mean) * (c[j][k] - mean);
+    const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        float g[V], b[V];
+        if (gamma != nullptr) load_row<T, V>(gamma, i, g);
+        if (beta != nullptr) load_row<T, V>(beta, i, b);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          float v = (c[j][k] - mean) * rstd;
+          if (gamma != nullptr) v *= g[k];
+          if (beta != nullptr) v += b[k];
+          c[j][k] = v;
+        }
+        store_row<T, V>(y + r * width, i, c[j]);
+      }
+    }
+  }
+}
+
+template <typename T, int V, int NV>
+__global__ void __launch_bounds__(256) softmax_cached_kernel(const T* __restrict__ x,
+                                                             T* __restrict__ y, int64_t rows,
+                                                             int64_t width) {
+  const int lane = threadIdx.x % 32;
+  const int nv = static_cast<int>(width / V);
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const T* xr = x + r * width;
+    float c[NV][V];
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        load_row<T, V>(xr, i, c[j]);
+#pragma unroll
+        for (int k = 0; k < V; ++k) m = fmaxf(m, c[j][k]);
+      }
+    }
+    m = warp_max(m);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv)
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          c[j][k] = __expf(c[j][k] - m);
+          s += c[j][k];
+        }
+    const float inv = 1.f / warp_sum(s);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) c[j][k] *= inv;
+        store_row<T, V>(y + r * width, i, c[j]);
+      }
+    }
+  }
+}
+
 // ---- elementwise ----------------------------------------------------------
 // y = alpha * x
 template <typename T, int V>
@@ -240,6 +370,13 @@ cudaError_t done() {
   return cudaGetLastError();
 }
 
+template <typename T, int V, int NV>
+void rowwise_cached(bool softmax, const T* X, const T* G, const T* B, T* Y, int64_t rows,
+                    int64_t width, float eps, int grid, cudaStream_t s) {
+  if (softmax) softmax_cached_kernel<T, V, NV><<<grid, 256, 0, s>>>(X, Y, rows, width);
+  else layernorm_cached_kernel<T, V, NV><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);
+}
+
 template <typename T>
 cudaError_t rowwise(bool softmax, const void* x, const void* g, const void* b, void* y,
                     int64_t rows, int64_t width, float eps, cudaStream_t s) {
@@ -249,12 +386,20 @@ cudaError_t rowwise(bool softmax, const void* x, const void* g, const void* b, v
   const int grid = grid_for(rows * 32);
   auto X = static_cast<const T*>(x);
   auto Y = static_cast<T*>(y);
+  auto G = static_cast<const T*>(g);
+  auto B = static_cast<const T*>(b);
+  const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;  // vectors each lane holds
+  if (per_lane >= 1 && per_lane <= 8) {
+    if (per_lane == 1) rowwise_cached<T, V, 1>(softmax, X, G, B, Y, rows, width, eps, grid, s);
+    else if (per_lane == 2) rowwise_cached<T, V, 2>(softmax, X, G, B, Y, rows, width, eps, grid, s);
+    else if (per_lane <= 4) rowwise_cached<T, V, 4>(softmax, X, G, B, Y, rows, width, eps, grid, s);
+    else rowwise_cached<T, V, 8>(softmax, X, G, B, Y, rows, width, eps, grid, s);
+    return done();
+  }
   if (softmax) {
     if (vec) softmax_kernel<T, V><<<grid, 256, 0, s>>>(X, Y, rows, width);
     else softmax_kernel<T, 1><<<grid, 256, 0, s>>>(X, Y, rows, width);
   } else {
-    auto G = static_cast<const T*>(g);
-    auto B = static_cast<const T*>(b);
     if (vec) layernorm_kernel<T, V><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);
     else layernorm_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);
   }
@@ -312,6 +457,55 @@ cudaError_t launch_embedding(const int64_t* ids, int64_t n, const void* table, i
   else
     embedding_kernel<uint8_t><<<grid_for(n * row), 256, 0, s>>>(
         ids, n, static_cast<const uint8_t*>(table), vocab, row, static_cast<uint8_t*>(out));
+  return done();
+}
+
+cudaError_t launch_embedding_blocks(const int64_t* ids, int64_t n, const void* const* blocks,
+                                    int vocab_blocks, int hidden_blocks, int64_t vocab,
+                                    int64_t width, int64_t col_begin, int64_t cols,
+                                    int elem_bytes, void* out, cudaStream_t s) {
+  if (n == 0 || cols == 0) return cudaSuccess;
+  if (vocab_blocks < 1 || hidden_blocks < 1 || vocab_blocks * hidden_blocks > kMaxBlocks ||
+      vocab % vocab_blocks || width % hidden_blocks)
+    return cudaErrorInvalidValue;
+  TableBlocks tb{};
+  uintptr_t align = reinterpret_cast<uintptr_t>(out);
+  for (int i = 0; i < vocab_blocks * hidden_blocks; ++i) {
+    tb.p[i] = blocks[i];
+    align |= reinterpret_cast<uintptr_t>(blocks[i]);
+  }
+  const int64_t vb_rows = vocab / vocab_blocks;
+  const int64_t hb = width / hidden_blocks * elem_bytes, c0 = col_begin * elem_bytes,
+                nc = cols * elem_bytes;
+  // the widest word every block row, the output slice and all bases divide
+  int wb = 16;
+  while (wb > 1 && ((hb | c0 | nc) % wb || align % wb)) wb >>= 1;
+  switch (wb) {
+    case 16:
+      embedding_blocks_kernel<uint4><<<grid_for(n * nc / 16), 256, 0, s>>>(
+          ids, n, tb, hidden_blocks, vb_rows, hb / 16, vocab, c0 / 16, nc / 16,
+          static_cast<uint4*>(out));
+      break;
+    case 8:
+      embedding_blocks_kernel<uint2><<<grid_for(n * nc / 8), 256, 0, s>>>(
+          ids, n, tb, hidden_blocks, vb_rows, hb / 8, vocab, c0 / 8, nc / 8,
+          static_cast<uint2*>(out));
+      break;
+    case 4:
+      embedding_blocks_kernel<uint32_t><<<grid_for(n * nc / 4), 256, 0, s>>>(
+          ids, n, tb, hidden_blocks, vb_rows, hb / 4, vocab, c0 / 4, nc / 4,
+          static_cast<uint32_t*>(out));
+      break;
+    case 2:
+      embedding_blocks_kernel<uint16_t><<<grid_for(n * nc / 2), 256, 0, s>>>(
+          ids, n, tb, hidden_blocks, vb_rows, hb / 2, vocab, c0 / 2, nc / 2,
+          static_cast<uint16_t*>(out));
+      break;
+    default:
+      embedding_blocks_kernel<uint8_t><<<grid_for(n * nc), 256, 0, s>>>(
+          ids, n, tb, hidden_blocks, vb_rows, hb, vocab, c0, nc, static_cast<uint8_t*>(out));
+      break;
+  }
   return done();
 }
 

@@ -59,6 +59,10 @@ cudaError_t launch_gelu_backward(const void* dy, const void* x, void* dx, size_t
 // Transformer-block node kinds on one shard (block_ops.cu).
 cudaError_t launch_embedding(const int64_t* ids, int64_t n, const void* table, int64_t vocab,
                              int64_t width, int elem_bytes, void* out, cudaStream_t s);
+cudaError_t launch_embedding_blocks(const int64_t* ids, int64_t n, const void* const* blocks,
+                                    int vocab_blocks, int hidden_blocks, int64_t vocab,
+                                    int64_t width, int64_t col_begin, int64_t cols,
+                                    int elem_bytes, void* out, cudaStream_t s);
 cudaError_t launch_layernorm(const void* x, const void* gamma, const void* beta, void* y,
                              int64_t rows, int64_t width, float eps, int dtype, cudaStream_t s);
 cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype,

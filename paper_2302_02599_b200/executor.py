@@ -301,7 +301,8 @@ class PlanExecutor:
                 values[nid] = v if isinstance(v, list) else self.shard(nid, v)
                 continue
             ins = []
-            gather_b = kind == "matmul" and not train and self._gatherable_b(nid)
+            gather_b = ((kind == "matmul" and not train and self._gatherable_b(nid))
+                        or (kind == "embedding-lookup" and self._gatherable_table(nid)))
             for slot, (src, _) in enumerate(n["inputs"]):
                 have, want = self.spec[src], self.required_spec(nid, slot)
                 if have == want or (slot == 1 and gather_b):
@@ -354,6 +355,8 @@ class PlanExecutor:
                     values[nid] = outs
             elif kind == "output":
                 values[nid] = ins[0]
+            elif kind == "embedding-lookup" and gather_b:
+                values[nid] = self._lookup_gathered_table(nid, ins[0], ins[1], stream)
             elif kind in _BLOCK_KINDS:
                 values[nid] = self._block_node(n, ins, stream)
             else:
@@ -488,6 +491,76 @@ class PlanExecutor:
                      stream)
         if peer:
             self.mesh.gather_end(stream)
+
+    # ---- all-gather -> embedding lookup fusion -------------------------------
+    def _block_owner(self, spec: ShardingSpec, index: tuple) -> int:
+        """A device holding block `index` of `spec` (mixed radix over each
+        dim's axes, first axis most significant -- the shard() layout)."""
+        shape = self.geo.shape
+        coord = [0] * self.geo.rank()
+        for dim, v in zip(spec.dims, index):
+            for a in reversed(dim.axes):
+                coord[a] = v % shape[a]
+                v //= shape[a]
+        return self.geo.device_of(coord)
+
+    def _block_index(self, dim, device: int) -> tuple:
+        """(index, count) of `device`'s block along a dim sharded over dim.axes."""
+        coord = self.geo.coord_of(device)
+        idx, cnt = 0, 1
+        for a in dim.axes:
+            idx = idx * self.geo.shape[a] + coord[a]
+            cnt *= self.geo.shape[a]
+        return idx, cnt
+
+    def _gatherable_table(self, nid: str) -> bool:
+        """An embedding whose table is stored sharded (`src:S0R` / `S0S1`
+        parameters of the reference's block plans) and consumed with more of
+        it replicated: the lookup reads each id's row from the device owning
+        that block -- the table's all-gather fused into the lookup, no
+        gathered copy of a [vocab, hidden] table per device. On by default
+        (fuse_gather=False disables it)."""
+        if self.fuse_gather is False:
+            return False
+        if self.mesh.distributed and not hasattr(self.mesh, "gather_begin"):
+            return False
+        src = self.nodes[nid]["inputs"][1][0]
+        have, want = self.spec[src], self.required_spec(nid, 1)
+        if have == want:
+            return False
+        nb = 1
+        for d in have.dims:
+            for a in d.axes:
+                nb *= self.geo.shape[a]
+        return nb <= 64
+
+    def _lookup_gathered_table(self, nid, ids, table, stream):
+        from . import block_ops as B
+
+        src = self.nodes[nid]["inputs"][1][0]
+        have, want = self.spec[src], self.required_spec(nid, 1)
+        (vocab, width), _ = self.shapes[src]
+        nvb = self._block_index(have.dims[0], 0)[1]
+        nhb = self._block_index(have.dims[1], 0)[1]
+        peer = self.mesh.distributed
+        if peer:  # publish this rank's block; read the owners' over peer memory
+            staged = self.mesh.gather_begin(table[0], stream)
+            ptr = lambda d: self.mesh.peer_ptr(staged, d)  # noqa: E731
+        else:
+            ptr = lambda d: table[d].data_ptr()  # noqa: E731
+        blocks = [ptr(self._block_owner(have, (i, j))) for i in range(nvb) for j in range(nhb)]
+        local = self.spec[nid].local_shape(self._meta(nid), self.geo)
+        devs = [self.mesh.first_local] if peer else range(self.mesh.num_local)
+        outs = []
+        for d, x in zip(devs, ids):
+            j, nw = self._block_index(want.dims[1], d)
+            o = self._empty(local, table[0].dtype, table[0].device)
+            B.embedding_blocks(x, blocks, nvb, nhb, vocab, width, j * (width // nw), o,
+                               stream=stream)
+            outs.append(o)
+        if peer:
+            self.mesh.gather_end(stream)
+        return outs
 
     # ---- backward (SURVEY 8f #2) ---------------------------------------------
     def _convert_grad(self, nid, shards, have, want, stream):

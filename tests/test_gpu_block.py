@@ -85,6 +85,24 @@ def test_embedding_rows_bit_exact(cuda, n, width, eb):
     assert (out[1] == 0).all()
 
 
+@pytest.mark.parametrize("vb,hb,eb,width", [(8, 1, 2, 1024), (2, 4, 2, 1024), (4, 2, 4, 24),
+                                             (2, 2, 2, 6), (1, 8, 1, 40)])
+def test_embedding_from_owner_blocks(cuda, vb, hb, eb, width):
+    """All-gather fused into the lookup: rows read from the owners' blocks
+    give exactly the rows of the gathered table, for any column slice."""
+    dt = {1: torch.uint8, 2: torch.bfloat16, 4: torch.float32}[eb]
+    vocab, n = 96 * vb, 777
+    table = torch.randint(0, 255, (vocab, width), device="cuda", dtype=torch.uint8).to(dt)
+    blocks = [table[i * (vocab // vb):(i + 1) * (vocab // vb),
+                    j * (width // hb):(j + 1) * (width // hb)].contiguous()
+              for i in range(vb) for j in range(hb)]
+    ids = torch.randint(0, vocab, (n,), device="cuda", dtype=torch.int64)
+    for c0, cols in ((0, width), (width // 2, width // 2), (width - width // hb, width // hb)):
+        out = torch.empty(n, cols, dtype=dt, device="cuda")
+        B.embedding_blocks(ids, [b.data_ptr() for b in blocks], vb, hb, vocab, width, c0, out)
+        assert torch.equal(out, table[ids, c0:c0 + cols])
+
+
 @pytest.mark.parametrize("shape", [(8, 1024, 1024), (3, 33, 65), (1, 7, 1), (2, 64, 16)])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.uint8, torch.int64])
 def test_transpose_bit_exact(cuda, shape, dtype):
@@ -177,7 +195,8 @@ def test_block_plans_execute(cuda, name, fuse):
     graph, feeds, ref = _case(name.split("_mesh")[0].removeprefix("gpt_block_"))
     plan = json.loads((PLANS / name).read_text())
     mesh = Mesh.local(plan["mesh"]["shape"])
-    ex = PlanExecutor(mesh, graph, plan, fuse=fuse)
+    # fuse=False also runs the table all-gather unfused (gather, then lookup)
+    ex = PlanExecutor(mesh, graph, plan, fuse=fuse, fuse_gather=None if fuse else False)
     ex.check_against_plan()
     before = launch_count()
     outs = ex.forward(feeds)
