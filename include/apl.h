@@ -420,6 +420,12 @@ int apl_layernorm(const void* x, const void* gamma, const void* beta, void* y, i
                   int64_t width, float eps, int dtype, void* stream);
 /* softmax over the last dim (rows of `width`). */
 int apl_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype, void* stream);
+/* softmax(alpha * x + fill * mask) over the last dim: the attention
+ * scale -> additive-mask -> softmax chain of the block graph (scaled, att_in,
+ * att) in one pass when the plan keeps the three in one layout. mask: u8
+ * [rows, width] or NULL. */
+int apl_softmax_ex(const void* x, void* y, int64_t rows, int64_t width, float alpha,
+                   const void* mask, float fill, int dtype, void* stream);
 /* transpose perm [0, 2, 1]: x [batch, rows, cols] -> y [batch, cols, rows]. */
 int apl_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                   int elem_bytes, void* stream);

@@ -168,6 +168,8 @@ _SIGS = {
                                 C.c_int64, C.c_float, C.c_int, C.c_void_p]),
     "apl_softmax": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                               C.c_void_p]),
+    "apl_softmax_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_float,
+                                 C.c_void_p, C.c_float, C.c_int, C.c_void_p]),
     "apl_transpose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                 C.c_void_p]),
     "apl_scale": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_float, C.c_int, C.c_void_p]),

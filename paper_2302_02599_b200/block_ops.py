@@ -59,6 +59,16 @@ def softmax(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
                               _stream_handle(stream)))
 
 
+def masked_softmax(x: torch.Tensor, y: torch.Tensor, alpha: float = 1.0,
+                   mask: torch.Tensor | None = None, fill: float = 0.0, stream=None) -> None:
+    """y = softmax(alpha * x + fill * mask) over the last dim, one pass."""
+    if mask is not None and (mask.dtype != torch.uint8 or mask.numel() != x.numel()):
+        raise TypeError("mask must be uint8 of x's size")
+    w = x.shape[-1]
+    check(A.lib().apl_softmax_ex(_p(x), _p(y), x.numel() // w, w, alpha, _p(mask), fill,
+                                 _DTYPE_CODE[x.dtype], _stream_handle(stream)))
+
+
 def transpose_last2(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
     """y = x with its last two dims swapped (perm [..., -1, -2])."""
     r, c = x.shape[-2], x.shape[-1]

@@ -994,15 +994,20 @@ int apl_layernorm(const void* x, const void* gamma, const void* beta, void* y, i
   });
 }
 
-int apl_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype, void* stream) {
+int apl_softmax_ex(const void* x, void* y, int64_t rows, int64_t width, float alpha,
+                   const void* mask, float fill, int dtype, void* stream) {
   return guarded([&] {
     need(rows >= 0 && width > 0, "bad extents");
     need((x && y) || rows == 0, "null buffer");
     need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
-    apl::check_cuda(
-        apl::launch_softmax(x, y, rows, width, dtype, static_cast<cudaStream_t>(stream)),
-        "softmax launch");
+    apl::check_cuda(apl::launch_softmax(x, y, rows, width, alpha, mask, fill, dtype,
+                                        static_cast<cudaStream_t>(stream)),
+                    "softmax launch");
   });
+}
+
+int apl_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype, void* stream) {
+  return apl_softmax_ex(x, y, rows, width, 1.f, nullptr, 0.f, dtype, stream);
 }
 
 int apl_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,

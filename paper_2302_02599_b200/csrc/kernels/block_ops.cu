@@ -165,19 +165,38 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x,
 }
 
 // ---- softmax over the last dim ------------------------------------------
+// Attention pre-op fused in: softmax(alpha * x + fill * mask), mask a u8
+// [rows, width] (or null); alpha = 1 / null mask is the plain softmax.
+template <int V>
+__device__ __forceinline__ void pre_op(float (&f)[V], const uint8_t* mrow, int64_t i, float alpha,
+                                       float fill) {
+  if (mrow != nullptr) {
+    const Vec<uint8_t, V> m = reinterpret_cast<const Vec<uint8_t, V>*>(mrow)[i];
+#pragma unroll
+    for (int k = 0; k < V; ++k) f[k] = alpha * f[k] + fill * static_cast<float>(m.v[k]);
+  } else if (alpha != 1.f) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) f[k] *= alpha;
+  }
+}
+
 template <typename T, int V>
 __global__ void __launch_bounds__(256) softmax_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                      int64_t rows, int64_t width) {
+                                                      int64_t rows, int64_t width, float alpha,
+                                                      const uint8_t* __restrict__ mask,
+                                                      float fill) {
   const int lane = threadIdx.x % 32;
   const int64_t nv = width / V;
   for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
     const T* xr = x + r * width;
     T* yr = y + r * width;
+    const uint8_t* mr = mask != nullptr ? mask + r * width : nullptr;
     float m = -INFINITY, s = 0.f;  // online max / sum per lane
     for (int64_t i = lane; i < nv; i += 32) {
       float f[V];
       load_row<T, V>(xr, i, f);
+      pre_op<V>(f, mr, i, alpha, fill);
       float mv = f[0];
 #pragma unroll
       for (int k = 1; k < V; ++k) mv = fmaxf(mv, f[k]);
@@ -193,6 +212,7 @@ __global__ void __launch_bounds__(256) softmax_kernel(const T* __restrict__ x, T
     for (int64_t i = lane; i < nv; i += 32) {
       float f[V];
       load_row<T, V>(xr, i, f);
+      pre_op<V>(f, mr, i, alpha, fill);
 #pragma unroll
       for (int k = 0; k < V; ++k) f[k] = __expf(f[k] - gm) * inv;
       store_row<T, V>(yr, i, f);
@@ -277,12 +297,15 @@ __global__ void __launch_bounds__(256) layernorm_cached_kernel(
 template <typename T, int V, int NV>
 __global__ void __launch_bounds__(256) softmax_cached_kernel(const T* __restrict__ x,
                                                              T* __restrict__ y, int64_t rows,
-                                                             int64_t width) {
+                                                             int64_t width, float alpha,
+                                                             const uint8_t* __restrict__ mask,
+                                                             float fill) {
   const int lane = threadIdx.x % 32;
   const int nv = static_cast<int>(width / V);
   for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
     const T* xr = x + r * width;
+    const uint8_t* mr = mask != nullptr ? mask + r * width : nullptr;
     float c[NV][V];
     float m = -INFINITY;
 #pragma unroll
@@ -290,6 +313,7 @@ __global__ void __launch_bounds__(256) softmax_cached_kernel(const T* __restrict
       const int i = lane + 32 * j;
       if (i < nv) {
         load_row<T, V>(xr, i, c[j]);
+        pre_op<V>(c[j], mr, i, alpha, fill);
 #pragma unroll
         for (int k = 0; k < V; ++k) m = fmaxf(m, c[j][k]);
       }
@@ -370,19 +394,28 @@ cudaError_t done() {
   return cudaGetLastError();
 }
 
+struct SoftmaxPre {
+  float alpha = 1.f;
+  const uint8_t* mask = nullptr;
+  float fill = 0.f;
+};
+
 template <typename T, int V, int NV>
 void rowwise_cached(bool softmax, const T* X, const T* G, const T* B, T* Y, int64_t rows,
-                    int64_t width, float eps, int grid, cudaStream_t s) {
-  if (softmax) softmax_cached_kernel<T, V, NV><<<grid, 256, 0, s>>>(X, Y, rows, width);
+                    int64_t width, float eps, const SoftmaxPre& p, int grid, cudaStream_t s) {
+  if (softmax)
+    softmax_cached_kernel<T, V, NV><<<grid, 256, 0, s>>>(X, Y, rows, width, p.alpha, p.mask,
+                                                         p.fill);
   else layernorm_cached_kernel<T, V, NV><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);
 }
 
 template <typename T>
 cudaError_t rowwise(bool softmax, const void* x, const void* g, const void* b, void* y,
-                    int64_t rows, int64_t width, float eps, cudaStream_t s) {
+                    int64_t rows, int64_t width, float eps, cudaStream_t s,
+                    const SoftmaxPre& p = SoftmaxPre{}) {
   constexpr int V = 16 / sizeof(T);
   const bool vec = width % V == 0 && aligned16(x) && aligned16(y) && (!g || aligned16(g)) &&
-                   (!b || aligned16(b));
+                   (!b || aligned16(b)) && reinterpret_cast<uintptr_t>(p.mask) % V == 0;
   const int grid = grid_for(rows * 32);
   auto X = static_cast<const T*>(x);
   auto Y = static_cast<T*>(y);
@@ -390,15 +423,15 @@ cudaError_t rowwise(bool softmax, const void* x, const void* g, const void* b, v
   auto B = static_cast<const T*>(b);
   const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;  // vectors each lane holds
   if (per_lane >= 1 && per_lane <= 8) {
-    if (per_lane == 1) rowwise_cached<T, V, 1>(softmax, X, G, B, Y, rows, width, eps, grid, s);
-    else if (per_lane == 2) rowwise_cached<T, V, 2>(softmax, X, G, B, Y, rows, width, eps, grid, s);
-    else if (per_lane <= 4) rowwise_cached<T, V, 4>(softmax, X, G, B, Y, rows, width, eps, grid, s);
-    else rowwise_cached<T, V, 8>(softmax, X, G, B, Y, rows, width, eps, grid, s);
+    if (per_lane == 1) rowwise_cached<T, V, 1>(softmax, X, G, B, Y, rows, width, eps, p, grid, s);
+    else if (per_lane == 2) rowwise_cached<T, V, 2>(softmax, X, G, B, Y, rows, width, eps, p, grid, s);
+    else if (per_lane <= 4) rowwise_cached<T, V, 4>(softmax, X, G, B, Y, rows, width, eps, p, grid, s);
+    else rowwise_cached<T, V, 8>(softmax, X, G, B, Y, rows, width, eps, p, grid, s);
     return done();
   }
   if (softmax) {
-    if (vec) softmax_kernel<T, V><<<grid, 256, 0, s>>>(X, Y, rows, width);
-    else softmax_kernel<T, 1><<<grid, 256, 0, s>>>(X, Y, rows, width);
+    if (vec) softmax_kernel<T, V><<<grid, 256, 0, s>>>(X, Y, rows, width, p.alpha, p.mask, p.fill);
+    else softmax_kernel<T, 1><<<grid, 256, 0, s>>>(X, Y, rows, width, p.alpha, p.mask, p.fill);
   } else {
     if (vec) layernorm_kernel<T, V><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);
     else layernorm_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);
@@ -517,11 +550,16 @@ cudaError_t launch_layernorm(const void* x, const void* gamma, const void* beta,
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype,
-                           cudaStream_t s) {
+cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, float alpha,
+                           const void* mask, float fill, int dtype, cudaStream_t s) {
   if (rows == 0) return cudaSuccess;
-  if (dtype == 0) return rowwise<float>(true, x, nullptr, nullptr, y, rows, width, 0.f, s);
-  if (dtype == 1) return rowwise<__nv_bfloat16>(true, x, nullptr, nullptr, y, rows, width, 0.f, s);
+  SoftmaxPre p;
+  p.alpha = alpha;
+  p.mask = static_cast<const uint8_t*>(mask);
+  p.fill = fill;
+  if (dtype == 0) return rowwise<float>(true, x, nullptr, nullptr, y, rows, width, 0.f, s, p);
+  if (dtype == 1)
+    return rowwise<__nv_bfloat16>(true, x, nullptr, nullptr, y, rows, width, 0.f, s, p);
   return cudaErrorInvalidValue;
 }
 

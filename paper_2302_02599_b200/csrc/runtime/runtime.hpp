@@ -65,8 +65,8 @@ cudaError_t launch_embedding_blocks(const int64_t* ids, int64_t n, const void* c
                                     int elem_bytes, void* out, cudaStream_t s);
 cudaError_t launch_layernorm(const void* x, const void* gamma, const void* beta, void* y,
                              int64_t rows, int64_t width, float eps, int dtype, cudaStream_t s);
-cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, int dtype,
-                           cudaStream_t s);
+cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, float alpha,
+                           const void* mask, float fill, int dtype, cudaStream_t s);
 cudaError_t launch_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                              int elem_bytes, cudaStream_t s);
 cudaError_t launch_scale(const void* x, void* y, size_t count, float alpha, int dtype,

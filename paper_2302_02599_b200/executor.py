@@ -149,6 +149,8 @@ class PlanExecutor:
                 self._consumers.setdefault(src, []).append((n["id"], slot))
         self._paths = {}
         self._convs = {}
+        self._attn = self._attention_chains()
+        self._attn_members = {m for ch in self._attn.values() for m in ch[1:3]}
 
     # ---- layout bookkeeping ------------------------------------------------
     def _meta(self, nid: str) -> TensorMeta:
@@ -195,6 +197,39 @@ class PlanExecutor:
             k = self.shapes[prod["inputs"][0][0]][0][-1]
             return ("scale", 1.0 / float(k) ** 0.5)
         return ("gelu",)
+
+    def _attention_chains(self) -> dict:
+        """softmax id -> (softmax, scale node, binary node, scores id, mask id,
+        alpha) for every `scaled -> att_in -> att` chain (scale, additive u8
+        mask, last-axis softmax) whose edges need no conversion under the
+        plan: run as one apl_softmax_ex pass instead of three kernels."""
+        out = {}
+        for n in self.graph["nodes"]:
+            if n["kind"] != "softmax" or n.get("attrs", {}).get("axis", -1) not in (
+                    -1, len(self.shapes[n["id"]][0]) - 1):
+                continue
+            sm = n["id"]
+            b = n["inputs"][0][0]
+            bn = self.nodes[b]
+            if (bn["kind"] != "elementwise-binary" or len(self._consumers.get(b, [])) != 1
+                    or self.spec[b] != self.in_specs[sm][0]):
+                continue
+            ins = [i[0] for i in bn["inputs"]]
+            mslot = [k for k, x in enumerate(ins) if self.shapes[x][1] == 1]
+            if len(mslot) != 1:
+                continue
+            u, m = ins[1 - mslot[0]], ins[mslot[0]]
+            un = self.nodes[u]
+            if (un["kind"] != "elementwise-unary" or len(self._consumers.get(u, [])) != 1
+                    or self.unary_op(u)[0] != "scale"):
+                continue
+            x = un["inputs"][0][0]
+            if not (self.spec[u] == self.in_specs[b][1 - mslot[0]]
+                    and self.spec[m] == self.in_specs[b][mslot[0]]
+                    and self.spec[x] == self.in_specs[u][0]):
+                continue
+            out[sm] = (sm, u, b, x, m, self.unary_op(u)[1])
+        return out
 
     def _fusable_gelu(self, mm: str):
         """The GELU node fused into matmul `mm`'s epilogue, if any."""
@@ -299,6 +334,16 @@ class PlanExecutor:
             if kind in ("placeholder", "parameter"):
                 v = feeds[nid]
                 values[nid] = v if isinstance(v, list) else self.shard(nid, v)
+                continue
+            if nid in self._attn_members and not train:
+                continue  # computed inside the fused softmax below
+            if nid in self._attn and not train:
+                from . import block_ops as B
+                _, _, _, x, m, alpha = self._attn[nid]
+                outs = [self._empty(t.shape, t.dtype, t.device) for t in values[x]]
+                for xs, ms, o in zip(values[x], values[m], outs):
+                    B.masked_softmax(xs, o, alpha, ms, MASK_FILL, stream=stream)
+                values[nid] = outs
                 continue
             ins = []
             gather_b = ((kind == "matmul" and not train and self._gatherable_b(nid))

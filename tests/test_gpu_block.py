@@ -65,6 +65,23 @@ def test_softmax_masked_rows(cuda):
     assert (y[m.bool()] == 0).all()
 
 
+@pytest.mark.parametrize("rows,width", [(8192, 1024), (100, 72), (9, 5)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_masked_softmax_fused(cuda, rows, width, dtype):
+    """softmax(alpha * x + fill * mask) in one pass == the three-node chain
+    computed in fp32."""
+    x = (torch.randn(rows, width, device="cuda") * 8).to(dtype)
+    m = (torch.rand(rows, width, device="cuda") < 0.4).to(torch.uint8)
+    m[:, -1] = 0
+    y = torch.empty_like(x)
+    B.masked_softmax(x, y, 0.125, m, MASK_FILL)
+    ref = torch.softmax(0.125 * x.float() + MASK_FILL * m.float(), -1)
+    assert (y.float() - ref).abs().max().item() <= (1e-2 if dtype == torch.bfloat16 else 1e-5)
+    B.masked_softmax(x, y, 0.5)
+    ref = torch.softmax(0.5 * x.float(), -1)
+    assert (y.float() - ref).abs().max().item() <= (1e-2 if dtype == torch.bfloat16 else 1e-5)
+
+
 @pytest.mark.parametrize("n,width,eb", [(8192, 1024, 2), (100, 7, 2), (33, 24, 4), (5, 3, 1)])
 def test_embedding_rows_bit_exact(cuda, n, width, eb):
     dt = {1: torch.uint8, 2: torch.bfloat16, 4: torch.float32}[eb]
@@ -221,3 +238,23 @@ def test_block_plans_agree_bytewise(cuda):
         ex = PlanExecutor(Mesh.local(plan["mesh"]["shape"]), graph, plan)
         outs.append(ex.forward(feeds)[0].clone())
     assert torch.equal(outs[0], outs[1])
+
+
+def test_attention_chain_fused(cuda):
+    """scaled -> att_in -> att runs as one masked-softmax pass when the plan
+    keeps the chain in one layout; the unfused chain (train=True forward)
+    gives the same block output within bf16 rounding."""
+    graph, feeds, ref = _case("b8s1024")
+    plan = json.loads((PLANS / "gpt_block_b8s1024_mesh8_unlimited.json").read_text())
+    ex = PlanExecutor(Mesh.local(plan["mesh"]["shape"]), graph, plan)
+    assert "att" in ex._attn
+    shards = {k: ex.shard(k, v) for k, v in feeds.items()}
+    n0 = launch_count()
+    fused = ex.forward(shards)[0].clone()
+    n1 = launch_count()
+    plain = ex.forward(shards, train=True)[0].clone()
+    n2 = launch_count()
+    torch.cuda.synchronize()
+    assert n2 - n1 > n1 - n0  # the unfused chain launches more kernels
+    assert _rel(fused, plain) <= 2e-2
+    assert _rel(fused, ref) <= 4e-2
