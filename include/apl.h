@@ -438,6 +438,29 @@ int apl_add(const void* a, const void* b, int b_mask, void* y, size_t count, flo
 /* elementwise-unary on a u8 mask: y = !x. */
 int apl_mask_not(const void* x, void* y, size_t count, void* stream);
 
+/* Backward of the block kinds (the training step of a gpt_block plan). */
+/* layernorm: dx; with dgamma / dbeta (fp32 [width], ACCUMULATED: +=) also the
+ * affine gradients, which need `stats` scratch of rows x 8 bytes. */
+int apl_layernorm_backward(const void* x, const void* gamma, const void* dy, void* dx,
+                           float* dgamma, float* dbeta, void* stats, int64_t rows, int64_t width,
+                           float eps, int dtype, void* stream);
+/* softmax (last dim) from its output y: dx = alpha * y * (dy - sum(dy * y)). */
+int apl_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows, int64_t width,
+                         float alpha, int dtype, void* stream);
+/* embedding: dtable[ids[t], :] += dy[t, :] (fp32 table gradient, accumulated). */
+int apl_embedding_backward(const int64_t* ids, int64_t n, const void* dy, float* dtable,
+                           int64_t vocab, int64_t width, int dtype, void* stream);
+
+/* Physical layout of the A operand. */
+#define APL_A_MK 0 /* A [M, K], K contiguous */
+#define APL_A_KM 1 /* A stored transposed, row-major [K, M] (an activation read as A^T) */
+/* Grouped tcgen05 GEMM with both operand layouts: C_g = A_g . B_g for
+ * `groups` equally shaped problems (batched matmul forward and backward). */
+int apl_gemm_bf16_grouped_ex(const void* const* A, const void* const* B, void* const* C,
+                             int groups, int64_t M, int64_t N, int64_t K, int64_t lda,
+                             int64_t ldb, int64_t ldc, int a_layout, int b_layout, int out_dtype,
+                             void* stream);
+
 #define APL_EPI_DGELU 2 /* backward epilogue: dA *= GELU'(aux) */
 
 /* Backward of apl_sharded_matmul for the same strategy and shards: per local

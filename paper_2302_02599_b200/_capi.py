@@ -175,6 +175,17 @@ _SIGS = {
     "apl_scale": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_float, C.c_int, C.c_void_p]),
     "apl_add": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_float,
                           C.c_int, C.c_void_p]),
+    "apl_layernorm_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                         C.c_int64, C.c_float, C.c_int, C.c_void_p]),
+    "apl_softmax_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                       C.c_float, C.c_int, C.c_void_p]),
+    "apl_embedding_backward": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                         C.c_int64, C.c_int64, C.c_int, C.c_void_p]),
+    "apl_gemm_bf16_grouped_ex": (C.c_int, [P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
+                                           C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                           C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                           C.c_void_p]),
     "apl_mask_not": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
 }
 

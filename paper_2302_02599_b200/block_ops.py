@@ -94,3 +94,56 @@ def add(a: torch.Tensor, b: torch.Tensor, y: torch.Tensor, alpha: float = 1.0,
 def mask_not(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
     """y = !x on a uint8 mask."""
     check(A.lib().apl_mask_not(_p(x), _p(y), x.numel(), _stream_handle(stream)))
+
+
+# ---- backward -----------------------------------------------------------------
+def layernorm_backward(x: torch.Tensor, gamma: torch.Tensor | None, dy: torch.Tensor,
+                       dx: torch.Tensor, dgamma: torch.Tensor | None = None,
+                       dbeta: torch.Tensor | None = None, eps: float = 1e-5,
+                       stream=None) -> None:
+    """dx of a layernorm; dgamma / dbeta (fp32) are ACCUMULATED into."""
+    w = x.shape[-1]
+    rows = x.numel() // w
+    stats = None
+    if dgamma is not None or dbeta is not None:
+        stats = torch.empty(rows * 2, dtype=torch.float32, device=x.device)
+    check(A.lib().apl_layernorm_backward(_p(x), _p(gamma), _p(dy), _p(dx), _p(dgamma),
+                                         _p(dbeta), _p(stats), rows, w, eps,
+                                         _DTYPE_CODE[x.dtype], _stream_handle(stream)))
+
+
+def softmax_backward(y: torch.Tensor, dy: torch.Tensor, dx: torch.Tensor, alpha: float = 1.0,
+                     stream=None) -> None:
+    w = y.shape[-1]
+    check(A.lib().apl_softmax_backward(_p(y), _p(dy), _p(dx), y.numel() // w, w, alpha,
+                                       _DTYPE_CODE[y.dtype], _stream_handle(stream)))
+
+
+def embedding_backward(ids: torch.Tensor, dy: torch.Tensor, dtable: torch.Tensor,
+                       stream=None) -> None:
+    """dtable[ids] += dy (dtable fp32 [vocab, width], accumulated)."""
+    if dtable.dtype != torch.float32:
+        raise TypeError("dtable must be fp32")
+    check(A.lib().apl_embedding_backward(_p(ids), ids.numel(), _p(dy), _p(dtable),
+                                         dtable.shape[0], dtable.shape[1],
+                                         _DTYPE_CODE[dy.dtype], _stream_handle(stream)))
+
+
+def bmm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, a_t: bool = False,
+        b_t: bool = False, stream=None) -> None:
+    """out[i] = op(a[i]) . op(b[i]) for every batch i on the tcgen05 tensor
+    cores (one grouped launch); op = transpose when a_t / b_t. bf16 in, fp32
+    accumulate, out bf16 or fp32."""
+    nb = a.shape[0]
+    M = a.shape[2] if a_t else a.shape[1]
+    K = a.shape[1] if a_t else a.shape[2]
+    N = b.shape[1] if b_t else b.shape[2]
+    ea, eb, eo = a.element_size(), b.element_size(), out.element_size()
+    P = C.c_void_p
+    arr = lambda xs: (P * len(xs))(*xs)  # noqa: E731
+    check(A.lib().apl_gemm_bf16_grouped_ex(
+        arr([a.data_ptr() + i * a[0].numel() * ea for i in range(nb)]),
+        arr([b.data_ptr() + i * b[0].numel() * eb for i in range(nb)]),
+        arr([out.data_ptr() + i * M * N * eo for i in range(nb)]), nb, M, N, K,
+        a.shape[2], b.shape[2], N, 1 if a_t else 0, 0 if b_t else 1, _DTYPE_CODE[out.dtype],
+        _stream_handle(stream)))

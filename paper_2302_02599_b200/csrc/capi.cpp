@@ -1046,6 +1046,70 @@ int apl_add(const void* a, const void* b, int b_mask, void* y, size_t count, flo
   });
 }
 
+int apl_layernorm_backward(const void* x, const void* gamma, const void* dy, void* dx,
+                           float* dgamma, float* dbeta, void* stats, int64_t rows, int64_t width,
+                           float eps, int dtype, void* stream) {
+  return guarded([&] {
+    need(rows >= 0 && width > 0, "bad extents");
+    need((x && dy && dx) || rows == 0, "null buffer");
+    need((dgamma == nullptr && dbeta == nullptr) || stats != nullptr || rows == 0,
+         "parameter gradients need the per-row stats scratch");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    apl::check_cuda(apl::launch_layernorm_backward(x, gamma, dy, dx, dgamma, dbeta, stats, rows,
+                                                   width, eps, dtype,
+                                                   static_cast<cudaStream_t>(stream)),
+                    "layernorm backward launch");
+  });
+}
+
+int apl_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows, int64_t width,
+                         float alpha, int dtype, void* stream) {
+  return guarded([&] {
+    need(rows >= 0 && width > 0, "bad extents");
+    need((y && dy && dx) || rows == 0, "null buffer");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    apl::check_cuda(apl::launch_softmax_backward(y, dy, dx, rows, width, alpha, dtype,
+                                                 static_cast<cudaStream_t>(stream)),
+                    "softmax backward launch");
+  });
+}
+
+int apl_embedding_backward(const int64_t* ids, int64_t n, const void* dy, float* dtable,
+                           int64_t vocab, int64_t width, int dtype, void* stream) {
+  return guarded([&] {
+    need(n >= 0 && vocab >= 0 && width >= 0, "negative extent");
+    need((ids && dy && dtable) || n == 0 || width == 0, "null buffer");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    apl::check_cuda(apl::launch_embedding_backward(ids, n, dy, dtable, vocab, width, dtype,
+                                                   static_cast<cudaStream_t>(stream)),
+                    "embedding backward launch");
+  });
+}
+
+int apl_gemm_bf16_grouped_ex(const void* const* A, const void* const* B, void* const* C,
+                             int groups, int64_t M, int64_t N, int64_t K, int64_t lda,
+                             int64_t ldb, int64_t ldc, int a_layout, int b_layout, int out_dtype,
+                             void* stream) {
+  return guarded([&] {
+    need(A && B && C && groups >= 1, "null operand table");
+    need(M > 0 && N > 0 && K > 0 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX,
+         "extents out of range");
+    need(a_layout == APL_A_MK || a_layout == APL_A_KM, "unknown A layout");
+    need(b_layout == APL_B_NK || b_layout == APL_B_KN, "unknown B layout");
+    const bool kn = b_layout == APL_B_KN, km = a_layout == APL_A_KM;
+    need(lda >= (km ? M : K) && ldb >= (kn ? N : K) && ldc >= N, "leading dimensions too small");
+    need(out_dtype == APL_F32 || out_dtype == APL_BF16, "output dtype must be f32 or bf16");
+    for (int i = 0; i < groups; ++i) need(A[i] && B[i] && C[i], "null operand");
+    apl::check_cuda(apl::gemm_bf16_grouped(A, B, C, groups, 1, 1, static_cast<int>(M),
+                                           static_cast<int>(N), static_cast<int>(K),
+                                           static_cast<int>(lda), static_cast<int>(ldb),
+                                           static_cast<int>(ldc), kn, out_dtype == APL_F32,
+                                           APL_EPI_NONE, km, nullptr, static_cast<int>(ldc),
+                                           static_cast<cudaStream_t>(stream)),
+                    "grouped GEMM launch");
+  });
+}
+
 int apl_mask_not(const void* x, void* y, size_t count, void* stream) {
   return guarded([&] {
     need((x && y) || count == 0, "null buffer");

@@ -341,6 +341,148 @@ __global__ void __launch_bounds__(256) softmax_cached_kernel(const T* __restrict
   }
 }
 
+// ---- backward ---------------------------------------------------------------
+// layernorm: dx = rstd * (g.dy - mean(g.dy) - xhat * mean(g.dy.xhat)), warp per
+// row (mean / rstd recomputed from x, kept per row for the column pass);
+// dgamma += sum_rows dy.xhat, dbeta += sum_rows dy in a second, column pass.
+template <typename T, int V>
+__global__ void __launch_bounds__(256) layernorm_bwd_kernel(
+    const T* __restrict__ x, const T* __restrict__ gamma, const T* __restrict__ dy,
+    T* __restrict__ dx, float2* __restrict__ stats, int64_t rows, int64_t width, float eps) {
+  const int lane = threadIdx.x % 32;
+  const int64_t nv = width / V;
+  const float inv_w = 1.f / static_cast<float>(width);
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const T* xr = x + r * width;
+    const T* gr = dy + r * width;
+    float s = 0.f;
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V];
+      load_row<T, V>(xr, i, f);
+#pragma unroll
+      for (int k = 0; k < V; ++k) s += f[k];
+    }
+    const float mean = warp_sum(s) * inv_w;
+    float q = 0.f;
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V];
+      load_row<T, V>(xr, i, f);
+#pragma unroll
+      for (int k = 0; k < V; ++k) q += (f[k] - mean) * (f[k] - mean);
+    }
+    const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
+    float a = 0.f, b = 0.f;  // sum g.dy, sum g.dy.xhat
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V], d[V], g[V];
+      load_row<T, V>(xr, i, f);
+      load_row<T, V>(gr, i, d);
+      if (gamma != nullptr) load_row<T, V>(gamma, i, g);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
+        a += gd;
+        b += gd * (f[k] - mean) * rstd;
+      }
+    }
+    a = warp_sum(a) * inv_w;
+    b = warp_sum(b) * inv_w;
+    for (int64_t i = lane; i < nv; i += 32) {
+      float f[V], d[V], g[V];
+      load_row<T, V>(xr, i, f);
+      load_row<T, V>(gr, i, d);
+      if (gamma != nullptr) load_row<T, V>(gamma, i, g);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
+        f[k] = rstd * (gd - a - (f[k] - mean) * rstd * b);
+      }
+      store_row<T, V>(dx + r * width, i, f);
+    }
+    if (lane == 0 && stats != nullptr) stats[r] = make_float2(mean, rstd);
+  }
+}
+
+// dgamma[c] += sum_r dy[r,c] * xhat[r,c], dbeta[c] += sum_r dy[r,c]: a 32-column
+// strip per warp lane group, row chunks across blockIdx.y, fp32 atomics.
+template <typename T>
+__global__ void __launch_bounds__(256) layernorm_param_grad_kernel(
+    const T* __restrict__ x, const T* __restrict__ dy, const float2* __restrict__ stats,
+    float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows, int64_t width,
+    int64_t rows_per_chunk) {
+  const int64_t c = blockIdx.x * 32 + threadIdx.x;
+  const int64_t r0 = blockIdx.y * rows_per_chunk;
+  const int64_t r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  float sg = 0.f, sb = 0.f;
+  if (c < width)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += blockDim.y) {
+      const float2 st = stats[r];
+      const float d = ld(dy + r * width + c);
+      sg += d * (ld(x + r * width + c) - st.x) * st.y;
+      sb += d;
+    }
+  __shared__ float red[2][8][33];
+  red[0][threadIdx.y][threadIdx.x] = sg;
+  red[1][threadIdx.y][threadIdx.x] = sb;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < width) {
+    for (int j = 1; j < blockDim.y; ++j) {
+      sg += red[0][j][threadIdx.x];
+      sb += red[1][j][threadIdx.x];
+    }
+    if (dgamma != nullptr) atomicAdd(dgamma + c, sg);
+    if (dbeta != nullptr) atomicAdd(dbeta + c, sb);
+  }
+}
+
+// softmax: dx = alpha * y * (dy - sum(dy * y)) per row (alpha: the fused
+// attention scale's chain rule; 1 for a plain softmax)
+template <typename T, int V>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(const T* __restrict__ y,
+                                                          const T* __restrict__ dy,
+                                                          T* __restrict__ dx, int64_t rows,
+                                                          int64_t width, float alpha) {
+  const int lane = threadIdx.x % 32;
+  const int64_t nv = width / V;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const T* yr = y + r * width;
+    const T* gr = dy + r * width;
+    float s = 0.f;
+    for (int64_t i = lane; i < nv; i += 32) {
+      float a[V], d[V];
+      load_row<T, V>(yr, i, a);
+      load_row<T, V>(gr, i, d);
+#pragma unroll
+      for (int k = 0; k < V; ++k) s += a[k] * d[k];
+    }
+    s = warp_sum(s);
+    for (int64_t i = lane; i < nv; i += 32) {
+      float a[V], d[V];
+      load_row<T, V>(yr, i, a);
+      load_row<T, V>(gr, i, d);
+#pragma unroll
+      for (int k = 0; k < V; ++k) a[k] = alpha * a[k] * (d[k] - s);
+      store_row<T, V>(dx + r * width, i, a);
+    }
+  }
+}
+
+// embedding: dtable[ids[t], :] += dy[t, :] (fp32 accumulation, atomics: ids repeat)
+template <typename T>
+__global__ void __launch_bounds__(256) embedding_bwd_kernel(const int64_t* __restrict__ ids,
+                                                            int64_t n, const T* __restrict__ dy,
+                                                            float* __restrict__ dtable,
+                                                            int64_t vocab, int64_t width) {
+  const int64_t total = n * width;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / width, c = i - t * width;
+    const int64_t id = __ldg(ids + t);
+    if (id >= 0 && id < vocab) atomicAdd(dtable + id * width + c, ld(dy + i));
+  }
+}
+
 // ---- elementwise ----------------------------------------------------------
 // y = alpha * x
 template <typename T, int V>
@@ -614,6 +756,92 @@ cudaError_t launch_mask_not(const void* x, void* y, size_t count, cudaStream_t s
   const int64_t n = static_cast<int64_t>(count);
   not_kernel<<<grid_for(n), 256, 0, s>>>(static_cast<const uint8_t*>(x), static_cast<uint8_t*>(y),
                                          n);
+  return done();
+}
+
+namespace {
+
+template <typename T>
+cudaError_t layernorm_bwd_typed(const void* x, const void* gamma, const void* dy, void* dx,
+                                float* dgamma, float* dbeta, float2* stats, int64_t rows,
+                                int64_t width, float eps, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const bool vec = width % V == 0 && aligned16(x) && aligned16(dy) && aligned16(dx) &&
+                   (!gamma || aligned16(gamma));
+  const int grid = grid_for(rows * 32);
+  auto X = static_cast<const T*>(x);
+  auto G = static_cast<const T*>(gamma);
+  auto D = static_cast<const T*>(dy);
+  auto O = static_cast<T*>(dx);
+  if (vec) layernorm_bwd_kernel<T, V><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+  else layernorm_bwd_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (dgamma != nullptr || dbeta != nullptr) {
+    const int64_t strips = (width + 31) / 32;
+    const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64,
+                                                                   (148 * 8 + strips - 1) / strips));
+    const int64_t per = (rows + chunks - 1) / chunks;
+    layernorm_param_grad_kernel<T><<<dim3(static_cast<unsigned>(strips),
+                                          static_cast<unsigned>(chunks)),
+                                     dim3(32, 8), 0, s>>>(X, D, stats, dgamma, dbeta, rows, width,
+                                                          per);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t softmax_bwd_typed(const void* y, const void* dy, void* dx, int64_t rows,
+                              int64_t width, float alpha, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const bool vec = width % V == 0 && aligned16(y) && aligned16(dy) && aligned16(dx);
+  const int grid = grid_for(rows * 32);
+  auto Y = static_cast<const T*>(y);
+  auto D = static_cast<const T*>(dy);
+  auto O = static_cast<T*>(dx);
+  if (vec) softmax_bwd_kernel<T, V><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+  else softmax_bwd_kernel<T, 1><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+  return done();
+}
+
+}  // namespace
+
+// stats: rows float2 scratch (mean, rstd), needed when dgamma / dbeta are
+// requested.
+cudaError_t launch_layernorm_backward(const void* x, const void* gamma, const void* dy, void* dx,
+                                      float* dgamma, float* dbeta, void* stats, int64_t rows,
+                                      int64_t width, float eps, int dtype, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  auto st = static_cast<float2*>(stats);
+  if (dtype == 0)
+    return layernorm_bwd_typed<float>(x, gamma, dy, dx, dgamma, dbeta, st, rows, width, eps, s);
+  if (dtype == 1)
+    return layernorm_bwd_typed<__nv_bfloat16>(x, gamma, dy, dx, dgamma, dbeta, st, rows, width,
+                                              eps, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows,
+                                    int64_t width, float alpha, int dtype, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  if (dtype == 0) return softmax_bwd_typed<float>(y, dy, dx, rows, width, alpha, s);
+  if (dtype == 1) return softmax_bwd_typed<__nv_bfloat16>(y, dy, dx, rows, width, alpha, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_embedding_backward(const int64_t* ids, int64_t n, const void* dy,
+                                      float* dtable, int64_t vocab, int64_t width, int dtype,
+                                      cudaStream_t s) {
+  if (n == 0 || width == 0) return cudaSuccess;
+  const int grid = grid_for(n * width);
+  if (dtype == 0)
+    embedding_bwd_kernel<float><<<grid, 256, 0, s>>>(ids, n, static_cast<const float*>(dy),
+                                                     dtable, vocab, width);
+  else if (dtype == 1)
+    embedding_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        ids, n, static_cast<const __nv_bfloat16*>(dy), dtable, vocab, width);
+  else
+    return cudaErrorInvalidValue;
   return done();
 }
 

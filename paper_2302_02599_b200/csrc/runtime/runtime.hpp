@@ -73,6 +73,14 @@ cudaError_t launch_scale(const void* x, void* y, size_t count, float alpha, int 
                          cudaStream_t s);
 cudaError_t launch_add(const void* a, const void* b, bool b_mask, void* y, size_t count,
                        float alpha, int dtype, cudaStream_t s);
+cudaError_t launch_layernorm_backward(const void* x, const void* gamma, const void* dy, void* dx,
+                                      float* dgamma, float* dbeta, void* stats, int64_t rows,
+                                      int64_t width, float eps, int dtype, cudaStream_t s);
+cudaError_t launch_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows,
+                                    int64_t width, float alpha, int dtype, cudaStream_t s);
+cudaError_t launch_embedding_backward(const int64_t* ids, int64_t n, const void* dy,
+                                      float* dtable, int64_t vocab, int64_t width, int dtype,
+                                      cudaStream_t s);
 cudaError_t launch_mask_not(const void* x, void* y, size_t count, cudaStream_t s);
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                       int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream);

@@ -402,8 +402,17 @@ class PlanExecutor:
                 values[nid] = ins[0]
             elif kind == "embedding-lookup" and gather_b:
                 values[nid] = self._lookup_gathered_table(nid, ins[0], ins[1], stream)
+                if train:
+                    self._saved[nid] = ins[0]
             elif kind in _BLOCK_KINDS:
                 values[nid] = self._block_node(n, ins, stream)
+                if train:  # what the node's backward reads (_block_backward)
+                    if kind in ("batched-matmul", "layernorm"):
+                        self._saved[nid] = ins
+                    elif kind == "embedding-lookup":
+                        self._saved[nid] = ins[0]
+                    elif kind == "softmax":
+                        self._saved[nid] = values[nid]
             else:
                 raise NotImplementedError(kind)
         return values[self.graph["output"]]
@@ -411,7 +420,6 @@ class PlanExecutor:
     def _block_node(self, n: dict, ins: list, stream) -> list:
         """One transformer-block node on every local shard (module docstring)."""
         from . import block_ops as B
-        from .runtime import gemm_grouped
 
         nid, kind = n["id"], n["kind"]
         spec = self.spec[nid]
@@ -454,13 +462,7 @@ class PlanExecutor:
             # one grouped tcgen05 GEMM per device: a problem per local batch
             st = self.strategy[nid]
             for a, b, o in zip(ins[0], ins[1], outs):
-                nb, m, k = a.shape
-                nn = b.shape[2]
-                ea, eo = a.element_size(), o.element_size()
-                gemm_grouped([a.data_ptr() + i * m * k * ea for i in range(nb)],
-                             [b.data_ptr() + i * k * nn * ea for i in range(nb)],
-                             [o.data_ptr() + i * m * nn * eo for i in range(nb)], 1, m, nn, k,
-                             k, nn, nn, "kn", o.dtype, False, stream)
+                B.bmm(a, b, o, stream=stream)
             if st.partial_sum:  # split-k strategies: `<host>.ar` (planner.cpp:263-282)
                 self.mesh.all_reduce(list(st.reduce_axes), outs, stream=stream)
         return outs
@@ -648,10 +650,6 @@ class PlanExecutor:
         take the reverse conversion back to the producer's layout."""
         if self._saved is None:
             raise RuntimeError("backward() needs a preceding forward(train=True)")
-        for n in self.graph["nodes"]:
-            if n["kind"] in _BLOCK_KINDS or (n["kind"] == "elementwise-unary"
-                                             and self.unary_op(n["id"]) != ("gelu",)):
-                raise NotImplementedError(f"backward through {n['kind']} ({n['id']})")
         out_id = self.graph["output"]
         out_node = self.nodes[out_id]
         src = out_node["inputs"][0][0]
@@ -664,10 +662,20 @@ class PlanExecutor:
         done = set()
         kinds = {"parameter"} | ({"placeholder"} if input_grads else set())
 
+        from . import block_ops as B
+
         def add(nid, shards):
-            if nid in grads:
+            if nid in grads:  # a value with several consumers: sum their gradients
+                # (out of place: a gradient list may be shared with another
+                # node's, e.g. both operands of a residual add)
+                summed = []
                 for acc, x in zip(grads[nid], shards):
-                    acc.add_(x)
+                    if acc.dtype != x.dtype:
+                        raise TypeError(f"{nid}: gradient dtypes differ")
+                    o = self._empty(acc.shape, acc.dtype, acc.device)
+                    B.add(acc, x, o, stream=stream)
+                    summed.append(o)
+                grads[nid] = summed
             else:
                 grads[nid] = shards
 
@@ -688,7 +696,8 @@ class PlanExecutor:
                 # GELU producing A in A's layout: its backward rides the dA epilogue.
                 aux, a_target = None, a_src
                 an = self.nodes[a_src]
-                if (an["kind"] == "elementwise-unary" and self.spec[a_src] == st.a
+                if (an["kind"] == "elementwise-unary" and self.unary_op(a_src) == ("gelu",)
+                        and self.spec[a_src] == st.a
                         and len(self._consumers.get(a_src, [])) == 1
                         and isinstance(self._saved.get(a_src), list)):
                     aux, a_target = self._saved[a_src], an["inputs"][0][0]
@@ -707,7 +716,7 @@ class PlanExecutor:
                                                       stream))
                 if need_b:
                     add(b_src, self._convert_grad(b_src, gb, st.b, self.spec[b_src], stream))
-            elif kind == "elementwise-unary":
+            elif kind == "elementwise-unary" and self.unary_op(nid)[0] == "gelu":
                 from .runtime import gelu_backward
                 x_src = n["inputs"][0][0]
                 pre = self._saved[nid]
@@ -715,9 +724,111 @@ class PlanExecutor:
                 for a, x, o in zip(dy, pre, dx):
                     gelu_backward(a, x, o, stream=stream)
                 add(x_src, self._convert_grad(x_src, dx, self.spec[nid], self.spec[x_src], stream))
+            elif kind in _BLOCK_KINDS or kind == "elementwise-unary":
+                for slot, g in self._block_backward(n, dy, wants_grad, stream):
+                    src = n["inputs"][slot][0]
+                    add(src, self._convert_grad(src, g, self.required_spec(nid, slot),
+                                                self.spec[src], stream))
         return {nid: grads[nid] for nid in grads
                 if self.nodes[nid]["kind"] in kinds}
 
+
+    def _block_backward(self, n: dict, dy: list, wants_grad, stream) -> list:
+        """Input gradients of one block node, each in the layout the node
+        consumed that input in (its strategy's input spec): [(slot, shards)].
+        Gradients that are partial sums over mesh axes (parameters shared by
+        sharded rows, batched-matmul contractions over a sharded dim) are
+        all-reduced here, before any reverse conversion (§4.4's rule)."""
+        from . import block_ops as B
+
+        nid, kind = n["id"], n["kind"]
+        ins = [i[0] for i in n["inputs"]]
+        like = lambda ts, dt=None: [self._empty(t.shape, dt or t.dtype, t.device)  # noqa: E731
+                                    for t in ts]
+        out = []
+        if kind == "reshape":
+            shape = self.required_spec(nid, 0).local_shape(self._meta(ins[0]), self.geo)
+            out.append((0, [g.view(shape) for g in dy]))
+        elif kind == "transpose":
+            dx = [self._empty(g.shape[:-2] + (g.shape[-1], g.shape[-2]), g.dtype, g.device)
+                  for g in dy]
+            for g, o in zip(dy, dx):
+                B.transpose_last2(g, o, stream=stream)
+            out.append((0, dx))
+        elif kind == "elementwise-unary":
+            op = self.unary_op(nid)
+            if op[0] == "scale" and wants_grad(ins[0]):
+                dx = like(dy)
+                for g, o in zip(dy, dx):
+                    B.scale(g, o, op[1], stream=stream)
+                out.append((0, dx))
+            elif op[0] != "not":
+                raise NotImplementedError(f"backward of unary {op}")
+        elif kind == "elementwise-binary":
+            for slot, src in enumerate(ins):
+                if self.shapes[src][1] != 1 and wants_grad(src):  # u8 masks carry no gradient
+                    out.append((slot, dy))
+        elif kind == "softmax":
+            y = self._saved[nid]
+            dx = like(dy)
+            for yy, g, o in zip(y, dy, dx):
+                B.softmax_backward(yy, g, o, stream=stream)
+            out.append((0, dx))
+        elif kind == "layernorm":
+            x, *aff = self._saved[nid]
+            gamma = aff[0] if aff else [None] * len(x)
+            dx = like(dy)
+            h = x[0].shape[-1]
+            dg = [torch.zeros(h, dtype=torch.float32, device=t.device) for t in x] if aff else None
+            db = ([torch.zeros(h, dtype=torch.float32, device=t.device) for t in x]
+                  if len(aff) > 1 else None)
+            for i, (xx, gg, g, o) in enumerate(zip(x, gamma, dy, dx)):
+                B.layernorm_backward(xx, gg, g, o, dg[i] if dg else None, db[i] if db else None,
+                                     stream=stream)
+            out.append((0, dx))
+            # gamma / beta are replicated; each device summed its own rows
+            row_axes = sorted({a for d in self.required_spec(nid, 0).dims[:-1] for a in d.axes})
+            for slot, pg in ((1, dg), (2, db)):
+                if pg is not None and wants_grad(ins[slot]):
+                    if row_axes:
+                        self.mesh.all_reduce(row_axes, pg, stream=stream)
+                    out.append((slot, pg))
+        elif kind == "embedding-lookup":
+            ids = self._saved[nid]
+            if wants_grad(ins[1]):
+                tspec = self.required_spec(nid, 1)
+                shape = tspec.local_shape(self._meta(ins[1]), self.geo)
+                dt = [torch.zeros(shape, dtype=torch.float32, device=g.device) for g in dy]
+                for i, g, o in zip(ids, dy, dt):
+                    B.embedding_backward(i, g, o, stream=stream)
+                id_axes = sorted({a for d in self.required_spec(nid, 0).dims for a in d.axes})
+                if id_axes:  # replicated table rows, ids sharded: partial sums
+                    self.mesh.all_reduce(id_axes, dt, stream=stream)
+                out.append((1, dt))
+        elif kind == "batched-matmul":
+            st = self.strategy[nid]
+            if st.partial_sum:
+                raise NotImplementedError("backward of split-k batched matmul strategies")
+            a, b = self._saved[nid]
+            # dA = dC . B^T partial over the axes sharding C's n dim, dB = A^T . dC
+            # over those sharding C's m dim (each device holds whole batches)
+            if wants_grad(ins[0]):
+                da = like(a)
+                for g, bb, o in zip(dy, b, da):
+                    B.bmm(g, bb, o, b_t=True, stream=stream)
+                if st.c.dims[2].axes:
+                    self.mesh.all_reduce(list(st.c.dims[2].axes), da, stream=stream)
+                out.append((0, da))
+            if wants_grad(ins[1]):
+                db = like(b)
+                for aa, g, o in zip(a, dy, db):
+                    B.bmm(aa, g, o, a_t=True, stream=stream)
+                if st.c.dims[1].axes:
+                    self.mesh.all_reduce(list(st.c.dims[1].axes), db, stream=stream)
+                out.append((1, db))
+        else:
+            raise NotImplementedError(f"backward through {kind} ({nid})")
+        return out
 
     # ---- CUDA graphs ---------------------------------------------------------
     def capture(self, feeds: dict, grad_out=None, warmup: int = 1):

@@ -258,3 +258,118 @@ def test_attention_chain_fused(cuda):
     assert n2 - n1 > n1 - n0  # the unfused chain launches more kernels
     assert _rel(fused, plain) <= 2e-2
     assert _rel(fused, ref) <= 4e-2
+
+
+# ---- backward ----------------------------------------------------------------
+@pytest.mark.parametrize("rows,width", [(2048, 1024), (77, 40), (9, 5)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_layernorm_softmax_backward(cuda, rows, width, dtype):
+    torch.manual_seed(rows)
+    x = (torch.randn(rows, width, device="cuda") * 2 + 0.5).to(dtype)
+    g = (1 + 0.1 * torch.randn(width, device="cuda")).to(dtype)
+    b = (0.1 * torch.randn(width, device="cuda")).to(dtype)
+    dy = torch.randn(rows, width, device="cuda").to(dtype)
+    tol = 2e-2 if dtype == torch.bfloat16 else 1e-4
+    xf, gf, bf = (t.float().requires_grad_() for t in (x, g, b))
+    F.layer_norm(xf, (width,), gf, bf, 1e-5).backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(width, device="cuda")
+    db = torch.zeros(width, device="cuda")
+    B.layernorm_backward(x, g, dy, dx, dg, db)
+    assert _rel(dx, xf.grad) <= tol
+    assert _rel(dg, gf.grad) <= tol and _rel(db, bf.grad) <= tol
+    yf = xf.detach().clone().requires_grad_()
+    y = torch.softmax(yf, -1)
+    (y * 0.5).backward(dy.float())  # alpha = 0.5 folds the chain's scale
+    B.softmax_backward(y.detach().to(dtype), dy, dx, 0.5)
+    assert _rel(dx, yf.grad) <= 3 * tol
+
+
+def test_embedding_backward_accumulates(cuda):
+    vocab, width, n = 300, 96, 5000
+    ids = torch.randint(0, vocab, (n,), device="cuda", dtype=torch.int64)
+    dy = torch.randn(n, width, device="cuda").bfloat16()
+    dt = torch.zeros(vocab, width, device="cuda")
+    B.embedding_backward(ids, dy, dt)
+    ref = torch.zeros(vocab, width, device="cuda").index_add_(0, ids, dy.float())
+    torch.testing.assert_close(dt, ref, atol=1e-3, rtol=1e-4)
+
+
+@pytest.mark.parametrize("a_t,b_t", [(False, False), (False, True), (True, False)])
+def test_bmm_layouts(cuda, a_t, b_t):
+    """The batched GEMM of batched-matmul nodes and their backward (dA =
+    dC.B^T, dB = A^T.dC) on the tcgen05 grouped kernel, fp32 out, vs fp32."""
+    nb, m, k, n = 4, 256, 192, 320
+    a = torch.randn(nb, k, m, device="cuda").bfloat16() if a_t else \
+        torch.randn(nb, m, k, device="cuda").bfloat16()
+    b = torch.randn(nb, n, k, device="cuda").bfloat16() if b_t else \
+        torch.randn(nb, k, n, device="cuda").bfloat16()
+    out = torch.empty(nb, m, n, device="cuda")
+    B.bmm(a, b, out, a_t=a_t, b_t=b_t)
+    ref = (a.float().transpose(1, 2) if a_t else a.float()) @ \
+        (b.float().transpose(1, 2) if b_t else b.float())
+    assert _rel(out, ref) <= 1e-5
+
+
+PARAMS = ("wte", "g1", "b1", "wq", "wk", "wv", "wo", "g2", "b2", "w1", "w2")
+
+
+def _unshard(ex, nid, shards):
+    """Global tensor from a simulated mesh's shards under nid's plan spec."""
+    shape, _ = ex.shapes[nid]
+    full = torch.empty(shape, dtype=shards[0].dtype, device=shards[0].device)
+    spec = ex.spec[nid]
+    for d, t in enumerate(shards):
+        coord = ex.geo.coord_of(d)
+        sl = []
+        for k, dim in enumerate(spec.dims):
+            s_, split = 0, 1
+            for a in dim.axes:
+                s_ = s_ * ex.geo.shape[a] + coord[a]
+                split *= ex.geo.shape[a]
+            L = shape[k] // split
+            sl.append(slice(s_ * L, (s_ + 1) * L))
+        full[tuple(sl)] = t
+    return full
+
+
+_GRAD_CACHE = {}
+
+
+def _reference_grads(tag):
+    if tag not in _GRAD_CACHE:
+        graph, feeds, _ = _case(tag)
+        leaves = {k: feeds[k].float().requires_grad_() for k in PARAMS}
+        p = dict(feeds)
+        p.update(leaves)
+        out = block_reference(p)
+        torch.manual_seed(7)
+        gy = torch.randn(out.shape, device="cuda").bfloat16()
+        out.backward(gy.float())
+        _GRAD_CACHE.clear()
+        _GRAD_CACHE[tag] = (gy, {k: v.grad for k, v in leaves.items()})
+    return _GRAD_CACHE[tag]
+
+
+@pytest.mark.parametrize("name", BLOCK_PLANS)
+def test_block_plans_backward(cuda, name):
+    """Training step of the block under each reference plan: every
+    parameter's gradient (in its plan layout, gathered here for the check)
+    against fp32 torch autograd of the same bf16 operands. Tolerance:
+    max|g - ref| / max|ref| <= 5e-2 and mean|g - ref| / mean|ref| <= 2e-2 per
+    parameter (bf16 activations and activation gradients throughout)."""
+    tag = name.split("_mesh")[0].removeprefix("gpt_block_")
+    graph, feeds, _ = _case(tag)
+    gy, ref = _reference_grads(tag)
+    plan = json.loads((PLANS / name).read_text())
+    ex = PlanExecutor(Mesh.local(plan["mesh"]["shape"]), graph, plan)
+    ex.forward(feeds, train=True)
+    grads = ex.backward(gy)
+    torch.cuda.synchronize()
+    assert set(grads) == set(PARAMS)
+    for k in PARAMS:
+        g = _unshard(ex, k, grads[k]).float()
+        r = ref[k]
+        mx = ((g - r).abs().max() / r.abs().max()).item()
+        mean = ((g - r).abs().mean() / r.abs().mean()).item()
+        assert mx <= 5e-2 and mean <= 2e-2, (k, mx, mean)
