@@ -356,8 +356,9 @@ def test_block_plans_backward(cuda, name):
     """Training step of the block under each reference plan: every
     parameter's gradient (in its plan layout, gathered here for the check)
     against fp32 torch autograd of the same bf16 operands. Tolerance:
-    max|g - ref| / max|ref| <= 5e-2 and mean|g - ref| / mean|ref| <= 2e-2 per
-    parameter (bf16 activations and activation gradients throughout)."""
+    max|g - ref| / max|ref| <= 2e-2 and mean|g - ref| / mean|ref| <= 1.5e-2 per
+    parameter (bf16 activations and activation gradients throughout; measured
+    <= 0.009 / 0.008, tools/block_grad_check.py)."""
     tag = name.split("_mesh")[0].removeprefix("gpt_block_")
     graph, feeds, _ = _case(tag)
     gy, ref = _reference_grads(tag)
@@ -372,4 +373,4 @@ def test_block_plans_backward(cuda, name):
         r = ref[k]
         mx = ((g - r).abs().max() / r.abs().max()).item()
         mean = ((g - r).abs().mean() / r.abs().mean()).item()
-        assert mx <= 5e-2 and mean <= 2e-2, (k, mx, mean)
+        assert mx <= 2e-2 and mean <= 1.5e-2, (k, mx, mean)

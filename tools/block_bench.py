@@ -8,6 +8,7 @@ conversions and the extra replicated work cost.
 
     python tools/block_bench.py [--quick]
     python tools/block_bench.py --once gpt_block_b8s1024_mesh8_unlimited   # ncu target
+    python tools/block_bench.py --once-train gpt_block_b8s1024_mesh8_unlimited
 
 FLOPs per forward: QKV + proj 4 x 2BSH^2, scores + ctx 2 x 2BS^2H, MLP
 2 x 2BSHF (the whole block, all devices together).
@@ -78,22 +79,28 @@ def time_forward(ex, feeds, iters):
     return a.elapsed_time(b) / iters, launch_count() - before
 
 
-def once(stem):
-    """Two eager forwards of one plan (for an ncu launch list)."""
+def once(stem, train=False):
+    """Two eager forwards (train: forward + backward steps) of one plan, for
+    an ncu launch list."""
     tag = stem.split("_mesh")[0]
     graph = json.loads((PLANS / f"{tag}_graph.json").read_text())
     plan = json.loads((PLANS / f"{stem}.json").read_text())
     feeds = _operands(graph)
     ex = PlanExecutor(Mesh.local(plan["mesh"]["shape"]), graph, plan)
     shards = {k: ex.shard(k, v) for k, v in feeds.items()}
+    gy = torch.randn(feeds["tok"].shape + (feeds["wte"].shape[1],), device="cuda").bfloat16()
     for _ in range(2):
-        ex.forward(shards)
+        ex.forward(shards, train=train)
+        if train:
+            ex.backward(gy)
     torch.cuda.synchronize()
 
 
 def main():
     if "--once" in sys.argv:
         return once(sys.argv[sys.argv.index("--once") + 1])
+    if "--once-train" in sys.argv:
+        return once(sys.argv[sys.argv.index("--once-train") + 1], train=True)
     quick = "--quick" in sys.argv
     iters = 5 if quick else 20
     rows = []
