@@ -451,6 +451,16 @@ int apl_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows, 
 int apl_embedding_backward(const int64_t* ids, int64_t n, const void* dy, float* dtable,
                            int64_t vocab, int64_t width, int dtype, void* stream);
 
+/* embedding backward with the gradient's reduce-scatter fused in: the block
+ * [rows, cols] of the table gradient at vocab rows [v0, v0 + rows) and columns
+ * [c0, c0 + cols) accumulates (+=, fp32) the rows of every source s -- ids[s]
+ * (n int64) with their output gradients dy[s] ([n, dy_width]) -- whose id
+ * falls in the block. One call per owner block replaces a per-device
+ * [vocab, width] partial gradient + all-reduce + slice. */
+int apl_embedding_backward_block(const int64_t* const* ids, const void* const* dy, int nsrc,
+                                 int64_t n, int64_t dy_width, float* dblock, int64_t v0,
+                                 int64_t rows, int64_t c0, int64_t cols, int dtype, void* stream);
+
 /* Physical layout of the A operand. */
 #define APL_A_MK 0 /* A [M, K], K contiguous */
 #define APL_A_KM 1 /* A stored transposed, row-major [K, M] (an activation read as A^T) */

@@ -182,6 +182,9 @@ _SIGS = {
                                        C.c_float, C.c_int, C.c_void_p]),
     "apl_embedding_backward": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                          C.c_int64, C.c_int64, C.c_int, C.c_void_p]),
+    "apl_embedding_backward_block": (C.c_int, [P(C.c_void_p), P(C.c_void_p), C.c_int, C.c_int64,
+                                               C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                                               C.c_int64, C.c_int64, C.c_int, C.c_void_p]),
     "apl_gemm_bf16_grouped_ex": (C.c_int, [P(C.c_void_p), P(C.c_void_p), P(C.c_void_p), C.c_int,
                                            C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                            C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,

@@ -129,6 +129,21 @@ def embedding_backward(ids: torch.Tensor, dy: torch.Tensor, dtable: torch.Tensor
                                          _DTYPE_CODE[dy.dtype], _stream_handle(stream)))
 
 
+def embedding_backward_block(ids: list, dys: list, dblock: torch.Tensor, v0: int, c0: int,
+                             stream=None) -> None:
+    """dblock += the rows of every (ids[s], dys[s]) source whose id lies in
+    [v0, v0 + dblock.shape[0]), columns [c0, c0 + dblock.shape[1]) of dy:
+    one owner block of a table gradient, reduce-scatter fused."""
+    P = C.c_void_p
+    n = ids[0].numel()
+    if any(i.numel() != n for i in ids):
+        raise ValueError("every source holds the same number of ids")
+    check(A.lib().apl_embedding_backward_block(
+        (P * len(ids))(*[i.data_ptr() for i in ids]), (P * len(dys))(*[d.data_ptr() for d in dys]),
+        len(ids), n, dys[0].shape[-1], _p(dblock), v0, dblock.shape[0], c0, dblock.shape[1],
+        _DTYPE_CODE[dys[0].dtype], _stream_handle(stream)))
+
+
 def bmm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, a_t: bool = False,
         b_t: bool = False, stream=None) -> None:
     """out[i] = op(a[i]) . op(b[i]) for every batch i on the tcgen05 tensor

@@ -1086,6 +1086,22 @@ int apl_embedding_backward(const int64_t* ids, int64_t n, const void* dy, float*
   });
 }
 
+int apl_embedding_backward_block(const int64_t* const* ids, const void* const* dy, int nsrc,
+                                 int64_t n, int64_t dy_width, float* dblock, int64_t v0,
+                                 int64_t rows, int64_t c0, int64_t cols, int dtype, void* stream) {
+  return guarded([&] {
+    need(nsrc >= 0 && nsrc <= 64, "0..64 sources");
+    need(n >= 0 && rows >= 0 && cols >= 0 && c0 >= 0 && c0 + cols <= dy_width, "bad extents");
+    need((ids && dy && dblock) || nsrc == 0 || n == 0, "null buffer");
+    for (int i = 0; ids && dy && i < nsrc; ++i) need(ids[i] && dy[i], "null source");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    apl::check_cuda(apl::launch_embedding_backward_block(ids, dy, nsrc, n, dy_width, dblock, v0,
+                                                         rows, c0, cols, dtype,
+                                                         static_cast<cudaStream_t>(stream)),
+                    "embedding backward launch");
+  });
+}
+
 int apl_gemm_bf16_grouped_ex(const void* const* A, const void* const* B, void* const* C,
                              int groups, int64_t M, int64_t N, int64_t K, int64_t lda,
                              int64_t ldb, int64_t ldc, int a_layout, int b_layout, int out_dtype,

@@ -483,6 +483,34 @@ __global__ void __launch_bounds__(256) embedding_bwd_kernel(const int64_t* __res
   }
 }
 
+// embedding backward with the gradient's reduce-scatter fused in: one owner's
+// block [rows x cols] of the table gradient (vocab rows [v0, v0 + rows),
+// columns [c0, c0 + cols)) accumulates every source's (ids, dy) rows that fall
+// in it -- instead of each device building a whole [vocab, width] partial
+// gradient that is then all-reduced and sliced. A warp per (source, token).
+struct EmbSources {
+  const int64_t* ids[kMaxBlocks];
+  const void* dy[kMaxBlocks];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) embedding_bwd_block_kernel(
+    const __grid_constant__ EmbSources src, int nsrc, int64_t n, int64_t dy_width,
+    float* __restrict__ dblock, int64_t v0, int64_t rows, int64_t c0, int64_t cols) {
+  const int lane = threadIdx.x % 32;
+  const int64_t total = static_cast<int64_t>(nsrc) * n;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; w < total;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const int e = static_cast<int>(w / n);
+    const int64_t t = w - e * n;
+    const int64_t id = src.ids[e][t] - v0;
+    if (id < 0 || id >= rows) continue;
+    const T* dr = static_cast<const T*>(src.dy[e]) + t * dy_width + c0;
+    float* out = dblock + id * cols;
+    for (int64_t c = lane; c < cols; c += 32) atomicAdd(out + c, ld(dr + c));
+  }
+}
+
 // ---- elementwise ----------------------------------------------------------
 // y = alpha * x
 template <typename T, int V>
@@ -840,6 +868,29 @@ cudaError_t launch_embedding_backward(const int64_t* ids, int64_t n, const void*
   else if (dtype == 1)
     embedding_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
         ids, n, static_cast<const __nv_bfloat16*>(dy), dtable, vocab, width);
+  else
+    return cudaErrorInvalidValue;
+  return done();
+}
+
+cudaError_t launch_embedding_backward_block(const int64_t* const* ids, const void* const* dy,
+                                            int nsrc, int64_t n, int64_t dy_width, float* dblock,
+                                            int64_t v0, int64_t rows, int64_t c0, int64_t cols,
+                                            int dtype, cudaStream_t s) {
+  if (nsrc == 0 || n == 0 || rows == 0 || cols == 0) return cudaSuccess;
+  if (nsrc > kMaxBlocks) return cudaErrorInvalidValue;
+  EmbSources src{};
+  for (int i = 0; i < nsrc; ++i) {
+    src.ids[i] = ids[i];
+    src.dy[i] = dy[i];
+  }
+  const int grid = grid_for(static_cast<int64_t>(nsrc) * n * 32);
+  if (dtype == 0)
+    embedding_bwd_block_kernel<float><<<grid, 256, 0, s>>>(src, nsrc, n, dy_width, dblock, v0,
+                                                           rows, c0, cols);
+  else if (dtype == 1)
+    embedding_bwd_block_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(src, nsrc, n, dy_width, dblock,
+                                                                   v0, rows, c0, cols);
   else
     return cudaErrorInvalidValue;
   return done();

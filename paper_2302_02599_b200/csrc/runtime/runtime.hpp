@@ -81,6 +81,10 @@ cudaError_t launch_softmax_backward(const void* y, const void* dy, void* dx, int
 cudaError_t launch_embedding_backward(const int64_t* ids, int64_t n, const void* dy,
                                       float* dtable, int64_t vocab, int64_t width, int dtype,
                                       cudaStream_t s);
+cudaError_t launch_embedding_backward_block(const int64_t* const* ids, const void* const* dy,
+                                            int nsrc, int64_t n, int64_t dy_width, float* dblock,
+                                            int64_t v0, int64_t rows, int64_t c0, int64_t cols,
+                                            int dtype, cudaStream_t s);
 cudaError_t launch_mask_not(const void* x, void* y, size_t count, cudaStream_t s);
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                       int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream);

@@ -725,10 +725,10 @@ class PlanExecutor:
                     gelu_backward(a, x, o, stream=stream)
                 add(x_src, self._convert_grad(x_src, dx, self.spec[nid], self.spec[x_src], stream))
             elif kind in _BLOCK_KINDS or kind == "elementwise-unary":
-                for slot, g in self._block_backward(n, dy, wants_grad, stream):
+                for slot, g, *lay in self._block_backward(n, dy, wants_grad, stream):
                     src = n["inputs"][slot][0]
-                    add(src, self._convert_grad(src, g, self.required_spec(nid, slot),
-                                                self.spec[src], stream))
+                    have = lay[0] if lay else self.required_spec(nid, slot)
+                    add(src, self._convert_grad(src, g, have, self.spec[src], stream))
         return {nid: grads[nid] for nid in grads
                 if self.nodes[nid]["kind"] in kinds}
 
@@ -795,8 +795,12 @@ class PlanExecutor:
                     out.append((slot, pg))
         elif kind == "embedding-lookup":
             ids = self._saved[nid]
-            if wants_grad(ins[1]):
-                tspec = self.required_spec(nid, 1)
+            tspec, tplan = self.required_spec(nid, 1), self.spec[ins[1]]
+            if (wants_grad(ins[1]) and not self.mesh.distributed and not tspec.dims[1].axes
+                    and tplan != tspec):
+                # straight into the table's own layout: reduce-scatter fused
+                out.append((1, self._embedding_grad_owned(nid, ids, dy, tplan, stream), tplan))
+            elif wants_grad(ins[1]):
                 shape = tspec.local_shape(self._meta(ins[1]), self.geo)
                 dt = [torch.zeros(shape, dtype=torch.float32, device=g.device) for g in dy]
                 for i, g, o in zip(ids, dy, dt):
@@ -829,6 +833,33 @@ class PlanExecutor:
         else:
             raise NotImplementedError(f"backward through {kind} ({nid})")
         return out
+
+    def _embedding_grad_owned(self, nid, ids, dy, tplan, stream) -> list:
+        """Table gradient of an embedding whose table is consumed with the
+        hidden dim whole (emb-batch) but stored sharded (`tplan`): every
+        device accumulates only its own block, from one representative
+        source per distinct id block (replicas counted once). Replaces a
+        [vocab, width] fp32 partial per device + all-reduce + slice."""
+        from . import block_ops as B
+
+        ispec = self.required_spec(nid, 0)
+        srcs = {}
+        for d in range(self.mesh.num_local):
+            key = tuple(self._block_index(dim, d)[0] for dim in ispec.dims)
+            srcs.setdefault(key, d)
+        order = sorted(srcs.values())
+        src_ids = [ids[d] for d in order]
+        src_dy = [dy[d] for d in order]
+        (vocab, width), _ = self.shapes[self.nodes[nid]["inputs"][1][0]]
+        outs = []
+        for d in range(self.mesh.num_local):
+            iv, nv = self._block_index(tplan.dims[0], d)
+            ih, nh = self._block_index(tplan.dims[1], d)
+            blk = torch.zeros(vocab // nv, width // nh, dtype=torch.float32, device=dy[0].device)
+            B.embedding_backward_block(src_ids, src_dy, blk, iv * (vocab // nv),
+                                       ih * (width // nh), stream=stream)
+            outs.append(blk)
+        return outs
 
     # ---- CUDA graphs ---------------------------------------------------------
     def capture(self, feeds: dict, grad_out=None, warmup: int = 1):

@@ -295,6 +295,21 @@ def test_embedding_backward_accumulates(cuda):
     torch.testing.assert_close(dt, ref, atol=1e-3, rtol=1e-4)
 
 
+def test_embedding_backward_owner_block(cuda):
+    """Reduce-scatter fused: one owner block of the table gradient from
+    several sources' (ids, dy) == that block of the summed full gradient."""
+    vocab, width, n, nsrc = 512, 64, 700, 4
+    ids = [torch.randint(0, vocab, (n,), device="cuda", dtype=torch.int64) for _ in range(nsrc)]
+    dys = [torch.randn(n, width, device="cuda").bfloat16() for _ in range(nsrc)]
+    full = torch.zeros(vocab, width, device="cuda")
+    for i, d in zip(ids, dys):
+        full.index_add_(0, i, d.float())
+    for v0, c0, rows, cols in ((0, 0, vocab, width), (128, 0, 128, width), (256, 32, 256, 32)):
+        blk = torch.zeros(rows, cols, device="cuda")
+        B.embedding_backward_block(ids, dys, blk, v0, c0)
+        torch.testing.assert_close(blk, full[v0:v0 + rows, c0:c0 + cols], atol=1e-3, rtol=1e-4)
+
+
 @pytest.mark.parametrize("a_t,b_t", [(False, False), (False, True), (True, False)])
 def test_bmm_layouts(cuda, a_t, b_t):
     """The batched GEMM of batched-matmul nodes and their backward (dA =
