@@ -14,7 +14,16 @@
 //     GEMMs on the shards, with the partial-sum all-reduce (`<host>.ar`,
 //     planner.cpp:263-282); a GELU consuming a non-partial matmul output in
 //     the same layout is fused into the GEMM epilogue;
+//   * the transformer-block kinds of gpt_block.json run their named strategy
+//     on the local shards (intraop.cpp:280-450): reshape = a view, transpose /
+//     layernorm / softmax / embedding / elementwise = block_ops kernels,
+//     batched matmul = one grouped tcgen05 GEMM per device (+ the split-k
+//     all-reduce); the attention chain scale -> u8 mask -> softmax runs as
+//     one pass and a sharded embedding table is read from its owners' blocks
+//     (simulated mesh) exactly when the Python executor does so;
 //   * the output node collects to RR (intraop.cpp:469-482).
+// Unary functions are bound by the Python executor's rule (u8 input: not;
+// "scale" id behind a batched matmul: 1/sqrt(k); else GELU).
 // The Python PlanExecutor (paper_2302_02599_b200/executor.py) is the same
 // algorithm plus the backward pass; tests/test_cpp_plan_executor.py checks
 // the two produce identical bytes.
@@ -22,6 +31,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <map>
 #include <nlohmann/json.hpp>
 #include <set>
@@ -59,24 +69,58 @@ class PlanExecutor {
         const TensorMeta& b = nodes_.at(nd.inputs.at(1)).meta;
         nd.meta = a;
         nd.meta.shape.back() = b.shape.back();
-      } else if (nd.kind == "elementwise-unary" || nd.kind == "output") {
+      } else if (nd.kind == "batched-matmul") {
+        const TensorMeta& a = nodes_.at(nd.inputs.at(0)).meta;
+        const TensorMeta& b = nodes_.at(nd.inputs.at(1)).meta;
+        nd.meta = a;
+        nd.meta.shape = {a.shape.at(0), a.shape.at(1), b.shape.at(2)};
+      } else if (nd.kind == "elementwise-unary" || nd.kind == "output" ||
+                 nd.kind == "layernorm" || nd.kind == "softmax") {
         nd.meta = nodes_.at(nd.inputs.at(0)).meta;
+      } else if (nd.kind == "elementwise-binary") {
+        nd.meta = nodes_.at(nd.inputs.at(0)).meta;
+        nd.meta.dtype_bytes =
+            std::max(nd.meta.dtype_bytes, nodes_.at(nd.inputs.at(1)).meta.dtype_bytes);
+      } else if (nd.kind == "reshape") {
+        nd.meta = nodes_.at(nd.inputs.at(0)).meta;
+        nd.meta.shape = node.at("attrs").at("target_shape").get<std::vector<int64_t>>();
+      } else if (nd.kind == "transpose") {
+        const TensorMeta& in = nodes_.at(nd.inputs.at(0)).meta;
+        nd.perm = node.at("attrs").at("perm").get<std::vector<int64_t>>();
+        nd.meta = in;
+        for (size_t i = 0; i < nd.perm.size(); ++i)
+          nd.meta.shape[i] = in.shape.at(static_cast<size_t>(nd.perm[i]));
+      } else if (nd.kind == "embedding-lookup") {
+        const TensorMeta& ids = nodes_.at(nd.inputs.at(0)).meta;
+        const TensorMeta& table = nodes_.at(nd.inputs.at(1)).meta;
+        nd.meta = table;
+        nd.meta.shape = ids.shape;
+        nd.meta.shape.push_back(table.shape.at(1));
       } else {
         throw SchemaError("node kind '" + nd.kind + "' is not executable");
       }
+      if (node.contains("attrs") && node.at("attrs").contains("axis"))
+        nd.axis = node.at("attrs").at("axis").get<int64_t>();
       const auto& pn = p.at("nodes").at(nd.id);
       nd.spec = ShardingSpec::parse(pn.at("spec").get<std::string>(), mesh_.rank());
-      if (nd.kind == "matmul") {
-        nd.strategy = find_matmul_strategy(pn.at("strategy").get<std::string>(),
-                                           nodes_.at(nd.inputs.at(0)).meta,
-                                           nodes_.at(nd.inputs.at(1)).meta, mesh_);
+      const std::string name = pn.at("strategy").get<std::string>();
+      if (nd.kind == "matmul" || nd.kind == "batched-matmul") {
+        nd.strategy = find_matmul_strategy(name, nodes_.at(nd.inputs.at(0)).meta,
+                                           nodes_.at(nd.inputs.at(1)).meta, mesh_,
+                                           nd.kind == "batched-matmul");
         if (!(nd.strategy.output_spec == nd.spec))
           throw ShapeError(nd.id + ": plan spec differs from its strategy's output spec");
+        nd.in_specs = nd.strategy.input_specs;
+      } else if (nd.kind != "placeholder" && nd.kind != "parameter") {
+        nd.in_specs = input_specs(nd, name);
       }
       order_.push_back(nd.id);
       for (const auto& in : nd.inputs) consumers_[in].push_back(nd.id);
       nodes_.emplace(nd.id, std::move(nd));
     }
+    for (auto& [id, nd] : nodes_)
+      if (nd.kind == "elementwise-unary") bind_unary(nd);
+    find_attention_chains();
   }
 
   PlanExecutor(const PlanExecutor&) = delete;
@@ -90,6 +134,15 @@ class PlanExecutor {
   int num_local() const { return num_local_; }
   const ShardingSpec& spec(const std::string& id) const { return nodes_.at(id).spec; }
   const TensorMeta& meta(const std::string& id) const { return nodes_.at(id).meta; }
+  // placeholders and parameters, in graph order (what forward() must be fed)
+  std::vector<std::string> sources() const {
+    std::vector<std::string> out;
+    for (const auto& id : order_) {
+      const std::string& k = nodes_.at(id).kind;
+      if (k == "placeholder" || k == "parameter") out.push_back(id);
+    }
+    return out;
+  }
 
   // feeds: for every placeholder / parameter, its local shards (one device
   // pointer per local device) in the node's plan spec. Returns the output's
@@ -110,12 +163,26 @@ class PlanExecutor {
         values[id] = f;
         continue;
       }
+      if (attn_members_.count(id)) continue;  // inside the fused softmax below
+      if (auto ch = attn_.find(id); ch != attn_.end()) {
+        auto out = buffers(id, nd.spec, nd.meta);
+        const auto& x = values.at(ch->second.x);
+        const auto& m = values.at(ch->second.mask);
+        const auto sh = local_shape(nd.spec, nd.meta);
+        const int64_t w = sh.back(), rows = numel(sh) / w;
+        for (int d = 0; d < num_local_; ++d)
+          apl_detail::check(apl_softmax_ex(x[d], out[d], rows, w, ch->second.alpha, m[d],
+                                           kMaskFill, dtype_of(nd.meta), stream));
+        values[id] = as_const(out);
+        continue;
+      }
+      const bool gather_t = nd.kind == "embedding-lookup" && gatherable_table(nd);
       std::vector<std::vector<const void*>> ins;
       for (size_t slot = 0; slot < nd.inputs.size(); ++slot) {
         const std::string& src = nd.inputs[slot];
         const ShardingSpec want = required_spec(nd, slot);
         const ShardingSpec& have = nodes_.at(src).spec;
-        if (have == want) {
+        if (have == want || (slot == 1 && gather_t)) {
           ins.push_back(values.at(src));
           continue;
         }
@@ -148,42 +215,293 @@ class PlanExecutor {
           continue;
         }
         auto out = buffers(id, nd.spec, nd.meta);
-        const size_t count = static_cast<size_t>(nd.spec.per_device_bytes(nd.meta, mesh_) /
-                                                 nd.meta.dtype_bytes);
-        for (int d = 0; d < num_local_; ++d)
-          apl_detail::check(apl_gelu(ins[0][d], out[d], count,
-                                     nd.meta.dtype_bytes == 4 ? APL_F32 : APL_BF16, stream));
+        const size_t count = static_cast<size_t>(numel(local_shape(nd.spec, nd.meta)));
+        for (int d = 0; d < num_local_; ++d) {
+          if (nd.unary == Unary::kGelu)
+            apl_detail::check(apl_gelu(ins[0][d], out[d], count, dtype_of(nd.meta), stream));
+          else if (nd.unary == Unary::kScale)
+            apl_detail::check(
+                apl_scale(ins[0][d], out[d], count, nd.alpha, dtype_of(nd.meta), stream));
+          else
+            apl_detail::check(apl_mask_not(ins[0][d], out[d], count, stream));
+        }
         values[id] = as_const(out);
-      } else {  // output: already collected to RR by the conversion above
+      } else if (nd.kind == "output") {  // already collected to RR by the conversion above
         values[id] = ins[0];
         if (id == output_)
           for (const void* v : ins[0]) result.push_back(const_cast<void*>(v));
+      } else if (nd.kind == "reshape") {  // a view: the plan's rewritten local shape
+        values[id] = ins[0];
+      } else if (nd.kind == "embedding-lookup" && gather_t) {
+        values[id] = lookup_gathered_table(nd, ins[0], values.at(nd.inputs[1]), stream);
+      } else {
+        values[id] = block_node(nd, ins, stream);
       }
     }
     return result;
   }
 
  private:
+  static constexpr float kMaskFill = -1e4f;  // additive attention mask
+  enum class Unary { kGelu, kScale, kNot };
+
   struct Node {
     std::string id, kind;
     std::vector<std::string> inputs;
     TensorMeta meta;
     ShardingSpec spec;
     OpStrategy strategy;
+    std::vector<ShardingSpec> in_specs;
+    std::vector<int64_t> perm;
+    int64_t axis = -1;
+    Unary unary = Unary::kGelu;
+    float alpha = 1.f;
   };
 
-  ShardingSpec required_spec(const Node& nd, size_t slot) const {
-    if (nd.kind == "matmul") return nd.strategy.input_specs.at(slot);
-    if (nd.kind == "output")
-      return ShardingSpec::replicated(static_cast<int>(nd.meta.shape.size()), mesh_.rank());
-    return nd.spec;  // elementwise: the node's layout mirrored onto its input
+  struct Chain {
+    std::string x, mask;
+    float alpha;
+  };
+
+  static int64_t numel(const std::vector<int64_t>& s) {
+    int64_t n = 1;
+    for (int64_t e : s) n *= e;
+    return n;
   }
+  static int dtype_of(const TensorMeta& m) { return m.dtype_bytes == 4 ? APL_F32 : APL_BF16; }
+
+  std::vector<int64_t> local_shape(const ShardingSpec& spec, const TensorMeta& m) const {
+    std::vector<int64_t> out = m.shape;
+    for (size_t k = 0; k < out.size(); ++k)
+      for (int a : spec.dims[k].axes) out[k] /= mesh_.shape[static_cast<size_t>(a)];
+    return out;
+  }
+
+  // (index, count) of `device`'s block along a dim sharded over dim.axes
+  std::pair<int64_t, int64_t> block_index(const DimSpec& dim, int64_t device) const {
+    const auto c = mesh_.coord_of(device);
+    int64_t idx = 0, cnt = 1;
+    for (int a : dim.axes) {
+      idx = idx * mesh_.shape[static_cast<size_t>(a)] + c[static_cast<size_t>(a)];
+      cnt *= mesh_.shape[static_cast<size_t>(a)];
+    }
+    return {idx, cnt};
+  }
+
+  // a device holding block (i, j) of a rank-2 spec (mixed radix, first axis
+  // most significant)
+  int64_t block_owner(const ShardingSpec& spec, int64_t i, int64_t j) const {
+    std::vector<int64_t> coord(static_cast<size_t>(mesh_.rank()), 0);
+    const int64_t idx[2] = {i, j};
+    for (int k = 0; k < 2; ++k) {
+      int64_t v = idx[k];
+      const auto& axes = spec.dims[static_cast<size_t>(k)].axes;
+      for (auto a = axes.rbegin(); a != axes.rend(); ++a) {
+        coord[static_cast<size_t>(*a)] = v % mesh_.shape[static_cast<size_t>(*a)];
+        v /= mesh_.shape[static_cast<size_t>(*a)];
+      }
+    }
+    return mesh_.device_of(coord);
+  }
+
+  // input layouts of a non-matmul node's named strategy (intraop.cpp:280-450)
+  std::vector<ShardingSpec> input_specs(const Node& nd, const std::string& name) const {
+    const int mr = mesh_.rank();
+    if (nd.kind == "output")
+      return {ShardingSpec::replicated(static_cast<int>(nd.meta.shape.size()), mr)};
+    if (nd.kind == "reshape" || nd.kind == "transpose" || nd.kind == "softmax" ||
+        nd.kind == "layernorm") {
+      const ShardingSpec in = ShardingSpec::parse(name.substr(name.find(':') + 1), mr);
+      std::vector<ShardingSpec> out = {in};
+      if (nd.kind == "layernorm")
+        for (size_t i = 1; i < nd.inputs.size(); ++i)
+          out.push_back(ShardingSpec::replicated(1, mr));
+      return out;
+    }
+    if (nd.kind == "embedding-lookup") {
+      const size_t ri = nodes_.at(nd.inputs.at(0)).meta.shape.size();
+      ShardingSpec ids = ShardingSpec::replicated(static_cast<int>(ri), mr);
+      for (size_t k = 0; k < ri; ++k) ids.dims[k] = nd.spec.dims[k];
+      ShardingSpec table = ShardingSpec::replicated(2, mr);
+      table.dims[1] = nd.spec.dims[ri];
+      return {ids, table};
+    }
+    return std::vector<ShardingSpec>(nd.inputs.size(), nd.spec);  // elementwise
+  }
+
+  void bind_unary(Node& nd) const {
+    const Node& src = nodes_.at(nd.inputs.at(0));
+    if (src.meta.dtype_bytes == 1) {
+      nd.unary = Unary::kNot;
+    } else if (nd.id.find("scale") != std::string::npos && src.kind == "batched-matmul") {
+      nd.unary = Unary::kScale;
+      const double k = static_cast<double>(nodes_.at(src.inputs.at(0)).meta.shape.back());
+      nd.alpha = static_cast<float>(1.0 / std::sqrt(k));
+    } else {
+      nd.unary = Unary::kGelu;
+    }
+  }
+
+  // scale -> u8 additive mask -> last-axis softmax, no conversion on the way
+  void find_attention_chains() {
+    auto single = [&](const std::string& id) {
+      auto it = consumers_.find(id);
+      return it != consumers_.end() && it->second.size() == 1;
+    };
+    for (const auto& [id, sm] : nodes_) {
+      if (sm.kind != "softmax" ||
+          (sm.axis != -1 && sm.axis != static_cast<int64_t>(sm.meta.shape.size()) - 1))
+        continue;
+      const Node& b = nodes_.at(sm.inputs.at(0));
+      if (b.kind != "elementwise-binary" || !single(b.id) || !(b.spec == sm.in_specs.at(0)))
+        continue;
+      int mslot = -1, nmask = 0;
+      for (int k = 0; k < 2; ++k)
+        if (nodes_.at(b.inputs[static_cast<size_t>(k)]).meta.dtype_bytes == 1) {
+          mslot = k;
+          ++nmask;
+        }
+      if (nmask != 1) continue;
+      const Node& u = nodes_.at(b.inputs[static_cast<size_t>(1 - mslot)]);
+      const Node& m = nodes_.at(b.inputs[static_cast<size_t>(mslot)]);
+      if (u.kind != "elementwise-unary" || !single(u.id) || u.unary != Unary::kScale) continue;
+      const Node& x = nodes_.at(u.inputs.at(0));
+      if (!(u.spec == b.in_specs[static_cast<size_t>(1 - mslot)]) ||
+          !(m.spec == b.in_specs[static_cast<size_t>(mslot)]) || !(x.spec == u.in_specs.at(0)))
+        continue;
+      attn_[id] = Chain{x.id, m.id, u.alpha};
+      attn_members_.insert(u.id);
+      attn_members_.insert(b.id);
+    }
+  }
+
+  ShardingSpec required_spec(const Node& nd, size_t slot) const { return nd.in_specs.at(slot); }
 
   std::string fusable_gelu(const Node& mm) const {
     auto it = consumers_.find(mm.id);
-    if (it == consumers_.end() || it->second.size() != 1 || mm.strategy.partial_sum) return "";
+    if (it == consumers_.end() || it->second.size() != 1 || mm.strategy.partial_sum ||
+        mm.kind != "matmul")
+      return "";
     const Node& g = nodes_.at(it->second[0]);
-    return g.kind == "elementwise-unary" && g.spec == mm.spec ? g.id : "";
+    return g.kind == "elementwise-unary" && g.unary == Unary::kGelu && g.spec == mm.spec ? g.id
+                                                                                        : "";
+  }
+
+  // an embedding whose sharded table is read from its owners' blocks
+  // (simulated mesh; the Python executor's auto rule)
+  bool gatherable_table(const Node& nd) const {
+    int n = 0, first = 0, nl = 0, dist = 0;
+    apl_detail::check(apl_mesh_info(rt_.get(), &n, &first, &nl, &dist));
+    if (dist) return false;
+    const ShardingSpec& have = nodes_.at(nd.inputs.at(1)).spec;
+    if (have == required_spec(nd, 1)) return false;
+    int64_t nb = 1;
+    for (const auto& d : have.dims)
+      for (int a : d.axes) nb *= mesh_.shape[static_cast<size_t>(a)];
+    return nb <= 64;
+  }
+
+  std::vector<const void*> lookup_gathered_table(const Node& nd,
+                                                 const std::vector<const void*>& ids,
+                                                 const std::vector<const void*>& table,
+                                                 void* stream) {
+    const Node& t = nodes_.at(nd.inputs.at(1));
+    const ShardingSpec& have = t.spec;
+    const ShardingSpec want = required_spec(nd, 1);
+    const int64_t vocab = t.meta.shape.at(0), width = t.meta.shape.at(1);
+    const int64_t nvb = block_index(have.dims[0], 0).second;
+    const int64_t nhb = block_index(have.dims[1], 0).second;
+    std::vector<const void*> blocks;
+    for (int64_t i = 0; i < nvb; ++i)
+      for (int64_t j = 0; j < nhb; ++j) blocks.push_back(table.at(static_cast<size_t>(
+          block_owner(have, i, j))));
+    auto out = buffers(nd.id, nd.spec, nd.meta);
+    const auto ls = local_shape(nd.spec, nd.meta);
+    const int64_t n = numel(ls) / ls.back();
+    for (int d = 0; d < num_local_; ++d) {
+      const auto [j, nw] = block_index(want.dims[1], d);
+      apl_detail::check(apl_embedding_lookup_blocks(
+          static_cast<const int64_t*>(ids[d]), n, blocks.data(), static_cast<int>(nvb),
+          static_cast<int>(nhb), vocab, width, j * (width / nw), ls.back(), t.meta.dtype_bytes,
+          out[d], stream));
+    }
+    return as_const(out);
+  }
+
+  std::vector<const void*> block_node(const Node& nd,
+                                      const std::vector<std::vector<const void*>>& ins,
+                                      void* stream) {
+    auto out = buffers(nd.id, nd.spec, nd.meta);
+    const auto ls = local_shape(nd.spec, nd.meta);
+    const int dt = dtype_of(nd.meta);
+    if (nd.kind == "embedding-lookup") {
+      const Node& t = nodes_.at(nd.inputs[1]);
+      const auto ts = local_shape(required_spec(nd, 1), t.meta);
+      const int64_t n = numel(ls) / ls.back();
+      for (int d = 0; d < num_local_; ++d)
+        apl_detail::check(apl_embedding_lookup(static_cast<const int64_t*>(ins[0][d]), n,
+                                               ins[1][d], ts[0], ts[1], t.meta.dtype_bytes,
+                                               out[d], stream));
+    } else if (nd.kind == "layernorm") {
+      const int64_t w = ls.back(), rows = numel(ls) / w;
+      for (int d = 0; d < num_local_; ++d)
+        apl_detail::check(apl_layernorm(ins[0][d], ins.size() > 1 ? ins[1][d] : nullptr,
+                                        ins.size() > 2 ? ins[2][d] : nullptr, out[d], rows, w,
+                                        1e-5f, dt, stream));
+    } else if (nd.kind == "softmax") {
+      if (nd.axis != -1 && nd.axis != static_cast<int64_t>(ls.size()) - 1)
+        throw SchemaError(nd.id + ": softmax over a non-last axis is not executable");
+      const int64_t w = ls.back(), rows = numel(ls) / w;
+      for (int d = 0; d < num_local_; ++d)
+        apl_detail::check(apl_softmax(ins[0][d], out[d], rows, w, dt, stream));
+    } else if (nd.kind == "transpose") {
+      const size_t r = nd.perm.size();
+      for (size_t i = 0; i + 2 < r; ++i)
+        if (nd.perm[i] != static_cast<int64_t>(i))
+          throw SchemaError(nd.id + ": only last-two-dim transposes are executable");
+      if (r < 2 || nd.perm[r - 2] != static_cast<int64_t>(r - 1) ||
+          nd.perm[r - 1] != static_cast<int64_t>(r - 2))
+        throw SchemaError(nd.id + ": only last-two-dim transposes are executable");
+      const auto is = local_shape(required_spec(nd, 0), nodes_.at(nd.inputs[0]).meta);
+      const int64_t rows = is[r - 2], cols = is[r - 1], batch = numel(is) / (rows * cols);
+      for (int d = 0; d < num_local_; ++d)
+        apl_detail::check(
+            apl_transpose(ins[0][d], out[d], batch, rows, cols, nd.meta.dtype_bytes, stream));
+    } else if (nd.kind == "elementwise-binary") {
+      int a = 0, b = 1;
+      if (nodes_.at(nd.inputs[0]).meta.dtype_bytes == 1) std::swap(a, b);
+      const bool mask = nodes_.at(nd.inputs[static_cast<size_t>(b)]).meta.dtype_bytes == 1;
+      const size_t count = static_cast<size_t>(numel(ls));
+      for (int d = 0; d < num_local_; ++d)
+        apl_detail::check(apl_add(ins[static_cast<size_t>(a)][d], ins[static_cast<size_t>(b)][d],
+                                  mask ? 1 : 0, out[d], count, mask ? kMaskFill : 1.f, dt,
+                                  stream));
+    } else if (nd.kind == "batched-matmul") {
+      const auto as = local_shape(required_spec(nd, 0), nodes_.at(nd.inputs[0]).meta);
+      const int64_t nb = as[0], m = as[1], k = as[2], n = ls[2];
+      const int64_t ea = nodes_.at(nd.inputs[0]).meta.dtype_bytes, eo = nd.meta.dtype_bytes;
+      for (int d = 0; d < num_local_; ++d) {
+        std::vector<const void*> A, B;
+        std::vector<void*> Cp;
+        for (int64_t i = 0; i < nb; ++i) {
+          A.push_back(static_cast<const char*>(ins[0][d]) + i * m * k * ea);
+          B.push_back(static_cast<const char*>(ins[1][d]) + i * k * n * ea);
+          Cp.push_back(static_cast<char*>(out[d]) + i * m * n * eo);
+        }
+        apl_detail::check(apl_gemm_bf16_grouped_ex(A.data(), B.data(), Cp.data(),
+                                                   static_cast<int>(nb), m, n, k, k, n, n,
+                                                   APL_A_MK, APL_B_KN, dt, stream));
+      }
+      if (nd.strategy.partial_sum) {
+        std::vector<int32_t> axes(nd.strategy.reduce_axes.begin(), nd.strategy.reduce_axes.end());
+        apl_detail::check(apl_all_reduce(rt_.get(), axes.data(), static_cast<int>(axes.size()),
+                                         out.data(), static_cast<size_t>(numel(ls)), dt,
+                                         stream));
+      }
+    } else {
+      throw SchemaError("node kind '" + nd.kind + "' is not executable");
+    }
+    return as_const(out);
   }
 
   static std::vector<const void*> as_const(const std::vector<void*>& v) {
@@ -231,6 +549,8 @@ class PlanExecutor {
   std::vector<std::string> order_;
   std::map<std::string, Node> nodes_;
   std::map<std::string, std::vector<std::string>> consumers_;
+  std::map<std::string, Chain> attn_;
+  std::set<std::string> attn_members_;
   std::map<std::string, std::vector<void*>> buffers_;
   std::map<std::string, std::pair<void*, size_t>> workspaces_;
 };

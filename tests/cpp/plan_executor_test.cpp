@@ -1,11 +1,13 @@
 // Runs a reference plan with the native C++ PlanExecutor on a simulated mesh:
 //   plan_executor_test <graph.json> <plan.json> <mesh AxB> <dir>
-// reads <dir>/<id>.bin (global row-major bf16 tensors of every placeholder
-// and parameter), shards them on the host by each node's plan spec, runs the
-// forward pass and writes device 0's output replica to <dir>/out.bin.
+// reads <dir>/<id>.bin (global row-major tensors of every placeholder and
+// parameter, any rank and element size), shards them on the host by each
+// node's plan spec, runs the forward pass and writes device 0's output
+// replica to <dir>/out.bin.
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstring>
 #include <fstream>
 #include <iostream>
 #include <sstream>
@@ -34,31 +36,43 @@ int main(int argc, char** argv) {
   PlanExecutor ex(rt, mesh, slurp(argv[1]), slurp(argv[2]));
   std::map<std::string, std::vector<const void*>> feeds;
   std::vector<void*> owned;
-  for (const std::string id : {"x", "w1", "w2"}) {
+  for (const std::string& id : ex.sources()) {
     const TensorMeta& m = ex.meta(id);
     const ShardingSpec& s = ex.spec(id);
     const std::string data = slurp(dir + "/" + id + ".bin");
-    const int64_t rows = m.shape[0], cols = m.shape[1], eb = m.dtype_bytes;
+    const size_t rank = m.shape.size();
+    const int64_t eb = m.dtype_bytes;
     std::vector<const void*> shards;
     for (int64_t d = 0; d < mesh.num_devices(); ++d) {
       const auto c = mesh.coord_of(d);
-      int64_t blk[2], cnt[2];
-      for (int k = 0; k < 2; ++k) {
-        blk[k] = 0;
-        cnt[k] = 1;
+      std::vector<int64_t> blk(rank, 0), loc(rank);
+      int64_t total = 1;
+      for (size_t k = 0; k < rank; ++k) {
+        int64_t cnt = 1;
         for (int a : s.dims[k].axes) {
           blk[k] = blk[k] * mesh.shape[a] + c[a];
-          cnt[k] *= mesh.shape[a];
+          cnt *= mesh.shape[a];
+        }
+        loc[k] = m.shape[k] / cnt;
+        total *= loc[k];
+      }
+      // copy the block run by run (runs = the local extent of the last dim)
+      std::vector<char> host(static_cast<size_t>(total * eb));
+      const int64_t run = loc[rank - 1];
+      std::vector<int64_t> idx(rank, 0);
+      for (int64_t r = 0; r < total / run; ++r) {
+        int64_t off = 0;
+        for (size_t k = 0; k < rank; ++k)
+          off = off * m.shape[k] + blk[k] * loc[k] + (k + 1 < rank ? idx[k] : 0);
+        std::memcpy(host.data() + r * run * eb, data.data() + off * eb,
+                    static_cast<size_t>(run * eb));
+        for (size_t k = rank - 1; k-- > 0;) {  // next run: odometer over the leading dims
+          if (++idx[k] < loc[k]) break;
+          idx[k] = 0;
         }
       }
-      const int64_t lr = rows / cnt[0], lc = cols / cnt[1];
-      std::vector<char> host(static_cast<size_t>(lr * lc * eb));
-      for (int64_t r = 0; r < lr; ++r)
-        std::memcpy(host.data() + r * lc * eb,
-                    data.data() + ((blk[0] * lr + r) * cols + blk[1] * lc) * eb,
-                    static_cast<size_t>(lc * eb));
       void* dptr = nullptr;
-      cudaMalloc(&dptr, host.size());
+      cudaMalloc(&dptr, host.size() < 256 ? 256 : host.size());
       cudaMemcpy(dptr, host.data(), host.size(), cudaMemcpyHostToDevice);
       owned.push_back(dptr);
       shards.push_back(dptr);

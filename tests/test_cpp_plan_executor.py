@@ -59,3 +59,42 @@ def test_native_executor_matches_python_executor(cuda, tmp_path, name):
     assert out.view(torch.int16).cpu().numpy().tobytes() == native
     ref = torch.nn.functional.gelu(feeds["x"].float() @ feeds["w1"].float()) @ feeds["w2"].float()
     assert ((out.double() - ref.double()).abs().max() / ref.abs().max()).item() <= 2e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["gpt_block_b8s1024_mesh8_unlimited.json",
+                                  "gpt_block_b4s1024_mesh2x4_unlimited.json",
+                                  "gpt_block_b8s1024_mesh2x2x2_unlimited.json",
+                                  "gpt_block_b1s4096_mesh2x2x2_unlimited.json"])
+def test_native_executor_runs_block_plans(cuda, tmp_path, name):
+    """The transformer block (embedding, layernorm, batched matmul, softmax,
+    the fused attention chain and owner-block table reads) from the native
+    executor: the same bytes as the Python executor."""
+    import sys
+
+    import torch
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from test_gpu_block import _operands
+
+    from paper_2302_02599_b200.executor import PlanExecutor
+    from paper_2302_02599_b200.runtime import Mesh
+
+    exe = build(tmp_path)
+    tag = name.split("_mesh")[0]
+    graph_path = PLANS / f"{tag}_graph.json"
+    graph = json.loads(graph_path.read_text())
+    feeds = _operands(graph)
+    for k, v in feeds.items():
+        (tmp_path / f"{k}.bin").write_bytes(v.contiguous().view(torch.uint8).cpu().numpy()
+                                            .tobytes())
+    plan = json.loads((PLANS / name).read_text())
+    mesh_arg = "x".join(map(str, plan["mesh"]["shape"]))
+    r = subprocess.run([str(exe), str(graph_path), str(PLANS / name), mesh_arg, str(tmp_path)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    native = (tmp_path / "out.bin").read_bytes()
+    ex = PlanExecutor(Mesh.local(plan["mesh"]["shape"]), graph, plan)
+    out = ex.forward(feeds)[0]
+    torch.cuda.synchronize()
+    assert out.contiguous().view(torch.uint8).cpu().numpy().tobytes() == native
