@@ -302,6 +302,13 @@ class PlanExecutor:
             return alloc(shape, dtype)
         return torch.empty(shape, dtype=dtype, device=device)
 
+    def _zeros(self, shape, device) -> torch.Tensor:
+        """fp32 accumulator from the mesh's allocator (the peer runtime's
+        all-reduce reads and writes its buffers in the symmetric heap)."""
+        t = self._empty(tuple(shape), torch.float32, device)
+        t.zero_()
+        return t
+
     def _alloc(self, nid: str, spec: ShardingSpec, like: torch.Tensor) -> list:
         shape = spec.local_shape(self._meta(nid), self.geo)
         return [self._empty(shape, like.dtype, like.device) for _ in range(self.mesh.num_local)]
@@ -779,9 +786,8 @@ class PlanExecutor:
             gamma = aff[0] if aff else [None] * len(x)
             dx = like(dy)
             h = x[0].shape[-1]
-            dg = [torch.zeros(h, dtype=torch.float32, device=t.device) for t in x] if aff else None
-            db = ([torch.zeros(h, dtype=torch.float32, device=t.device) for t in x]
-                  if len(aff) > 1 else None)
+            dg = [self._zeros((h,), t.device) for t in x] if aff else None
+            db = [self._zeros((h,), t.device) for t in x] if len(aff) > 1 else None
             for i, (xx, gg, g, o) in enumerate(zip(x, gamma, dy, dx)):
                 B.layernorm_backward(xx, gg, g, o, dg[i] if dg else None, db[i] if db else None,
                                      stream=stream)
@@ -802,7 +808,7 @@ class PlanExecutor:
                 out.append((1, self._embedding_grad_owned(nid, ids, dy, tplan, stream), tplan))
             elif wants_grad(ins[1]):
                 shape = tspec.local_shape(self._meta(ins[1]), self.geo)
-                dt = [torch.zeros(shape, dtype=torch.float32, device=g.device) for g in dy]
+                dt = [self._zeros(shape, g.device) for g in dy]
                 for i, g, o in zip(ids, dy, dt):
                     B.embedding_backward(i, g, o, stream=stream)
                 id_axes = sorted({a for d in self.required_spec(nid, 0).dims for a in d.axes})
@@ -855,7 +861,7 @@ class PlanExecutor:
         for d in range(self.mesh.num_local):
             iv, nv = self._block_index(tplan.dims[0], d)
             ih, nh = self._block_index(tplan.dims[1], d)
-            blk = torch.zeros(vocab // nv, width // nh, dtype=torch.float32, device=dy[0].device)
+            blk = self._zeros((vocab // nv, width // nh), dy[0].device)
             B.embedding_backward_block(src_ids, src_dy, blk, iv * (vocab // nv),
                                        ih * (width // nh), stream=stream)
             outs.append(blk)
