@@ -197,6 +197,11 @@ _CACHE = {}
 def _case(tag):
     if tag not in _CACHE:
         graph = json.loads((PLANS / f"gpt_block_{tag}_graph.json").read_text())
+        if tag == "fixture":  # the reference's own fp32 [4,16,64] block, run in bf16
+            for n in graph["nodes"]:
+                for o in n["outputs"]:
+                    if o["dtype_bytes"] == 4:
+                        o["dtype_bytes"] = 2
         p = _operands(graph)
         _CACHE.clear()
         _CACHE[tag] = (graph, p, block_reference(p))
@@ -204,9 +209,12 @@ def _case(tag):
 
 
 BLOCK_PLANS = sorted(p.name for p in PLANS.glob("gpt_block_b*_mesh*.json"))
+# the reference fixture's own plans: ragged tiny shards (2-row GEMMs, 8-wide
+# softmax rows, split-bm / split-bn / emb-h forms) on the same code path
+FIXTURE_PLANS = sorted(p.name for p in PLANS.glob("gpt_block_fixture_mesh*.json"))
 
 
-@pytest.mark.parametrize("name", BLOCK_PLANS)
+@pytest.mark.parametrize("name", BLOCK_PLANS + FIXTURE_PLANS)
 @pytest.mark.parametrize("fuse", [True, False])
 def test_block_plans_execute(cuda, name, fuse):
     graph, feeds, ref = _case(name.split("_mesh")[0].removeprefix("gpt_block_"))
@@ -366,7 +374,7 @@ def _reference_grads(tag):
     return _GRAD_CACHE[tag]
 
 
-@pytest.mark.parametrize("name", BLOCK_PLANS)
+@pytest.mark.parametrize("name", BLOCK_PLANS + FIXTURE_PLANS)
 def test_block_plans_backward(cuda, name):
     """Training step of the block under each reference plan: every
     parameter's gradient (in its plan layout, gathered here for the check)
