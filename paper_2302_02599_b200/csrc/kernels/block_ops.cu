@@ -102,20 +102,25 @@ __global__ void __launch_bounds__(256) embedding_blocks_kernel(
     const int64_t* __restrict__ ids, int64_t n, const __grid_constant__ TableBlocks blocks,
     int hidden_blocks, int64_t vb_rows, int64_t hb_words, int64_t vocab, int64_t col0,
     int64_t out_words, W* __restrict__ out) {
-  const int64_t total = n * out_words;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += stride) {
-    const int64_t t = i / out_words, w = i - t * out_words;
+  // a warp per id: the owner block row is found once, then the output row is
+  // copied run by run (one run per hidden block it spans), no per-word division
+  const int lane = threadIdx.x % 32;
+  for (int64_t t = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    W* orow = out + t * out_words;
     const int64_t id = __ldg(ids + t);
-    W v{};
-    if (id >= 0 && id < vocab) {
-      const int64_t col = col0 + w;
-      const int64_t vb = id / vb_rows, hb = col / hb_words;
-      const W* blk = static_cast<const W*>(blocks.p[vb * hidden_blocks + hb]);
-      v = blk[(id - vb * vb_rows) * hb_words + (col - hb * hb_words)];
+    if (id < 0 || id >= vocab) {
+      for (int64_t w = lane; w < out_words; w += 32) orow[w] = W{};
+      continue;
     }
-    out[i] = v;
+    const int64_t vb = id / vb_rows, r = id - vb * vb_rows;
+    for (int64_t w = 0; w < out_words;) {
+      const int64_t col = col0 + w, hb = col / hb_words, off = col - hb * hb_words;
+      const int64_t len = min(hb_words - off, out_words - w);
+      const W* src = static_cast<const W*>(blocks.p[vb * hidden_blocks + hb]) + r * hb_words + off;
+      for (int64_t k = lane; k < len; k += 32) orow[w + k] = src[k];
+      w += len;
+    }
   }
 }
 
@@ -727,27 +732,27 @@ cudaError_t launch_embedding_blocks(const int64_t* ids, int64_t n, const void* c
   while (wb > 1 && ((hb | c0 | nc) % wb || align % wb)) wb >>= 1;
   switch (wb) {
     case 16:
-      embedding_blocks_kernel<uint4><<<grid_for(n * nc / 16), 256, 0, s>>>(
+      embedding_blocks_kernel<uint4><<<grid_for(n * 32), 256, 0, s>>>(
           ids, n, tb, hidden_blocks, vb_rows, hb / 16, vocab, c0 / 16, nc / 16,
           static_cast<uint4*>(out));
       break;
     case 8:
-      embedding_blocks_kernel<uint2><<<grid_for(n * nc / 8), 256, 0, s>>>(
+      embedding_blocks_kernel<uint2><<<grid_for(n * 32), 256, 0, s>>>(
           ids, n, tb, hidden_blocks, vb_rows, hb / 8, vocab, c0 / 8, nc / 8,
           static_cast<uint2*>(out));
       break;
     case 4:
-      embedding_blocks_kernel<uint32_t><<<grid_for(n * nc / 4), 256, 0, s>>>(
+      embedding_blocks_kernel<uint32_t><<<grid_for(n * 32), 256, 0, s>>>(
           ids, n, tb, hidden_blocks, vb_rows, hb / 4, vocab, c0 / 4, nc / 4,
           static_cast<uint32_t*>(out));
       break;
     case 2:
-      embedding_blocks_kernel<uint16_t><<<grid_for(n * nc / 2), 256, 0, s>>>(
+      embedding_blocks_kernel<uint16_t><<<grid_for(n * 32), 256, 0, s>>>(
           ids, n, tb, hidden_blocks, vb_rows, hb / 2, vocab, c0 / 2, nc / 2,
           static_cast<uint16_t*>(out));
       break;
     default:
-      embedding_blocks_kernel<uint8_t><<<grid_for(n * nc), 256, 0, s>>>(
+      embedding_blocks_kernel<uint8_t><<<grid_for(n * 32), 256, 0, s>>>(
           ids, n, tb, hidden_blocks, vb_rows, hb, vocab, c0, nc, static_cast<uint8_t*>(out));
       break;
   }
