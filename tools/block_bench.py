@@ -6,7 +6,7 @@ one CUDA graph per forward. The 1-device plan (everything replicated, no
 communication) is the dense baseline: the gap to it is what the plan's
 conversions and the extra replicated work cost.
 
-    python tools/block_bench.py [--quick]
+    python tools/block_bench.py [--quick] [--fuse-gather]   # weight all-gathers fused into GEMMs
     python tools/block_bench.py --once gpt_block_b8s1024_mesh8_unlimited   # ncu target
     python tools/block_bench.py --once-train gpt_block_b8s1024_mesh8_unlimited
 
@@ -118,7 +118,8 @@ def main():
             for x in shape:
                 ndev *= x
             for fuse in ((True,) if ndev == 1 else (True, False)):
-                ex = PlanExecutor(mesh, graph, plan, fuse=fuse)
+                ex = PlanExecutor(mesh, graph, plan, fuse=fuse,
+                                  fuse_gather=True if "--fuse-gather" in sys.argv else None)
                 ms, launches = time_forward(ex, feeds, iters)
                 row = {"graph": tag, "plan": name, "devices": ndev, "fuse": fuse,
                        "ms_per_forward": round(ms, 4), "kernel_launches": launches,
