@@ -272,19 +272,24 @@ namespace {
 //   1: U=4  @ 4 CTAs/SM   -- plain contiguous runs (r01 sweep: 96% of copy peak)
 //   2: U=16 @ 1 CTA/SM    -- fan-out tables (one load, many stores: 92%)
 //   3: U=8  @ 3 CTAs/SM   -- strided boxes (all-to-all packs: 80%)
-// The launch picks by table shape (profiles/r01_copy_sweep.md);
+// The launch picks by table shape (profiles/r01_copy_sweep.md) and size;
 // APL_COPY_VARIANT forces one, APL_COPY_CTAS_PER_SM overrides the grid.
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
 }
 
-int copy_variant(int max_outer, int max_fan) {
+// Launch-bound regime (r01 crossover probe, profiles/r01_crossover.jsonl):
+// below 8 MiB read by a fan-out gather, or 64 MiB moved by a strided table,
+// U=4 @ 4 CTAs/SM finishes first (AG fan-out of 1 MiB: 4.6 vs 12.4 us;
+// 256 B-run all-to-all of 16 MiB: 8.3 vs 9.2 us); the wide variants only pay
+// off once the launch streams.
+int copy_variant(int max_outer, int max_fan, int64_t write_bytes) {
   static int forced = env_int("APL_COPY_VARIANT", -1);
   if (forced >= 0) return forced;
-  if (max_fan > 1) return 2;
+  if (max_fan > 1) return write_bytes / max_fan < (int64_t{8} << 20) ? 1 : 2;
   if (max_outer == 0) return 1;
-  return 3;
+  return write_bytes < (int64_t{64} << 20) ? 1 : 3;
 }
 
 template <int V, int U, int MINB, bool SPLIT = false>
@@ -349,7 +354,7 @@ void launch_v(int no, int fan, bool split, int64_t total_units, const DevCopy* t
   // not cost the common kernels registers (U=8 @ 2 CTAs/SM: no spills).
   if (split) return launch_vu<V, 8, 2, true>(no, total_units, t, begins, n, p, s, lock, streaming, spanning);
   if constexpr (V == 16) {
-    switch (copy_variant(no, fan)) {
+    switch (copy_variant(no, fan, wbytes)) {
       case 1:
         return launch_vu<V, 4, 4>(no, total_units, t, begins, n, p, s, lock, streaming, spanning);
       case 2:

@@ -149,6 +149,10 @@ int copy_engine_forced() {  // APL_COPY_ENGINE = ldg | bulk | tile, unset = auto
 
 // The tile engine's place in the automatic policy (APL_TILE_AUTO=0 keeps
 // short strided rows on the LDG engine).
+constexpr int64_t kSmallCopyBytes = int64_t{8} << 20;   // below: LDG small-launch variant
+constexpr int64_t kFanRingMaxBytes = int64_t{64} << 20;  // fan-out gathers on the ring below
+constexpr int64_t kTileMinBytes = int64_t{64} << 20;     // TMA tensor tiles from
+
 bool tile_auto_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("APL_TILE_AUTO");
@@ -158,6 +162,12 @@ bool tile_auto_enabled() {
 }
 
 }  // namespace
+
+int64_t copy_read_bytes(const std::vector<CopyDesc>& descs) {
+  int64_t r = 0;
+  for (const CopyDesc& d : descs) r += d.bytes();
+  return r;
+}
 
 bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec) {
   const int forced = copy_engine_forced();
@@ -174,7 +184,14 @@ bool bulk_eligible(const std::vector<CopyDesc>& descs, int vec) {
   // r01 sweep (profiles/r01_copy_engines.md): the TMA ring wins on strided
   // rows (all-to-all packs: 97% vs 80% of copy peak); the LDG kernel keeps
   // plain contiguous copies (95% vs 94%) and fan-out gathers (90% vs 89%).
-  return strided && !fan;
+  // By size (profiles/r01_crossover.jsonl): under 8 MiB read the LDG kernel's
+  // small-launch variant finishes first (4 MiB 2 KiB-row all-to-all: 4.2 vs
+  // 5.8 us); fan-out gathers of 8-64 MiB run faster on the ring (16 MiB
+  // all-gather: 24.6 vs 30.6 us; equal at 64 MiB).
+  const int64_t r = copy_read_bytes(descs);
+  if (r < kSmallCopyBytes) return false;
+  if (fan) return !strided && r < kFanRingMaxBytes;
+  return strided;
 }
 
 namespace {
@@ -294,6 +311,10 @@ bool tile_eligible(const std::vector<CopyDesc>& descs, int vec) {
         return false;
     }
   }
+  // under 64 MiB the tiles' fixed cost (~12 us: tensor-map fetches, ring
+  // ramp) loses to the LDG kernel's small-launch variant (16 MiB 256 B-run
+  // all-to-all: 8.3 vs 13.8 us; profiles/r01_crossover.jsonl)
+  if (forced != 2 && copy_read_bytes(descs) < kTileMinBytes) return false;
   return forced == 2 || tile_auto_enabled();
 }
 

@@ -211,17 +211,20 @@ def test_partial_sum_all_reduce(cuda, dtype, code):
 # over slices of the table: 16-device all-to-alls have 256 pieces. The
 # column count picks the engine through the run length (2 KiB rows: TMA bulk
 # ring; 256 B: TMA tensor tiles; 32 B: LDG).
-@pytest.mark.parametrize("cols,engine", [(16384, "bulk"), (2048, "tile"), (256, "ldg")])
-def test_many_descriptor_tables_span_launches(cuda, cols, engine):
+# The engines also switch by size (8 MiB: bulk ring; 64 MiB: tensor tiles;
+# below, the LDG kernel's small-launch variant), so the tile case is 64 MiB.
+@pytest.mark.parametrize("rows,cols,engine", [(256, 16384, "bulk"), (16384, 2048, "tile"),
+                                              (256, 2048, "ldg"), (256, 256, "ldg")])
+def test_many_descriptor_tables_span_launches(cuda, rows, cols, engine):
     import os
 
     mesh = Mesh.local([16])
-    meta = TensorMeta((256, cols), 2)
+    meta = TensorMeta((rows, cols), 2)
     s, t = ShardingSpec.parse("S0R", 1), ShardingSpec.parse("RS0", 1)
     if "APL_COPY_ENGINE" not in os.environ and "APL_TILE_AUTO" not in os.environ:
         assert mesh.exchange_engine(s, t, meta) == engine
-    check_conversion([16], (256, cols), 2, "S0R", "RS0", True)
-    check_conversion([4, 4], (256, cols), 2, "S01R", "RS10", True)
+    check_conversion([16], (rows, cols), 2, "S0R", "RS0", True)
+    check_conversion([4, 4], (rows, cols), 2, "S01R", "RS10", True)
 
 
 # BASELINE config 2 at full size (1 GiB and 4 GiB bf16 on [8]) -- too big for

@@ -5,7 +5,7 @@ conversion (S0R->S0R: a plain copy through the box-copy machinery), the
 all-to-all S0R->RS0, and the BASELINE config-3/4 conversions at 128 MiB.
 Device time of 10 back-to-back calls captured in a CUDA graph.
 
-    APL_COPY_ENGINE=ldg|bulk python tools/size_probe.py
+    APL_COPY_ENGINE=ldg|bulk python tools/size_probe.py [--quick | --small]
 """
 import json
 import os
@@ -86,6 +86,20 @@ def main():
     eng = os.environ.get("APL_COPY_ENGINE", "auto")
     quick = "--quick" in sys.argv
     tag = os.environ.get("PROBE_TAG", "")
+    small = "--small" in sys.argv  # launch-bound regime: the block / MLP plans' conversions
+    if small:
+        for kib in (256, 1024, 4096, 16384):
+            n = kib << 9
+            x = torch.empty(n, dtype=torch.int16, device="cuda")
+            y = torch.empty_like(x)
+            ms = graph_ms(lambda st: y.copy_(x))
+            print(json.dumps({"case": f"torch copy_ {kib} KiB", "us": round(ms * 1e3, 2)}),
+                  flush=True)
+            rows = (kib << 10) // (2 * 1024)
+            for a, t in (("S0R", "RR"), ("S0R", "RS0"), ("S0R", "S0R")):
+                r = conv_row([8], (rows, 1024), 2, a, t, peak)
+                print(json.dumps(r), flush=True)
+        return
     for mib in ((128, 1024) if quick else (32, 64, 128, 256, 512, 1024)):
         n = mib << 19  # bf16 elements
         x = torch.empty(n, dtype=torch.int16, device="cuda")
