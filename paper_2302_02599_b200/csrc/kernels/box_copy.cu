@@ -271,7 +271,8 @@ namespace {
 //   0: U=8  @ 2 CTAs/SM (128 regs, no spills)
 //   1: U=4  @ 4 CTAs/SM   -- plain contiguous runs (r01 sweep: 96% of copy peak)
 //   2: U=16 @ 1 CTA/SM    -- fan-out tables (one load, many stores: 92%)
-//   3: U=8  @ 3 CTAs/SM   -- strided boxes (all-to-all packs: 80%)
+//   3: U=8  @ 3 CTAs/SM   -- strided boxes (the r01 copy sweep's pick; variant 1
+//                            measured ahead of it at every size since)
 // The launch picks by table shape (profiles/r01_copy_sweep.md) and size;
 // APL_COPY_VARIANT forces one, APL_COPY_CTAS_PER_SM overrides the grid.
 int env_int(const char* name, int dflt) {
@@ -284,12 +285,15 @@ int env_int(const char* name, int dflt) {
 // U=4 @ 4 CTAs/SM finishes first (AG fan-out of 1 MiB: 4.6 vs 12.4 us;
 // 256 B-run all-to-all of 16 MiB: 8.3 vs 9.2 us); the wide variants only pay
 // off once the launch streams.
+// Strided tables: U=4 @ 4 CTAs/SM as well (r01 short-row probe: 0.92 vs
+// 0.85 for U=8 @ 3 on 256 B rows at 512 MiB, ahead at every size measured,
+// profiles/r01_short_row_probe.jsonl); U=8 @ 3 stays selectable (variant 3).
 int copy_variant(int max_outer, int max_fan, int64_t write_bytes) {
   static int forced = env_int("APL_COPY_VARIANT", -1);
   if (forced >= 0) return forced;
   if (max_fan > 1) return write_bytes / max_fan < (int64_t{8} << 20) ? 1 : 2;
-  if (max_outer == 0) return 1;
-  return write_bytes < (int64_t{64} << 20) ? 1 : 3;
+  (void)max_outer;
+  return 1;
 }
 
 template <int V, int U, int MINB, bool SPLIT = false>

@@ -147,16 +147,20 @@ int copy_engine_forced() {  // APL_COPY_ENGINE = ldg | bulk | tile, unset = auto
   return forced;
 }
 
-// The tile engine's place in the automatic policy (APL_TILE_AUTO=0 keeps
-// short strided rows on the LDG engine).
 constexpr int64_t kSmallCopyBytes = int64_t{8} << 20;   // below: LDG small-launch variant
 constexpr int64_t kFanRingMaxBytes = int64_t{64} << 20;  // fan-out gathers on the ring below
-constexpr int64_t kTileMinBytes = int64_t{64} << 20;     // TMA tensor tiles from
+constexpr int64_t kTileMinBytes = int64_t{64} << 20;     // TMA tensor tiles from (when on)
 
+// The tile engine's place in the automatic policy: off unless APL_TILE_AUTO=1.
+// r01 short-row probe (profiles/r01_short_row_probe.jsonl): for strided rows
+// of 64 B - 1 KiB the LDG kernel at U=4 @ 4 CTAs/SM matches the tensor tiles
+// at 128 MiB (0.84 vs 0.85) and beats them from 512 MiB (0.92 vs 0.88 at
+// 256 B rows; 0.81 vs 0.72 at 128 B) and on the rank-3 2x2x2 case (0.94 vs
+// 0.91). The engine stays available (APL_COPY_ENGINE=tile) and tested.
 bool tile_auto_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("APL_TILE_AUTO");
-    return e == nullptr || std::string(e) != "0";
+    return e != nullptr && std::string(e) == "1";
   }();
   return on;
 }

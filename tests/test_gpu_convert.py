@@ -211,9 +211,10 @@ def test_partial_sum_all_reduce(cuda, dtype, code):
 # over slices of the table: 16-device all-to-alls have 256 pieces. The
 # column count picks the engine through the run length (2 KiB rows: TMA bulk
 # ring; 256 B: TMA tensor tiles; 32 B: LDG).
-# The engines also switch by size (8 MiB: bulk ring; 64 MiB: tensor tiles;
-# below, the LDG kernel's small-launch variant), so the tile case is 64 MiB.
-@pytest.mark.parametrize("rows,cols,engine", [(256, 16384, "bulk"), (16384, 2048, "tile"),
+# The engines also switch by size (8 MiB: bulk ring; below, the LDG kernel's
+# small-launch variant); short strided rows stay on LDG (the tensor-tile
+# engine is opt-in, test_tile_engine_forced_parity runs it).
+@pytest.mark.parametrize("rows,cols,engine", [(256, 16384, "bulk"), (16384, 2048, "ldg"),
                                               (256, 2048, "ldg"), (256, 256, "ldg")])
 def test_many_descriptor_tables_span_launches(cuda, rows, cols, engine):
     import os
@@ -260,3 +261,21 @@ def test_config2_full_size_properties(cuda, gib):
         torch.cuda.synchronize()
         for d in range(8):
             assert torch.equal(ag[d], full), d
+
+
+@pytest.mark.parametrize("engine", ["tile", "bulk", "ldg"])
+def test_engine_forced_parity(cuda, engine):
+    """Every copy engine, forced for a whole process (the policy is read once
+    per process), passes this module's parity tests: the TMA tensor-tile
+    engine is opt-in in the automatic policy, so this is where it runs."""
+    import os
+    import subprocess
+    import sys
+
+    if os.environ.get("APL_COPY_ENGINE"):
+        pytest.skip("already running under a forced engine")
+    env = dict(os.environ, APL_COPY_ENGINE=engine)
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-m", "gpu",
+                        "-k", "not engine_forced_parity and not full_size"],
+                       env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
