@@ -76,3 +76,36 @@ def test_runtime_refuses_without_gpu_instead_of_falling_back():
     h = C.c_void_p()
     rc = lib.apl_mesh_create_local(C.byref(L.DeviceMesh.uniform([2, 2]).c()), 0, C.byref(h))
     assert rc in (A.ERR_CUDA, A.ERR_ARG)
+
+
+def test_block_entry_points_validate_arguments_without_a_gpu():
+    """The transformer-block entry points reject bad arguments with
+    APL_ERR_ARG before touching the device (host-side validation)."""
+    lib = A.lib()
+    P = C.c_void_p
+    one = P(16)  # never dereferenced: validation fails first
+    err = A.ERR_ARG
+    assert lib.apl_layernorm(one, None, None, one, 4, 8, 1e-5, 7, None) == err  # dtype
+    assert lib.apl_layernorm(one, None, None, one, 4, 0, 1e-5, A.BF16, None) == err  # width
+    assert lib.apl_softmax_ex(one, one, 4, 0, 1.0, None, 0.0, A.BF16, None) == err
+    assert lib.apl_transpose(one, one, 1, 4, 4, 2, None) == err  # in place
+    assert lib.apl_transpose(one, P(32), 1, 4, 4, 3, None) == err  # element size
+    assert lib.apl_embedding_lookup(one, 4, one, 10, 8, 3, one, None) == err
+    blocks = (P * 65)(*([16] * 65))
+    assert lib.apl_embedding_lookup_blocks(one, 4, blocks, 65, 1, 65, 8, 0, 8, 2, one,
+                                           None) == err  # > 64 blocks
+    assert lib.apl_embedding_lookup_blocks(one, 4, blocks, 2, 1, 65, 8, 0, 8, 2, one,
+                                           None) == err  # vocab not divisible
+    assert lib.apl_embedding_lookup_blocks(one, 4, blocks, 1, 1, 64, 8, 4, 8, 2, one,
+                                           None) == err  # slice outside the table
+    assert lib.apl_layernorm_backward(one, None, one, one, P(16), None, None, 4, 8, 1e-5,
+                                      A.BF16, None) == err  # dgamma without stats scratch
+    ptrs = (P * 1)(16)
+    assert lib.apl_gemm_bf16_grouped_ex(ptrs, ptrs, ptrs, 1, 8, 8, 8, 4, 8, 8, 0, 1, A.BF16,
+                                        None) == err  # lda < K (A as [M, K])
+    assert lib.apl_gemm_bf16_grouped_ex(ptrs, ptrs, ptrs, 1, 8, 8, 8, 8, 8, 8, 5, 1, A.BF16,
+                                        None) == err  # A layout
+    for fn in ("apl_layernorm", "apl_softmax_ex", "apl_embedding_lookup_blocks",
+               "apl_gemm_bf16_grouped_ex"):
+        assert hasattr(lib, fn)
+    assert lib.apl_last_error()  # a message is recorded
