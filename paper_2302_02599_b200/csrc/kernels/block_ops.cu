@@ -350,7 +350,8 @@ __global__ void __launch_bounds__(256) softmax_cached_kernel(const T* __restrict
 
 // ---- backward ---------------------------------------------------------------
 // layernorm: dx = rstd * (g.dy - mean(g.dy) - xhat * mean(g.dy.xhat)), warp per
-// row (mean / rstd recomputed from x, kept per row for the column pass);
+// row: one pass for the four row sums (mean / rstd recomputed from x, kept per
+// row for the column pass), one for dx;
 // dgamma += sum_rows dy.xhat, dbeta += sum_rows dy in a second, column pass.
 template <typename T, int V>
 __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
@@ -363,23 +364,9 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
        r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
     const T* xr = x + r * width;
     const T* gr = dy + r * width;
-    float s = 0.f;
-    for (int64_t i = lane; i < nv; i += 32) {
-      float f[V];
-      load_row<T, V>(xr, i, f);
-#pragma unroll
-      for (int k = 0; k < V; ++k) s += f[k];
-    }
-    const float mean = warp_sum(s) * inv_w;
-    float q = 0.f;
-    for (int64_t i = lane; i < nv; i += 32) {
-      float f[V];
-      load_row<T, V>(xr, i, f);
-#pragma unroll
-      for (int k = 0; k < V; ++k) q += (f[k] - mean) * (f[k] - mean);
-    }
-    const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
-    float a = 0.f, b = 0.f;  // sum g.dy, sum g.dy.xhat
+    // one pass over (x, dy) for all four row sums: sum x, sum x^2, sum g.dy,
+    // sum g.dy.x (mean / var / the two projections follow from them)
+    float sx = 0.f, sxx = 0.f, sa = 0.f, sax = 0.f;
     for (int64_t i = lane; i < nv; i += 32) {
       float f[V], d[V], g[V];
       load_row<T, V>(xr, i, f);
@@ -388,12 +375,17 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
 #pragma unroll
       for (int k = 0; k < V; ++k) {
         const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
-        a += gd;
-        b += gd * (f[k] - mean) * rstd;
+        sx += f[k];
+        sxx += f[k] * f[k];
+        sa += gd;
+        sax += gd * f[k];
       }
     }
-    a = warp_sum(a) * inv_w;
-    b = warp_sum(b) * inv_w;
+    const float mean = warp_sum(sx) * inv_w;
+    const float var = fmaxf(warp_sum(sxx) * inv_w - mean * mean, 0.f);
+    const float rstd = rsqrtf(var + eps);
+    const float a = warp_sum(sa) * inv_w;
+    const float b = rstd * (warp_sum(sax) * inv_w - mean * a);  // mean(g.dy.xhat)
     for (int64_t i = lane; i < nv; i += 32) {
       float f[V], d[V], g[V];
       load_row<T, V>(xr, i, f);
@@ -873,8 +865,8 @@ cudaError_t layernorm_bwd_typed(const void* x, const void* gamma, const void* dy
   auto G = static_cast<const T*>(gamma);
   auto D = static_cast<const T*>(dy);
   auto O = static_cast<T*>(dx);
-  // (a register-cached variant measured slower here: 0.54 vs 0.63 of the
-  // HBM roofline at 131072 x 1024 -- its occupancy halves)
+  // (a register-cached variant measured slower: 0.54 vs 0.63 of the HBM
+  // roofline at 131072 x 1024 -- its occupancy halves)
   if (vec) layernorm_bwd_kernel<T, V><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
   else layernorm_bwd_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
   g_launches.fetch_add(1, std::memory_order_relaxed);
