@@ -31,6 +31,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <nlohmann/json.hpp>
@@ -44,6 +45,8 @@
 namespace autoplan {
 
 class PlanExecutor {
+  struct Node;
+
  public:
   PlanExecutor(MeshRuntime& rt, const DeviceMesh& mesh, const std::string& graph_json,
                const std::string& plan_json, bool fuse_chain = true)
@@ -148,8 +151,14 @@ class PlanExecutor {
   // pointer per local device) in the node's plan spec. Returns the output's
   // local shards (replicated), owned by the executor, valid until the next
   // forward. Stream-ordered on `stream` (a cudaStream_t).
+  // train = true keeps what backward() reads (the Python executor's rule:
+  // matmul / batched-matmul / layernorm operands as consumed, GELU
+  // pre-activations -- a fused GELU's epilogue stores it -- softmax outputs,
+  // embedding ids) and runs the attention chain unfused.
   std::vector<void*> forward(const std::map<std::string, std::vector<const void*>>& feeds,
-                             void* stream) {
+                             void* stream, bool train = false) {
+    saved_.clear();
+    trained_ = train;
     std::map<std::string, std::vector<const void*>> values;
     std::map<std::string, std::vector<const void*>> converted;
     std::set<std::string> fused;
@@ -163,8 +172,8 @@ class PlanExecutor {
         values[id] = f;
         continue;
       }
-      if (attn_members_.count(id)) continue;  // inside the fused softmax below
-      if (auto ch = attn_.find(id); ch != attn_.end()) {
+      if (!train && attn_members_.count(id)) continue;  // inside the fused softmax below
+      if (auto ch = attn_.find(id); !train && ch != attn_.end()) {
         auto out = buffers(id, nd.spec, nd.meta);
         const auto& x = values.at(ch->second.x);
         const auto& m = values.at(ch->second.mask);
@@ -203,10 +212,19 @@ class PlanExecutor {
         for (size_t i = 0; i < st.reduce_axes.size(); ++i) c.reduce_axes[i] = st.reduce_axes[i];
         const apl_meta am = apl_detail::to_c(nodes_.at(nd.inputs[0]).meta);
         const apl_meta bm = apl_detail::to_c(nodes_.at(nd.inputs[1]).meta);
+        std::vector<void*> pre;
+        if (train) {
+          saved_[id] = {ins[0], ins[1]};
+          if (!gelu.empty()) {  // one pass writes GELU(acc) and keeps acc for backward
+            pre = buffers(id + ".pre", nd.spec, nd.meta);
+            saved_[gelu] = {as_const(pre)};
+          }
+        }
         apl_detail::check(apl_sharded_matmul_ex(
             rt_.get(), &c, &am, &bm, ins[0].data(), ins[1].data(), out.data(), APL_B_KN,
             nd.meta.dtype_bytes == 4 ? APL_F32 : APL_BF16,
-            gelu.empty() ? APL_EPI_NONE : APL_EPI_GELU, nullptr, stream));
+            gelu.empty() ? APL_EPI_NONE : (pre.empty() ? APL_EPI_GELU : APL_EPI_GELU_SAVE),
+            pre.empty() ? nullptr : pre.data(), stream));
         if (!gelu.empty()) fused.insert(gelu);
         values[id] = as_const(out);
       } else if (nd.kind == "elementwise-unary") {
@@ -225,6 +243,7 @@ class PlanExecutor {
           else
             apl_detail::check(apl_mask_not(ins[0][d], out[d], count, stream));
         }
+        if (train && nd.unary == Unary::kGelu) saved_[id] = {ins[0]};  // the pre-activation
         values[id] = as_const(out);
       } else if (nd.kind == "output") {  // already collected to RR by the conversion above
         values[id] = ins[0];
@@ -234,14 +253,397 @@ class PlanExecutor {
         values[id] = ins[0];
       } else if (nd.kind == "embedding-lookup" && gather_t) {
         values[id] = lookup_gathered_table(nd, ins[0], values.at(nd.inputs[1]), stream);
+        if (train) saved_[id] = {ins[0]};
       } else {
         values[id] = block_node(nd, ins, stream);
+        if (train) {
+          if (nd.kind == "batched-matmul" || nd.kind == "layernorm") saved_[id] = ins;
+          else if (nd.kind == "embedding-lookup") saved_[id] = {ins[0]};
+          else if (nd.kind == "softmax") saved_[id] = {values[id]};
+        }
       }
     }
     return result;
   }
 
+  // Backward of the last forward(train = true): grad_out = the output's
+  // gradient, one bf16 RR shard per local device. Returns every parameter's
+  // gradient (fp32, in its plan spec), owned by the executor -- the
+  // Python PlanExecutor.backward algorithm step for step (same kernels, same
+  // order, same bytes): reverse graph walk, per-node input gradients in the
+  // layouts the strategy consumed, partial sums reduced where they are made,
+  // reverse conversions back to the producers' layouts, out-of-place sums for
+  // values with several consumers.
+  std::map<std::string, std::vector<void*>> backward(const std::vector<const void*>& grad_out,
+                                                     void* stream) {
+    if (!trained_) throw PlanError("backward() needs a preceding forward(train = true)");
+    if (static_cast<int>(grad_out.size()) != num_local_)
+      throw ShapeError("grad_out: expected one shard per local device");
+    gcount_ = 0;
+    const Node& out = nodes_.at(output_);
+    const std::string src = out.inputs.at(0);
+    std::map<std::string, Grad> grads;
+    grads[src] = convert_grad(src, Grad{grad_out, 2}, required_spec(out, 0), nodes_.at(src).spec,
+                              stream);
+    std::set<std::string> done;
+    auto wants = [&](const std::string& id) {
+      const std::string& k = nodes_.at(id).kind;
+      return k != "placeholder";  // parameters and every computed value
+    };
+    auto add = [&](const std::string& id, const Grad& g) {
+      auto it = grads.find(id);
+      if (it == grads.end()) {
+        grads[id] = g;
+        return;
+      }
+      if (it->second.eb != g.eb) throw PlanError(id + ": gradient dtypes differ");
+      const size_t count = static_cast<size_t>(numel(local_shape(nodes_.at(id).spec,
+                                                                 nodes_.at(id).meta)));
+      const size_t bytes = count * static_cast<size_t>(g.eb);
+      std::vector<const void*> sum;
+      for (int d = 0; d < num_local_; ++d) {
+        void* o = grad_buf(bytes);
+        apl_detail::check(apl_add(it->second.p[d], g.p[d], 0, o, count, 1.f,
+                                  g.eb == 4 ? APL_F32 : APL_BF16, stream));
+        sum.push_back(o);
+      }
+      it->second.p = sum;
+    };
+    for (auto r = order_.rbegin(); r != order_.rend(); ++r) {
+      const std::string& id = *r;
+      if (done.count(id) || !grads.count(id)) continue;
+      const Node& nd = nodes_.at(id);
+      const Grad dy = grads.at(id);
+      if (nd.kind == "matmul") {
+        const OpStrategy& st = nd.strategy;
+        const auto& sv = saved_.at(id);
+        const std::string a_src = nd.inputs[0], b_src = nd.inputs[1];
+        const Node& an = nodes_.at(a_src);
+        std::string a_target = a_src;
+        const std::vector<const void*>* aux = nullptr;
+        auto cons = consumers_.find(a_src);
+        if (an.kind == "elementwise-unary" && an.unary == Unary::kGelu &&
+            an.spec == st.input_specs[0] && cons != consumers_.end() &&
+            cons->second.size() == 1 && saved_.count(a_src)) {
+          aux = &saved_.at(a_src)[0];
+          a_target = an.inputs[0];
+          done.insert(a_src);
+        }
+        const bool need_a = wants(a_target), need_b = wants(b_src);
+        const TensorMeta& am = nodes_.at(a_src).meta;
+        const TensorMeta& bm = nodes_.at(b_src).meta;
+        std::vector<void*> ga, gb;
+        if (need_a)
+          for (int d = 0; d < num_local_; ++d)
+            ga.push_back(grad_buf(static_cast<size_t>(numel(local_shape(st.input_specs[0], am))) *
+                                  2));
+        if (need_b)
+          for (int d = 0; d < num_local_; ++d)
+            gb.push_back(grad_buf(static_cast<size_t>(numel(local_shape(st.input_specs[1], bm))) *
+                                  4));
+        if (need_a || need_b) {
+          apl_matmul_strategy c = to_c_strategy(st);
+          const apl_meta amc = apl_detail::to_c(am), bmc = apl_detail::to_c(bm);
+          apl_detail::check(apl_sharded_matmul_backward(
+              rt_.get(), &c, &amc, &bmc, sv[0].data(), sv[1].data(), dy.p.data(),
+              need_a ? ga.data() : nullptr, need_b ? gb.data() : nullptr, APL_B_KN,
+              aux ? APL_EPI_DGELU : APL_EPI_NONE, aux ? aux->data() : nullptr, APL_F32, stream));
+        }
+        if (need_a)
+          add(a_target, convert_grad(a_target, Grad{as_const(ga), 2}, st.input_specs[0],
+                                     nodes_.at(a_target).spec, stream));
+        if (need_b)
+          add(b_src, convert_grad(b_src, Grad{as_const(gb), 4}, st.input_specs[1],
+                                  nodes_.at(b_src).spec, stream));
+      } else if (nd.kind == "elementwise-unary" && nd.unary == Unary::kGelu) {
+        const std::string x = nd.inputs[0];
+        const auto& pre = saved_.at(id)[0];
+        const size_t count = static_cast<size_t>(numel(local_shape(nd.spec, nd.meta)));
+        std::vector<const void*> dx;
+        for (int d = 0; d < num_local_; ++d) {
+          void* o = grad_buf(count * 2);
+          apl_detail::check(apl_gelu_backward(dy.p[d], pre[d], o, count, APL_BF16, stream));
+          dx.push_back(o);
+        }
+        add(x, convert_grad(x, Grad{dx, 2}, nd.spec, nodes_.at(x).spec, stream));
+      } else if (nd.kind != "output" && nd.kind != "placeholder" && nd.kind != "parameter") {
+        for (auto& [slot, g, layout] : block_backward(nd, dy, wants, stream)) {
+          const std::string& in = nd.inputs[static_cast<size_t>(slot)];
+          add(in, convert_grad(in, g, layout, nodes_.at(in).spec, stream));
+        }
+      }
+    }
+    std::map<std::string, std::vector<void*>> result;
+    for (auto& [id, g] : grads)
+      if (nodes_.at(id).kind == "parameter") {
+        std::vector<void*> v;
+        for (const void* q : g.p) v.push_back(const_cast<void*>(q));
+        result[id] = v;
+      }
+    return result;
+  }
+
  private:
+  struct Grad {
+    std::vector<const void*> p;
+    int eb = 2;  // element bytes: 2 bf16 (activations), 4 fp32 (parameters)
+  };
+
+  static apl_matmul_strategy to_c_strategy(const OpStrategy& st) {
+    apl_matmul_strategy c{};
+    c.a = apl_detail::to_c(st.input_specs.at(0));
+    c.b = apl_detail::to_c(st.input_specs.at(1));
+    c.c = apl_detail::to_c(st.output_spec);
+    c.partial_sum = st.partial_sum ? 1 : 0;
+    c.nreduce = static_cast<int32_t>(st.reduce_axes.size());
+    for (size_t i = 0; i < st.reduce_axes.size(); ++i) c.reduce_axes[i] = st.reduce_axes[i];
+    return c;
+  }
+
+  // gradient scratch: one cached buffer per allocation index of a backward
+  // pass (the sequence repeats every step, so buffers are reused)
+  void* grad_buf(size_t bytes) {
+    const std::string key = "grad#" + std::to_string(gcount_++);
+    auto it = workspaces_.find(key);
+    if (it != workspaces_.end() && it->second.second >= bytes) return it->second.first;
+    if (it != workspaces_.end()) {
+      cudaFree(it->second.first);
+      workspaces_.erase(it);
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes < 256 ? 256 : bytes) != cudaSuccess)
+      throw RuntimeFailure(APL_ERR_CUDA, "cudaMalloc of a gradient buffer failed");
+    workspaces_.emplace(key, std::make_pair(p, bytes));
+    return p;
+  }
+
+  void* grad_zeros(size_t bytes, void* stream) {
+    void* p = grad_buf(bytes);
+    if (cudaMemsetAsync(p, 0, bytes, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+      throw RuntimeFailure(APL_ERR_CUDA, "memset of a gradient accumulator failed");
+    return p;
+  }
+
+  // A gradient held in `have` into `want`: the reverse conversion (a layout
+  // conversion is the identity on the global tensor; its adjoint is too).
+  Grad convert_grad(const std::string& id, const Grad& g, const ShardingSpec& have,
+                    const ShardingSpec& want, void* stream) {
+    if (have == want) return g;
+    TensorMeta m = nodes_.at(id).meta;
+    m.dtype_bytes = g.eb;
+    const TransformPath path = find_transform_path(have, want, mesh_, m);
+    const size_t out_b = static_cast<size_t>(want.per_device_bytes(m, mesh_));
+    std::vector<void*> out;
+    for (int d = 0; d < num_local_; ++d) out.push_back(grad_buf(out_b));
+    const size_t wsb = workspace_bytes(rt_, path, m, fuse_);
+    void* ws = grad_buf(wsb < 256 ? 256 : wsb);
+    execute(rt_, path, m, g.p.data(), out.data(), ws, wsb, fuse_, stream);
+    return Grad{as_const(out), g.eb};
+  }
+
+  struct SlotGrad {
+    int slot;
+    Grad g;
+    ShardingSpec layout;
+  };
+
+  // input gradients of one block node (PlanExecutor._block_backward)
+  template <typename Wants>
+  std::vector<SlotGrad> block_backward(const Node& nd, const Grad& dy, Wants wants,
+                                       void* stream) {
+    std::vector<SlotGrad> out;
+    const auto ls = local_shape(nd.spec, nd.meta);
+    const size_t count = static_cast<size_t>(numel(ls));
+    if (nd.kind == "reshape") {
+      out.push_back({0, dy, required_spec(nd, 0)});
+    } else if (nd.kind == "transpose") {
+      const size_t r = ls.size();
+      const int64_t rows = ls[r - 2], cols = ls[r - 1], batch = numel(ls) / (rows * cols);
+      std::vector<const void*> dx;
+      for (int d = 0; d < num_local_; ++d) {
+        void* o = grad_buf(count * 2);
+        apl_detail::check(apl_transpose(dy.p[d], o, batch, rows, cols, 2, stream));
+        dx.push_back(o);
+      }
+      out.push_back({0, Grad{dx, 2}, required_spec(nd, 0)});
+    } else if (nd.kind == "elementwise-unary") {
+      if (nd.unary == Unary::kScale && wants(nd.inputs[0])) {
+        std::vector<const void*> dx;
+        for (int d = 0; d < num_local_; ++d) {
+          void* o = grad_buf(count * 2);
+          apl_detail::check(apl_scale(dy.p[d], o, count, nd.alpha, APL_BF16, stream));
+          dx.push_back(o);
+        }
+        out.push_back({0, Grad{dx, 2}, required_spec(nd, 0)});
+      }
+    } else if (nd.kind == "elementwise-binary") {
+      for (int slot = 0; slot < 2; ++slot) {
+        const std::string& in = nd.inputs[static_cast<size_t>(slot)];
+        if (nodes_.at(in).meta.dtype_bytes != 1 && wants(in))
+          out.push_back({slot, dy, required_spec(nd, static_cast<size_t>(slot))});
+      }
+    } else if (nd.kind == "softmax") {
+      const auto& y = saved_.at(nd.id)[0];
+      const int64_t w = ls.back(), rows = numel(ls) / w;
+      std::vector<const void*> dx;
+      for (int d = 0; d < num_local_; ++d) {
+        void* o = grad_buf(count * 2);
+        apl_detail::check(apl_softmax_backward(y[d], dy.p[d], o, rows, w, 1.f, APL_BF16, stream));
+        dx.push_back(o);
+      }
+      out.push_back({0, Grad{dx, 2}, required_spec(nd, 0)});
+    } else if (nd.kind == "layernorm") {
+      const auto& sv = saved_.at(nd.id);
+      const int64_t h = ls.back(), rows = numel(ls) / h;
+      const bool has_g = sv.size() > 1, has_b = sv.size() > 2;
+      std::vector<const void*> dx;
+      std::vector<void*> dg, db;
+      for (int d = 0; d < num_local_; ++d) {
+        void* o = grad_buf(count * 2);
+        void* g = has_g ? grad_zeros(static_cast<size_t>(h) * 4, stream) : nullptr;
+        void* b = has_b ? grad_zeros(static_cast<size_t>(h) * 4, stream) : nullptr;
+        void* stats = has_g || has_b ? grad_buf(static_cast<size_t>(rows) * 8) : nullptr;
+        apl_detail::check(apl_layernorm_backward(sv[0][d], has_g ? sv[1][d] : nullptr, dy.p[d],
+                                                 o, static_cast<float*>(g),
+                                                 static_cast<float*>(b), stats, rows, h, 1e-5f,
+                                                 APL_BF16, stream));
+        dx.push_back(o);
+        if (has_g) dg.push_back(g);
+        if (has_b) db.push_back(b);
+      }
+      out.push_back({0, Grad{dx, 2}, required_spec(nd, 0)});
+      std::set<int> axes_set;
+      const ShardingSpec in0 = required_spec(nd, 0);
+      for (size_t k = 0; k + 1 < in0.dims.size(); ++k)
+        for (int a : in0.dims[k].axes) axes_set.insert(a);
+      std::vector<int32_t> axes(axes_set.begin(), axes_set.end());
+      for (int slot = 1; slot <= 2; ++slot) {
+        std::vector<void*>& pg = slot == 1 ? dg : db;
+        if (pg.empty() || !wants(nd.inputs[static_cast<size_t>(slot)])) continue;
+        if (!axes.empty())
+          apl_detail::check(apl_all_reduce(rt_.get(), axes.data(), static_cast<int>(axes.size()),
+                                           pg.data(), static_cast<size_t>(h), APL_F32, stream));
+        out.push_back({slot, Grad{as_const(pg), 4}, required_spec(nd, static_cast<size_t>(slot))});
+      }
+    } else if (nd.kind == "embedding-lookup") {
+      const auto& ids = saved_.at(nd.id)[0];
+      const std::string& tab = nd.inputs[1];
+      const ShardingSpec tspec = required_spec(nd, 1);
+      const ShardingSpec& tplan = nodes_.at(tab).spec;
+      const TensorMeta& tm = nodes_.at(tab).meta;
+      const int64_t n = numel(ls) / ls.back();
+      int nn = 0, first = 0, nl = 0, dist = 0;
+      apl_detail::check(apl_mesh_info(rt_.get(), &nn, &first, &nl, &dist));
+      if (wants(tab) && !dist && tspec.dims[1].replicated() && !(tplan == tspec)) {
+        // reduce-scatter fused: each owner block from every distinct id block
+        const ShardingSpec ispec = required_spec(nd, 0);
+        std::map<std::vector<int64_t>, int> srcs;
+        for (int d = 0; d < num_local_; ++d) {
+          std::vector<int64_t> key;
+          for (const auto& dim : ispec.dims) key.push_back(block_index(dim, d).first);
+          srcs.emplace(key, d);
+        }
+        std::vector<int> order;
+        for (auto& [k, d] : srcs) order.push_back(d);
+        std::sort(order.begin(), order.end());
+        std::vector<const int64_t*> sid;
+        std::vector<const void*> sdy;
+        for (int d : order) {
+          sid.push_back(static_cast<const int64_t*>(ids[d]));
+          sdy.push_back(dy.p[d]);
+        }
+        const int64_t vocab = tm.shape[0], width = tm.shape[1];
+        std::vector<const void*> blks;
+        for (int d = 0; d < num_local_; ++d) {
+          const auto [iv, nv] = block_index(tplan.dims[0], d);
+          const auto [ih, nh] = block_index(tplan.dims[1], d);
+          const int64_t rows = vocab / nv, cols = width / nh;
+          void* blk = grad_zeros(static_cast<size_t>(rows * cols) * 4, stream);
+          apl_detail::check(apl_embedding_backward_block(
+              sid.data(), sdy.data(), static_cast<int>(sid.size()), n, ls.back(),
+              static_cast<float*>(blk), iv * rows, rows, ih * cols, cols, APL_BF16, stream));
+          blks.push_back(blk);
+        }
+        out.push_back({1, Grad{blks, 4}, tplan});
+      } else if (wants(tab)) {
+        const auto ts = local_shape(tspec, tm);
+        std::vector<void*> dt;
+        for (int d = 0; d < num_local_; ++d) {
+          void* t = grad_zeros(static_cast<size_t>(numel(ts)) * 4, stream);
+          apl_detail::check(apl_embedding_backward(static_cast<const int64_t*>(ids[d]), n,
+                                                   dy.p[d], static_cast<float*>(t), ts[0], ts[1],
+                                                   APL_BF16, stream));
+          dt.push_back(t);
+        }
+        std::set<int> axes_set;
+        for (const auto& dim : required_spec(nd, 0).dims)
+          for (int a : dim.axes) axes_set.insert(a);
+        std::vector<int32_t> axes(axes_set.begin(), axes_set.end());
+        if (!axes.empty())
+          apl_detail::check(apl_all_reduce(rt_.get(), axes.data(), static_cast<int>(axes.size()),
+                                           dt.data(), static_cast<size_t>(numel(ts)), APL_F32,
+                                           stream));
+        out.push_back({1, Grad{as_const(dt), 4}, tspec});
+      }
+    } else if (nd.kind == "batched-matmul") {
+      const OpStrategy& st = nd.strategy;
+      if (st.partial_sum) throw PlanError("backward of split-k batched matmul strategies");
+      const auto& sv = saved_.at(nd.id);
+      const auto as = local_shape(required_spec(nd, 0), nodes_.at(nd.inputs[0]).meta);
+      const auto bs = local_shape(required_spec(nd, 1), nodes_.at(nd.inputs[1]).meta);
+      const int64_t nb = as[0], m = as[1], k = as[2], nn = bs[2];
+      auto bmm = [&](const void* a, const void* b, void* o, int64_t M, int64_t N, int64_t K,
+                     int64_t lda, int64_t ldb, int a_layout, int b_layout, int64_t a_step,
+                     int64_t b_step) {
+        std::vector<const void*> A, B;
+        std::vector<void*> Cp;
+        for (int64_t i = 0; i < nb; ++i) {
+          A.push_back(static_cast<const char*>(a) + i * a_step * 2);
+          B.push_back(static_cast<const char*>(b) + i * b_step * 2);
+          Cp.push_back(static_cast<char*>(o) + i * M * N * 2);
+        }
+        apl_detail::check(apl_gemm_bf16_grouped_ex(A.data(), B.data(), Cp.data(),
+                                                   static_cast<int>(nb), M, N, K, lda, ldb, N,
+                                                   a_layout, b_layout, APL_BF16, stream));
+      };
+      if (wants(nd.inputs[0])) {  // dA = dC . B^T
+        std::vector<void*> da;
+        for (int d = 0; d < num_local_; ++d) {
+          void* o = grad_buf(static_cast<size_t>(nb * m * k) * 2);
+          bmm(dy.p[d], sv[1][d], o, m, k, nn, nn, nn, APL_A_MK, APL_B_NK, m * nn, k * nn);
+          da.push_back(o);
+        }
+        if (!st.output_spec.dims[2].axes.empty()) {
+          std::vector<int32_t> axes(st.output_spec.dims[2].axes.begin(),
+                                    st.output_spec.dims[2].axes.end());
+          apl_detail::check(apl_all_reduce(rt_.get(), axes.data(), static_cast<int>(axes.size()),
+                                           da.data(), static_cast<size_t>(nb * m * k), APL_BF16,
+                                           stream));
+        }
+        out.push_back({0, Grad{as_const(da), 2}, required_spec(nd, 0)});
+      }
+      if (wants(nd.inputs[1])) {  // dB = A^T . dC
+        std::vector<void*> db;
+        for (int d = 0; d < num_local_; ++d) {
+          void* o = grad_buf(static_cast<size_t>(nb * k * nn) * 2);
+          bmm(sv[0][d], dy.p[d], o, k, nn, m, k, nn, APL_A_KM, APL_B_KN, m * k, m * nn);
+          db.push_back(o);
+        }
+        if (!st.output_spec.dims[1].axes.empty()) {
+          std::vector<int32_t> axes(st.output_spec.dims[1].axes.begin(),
+                                    st.output_spec.dims[1].axes.end());
+          apl_detail::check(apl_all_reduce(rt_.get(), axes.data(), static_cast<int>(axes.size()),
+                                           db.data(), static_cast<size_t>(nb * k * nn), APL_BF16,
+                                           stream));
+        }
+        out.push_back({1, Grad{as_const(db), 2}, required_spec(nd, 1)});
+      }
+    } else {
+      throw PlanError("backward through " + nd.kind + " (" + nd.id + ")");
+    }
+    return out;
+  }
+
   static constexpr float kMaskFill = -1e4f;  // additive attention mask
   enum class Unary { kGelu, kScale, kNot };
 
@@ -551,6 +953,9 @@ class PlanExecutor {
   std::map<std::string, std::vector<std::string>> consumers_;
   std::map<std::string, Chain> attn_;
   std::set<std::string> attn_members_;
+  std::map<std::string, std::vector<std::vector<const void*>>> saved_;
+  bool trained_ = false;
+  int gcount_ = 0;
   std::map<std::string, std::vector<void*>> buffers_;
   std::map<std::string, std::pair<void*, size_t>> workspaces_;
 };

@@ -3,12 +3,14 @@
 // reads <dir>/<id>.bin (global row-major tensors of every placeholder and
 // parameter, any rank and element size), shards them on the host by each
 // node's plan spec, runs the forward pass and writes device 0's output
-// replica to <dir>/out.bin.
+// replica to <dir>/out.bin. With "train" it runs forward + backward against
+// <dir>/dy.bin and writes every parameter gradient to <dir>/grad_<id>.bin.
 #include <cuda_runtime.h>
 
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <iostream>
 #include <sstream>
 #include <string>
@@ -26,10 +28,11 @@ static std::string slurp(const std::string& path) {
 }
 
 int main(int argc, char** argv) {
-  if (argc != 5) {
-    std::fprintf(stderr, "usage: plan_executor_test graph.json plan.json AxB dir\n");
+  if (argc != 5 && argc != 6) {
+    std::fprintf(stderr, "usage: plan_executor_test graph.json plan.json AxB dir [train]\n");
     return 2;
   }
+  const bool train = argc == 6 && std::string(argv[5]) == "train";
   const std::string dir = argv[4];
   const DeviceMesh mesh = DeviceMesh::uniform(parse_mesh_shape(argv[3]));
   MeshRuntime rt = MeshRuntime::Simulated(mesh, 0);
@@ -82,7 +85,21 @@ int main(int argc, char** argv) {
   cudaStream_t stream;
   cudaStreamCreate(&stream);
   std::vector<void*> out;
-  for (int i = 0; i < 2; ++i) out = ex.forward(feeds, stream);  // second call reuses buffers
+  std::map<std::string, std::vector<void*>> grads;
+  std::vector<void*> dys;
+  if (train) {  // <dir>/dy.bin: the output gradient (global bf16), replicated
+    const std::string dy = slurp(dir + "/dy.bin");
+    for (int64_t d = 0; d < mesh.num_devices(); ++d) {
+      void* p = nullptr;
+      cudaMalloc(&p, dy.size());
+      cudaMemcpy(p, dy.data(), dy.size(), cudaMemcpyHostToDevice);
+      dys.push_back(p);
+    }
+  }
+  for (int i = 0; i < 2; ++i) {  // the second step reuses every buffer
+    out = ex.forward(feeds, stream, train);
+    if (train) grads = ex.backward(std::vector<const void*>(dys.begin(), dys.end()), stream);
+  }
   cudaStreamSynchronize(stream);
   const TensorMeta& om = ex.meta("out");
   size_t bytes = static_cast<size_t>(om.dtype_bytes);
@@ -93,6 +110,19 @@ int main(int argc, char** argv) {
     return 1;
   }
   std::ofstream(dir + "/out.bin", std::ios::binary).write(host.data(), static_cast<long>(bytes));
+  for (auto& [id, shards] : grads) {  // grad_<id>.bin: fp32 shards in device order
+    const TensorMeta& m = ex.meta(id);
+    TensorMeta m4 = m;
+    m4.dtype_bytes = 4;
+    const size_t sb = static_cast<size_t>(ex.spec(id).per_device_bytes(m4, mesh));
+    std::ofstream f(dir + "/grad_" + id + ".bin", std::ios::binary);
+    std::vector<char> h(sb);
+    for (void* p : shards) {
+      cudaMemcpy(h.data(), p, sb, cudaMemcpyDeviceToHost);
+      f.write(h.data(), static_cast<long>(sb));
+    }
+  }
+  for (void* p : dys) cudaFree(p);
   for (void* p : owned) cudaFree(p);
   std::cout << "plan executed on " << mesh.num_devices() << " simulated devices\n";
   return 0;
