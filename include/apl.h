@@ -440,7 +440,10 @@ int apl_mask_not(const void* x, void* y, size_t count, void* stream);
 
 /* Backward of the block kinds (the training step of a gpt_block plan). */
 /* layernorm: dx; with dgamma / dbeta (fp32 [width], ACCUMULATED: +=) also the
- * affine gradients, which need `stats` scratch of rows x 8 bytes. */
+ * affine gradients, which need `stats` scratch of
+ * apl_layernorm_backward_scratch() bytes (16-byte aligned). The affine
+ * gradients are reduced without atomics: bit-reproducible. */
+int apl_layernorm_backward_scratch(int64_t rows, int64_t width, size_t* bytes);
 int apl_layernorm_backward(const void* x, const void* gamma, const void* dy, void* dx,
                            float* dgamma, float* dbeta, void* stats, int64_t rows, int64_t width,
                            float eps, int dtype, void* stream);

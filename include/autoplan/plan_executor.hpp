@@ -502,7 +502,9 @@ class PlanExecutor {
         void* o = grad_buf(count * 2);
         void* g = has_g ? grad_zeros(static_cast<size_t>(h) * 4, stream) : nullptr;
         void* b = has_b ? grad_zeros(static_cast<size_t>(h) * 4, stream) : nullptr;
-        void* stats = has_g || has_b ? grad_buf(static_cast<size_t>(rows) * 8) : nullptr;
+        size_t sb = 0;
+        if (has_g || has_b) apl_detail::check(apl_layernorm_backward_scratch(rows, h, &sb));
+        void* stats = has_g || has_b ? grad_buf(sb) : nullptr;
         apl_detail::check(apl_layernorm_backward(sv[0][d], has_g ? sv[1][d] : nullptr, dy.p[d],
                                                  o, static_cast<float*>(g),
                                                  static_cast<float*>(b), stats, rows, h, 1e-5f,

@@ -178,6 +178,7 @@ _SIGS = {
     "apl_layernorm_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                          C.c_int64, C.c_float, C.c_int, C.c_void_p]),
+    "apl_layernorm_backward_scratch": (C.c_int, [C.c_int64, C.c_int64, P(C.c_size_t)]),
     "apl_softmax_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                        C.c_float, C.c_int, C.c_void_p]),
     "apl_embedding_backward": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,

@@ -106,7 +106,9 @@ def layernorm_backward(x: torch.Tensor, gamma: torch.Tensor | None, dy: torch.Te
     rows = x.numel() // w
     stats = None
     if dgamma is not None or dbeta is not None:
-        stats = torch.empty(rows * 2, dtype=torch.float32, device=x.device)
+        n = C.c_size_t()
+        check(A.lib().apl_layernorm_backward_scratch(rows, w, C.byref(n)))
+        stats = torch.empty((n.value + 15) // 16 * 4, dtype=torch.float32, device=x.device)
     check(A.lib().apl_layernorm_backward(_p(x), _p(gamma), _p(dy), _p(dx), _p(dgamma),
                                          _p(dbeta), _p(stats), rows, w, eps,
                                          _DTYPE_CODE[x.dtype], _stream_handle(stream)))

@@ -1062,6 +1062,13 @@ int apl_layernorm_backward(const void* x, const void* gamma, const void* dy, voi
   });
 }
 
+int apl_layernorm_backward_scratch(int64_t rows, int64_t width, size_t* bytes) {
+  return guarded([&] {
+    need(rows >= 0 && width > 0 && bytes != nullptr, "bad arguments");
+    *bytes = apl::layernorm_backward_scratch_bytes(rows, width);
+  });
+}
+
 int apl_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows, int64_t width,
                          float alpha, int dtype, void* stream) {
   return guarded([&] {

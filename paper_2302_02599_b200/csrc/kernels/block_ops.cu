@@ -403,12 +403,11 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
 }
 
 // dgamma[c] += sum_r dy[r,c] * xhat[r,c], dbeta[c] += sum_r dy[r,c]: a 32-column
-// strip per warp lane group, row chunks across blockIdx.y, fp32 atomics.
+// strip per warp lane group, row chunks across blockIdx.y, partials per chunk.
 template <typename T>
 __global__ void __launch_bounds__(256) layernorm_param_grad_kernel(
     const T* __restrict__ x, const T* __restrict__ dy, const float2* __restrict__ stats,
-    float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows, int64_t width,
-    int64_t rows_per_chunk) {
+    float* __restrict__ part, int64_t rows, int64_t width, int64_t rows_per_chunk) {
   const int64_t c = blockIdx.x * 32 + threadIdx.x;
   const int64_t r0 = blockIdx.y * rows_per_chunk;
   const int64_t r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
@@ -429,9 +428,30 @@ __global__ void __launch_bounds__(256) layernorm_param_grad_kernel(
       sg += red[0][j][threadIdx.x];
       sb += red[1][j][threadIdx.x];
     }
-    if (dgamma != nullptr) atomicAdd(dgamma + c, sg);
-    if (dbeta != nullptr) atomicAdd(dbeta + c, sb);
+    // per-chunk partials, summed in chunk order by the next kernel: no
+    // atomics, so the parameter gradients are bit-reproducible
+    part[blockIdx.y * width + c] = sg;
+    part[(gridDim.y + blockIdx.y) * width + c] = sb;
   }
+}
+
+__global__ void __launch_bounds__(256) layernorm_param_reduce_kernel(
+    const float* __restrict__ part, int64_t chunks, int64_t width, float* __restrict__ dgamma,
+    float* __restrict__ dbeta) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= width) return;
+  float sg = 0.f, sb = 0.f;
+  for (int64_t j = 0; j < chunks; ++j) {
+    sg += part[j * width + c];
+    sb += part[(chunks + j) * width + c];
+  }
+  if (dgamma != nullptr) dgamma[c] += sg;
+  if (dbeta != nullptr) dbeta[c] += sb;
+}
+
+int64_t layernorm_param_chunks(int64_t rows, int64_t width) {
+  const int64_t strips = (width + 31) / 32;
+  return std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, (148 * 8 + strips - 1) / strips));
 }
 
 // softmax: dx = alpha * y * (dy - sum(dy * y)) per row (alpha: the fused
@@ -872,14 +892,16 @@ cudaError_t layernorm_bwd_typed(const void* x, const void* gamma, const void* dy
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (dgamma != nullptr || dbeta != nullptr) {
     const int64_t strips = (width + 31) / 32;
-    const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64,
-                                                                   (148 * 8 + strips - 1) / strips));
+    const int64_t chunks = layernorm_param_chunks(rows, width);
     const int64_t per = (rows + chunks - 1) / chunks;
+    // partials live after the per-row stats in the scratch (16-byte aligned)
+    float* part = reinterpret_cast<float*>(stats + ((rows + 1) / 2) * 2);
     layernorm_param_grad_kernel<T><<<dim3(static_cast<unsigned>(strips),
                                           static_cast<unsigned>(chunks)),
-                                     dim3(32, 8), 0, s>>>(X, D, stats, dgamma, dbeta, rows, width,
-                                                          per);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+                                     dim3(32, 8), 0, s>>>(X, D, stats, part, rows, width, per);
+    layernorm_param_reduce_kernel<<<static_cast<unsigned>((width + 255) / 256), 256, 0, s>>>(
+        part, chunks, width, dgamma, dbeta);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
   }
   return cudaGetLastError();
 }
@@ -960,6 +982,11 @@ cudaError_t launch_embedding_backward_block(const int64_t* const* ids, const voi
   else
     return cudaErrorInvalidValue;
   return done();
+}
+
+size_t layernorm_backward_scratch_bytes(int64_t rows, int64_t width) {
+  const int64_t chunks = layernorm_param_chunks(rows, width);
+  return static_cast<size_t>(((rows + 1) / 2) * 2 * 8 + 2 * chunks * width * 4);
 }
 
 }  // namespace apl

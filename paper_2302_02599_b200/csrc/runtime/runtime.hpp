@@ -76,6 +76,7 @@ cudaError_t launch_add(const void* a, const void* b, bool b_mask, void* y, size_
 cudaError_t launch_layernorm_backward(const void* x, const void* gamma, const void* dy, void* dx,
                                       float* dgamma, float* dbeta, void* stats, int64_t rows,
                                       int64_t width, float eps, int dtype, cudaStream_t s);
+size_t layernorm_backward_scratch_bytes(int64_t rows, int64_t width);
 cudaError_t launch_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows,
                                     int64_t width, float alpha, int dtype, cudaStream_t s);
 cudaError_t launch_embedding_backward(const int64_t* ids, int64_t n, const void* dy,

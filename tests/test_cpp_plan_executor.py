@@ -108,10 +108,10 @@ def test_native_executor_runs_block_plans(cuda, tmp_path, name):
 def test_native_executor_backward_matches_python(cuda, tmp_path, name):
     """Training step from the native executor: every parameter gradient
     (fp32, plan layout, all devices) byte-identical to the Python
-    PlanExecutor.backward on the same plan and operands -- except the ones
-    accumulated with fp32 atomics (layernorm gamma / beta, the embedding
-    table), whose summation order is not fixed even between two runs of the
-    same executor: those within 1e-5 of the largest entry."""
+    PlanExecutor.backward on the same plan and operands -- except the
+    embedding table's, accumulated with fp32 atomics (repeated ids), whose
+    summation order is not fixed even between two runs of the same executor:
+    within 1e-5 of the largest entry."""
     import sys
 
     import torch
@@ -151,7 +151,7 @@ def test_native_executor_backward_matches_python(cuda, tmp_path, name):
     grads = ex.backward(gy)
     torch.cuda.synchronize()
     assert grads
-    atomic = {"g1", "b1", "g2", "b2", "wte"}
+    atomic = {"wte"}
     for k, shards in grads.items():
         mine = b"".join(t.contiguous().view(torch.uint8).cpu().numpy().tobytes() for t in shards)
         native = (tmp_path / f"grad_{k}.bin").read_bytes()
