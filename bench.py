@@ -3,24 +3,30 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Workload (BASELINE.json configs[1], "1D mesh of 8: all-gather S0 -> R and
-all-to-all S0R -> RS0"): one step converts a [65536, 8192] bf16 tensor
-(1 GiB) S0R -> RR (all-gather) and S0R -> RS0 (all-to-all) on a mesh of 8.
+all-to-all S0R -> RS0"): one step converts a bf16 tensor S0R -> RR
+(all-gather) and S0R -> RS0 (all-to-all).
 
-  N = 1 : the 8 mesh devices are simulated as buffers on one B200, so each
-          conversion is one collapsed exchange = one box-copy kernel over HBM
-          (the "pack/unpack only" point of the north star). value = pack HBM
-          GB/s: algorithmic bytes (every source byte read once + every
-          destination byte written, i.e. the minimal HBM traffic of the
-          conversion) / device time.
-  N > 1 : one process per GPU over NCCL (mesh [N]), weak scaling with a
-          128 MiB shard per GPU; value = bus bytes received by all ranks /
-          max-over-ranks device time (aggregate bus GB/s).
+  N = 1 : [65536, 8192] (1 GiB) on a mesh of 8 simulated as buffers on one
+          B200, so each conversion is one collapsed exchange = one copy
+          kernel over HBM (the "pack/unpack only" point of the north star).
+          value = pack HBM GB/s: algorithmic bytes (every source byte read
+          once + every destination byte written, i.e. the minimal HBM traffic
+          of the conversion) / device time.
+  N > 1 : one process per GPU (mesh [N]), weak scaling with a [8192, 8192]
+          (128 MiB) S0R shard per GPU. value = bus GB/s PER GPU: the bytes a
+          rank receives per step / max-over-ranks device time (NCCL busBW
+          convention), roofline against the nominal 900 GB/s NVLink 5 per
+          direction (the measured 770 GB/s peer copy is a second field).
+          `aggregate_bus_gbs` = value x N.
+  `--gpus N` without torchrun re-launches itself under
+  torch.distributed.run with N ranks (127.0.0.1 rendezvous); under torchrun
+  WORLD_SIZE must equal N.
 
-Inputs are 1 GiB (> 126 MB L2), so no L2 flush is needed between steps.
-The reference arm (--impl reference) runs the reference's own planner
-(oracle/_ref: find_transform_path + conversion_cost compiled from
+Inputs are >= 128 MiB per GPU (> 126 MB L2), so no L2 flush is needed
+between steps. The reference arm (--impl reference) runs the reference's own
+planner (oracle/_ref: find_transform_path + conversion_cost compiled from
 /root/reference) and the C oracle executing the returned steps in host RAM
-with all host threads, on a bounded sample of the same workload.
+with all host threads, on the SAME tensor and mesh as this arm.
 """
 from __future__ import annotations
 
@@ -39,8 +45,11 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "layout-conversion bus GB/s per GPU vs 900 GB/s at 2/4/8 B200; pack HBM GB/s"
 SHAPE_1GPU = (65536, 8192)   # bf16, 1 GiB
+SHAPE_4GIB = (262144, 8192)  # bf16, 4 GiB: the top of config 2's 1 MB - 4 GB sweep
 SHARD_ROWS_NGPU = 8192       # per-GPU shard rows of [*, 8192] bf16 = 128 MiB
 EB = 2
+NVLINK_PEAK = 900.0          # NVLink 5, GB/s per direction per GPU (nominal, BASELINE metric)
+PEER_COPY_MEASURED = 770.0   # measured peer copy per direction (B200_PROFILING.md)
 CONVERSIONS = [("S0R", "RR"), ("S0R", "RS0")]
 
 
@@ -108,11 +117,73 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+KERNEL_SOURCES = ["paper_2302_02599_b200/csrc/kernels/box_copy.cu",
+                  "paper_2302_02599_b200/csrc/kernels/box_copy.cuh",
+                  "paper_2302_02599_b200/csrc/kernels/bulk_copy.cu",
+                  "paper_2302_02599_b200/csrc/runtime/runtime.cpp",
+                  "paper_2302_02599_b200/csrc/runtime/plan.cpp"]
+
+
+def kernel_sources_sha():
+    """sha256 (16 hex) over the copy-kernel sources and the exchange compiler:
+    the key under which profiles/traffic.json records ncu DRAM bytes."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in KERNEL_SOURCES:
+        p = ROOT / f
+        h.update(p.read_bytes() if p.exists() else b"")
+    return h.hexdigest()[:16]
+
+
+def stamped_traffic(key):
+    """ncu dram__bytes_read+write of the dominant launch from one `ncu --set
+    full` capture (tools/ncu_traffic.py writes profiles/traffic.json). Used
+    only when the capture was taken from the same kernel sources as this
+    build (sha stamp); otherwise null, with the reason."""
+    tf = ROOT / "profiles" / "traffic.json"
+    if not tf.exists():
+        return None, "no ncu capture (profiles/traffic.json absent)"
+    entry = json.loads(tf.read_text()).get(key)
+    if not entry:
+        return None, f"no ncu capture for {key}"
+    sha = kernel_sources_sha()
+    if entry.get("kernel_sources_sha") != sha:
+        return None, f"stale ncu capture (sources {entry.get('kernel_sources_sha')} != {sha})"
+    return entry["dram_bytes"], f"{entry['source']} (kernel sources {sha})"
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def workload_shape(ws):
+    """The tensor this arm (and the reference arm) converts at N GPUs."""
+    return SHAPE_1GPU if ws == 1 else (SHARD_ROWS_NGPU * ws, 8192)
+
+
+def rank_bus_bytes(conv, ws, shard_bytes):
+    """Bytes one rank receives for S0R -> `conv` on a mesh of ws (NCCL busBW
+    convention: an all-gather receives (n-1) shards, an all-to-all (n-1)/n
+    of one)."""
+    return (ws - 1) * shard_bytes if conv == "RR" else (ws - 1) * shard_bytes // ws
+
+
+def nvlink_roofline(kernel, bus_bytes, launch_ms, gpus_shared):
+    achieved = bus_bytes / (launch_ms * 1e-3) / 1e9
+    return {"bound": "nvlink", "kernel": kernel, "achieved": round(achieved, 1),
+            "peak": NVLINK_PEAK, "peak_kind": "nominal NVLink 5 per direction per GPU",
+            "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK, 4),
+            "frac_vs_measured_peer_copy": round(achieved / PEER_COPY_MEASURED, 4),
+            "measured_peer_copy_gbs": PEER_COPY_MEASURED, "traffic": None,
+            "algorithmic_bytes_per_launch": int(bus_bytes),
+            "bytes_definition": "bytes this rank receives from its peers per launch",
+            "launch_ms": round(launch_ms, 4),
+            "note": ("ranks share one GPU: functional run, not an NVLink number"
+                     if gpus_shared else "one GPU per rank")}
 
 
 # ----------------------------------------------------------------------------- ours (N>1, peer)
@@ -135,7 +206,8 @@ def run_ours_peer(args):
     torch.cuda.set_device(dev_idx)
     dev = torch.device("cuda", dev_idx)
     dist.init_process_group("gloo")
-    shape = (SHARD_ROWS_NGPU * ws, 8192)
+    shape = workload_shape(ws)
+    gpus_shared = torch.cuda.device_count() < ws
     meta = TensorMeta(shape, EB)
     s = ShardingSpec.parse("S0R", 1)
     pm_geo = DeviceMesh.uniform([ws])
@@ -164,8 +236,7 @@ def run_ours_peer(args):
     for a, b in CONVERSIONS:
         t = ShardingSpec.parse(b, 1)
         out = torch.empty(t.local_shape(meta, pm_geo), dtype=torch.bfloat16, device=dev)
-        bus = (ws - 1) * in_bytes if b == "RR" else (ws - 1) * in_bytes // ws
-        convs.append(dict(name=f"{a}->{b}", tgt=t, out=out, bus=bus))
+        convs.append(dict(name=f"{a}->{b}", tgt=t, out=out, bus=rank_bus_bytes(b, ws, in_bytes)))
     torch.cuda.synchronize()
     dist.barrier()
 
@@ -201,17 +272,11 @@ def run_ours_peer(args):
     dist.all_reduce(v, op=dist.ReduceOp.MAX)
     ms_per_step = float(v[0]) / args.steps
     per_ms = {c["name"]: float(v[1 + i]) for i, c in enumerate(convs)}
-    step_bus = sum(c["bus"] for c in convs) * ws
+    step_bus = sum(c["bus"] for c in convs)  # per rank (every rank receives the same)
     value = step_bus / (ms_per_step * 1e-3) / 1e9
     dom = max(convs, key=lambda c: per_ms[c["name"]])
-    achieved = dom["bus"] / (per_ms[dom["name"]] * 1e-3) / 1e9
-    roof = {"bound": "nvlink", "kernel": f"box_copy/bulk pull kernel over peer pointers ({dom['name']})",
-            "achieved": round(achieved, 1), "peak": 770.0,
-            "peak_kind": "measured peer copy per direction per GPU (B200_PROFILING.md)",
-            "unit": "GB/s", "frac": round(achieved / 770.0, 4), "traffic": None,
-            "algorithmic_bytes_per_launch": dom["bus"],
-            "bytes_definition": "bytes this rank receives over NVLink (NCCL busBW convention)",
-            "launch_ms": round(per_ms[dom["name"]], 4)}
+    roof = nvlink_roofline(f"box_copy pull kernel over peer pointers ({dom['name']})",
+                           dom["bus"], per_ms[dom["name"]], gpus_shared)
     # e2e through the public API with host buffers: H2D of this rank's source
     # shard (after the readers of the last epoch finished), both exchanges,
     # D2H of both converted shards -- every step, one stream.
@@ -239,19 +304,21 @@ def run_ours_peer(args):
     torch.cuda.synchronize()
     et = torch.tensor([ea.elapsed_time(ez) / e_steps], dtype=torch.float64)
     dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e = {"value": round(step_bus / (float(et[0]) * 1e-3) / 1e9, 2), "unit": "GB/s",
+    e2e = {"value": round(step_bus / (float(et[0]) * 1e-3) / 1e9, 2), "unit": "GB/s per GPU",
            "h2d_bytes_per_step": in_bytes,
            "d2h_bytes_per_step": sum(h.numel() * h.element_size() for h in host_out),
            "ms_per_step": round(float(et[0]), 3), "steps": e_steps,
            "note": "per rank: pinned H2D of its source shard, both exchanges, D2H of both "
                    "converted shards; one stream; max over ranks"}
     result = {
-        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws,
+        "metric": METRIC, "value": round(value, 1), "unit": "GB/s per GPU", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random bf16 bit patterns generated on device)",
+        "data": "synthetic (random bf16 bit patterns, torch.random_ on device)",
+        "aggregate_bus_gbs": round(value * ws, 1), "bus_bytes_per_rank_per_step": int(step_bus),
         "config": {"workload": "configs[1]: mesh of N, S0R->RR all-gather + S0R->RS0 all-to-all",
                    "tensor": list(shape), "mesh": [ws], "transport": "peer",
+                   "gpus_shared": gpus_shared,
                    "mode": "one process per GPU, fused pull kernel over peer memory, "
                            "device-side epoch flags",
                    "path": "collapsed exchange (one pull kernel per rank)",
@@ -274,7 +341,7 @@ def peer_mesh_sweep(ws, rank, dev_idx, iters=10):
     """configs 3/4 on the real 2-D / 3-D meshes ([2,2] at N=4; [2,4] and
     [2,2,2] at N=8) over the peer transport: bus GB/s per GPU = max over ranks
     of the bytes a rank pulls / max-over-ranks time per exchange (flags
-    included), vs the measured 770 GB/s peer copy."""
+    included), vs the nominal 900 GB/s (and the measured 770 GB/s peer copy)."""
     import torch
     import torch.distributed as dist
 
@@ -311,14 +378,16 @@ def peer_mesh_sweep(ws, rank, dev_idx, iters=10):
             rows.append({"mesh": ms, "tensor": list(shape), "conversion": f"{a}->{b}",
                          "us": round(ms_t * 1e3, 2), "bus_bytes": int(wire),
                          "bus_gbs": round(wire / ms_t / 1e6, 1) if wire else None,
-                         "frac": round(wire / ms_t / 1e6 / 770.0, 3) if wire else None})
+                         "frac": round(wire / ms_t / 1e6 / NVLINK_PEAK, 3) if wire else None,
+                         "frac_vs_measured_peer_copy":
+                             round(wire / ms_t / 1e6 / PEER_COPY_MEASURED, 3) if wire else None})
             del out
         torch.cuda.synchronize()
         dist.barrier()
         pm.close()
     fr = [r["frac"] for r in rows if r.get("frac") is not None]
     return {"rows": rows, "frac_min": min(fr) if fr else None,
-            "frac_median": statistics.median(fr) if fr else None, "peak": 770.0,
+            "frac_median": statistics.median(fr) if fr else None, "peak": NVLINK_PEAK,
             "kind": "bus GB/s per GPU (bytes pulled over peer memory), transport peer"}
 
 
@@ -338,7 +407,7 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=dev)
         mesh = Mesh.from_process_group([ws])
-        shape = (SHARD_ROWS_NGPU * ws, 8192)
+        shape = workload_shape(ws)
         ndev = ws
     else:
         mesh = Mesh.local([8], device=local)
@@ -369,11 +438,7 @@ def run_ours(args):
         # of the compiled exchange, identical to what the kernel moves)
         traffic = mesh.exchange_traffic(s, t, meta)
         hbm = traffic["hbm_read"] + traffic["hbm_write"]
-        # bus bytes each rank must receive (NCCL busBW convention)
-        if (a, b) == ("S0R", "RR"):
-            bus = (ndev - 1) * in_bytes
-        else:
-            bus = (ndev - 1) * in_bytes // ndev
+        bus = rank_bus_bytes(b, ndev, in_bytes)  # bytes each rank receives
         engine = mesh.exchange_engine(s, t, meta)
         conv = mesh.prepare(path, meta, fuse=True)  # public API: compiled once, launched per step
         convs.append(dict(name=f"{a}->{b}", path=path, conv=conv, ins=ins, outs=outs, hbm=hbm, bus=bus,
@@ -430,58 +495,57 @@ def run_ours(args):
     hbm_peak, peak_kind = peaks()
     if ws == 1:
         step_bytes = sum(c["hbm"] for c in convs)
-        value = step_bytes / (ms_per_step * 1e-3) / 1e9
         unit = "GB/s"
-    else:
-        step_bytes = sum(c["bus"] for c in convs) * ws
-        value = step_bytes / (ms_per_step * 1e-3) / 1e9
-        unit = "GB/s"
+    else:  # per-GPU bus bytes (every rank receives the same)
+        step_bytes = sum(c["bus"] for c in convs)
+        unit = "GB/s per GPU"
+    value = step_bytes / (ms_per_step * 1e-3) / 1e9
 
     # roofline of the dominant kernel (the box-copy of S0R->RR, largest share)
     dom = max(convs, key=lambda c: statistics.mean(per_conv_ms[c["name"]]))
     dom_ms = statistics.mean(per_conv_ms[dom["name"]])
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        entry = json.loads(tf.read_text()).get(f"n{ws}:{dom['name']}")
-        traffic = entry["dram_bytes"] if entry else None
     if ws == 1:
+        traffic, traffic_src = stamped_traffic(f"n1:{dom['name']}")
         achieved = dom["hbm"] / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": f"{dom['kernel']} ({dom['name']}, 8 simulated devices)",
                 "achieved": round(achieved, 1), "peak": hbm_peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": dom["hbm"],
                 "bytes_definition": "source bytes read once + destination bytes written",
                 "launch_ms": round(dom_ms, 4)}
     else:
-        achieved = dom["bus"] / (dom_ms * 1e-3) / 1e9
-        roof = {"bound": "nvlink", "kernel": f"{dom['name']} exchange (NCCL p2p + box_copy)",
-                "achieved": round(achieved, 1), "peak": 770.0, "peak_kind": "measured peer copy (B200_PROFILING.md)",
-                "unit": "GB/s", "frac": round(achieved / 770.0, 4), "traffic": traffic,
-                "algorithmic_bytes_per_launch": dom["bus"], "launch_ms": round(dom_ms, 4)}
+        roof = nvlink_roofline(f"{dom['name']} exchange (NCCL collective + box_copy pack/unpack)",
+                               dom["bus"], dom_ms, torch.cuda.device_count() < ws)
 
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": unit, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (index-hashed bf16 bit patterns generated on device)",
-        "config": {"workload": "configs[1]: mesh of 8, S0R->RR all-gather + S0R->RS0 all-to-all",
-                   "tensor": list(shape), "mesh": [8] if ws == 1 else [ws],
+        "data": "synthetic (random bf16 bit patterns, torch.random_ on device)",
+        "config": {"workload": f"configs[1]: mesh of {ndev}, S0R->RR all-gather + S0R->RS0 "
+                               "all-to-all",
+                   "tensor": list(shape), "mesh": [ndev],
                    "mode": "simulated 8-device mesh on 1 GPU (pack/unpack only)" if ws == 1
-                   else "one process per GPU, NCCL",
+                   else "one process per GPU, NCCL per mesh-axis communicator",
+                   "transport": "simulated" if ws == 1 else "nccl",
                    "path": "collapsed exchange (APL_FUSE_CHAIN)",
                    "l2": "inputs 1 GiB > 126 MB L2, no flush needed" if ws == 1 else
                    "per-GPU shard 128 MiB > L2",
-                   "parallelism": f"mesh[{8 if ws == 1 else ws}]"},
+                   "parallelism": f"mesh[{ndev}]"},
         "per_conversion_ms": {k: round(statistics.mean(v), 4) for k, v in per_conv_ms.items()},
         "roofline": roof,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if ws > 1:
+        result["aggregate_bus_gbs"] = round(value * ws, 1)
     result["e2e"] = run_e2e(args, mesh, meta, convs, stream, ws)
     if not args.no_sweep:
         result["mesh_sweep"] = mesh_sweep(ws, rank, dev, stream, hbm_peak)
-    if ws == 1:
+        if ws == 1:
+            result["config2_4gib"] = size_point(args, SHAPE_4GIB, dev, hbm_peak)
+    if ws == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
         print(json.dumps(result))
@@ -593,10 +657,11 @@ def run_e2e(args, mesh, meta, convs, stream, ws=1):
         t = torch.tensor([ms], device=f"cuda:{mesh.device}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        step_bytes = sum(c["bus"] for c in convs) * ws  # same metric as `value`
+        step_bytes = sum(c["bus"] for c in convs)  # per GPU, the same metric as `value`
     else:
         step_bytes = sum(c["hbm"] for c in convs)
-    return {"value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+    return {"value": round(step_bytes / (ms * 1e-3) / 1e9, 2),
+            "unit": "GB/s" if ws == 1 else "GB/s per GPU",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3),
             "steps": steps,
             "note": "pinned H2D of the input tensor's shards (once: both conversions read the "
@@ -624,7 +689,8 @@ def mesh_sweep(ws, rank, dev, stream, hbm_peak, iters=20):
     measured copy peak. N = 4 / 8: the real meshes ([2,2]; [2,4] and [2,2,2])
     over NCCL -> bus GB/s per GPU = max over ranks of the minimal one-shot
     bytes a rank receives / max-over-ranks time, vs the
-    measured 770 GB/s peer copy. Collapsed exchanges, events on the launch
+    nominal 900 GB/s NVLink (and the measured 770 GB/s peer copy). Collapsed
+    exchanges, events on the launch
     stream."""
     import torch
 
@@ -674,7 +740,9 @@ def mesh_sweep(ws, rank, dev, stream, hbm_peak, iters=20):
                 ms_t, wire = float(v[0]), float(v[1])
                 row.update(us=round(ms_t * 1e3, 2), bus_bytes=int(wire),
                            bus_gbs=round(wire / ms_t / 1e6, 1) if wire else None,
-                           frac=round(wire / ms_t / 1e6 / 770.0, 3) if wire else None)
+                           frac=round(wire / ms_t / 1e6 / NVLINK_PEAK, 3) if wire else None,
+                           frac_vs_measured_peer_copy=round(
+                               wire / ms_t / 1e6 / PEER_COPY_MEASURED, 3) if wire else None)
             rows.append(row)
             conv.close()
             del ins, outs
@@ -683,58 +751,93 @@ def mesh_sweep(ws, rank, dev, stream, hbm_peak, iters=20):
     fr = [r["frac"] for r in rows if r.get("frac") is not None]
     return {"rows": rows, "frac_min": min(fr) if fr else None,
             "frac_median": statistics.median(fr) if fr else None,
-            "peak": hbm_peak if ws == 1 else 770.0,
+            "peak": hbm_peak if ws == 1 else NVLINK_PEAK,
             "kind": "pack HBM GB/s (simulated mesh)" if ws == 1 else
                     "bus GB/s per GPU (minimal one-shot bytes, NCCL)"}
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def _cpu_sample_shape():
-    # bounded sample of the same workload: 1/16 of the rows (64 MiB global)
-    return (SHAPE_1GPU[0] // 16, SHAPE_1GPU[1])
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
-def cpu_convert_once(shape, threads):
-    """Reference planner path + oracle step execution in host RAM, all 8
-    simulated devices; returns (seconds, algorithmic bytes)."""
-    import numpy as np
+class CpuWorkload:
+    """The reference CPU path of one step on host RAM: the reference planner
+    (oracle/_ref find_transform_path, compiled from /root/reference) picks each
+    conversion's steps, the C oracle executes them on the N simulated devices.
+    Source shards and destination buffers are allocated once (reused every
+    step, as the GPU arm's are), so a step times the byte movement."""
 
-    from oracle import data as O
-    from oracle import ref as R
+    def __init__(self, ndev, shape):
+        from oracle import data as O
+        from oracle import ref as R
 
-    O.set_threads(threads)
-    g = O.fill_global(shape, EB)
-    total_s, total_b = 0.0, 0
-    for a, b in CONVERSIONS:
-        ins = O.shards(g, O.parse_spec(a, 1), [8])
-        t0 = time.perf_counter()
-        if R.available():
-            rc, steps, _ = R.find_path([8], list(shape), EB, a, b)
-            assert rc == 0
-        else:
-            steps = [(0, 0, -1, 0, "R")] if b == "RR" else [(3, 0, 1, 0, "RS0")]
-        outs = O.replay(shape, O.parse_spec(a, 1), [8], steps, ins)
-        total_s += time.perf_counter() - t0
-        # same accounting as the GPU arm: distinct source bytes read + output bytes written
-        total_b += sum(i.nbytes for i in ins) + sum(o.nbytes for o in outs)
-    return total_s, total_b
+        self.O, self.R = O, R
+        self.ndev, self.shape = ndev, tuple(shape)
+        g = O.fill_global(self.shape, EB)
+        self.ins = O.shards(g, O.parse_spec("S0R", 1), [ndev])
+        del g
+        self.outs = {}
+        for _, b in CONVERSIONS:
+            dims = O.parse_spec(b, 1)
+            ls = O.local_shape(self.shape, dims, [ndev])
+            self.outs[b] = [O.np.empty(ls, dtype=self.ins[0].dtype) for _ in range(ndev)]
+            for o in self.outs[b]:
+                o.fill(0)  # first touch outside the timed steps
+        self.in_bytes = sum(x.nbytes for x in self.ins)
+
+    def step(self, threads):
+        """-> (seconds, algorithmic bytes, per-GPU bus bytes)."""
+        O, R = self.O, self.R
+        O.set_threads(threads)
+        total_s, total_b, bus = 0.0, 0, 0
+        for a, b in CONVERSIONS:
+            t0 = time.perf_counter()
+            if R.available():
+                rc, steps, _ = R.find_path([self.ndev], list(self.shape), EB, a, b)
+                assert rc == 0, steps
+            else:
+                steps = [(0, 0, -1, 0, "R")] if b == "RR" else [(3, 0, 1, 0, "RS0")]
+            O.replay(self.shape, O.parse_spec(a, 1), [self.ndev], steps, self.ins,
+                     outs=self.outs[b])
+            total_s += time.perf_counter() - t0
+            # same accounting as the GPU arm: source bytes read once + bytes written
+            total_b += self.in_bytes + sum(o.nbytes for o in self.outs[b])
+            bus += rank_bus_bytes(b, self.ndev, self.ins[0].nbytes)
+        return total_s, total_b, bus
 
 
 def cpu_baseline(args):
+    """The reference CPU path on the SAME [65536, 8192] tensor and mesh [8] as
+    the GPU arm, all host threads, bounded to ~10 s; plus one single-thread
+    step."""
     threads = os.cpu_count() or 1
-    shape = _cpu_sample_shape()
+    w = CpuWorkload(8, SHAPE_1GPU)
+    w.step(threads)  # warm-up
     secs, nbytes, reps = 0.0, 0, 0
-    while secs < 10.0 and reps < 50:
-        s, b = cpu_convert_once(shape, threads)
-        secs += s
+    while secs < 10.0 and reps < 20:
+        s_, b, _ = w.step(threads)
+        secs += s_
         nbytes += b
         reps += 1
+    s1, b1, _ = w.step(1)
     return {"value": round(nbytes / secs / 1e9, 3), "unit": "GB/s", "cores": threads,
-            "kind": "port" if not _ref_available() else "reference",
-            "sample": f"{reps} x (S0R->RR + S0R->RS0) on [{shape[0]},{shape[1]}] bf16, mesh [8] "
-                      f"simulated in host RAM; path from the reference planner "
-                      f"({'oracle/_ref' if _ref_available() else 'n/a'}), bytes moved by the C "
-                      f"oracle with {threads} threads"}
+            "kind": "reference" if _ref_available() else "port",
+            "single_thread": {"value": round(b1 / s1 / 1e9, 3), "unit": "GB/s", "cores": 1,
+                              "ms_per_step": round(1e3 * s1, 1)},
+            "cpu_model": cpu_model(),
+            "sample": f"{reps} full steps (S0R->RR + S0R->RS0 of the same [{SHAPE_1GPU[0]},"
+                      f"{SHAPE_1GPU[1]}] bf16 tensor, mesh [8] simulated in host RAM); path "
+                      f"from the reference planner ("
+                      f"{'oracle/_ref' if _ref_available() else 'n/a'}), bytes moved by the C "
+                      f"oracle with {threads} threads; same algorithmic-byte accounting as "
+                      f"the GPU arm"}
 
 
 def _ref_available():
@@ -743,45 +846,151 @@ def _ref_available():
     return R.available()
 
 
+def planner_timings(iters=2000):
+    """Reference planner (oracle/_ref) per BASELINE config 1-4: mean us per
+    uncached find_transform_path + conversion_cost, and per cached
+    PathCache::get hit (layout.cpp:331-346)."""
+    if not _ref_available():
+        return None
+    from oracle import ref as R
+
+    cases = [
+        (1, [2, 2], [1024, 1024], 4, [("S0R", "RS0")]),
+        (2, [8], list(SHAPE_1GPU), 2, list(CONVERSIONS)),
+        (3, [2, 4], [8192, 8192], 2,
+         [(a, b) for a in CONFIG3_SPECS for b in CONFIG3_SPECS if a != b]),
+        (4, [2, 2, 2], [8192, 8192], 2, [("S012R", "RS012"), ("RS012", "S012R")]),
+        (4, [2, 2, 2], [512, 512, 256], 2, [("S0S1R", "RS1S0"), ("RS1S0", "S0S1R")]),
+    ]
+    out = []
+    for cfg, mesh, shape, eb, pairs in cases:
+        miss = [R.time_paths(mesh, shape, eb, a, b, iters, hits=False) for a, b in pairs]
+        hit = [R.time_paths(mesh, shape, eb, a, b, iters * 10, hits=True) for a, b in pairs]
+        out.append({"config": cfg, "mesh": mesh, "tensor": shape, "pairs": len(pairs),
+                    "search_us_mean": round(1e6 * statistics.mean(miss), 3),
+                    "search_us_max": round(1e6 * max(miss), 3),
+                    "cache_hit_us_mean": round(1e6 * statistics.mean(hit), 4)})
+    return out
+
+
 def run_reference(args):
+    """--impl reference: the reference's CPU path (reference planner + C
+    oracle byte movement) on this arm's config at N: tensor and mesh are
+    exactly the GPU arm's (`workload_shape`), so the two lines are like for
+    like. At N > 1 the value is per-GPU bus GB/s (bytes one simulated device
+    receives / step time), the GPU arm's N > 1 metric."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    n = max(ws, args.gpus)
+    ndev = 8 if n == 1 else n
+    shape = workload_shape(n)
     threads = os.cpu_count() or 1
-    shape = _cpu_sample_shape()
+    w = CpuWorkload(ndev, shape)
     for _ in range(args.warmup):
-        cpu_convert_once(shape, threads)
-    secs, nbytes = 0.0, 0
+        w.step(threads)
+    secs, nbytes, bus = 0.0, 0, 0
     for _ in range(args.steps):
-        s, b = cpu_convert_once(shape, threads)
-        secs += s
+        s_, b, bb = w.step(threads)
+        secs += s_
         nbytes += b
-    value = nbytes / secs / 1e9
-    planner_us = None
-    if _ref_available():
-        from oracle import ref as R
-
-        planner_us = round(1e6 * R.time_paths([8], list(SHAPE_1GPU), EB, "S0R", "RS0", 2000), 3)
+        bus += bb
+    value = (nbytes if n == 1 else bus) / secs / 1e9
+    unit = "GB/s" if n == 1 else "GB/s per GPU"
+    s1, b1, bb1 = w.step(1)
     line = {
-        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": ws,
+        "metric": METRIC, "value": round(value, 3), "unit": unit, "n_gpus": n,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * secs / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (splitmix64 bit patterns, oracle_fill)",
         "impl": "reference",
-        "config": {"workload": "configs[1]: mesh of 8, S0R->RR all-gather + S0R->RS0 all-to-all",
-                   "tensor": list(shape), "mesh": [8], "mode": "host RAM, all host threads",
-                   "parallelism": "cpu"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
+        "config": {"workload": f"configs[1]: mesh of {ndev}, S0R->RR all-gather + S0R->RS0 "
+                               "all-to-all",
+                   "tensor": list(shape), "mesh": [ndev],
+                   "mode": "host RAM, all host threads", "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 3), "unit": unit, "cores": threads,
                          "kind": "reference" if _ref_available() else "port",
-                         "sample": f"per step: S0R->RR + S0R->RS0 of a [{shape[0]},{shape[1]}] "
-                                   "bf16 tensor on 8 simulated devices (1/16 of the GPU "
-                                   "workload); reference planner (oracle/_ref) picks the path, "
-                                   "the C oracle moves the bytes"},
-        "reference_planner_us_per_path": planner_us,
-        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                         "cpu_model": cpu_model(),
+                         "single_thread": {"value": round((b1 if n == 1 else bb1) / s1 / 1e9, 3),
+                                           "unit": unit, "cores": 1,
+                                           "ms_per_step": round(1e3 * s1, 1)},
+                         "sample": f"per step: S0R->RR + S0R->RS0 of the full "
+                                   f"[{shape[0]},{shape[1]}] bf16 tensor on {ndev} simulated "
+                                   "devices (the GPU arm's exact workload); the reference "
+                                   "planner (oracle/_ref) picks the path, the C oracle moves "
+                                   "the bytes"},
+        "planner": planner_timings(),
+        "e2e": {"value": round(value, 3), "unit": unit, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
+
+
+def size_point(args, shape, dev, hbm_peak, iters=10):
+    """One extra config-2 size on the simulated mesh of 8 (e.g. the sweep's
+    4 GiB top): S0R->RR + S0R->RS0, device time per step, pack HBM GB/s."""
+    import torch
+
+    from paper_2302_02599_b200 import ShardingSpec, TensorMeta, find_transform_path
+    from paper_2302_02599_b200.runtime import Mesh
+
+    mesh = Mesh.local([8], device=dev.index or 0)
+    meta = TensorMeta(shape, EB)
+    s = ShardingSpec.parse("S0R", 1)
+    ins = [torch.empty(s.local_shape(meta, mesh.geo), dtype=torch.bfloat16, device=dev)
+           for _ in range(8)]
+    for x in ins:
+        x.view(torch.int16).random_(-32768, 32767)
+    stream = torch.cuda.current_stream()
+    rows, total_b, total_ms = [], 0, 0.0
+    for a, b in CONVERSIONS:
+        t = ShardingSpec.parse(b, 1)
+        outs = [torch.empty(t.local_shape(meta, mesh.geo), dtype=torch.bfloat16, device=dev)
+                for _ in range(8)]
+        conv = mesh.prepare(find_transform_path(s, t, mesh.geo, meta), meta, fuse=True)
+        tr = mesh.exchange_traffic(s, t, meta)
+        nbytes = tr["hbm_read"] + tr["hbm_write"]
+        for _ in range(3):
+            conv(ins, outs, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            conv(ins, outs, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        rows.append({"conversion": f"{a}->{b}", "ms": round(ms, 4), "hbm_bytes": nbytes,
+                     "gbs": round(nbytes / ms / 1e6, 1),
+                     "frac": round(nbytes / ms / 1e6 / hbm_peak, 4)})
+        total_b += nbytes
+        total_ms += ms
+        conv.close()
+        del outs
+        torch.cuda.empty_cache()
+    mesh.close()
+    del ins
+    torch.cuda.empty_cache()
+    return {"tensor": list(shape), "mesh": [8], "ms_per_step": round(total_ms, 4),
+            "value": round(total_b / total_ms / 1e6, 1), "unit": "GB/s",
+            "frac": round(total_b / total_ms / 1e6 / hbm_peak, 4), "per_conversion": rows}
+
+
+def spawn(args):
+    """`--gpus N` outside torchrun: re-launch this script as N ranks under
+    torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous) and
+    pass rank 0's line through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -791,13 +1000,21 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs 3/4 mesh sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
-                    help="N > 1: fused peer-memory pull (default) or NCCL p2p + pack/unpack")
+                    help="N > 1: fused peer-memory pull (default) or NCCL per mesh-axis "
+                         "communicator + pack/unpack kernels")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    ws = dist_env()[0]
+    if "WORLD_SIZE" in os.environ and ws != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}")
     if args.impl == "reference":
         run_reference(args)
-    elif dist_env()[0] > 1 and args.transport == "peer":
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
+    if ws > 1 and args.transport == "peer":
         if not run_ours_peer(args):
             run_ours(args)
     else:

@@ -111,8 +111,10 @@ def shards(global_: np.ndarray, dims: list, mesh) -> list:
     return [local(global_, dims, mesh, d) for d in range(n)]
 
 
-def apply_step(kind, tdim, target, axis, shape, dims, mesh, inputs: list) -> list:
-    """One reference step on simulated devices (C restatement)."""
+def apply_step(kind, tdim, target, axis, shape, dims, mesh, inputs: list, outs=None) -> list:
+    """One reference step on simulated devices (C restatement). `outs`:
+    optional preallocated output shards (reused across calls by the CPU
+    baseline, so it times the byte movement, not page faults)."""
     new = [list(a) for a in dims]
     if kind == 0:
         new[tdim].pop()
@@ -121,7 +123,8 @@ def apply_step(kind, tdim, target, axis, shape, dims, mesh, inputs: list) -> lis
     elif kind == 3:
         new[tdim].pop()
         new[target].append(axis)
-    outs = [np.empty(local_shape(shape, new, mesh), dtype=inputs[0].dtype) for _ in inputs]
+    if outs is None:
+        outs = [np.empty(local_shape(shape, new, mesh), dtype=inputs[0].dtype) for _ in inputs]
     ins = (C.c_void_p * len(inputs))(*[a.ctypes.data for a in inputs])
     ops = (C.c_void_p * len(outs))(*[a.ctypes.data for a in outs])
     rc = lib().oracle_apply_step(kind, tdim, target, axis, (C.c_int64 * len(shape))(*shape),
@@ -131,11 +134,13 @@ def apply_step(kind, tdim, target, axis, shape, dims, mesh, inputs: list) -> lis
     return outs, new
 
 
-def replay(shape, src_dims, mesh, steps, inputs: list) -> list:
-    """Replay steps [(kind, tdim, target, axis, ...)] from src shards."""
+def replay(shape, src_dims, mesh, steps, inputs: list, outs=None) -> list:
+    """Replay steps [(kind, tdim, target, axis, ...)] from src shards
+    (`outs`: optional preallocated shards for the last step's result)."""
     cur, dims = inputs, [list(a) for a in src_dims]
-    for s in steps:
-        cur, dims = apply_step(s[0], s[1], s[2], s[3], shape, dims, mesh, cur)
+    for i, s in enumerate(steps):
+        last = outs if i + 1 == len(steps) else None
+        cur, dims = apply_step(s[0], s[1], s[2], s[3], shape, dims, mesh, cur, last)
     return cur
 
 
