@@ -400,11 +400,19 @@ def run_ours(args):
     from paper_2302_02599_b200.runtime import Mesh, launch_count
 
     ws, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
 
+        if torch.cuda.device_count() < ws:
+            # ranks share a GPU (functional run): NCCL refuses two ranks of one
+            # host on one device, so each rank poses as its own host and NCCL
+            # connects them over sockets on loopback (tests/test_gpu_nccl.py)
+            os.environ.setdefault("NCCL_HOSTID", f"apl-bench-host-{rank}")
+            os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+            os.environ.setdefault("NCCL_IB_DISABLE", "1")
         dist.init_process_group("nccl", device_id=dev)
         mesh = Mesh.from_process_group([ws])
         shape = workload_shape(ws)

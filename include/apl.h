@@ -174,6 +174,17 @@ int apl_mesh_create_nccl(const apl_mesh_desc* mesh, int rank, const uint8_t* ncc
                          int cuda_device, apl_mesh** out);
 int apl_mesh_destroy(apl_mesh* mesh);
 
+/* Failure detection for NCCL meshes (the reference has no
+ * runtime): polls ncclCommGetAsyncError on the world and every axis-subset
+ * communicator. *state = 0 healthy, 7 (ncclInProgress) an operation still
+ * completing, else the first ncclResult_t error. Simulated and peer meshes
+ * report 0. apl_mesh_abort runs ncclCommAbort on every communicator (after a
+ * timeout or an async error): pending NCCL kernels return, the mesh becomes
+ * unusable (later NCCL calls fail with APL_ERR_NCCL) and destroy skips
+ * ncclCommDestroy. */
+int apl_mesh_health(apl_mesh* mesh, int* state);
+int apl_mesh_abort(apl_mesh* mesh);
+
 /* Distributed mesh over peer memory only (no NCCL): the transport is CUDA
  * IPC-mapped peer pointers (NVLink through NVSwitch between GPUs; also valid
  * between processes sharing one GPU). Used by apl_run_pull. */

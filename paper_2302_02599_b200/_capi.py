@@ -96,6 +96,8 @@ _SIGS = {
     "apl_mesh_create_nccl": (C.c_int, [P(MeshDesc), C.c_int, P(C.c_uint8), C.c_int,
                                        P(C.c_void_p)]),
     "apl_mesh_destroy": (C.c_int, [C.c_void_p]),
+    "apl_mesh_health": (C.c_int, [C.c_void_p, P(C.c_int)]),
+    "apl_mesh_abort": (C.c_int, [C.c_void_p]),
     "apl_mesh_create_peer": (C.c_int, [P(MeshDesc), C.c_int, C.c_int, P(C.c_void_p)]),
     "apl_peer_alloc": (C.c_int, [C.c_void_p, C.c_size_t, P(C.c_void_p), P(C.c_uint8)]),
     "apl_peer_open": (C.c_int, [C.c_void_p, P(C.c_uint8), P(C.c_void_p)]),

@@ -558,6 +558,38 @@ int apl_mesh_destroy(apl_mesh* mesh) {
   return guarded([&] { delete mesh; });
 }
 
+int apl_mesh_health(apl_mesh* mesh, int* state) {
+  return guarded([&] {
+    need(mesh && state, "null argument");
+    apl::Mesh& m = mesh->impl;
+    *state = 0;
+    if (m.aborted) {
+      *state = static_cast<int>(ncclInvalidUsage);
+      return;
+    }
+    auto poll = [&](ncclComm_t c) {
+      if (c == nullptr || (*state != 0 && *state != static_cast<int>(ncclInProgress))) return;
+      ncclResult_t r = ncclSuccess;
+      apl::check_nccl(ncclCommGetAsyncError(c, &r), "ncclCommGetAsyncError");
+      if (r != ncclSuccess) *state = static_cast<int>(r);
+    };
+    poll(m.world);
+    for (auto& [mask, c] : m.sub) poll(c);
+  });
+}
+
+int apl_mesh_abort(apl_mesh* mesh) {
+  return guarded([&] {
+    need(mesh, "null mesh");
+    apl::Mesh& m = mesh->impl;
+    if (m.aborted) return;
+    m.aborted = true;
+    for (auto& [mask, c] : m.sub)
+      if (c != nullptr) ncclCommAbort(c);
+    if (m.world != nullptr) ncclCommAbort(m.world);
+  });
+}
+
 int apl_mesh_info(const apl_mesh* mesh, int* num_devices, int* first_local, int* num_local,
                   int* is_distributed) {
   return guarded([&] {

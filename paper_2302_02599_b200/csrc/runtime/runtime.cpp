@@ -445,8 +445,10 @@ Mesh::~Mesh() {
   for (auto& [ptr, owned] : peer_buffers)
     if (owned) cudaFree(ptr);
     else cudaIpcCloseMemHandle(ptr);
-  for (auto& [mask, comm] : sub) ncclCommDestroy(comm);
-  if (world != nullptr) ncclCommDestroy(world);
+  if (!aborted) {
+    for (auto& [mask, comm] : sub) ncclCommDestroy(comm);
+    if (world != nullptr) ncclCommDestroy(world);
+  }
 }
 
 std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec& src,
@@ -677,6 +679,7 @@ void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* 
     run_copies(compiled_for(ex.copies, ex.host_copies, align), t, stream);
     return;
   }
+  if (mesh.aborted) throw RuntimeError(APL_ERR_NCCL, "mesh communicators were aborted");
   if (ws_bytes < exchange_workspace(ex))
     throw RuntimeError(APL_ERR_ARG, "workspace smaller than apl_path_workspace_bytes");
   char* send = static_cast<char*>(ws);
@@ -922,6 +925,7 @@ void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, siz
   }
   if (mask == 0 || count == 0) return;
   if (mesh.distributed) {
+    if (mesh.aborted) throw RuntimeError(APL_ERR_NCCL, "mesh communicators were aborted");
     ncclDataType_t t = dtype == APL_F32 ? ncclFloat32 : dtype == APL_BF16 ? ncclBfloat16 : ncclFloat16;
     check_nccl(ncclAllReduce(bufs[0], bufs[0], count, t, ncclSum, mesh.sub.at(mask), stream),
                "ncclAllReduce");

@@ -187,6 +187,7 @@ struct Mesh {
   int rank = 0;  // distributed: this process's mesh device index
   ncclComm_t world = nullptr;
   std::map<uint32_t, ncclComm_t> sub;  // axis-subset mask -> communicator
+  bool aborted = false;                // apl_mesh_abort ran: communicators are gone
   std::mutex mu;
   std::unordered_map<std::string, std::shared_ptr<Exchange>> exchanges;
   // Peer memory: buffers this process allocated for export (true) or opened

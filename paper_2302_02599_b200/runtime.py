@@ -155,6 +155,46 @@ class Mesh:
         except Exception:
             pass
 
+    # ---- failure detection (NCCL meshes) ---------------------------------------
+    def health(self) -> int:
+        """0 healthy, 7 (ncclInProgress) still completing, else the first
+        ncclResult_t async error of any of the mesh's communicators."""
+        st = C.c_int()
+        check(A.lib().apl_mesh_health(self._h, C.byref(st)))
+        return st.value
+
+    def abort(self) -> None:
+        """ncclCommAbort on every communicator: pending NCCL kernels return."""
+        check(A.lib().apl_mesh_abort(self._h))
+
+    def synchronize(self, stream=None, timeout_s: float = 300.0, poll_s: float = 1e-3) -> None:
+        """Wait for `stream` while polling the communicators' async errors:
+        raises NcclError on an async error, and on a timeout aborts the
+        communicators (so the stream drains instead of hanging) and raises
+        TimeoutError. Simulated meshes just synchronize."""
+        import time
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if not self.distributed:
+            s.synchronize()
+            return
+        from .layout import NcclError
+
+        t0 = time.monotonic()
+        while not s.query():
+            st = self.health()
+            if st not in (0, 7):
+                self.abort()
+                raise NcclError(f"NCCL async error {st} on the mesh's communicators")
+            if time.monotonic() - t0 > timeout_s:
+                self.abort()
+                raise TimeoutError(f"mesh stream did not finish within {timeout_s} s; "
+                                   "communicators aborted")
+            time.sleep(poll_s)
+        st = self.health()
+        if st not in (0, 7):
+            raise NcclError(f"NCCL async error {st} on the mesh's communicators")
+
     # ---- conversions ---------------------------------------------------------
     def workspace_bytes(self, path: TransformPath, meta: TensorMeta, fuse: bool = False) -> int:
         out = C.c_size_t()

@@ -10,6 +10,8 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
+from test_gpu_nccl import drain
+
 pytestmark = pytest.mark.gpu
 
 CASES = {
@@ -78,6 +80,31 @@ def test_peer_pull_exchange_multiprocess(cuda, world):
         res.append(q.get())
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert len(res) == world * len(CASES[world])
+    assert all(ok for *_, ok in res), [r for r in res if not r[-1]]
+
+
+CONFIG3 = ["S01R", "S0S1", "S1S0", "RS01", "RR"]
+FULL_CASES = (
+    [([2, 4], (8192, 8192), 2, a, b) for a in CONFIG3 for b in CONFIG3 if a != b]
+    + [([2, 2, 2], (8192, 8192), 2, "S012R", "RS012"), ([2, 2, 2], (8192, 8192), 2, "RS012", "S012R"),
+       ([2, 2, 2], (512, 512, 256), 2, "S0S1R", "RS1S0"),
+       ([2, 2, 2], (512, 512, 256), 2, "RS1S0", "S0S1R")])
+
+
+def test_peer_pull_config3_config4_full_size(cuda):
+    """BASELINE configs 3 and 4 at their named sizes on 8 ranks: all 20
+    config-3 pairs on 2x4 ([8192, 8192] bf16) and the config-4 chains on
+    2x2x2 ([8192, 8192] and [512, 512, 256]), one pull kernel per rank,
+    bytewise vs the oracle on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 8, port, FULL_CASES, q)) for r in range(8)]
+    for p in procs:
+        p.start()
+    res = drain(procs, q, 900)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert len(res) == 8 * len(FULL_CASES)
     assert all(ok for *_, ok in res), [r for r in res if not r[-1]]
 
 
