@@ -244,6 +244,33 @@ int apl_peer_allreduce(void* const* members, int P, size_t count, int dtype, voi
  * source shards and keeps them unchanged until every rank has pulled. */
 int apl_run_pull(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt, const apl_meta* meta,
                  const void* const* peer_in, void* out, void* stream);
+
+/* The same exchange with its ordering fused in: ONE launch per exchange.
+ * CTA 0 stores `epoch` into slot `rank` of every peer's flag array (this
+ * rank's source is ready), every CTA waits (acquire, system scope, trap after
+ * timeout_ms) until the ranks it actually reads from announced `epoch`, the
+ * pull runs, and the last CTA stores `epoch` into slot P + rank of every
+ * peer's array (done reading). peer_flags[q] = rank q's flag array mapped
+ * here (own entry unused); counter = a zeroed 4-byte device word used by
+ * one exchange at a time (stream-serial). Before overwriting its source the
+ * caller waits for `done` of the ranks apl_exchange_peers lists as readers
+ * (apl_peer_flags_wait). Replaces the store/wait/pull/store sequence. */
+typedef struct {
+  void* const* peer_flags;
+  const void* local_flags;
+  void* counter;
+  uint32_t epoch;
+  uint32_t timeout_ms;
+} apl_peer_sync;
+int apl_run_pull_sync(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                      const apl_meta* meta, const void* const* peer_in, void* out,
+                      const apl_peer_sync* sync, void* stream);
+/* Peers of this rank in a src -> tgt peer exchange: the ranks it reads from
+ * (senders) and the ranks that read its source (readers); arrays of
+ * num_devices entries (either may be NULL to count only). */
+int apl_exchange_peers(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                       const apl_meta* meta, int32_t* senders, int* n_senders, int32_t* readers,
+                       int* n_readers);
 int apl_mesh_info(const apl_mesh* mesh, int* num_devices, int* first_local, int* num_local,
                   int* is_distributed);
 

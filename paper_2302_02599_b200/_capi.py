@@ -54,6 +54,11 @@ class StrategyInfoC(C.Structure):
                 ("comm_buffer_bytes", C.c_int64), ("memory_bytes", C.c_int64)]
 
 
+class PeerSyncC(C.Structure):
+    _fields_ = [("peer_flags", C.POINTER(C.c_void_p)), ("local_flags", C.c_void_p),
+                ("counter", C.c_void_p), ("epoch", C.c_uint32), ("timeout_ms", C.c_uint32)]
+
+
 class PieceC(C.Structure):
     _fields_ = [("sender", C.c_int32), ("receiver", C.c_int32),
                 ("src_lo", C.c_int64 * MAX_DIMS), ("dst_lo", C.c_int64 * MAX_DIMS),
@@ -103,6 +108,10 @@ _SIGS = {
     "apl_peer_open": (C.c_int, [C.c_void_p, P(C.c_uint8), P(C.c_void_p)]),
     "apl_run_pull": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_void_p), C.c_void_p,
                                C.c_void_p]),
+    "apl_run_pull_sync": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_void_p),
+                                    C.c_void_p, P(PeerSyncC), C.c_void_p]),
+    "apl_exchange_peers": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_int32),
+                                     P(C.c_int), P(C.c_int32), P(C.c_int)]),
     "apl_mesh_info": (C.c_int, [C.c_void_p, P(C.c_int), P(C.c_int), P(C.c_int), P(C.c_int)]),
     "apl_path_workspace_bytes": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Step), C.c_int,
                                            P(Meta), C.c_uint, P(C.c_size_t)]),

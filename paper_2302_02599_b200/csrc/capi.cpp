@@ -479,6 +479,36 @@ int apl_run_pull(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt, const
   });
 }
 
+int apl_run_pull_sync(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                      const apl_meta* meta, const void* const* peer_in, void* out,
+                      const apl_peer_sync* sync, void* stream) {
+  return guarded([&] {
+    need(mesh && peer_in && out && sync, "null argument");
+    apl::PeerSyncArgs a{sync->peer_flags, sync->local_flags, sync->counter, sync->epoch,
+                        static_cast<uint64_t>(sync->timeout_ms) * 1000000ull};
+    apl::run_pull_sync(mesh->impl, to_spec(src), to_spec(tgt), to_meta(meta), peer_in, out, a,
+                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+int apl_exchange_peers(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                       const apl_meta* meta, int32_t* senders, int* n_senders, int32_t* readers,
+                       int* n_readers) {
+  return guarded([&] {
+    need(mesh && n_senders && n_readers, "null argument");
+    need(mesh->impl.distributed, "needs a distributed mesh");
+    const autoplan::ShardingSpec s = to_spec(src), t = to_spec(tgt);
+    const autoplan::TensorMeta m = to_meta(meta);
+    if (!s.valid_for(m, mesh->impl.geo) || !t.valid_for(m, mesh->impl.geo))
+      throw apl::RuntimeError(APL_ERR_SHAPE, "spec is not valid for the tensor/mesh");
+    auto ex = apl::get_exchange(mesh->impl, s, t, m);
+    *n_senders = static_cast<int>(ex->pull_senders.size());
+    *n_readers = static_cast<int>(ex->pull_readers.size());
+    for (size_t i = 0; senders && i < ex->pull_senders.size(); ++i) senders[i] = ex->pull_senders[i];
+    for (size_t i = 0; readers && i < ex->pull_readers.size(); ++i) readers[i] = ex->pull_readers[i];
+  });
+}
+
 int apl_peer_flags_store(void* const* remote_flags, int n, int slot, uint32_t epoch,
                          void* stream) {
   return guarded([&] {

@@ -72,6 +72,30 @@ __device__ __forceinline__ uint32_t load_stream(const uint32_t* p) { return __ld
 __device__ __forceinline__ uint16_t load_stream(const uint16_t* p) { return __ldg(p); }
 __device__ __forceinline__ uint8_t load_stream(const uint8_t* p) { return __ldg(p); }
 
+// Coherent (weak, L1-bypassing) loads for the fused peer exchange: its
+// sources are written by other GPUs while the kernel is already running
+// (it acquires their ready flags first), so the non-coherent path is not
+// allowed there.
+template <typename T>
+__device__ __forceinline__ T load_coherent(const T* p) {
+  return *reinterpret_cast<const volatile T*>(p);
+}
+template <>
+__device__ __forceinline__ uint4 load_coherent<uint4>(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 load_coherent<uint2>(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+  return r;
+}
+
 // Stores; `cs` = cache-streaming (evict-first) for outputs far larger than L2.
 template <typename T>
 __device__ __forceinline__ void store_v(T* p, const T& v, bool cs) {
@@ -119,10 +143,10 @@ __device__ __forceinline__ void resolve(const DevCopy& c, uint32_t local, const 
   }
 }
 
-template <int V, int U, int NO, int MINB, bool SPLIT>
-__global__ void __launch_bounds__(256, MINB)
-    box_copy_kernel(const DevCopy* __restrict__ table, int ntasks, int64_t first, int64_t total,
-                    int lockstep, const __grid_constant__ PtrTable ptrs) {
+template <int V, int U, int NO, bool SPLIT, bool COHERENT>
+__device__ __forceinline__ void box_copy_body(const DevCopy* __restrict__ table, int ntasks,
+                                              int64_t first, int64_t total, int lockstep,
+                                              const PtrTable& ptrs) {
   using T = typename Vec<V>::T;
   constexpr int NR = NO > 0 ? NO : 1;
   // The launch's descriptor table (<= kCopySmemTasks entries) is staged in
@@ -239,7 +263,10 @@ __global__ void __launch_bounds__(256, MINB)
           sp = ptrs.src[c.src_buf];
           slow_task[u] = t;
         }
-        v[u] = load_stream(reinterpret_cast<const T*>(sp + so));
+        if constexpr (COHERENT)
+          v[u] = load_coherent(reinterpret_cast<const T*>(sp + so));
+        else
+          v[u] = load_stream(reinterpret_cast<const T*>(sp + so));
       }
     }
 #pragma unroll
@@ -258,6 +285,71 @@ __global__ void __launch_bounds__(256, MINB)
       }
     }
     if (lockstep & 1) __syncthreads();
+  }
+}
+
+template <int V, int U, int NO, int MINB, bool SPLIT>
+__global__ void __launch_bounds__(256, MINB)
+    box_copy_kernel(const DevCopy* __restrict__ table, int ntasks, int64_t first, int64_t total,
+                    int lockstep, const __grid_constant__ PtrTable ptrs) {
+  box_copy_body<V, U, NO, SPLIT, false>(table, ntasks, first, total, lockstep, ptrs);
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The whole peer exchange of one rank in ONE launch (box_copy.cuh,
+// PeerSync): CTA 0 announces this rank's source (stores `ready` into every
+// peer's flag array), every CTA acquires the ready flags of the ranks it
+// actually reads from, the copy body pulls over peer pointers with coherent
+// loads, and the last CTA to finish announces `done` to every peer.
+template <int V, int U, int NO, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    box_pull_sync_kernel(const DevCopy* __restrict__ table, int ntasks, int64_t first,
+                         int64_t total, int lockstep, const __grid_constant__ PtrTable ptrs,
+                         const __grid_constant__ PeerSync sync) {
+  const int t = threadIdx.x;
+  if (sync.mode & PeerSync::kAnnounce) {
+    if (blockIdx.x == 0 && t < sync.n_remote) {
+      __threadfence_system();  // the source (written by earlier kernels) before the flag
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sync.remote[t] + sync.ready_slot),
+                   "r"(sync.epoch)
+                   : "memory");
+    }
+    if (t < sync.n_wait) {
+      const uint32_t* f = sync.local + sync.wait_slot[t];
+      const uint64_t t0 = global_ns();
+      while (true) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (static_cast<int32_t>(v - sync.epoch) >= 0) break;  // wrap-safe v >= epoch
+        __nanosleep(128);
+        if (global_ns() - t0 > sync.timeout_ns) __trap();  // a lost peer: fail, do not hang
+      }
+    }
+    __syncthreads();
+  }
+  box_copy_body<V, U, NO, false, true>(table, ntasks, first, total, lockstep, ptrs);
+  if (sync.mode & PeerSync::kDone) {
+    __syncthreads();  // every load of this CTA has returned (its stores consumed them)
+    __shared__ unsigned int last;
+    if (t == 0) {
+      __threadfence();
+      last = atomicAdd(sync.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (last) {
+      if (t == 0) *sync.counter = 0;  // stream-serial reuse by the next exchange
+      if (t < sync.n_remote) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sync.remote[t] + sync.done_slot),
+                     "r"(sync.epoch)
+                     : "memory");
+      }
+    }
   }
 }
 
@@ -397,6 +489,80 @@ int sm_count() {
     if (g_num_sms <= 0) g_num_sms = 148;
   }
   return g_num_sms;
+}
+
+namespace {
+
+template <int V, int U, int MINB>
+void launch_pull_sync_v(int no, int64_t total, const DevCopy* t, const int64_t* begins, int n,
+                        const PtrTable& p, const PeerSync& sync, cudaStream_t s) {
+  constexpr int kThreads = 256;
+  // An exchange with nothing to move still runs (grid 1): its flags order
+  // the epoch for every peer.
+  const int slices = n > 0 ? (n + kCopySmemTasks - 1) / kCopySmemTasks : 1;
+  for (int sl = 0; sl < slices; ++sl) {
+    const int k = sl * kCopySmemTasks;
+    const int m = n > 0 ? std::min(kCopySmemTasks, n - k) : 0;
+    const int64_t first = n > 0 ? begins[k] : 0;
+    const int64_t end = k + m < n ? begins[k + m] : total;
+    const int64_t chunk = int64_t{kThreads} * U;
+    const int64_t chunks = std::max<int64_t>(1, (end - first + chunk - 1) / chunk);
+    const int grid = static_cast<int>(std::min<int64_t>(chunks, static_cast<int64_t>(sm_count()) * MINB));
+    const size_t smem = static_cast<size_t>(m) * sizeof(DevCopy);
+    PeerSync y = sync;
+    y.mode = (sl == 0 ? (sync.mode & PeerSync::kAnnounce) : 0) |
+             (sl + 1 == slices ? (sync.mode & PeerSync::kDone) : 0);
+    const DevCopy* tk = t + k;
+    const int lockstep = no == 0 ? 1 : 0;
+    switch (no) {
+      case 0:
+        box_pull_sync_kernel<V, U, 0, MINB><<<grid, kThreads, smem, s>>>(tk, m, first, end, lockstep, p, y);
+        break;
+      case 1:
+        box_pull_sync_kernel<V, U, 1, MINB><<<grid, kThreads, smem, s>>>(tk, m, first, end, lockstep, p, y);
+        break;
+      case 2:
+        box_pull_sync_kernel<V, U, 2, MINB><<<grid, kThreads, smem, s>>>(tk, m, first, end, lockstep, p, y);
+        break;
+      case 3:
+        box_pull_sync_kernel<V, U, 3, MINB><<<grid, kThreads, smem, s>>>(tk, m, first, end, lockstep, p, y);
+        break;
+      default:
+        box_pull_sync_kernel<V, U, kCopyMaxOuter, MINB>
+            <<<grid, kThreads, smem, s>>>(tk, m, first, end, lockstep, p, y);
+        break;
+    }
+  }
+}
+
+}  // namespace
+
+// One launch per fused peer exchange (tables over kCopySmemTasks descriptors
+// take one launch per slice: the first announces and acquires, the last
+// announces done).
+cudaError_t launch_box_pull_sync(const DevCopy* d_table, const int64_t* begins, int ntasks,
+                                 int64_t total_units, int vec_bytes, int max_outer,
+                                 const PtrTable& ptrs, const PeerSync& sync, cudaStream_t stream) {
+  if (sync.n_remote > kPeerMaxRanks || sync.n_wait > kPeerMaxRanks) return cudaErrorInvalidValue;
+  switch (ntasks > 0 ? vec_bytes : 16) {
+    case 16:
+      launch_pull_sync_v<16, 4, 4>(max_outer, total_units, d_table, begins, ntasks, ptrs, sync, stream);
+      break;
+    case 8:
+      launch_pull_sync_v<8, 8, 2>(max_outer, total_units, d_table, begins, ntasks, ptrs, sync, stream);
+      break;
+    case 4:
+      launch_pull_sync_v<4, 8, 2>(max_outer, total_units, d_table, begins, ntasks, ptrs, sync, stream);
+      break;
+    case 2:
+      launch_pull_sync_v<2, 8, 2>(max_outer, total_units, d_table, begins, ntasks, ptrs, sync, stream);
+      break;
+    default:
+      launch_pull_sync_v<1, 8, 2>(max_outer, total_units, d_table, begins, ntasks, ptrs, sync, stream);
+      break;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_box_copy(const DevCopy* d_table, const int64_t* begins, int ntasks,

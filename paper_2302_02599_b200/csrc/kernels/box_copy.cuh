@@ -78,4 +78,19 @@ struct PtrTable {
   char* dst[kCopyMaxPtrs];
 };
 
+// Device-side ordering of a fused peer exchange (box_pull_sync_kernel).
+// Flag arrays hold uint32 epochs: slot p = "rank p's source of this epoch is
+// written", slot P + p = "rank p finished reading its sources".
+constexpr int kPeerMaxRanks = 64;
+struct PeerSync {
+  enum : int { kAnnounce = 1, kDone = 2 };
+  uint32_t* remote[kPeerMaxRanks];   // every peer's flag array (mapped here)
+  const uint32_t* local;             // this rank's flag array
+  unsigned int* counter;             // zeroed device counter (last-CTA election)
+  int32_t wait_slot[kPeerMaxRanks];  // ready slots of the ranks this pull reads from
+  int32_t n_remote, n_wait, ready_slot, done_slot, mode;
+  uint32_t epoch;
+  uint64_t timeout_ns;
+};
+
 }  // namespace apl

@@ -502,6 +502,10 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
       // the table of peer-mapped source shards.
       ex->host_pull.push_back(make_copy(static_cast<int>(p.sender), ls, p.src_lo, 0, lt, p.dst_lo,
                                         p.ext, eb));
+      if (p.sender != me &&
+          std::find(ex->pull_senders.begin(), ex->pull_senders.end(), p.sender) ==
+              ex->pull_senders.end())
+        ex->pull_senders.push_back(static_cast<int>(p.sender));
       const int64_t bytes = p.elements() * eb;
       if (p.sender == me) {
         ex->host_pre.push_back(make_copy(0, ls, p.src_lo, 0, lt, p.dst_lo, p.ext, eb));
@@ -522,6 +526,9 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
     }
     for (const Piece& p : pieces_for_sender(src, tgt, mesh.geo, meta, me)) {
       if (p.receiver == me) continue;
+      if (std::find(ex->pull_readers.begin(), ex->pull_readers.end(), p.receiver) ==
+          ex->pull_readers.end())
+        ex->pull_readers.push_back(static_cast<int>(p.receiver));
       const int64_t bytes = p.elements() * eb;
       ex->wire_bytes_out += bytes;
       if (box_contiguous(ls, p.ext)) {
@@ -777,6 +784,50 @@ void run_pull(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::Sha
   auto it = ex->pull.find(align);
   if (it == ex->pull.end()) it = ex->pull.emplace(align, compile_copies(ex->host_pull, align, false)).first;
   run_copies(it->second, t, stream);
+}
+
+void run_pull_sync(Mesh& mesh, const autoplan::ShardingSpec& src,
+                   const autoplan::ShardingSpec& tgt, const autoplan::TensorMeta& meta,
+                   const void* const* peer_in, void* out, const PeerSyncArgs& sync,
+                   cudaStream_t stream) {
+  if (!mesh.distributed) throw RuntimeError(APL_ERR_ARG, "peer pull needs a distributed mesh");
+  if (!src.valid_for(meta, mesh.geo) || !tgt.valid_for(meta, mesh.geo))
+    throw RuntimeError(APL_ERR_SHAPE, "spec is not valid for the tensor/mesh");
+  const int64_t p = mesh.geo.num_devices();
+  if (p > kCopyMaxPtrs || p > kPeerMaxRanks)
+    throw RuntimeError(APL_ERR_ARG, "mesh too large for one pull launch");
+  if (sync.flags == nullptr || sync.local_flags == nullptr || sync.counter == nullptr)
+    throw RuntimeError(APL_ERR_ARG, "null flag arrays / counter");
+  DeviceGuard guard(mesh.device);
+  auto ex = get_exchange(mesh, src, tgt, meta);
+  PtrTable t{};
+  int align = std::min(natural_vec(ex->host_pull), ptr_align(out));
+  for (int64_t i = 0; i < p; ++i) {
+    t.src[i] = static_cast<const char*>(peer_in[i]);
+    align = std::min(align, ptr_align(peer_in[i]));
+  }
+  t.dst[0] = static_cast<char*>(out);
+  PeerSync y{};
+  for (int64_t q = 0; q < p; ++q) {
+    if (q == mesh.rank) continue;
+    y.remote[y.n_remote++] = static_cast<uint32_t*>(sync.flags[q]);
+  }
+  for (int s : ex->pull_senders) y.wait_slot[y.n_wait++] = s;
+  y.local = static_cast<const uint32_t*>(sync.local_flags);
+  y.counter = static_cast<unsigned int*>(sync.counter);
+  y.ready_slot = mesh.rank;
+  y.done_slot = static_cast<int32_t>(p) + mesh.rank;
+  y.mode = PeerSync::kAnnounce | PeerSync::kDone;
+  y.epoch = sync.epoch;
+  y.timeout_ns = sync.timeout_ns;
+  std::lock_guard<std::mutex> hold(mesh.mu);
+  auto it = ex->pull.find(align);
+  if (it == ex->pull.end())
+    it = ex->pull.emplace(align, compile_copies(ex->host_pull, align, false)).first;
+  const CompiledCopies& c = it->second;
+  check_cuda(launch_box_pull_sync(c.table, c.begins.data(), c.ntasks, c.total_units, c.vec,
+                                  c.max_outer, t, y, stream),
+             "fused peer exchange launch");
 }
 
 namespace {

@@ -35,6 +35,11 @@ cudaError_t launch_box_copy(const DevCopy* d_table, const int64_t* begins, int n
                             int64_t total_units, int vec_bytes, int max_outer, int max_fan, bool split,
                             const PtrTable& ptrs, cudaStream_t stream,
                             int64_t write_bytes = 0);
+// Fused peer exchange: ready-flag announce + acquire, pull, done-flag
+// announce in one launch (box_copy.cu, box_pull_sync_kernel).
+cudaError_t launch_box_pull_sync(const DevCopy* d_table, const int64_t* begins, int ntasks,
+                                 int64_t total_units, int vec_bytes, int max_outer,
+                                 const PtrTable& ptrs, const PeerSync& sync, cudaStream_t stream);
 cudaError_t launch_allreduce_local(void* const* bufs, const int* members, int groups,
                                    int group_size, size_t count, int dtype,
                                    cudaStream_t stream);
@@ -151,6 +156,8 @@ struct Exchange {
   std::vector<CopyDesc> host_post;    // distributed: unpack
   std::vector<CopyDesc> host_pull;    // distributed, peer mode: one kernel pulls every
                                       // piece straight from the senders' shards
+  std::vector<int> pull_senders;      // peer mode: ranks this rank reads from (not itself)
+  std::vector<int> pull_readers;      // peer mode: ranks that read this rank's source
   std::map<int, CompiledCopies> copies, pre, post, pull;  // keyed by vector width
   struct Xfer {
     int peer;
@@ -244,6 +251,20 @@ void run_conversion(Conversion& cv, const void* const* in, void* const* out, voi
 void run_pull(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::ShardingSpec& tgt,
               const autoplan::TensorMeta& meta, const void* const* peer_in, void* out,
               cudaStream_t stream);
+
+// The fused peer exchange in one launch: flags (every rank's flag array
+// mapped here, own entry ignored), a zeroed device counter, the epoch.
+struct PeerSyncArgs {
+  void* const* flags;
+  const void* local_flags;
+  void* counter;
+  uint32_t epoch;
+  uint64_t timeout_ns;
+};
+void run_pull_sync(Mesh& mesh, const autoplan::ShardingSpec& src,
+                   const autoplan::ShardingSpec& tgt, const autoplan::TensorMeta& meta,
+                   const void* const* peer_in, void* out, const PeerSyncArgs& sync,
+                   cudaStream_t stream);
 
 size_t path_workspace(Mesh& mesh, const autoplan::ShardingSpec& src,
                       const autoplan::ShardingSpec& tgt,

@@ -432,6 +432,10 @@ class PeerMesh:
             self.peer_ptrs.append(p.value)
             flag_ptrs.append(q.value)
         self._table = (C.c_void_p * len(self.peer_ptrs))(*self.peer_ptrs)
+        self._all_flags = (C.c_void_p * P)(*flag_ptrs)
+        self._counter = torch.zeros(4, dtype=torch.int32, device=f"cuda:{device}")
+        self._peers = {}           # (src, tgt, shape, eb) -> (senders, readers)
+        self._last_readers = None  # done slots wait_readers() waits on
         others = [q for q in range(P) if q != rank]
         self._peer_flags = (C.c_void_p * len(others))(*[flag_ptrs[q] for q in others])
         self._n_others = len(others)
@@ -471,22 +475,57 @@ class PeerMesh:
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)
 
+    def exchange_peers(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta):
+        """(ranks this rank reads from, ranks that read this rank's source)."""
+        key = (src.to_string(), tgt.to_string(), tuple(meta.shape), meta.dtype_bytes)
+        hit = self._peers.get(key)
+        if hit is None:
+            P = self.geo.num_devices()
+            sa, ra = (C.c_int32 * P)(), (C.c_int32 * P)()
+            ns, nr = C.c_int(), C.c_int()
+            check(A.lib().apl_exchange_peers(self._h, C.byref(src.c()), C.byref(tgt.c()),
+                                             C.byref(meta.c()), sa, C.byref(ns), ra,
+                                             C.byref(nr)))
+            hit = self._peers[key] = (list(sa[:ns.value]), list(ra[:nr.value]))
+        return hit
+
     def exchange_async(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta,
-                       out: torch.Tensor, stream=None) -> int:
+                       out: torch.Tensor, stream=None, fused: bool | None = None) -> int:
         """Stream-ordered exchange synchronised on the device, no host
-        barrier: announce this rank's source (ready flag at every peer), wait
-        until every peer announced theirs, pull (one kernel), announce that
-        this rank finished reading. Returns the epoch. Call wait_readers()
-        before overwriting the exported source for the next epoch."""
+        barrier. fused (default; APL_PEER_FUSED=0 selects the 4-launch form):
+        ONE kernel announces this rank's source (ready flag at every peer),
+        acquires the ready flags of the ranks it actually reads from, pulls,
+        and its last CTA announces that this rank finished reading
+        (apl_run_pull_sync). Unfused: flag-store kernel, flag-wait kernel on
+        every peer, pull kernel, flag-store kernel. Returns the epoch. Call
+        wait_readers() before overwriting the exported source."""
+        if fused is None:
+            import os
+
+            fused = os.environ.get("APL_PEER_FUSED", "1") != "0"
         self.epoch += 1
         e, r, P = self.epoch, self.rank, self.geo.num_devices()
         sh = _stream_handle(stream)
         lib = A.lib()
+        if fused:
+            if src.per_device_bytes(meta, self.geo) > self.shard_bytes:
+                raise ValueError("source shard larger than the exported buffer")
+            if out.numel() * out.element_size() < tgt.per_device_bytes(meta, self.geo):
+                raise ValueError("output too small")
+            _, readers = self.exchange_peers(src, tgt, meta)
+            sync = A.PeerSyncC(self._all_flags, self.flags.data_ptr(), self._counter.data_ptr(),
+                               e, self.timeout_ms)
+            check(lib.apl_run_pull_sync(self._h, C.byref(src.c()), C.byref(tgt.c()),
+                                        C.byref(meta.c()), self._table,
+                                        C.c_void_p(out.data_ptr()), C.byref(sync), sh))
+            self._last_readers = readers
+            return e
         check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, r, e, sh))
         check(lib.apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), self._ready_slots,
                                       self._n_others, e, self.timeout_ms, sh))
         self.pull(src, tgt, meta, out, stream=stream)
         check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, P + r, e, sh))
+        self._last_readers = None
         return e
 
     def shared_buffer(self, nbytes: int):
@@ -546,6 +585,7 @@ class PeerMesh:
         staging, c_out, slabs, outs = bufs[key]
         self.epoch += 1
         e = self.epoch
+        self._last_readers = None  # every rank reads every slab
         sh = _stream_handle(stream)
         lib = A.lib()
         check(lib.apl_peer_gemm_scatter(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), slabs, P,
@@ -585,6 +625,15 @@ class PeerMesh:
         """Stream-ordered: block until every peer finished reading this
         rank's source of the last epoch (then it may be overwritten)."""
         if self.epoch == 0:
+            return
+        if self._last_readers is not None:  # only the ranks that read it
+            if not self._last_readers:
+                return
+            P = self.geo.num_devices()
+            slots = (C.c_int32 * len(self._last_readers))(*[P + q for q in self._last_readers])
+            check(A.lib().apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), slots,
+                                              len(self._last_readers), self.epoch,
+                                              self.timeout_ms, _stream_handle(stream)))
             return
         check(A.lib().apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), self._done_slots,
                                           self._n_others, self.epoch, self.timeout_ms,
