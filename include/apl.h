@@ -118,6 +118,14 @@ const char* apl_last_error(void); /* thread-local message of the last failure */
 /* ---- spec algebra + path search (host only; no GPU needed) ------------ */
 int apl_mesh_desc_uniform(const int64_t* shape, int ndim, apl_mesh_desc* out);
 int apl_parse_mesh_shape(const char* text, int64_t* shape, int cap, int* ndim);
+/* Mesh documents (reference mesh_to_json / mesh_from_json, cluster.hpp:95-96,
+ * cluster.cpp:417-450): to_json writes the reference's five fields with the
+ * uniform assignment "d0".."dN-1" (*len = length without the NUL; buf NULL
+ * to size); from_json validates like the reference (APL_ERR_SCHEMA on a
+ * malformed or inconsistent document) and returns the geometry. */
+int apl_mesh_to_json(const apl_mesh_desc* mesh, double device_flops_per_s, char* buf,
+                     size_t cap, size_t* len);
+int apl_mesh_from_json(const char* text, apl_mesh_desc* out, double* device_flops_per_s);
 int apl_spec_parse(const char* text, int mesh_rank, apl_spec* out);
 int apl_spec_to_string(const apl_spec* spec, char* buf, size_t cap);
 int apl_spec_valid(const apl_spec* spec, const apl_mesh_desc* mesh, const apl_meta* meta,

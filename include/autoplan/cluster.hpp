@@ -61,3 +61,15 @@ double collective_cost(const DeviceMesh& mesh, const std::vector<int>& axes,
 std::string mesh_report(const DeviceMesh& mesh);
 
 }  // namespace autoplan
+
+// Mesh round-trip helpers (reference cluster.hpp:93-96, cluster.cpp:417-450):
+// solution and plan documents embed the mesh. Declared when nlohmann/json is
+// on the include path (the reference's own JSON library); libapl.so is built
+// with it and exports both. Same fields, same SchemaError cases.
+#if __has_include(<nlohmann/json.hpp>)
+#include <nlohmann/json.hpp>
+namespace autoplan {
+nlohmann::json mesh_to_json(const DeviceMesh& mesh);
+DeviceMesh mesh_from_json(const nlohmann::json& doc);
+}  // namespace autoplan
+#endif

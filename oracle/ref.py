@@ -39,6 +39,7 @@ def lib() -> C.CDLL:
         h.ref_time_paths.argtypes = [I64P, C.c_int, I64P, C.c_int, C.c_int, C.c_char_p,
                                      C.c_char_p, C.c_int, C.c_int]
         h.ref_time_paths.restype = C.c_double
+        h.ref_mesh_json.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
         _lib = h
     return _lib
 
@@ -119,3 +120,10 @@ def spec_valid(mesh, shape, eb, spec):
 def time_paths(mesh, shape, eb, src, tgt, iters=1000, hits=False) -> float:
     return lib().ref_time_paths(_arr(mesh), len(mesh), _arr(shape), len(shape), eb,
                                 src.encode(), tgt.encode(), iters, 1 if hits else 0)
+
+
+def mesh_json(text: str):
+    """Reference mesh_from_json -> mesh_to_json: (code, canonical text or message)."""
+    buf = C.create_string_buffer(1 << 16)
+    rc = lib().ref_mesh_json(text.encode(), buf, len(buf))
+    return rc, buf.value.decode()

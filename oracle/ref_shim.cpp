@@ -15,6 +15,7 @@
 //   find_transform_path / conversion_cost        src/layout.cpp:253-329
 //   PathCache::get                               src/layout.cpp:331-346
 //   collective_cost                              src/cluster.cpp:374-400
+//   mesh_to_json / mesh_from_json                src/cluster.cpp:417-450
 //   testutil::all_valid_specs / bfs_min_steps /
 //   replay_path_error                            tests/helpers.hpp:245-363
 //   matmul strategy catalog (generate_strategies) src/intraop.cpp:141-234,497-555,719-767
@@ -166,6 +167,22 @@ int ref_spec_valid(const int64_t* mesh, int mr, const int64_t* shape, int rank, 
     return ShardingSpec::parse(spec, mr).valid_for(meta_of(shape, rank, eb), mesh_of(mesh, mr)) ? 1 : 0;
   } catch (const std::exception& e) {
     return -code_of(e);
+  }
+}
+
+// Reference mesh_from_json -> mesh_to_json round trip of a document
+// (cluster.cpp:417-450): 0 and the canonical dump, or the error class code
+// and message.
+int ref_mesh_json(const char* text, char* out, size_t cap) {
+  try {
+    const DeviceMesh m = mesh_from_json(nlohmann::json::parse(text));
+    return put(mesh_to_json(m).dump(), out, cap);
+  } catch (const nlohmann::json::exception& e) {
+    put(e.what(), out, cap);
+    return 11;
+  } catch (const std::exception& e) {
+    put(e.what(), out, cap);
+    return code_of(e);
   }
 }
 

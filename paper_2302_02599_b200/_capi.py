@@ -100,6 +100,9 @@ _SIGS = {
     "apl_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
     "apl_mesh_create_nccl": (C.c_int, [P(MeshDesc), C.c_int, P(C.c_uint8), C.c_int,
                                        P(C.c_void_p)]),
+    "apl_mesh_to_json": (C.c_int, [P(MeshDesc), C.c_double, C.c_char_p, C.c_size_t,
+                                   P(C.c_size_t)]),
+    "apl_mesh_from_json": (C.c_int, [C.c_char_p, P(MeshDesc), P(C.c_double)]),
     "apl_mesh_destroy": (C.c_int, [C.c_void_p]),
     "apl_mesh_health": (C.c_int, [C.c_void_p, P(C.c_int)]),
     "apl_mesh_abort": (C.c_int, [C.c_void_p]),

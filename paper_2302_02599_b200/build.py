@@ -38,6 +38,23 @@ def _nccl_root() -> Path:
     raise RuntimeError("NCCL headers (nvidia/nccl from the torch wheel set) not found")
 
 
+def _nlohmann_include() -> Path | None:
+    """Directory holding nlohmann/json.hpp (the reference's JSON library;
+    in this image it ships inside cudnn_frontend's third-party tree)."""
+    import importlib.util
+
+    for cand in [Path("/usr/include"), Path("/usr/local/include")]:
+        if (cand / "nlohmann" / "json.hpp").exists():
+            return cand
+    spec = importlib.util.find_spec("torch")
+    if spec and spec.origin:
+        site = Path(spec.origin).parent.parent
+        for cand in [site / "include" / "cudnn_frontend" / "thirdparty"]:
+            if (cand / "nlohmann" / "json.hpp").exists():
+                return cand
+    return None
+
+
 HOST_SRCS = [
     CSRC / "host" / "mesh.cpp",
     CSRC / "host" / "spec.cpp",
@@ -85,6 +102,9 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     nccl = _nccl_root()
     incs = [f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{CUDA_HOME / 'include'}",
             f"-I{nccl / 'include'}"]
+    nl = _nlohmann_include()
+    if nl is not None:
+        incs.append(f"-I{nl}")
     BUILD.mkdir(parents=True, exist_ok=True)
     headers = _headers()
     jobs = []

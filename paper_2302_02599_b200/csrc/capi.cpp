@@ -197,6 +197,43 @@ int apl_mesh_desc_uniform(const int64_t* shape, int ndim, apl_mesh_desc* out) {
   });
 }
 
+int apl_mesh_to_json(const apl_mesh_desc* mesh, double device_flops_per_s, char* buf,
+                     size_t cap, size_t* len) {
+  return guarded([&] {
+    need(len, "null out");
+    DeviceMesh m = to_mesh(mesh);
+    m.device_flops_per_s = device_flops_per_s;
+    const std::string text = autoplan::mesh_to_json(m).dump();
+    *len = text.size();
+    if (buf != nullptr) {
+      need(cap > text.size(), "buffer too small");
+      std::memcpy(buf, text.c_str(), text.size() + 1);
+    }
+  });
+}
+
+int apl_mesh_from_json(const char* text, apl_mesh_desc* out, double* device_flops_per_s) {
+  return guarded([&] {
+    need(text && out, "null argument");
+    nlohmann::json doc;
+    try {
+      doc = nlohmann::json::parse(text);
+    } catch (const nlohmann::json::exception& e) {
+      throw autoplan::SchemaError(std::string("mesh document is not JSON: ") + e.what());
+    }
+    const DeviceMesh m = autoplan::mesh_from_json(doc);
+    need(m.rank() >= 1 && m.rank() <= APL_MAX_MESH, "mesh rank outside [1, APL_MAX_MESH]");
+    std::memset(out, 0, sizeof(*out));
+    out->ndim = m.rank();
+    for (int i = 0; i < m.rank(); ++i) {
+      out->shape[i] = m.shape[static_cast<size_t>(i)];
+      out->alpha[i] = m.axis_alpha[static_cast<size_t>(i)];
+      out->beta_inv[i] = m.axis_beta_inv[static_cast<size_t>(i)];
+    }
+    if (device_flops_per_s) *device_flops_per_s = m.device_flops_per_s;
+  });
+}
+
 int apl_parse_mesh_shape(const char* text, int64_t* shape, int cap, int* ndim) {
   return guarded([&] {
     need(text && shape && ndim, "null argument");

@@ -130,4 +130,42 @@ std::string mesh_report(const DeviceMesh& mesh) {
   return os.str();
 }
 
+#if __has_include(<nlohmann/json.hpp>)
+// Document form of a mesh (cluster.cpp:417-450): the five tabled fields;
+// `warnings` is diagnostic and not serialised.
+nlohmann::json mesh_to_json(const DeviceMesh& mesh) {
+  nlohmann::json doc;
+  doc["shape"] = mesh.shape;
+  doc["assignment"] = mesh.assignment;
+  doc["axis_alpha"] = mesh.axis_alpha;
+  doc["axis_beta_inv"] = mesh.axis_beta_inv;
+  doc["device_flops_per_s"] = mesh.device_flops_per_s;
+  return doc;
+}
+
+DeviceMesh mesh_from_json(const nlohmann::json& doc) {
+  if (!doc.is_object()) throw SchemaError("mesh document must be an object");
+  DeviceMesh mesh;
+  try {
+    doc.at("shape").get_to(mesh.shape);
+    doc.at("assignment").get_to(mesh.assignment);
+    doc.at("axis_alpha").get_to(mesh.axis_alpha);
+    doc.at("axis_beta_inv").get_to(mesh.axis_beta_inv);
+    mesh.device_flops_per_s = doc.at("device_flops_per_s").get<double>();
+  } catch (const nlohmann::json::exception& e) {
+    throw SchemaError(std::string("malformed mesh document: ") + e.what());
+  }
+  int64_t devices = 1;
+  for (const int64_t n : mesh.shape) {
+    if (n < 1) throw SchemaError("mesh extents must be positive");
+    devices *= n;
+  }
+  const size_t r = mesh.shape.size();
+  if (static_cast<int64_t>(mesh.assignment.size()) != devices || mesh.axis_alpha.size() != r ||
+      mesh.axis_beta_inv.size() != r)
+    throw SchemaError("mesh document fields have inconsistent sizes");
+  return mesh;
+}
+#endif
+
 }  // namespace autoplan

@@ -507,7 +507,13 @@ void launch_pull_sync_v(int no, int64_t total, const DevCopy* t, const int64_t* 
     const int64_t end = k + m < n ? begins[k + m] : total;
     const int64_t chunk = int64_t{kThreads} * U;
     const int64_t chunks = std::max<int64_t>(1, (end - first + chunk - 1) / chunk);
-    const int grid = static_cast<int>(std::min<int64_t>(chunks, static_cast<int64_t>(sm_count()) * MINB));
+    // APL_PULL_GRID_CAP: at most this many CTAs per launch (the single-process
+    // loopback harness runs every rank's kernel concurrently on one GPU, so
+    // each must leave room for the others to be resident).
+    static const int cap = env_int("APL_PULL_GRID_CAP", 0);
+    int64_t g = std::min<int64_t>(chunks, static_cast<int64_t>(sm_count()) * MINB);
+    if (cap > 0) g = std::min<int64_t>(g, cap);
+    const int grid = static_cast<int>(g);
     const size_t smem = static_cast<size_t>(m) * sizeof(DevCopy);
     PeerSync y = sync;
     y.mode = (sl == 0 ? (sync.mode & PeerSync::kAnnounce) : 0) |

@@ -154,6 +154,25 @@ class DeviceMesh:
     def assignment(self) -> list:
         return [f"d{i}" for i in range(self.num_devices())]
 
+    def to_json(self) -> str:
+        """Reference mesh_to_json (cluster.cpp:417-425) through the C-ABI."""
+        n = C.c_size_t()
+        check(A.lib().apl_mesh_to_json(C.byref(self.c()), self.device_flops_per_s, None, 0,
+                                       C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(A.lib().apl_mesh_to_json(C.byref(self.c()), self.device_flops_per_s, buf,
+                                       n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    @staticmethod
+    def from_json(text: str) -> "DeviceMesh":
+        """Reference mesh_from_json (cluster.cpp:427-450): SchemaError on a
+        malformed or inconsistent document."""
+        m, fl = A.MeshDesc(), C.c_double()
+        check(A.lib().apl_mesh_from_json(text.encode(), C.byref(m), C.byref(fl)))
+        return DeviceMesh(tuple(m.shape[:m.ndim]), list(m.alpha[:m.ndim]),
+                          list(m.beta_inv[:m.ndim]), fl.value)
+
     def c(self) -> A.MeshDesc:
         if not 1 <= len(self.shape) <= A.MAX_MESH:
             raise ArgumentError("mesh rank outside [1, 8]")

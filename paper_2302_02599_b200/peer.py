@@ -10,8 +10,10 @@ top of a `runtime.PeerMesh`:
     tensor lives at the same offset on every rank and its peers' copies are
     `peer_base[q] + offset`;
   * conversions (the reference's insert_comm_nodes chains, planner.cpp:
-    284-347) collapse to ONE pull kernel per rank reading the target pieces
-    straight out of the peers' heap tensors (apl_run_pull);
+    284-347) collapse to ONE launch per rank (apl_run_pull_sync): it
+    announces this rank's ready flag, acquires the flags of the ranks it
+    reads from, pulls the target pieces straight out of the peers' heap
+    tensors and announces done from its last CTA;
   * partial sums (`<host>.ar`, planner.cpp:263-282, over any mesh-axis group)
     are ONE in-place peer all-reduce kernel per rank (apl_peer_allreduce);
   * ordering is device-side epoch flags (apl_peer_flags_*), no host barrier:
@@ -71,6 +73,10 @@ class PeerRuntime:
         self.heap_bytes = heap_bytes
         self._off = 0
         self._local = Mesh.local([1], device=device)  # per-rank GEMMs on the local shards
+        import os
+
+        # conversions as one fused launch (APL_PEER_FUSED=0: flag kernels + pull)
+        self.fused = os.environ.get("APL_PEER_FUSED", "1") != "0"
 
     # ---- symmetric heap ------------------------------------------------------
     def empty(self, shape, dtype) -> torch.Tensor:
@@ -132,9 +138,17 @@ class PeerRuntime:
         pm = self.pm
         pm.epoch += 1
         e = pm.epoch
+        table = (C.c_void_p * self.num_devices)(*self._peer_ptrs(x, range(self.num_devices)))
+        if self.fused:
+            # one launch: announce, acquire the actual senders, pull, announce done
+            sync = A.PeerSyncC(pm._all_flags, pm.flags.data_ptr(), pm._counter.data_ptr(), e,
+                               pm.timeout_ms)
+            check(A.lib().apl_run_pull_sync(pm._h, C.byref(src.c()), C.byref(tgt.c()),
+                                            C.byref(meta.c()), table, C.c_void_p(out.data_ptr()),
+                                            C.byref(sync), _stream_handle(stream)))
+            return
         self._store(False, stream)
         self._wait(self._all_others(), e, False, stream)
-        table = (C.c_void_p * self.num_devices)(*self._peer_ptrs(x, range(self.num_devices)))
         check(A.lib().apl_run_pull(pm._h, C.byref(src.c()), C.byref(tgt.c()), C.byref(meta.c()),
                                    table, C.c_void_p(out.data_ptr()), _stream_handle(stream)))
         self._store(True, stream)

@@ -115,7 +115,7 @@ EPOCH_CASES = {
 EPOCHS = 3
 
 
-def _epoch_worker(rank, world, port, cases, q):
+def _epoch_worker(rank, world, port, cases, q, fused=True):
     """Repeated exchanges synchronised only on the device: each epoch the
     rank rewrites its exported source (after wait_readers) with a different
     tensor, then exchange_async; no host barrier between epochs."""
@@ -150,7 +150,8 @@ def _epoch_worker(rank, world, port, cases, q):
                 pm.wait_readers()
                 pm.shard(srcs[e].shape, dt[eb]).copy_(srcs[e])
                 out = torch.full(wants[e].shape, -1, dtype=dt[eb], device="cuda:0")
-                pm.exchange_async(ShardingSpec.parse(a, mr), ShardingSpec.parse(b, mr), meta, out)
+                pm.exchange_async(ShardingSpec.parse(a, mr), ShardingSpec.parse(b, mr), meta, out,
+                                  fused=fused)
                 outs.append(out)
             pm.wait_readers()
             torch.cuda.synchronize()
@@ -163,12 +164,15 @@ def _epoch_worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("world", [4, 8])
-def test_peer_exchange_device_synchronised_epochs(cuda, world):
+def test_peer_exchange_device_synchronised_epochs(cuda, world, fused):
+    """fused: one launch per exchange (apl_run_pull_sync); unfused: flag
+    store / flag wait / pull / flag store kernels."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_epoch_worker, args=(r, world, port, EPOCH_CASES[world], q))
+    procs = [ctx.Process(target=_epoch_worker, args=(r, world, port, EPOCH_CASES[world], q, fused))
              for r in range(world)]
     for p in procs:
         p.start()
