@@ -496,11 +496,16 @@ int apl_layernorm_backward(const void* x, const void* gamma, const void* dy, voi
 /* softmax (last dim) from its output y: dx = alpha * y * (dy - sum(dy * y)). */
 int apl_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows, int64_t width,
                          float alpha, int dtype, void* stream);
-/* embedding: dtable[ids[t], :] += dy[t, :] (fp32 table gradient, accumulated). */
+/* embedding: dtable[ids[t], :] += dy[t, :] (fp32 table gradient, accumulated).
+ * Deterministic: the (id, token) keys are radix-sorted, each distinct id's
+ * tokens are summed in ascending token order by one warp and added to its
+ * row once -- no float atomics, the same bytes on every run. Scratch comes
+ * from the stream-ordered allocator (cudaMallocAsync). */
 int apl_embedding_backward(const int64_t* ids, int64_t n, const void* dy, float* dtable,
                            int64_t vocab, int64_t width, int dtype, void* stream);
 
-/* embedding backward with the gradient's reduce-scatter fused in: the block
+/* embedding backward with the gradient's reduce-scatter fused in (same
+ * deterministic id-sorted accumulation, tokens ordered by (source, token)): the block
  * [rows, cols] of the table gradient at vocab rows [v0, v0 + rows) and columns
  * [c0, c0 + cols) accumulates (+=, fp32) the rows of every source s -- ids[s]
  * (n int64) with their output gradients dy[s] ([n, dy_width]) -- whose id

@@ -135,6 +135,22 @@ class PlanExecutor {
   }
 
   int num_local() const { return num_local_; }
+
+  // backward() computes in bf16 (gradient buffers, GELU / softmax /
+  // layernorm backward kernels, transposes of 2-byte elements), so a
+  // training forward refuses plans whose differentiable values -- parameters
+  // and computed nodes; u8 masks and placeholders (ids, inputs) are not
+  // differentiated -- have any other width, instead of reading fp32 buffers
+  // as bf16.
+  void check_trainable() const {
+    for (const auto& id : order_) {
+      const Node& nd = nodes_.at(id);
+      if (nd.kind == "placeholder" || nd.meta.dtype_bytes == 1) continue;
+      if (nd.meta.dtype_bytes != 2)
+        throw PlanError("backward supports bf16 plans only: node '" + id + "' has dtype_bytes " +
+                        std::to_string(nd.meta.dtype_bytes));
+    }
+  }
   const ShardingSpec& spec(const std::string& id) const { return nodes_.at(id).spec; }
   const TensorMeta& meta(const std::string& id) const { return nodes_.at(id).meta; }
   // placeholders and parameters, in graph order (what forward() must be fed)
@@ -157,6 +173,7 @@ class PlanExecutor {
   // embedding ids) and runs the attention chain unfused.
   std::vector<void*> forward(const std::map<std::string, std::vector<const void*>>& feeds,
                              void* stream, bool train = false) {
+    if (train) check_trainable();
     saved_.clear();
     trained_ = train;
     std::map<std::string, std::vector<const void*>> values;

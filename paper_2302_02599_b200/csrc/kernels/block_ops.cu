@@ -19,6 +19,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -487,46 +489,59 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const T* __restrict__ 
   }
 }
 
-// embedding: dtable[ids[t], :] += dy[t, :] (fp32 accumulation, atomics: ids repeat)
-template <typename T>
-__global__ void __launch_bounds__(256) embedding_bwd_kernel(const int64_t* __restrict__ ids,
-                                                            int64_t n, const T* __restrict__ dy,
-                                                            float* __restrict__ dtable,
-                                                            int64_t vocab, int64_t width) {
-  const int64_t total = n * width;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = i / width, c = i - t * width;
-    const int64_t id = __ldg(ids + t);
-    if (id >= 0 && id < vocab) atomicAdd(dtable + id * width + c, ld(dy + i));
-  }
-}
-
-// embedding backward with the gradient's reduce-scatter fused in: one owner's
-// block [rows x cols] of the table gradient (vocab rows [v0, v0 + rows),
-// columns [c0, c0 + cols)) accumulates every source's (ids, dy) rows that fall
-// in it -- instead of each device building a whole [vocab, width] partial
-// gradient that is then all-reduced and sliced. A warp per (source, token).
+// ---- embedding backward: deterministic, id-sorted -------------------------
+// dtable[id, :] += sum of dy[t, :] over the tokens t with ids[t] == id.
+// Instead of fp32 atomics (whose summation order -- and so the bytes --
+// changes run to run when ids repeat), every (source e, token t) gets the
+// unique key (id << 32 | e * n + t); a radix sort groups the keys by id with
+// the tokens in ascending order, and one warp per distinct id sums its tokens
+// in that order and updates the row once. The result is bit-reproducible.
+// The same path serves the fused reduce-scatter form (an owner's block of
+// vocab rows [v0, v0 + rows) x columns [c0, c0 + cols), sources from every
+// device); ids outside the block get a sentinel key that sorts last.
 struct EmbSources {
   const int64_t* ids[kMaxBlocks];
   const void* dy[kMaxBlocks];
 };
 
-template <typename T>
-__global__ void __launch_bounds__(256) embedding_bwd_block_kernel(
-    const __grid_constant__ EmbSources src, int nsrc, int64_t n, int64_t dy_width,
-    float* __restrict__ dblock, int64_t v0, int64_t rows, int64_t c0, int64_t cols) {
-  const int lane = threadIdx.x % 32;
+__global__ void __launch_bounds__(256) embedding_keys_kernel(const __grid_constant__ EmbSources src,
+                                                             int nsrc, int64_t n, int64_t v0,
+                                                             int64_t rows,
+                                                             uint64_t* __restrict__ keys) {
   const int64_t total = static_cast<int64_t>(nsrc) * n;
-  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; w < total;
-       w += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
-    const int e = static_cast<int>(w / n);
-    const int64_t t = w - e * n;
-    const int64_t id = src.ids[e][t] - v0;
-    if (id < 0 || id >= rows) continue;
-    const T* dr = static_cast<const T*>(src.dy[e]) + t * dy_width + c0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int e = static_cast<int>(i / n);
+    const int64_t id = __ldg(src.ids[e] + (i - e * n)) - v0;
+    keys[i] = (id >= 0 && id < rows) ? (static_cast<uint64_t>(id) << 32) | static_cast<uint64_t>(i)
+                                     : ~uint64_t{0};
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) embedding_accum_kernel(
+    const uint64_t* __restrict__ keys, int64_t m, const __grid_constant__ EmbSources src,
+    int64_t n, int64_t dy_width, float* __restrict__ dblock, int64_t rows, int64_t c0,
+    int64_t cols) {
+  const int lane = threadIdx.x % 32;
+  for (int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; p < m;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const uint64_t k = keys[p];
+    const int64_t id = static_cast<int64_t>(k >> 32);
+    if (id >= rows) continue;                             // sentinel (outside the block)
+    if (p > 0 && (keys[p - 1] >> 32) == k >> 32) continue;  // not the first token of its id
+    int64_t q_end = p + 1;
+    while (q_end < m && (keys[q_end] >> 32) == k >> 32) ++q_end;
     float* out = dblock + id * cols;
-    for (int64_t c = lane; c < cols; c += 32) atomicAdd(out + c, ld(dr + c));
+    for (int64_t c = lane; c < cols; c += 32) {
+      float acc = 0.f;
+      for (int64_t q = p; q < q_end; ++q) {  // tokens in ascending (source, token) order
+        const int64_t i = static_cast<int64_t>(keys[q] & 0xffffffffu);
+        const int e = static_cast<int>(i / n);
+        acc += ld(static_cast<const T*>(src.dy[e]) + (i - e * n) * dy_width + c0 + c);
+      }
+      out[c] += acc;
+    }
   }
 }
 
@@ -945,20 +960,53 @@ cudaError_t launch_softmax_backward(const void* y, const void* dy, void* dx, int
   return cudaErrorInvalidValue;
 }
 
+namespace {
+
+cudaError_t embedding_backward_sorted(const EmbSources& src, int nsrc, int64_t n, int64_t dy_width,
+                                      float* dblock, int64_t v0, int64_t rows, int64_t c0,
+                                      int64_t cols, int dtype, cudaStream_t s) {
+  const int64_t m = static_cast<int64_t>(nsrc) * n;
+  if (m >= (int64_t{1} << 32) - 1 || rows >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+  if (dtype != 0 && dtype != 1) return cudaErrorInvalidValue;
+  int id_bits = 1;
+  while ((int64_t{1} << id_bits) <= rows) ++id_bits;  // the sentinel's id field exceeds rows
+  const int end_bit = 32 + id_bits;
+  size_t temp = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, temp, static_cast<const uint64_t*>(nullptr),
+                                                 static_cast<uint64_t*>(nullptr), m, 0, end_bit, s);
+  if (e != cudaSuccess) return e;
+  const size_t kb = (static_cast<size_t>(m) * 8 + 255) / 256 * 256;
+  void* scratch = nullptr;
+  if ((e = cudaMallocAsync(&scratch, 2 * kb + temp, s)) != cudaSuccess) return e;
+  uint64_t* k_in = static_cast<uint64_t*>(scratch);
+  uint64_t* k_out = reinterpret_cast<uint64_t*>(static_cast<char*>(scratch) + kb);
+  void* t = static_cast<char*>(scratch) + 2 * kb;
+  embedding_keys_kernel<<<grid_for(m), 256, 0, s>>>(src, nsrc, n, v0, rows, k_in);
+  e = cub::DeviceRadixSort::SortKeys(t, temp, k_in, k_out, m, 0, end_bit, s);
+  if (e == cudaSuccess) {
+    if (dtype == 0)
+      embedding_accum_kernel<float><<<grid_for(m * 32), 256, 0, s>>>(k_out, m, src, n, dy_width,
+                                                                    dblock, rows, c0, cols);
+    else
+      embedding_accum_kernel<__nv_bfloat16><<<grid_for(m * 32), 256, 0, s>>>(
+          k_out, m, src, n, dy_width, dblock, rows, c0, cols);
+  }
+  const cudaError_t f = cudaFreeAsync(scratch, s);
+  return e != cudaSuccess ? e : f;
+}
+
+}  // namespace
+
 cudaError_t launch_embedding_backward(const int64_t* ids, int64_t n, const void* dy,
                                       float* dtable, int64_t vocab, int64_t width, int dtype,
                                       cudaStream_t s) {
   if (n == 0 || width == 0) return cudaSuccess;
-  const int grid = grid_for(n * width);
-  if (dtype == 0)
-    embedding_bwd_kernel<float><<<grid, 256, 0, s>>>(ids, n, static_cast<const float*>(dy),
-                                                     dtable, vocab, width);
-  else if (dtype == 1)
-    embedding_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
-        ids, n, static_cast<const __nv_bfloat16*>(dy), dtable, vocab, width);
-  else
-    return cudaErrorInvalidValue;
-  return done();
+  EmbSources src{};
+  src.ids[0] = ids;
+  src.dy[0] = dy;
+  const cudaError_t e =
+      embedding_backward_sorted(src, 1, n, width, dtable, 0, vocab, 0, width, dtype, s);
+  return e != cudaSuccess ? e : done();
 }
 
 cudaError_t launch_embedding_backward_block(const int64_t* const* ids, const void* const* dy,
@@ -972,16 +1020,9 @@ cudaError_t launch_embedding_backward_block(const int64_t* const* ids, const voi
     src.ids[i] = ids[i];
     src.dy[i] = dy[i];
   }
-  const int grid = grid_for(static_cast<int64_t>(nsrc) * n * 32);
-  if (dtype == 0)
-    embedding_bwd_block_kernel<float><<<grid, 256, 0, s>>>(src, nsrc, n, dy_width, dblock, v0,
-                                                           rows, c0, cols);
-  else if (dtype == 1)
-    embedding_bwd_block_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(src, nsrc, n, dy_width, dblock,
-                                                                   v0, rows, c0, cols);
-  else
-    return cudaErrorInvalidValue;
-  return done();
+  const cudaError_t e =
+      embedding_backward_sorted(src, nsrc, n, dy_width, dblock, v0, rows, c0, cols, dtype, s);
+  return e != cudaSuccess ? e : done();
 }
 
 size_t layernorm_backward_scratch_bytes(int64_t rows, int64_t width) {

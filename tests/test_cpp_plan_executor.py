@@ -151,14 +151,38 @@ def test_native_executor_backward_matches_python(cuda, tmp_path, name):
     grads = ex.backward(gy)
     torch.cuda.synchronize()
     assert grads
-    atomic = {"wte"}
-    for k, shards in grads.items():
+    for k, shards in grads.items():  # every gradient, the embedding table's included
         mine = b"".join(t.contiguous().view(torch.uint8).cpu().numpy().tobytes() for t in shards)
         native = (tmp_path / f"grad_{k}.bin").read_bytes()
-        if k not in atomic:
-            assert native == mine, k
-            continue
-        a = torch.frombuffer(bytearray(native), dtype=torch.float32)
-        b = torch.frombuffer(bytearray(mine), dtype=torch.float32)
-        assert a.shape == b.shape, k
-        assert ((a - b).abs().max() / b.abs().max()).item() <= 1e-5, k
+        assert native == mine, k
+
+
+@pytest.mark.gpu
+def test_native_training_forward_rejects_fp32_plans(cuda, tmp_path):
+    """The native backward computes in bf16: a training forward of the
+    reference's fp32 fixture plan is refused up front, while
+    the inference forward of the same plan runs."""
+    import sys
+
+    import torch
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from test_gpu_block import _operands
+
+    exe = build(tmp_path)
+    graph_path = PLANS / "gpt_block_fixture_graph.json"
+    graph = json.loads(graph_path.read_text())
+    feeds = _operands(graph)
+    for k, v in feeds.items():
+        (tmp_path / f"{k}.bin").write_bytes(v.contiguous().view(torch.uint8).cpu().numpy()
+                                            .tobytes())
+    out_shape = tuple(feeds["tok"].shape) + (feeds["wte"].shape[1],)
+    (tmp_path / "dy.bin").write_bytes(torch.zeros(out_shape, dtype=torch.bfloat16)
+                                      .view(torch.uint8).numpy().tobytes())
+    name = "gpt_block_fixture_mesh2x2_unlimited.json"
+    args = [str(exe), str(graph_path), str(PLANS / name), "2x2", str(tmp_path)]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    r = subprocess.run(args + ["train"], capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "backward supports bf16 plans only" in r.stdout + r.stderr

@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--iters", type=int, default=200)
     args = ap.parse_args()
     P = args.ranks
+    # one hardware queue per stream: two ranks' streams sharing a queue would
+    # serialise a spinning kernel in front of the kernel it waits for
+    os.environ["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"
     import torch
 
     os.environ.setdefault("APL_PULL_GRID_CAP", str(max(1, 148 * 4 // P)))
@@ -72,11 +75,11 @@ def main():
                 if e > 1:  # wait_readers of the previous epoch (every rank reads every rank here)
                     slots = (C.c_int32 * (P - 1))(*[P + q for q in others[r]])
                     check(lib.apl_peer_flags_wait(C.c_void_p(flags[r].data_ptr()), slots, P - 1,
-                                                  e - 1, 5000, sh))
+                                                  e - 1, 3000, sh))
                 out = C.c_void_p(outs["fused" if fused else "unfused"][r].data_ptr())
                 if fused:
                     sync = A.PeerSyncC(all_flags, flags[r].data_ptr(), counters[r].data_ptr(), e,
-                                       5000)
+                                       3000)
                     check(lib.apl_run_pull_sync(meshes[r], C.byref(s.c()), C.byref(t.c()),
                                                 C.byref(meta.c()), table, out, C.byref(sync), sh))
                 else:
@@ -84,15 +87,14 @@ def main():
                     ready = (C.c_int32 * (P - 1))(*others[r])
                     check(lib.apl_peer_flags_store(peers, P - 1, r, e, sh))
                     check(lib.apl_peer_flags_wait(C.c_void_p(flags[r].data_ptr()), ready, P - 1,
-                                                  e, 5000, sh))
+                                                  e, 3000, sh))
                     check(lib.apl_run_pull(meshes[r], C.byref(s.c()), C.byref(t.c()),
                                            C.byref(meta.c()), table, out, sh))
                     check(lib.apl_peer_flags_store(peers, P - 1, P + r, e, sh))
 
         row = {"case": name, "ranks": P, "tensor": list(shape), "conversion": f"{a}->{b}",
                "grid_cap": int(os.environ["APL_PULL_GRID_CAP"]),
-               "bytes_pulled_per_rank": int(s.per_device_bytes(meta, geo) * (P - 1)
-                                            * (1 if b == "RR" else 1) // (1 if b == "RR" else P))}
+               "bytes_pulled_per_rank": s.per_device_bytes(meta, geo) * (P - 1) // (1 if b == "RR" else P)}
         for fused in (True, False):
             for _ in range(5):
                 epoch += 1
