@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 namespace apl {
 
@@ -350,6 +351,362 @@ __global__ void __launch_bounds__(256) softmax_cached_kernel(const T* __restrict
   }
 }
 
+// ---- software-pipelined row kernels ------------------------------------------
+// A warp per row, the row held in registers as raw 16-byte vectors (4 regs per
+// 8 bf16 / 4 fp32 elements, unpacked to fp32 on use), and the NEXT row's loads
+// issued before the current row's reductions: every warp keeps a row of reads
+// in flight through its whole compute phase. The r01 row-cached kernels
+// stalled on long_scoreboard with half the warps resident (fp32 row registers
+// limit occupancy), so HBM saw a bubble per row.
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint2 ldg_stream8(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ldg_stream4(const void* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg16(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ float ex2_ftz(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+template <typename T>
+struct Raw;  // 16-byte vector <-> fp32
+template <>
+struct Raw<__nv_bfloat16> {
+  static constexpr int V = 8;
+  using Mask = uint2;  // 8 mask bytes
+  __device__ static void unpack(const uint4& u, float (&f)[8]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+  __device__ static uint4 pack(const float (&f)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __device__ static Mask load_mask(const uint8_t* p) { return ldg_stream8(p); }
+  __device__ static float mask_at(const Mask& m, int k) {
+    return static_cast<float>(((k < 4 ? m.x : m.y) >> (8 * (k & 3))) & 0xFFu);
+  }
+};
+template <>
+struct Raw<float> {
+  static constexpr int V = 4;
+  using Mask = uint32_t;  // 4 mask bytes
+  __device__ static void unpack(const uint4& u, float (&f)[4]) {
+    f[0] = __uint_as_float(u.x);
+    f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z);
+    f[3] = __uint_as_float(u.w);
+  }
+  __device__ static uint4 pack(const float (&f)[4]) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+  __device__ static Mask load_mask(const uint8_t* p) { return ldg_stream4(p); }
+  __device__ static float mask_at(const Mask& m, int k) {
+    return static_cast<float>((m >> (8 * k)) & 0xFFu);
+  }
+};
+
+// softmax(alpha * x + fill * mask) over rows of width <= 32 * NV * V.
+template <typename T, int NV, bool kMask>
+__global__ void __launch_bounds__(256) softmax_pipe_kernel(const T* __restrict__ x,
+                                                           T* __restrict__ y, int64_t rows,
+                                                           int64_t width, float alpha,
+                                                           const uint8_t* __restrict__ mask,
+                                                           float fill) {
+  using R = Raw<T>;
+  constexpr int V = R::V;
+  const int lane = threadIdx.x % 32;
+  const int nv = static_cast<int>(width / V);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / 32;
+  int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+  uint4 cur[NV], nxt[NV];
+  typename R::Mask mc[NV], mn[NV];
+  auto load = [&](int64_t row, uint4 (&d)[NV], typename R::Mask (&m)[NV]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        d[j] = ldg_stream(x + row * width + static_cast<int64_t>(i) * V);
+        if constexpr (kMask) m[j] = R::load_mask(mask + row * width + static_cast<int64_t>(i) * V);
+      }
+    }
+  };
+  if (r < rows) load(r, cur, mc);
+  for (; r < rows; r += stride) {
+    if (r + stride < rows) load(r + stride, nxt, mn);
+    float f[NV][V];
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv) {
+        R::unpack(cur[j], f[j]);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          if constexpr (kMask) f[j][k] = fmaf(alpha, f[j][k], fill * R::mask_at(mc[j], k));
+          else f[j][k] *= alpha;
+          m = fmaxf(m, f[j][k]);
+        }
+      }
+    m = warp_max(m);
+    const float ml = m * 1.4426950408889634f;
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv)
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          f[j][k] = ex2_ftz(fmaf(f[j][k], 1.4426950408889634f, -ml));
+          s += f[j][k];
+        }
+    const float inv = 1.f / warp_sum(s);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) f[j][k] *= inv;
+        stg16(y + r * width + static_cast<int64_t>(i) * V, R::pack(f[j]));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      cur[j] = nxt[j];
+      if constexpr (kMask) mc[j] = mn[j];
+    }
+  }
+}
+
+// layernorm forward, rows of width <= 32 * NV * V; two-pass mean / variance
+// from the registers (the same arithmetic as layernorm_backward's pipe kernel,
+// so backward's recomputed statistics equal forward's bit for bit).
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) layernorm_pipe_kernel(
+    const T* __restrict__ x, const T* __restrict__ gamma, const T* __restrict__ beta,
+    T* __restrict__ y, int64_t rows, int64_t width, float eps) {
+  using R = Raw<T>;
+  constexpr int V = R::V;
+  const int lane = threadIdx.x % 32;
+  const int nv = static_cast<int>(width / V);
+  const float inv_w = 1.f / static_cast<float>(width);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / 32;
+  int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+  uint4 cur[NV], nxt[NV];
+  typename R::Mask unused[NV];
+  (void)unused;
+  auto load = [&](int64_t row, uint4 (&d)[NV]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv) d[j] = ldg_stream(x + row * width + static_cast<int64_t>(lane + 32 * j) * V);
+  };
+  if (r < rows) load(r, cur);
+  for (; r < rows; r += stride) {
+    if (r + stride < rows) load(r + stride, nxt);
+    float f[NV][V];
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv) {
+        R::unpack(cur[j], f[j]);
+#pragma unroll
+        for (int k = 0; k < V; ++k) s += f[j][k];
+      }
+    const float mean = warp_sum(s) * inv_w;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv)
+#pragma unroll
+        for (int k = 0; k < V; ++k) q += (f[j][k] - mean) * (f[j][k] - mean);
+    const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        float g[V], b[V];
+        if (gamma != nullptr) load_row<T, V>(gamma, i, g);
+        if (beta != nullptr) load_row<T, V>(beta, i, b);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          float v = (f[j][k] - mean) * rstd;
+          if (gamma != nullptr) v *= g[k];
+          if (beta != nullptr) v += b[k];
+          f[j][k] = v;
+        }
+        stg16(y + r * width + static_cast<int64_t>(i) * V, R::pack(f[j]));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) cur[j] = nxt[j];
+  }
+}
+
+// layernorm backward (dx and the per-row statistics for the parameter pass),
+// x and dy of the next row prefetched; mean / rstd computed exactly as the
+// forward pipe kernel does (two passes over the registers).
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) layernorm_bwd_pipe_kernel(
+    const T* __restrict__ x, const T* __restrict__ gamma, const T* __restrict__ dy,
+    T* __restrict__ dx, float2* __restrict__ stats, int64_t rows, int64_t width, float eps) {
+  using R = Raw<T>;
+  constexpr int V = R::V;
+  const int lane = threadIdx.x % 32;
+  const int nv = static_cast<int>(width / V);
+  const float inv_w = 1.f / static_cast<float>(width);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / 32;
+  int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+  uint4 cx[NV], cd[NV], nx[NV], nd[NV];
+  auto load = [&](int64_t row, uint4 (&a)[NV], uint4 (&b)[NV]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv) {
+        const int64_t o = row * width + static_cast<int64_t>(lane + 32 * j) * V;
+        a[j] = ldg_stream(x + o);
+        b[j] = ldg_stream(dy + o);
+      }
+  };
+  if (r < rows) load(r, cx, cd);
+  for (; r < rows; r += stride) {
+    if (r + stride < rows) load(r + stride, nx, nd);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv) {
+        float f[V];
+        R::unpack(cx[j], f);
+#pragma unroll
+        for (int k = 0; k < V; ++k) s += f[k];
+      }
+    const float mean = warp_sum(s) * inv_w;
+    float q = 0.f, sa = 0.f, sax = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv) {
+        float f[V], d[V], g[V];
+        R::unpack(cx[j], f);
+        R::unpack(cd[j], d);
+        if (gamma != nullptr) load_row<T, V>(gamma, lane + 32 * j, g);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const float c = f[k] - mean;
+          const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
+          q += c * c;
+          sa += gd;
+          sax += gd * c;
+        }
+      }
+    const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
+    const float a = warp_sum(sa) * inv_w;
+    const float b = rstd * warp_sum(sax) * inv_w;  // mean(g.dy.xhat)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        float f[V], d[V], g[V];
+        R::unpack(cx[j], f);
+        R::unpack(cd[j], d);
+        if (gamma != nullptr) load_row<T, V>(gamma, i, g);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
+          f[k] = rstd * (gd - a - (f[k] - mean) * rstd * b);
+        }
+        stg16(dx + r * width + static_cast<int64_t>(i) * V, R::pack(f));
+      }
+    }
+    if (lane == 0 && stats != nullptr) stats[r] = make_float2(mean, rstd);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      cx[j] = nx[j];
+      cd[j] = nd[j];
+    }
+  }
+}
+
+// softmax backward, y and dy of the next row prefetched.
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) softmax_bwd_pipe_kernel(const T* __restrict__ y,
+                                                               const T* __restrict__ dy,
+                                                               T* __restrict__ dx, int64_t rows,
+                                                               int64_t width, float alpha) {
+  using R = Raw<T>;
+  constexpr int V = R::V;
+  const int lane = threadIdx.x % 32;
+  const int nv = static_cast<int>(width / V);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / 32;
+  int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+  uint4 cy[NV], cd[NV], ny[NV], nd[NV];
+  auto load = [&](int64_t row, uint4 (&a)[NV], uint4 (&b)[NV]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv) {
+        const int64_t o = row * width + static_cast<int64_t>(lane + 32 * j) * V;
+        a[j] = ldg_stream(y + o);
+        b[j] = ldg_stream(dy + o);
+      }
+  };
+  if (r < rows) load(r, cy, cd);
+  for (; r < rows; r += stride) {
+    if (r + stride < rows) load(r + stride, ny, nd);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nv) {
+        float a[V], d[V];
+        R::unpack(cy[j], a);
+        R::unpack(cd[j], d);
+#pragma unroll
+        for (int k = 0; k < V; ++k) s += a[k] * d[k];
+      }
+    s = warp_sum(s);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        float a[V], d[V];
+        R::unpack(cy[j], a);
+        R::unpack(cd[j], d);
+#pragma unroll
+        for (int k = 0; k < V; ++k) a[k] = alpha * a[k] * (d[k] - s);
+        stg16(dx + r * width + static_cast<int64_t>(i) * V, R::pack(a));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      cy[j] = ny[j];
+      cd[j] = nd[j];
+    }
+  }
+}
+
 // ---- backward ---------------------------------------------------------------
 // layernorm: dx = rstd * (g.dy - mean(g.dy) - xhat * mean(g.dy.xhat)), warp per
 // row: one pass for the four row sums (mean / rstd recomputed from x, kept per
@@ -638,6 +995,15 @@ cudaError_t done() {
   return cudaGetLastError();
 }
 
+// APL_ROW_PIPE=0 selects the r01 row kernels (A/B of the prefetching ones).
+bool pipe_rows_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_ROW_PIPE");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 struct SoftmaxPre {
   float alpha = 1.f;
   const uint8_t* mask = nullptr;
@@ -666,6 +1032,24 @@ cudaError_t rowwise(bool softmax, const void* x, const void* g, const void* b, v
   auto G = static_cast<const T*>(g);
   auto B = static_cast<const T*>(b);
   const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;  // vectors each lane holds
+  if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
+    const bool masked = p.mask != nullptr;
+    const int nv = per_lane == 1 ? 1 : per_lane == 2 ? 2 : 4;
+#define APL_ROW_PIPE(NVC)                                                                      \
+    if (!softmax)                                                                              \
+      layernorm_pipe_kernel<T, NVC><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);        \
+    else if (masked)                                                                           \
+      softmax_pipe_kernel<T, NVC, true><<<grid, 256, 0, s>>>(X, Y, rows, width, p.alpha, p.mask, \
+                                                             p.fill);                          \
+    else                                                                                       \
+      softmax_pipe_kernel<T, NVC, false><<<grid, 256, 0, s>>>(X, Y, rows, width, p.alpha,      \
+                                                              nullptr, 0.f);
+    if (nv == 1) { APL_ROW_PIPE(1) }
+    else if (nv == 2) { APL_ROW_PIPE(2) }
+    else { APL_ROW_PIPE(4) }
+#undef APL_ROW_PIPE
+    return done();
+  }
   if (per_lane >= 1 && per_lane <= 8) {
     if (per_lane == 1) rowwise_cached<T, V, 1>(softmax, X, G, B, Y, rows, width, eps, p, grid, s);
     else if (per_lane == 2) rowwise_cached<T, V, 2>(softmax, X, G, B, Y, rows, width, eps, p, grid, s);
@@ -900,10 +1284,22 @@ cudaError_t layernorm_bwd_typed(const void* x, const void* gamma, const void* dy
   auto G = static_cast<const T*>(gamma);
   auto D = static_cast<const T*>(dy);
   auto O = static_cast<T*>(dx);
-  // (a register-cached variant measured slower: 0.54 vs 0.63 of the HBM
-  // roofline at 131072 x 1024 -- its occupancy halves)
-  if (vec) layernorm_bwd_kernel<T, V><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
-  else layernorm_bwd_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+  // rows of up to 4 vectors per lane: the prefetching register kernel (raw
+  // 16-byte vectors keep its occupancy up; the r01 fp32-register variant
+  // halved it and measured 0.54 of the roofline); longer rows stream.
+  const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;
+  if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
+    if (per_lane == 1)
+      layernorm_bwd_pipe_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+    else if (per_lane == 2)
+      layernorm_bwd_pipe_kernel<T, 2><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+    else
+      layernorm_bwd_pipe_kernel<T, 4><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+  } else if (vec) {
+    layernorm_bwd_kernel<T, V><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+  } else {
+    layernorm_bwd_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (dgamma != nullptr || dbeta != nullptr) {
     const int64_t strips = (width + 31) / 32;
@@ -930,8 +1326,16 @@ cudaError_t softmax_bwd_typed(const void* y, const void* dy, void* dx, int64_t r
   auto Y = static_cast<const T*>(y);
   auto D = static_cast<const T*>(dy);
   auto O = static_cast<T*>(dx);
-  if (vec) softmax_bwd_kernel<T, V><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
-  else softmax_bwd_kernel<T, 1><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+  const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;
+  if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
+    if (per_lane == 1) softmax_bwd_pipe_kernel<T, 1><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+    else if (per_lane == 2) softmax_bwd_pipe_kernel<T, 2><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+    else softmax_bwd_pipe_kernel<T, 4><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+  } else if (vec) {
+    softmax_bwd_kernel<T, V><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+  } else {
+    softmax_bwd_kernel<T, 1><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+  }
   return done();
 }
 

@@ -21,6 +21,7 @@ void sharded_matmul(Mesh& mesh, const MatmulStrategy& s, const autoplan::TensorM
                     const autoplan::TensorMeta& b_meta, const void* const* A,
                     const void* const* B, void* const* C, bool b_kn, int out_dtype, int epilogue,
                     cudaStream_t stream, void* const* aux) {
+  NvtxRange range("apl.sharded_matmul");
   const bool save = epilogue == APL_EPI_GELU_SAVE;
   if (save && (aux == nullptr || out_dtype != APL_BF16))
     throw RuntimeError(APL_ERR_ARG, "GELU_SAVE needs bf16 output and aux buffers");
@@ -241,6 +242,7 @@ void sharded_matmul_backward(Mesh& mesh, const MatmulStrategy& s,
                              const void* const* B, const void* const* dC, void* const* dA,
                              void* const* dB, bool b_kn, bool dgelu, const void* const* aux,
                              int dB_dtype, cudaStream_t stream) {
+  NvtxRange range("apl.sharded_matmul_backward");
   const LocalDims d = local_dims(mesh, s, a_meta, b_meta);
   const bool batched = b_meta.rank() == 3;
   if (dgelu && aux == nullptr) throw RuntimeError(APL_ERR_ARG, "GELU backward needs aux");

@@ -10,8 +10,13 @@
 #include <cuda.h>
 
 #include "apl.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace apl {
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
+
 
 namespace {
 
@@ -546,6 +551,7 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
     merge_splits(ex->host_pre);
   }
   std::lock_guard<std::mutex> hold(mesh.mu);
+  ex->label = key;
   auto [it, fresh] = mesh.exchanges.emplace(key, ex);
   return it->second;
 }
@@ -590,6 +596,7 @@ std::shared_ptr<Exchange> get_allgather(Mesh& mesh, const autoplan::ShardingSpec
     ex->recv_staging = align_up(n * ex->in_bytes);
   }
   std::lock_guard<std::mutex> hold(mesh.mu);
+  ex->label = key;
   auto [it, fresh] = mesh.exchanges.emplace(key, ex);
   return it->second;
 }
@@ -648,6 +655,7 @@ std::shared_ptr<Exchange> get_alltoall(Mesh& mesh, const autoplan::ShardingSpec&
   ex->wire_bytes_out = (n - 1) * ex->a2a_chunk;
   merge_splits(ex->host_pre);
   std::lock_guard<std::mutex> hold(mesh.mu);
+  ex->label = key;
   auto [it, fresh] = mesh.exchanges.emplace(key, ex);
   return it->second;
 }
@@ -672,6 +680,7 @@ const CompiledCopies& compiled_for(std::map<int, CompiledCopies>& cache,
 
 void run_exchange(Mesh& mesh, Exchange& ex, const void* const* in, void* const* out, void* ws,
                   size_t ws_bytes, cudaStream_t stream) {
+  NvtxRange range(ex.label.c_str());
   DeviceGuard guard(mesh.device);
   const int nl = mesh.num_local();
   if (!mesh.distributed) {
@@ -771,6 +780,7 @@ void run_pull(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::Sha
   if (p > kCopyMaxPtrs) throw RuntimeError(APL_ERR_ARG, "mesh too large for one pull launch");
   DeviceGuard guard(mesh.device);
   auto ex = get_exchange(mesh, src, tgt, meta);
+  NvtxRange range(ex->label.c_str());
   PtrTable t{};
   int align = std::min(natural_vec(ex->host_pull), ptr_align(out));
   for (int64_t i = 0; i < p; ++i) {
@@ -800,6 +810,7 @@ void run_pull_sync(Mesh& mesh, const autoplan::ShardingSpec& src,
     throw RuntimeError(APL_ERR_ARG, "null flag arrays / counter");
   DeviceGuard guard(mesh.device);
   auto ex = get_exchange(mesh, src, tgt, meta);
+  NvtxRange range(ex->label.c_str());
   PtrTable t{};
   int align = std::min(natural_vec(ex->host_pull), ptr_align(out));
   for (int64_t i = 0; i < p; ++i) {
@@ -925,6 +936,7 @@ size_t conversion_workspace(const Conversion& cv) {
 
 void run_conversion(Conversion& cv, const void* const* in, void* const* out, void* ws,
                     size_t ws_bytes, cudaStream_t stream) {
+  NvtxRange range(cv.hops.size() == 1 ? "apl.convert" : "apl.convert.stepwise");
   Mesh& mesh = *cv.mesh;
   if (ws_bytes < conversion_workspace(cv))
     throw RuntimeError(APL_ERR_ARG, "workspace smaller than apl_path_workspace_bytes");
@@ -968,6 +980,7 @@ void run_path(Mesh& mesh, const autoplan::ShardingSpec& src, const autoplan::Sha
 
 void all_reduce(Mesh& mesh, const std::vector<int>& axes, void* const* bufs, size_t count,
                 int dtype, cudaStream_t stream) {
+  NvtxRange range("apl.all_reduce");
   DeviceGuard guard(mesh.device);
   uint32_t mask = 0;
   for (int a : axes) {

@@ -19,6 +19,16 @@
 
 namespace apl {
 
+// NVTX range for the lifetime of the object (one per conversion, exchange
+// step, all-reduce and sharded matmul; SURVEY §5 tracing). A push/pop pair
+// costs a few ns when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Error raised by the runtime; `code` is an apl_status value.
 struct RuntimeError : std::runtime_error {
   int code;
@@ -149,6 +159,7 @@ void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stre
 
 // One direct src -> tgt redistribution, compiled for the local devices.
 struct Exchange {
+  std::string label;      // NVTX range name: "<kind>|<src>><tgt>" (the cache key)
   int64_t in_bytes = 0;   // per-device source shard bytes
   int64_t out_bytes = 0;  // per-device target shard bytes
   std::vector<CopyDesc> host_copies;  // simulated mesh: everything

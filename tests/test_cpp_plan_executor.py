@@ -160,8 +160,9 @@ def test_native_executor_backward_matches_python(cuda, tmp_path, name):
 @pytest.mark.gpu
 def test_native_training_forward_rejects_fp32_plans(cuda, tmp_path):
     """The native backward computes in bf16: a training forward of the
-    reference's fp32 fixture plan is refused up front, while
-    the inference forward of the same plan runs."""
+    reference's fp32 fixture plan (every parameter dtype_bytes 4) is refused
+    up front with a PlanError, before any kernel reads an fp32
+    buffer as bf16. The operands are written at the graph's own widths."""
     import sys
 
     import torch
@@ -172,17 +173,20 @@ def test_native_training_forward_rejects_fp32_plans(cuda, tmp_path):
     exe = build(tmp_path)
     graph_path = PLANS / "gpt_block_fixture_graph.json"
     graph = json.loads(graph_path.read_text())
+    widths = {n["id"]: n["outputs"][0]["dtype_bytes"] for n in graph["nodes"] if n["outputs"]}
     feeds = _operands(graph)
     for k, v in feeds.items():
+        if v.is_floating_point() and widths[k] == 4:
+            v = v.float()
+        assert v.element_size() == widths[k], k
         (tmp_path / f"{k}.bin").write_bytes(v.contiguous().view(torch.uint8).cpu().numpy()
                                             .tobytes())
     out_shape = tuple(feeds["tok"].shape) + (feeds["wte"].shape[1],)
     (tmp_path / "dy.bin").write_bytes(torch.zeros(out_shape, dtype=torch.bfloat16)
                                       .view(torch.uint8).numpy().tobytes())
     name = "gpt_block_fixture_mesh2x2_unlimited.json"
-    args = [str(exe), str(graph_path), str(PLANS / name), "2x2", str(tmp_path)]
+    args = [str(exe), str(graph_path), str(PLANS / name), "2x2", str(tmp_path), "train"]
     r = subprocess.run(args, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stdout + r.stderr
-    r = subprocess.run(args + ["train"], capture_output=True, text=True, timeout=300)
     assert r.returncode != 0
+    assert r.returncode != -11, "segfault instead of a PlanError"
     assert "backward supports bf16 plans only" in r.stdout + r.stderr

@@ -31,7 +31,8 @@ def _rel(out, ref):
 
 
 # ---- kernels ---------------------------------------------------------------
-@pytest.mark.parametrize("rows,width", [(4096, 1024), (333, 64), (17, 1000), (5, 3)])
+@pytest.mark.parametrize("rows,width", [(4096, 1024), (333, 64), (17, 1000), (5, 3), (1000, 512),
+                                        (300, 2048), (64, 4096)])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 def test_layernorm_softmax(cuda, rows, width, dtype):
     torch.manual_seed(rows + width)
@@ -269,7 +270,7 @@ def test_attention_chain_fused(cuda):
 
 
 # ---- backward ----------------------------------------------------------------
-@pytest.mark.parametrize("rows,width", [(2048, 1024), (77, 40), (9, 5)])
+@pytest.mark.parametrize("rows,width", [(2048, 1024), (77, 40), (9, 5), (1000, 512), (64, 4096)])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 def test_layernorm_softmax_backward(cuda, rows, width, dtype):
     torch.manual_seed(rows)
