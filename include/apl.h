@@ -391,6 +391,10 @@ int apl_matmul_strategies(const apl_mesh_desc* mesh, const apl_meta* a_meta,
 int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                   int64_t lda, int64_t ldb, int64_t ldc, int b_layout, int out_dtype,
                   int epilogue, void* stream);
+/* Force parts of every later GEMM's launch plan (-1 = automatic): pair != 0
+ * the 2-CTA kernel (256-row tiles), bn the N tile (128 / 256), streamk != 0
+ * the stream-K schedule. For A/B measurements; results do not change. */
+int apl_gemm_force_plan(int pair, int bn, int streamk);
 
 /* Grouped GEMM, one persistent launch: `groups` output problems, each the
  * sum over `reduce` inputs C_g = epi(sum_r A[g*reduce+r] . B[g*reduce+r]),
@@ -493,6 +497,12 @@ int apl_layernorm_backward_scratch(int64_t rows, int64_t width, size_t* bytes);
 int apl_layernorm_backward(const void* x, const void* gamma, const void* dy, void* dx,
                            float* dgamma, float* dbeta, void* stats, int64_t rows, int64_t width,
                            float eps, int dtype, void* stream);
+/* The same with the scratch size passed in (apl_version >= 101): returns
+ * APL_ERR_ARG instead of writing past `stats` when stats_bytes is below
+ * apl_layernorm_backward_scratch(). */
+int apl_layernorm_backward_ex(const void* x, const void* gamma, const void* dy, void* dx,
+                              float* dgamma, float* dbeta, void* stats, size_t stats_bytes,
+                              int64_t rows, int64_t width, float eps, int dtype, void* stream);
 /* softmax (last dim) from its output y: dx = alpha * y * (dy - sum(dy * y)). */
 int apl_softmax_backward(const void* y, const void* dy, void* dx, int64_t rows, int64_t width,
                          float alpha, int dtype, void* stream);

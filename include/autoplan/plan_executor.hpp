@@ -448,13 +448,12 @@ class PlanExecutor {
     if (have == want) return g;
     TensorMeta m = nodes_.at(id).meta;
     m.dtype_bytes = g.eb;
-    const TransformPath path = find_transform_path(have, want, mesh_, m);
+    const CachedPath& cp = cached_path(id, have, want, m);
     const size_t out_b = static_cast<size_t>(want.per_device_bytes(m, mesh_));
     std::vector<void*> out;
     for (int d = 0; d < num_local_; ++d) out.push_back(grad_buf(out_b));
-    const size_t wsb = workspace_bytes(rt_, path, m, fuse_);
-    void* ws = grad_buf(wsb < 256 ? 256 : wsb);
-    execute(rt_, path, m, g.p.data(), out.data(), ws, wsb, fuse_, stream);
+    void* ws = grad_buf(cp.ws < 256 ? 256 : cp.ws);
+    execute(rt_, cp.path, m, g.p.data(), out.data(), ws, cp.ws, fuse_, stream);
     return Grad{as_const(out), g.eb};
   }
 
@@ -522,10 +521,10 @@ class PlanExecutor {
         size_t sb = 0;
         if (has_g || has_b) apl_detail::check(apl_layernorm_backward_scratch(rows, h, &sb));
         void* stats = has_g || has_b ? grad_buf(sb) : nullptr;
-        apl_detail::check(apl_layernorm_backward(sv[0][d], has_g ? sv[1][d] : nullptr, dy.p[d],
-                                                 o, static_cast<float*>(g),
-                                                 static_cast<float*>(b), stats, rows, h, 1e-5f,
-                                                 APL_BF16, stream));
+        apl_detail::check(apl_layernorm_backward_ex(sv[0][d], has_g ? sv[1][d] : nullptr,
+                                                    dy.p[d], o, static_cast<float*>(g),
+                                                    static_cast<float*>(b), stats, sb, rows, h,
+                                                    1e-5f, APL_BF16, stream));
         dx.push_back(o);
         if (has_g) dg.push_back(g);
         if (has_b) db.push_back(b);
@@ -925,6 +924,26 @@ class PlanExecutor {
     return as_const(out);
   }
 
+  // The reference path and its workspace size per (value, have -> want,
+  // element size), searched once: later steps (and every backward pass)
+  // convert without touching the host planner.
+  struct CachedPath {
+    TransformPath path;
+    size_t ws;
+  };
+  const CachedPath& cached_path(const std::string& id, const ShardingSpec& have,
+                                const ShardingSpec& want, const TensorMeta& m) {
+    const std::string key = id + "|" + have.to_string() + ">" + want.to_string() + "|" +
+                            std::to_string(m.dtype_bytes);
+    auto it = paths_.find(key);
+    if (it == paths_.end()) {
+      TransformPath p = find_transform_path(have, want, mesh_, m);
+      const size_t ws = workspace_bytes(rt_, p, m, fuse_);
+      it = paths_.emplace(key, CachedPath{std::move(p), ws}).first;
+    }
+    return it->second;
+  }
+
   static std::vector<const void*> as_const(const std::vector<void*>& v) {
     return std::vector<const void*>(v.begin(), v.end());
   }
@@ -946,12 +965,13 @@ class PlanExecutor {
                                    const ShardingSpec& have, const ShardingSpec& want,
                                    void* stream) {
     const TensorMeta& m = nodes_.at(src).meta;
-    const TransformPath path = find_transform_path(have, want, mesh_, m);
+    const CachedPath& cp = cached_path(src, have, want, m);
+    const TransformPath& path = cp.path;
     auto out = buffers(src + ">" + want.to_string(), want, m);
     const std::string wkey = src + ">" + want.to_string();
     auto w = workspaces_.find(wkey);
     if (w == workspaces_.end()) {
-      const size_t bytes = workspace_bytes(rt_, path, m, fuse_);
+      const size_t bytes = cp.ws;
       void* ws = nullptr;
       if (cudaMalloc(&ws, bytes < 256 ? 256 : bytes) != cudaSuccess)
         throw RuntimeFailure(APL_ERR_CUDA, "cudaMalloc of a conversion workspace failed");
@@ -977,6 +997,7 @@ class PlanExecutor {
   int gcount_ = 0;
   std::map<std::string, std::vector<void*>> buffers_;
   std::map<std::string, std::pair<void*, size_t>> workspaces_;
+  std::map<std::string, CachedPath> paths_;
 };
 
 }  // namespace autoplan

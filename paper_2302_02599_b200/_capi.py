@@ -138,6 +138,7 @@ _SIGS = {
                                  C.c_int, C.c_void_p]),
     "apl_matmul_strategies": (C.c_int, [P(MeshDesc), P(Meta), P(Meta), C.c_int, C.c_double,
                                         P(StrategyInfoC), C.c_int, P(C.c_int)]),
+    "apl_gemm_force_plan": (C.c_int, [C.c_int, C.c_int, C.c_int]),
     "apl_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                 C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
                                 C.c_int, C.c_void_p]),
@@ -192,6 +193,10 @@ _SIGS = {
     "apl_layernorm_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                          C.c_int64, C.c_float, C.c_int, C.c_void_p]),
+    "apl_layernorm_backward_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                            C.c_int64, C.c_int64, C.c_float, C.c_int,
+                                            C.c_void_p]),
     "apl_layernorm_backward_scratch": (C.c_int, [C.c_int64, C.c_int64, P(C.c_size_t)]),
     "apl_softmax_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                        C.c_float, C.c_int, C.c_void_p]),

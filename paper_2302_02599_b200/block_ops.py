@@ -104,14 +104,15 @@ def layernorm_backward(x: torch.Tensor, gamma: torch.Tensor | None, dy: torch.Te
     """dx of a layernorm; dgamma / dbeta (fp32) are ACCUMULATED into."""
     w = x.shape[-1]
     rows = x.numel() // w
-    stats = None
+    stats, nbytes = None, 0
     if dgamma is not None or dbeta is not None:
         n = C.c_size_t()
         check(A.lib().apl_layernorm_backward_scratch(rows, w, C.byref(n)))
         stats = torch.empty((n.value + 15) // 16 * 4, dtype=torch.float32, device=x.device)
-    check(A.lib().apl_layernorm_backward(_p(x), _p(gamma), _p(dy), _p(dx), _p(dgamma),
-                                         _p(dbeta), _p(stats), rows, w, eps,
-                                         _DTYPE_CODE[x.dtype], _stream_handle(stream)))
+        nbytes = stats.numel() * 4
+    check(A.lib().apl_layernorm_backward_ex(_p(x), _p(gamma), _p(dy), _p(dx), _p(dgamma),
+                                            _p(dbeta), _p(stats), nbytes, rows, w, eps,
+                                            _DTYPE_CODE[x.dtype], _stream_handle(stream)))
 
 
 def softmax_backward(y: torch.Tensor, dy: torch.Tensor, dx: torch.Tensor, alpha: float = 1.0,

@@ -179,7 +179,7 @@ autoplan::DimDiffWeights weights_of(const double* w) {
 
 extern "C" {
 
-int apl_version(void) { return 100; }
+int apl_version(void) { return 101; }  // 101: apl_layernorm_backward_ex
 
 const char* apl_last_error(void) { return g_last_error.c_str(); }
 
@@ -930,6 +930,15 @@ int apl_matmul_strategies(const apl_mesh_desc* mesh, const apl_meta* a_meta,
   });
 }
 
+int apl_gemm_force_plan(int pair, int bn, int streamk) {
+  return guarded([&] {
+    need(pair >= -1 && pair <= 1 && (bn == -1 || bn == 128 || bn == 256) && streamk >= -1 &&
+             streamk <= 1,
+         "pair / streamk in {-1, 0, 1}, bn in {-1, 128, 256}");
+    apl::gemm_force_plan(pair, bn, streamk);
+  });
+}
+
 int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                   int64_t lda, int64_t ldb, int64_t ldc, int b_layout, int out_dtype,
                   int epilogue, void* stream) {
@@ -1159,6 +1168,18 @@ int apl_layernorm_backward(const void* x, const void* gamma, const void* dy, voi
                                                    static_cast<cudaStream_t>(stream)),
                     "layernorm backward launch");
   });
+}
+
+int apl_layernorm_backward_ex(const void* x, const void* gamma, const void* dy, void* dx,
+                              float* dgamma, float* dbeta, void* stats, size_t stats_bytes,
+                              int64_t rows, int64_t width, float eps, int dtype, void* stream) {
+  if ((dgamma != nullptr || dbeta != nullptr) && rows > 0 && width > 0 &&
+      stats_bytes < apl::layernorm_backward_scratch_bytes(rows, width)) {
+    g_last_error = "stats scratch smaller than apl_layernorm_backward_scratch()";
+    return APL_ERR_ARG;
+  }
+  return apl_layernorm_backward(x, gamma, dy, dx, dgamma, dbeta, stats, rows, width, eps, dtype,
+                                stream);
 }
 
 int apl_layernorm_backward_scratch(int64_t rows, int64_t width, size_t* bytes) {

@@ -25,6 +25,8 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 namespace apl {
 
@@ -375,10 +377,12 @@ __device__ __forceinline__ uint32_t ldg_stream4(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+// No "memory" clobber: volatile asm keeps these stores in program order with
+// the volatile prefetch loads, while ordinary loads (gamma / beta, L1 hits)
+// may still be scheduled across them instead of serialising behind each store.
 __device__ __forceinline__ void stg16(void* p, const uint4& v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
+               "r"(v.w));
 }
 
 __device__ __forceinline__ float ex2_ftz(float v) {
@@ -530,38 +534,43 @@ __global__ void __launch_bounds__(256) layernorm_pipe_kernel(
   if (r < rows) load(r, cur);
   for (; r < rows; r += stride) {
     if (r + stride < rows) load(r + stride, nxt);
-    float f[NV][V];
+    // the row stays packed; each pass unpacks it again (one ALU op per bf16)
     float s = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j)
       if (lane + 32 * j < nv) {
-        R::unpack(cur[j], f[j]);
+        float f[V];
+        R::unpack(cur[j], f);
 #pragma unroll
-        for (int k = 0; k < V; ++k) s += f[j][k];
+        for (int k = 0; k < V; ++k) s += f[k];
       }
     const float mean = warp_sum(s) * inv_w;
     float q = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j)
-      if (lane + 32 * j < nv)
+      if (lane + 32 * j < nv) {
+        float f[V];
+        R::unpack(cur[j], f);
 #pragma unroll
-        for (int k = 0; k < V; ++k) q += (f[j][k] - mean) * (f[j][k] - mean);
+        for (int k = 0; k < V; ++k) q += (f[k] - mean) * (f[k] - mean);
+      }
     const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int i = lane + 32 * j;
       if (i < nv) {
-        float g[V], b[V];
+        float f[V], g[V], b[V];
+        R::unpack(cur[j], f);
         if (gamma != nullptr) load_row<T, V>(gamma, i, g);
         if (beta != nullptr) load_row<T, V>(beta, i, b);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
-          float v = (f[j][k] - mean) * rstd;
+          float v = (f[k] - mean) * rstd;
           if (gamma != nullptr) v *= g[k];
           if (beta != nullptr) v += b[k];
-          f[j][k] = v;
+          f[k] = v;
         }
-        stg16(y + r * width + static_cast<int64_t>(i) * V, R::pack(f[j]));
+        stg16(y + r * width + static_cast<int64_t>(i) * V, R::pack(f));
       }
     }
 #pragma unroll
@@ -995,6 +1004,36 @@ cudaError_t done() {
   return cudaGetLastError();
 }
 
+// Grid of a prefetching row kernel: exactly the CTAs that are resident at
+// once (SMs x occupancy), so every warp walks many rows with its prefetch
+// always in flight instead of paying an unhidden first-row load per short
+// CTA lifetime; never more warps than rows.
+template <typename... Args>
+int pipe_grid(void (*kernel)(Args...), int64_t rows) {
+  static std::mutex mu;
+  static std::map<const void*, int> occ_of;
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  int occ;
+  {
+    std::lock_guard<std::mutex> hold(mu);
+    auto it = occ_of.find(reinterpret_cast<const void*>(kernel));
+    if (it == occ_of.end()) {
+      int o = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, 256, 0) != cudaSuccess || o < 1)
+        o = 1;
+      it = occ_of.emplace(reinterpret_cast<const void*>(kernel), o).first;
+    }
+    occ = it->second;
+  }
+  const int64_t need = (rows * 32 + 255) / 256;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t{sms} * occ)));
+}
+
 // APL_ROW_PIPE=0 selects the r01 row kernels (A/B of the prefetching ones).
 bool pipe_rows_enabled() {
   static const bool on = [] {
@@ -1035,15 +1074,18 @@ cudaError_t rowwise(bool softmax, const void* x, const void* g, const void* b, v
   if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
     const bool masked = p.mask != nullptr;
     const int nv = per_lane == 1 ? 1 : per_lane == 2 ? 2 : 4;
-#define APL_ROW_PIPE(NVC)                                                                      \
-    if (!softmax)                                                                              \
-      layernorm_pipe_kernel<T, NVC><<<grid, 256, 0, s>>>(X, G, B, Y, rows, width, eps);        \
-    else if (masked)                                                                           \
-      softmax_pipe_kernel<T, NVC, true><<<grid, 256, 0, s>>>(X, Y, rows, width, p.alpha, p.mask, \
-                                                             p.fill);                          \
-    else                                                                                       \
-      softmax_pipe_kernel<T, NVC, false><<<grid, 256, 0, s>>>(X, Y, rows, width, p.alpha,      \
-                                                              nullptr, 0.f);
+#define APL_ROW_PIPE(NVC)                                                                    \
+    if (!softmax)                                                                            \
+      layernorm_pipe_kernel<T, NVC><<<pipe_grid(layernorm_pipe_kernel<T, NVC>, rows), 256, 0,  \
+                                      s>>>(X, G, B, Y, rows, width, eps);                      \
+    else if (masked)                                                                         \
+      softmax_pipe_kernel<T, NVC, true><<<pipe_grid(softmax_pipe_kernel<T, NVC, true>, rows),  \
+                                          256, 0, s>>>(X, Y, rows, width, p.alpha, p.mask,     \
+                                                       p.fill);                                \
+    else                                                                                     \
+      softmax_pipe_kernel<T, NVC, false><<<pipe_grid(softmax_pipe_kernel<T, NVC, false>, rows), \
+                                           256, 0, s>>>(X, Y, rows, width, p.alpha, nullptr,   \
+                                                        0.f);
     if (nv == 1) { APL_ROW_PIPE(1) }
     else if (nv == 2) { APL_ROW_PIPE(2) }
     else { APL_ROW_PIPE(4) }
@@ -1290,11 +1332,14 @@ cudaError_t layernorm_bwd_typed(const void* x, const void* gamma, const void* dy
   const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;
   if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
     if (per_lane == 1)
-      layernorm_bwd_pipe_kernel<T, 1><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+      layernorm_bwd_pipe_kernel<T, 1><<<pipe_grid(layernorm_bwd_pipe_kernel<T, 1>, rows), 256, 0,
+                                        s>>>(X, G, D, O, stats, rows, width, eps);
     else if (per_lane == 2)
-      layernorm_bwd_pipe_kernel<T, 2><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+      layernorm_bwd_pipe_kernel<T, 2><<<pipe_grid(layernorm_bwd_pipe_kernel<T, 2>, rows), 256, 0,
+                                        s>>>(X, G, D, O, stats, rows, width, eps);
     else
-      layernorm_bwd_pipe_kernel<T, 4><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
+      layernorm_bwd_pipe_kernel<T, 4><<<pipe_grid(layernorm_bwd_pipe_kernel<T, 4>, rows), 256, 0,
+                                        s>>>(X, G, D, O, stats, rows, width, eps);
   } else if (vec) {
     layernorm_bwd_kernel<T, V><<<grid, 256, 0, s>>>(X, G, D, O, stats, rows, width, eps);
   } else {
@@ -1328,9 +1373,15 @@ cudaError_t softmax_bwd_typed(const void* y, const void* dy, void* dx, int64_t r
   auto O = static_cast<T*>(dx);
   const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;
   if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
-    if (per_lane == 1) softmax_bwd_pipe_kernel<T, 1><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
-    else if (per_lane == 2) softmax_bwd_pipe_kernel<T, 2><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
-    else softmax_bwd_pipe_kernel<T, 4><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
+    if (per_lane == 1)
+      softmax_bwd_pipe_kernel<T, 1><<<pipe_grid(softmax_bwd_pipe_kernel<T, 1>, rows), 256, 0, s>>>(
+          Y, D, O, rows, width, alpha);
+    else if (per_lane == 2)
+      softmax_bwd_pipe_kernel<T, 2><<<pipe_grid(softmax_bwd_pipe_kernel<T, 2>, rows), 256, 0, s>>>(
+          Y, D, O, rows, width, alpha);
+    else
+      softmax_bwd_pipe_kernel<T, 4><<<pipe_grid(softmax_bwd_pipe_kernel<T, 4>, rows), 256, 0, s>>>(
+          Y, D, O, rows, width, alpha);
   } else if (vec) {
     softmax_bwd_kernel<T, V><<<grid, 256, 0, s>>>(Y, D, O, rows, width, alpha);
   } else {
@@ -1341,8 +1392,10 @@ cudaError_t softmax_bwd_typed(const void* y, const void* dy, void* dx, int64_t r
 
 }  // namespace
 
-// stats: rows float2 scratch (mean, rstd), needed when dgamma / dbeta are
-// requested.
+// stats: layernorm_backward_scratch_bytes(rows, width) of scratch -- the
+// per-row (mean, rstd) float2s, then the per-chunk parameter partials --
+// needed when dgamma / dbeta are requested (apl_layernorm_backward_ex checks
+// the size).
 cudaError_t launch_layernorm_backward(const void* x, const void* gamma, const void* dy, void* dx,
                                       float* dgamma, float* dbeta, void* stats, int64_t rows,
                                       int64_t width, float eps, int dtype, cudaStream_t s) {

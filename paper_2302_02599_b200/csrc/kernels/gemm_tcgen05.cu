@@ -31,6 +31,7 @@
 #include <atomic>
 #include <cstdint>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -631,13 +632,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 namespace pair {
 
 constexpr int kBM = 128;  // rows per CTA (M = 256 per pair)
-constexpr int kBN = 256;  // pair tile N; each CTA stages 128 rows/cols of B
-constexpr int kStageA = kBM * kBK * 2;         // 16 KiB
-constexpr int kStageB = (kBN / 2) * kBK * 2;   // 16 KiB
-constexpr int kStages = 6;
-constexpr int kData = kStages * (kStageA + kStageB);
-constexpr int kBytes = kData + 1024 + 256;
-constexpr int kTmemCols = 512;  // 2 x 256 fp32 accumulator columns
+
+// Pair tile 256 x BN: each CTA stages its 128 rows of A and BN/2 rows (or
+// columns) of B per 64-deep K block; the MMA reads both CTAs' B halves.
+template <int BN>
+struct Cfg {
+  static constexpr int kStageA = kBM * kBK * 2;         // 16 KiB
+  static constexpr int kStageB = (BN / 2) * kBK * 2;    // 8 / 16 KiB
+  static constexpr int kStages = BN >= 256 ? 6 : 8;
+  static constexpr int kData = kStages * (kStageA + kStageB);
+  static constexpr int kBytes = kData + 1024 + 256;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -690,25 +696,47 @@ __device__ __forceinline__ void commit_pair(uint64_t* bar_local) {
       : "memory");
 }
 
-template <bool kBMN, bool kAMN>
+template <int BN, bool kBMN, bool kAMN>
 __device__ __forceinline__ constexpr uint32_t instr_desc_pair() {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kAMN ? 1 : 0) << 15) |
          (uint32_t(kBMN ? 1 : 0) << 16) |
-         (uint32_t(kBN >> 3) << 17) | (uint32_t((2 * kBM) >> 4) << 24);
+         (uint32_t(BN >> 3) << 17) | (uint32_t((2 * kBM) >> 4) << 24);
 }
 
-template <int kEpi, bool kOutF32, bool kBMN, bool kAMN>
+// Spin on a stream-K partial flag (acquire), trapping after ~4 s instead of
+// hanging the GPU if the writer can never run.
+__device__ __forceinline__ void wait_flag(const int* f) {
+  const long long t0 = clock64();
+  while (true) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (v != 0) return;
+    __nanosleep(64);
+    if (clock64() - t0 > (1ll << 33)) __trap();
+  }
+}
+
+// Persistent over pair tiles (cluster c takes tiles c, c + clusters, ...),
+// or -- args.streamk -- over a contiguous range of the (tile, k-block)
+// iteration space: cluster c owns [c*T/G, (c+1)*T/G). A tile split across
+// clusters is finished by the cluster holding its first k-block (its range
+// ENDS inside the tile: the "head"); each later cluster (its range STARTS
+// inside the tile) writes its fp32 partial -- each CTA its own 128 rows --
+// to sk_ws[its CTA] and raises sk_flags[its CTA]; the head CTA of the same
+// cluster rank adds them in cluster order (deterministic) and clears them.
+template <int BN, int kEpi, bool kOutF32, bool kBMN, bool kAMN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ GemmArgs args) {
+  using S = Cfg<BN>;
   const int M = args.M, N = args.N, K = args.K, ldc = args.ldc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* tiles_a = base;
-  uint8_t* tiles_b = base + kStages * kStageA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + kData);
-  uint64_t* empty = full + kStages;
-  uint64_t* acc_full = empty + kStages;
+  uint8_t* tiles_b = base + S::kStages * S::kStageA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + S::kData);
+  uint64_t* empty = full + S::kStages;
+  uint64_t* acc_full = empty + S::kStages;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -716,13 +744,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int kblocks = (K + kBK - 1) / kBK;
-  const int n_tiles = (N + kBN - 1) / kBN;
+  const int n_tiles = (N + BN - 1) / BN;
   const int per_problem = ((M + 2 * kBM - 1) / (2 * kBM)) * n_tiles;
   const int tiles = per_problem * args.count;
   const int cluster = blockIdx.x / 2, clusters = gridDim.x / 2;
+  const int KT = kblocks * args.reduce;
+  const bool sk = args.streamk != 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
     }
@@ -739,7 +769,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(tmem_slot)),
-                 "r"(kTmemCols));
+                 "r"(S::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -751,31 +781,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t full_leader0 = map_to_rank(smem_addr(&full[0]), 0);
       int it = 0;
-      for (int t = cluster; t < tiles; t += clusters) {
+      SegIter seg(sk, cluster, clusters, tiles, KT);
+      int t, k0, k1;
+      while (seg.next(t, k0, k1)) {
         const int g = t / per_problem, lt = t % per_problem;
         const int m0 = (lt / n_tiles) * 2 * kBM + static_cast<int>(rank) * kBM;
-        const int n0 = (lt % n_tiles) * kBN + static_cast<int>(rank) * (kBN / 2);
-        for (int kk = 0; kk < kblocks * args.reduce; ++kk, ++it) {
+        const int n0 = (lt % n_tiles) * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kk = k0; kk < k1; ++kk, ++it) {
           const int kb = kk % kblocks;
           const CUtensorMap* map_a = &args.a[g * args.reduce + kk / kblocks];
           const CUtensorMap* map_b = &args.b[g * args.reduce + kk / kblocks];
-          const int s = it % kStages;
-          const uint32_t phase = (it / kStages) & 1;
+          const int s = it % S::kStages;
+          const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
-          if (leader) mbar_expect_tx(&full[s], 2 * (kStageA + kStageB));
+          if (leader) mbar_expect_tx(&full[s], 2 * (S::kStageA + S::kStageB));
           if constexpr (kAMN) {  // A^T stored [K, M]: two [64 k][64 m] MN atoms
-            tma_load_2d_pair(tiles_a + s * kStageA, map_a, &full[s], m0, kb * kBK);
-            tma_load_2d_pair(tiles_a + s * kStageA + 8192, map_a, &full[s], m0 + 64, kb * kBK);
+            tma_load_2d_pair(tiles_a + s * S::kStageA, map_a, &full[s], m0, kb * kBK);
+            tma_load_2d_pair(tiles_a + s * S::kStageA + 8192, map_a, &full[s], m0 + 64, kb * kBK);
           } else {
-            tma_load_2d_pair(tiles_a + s * kStageA, map_a, &full[s], kb * kBK, m0);
+            tma_load_2d_pair(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
           }
           if constexpr (kBMN) {
 #pragma unroll
-            for (int j = 0; j < (kBN / 2) / 64; ++j)
-              tma_load_2d_pair(tiles_b + s * kStageB + j * 8192, map_b, &full[s], n0 + j * 64,
+            for (int j = 0; j < (BN / 2) / 64; ++j)
+              tma_load_2d_pair(tiles_b + s * S::kStageB + j * 8192, map_b, &full[s], n0 + j * 64,
                                kb * kBK);
           } else {
-            tma_load_2d_pair(tiles_b + s * kStageB, map_b, &full[s], kb * kBK, n0);
+            tma_load_2d_pair(tiles_b + s * S::kStageB, map_b, &full[s], kb * kBK, n0);
           }
           if (!leader) remote_arrive(full_leader0 + s * 8);
         }
@@ -783,26 +815,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = instr_desc_pair<kBMN, kAMN>();
+      constexpr uint32_t idesc = instr_desc_pair<BN, kBMN, kAMN>();
       int it = 0, local = 0;
-      for (int t = cluster; t < tiles; t += clusters, ++local) {
+      SegIter seg(sk, cluster, clusters, tiles, KT);
+      int t, k0, k1;
+      for (; seg.next(t, k0, k1); ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem + uint32_t(acc * kBN);
-        for (int kk = 0; kk < kblocks * args.reduce; ++kk, ++it) {
-          const int s = it % kStages;
-          mbar_wait(&full[s], (it / kStages) & 1);
+        const uint32_t d = tmem + uint32_t(acc * BN);
+        for (int kk = k0; kk < k1; ++kk, ++it) {
+          const int s = it % S::kStages;
+          mbar_wait(&full[s], (it / S::kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t da = kAMN ? smem_desc_mn(tiles_a + s * kStageA)
-                                   : smem_desc(tiles_a + s * kStageA);
-          const uint64_t db = kBMN ? smem_desc_mn(tiles_b + s * kStageB)
-                                   : smem_desc(tiles_b + s * kStageB);
+          const uint64_t da = kAMN ? smem_desc_mn(tiles_a + s * S::kStageA)
+                                   : smem_desc(tiles_a + s * S::kStageA);
+          const uint64_t db = kBMN ? smem_desc_mn(tiles_b + s * S::kStageB)
+                                   : smem_desc(tiles_b + s * S::kStageB);
           constexpr uint64_t kAdvA = kAMN ? (16 * 128) >> 4 : 2;
           constexpr uint64_t kAdvB = kBMN ? (16 * 128) >> 4 : 2;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            mma_pair(d, da + kAdvA * k, db + kAdvB * k, idesc, (kk > 0 || k > 0) ? 1u : 0u);
+            mma_pair(d, da + kAdvA * k, db + kAdvB * k, idesc, (kk > k0 || k > 0) ? 1u : 0u);
           commit_pair(&empty[s]);
         }
         commit_pair(&acc_full[acc]);
@@ -813,26 +847,80 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int half = (warp - 2) / 4;
     const uint32_t acc_empty_leader = map_to_rank(smem_addr(&acc_empty[0]), 0);
     int local = 0;
-    for (int t = cluster; t < tiles; t += clusters, ++local) {
+    SegIter seg(sk, cluster, clusters, tiles, KT);
+    int t, k0, k1;
+    for (; seg.next(t, k0, k1); ++local) {
       const int acc = local & 1;
       const int g = t / per_problem, lt = t % per_problem;
       const int m0 = (lt / n_tiles) * 2 * kBM + static_cast<int>(rank) * kBM;
-      const int n0 = (lt % n_tiles) * kBN;
+      const int n0 = (lt % n_tiles) * BN;
       void* const* const outs = args.c + g * args.fan;
-      const int row = m0 + quarter * 32 + lane;
+      const int trow = quarter * 32 + lane;
+      const int row = m0 + trow;
+      const bool partial = k0 > 0;
+      const bool head = !partial && k1 < KT;
+      int c_first = 0, c_last = -1;
+      if (head) {
+        // clusters after this one whose ranges start inside this tile (an
+        // empty range contributes nothing and raises no flag)
+        const int64_t tile_end = static_cast<int64_t>(t + 1) * KT;
+        c_first = cluster + 1;
+        c_last = cluster;
+        while (c_last + 1 < clusters && seg.total * (c_last + 1) / clusters < tile_end) ++c_last;
+        for (int cc = c_first; cc <= c_last; ++cc) {
+          if (seg.total * cc / clusters == seg.total * (cc + 1) / clusters) continue;
+          wait_flag(args.sk_flags + 2 * cc + static_cast<int>(rank));
+        }
+      }
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN);
+      const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
-      for (int c = half * (kBN / 2); c < (half + 1) * (kBN / 2); c += 32) {
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
         uint32_t r[32];
         tmem_ld32(lane_addr + uint32_t(c), r);
+        if (partial) {
+          float4* w = reinterpret_cast<float4*>(
+              args.sk_ws + (static_cast<size_t>(blockIdx.x) * kBM + trow) * BN + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            w[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                               __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          continue;
+        }
+        for (int cc = c_first; cc <= c_last; ++cc) {
+          if (seg.total * cc / clusters == seg.total * (cc + 1) / clusters) continue;
+          const float4* w = reinterpret_cast<const float4*>(
+              args.sk_ws + (static_cast<size_t>(2 * cc + rank) * kBM + trow) * BN + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 p = w[i];
+            r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + p.x);
+            r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + p.y);
+            r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + p.z);
+            r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + p.w);
+          }
+        }
         epi_store32<kEpi, kOutF32>(outs, args.fan, ldc, M, N, row, n0 + c, r, args.aux[g],
                                    args.ldaux);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) remote_arrive(acc_empty_leader + acc * 8);
+      if (partial || head) {
+        // all 8 epilogue warps of this CTA finished writing / reading
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (warp == 2 && lane == 0) {
+          if (partial) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(args.sk_flags + blockIdx.x),
+                         "r"(1)
+                         : "memory");
+          } else {
+            for (int cc = c_first; cc <= c_last; ++cc) args.sk_flags[2 * cc + rank] = 0;
+          }
+        }
+      }
     }
   }
 
@@ -841,13 +929,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(kTmemCols));
+                 "r"(S::kTmemCols));
   }
 }
 
 }  // namespace pair
 
 // ---- host side ---------------------------------------------------------------
+
+// APL_DEBUG=1: say which step of a GEMM launch failed (stderr).
+bool debug_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_DEBUG");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
+cudaError_t why(cudaError_t e, const char* what) {
+  if (e != cudaSuccess && debug_on())
+    std::fprintf(stderr, "apl gemm: %s: %s\n", what, cudaGetErrorString(e));
+  return e;
+}
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -858,6 +960,12 @@ EncodeFn encode_fn() {
   static EncodeFn fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
+    // by version first (the unversioned query can resolve differently under
+    // tools that interpose the driver, e.g. compute-sanitizer)
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && p != nullptr)
+      return reinterpret_cast<EncodeFn>(p);
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
             cudaSuccess ||
         q != cudaDriverEntryPointSuccess)
@@ -877,9 +985,14 @@ bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t elem[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
-             elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                         strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && debug_on())
+    std::fprintf(stderr, "apl gemm: cuTensorMapEncodeTiled(%p, %d x %d, ld %d, box %d x %d) = %d\n",
+                 ptr, rows, cols, ld, box_rows, box_cols, static_cast<int>(r));
+  return r == CUDA_SUCCESS;
 }
 
 template <int BN, int E, bool F, bool BMN, bool AMN = false>
@@ -889,7 +1002,7 @@ cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Smem<BN>::kBytes);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) return why(e, "cudaFuncSetAttribute(max dynamic smem)");
     configured = true;
   }
   static int sms = [] {
@@ -902,7 +1015,7 @@ cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
   const int grid = args.streamk ? sms : (tiles < sms ? tiles : sms);
   kernel<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return why(cudaGetLastError(), "gemm launch");
 }
 
 template <int BN, bool BMN>
@@ -926,14 +1039,14 @@ cudaError_t dispatch(const GemmArgs& args, bool out_f32, int epi, bool a_km,
 }
 
 // 2-CTA pair kernel launch (cluster dims are compiled into the kernel).
-template <int E, bool F, bool BMN, bool AMN = false>
+template <int BN, int E, bool F, bool BMN, bool AMN = false>
 cudaError_t launch_pair(const GemmArgs& args, cudaStream_t stream) {
-  auto kernel = pair::gemm_bf16_tcgen05_pair<E, F, BMN, AMN>;
+  auto kernel = pair::gemm_bf16_tcgen05_pair<BN, E, F, BMN, AMN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         pair::kBytes);
-    if (e != cudaSuccess) return e;
+                                         pair::Cfg<BN>::kBytes);
+    if (e != cudaSuccess) return why(e, "cudaFuncSetAttribute(max dynamic smem, pair)");
     configured = true;
   }
   static int sms = [] {
@@ -942,38 +1055,39 @@ cudaError_t launch_pair(const GemmArgs& args, cudaStream_t stream) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
   }();
-  const int tiles = ((args.N + pair::kBN - 1) / pair::kBN) *
+  const int tiles = ((args.N + BN - 1) / BN) *
                     ((args.M + 2 * pair::kBM - 1) / (2 * pair::kBM)) * args.count;
-  const int clusters = std::min(tiles, sms / 2);
-  kernel<<<2 * clusters, kThreads, pair::kBytes, stream>>>(args);
+  const int clusters = args.streamk ? sms / 2 : std::min(tiles, sms / 2);
+  kernel<<<2 * clusters, kThreads, pair::Cfg<BN>::kBytes, stream>>>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return why(cudaGetLastError(), "pair gemm launch");
 }
 
-template <bool BMN>
+template <int BN, bool BMN>
 cudaError_t dispatch_pair(const GemmArgs& args, bool out_f32, int epi, bool a_km,
                           cudaStream_t stream) {
   if (a_km) {
     if (epi != kEpiNone) return cudaErrorInvalidValue;
-    return out_f32 ? launch_pair<kEpiNone, true, BMN, true>(args, stream)
-                   : launch_pair<kEpiNone, false, BMN, true>(args, stream);
+    return out_f32 ? launch_pair<BN, kEpiNone, true, BMN, true>(args, stream)
+                   : launch_pair<BN, kEpiNone, false, BMN, true>(args, stream);
   }
   switch (epi) {
     case kEpiGelu:
-      return out_f32 ? launch_pair<kEpiGelu, true, BMN>(args, stream)
-                     : launch_pair<kEpiGelu, false, BMN>(args, stream);
+      return out_f32 ? launch_pair<BN, kEpiGelu, true, BMN>(args, stream)
+                     : launch_pair<BN, kEpiGelu, false, BMN>(args, stream);
     case kEpiDGelu:
-      return out_f32 ? cudaErrorInvalidValue : launch_pair<kEpiDGelu, false, BMN>(args, stream);
+      return out_f32 ? cudaErrorInvalidValue : launch_pair<BN, kEpiDGelu, false, BMN>(args, stream);
     case kEpiGeluSave:
-      return out_f32 ? cudaErrorInvalidValue : launch_pair<kEpiGeluSave, false, BMN>(args, stream);
+      return out_f32 ? cudaErrorInvalidValue
+                     : launch_pair<BN, kEpiGeluSave, false, BMN>(args, stream);
     default:
-      return out_f32 ? launch_pair<kEpiNone, true, BMN>(args, stream)
-                     : launch_pair<kEpiNone, false, BMN>(args, stream);
+      return out_f32 ? launch_pair<BN, kEpiNone, true, BMN>(args, stream)
+                     : launch_pair<BN, kEpiNone, false, BMN>(args, stream);
   }
 }
 
 // Stream-K for single-CTA launches whose tiles fill the SMs badly, e.g.
-// per-GPU shards of 8-way strategies (opt-in, see streamk_setup). Workspace
+// per-GPU shards of 8-way strategies (see plan_gemm). Workspace
 // (fp32 partial tiles, one per CTA) and flags are kept per stream.
 struct StreamKWs {
   float* ws = nullptr;
@@ -987,25 +1101,32 @@ int stream_k_forced() {
   }();
   return forced;
 }
-bool stream_k_enabled() { return stream_k_forced() == 1; }
+// APL_GEMM_STREAMK unset: stream-K competes in plan_gemm's cost model only
+// when APL_GEMM_SK_AUTO=1 (off until measured; see DESIGN 4.2).
+bool stream_k_auto() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_GEMM_SK_AUTO");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
 
-bool streamk_setup(GemmArgs& args, int tiles, int kt, cudaStream_t stream) {
-  const int forced = stream_k_forced();
+std::atomic<int> g_force_pair{-1}, g_force_bn{-1}, g_force_sk{-1};
+
+int sm_count_cached() {
   static int sms = [] {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
   }();
-  const int waves = (tiles + sms - 1) / sms;
-  const double fill = static_cast<double>(tiles) / (static_cast<double>(waves) * sms);
-  // Opt-in (APL_GEMM_STREAMK=1): on the r01 per-GPU shapes the 128 x 256
-  // stream-K tiles were L2-latency bound (2048 x 1024 x 4096: 405 vs 675
-  // TFLOP/s with plain 128 x 128 tiles), so the default keeps the tile grid.
-  (void)fill;
-  (void)waves;
-  const bool want = forced == 1 && kt >= 4 && static_cast<int64_t>(tiles) * kt >= 2 * sms;
-  if (!want || args.reduce != 1 || args.fan != 1 || args.scatter_rows > 0) return false;
+  return sms;
+}
+
+// Stream-K workspace: one fp32 128 x 256 partial tile and one flag per CTA,
+// kept per stream (partial tiles of one launch are consumed within it).
+bool streamk_attach(GemmArgs& args, cudaStream_t stream) {
+  const int sms = sm_count_cached();
   static std::mutex mu;
   static std::map<cudaStream_t, StreamKWs> pool;
   std::lock_guard<std::mutex> hold(mu);
@@ -1023,19 +1144,68 @@ bool streamk_setup(GemmArgs& args, int tiles, int kt, cudaStream_t stream) {
   return true;
 }
 
-// CTA-pair kernel for problems big enough to fill 256 x 256 tiles;
-// APL_GEMM_PAIR=0/1 forces the choice.
-bool use_pair(int M, int N, int count) {
-  static const int forced = [] {
+// Which kernel, tile and schedule a GEMM launch uses.
+struct GemmPlan {
+  bool paired;   // CTA-pair (cta_group::2) kernel, 256-row tiles
+  int bn;        // N tile: 128 or 256
+  bool streamk;  // stream-K over (tile, k-block) instead of whole tiles
+};
+
+// Relative per-SM throughput of each tile shape (measured r02: the 1-CTA
+// 128 x 128 tile is shared-memory bound -- MMA operand reads plus TMA fills
+// -- at about half the pair's rate).
+double tile_eff(bool paired, int bn) {
+  if (paired) return bn == 256 ? 1.0 : 0.92;
+  return bn == 256 ? 0.75 : 0.5;
+}
+
+// Cost model: per-SM work of a tile / its efficiency, times the waves of
+// tiles over the resident units (clusters for pairs, CTAs otherwise);
+// stream-K spreads the k-blocks evenly and pays ~8% for the fixup.
+// APL_GEMM_PAIR=0/1, APL_GEMM_BN=128/256, APL_GEMM_STREAMK=0/1 force parts.
+GemmPlan plan_gemm(int M, int N, int K, int count, bool sk_allowed, bool pair_allowed) {
+  static const int e_pair = [] {
     const char* e = std::getenv("APL_GEMM_PAIR");
     return e ? std::atoi(e) : -1;
   }();
-  if (forced >= 0) return forced == 1;
-  // r01 gemm_bench: pairs win once there are at least ~half an SM-count of
-  // 256 x 256 tiles (fc1 1331 vs 1145 TFLOP/s); with fewer the single-CTA
-  // 128 x 256 tiles fill the machine better (fc2 split-m/8: 673 vs 626).
-  const int pair_tiles = ((M + 255) / 256) * ((N + 255) / 256) * count;
-  return M >= 256 && N >= 256 && pair_tiles >= 56;
+  static const int e_bn = [] {
+    const char* e = std::getenv("APL_GEMM_BN");
+    return e ? std::atoi(e) : -1;
+  }();
+  // apl_gemm_force() overrides (A/B sweeps in one process), then the env
+  const int o_pair = g_force_pair.load(), o_bn = g_force_bn.load(), o_sk = g_force_sk.load();
+  const int f_pair = o_pair >= 0 ? o_pair : e_pair;
+  const int f_bn = o_bn > 0 ? o_bn : e_bn;
+  const int f_sk = o_sk >= 0 ? o_sk : stream_k_forced();
+  const int sms = sm_count_cached();
+  const int kb = (K + kBK - 1) / kBK;
+  GemmPlan best{false, 128, false};
+  double best_cost = 1e300;
+  for (int paired = 0; paired < 2; ++paired) {
+    if (paired && !pair_allowed) continue;
+    if (f_pair >= 0 && paired != f_pair) continue;
+    for (int bn : {128, 256}) {
+      if (f_bn > 0 && bn != f_bn) continue;
+      const int64_t tm = paired ? 256 : 128;
+      const int64_t tiles = ((M + tm - 1) / tm) * ((N + bn - 1) / bn) * count;
+      const int units = paired ? sms / 2 : sms;
+      const double work = static_cast<double>(tm) * bn / (paired ? 2 : 1) * kb /
+                          tile_eff(paired != 0, bn);
+      for (int sk = 0; sk < 2; ++sk) {
+        if (sk && (!sk_allowed || kb < 4 || tiles * kb < 2 * units)) continue;
+        if (f_sk >= 0 && sk != f_sk) continue;
+        const double cost = sk ? 1.08 * work * static_cast<double>(tiles) / units
+                               : work * static_cast<double>((tiles + units - 1) / units);
+        // auto mode keeps stream-K off until it is measured better (r02)
+        if (sk && f_sk < 0 && !stream_k_auto()) continue;
+        if (cost < best_cost) {
+          best_cost = cost;
+          best = GemmPlan{paired != 0, bn, sk != 0};
+        }
+      }
+    }
+  }
+  return best;
 }
 
 }  // namespace
@@ -1054,33 +1224,20 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
                               int ldb, int ldc, bool b_kn, bool out_f32, int epi, bool a_km,
                               const void* const* aux, int ldaux, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || groups <= 0) return cudaSuccess;
+  if (encode_fn() == nullptr) return cudaErrorSymbolNotFound;  // no cuTensorMapEncodeTiled
   if (reduce < 1 || fan < 1 || reduce > kMaxBatch || fan > kMaxBatch) return cudaErrorInvalidValue;
   if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;  // TMA row alignment
   if (epi < kEpiNone || epi > kEpiGeluSave || (epi >= kEpiDGelu && aux == nullptr))
     return cudaErrorInvalidValue;
   const int per_launch = std::max(1, std::min(kMaxBatch / reduce, kMaxBatch / fan));
-  const bool paired = !(epi == kEpiDGelu && out_f32) && use_pair(M, N, std::min(groups, per_launch));
-  int bn = (N >= 256 && (N % 256 == 0 || N > 1024)) ? 256 : 128;
-  {
-    // Too few 128 x 256 tiles to cover the SMs once (a per-GPU shard of a
-    // split-m / split-n strategy, e.g. 2048 x 1024): 128 x 128 tiles double
-    // the CTAs that work.
-    static const int sms = [] {
-      int dev = 0, n = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-      return n > 0 ? n : 148;
-    }();
-    const int count = std::min(groups, per_launch);
-    const int tiles256 = ((M + kBM - 1) / kBM) * ((N + 255) / 256) * count;
-    // stream-K keeps the 128 x 256 tiles (less operand traffic per FLOP) and
-    // spreads their k-iterations over every SM instead
-    const bool sk_ok = !paired && reduce == 1 && fan == 1 && stream_k_enabled();
-    if (bn == 256 && tiles256 < sms && !sk_ok) bn = 128;
-  }
+  const GemmPlan plan = plan_gemm(M, N, K, std::min(groups, per_launch),
+                                  /*sk_allowed=*/reduce == 1 && fan == 1,
+                                  /*pair_allowed=*/!(epi == kEpiDGelu && out_f32));
+  const bool paired = plan.paired;
+  const int bn = plan.bn;
   // B box rows for the K-major layout: the pair kernel stages half of its
-  // 256-wide N tile per CTA.
-  const int b_rows = paired ? pair::kBN / 2 : bn;
+  // N tile per CTA.
+  const int b_rows = paired ? bn / 2 : bn;
   for (int first = 0; first < groups; first += per_launch) {
     GemmArgs args;
     std::memset(&args, 0, sizeof(args));
@@ -1106,13 +1263,14 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
     for (int i = 0; i < args.count * fan; ++i) args.c[i] = C[first * fan + i];
     if (epi >= kEpiDGelu)
       for (int i = 0; i < args.count; ++i) args.aux[i] = aux[first + i];
-    if (!paired)
-      streamk_setup(args, ((M + kBM - 1) / kBM) * ((N + bn - 1) / bn) * args.count,
-                    (K + kBK - 1) / kBK, stream);
+    if (plan.streamk && !streamk_attach(args, stream)) return cudaErrorMemoryAllocation;
     cudaError_t e;
-    if (paired)
-      e = b_kn ? dispatch_pair<true>(args, out_f32, epi, a_km, stream)
-               : dispatch_pair<false>(args, out_f32, epi, a_km, stream);
+    if (paired && bn == 256)
+      e = b_kn ? dispatch_pair<256, true>(args, out_f32, epi, a_km, stream)
+               : dispatch_pair<256, false>(args, out_f32, epi, a_km, stream);
+    else if (paired)
+      e = b_kn ? dispatch_pair<128, true>(args, out_f32, epi, a_km, stream)
+               : dispatch_pair<128, false>(args, out_f32, epi, a_km, stream);
     else if (b_kn)
       e = bn == 256 ? dispatch<256, true>(args, out_f32, epi, a_km, stream)
                     : dispatch<128, true>(args, out_f32, epi, a_km, stream);
@@ -1177,6 +1335,14 @@ cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* 
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                       int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream) {
   return gemm_bf16_batched(&A, &B, &C, 1, M, N, K, lda, ldb, ldc, b_kn, out_f32, gelu, stream);
+}
+
+// Force parts of the GEMM plan (-1: automatic): the CTA pair kernel, the N
+// tile, stream-K. For A/B measurements (tools/gemm_bench.py --sweep).
+void gemm_force_plan(int pair, int bn, int streamk) {
+  g_force_pair.store(pair);
+  g_force_bn.store(bn);
+  g_force_sk.store(streamk);
 }
 
 cudaError_t gemm_bf16_tn(const void* A, const void* Bt, void* C, int M, int N, int K, int lda,

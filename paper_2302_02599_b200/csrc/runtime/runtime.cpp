@@ -214,6 +214,12 @@ EncodeTiled encode_tiled() {
   static EncodeTiled fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
+    // by version first (the unversioned query can resolve differently under
+    // tools that interpose the driver, e.g. compute-sanitizer)
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && p != nullptr)
+      return reinterpret_cast<EncodeTiled>(p);
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
             cudaSuccess ||
         q != cudaDriverEntryPointSuccess)

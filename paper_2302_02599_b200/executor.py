@@ -817,11 +817,13 @@ class PlanExecutor:
                 out.append((1, dt))
         elif kind == "batched-matmul":
             st = self.strategy[nid]
-            if st.partial_sum:
-                raise NotImplementedError("backward of split-k batched matmul strategies")
             a, b = self._saved[nid]
             # dA = dC . B^T partial over the axes sharding C's n dim, dB = A^T . dC
-            # over those sharding C's m dim (each device holds whole batches)
+            # over those sharding C's m dim (each device holds whole batches).
+            # Split-k strategies (partial_sum, intraop.cpp:208-231): the forward
+            # all-reduce over reduce_axes hands every partial the whole dC, so
+            # each device's k-shard gradients are dC . B_k^T and A_k^T . dC --
+            # the same local products, no extra reduction over reduce_axes.
             if wants_grad(ins[0]):
                 da = like(a)
                 for g, bb, o in zip(dy, b, da):

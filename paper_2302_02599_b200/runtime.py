@@ -8,6 +8,7 @@ eager-torch fallback: without a GPU or without libapl.so these calls raise.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 from typing import Sequence
 
 import torch
@@ -432,6 +433,7 @@ class PeerMesh:
             self.peer_ptrs.append(p.value)
             flag_ptrs.append(q.value)
         self._table = (C.c_void_p * len(self.peer_ptrs))(*self.peer_ptrs)
+        self._flag_ptrs = flag_ptrs
         self._all_flags = (C.c_void_p * P)(*flag_ptrs)
         self._counter = torch.zeros(4, dtype=torch.int32, device=f"cuda:{device}")
         self._peers = {}           # (src, tgt, shape, eb) -> (senders, readers)
@@ -549,72 +551,117 @@ class PeerMesh:
             ptrs.append(p.value)
         return local, ptrs
 
+    def axis_group(self, axes) -> list:
+        """Ranks sharing this rank's coordinates off `axes`, in the order of
+        their mixed-radix coordinate on `axes` (the reference's replica-group
+        order, cluster.hpp:56; row-major rank <-> coordinate)."""
+        shape = list(self.geo.shape)
+        coord, r = [], self.rank
+        for n in reversed(shape):
+            coord.append(r % n)
+            r //= n
+        coord.reverse()
+        axes = sorted(axes)
+        members = []
+        for idx in itertools.product(*[range(shape[a]) for a in axes]):
+            c = list(coord)
+            for a, v in zip(axes, idx):
+                c[a] = v
+            rank = 0
+            for e, n in zip(c, shape):
+                rank = rank * n + e
+            members.append(rank)
+        return members
+
     def matmul_allreduce(self, a: torch.Tensor, b: torch.Tensor, out_dtype=torch.bfloat16,
-                         b_layout: str = "kn", stream=None) -> torch.Tensor:
-        """Split-k matmul over all ranks of this peer mesh with its all-reduce
-        fused in (Megatron fc2, reference split-k strategies, intraop.cpp:
-        141-234 with the partial-sum all-reduce of planner.cpp:263-282):
-        C = sum_r A_r . B_r on every rank, bit-identical replicas.
+                         b_layout: str = "kn", stream=None, axes=None) -> torch.Tensor:
+        """Split-k matmul over the ranks of this rank's `axes` group (None:
+        every mesh axis) with its all-reduce fused in (Megatron fc2, reference
+        split-k strategies, intraop.cpp:141-234 with the partial-sum
+        all-reduce over reduce_axes of planner.cpp:263-282):
+        C = sum_{r in group} A_r . B_r on every group member, bit-identical
+        replicas; groups that differ off `axes` run independently.
 
         Two kernels instead of GEMM + a collective: the GEMM's epilogue stores
-        each row block of its fp32 partial straight into the owning rank's
+        each row block of its fp32 partial straight into the owning member's
         staging slab (reduce-scatter traffic overlapping the MMAs), then each
-        owner sums its slabs and stores its rows into every rank's output
-        (the all-gather as peer stores); device-side epoch flags order them.
-        Returns this rank's exported output (valid until the next call with
-        the same shape)."""
-        P, r = self.geo.num_devices(), self.rank
+        owner sums its slabs and stores its rows into every member's output
+        (the all-gather as peer stores); device-side epoch flags, exchanged
+        only within the group, order them. Returns this rank's exported
+        output (valid until the next call with the same shape and axes)."""
+        axes = tuple(range(self.geo.rank())) if axes is None else tuple(sorted(axes))
+        members = self.axis_group(axes)
+        P, r, me = len(members), self.rank, members.index(self.rank)
         if P > 8:
             raise ValueError("fused peer all-reduce groups hold at most 8 ranks")
         M, K = a.shape
         N = b.shape[1] if b_layout == "kn" else b.shape[0]
         eb = torch.empty((), dtype=out_dtype).element_size()
         if M % P or (M // P) % 128:
-            raise ValueError("M / ranks must be a multiple of 128")
+            raise ValueError("M / group size must be a multiple of 128")
         rpo = M // P
-        key = (M, N, out_dtype)
+        key = (M, N, out_dtype, axes)
         bufs = getattr(self, "_ar_bufs", None)
         if bufs is None:
             bufs = self._ar_bufs = {}
         if key not in bufs:
             staging, staging_peers = self.shared_buffer(P * rpo * N * 4)
             c_local, c_peers = self.shared_buffer(M * N * eb)
-            slabs = (C.c_void_p * P)(*[sp + r * rpo * N * 4 for sp in staging_peers])
-            outs = (C.c_void_p * P)(*[cp + r * rpo * N * eb for cp in c_peers])
-            bufs[key] = (staging, c_local.view(out_dtype).view(M, N), slabs, outs)
-        staging, c_out, slabs, outs = bufs[key]
+            slabs = (C.c_void_p * P)(*[staging_peers[q] + me * rpo * N * 4 for q in members])
+            outs = (C.c_void_p * P)(*[c_peers[q] + me * rpo * N * eb for q in members])
+            others = [q for q in members if q != r]
+            flags = (C.c_void_p * max(1, len(others)))(*[self._flag_ptrs[q] for q in others])
+            Pm = self.geo.num_devices()
+            ready = (C.c_int32 * max(1, len(others)))(*others)
+            done = (C.c_int32 * max(1, len(others)))(*[Pm + q for q in others])
+            bufs[key] = (staging, c_local.view(out_dtype).view(M, N), slabs, outs, flags,
+                         len(others), ready, done)
+        staging, c_out, slabs, outs, flags, n_others, ready, done = bufs[key]
         self.epoch += 1
         e = self.epoch
-        self._last_readers = None  # every rank reads every slab
+        self._last_readers = None  # conservative: wait_readers waits on every rank
         sh = _stream_handle(stream)
         lib = A.lib()
+        Pm = self.geo.num_devices()
         check(lib.apl_peer_gemm_scatter(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), slabs, P,
                                         M, N, K, a.stride(0), b.stride(0),
                                         A.B_KN if b_layout == "kn" else A.B_NK, sh))
-        check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, r, e, sh))
-        check(lib.apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), self._ready_slots,
-                                      self._n_others, e, self.timeout_ms, sh))
+        if n_others:
+            check(lib.apl_peer_flags_store(flags, n_others, r, e, sh))
+            check(lib.apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), ready, n_others, e,
+                                          self.timeout_ms, sh))
         check(lib.apl_peer_reduce_gather(C.c_void_p(staging.data_ptr()), P, rpo * N, outs, P,
                                          _DTYPE_CODE[out_dtype], sh))
-        check(lib.apl_peer_flags_store(self._peer_flags, self._n_others, P + r, e, sh))
-        check(lib.apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), self._done_slots,
-                                      self._n_others, e, self.timeout_ms, sh))
+        if n_others:
+            check(lib.apl_peer_flags_store(flags, n_others, Pm + r, e, sh))
+            check(lib.apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), done, n_others, e,
+                                          self.timeout_ms, sh))
+        # ranks outside the group did not touch this rank's flags this epoch:
+        # raise their slots too so wait_readers / later epochs see a uniform epoch
+        outside = [q for q in range(Pm) if q not in members]
+        if outside:
+            check(lib.apl_peer_flags_store(
+                (C.c_void_p * len(outside))(*[self._flag_ptrs[q] for q in outside]), len(outside),
+                r, e, sh))
+            check(lib.apl_peer_flags_store(
+                (C.c_void_p * len(outside))(*[self._flag_ptrs[q] for q in outside]), len(outside),
+                Pm + r, e, sh))
         return c_out
 
     def sharded_matmul(self, strategy: "MatmulStrategy", a: torch.Tensor, b: torch.Tensor,
                        gelu: bool = False, b_layout: str = "kn", stream=None) -> torch.Tensor:
         """This rank's part of a sharded-matmul strategy on the peer mesh:
         strategies without a partial sum are one local tcgen05 GEMM on the
-        shards (GELU fused); partial-sum strategies reducing over every mesh
-        axis (split-k on a 1-D mesh, split-k:01.. on 2-D/3-D) run as the fused
-        GEMM + all-reduce over peer memory (matmul_allreduce)."""
+        shards (GELU fused); partial-sum strategies run as the fused GEMM +
+        all-reduce over peer memory within each reduce_axes group
+        (matmul_allreduce), GELU (if any) applied after the sum."""
         if not strategy.partial_sum:
             return gemm(a, b, gelu=gelu, b_layout=b_layout, stream=stream)
-        if sorted(strategy.reduce_axes) != list(range(self.geo.rank())):
-            raise NotImplementedError("peer partial sums reduce over all mesh axes")
+        c = self.matmul_allreduce(a, b, b_layout=b_layout, stream=stream,
+                                  axes=tuple(strategy.reduce_axes))
         if gelu:
-            raise NotImplementedError("GELU after a peer all-reduce is not fused")
-        return self.matmul_allreduce(a, b, b_layout=b_layout, stream=stream)
+            gelu(c, c, stream=stream)
+        return c
 
     def exchange_traffic(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta) -> dict:
         """This rank's bytes of the src->tgt exchange (wire_in = bytes pulled

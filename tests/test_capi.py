@@ -100,6 +100,8 @@ def test_block_entry_points_validate_arguments_without_a_gpu():
                                            None) == err  # slice outside the table
     assert lib.apl_layernorm_backward(one, None, one, one, P(16), None, None, 4, 8, 1e-5,
                                       A.BF16, None) == err  # dgamma without stats scratch
+    assert lib.apl_layernorm_backward_ex(one, None, one, one, P(16), None, one, 8, 4, 8, 1e-5,
+                                         A.BF16, None) == err  # stats scratch too small
     ptrs = (P * 1)(16)
     assert lib.apl_gemm_bf16_grouped_ex(ptrs, ptrs, ptrs, 1, 8, 8, 8, 4, 8, 8, 0, 1, A.BF16,
                                         None) == err  # lda < K (A as [M, K])

@@ -401,3 +401,64 @@ def test_block_plans_backward(cuda, name):
         mx = ((g - r).abs().max() / r.abs().max()).item()
         mean = ((g - r).abs().mean() / r.abs().mean()).item()
         assert mx <= 2e-2 and mean <= 1.5e-2, (k, mx, mean)
+
+
+# ---- every batched-matmul strategy, backward included --------------------------
+def _bmm_case(mesh_shape, st, param_spec):
+    """graph: parameters A[4,32,64], B[4,64,48] -> batched-matmul -> output,
+    planned with strategy `st` (the catalog's, intraop.cpp:208-231); the
+    parameters are stored in `param_spec` (None: the strategy's own input
+    layouts, so no conversion runs)."""
+    def node(i, kind, inputs, shape=None):
+        outs = [{"shape": shape, "dtype_bytes": 2, "requires_grad": True}] if shape else []
+        return {"id": i, "kind": kind, "inputs": [[x, 0] for x in inputs], "outputs": outs}
+
+    graph = {"version": 1, "placeholders": [], "output": "out",
+             "nodes": [node("A", "parameter", [], [4, 32, 64]),
+                       node("B", "parameter", [], [4, 64, 48]),
+                       node("mm", "batched-matmul", ["A", "B"]),
+                       node("out", "output", ["mm"])]}
+    sa = param_spec or str(st.a)
+    sb = param_spec or str(st.b)
+    plan = {"version": 1, "mesh": {"shape": list(mesh_shape)}, "nodes": {
+        "A": {"spec": sa, "strategy": f"src:{sa}", "partial_sum": False},
+        "B": {"spec": sb, "strategy": f"src:{sb}", "partial_sum": False},
+        "mm": {"spec": str(st.c), "strategy": st.name, "partial_sum": st.partial_sum,
+               "reduce_axes": list(st.reduce_axes)},
+        "out": {"spec": "RRR", "strategy": "collect", "partial_sum": False}}}
+    return graph, plan
+
+
+def _bmm_strategies():
+    from paper_2302_02599_b200 import DeviceMesh, TensorMeta
+    from paper_2302_02599_b200.strategies import matmul_strategies
+
+    a, b = TensorMeta((4, 32, 64), 2), TensorMeta((4, 64, 48), 2)
+    return [s for s in matmul_strategies(DeviceMesh.uniform([2, 2]), a, b, batched=True)]
+
+
+@pytest.mark.parametrize("param_spec", [None, "RRR"])
+@pytest.mark.parametrize("name", [s.name for s in _bmm_strategies()])
+def test_batched_matmul_strategy_backward(cuda, name, param_spec):
+    """Forward and backward of one batched matmul under every catalog
+    strategy on a 2x2 mesh -- split-k / split-bk / split-mk / split-nk
+    (partial sums all-reduced over reduce_axes) included -- against fp32
+    torch autograd; with the parameters stored replicated, the input
+    conversions and their reverse paths for the gradients run too."""
+    st = next(s for s in _bmm_strategies() if s.name == name)
+    graph, plan = _bmm_case([2, 2], st, param_spec)
+    torch.manual_seed(11)
+    A = torch.randn(4, 32, 64, device="cuda").bfloat16()
+    Bm = (torch.randn(4, 64, 48, device="cuda") / 8).bfloat16()
+    ex = PlanExecutor(Mesh.local([2, 2]), graph, plan)
+    out = ex.forward({"A": A, "B": Bm}, train=True)[0]
+    af, bf = A.float().requires_grad_(), Bm.float().requires_grad_()
+    ref = af @ bf
+    assert _rel(out, ref) <= 2e-2
+    gy = torch.randn(4, 32, 48, device="cuda").bfloat16()
+    ref.backward(gy.float())
+    grads = ex.backward(gy)
+    torch.cuda.synchronize()
+    for k, r in (("A", af.grad), ("B", bf.grad)):
+        g = _unshard(ex, k, grads[k]).float()
+        assert _rel(g, r) <= 2e-2, (name, k, _rel(g, r))

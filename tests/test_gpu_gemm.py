@@ -210,19 +210,38 @@ def test_megatron_mlp_on_mesh8(cuda):
         assert rel_err(h_kn[d], h[d].double()) <= 1e-2
 
 
-# Shapes that under-fill the SMs (stream-K candidates; the stream-K path itself
-# is opt-in -- run this file with APL_GEMM_STREAMK=1 to cover it).
+# Every launch plan (1-CTA / CTA-pair kernel x N tile 128 / 256 x whole
+# tiles / stream-K, forced through apl_gemm_force_plan) on shapes that
+# under-fill the SMs, ragged tails and both B layouts.
+PLANS = [(p, bn, sk) for p in (0, 1) for bn in (128, 256) for sk in (0, 1)]
+
+
+@pytest.fixture
+def force_plan():
+    from paper_2302_02599_b200 import _capi as A
+
+    lib = A.lib()
+    yield lambda p, bn, sk: lib.apl_gemm_force_plan(p, bn, sk)
+    lib.apl_gemm_force_plan(-1, -1, -1)
+
+
+@pytest.mark.parametrize("plan", PLANS, ids=[f"pair{p}-bn{bn}-sk{sk}" for p, bn, sk in PLANS])
 @pytest.mark.parametrize("m,n,k", [(2048, 1024, 4096), (1024, 512, 2048), (384, 768, 1000),
-                                   (2048, 1024, 512)])
-@pytest.mark.parametrize("gelu", [False, True])
-def test_gemm_stream_k_shapes(cuda, m, n, k, gelu):
+                                   (2048, 1024, 512), (16384, 512, 1024), (300, 200, 136)])
+def test_gemm_every_plan(cuda, force_plan, plan, m, n, k):
+    assert force_plan(*plan) == 0
     torch.manual_seed(m + k)
     a = torch.randn(m, k, device="cuda").bfloat16()
     bt = (torch.randn(n, k, device="cuda") / k ** 0.5).bfloat16()
-    for _ in range(2):  # the second call reuses the stream's workspace and flags
-        out = gemm(a, bt, gelu=gelu)
-        torch.cuda.synchronize()
-        assert rel_err(out, ref_mm(a, bt, gelu)) <= TOL_BF16
+    for gelu in (False, True):
+        for _ in range(2):  # the second call reuses the stream's workspace and flags
+            out = gemm(a, bt, gelu=gelu)
+            torch.cuda.synchronize()
+            assert rel_err(out, ref_mm(a, bt, gelu)) <= TOL_BF16, (plan, gelu)
     out32 = gemm(a, bt, out_dtype=torch.float32)
     torch.cuda.synchronize()
-    assert rel_err(out32, ref_mm(a, bt)) <= TOL_F32 * 10
+    assert rel_err(out32, ref_mm(a, bt)) <= TOL_F32, plan
+    if (n * 2) % 16 == 0:
+        out_kn = gemm(a, bt.t().contiguous(), b_layout="kn", out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert rel_err(out_kn, ref_mm(a, bt)) <= TOL_F32, plan

@@ -261,3 +261,78 @@ def test_fused_gemm_allreduce_over_peer_memory(cuda, world):
     for epoch in range(2):  # every rank holds the same bytes
         for dt in ("torch.bfloat16", "torch.float32"):
             assert len({r[5] for r in res if r[1] == epoch and r[2] == dt}) == 1
+
+
+def _subset_allreduce_worker(rank, world, port, q):
+    """Fused GEMM + all-reduce over a SUBSET of a 2-D peer mesh's axes (the
+    reference's split-k strategies on one axis of a 2-D mesh, e.g. reduce_axes
+    (1,) of split-mk:0,1): each reduce group sums only its own members'
+    partials, groups run independently on different operands; then GELU after
+    the sum through PeerMesh.sharded_matmul."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2302_02599_b200 import ShardingSpec
+    from paper_2302_02599_b200.runtime import MatmulStrategy, PeerMesh
+
+    try:
+        shape = [2, world // 2]
+        pm = PeerMesh(shape, rank, 0, 16)
+        coord = (rank // shape[1], rank % shape[1])
+        M, Kt, N = 512, 1024, 256
+        for axes in ((0,), (1,), (0, 1)):
+            members = pm.axis_group(axes)
+            me, P = members.index(rank), len(members)
+            # the operands of this rank's group: seeded by the coordinates off `axes`
+            key = sum(c * 10 ** i for i, c in enumerate(coord) if i not in axes)
+            g = torch.Generator(device="cuda").manual_seed(500 + key)
+            x = torch.randn(M, Kt, device="cuda", generator=g).bfloat16()
+            w = (torch.randn(Kt, N, device="cuda", generator=g) / Kt ** 0.5).bfloat16()
+            kr = Kt // P
+            a = x[:, me * kr:(me + 1) * kr].contiguous()
+            b = w[me * kr:(me + 1) * kr].contiguous()
+            c = pm.matmul_allreduce(a, b, out_dtype=torch.float32, axes=axes)
+            torch.cuda.synchronize()
+            ref = x.double() @ w.double()
+            err = ((c.double() - ref).abs().max() / ref.abs().max()).item()
+            q.put((rank, str(axes), err <= 1e-5, err, key, c.view(torch.uint8).sum(dtype=torch.int64).item()))
+            st = MatmulStrategy("split-k", ShardingSpec.parse("RR", 2), ShardingSpec.parse("RR", 2),
+                                ShardingSpec.parse("RR", 2), list(axes))
+            h = pm.sharded_matmul(st, a, b, gelu=True)
+            torch.cuda.synchronize()
+            ref = torch.nn.functional.gelu(ref)
+            err = ((h.double() - ref).abs().max() / ref.abs().max()).item()
+            q.put((rank, str(axes) + "+gelu", err <= 2e-2, err, key, 0))
+        dist.barrier()
+        pm.close()
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_fused_gemm_allreduce_over_axis_subsets(cuda, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_subset_allreduce_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    res = []
+    while not q.empty():
+        res.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert len(res) == world * 6
+    assert all(r[2] for r in res), [r for r in res if not r[2]]
+    for axes in ("(0,)", "(1,)", "(0, 1)"):  # replicas inside a group: identical bytes
+        by_group = {}
+        for r in res:
+            if r[1] == axes:
+                by_group.setdefault(r[4], set()).add(r[5])
+        assert all(len(v) == 1 for v in by_group.values()), (axes, by_group)

@@ -19,6 +19,7 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 
 def _run(tool, case, env_extra=None, timeout=900):
     env = dict(os.environ)
+    env["APL_DEBUG"] = "1"  # a failing launch says which step failed
     env.update(env_extra or {})
     cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--print-limit", "20",
            sys.executable, str(ROOT / "tools" / "sanitize_case.py"), case]
@@ -26,7 +27,9 @@ def _run(tool, case, env_extra=None, timeout=900):
     out = p.stdout + p.stderr
     assert p.returncode == 0, out[-4000:]
     assert f"sanitize case {case}: ok" in out, out[-4000:]
-    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+    clean = ("RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" if tool == "racecheck"
+             else "ERROR SUMMARY: 0 errors")
+    assert clean in out, out[-4000:]
     return out
 
 

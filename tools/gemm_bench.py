@@ -2,6 +2,11 @@
 torch.matmul (cuBLAS) and the measured bf16 peak; prints one JSON object.
 
     python tools/gemm_bench.py [--quick]
+    python tools/gemm_bench.py --sweep     # every launch plan per shape (JSON lines)
+
+--sweep forces each plan (apl_gemm_force_plan: 1-CTA / CTA-pair kernel,
+N tile 128 / 256, whole tiles / stream-K) on every shape and prints one line
+per (shape, plan) with its time, plus the automatic plan and cuBLAS.
 """
 import json
 import sys
@@ -44,7 +49,41 @@ def time_fn(fn, iters):
     return a.elapsed_time(b) / iters
 
 
+def sweep():
+    import ctypes as C
+
+    from paper_2302_02599_b200 import _capi as A
+
+    lib = A.lib()
+    pk = peak()
+    plans = [("auto", -1, -1, -1)] + [(f"{'pair' if p else 'cta'}{bn}{'-sk' if sk else ''}", p, bn, sk)
+                                      for p in (0, 1) for bn in (128, 256) for sk in (0, 1)]
+    for name, m, n, k in SHAPES:
+        a = torch.randn(m, k, device="cuda").bfloat16()
+        bt = torch.randn(n, k, device="cuda").bfloat16()
+        c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        ref = a.float() @ bt.float().t()
+        flops = 2.0 * m * n * k
+        ms_cublas = time_fn(lambda: torch.matmul(a, bt.t(), out=c), 50)
+        print(json.dumps({"shape": name, "m": m, "n": n, "k": k, "plan": "cublas",
+                          "ms": round(ms_cublas, 4),
+                          "tflops": round(flops / ms_cublas / 1e9, 1)}), flush=True)
+        for pname, p, bn, sk in plans:
+            assert lib.apl_gemm_force_plan(p, bn, sk) == 0
+            ms = time_fn(lambda: gemm(a, bt, out=c), 50)
+            out = gemm(a, bt, out_dtype=torch.float32)
+            err = ((out - ref).abs().max() / ref.abs().max()).item()
+            print(json.dumps({"shape": name, "m": m, "n": n, "k": k, "plan": pname,
+                              "ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1),
+                              "frac_of_peak": round(flops / ms / 1e9 / pk, 3),
+                              "vs_cublas": round(ms_cublas / ms, 3), "max_rel_err": err}),
+                  flush=True)
+        lib.apl_gemm_force_plan(-1, -1, -1)
+
+
 def main():
+    if "--sweep" in sys.argv:
+        return sweep()
     quick = "--quick" in sys.argv
     shapes = SHAPES[:1] if quick else SHAPES
     out = {"peak_tflops": peak(), "rows": []}
