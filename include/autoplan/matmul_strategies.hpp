@@ -18,6 +18,10 @@
 
 namespace autoplan {
 
+// The reference's own definition when its intraop.hpp is already included
+// (a caller mixing the reference planner with this drop-in); the layouts
+// are identical (intraop.hpp:34-49).
+#ifndef AUTOPLAN_INTRAOP_HPP_
 struct OpStrategy {
   std::string node;
   std::string name;
@@ -32,6 +36,7 @@ struct OpStrategy {
   int64_t comm_buffer_bytes = 0;
   int64_t memory_bytes = 0;
 };
+#endif
 
 // Every valid strategy of C[..m.., n] = A[..m.., k] . B[k, n] (batched ==
 // false) or C[b,m,n] = A[b,m,k] . B[b,k,n] (batched == true) on `mesh`, in

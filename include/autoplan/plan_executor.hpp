@@ -37,6 +37,7 @@
 #include <nlohmann/json.hpp>
 #include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "autoplan/execute.hpp"
@@ -51,11 +52,53 @@ class PlanExecutor {
   PlanExecutor(MeshRuntime& rt, const DeviceMesh& mesh, const std::string& graph_json,
                const std::string& plan_json, bool fuse_chain = true)
       : rt_(rt), mesh_(mesh), fuse_(fuse_chain) {
+    init(nlohmann::json::parse(graph_json), nlohmann::json::parse(plan_json));
+  }
+
+  // From the reference planner's in-memory result: its ComputationGraph
+  // (graph_ir.hpp:110-124, GraphNode :92-104) and ExecutionPlan
+  // (planner.hpp:99-122), whose node_plans (NodePlan, intraop.hpp:120-127)
+  // give every node's output spec and strategy and whose mesh is the
+  // DeviceMesh. Templated on both types, so this header needs none of the
+  // planner's headers (any types with these members work); the node kinds
+  // are named through the reference's own to_string(NodeKind)
+  // (graph_ir.cpp:408-413), found by argument-dependent lookup.
+  template <class Graph, class Plan,
+            class = decltype(std::declval<const Plan&>().node_plans,
+                             std::declval<const Graph&>().nodes)>
+  PlanExecutor(MeshRuntime& rt, const Graph& graph, const Plan& plan, bool fuse_chain = true)
+      : rt_(rt), mesh_(plan.mesh), fuse_(fuse_chain) {
+    nlohmann::json g, p;
+    g["output"] = graph.output;
+    g["nodes"] = nlohmann::json::array();
+    for (const auto& n : graph.nodes) {
+      nlohmann::json j;
+      j["id"] = n.id;
+      j["kind"] = std::string(to_string(n.kind));
+      j["inputs"] = nlohmann::json::array();
+      for (const auto& in : n.inputs) j["inputs"].push_back({in.node, in.out_index});
+      j["outputs"] = nlohmann::json::array();
+      for (const auto& o : n.outputs)
+        j["outputs"].push_back({{"shape", o.shape}, {"dtype_bytes", o.dtype_bytes}});
+      j["attrs"] = {{"target_shape", n.attrs.target_shape},
+                    {"perm", n.attrs.perm},
+                    {"axis", n.attrs.axis}};
+      g["nodes"].push_back(std::move(j));
+    }
+    p["nodes"] = nlohmann::json::object();
+    for (const auto& np : plan.node_plans)
+      p["nodes"][np.node] = {{"spec", np.spec.to_string()},
+                             {"strategy", np.strategy},
+                             {"partial_sum", np.partial_sum},
+                             {"reduce_axes", np.reduce_axes}};
+    init(g, p);
+  }
+
+ private:
+  void init(const nlohmann::json& g, const nlohmann::json& p) {
     int n = 0, first = 0, nl = 0, dist = 0;
     apl_detail::check(apl_mesh_info(rt_.get(), &n, &first, &nl, &dist));
     num_local_ = nl;
-    const nlohmann::json g = nlohmann::json::parse(graph_json);
-    const nlohmann::json p = nlohmann::json::parse(plan_json);
     output_ = g.at("output").get<std::string>();
     for (const auto& node : g.at("nodes")) {
       Node nd;
@@ -125,6 +168,8 @@ class PlanExecutor {
       if (nd.kind == "elementwise-unary") bind_unary(nd);
     find_attention_chains();
   }
+
+ public:
 
   PlanExecutor(const PlanExecutor&) = delete;
   PlanExecutor& operator=(const PlanExecutor&) = delete;
@@ -697,9 +742,20 @@ class PlanExecutor {
     return out;
   }
 
+  // row-major device -> coordinate (cluster.hpp:56); a free computation, so
+  // this header also compiles against the reference's own DeviceMesh
+  std::vector<int64_t> mesh_coord(int64_t device) const {
+    std::vector<int64_t> c(mesh_.shape.size());
+    for (size_t k = c.size(); k-- > 0;) {
+      c[k] = device % mesh_.shape[k];
+      device /= mesh_.shape[k];
+    }
+    return c;
+  }
+
   // (index, count) of `device`'s block along a dim sharded over dim.axes
   std::pair<int64_t, int64_t> block_index(const DimSpec& dim, int64_t device) const {
-    const auto c = mesh_.coord_of(device);
+    const auto c = mesh_coord(device);
     int64_t idx = 0, cnt = 1;
     for (int a : dim.axes) {
       idx = idx * mesh_.shape[static_cast<size_t>(a)] + c[static_cast<size_t>(a)];
@@ -721,7 +777,9 @@ class PlanExecutor {
         v /= mesh_.shape[static_cast<size_t>(*a)];
       }
     }
-    return mesh_.device_of(coord);
+    int64_t d = 0;  // row-major coordinate -> device (cluster.hpp:56)
+    for (size_t k = 0; k < coord.size(); ++k) d = d * mesh_.shape[k] + coord[k];
+    return d;
   }
 
   // input layouts of a non-matmul node's named strategy (intraop.cpp:280-450)

@@ -20,6 +20,8 @@ def build(ref: bool = True) -> None:
     reference library (building the checker is not using it)."""
     import subprocess
 
-    targets = ["all"] if ref and Path("/root/reference/proj/src").exists() else [
+    # "in_memory": the reference planner TUs linked against the built
+    # libapl.so (tests/cpp/plan_in_memory_test.cpp), so build() runs it last
+    targets = ["all", "in_memory"] if ref and Path("/root/reference/proj/src").exists() else [
         str(HERE / "_build" / "libapl_oracle.so")]
     subprocess.run(["make", "-s", "-C", str(HERE), *targets], check=True)

@@ -1224,11 +1224,14 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
                               int ldb, int ldc, bool b_kn, bool out_f32, int epi, bool a_km,
                               const void* const* aux, int ldaux, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || groups <= 0) return cudaSuccess;
-  if (encode_fn() == nullptr) return cudaErrorSymbolNotFound;  // no cuTensorMapEncodeTiled
-  if (reduce < 1 || fan < 1 || reduce > kMaxBatch || fan > kMaxBatch) return cudaErrorInvalidValue;
-  if ((lda * 2) % 16 || (ldb * 2) % 16) return cudaErrorInvalidValue;  // TMA row alignment
+  if (encode_fn() == nullptr)
+    return why(cudaErrorSymbolNotFound, "no cuTensorMapEncodeTiled entry point");
+  if (reduce < 1 || fan < 1 || reduce > kMaxBatch || fan > kMaxBatch)
+    return why(cudaErrorInvalidValue, "reduce / fan outside [1, 8]");
+  if ((lda * 2) % 16 || (ldb * 2) % 16)
+    return why(cudaErrorInvalidValue, "lda / ldb rows not 16-byte multiples (TMA)");
   if (epi < kEpiNone || epi > kEpiGeluSave || (epi >= kEpiDGelu && aux == nullptr))
-    return cudaErrorInvalidValue;
+    return why(cudaErrorInvalidValue, "bad epilogue / missing aux");
   const int per_launch = std::max(1, std::min(kMaxBatch / reduce, kMaxBatch / fan));
   const GemmPlan plan = plan_gemm(M, N, K, std::min(groups, per_launch),
                                   /*sk_allowed=*/reduce == 1 && fan == 1,
@@ -1253,12 +1256,12 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
       const void* a = A[first * reduce + i];
       const void* b = B[first * reduce + i];
       if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
-        return cudaErrorInvalidValue;
+        return why(cudaErrorInvalidValue, "operand base not 16-byte aligned (TMA)");
       const bool oka = a_km ? make_map(&args.a[i], a, K, M, lda, kBK, 64)
                             : make_map(&args.a[i], a, M, K, lda, kBM);
       const bool okb = b_kn ? make_map(&args.b[i], b, K, N, ldb, kBK, 64)
                             : make_map(&args.b[i], b, N, K, ldb, b_rows);
-      if (!oka || !okb) return cudaErrorInvalidValue;
+      if (!oka || !okb) return why(cudaErrorInvalidValue, "tensor map encode");
     }
     for (int i = 0; i < args.count * fan; ++i) args.c[i] = C[first * fan + i];
     if (epi >= kEpiDGelu)

@@ -55,6 +55,9 @@ def gelu(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
                            _DTYPE_CODE[x.dtype], _stream_handle(stream)))
 
 
+_gelu = gelu
+
+
 def gelu_backward(dy: torch.Tensor, x: torch.Tensor, dx: torch.Tensor, stream=None) -> None:
     """dx = dy * GELU'(x) on the device."""
     check(A.lib().apl_gelu_backward(C.c_void_p(dy.data_ptr()), C.c_void_p(x.data_ptr()),
@@ -660,7 +663,7 @@ class PeerMesh:
         c = self.matmul_allreduce(a, b, b_layout=b_layout, stream=stream,
                                   axes=tuple(strategy.reduce_axes))
         if gelu:
-            gelu(c, c, stream=stream)
+            _gelu(c, c, stream=stream)  # (the `gelu` argument shadows the module function)
         return c
 
     def exchange_traffic(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta) -> dict:

@@ -405,7 +405,7 @@ def test_block_plans_backward(cuda, name):
 
 # ---- every batched-matmul strategy, backward included --------------------------
 def _bmm_case(mesh_shape, st, param_spec):
-    """graph: parameters A[4,32,64], B[4,64,48] -> batched-matmul -> output,
+    """graph: parameters A[4,32,64], B[4,64,64] -> batched-matmul -> output,
     planned with strategy `st` (the catalog's, intraop.cpp:208-231); the
     parameters are stored in `param_spec` (None: the strategy's own input
     layouts, so no conversion runs)."""
@@ -415,7 +415,7 @@ def _bmm_case(mesh_shape, st, param_spec):
 
     graph = {"version": 1, "placeholders": [], "output": "out",
              "nodes": [node("A", "parameter", [], [4, 32, 64]),
-                       node("B", "parameter", [], [4, 64, 48]),
+                       node("B", "parameter", [], [4, 64, 64]),
                        node("mm", "batched-matmul", ["A", "B"]),
                        node("out", "output", ["mm"])]}
     sa = param_spec or str(st.a)
@@ -433,7 +433,7 @@ def _bmm_strategies():
     from paper_2302_02599_b200 import DeviceMesh, TensorMeta
     from paper_2302_02599_b200.strategies import matmul_strategies
 
-    a, b = TensorMeta((4, 32, 64), 2), TensorMeta((4, 64, 48), 2)
+    a, b = TensorMeta((4, 32, 64), 2), TensorMeta((4, 64, 64), 2)
     return [s for s in matmul_strategies(DeviceMesh.uniform([2, 2]), a, b, batched=True)]
 
 
@@ -449,13 +449,13 @@ def test_batched_matmul_strategy_backward(cuda, name, param_spec):
     graph, plan = _bmm_case([2, 2], st, param_spec)
     torch.manual_seed(11)
     A = torch.randn(4, 32, 64, device="cuda").bfloat16()
-    Bm = (torch.randn(4, 64, 48, device="cuda") / 8).bfloat16()
+    Bm = (torch.randn(4, 64, 64, device="cuda") / 8).bfloat16()
     ex = PlanExecutor(Mesh.local([2, 2]), graph, plan)
     out = ex.forward({"A": A, "B": Bm}, train=True)[0]
     af, bf = A.float().requires_grad_(), Bm.float().requires_grad_()
     ref = af @ bf
     assert _rel(out, ref) <= 2e-2
-    gy = torch.randn(4, 32, 48, device="cuda").bfloat16()
+    gy = torch.randn(4, 32, 64, device="cuda").bfloat16()
     ref.backward(gy.float())
     grads = ex.backward(gy)
     torch.cuda.synchronize()
