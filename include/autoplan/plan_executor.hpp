@@ -132,8 +132,8 @@ class PlanExecutor {
         nd.meta.shape = node.at("attrs").at("target_shape").get<std::vector<int64_t>>();
       } else if (nd.kind == "transpose") {
         const TensorMeta& in = nodes_.at(nd.inputs.at(0)).meta;
-        nd.perm = node.at("attrs").at("perm").get<std::vector<int64_t>>();
         nd.meta = in;
+        nd.perm = node.at("attrs").at("perm").get<std::vector<int64_t>>();
         for (size_t i = 0; i < nd.perm.size(); ++i)
           nd.meta.shape[i] = in.shape.at(static_cast<size_t>(nd.perm[i]));
       } else if (nd.kind == "embedding-lookup") {
@@ -145,6 +145,10 @@ class PlanExecutor {
       } else {
         throw SchemaError("node kind '" + nd.kind + "' is not executable");
       }
+      // attributes are read whether or not the outputs were declared (an
+      // in-memory graph after infer_meta carries every node's outputs)
+      if (nd.kind == "transpose")
+        nd.perm = node.at("attrs").at("perm").get<std::vector<int64_t>>();
       if (node.contains("attrs") && node.at("attrs").contains("axis"))
         nd.axis = node.at("attrs").at("axis").get<int64_t>();
       const auto& pn = p.at("nodes").at(nd.id);

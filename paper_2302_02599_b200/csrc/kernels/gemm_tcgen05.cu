@@ -1151,12 +1151,14 @@ struct GemmPlan {
   bool streamk;  // stream-K over (tile, k-block) instead of whole tiles
 };
 
-// Relative per-SM throughput of each tile shape (measured r02: the 1-CTA
-// 128 x 128 tile is shared-memory bound -- MMA operand reads plus TMA fills
-// -- at about half the pair's rate).
+// Relative per-SM throughput of each tile shape, calibrated on 8192^3 where
+// wave quantisation is negligible (profiles/r02_gemm_sweep.jsonl: pair256
+// 1393, cta256 1171, pair128 954, cta128 923 TFLOP/s). Operand fill per MMA
+// cycle sets the order: the 256 x 256 pair tile needs 64 B/clk per SM, the
+// others 96-128 B/clk.
 double tile_eff(bool paired, int bn) {
-  if (paired) return bn == 256 ? 1.0 : 0.92;
-  return bn == 256 ? 0.75 : 0.5;
+  if (paired) return bn == 256 ? 1.0 : 0.685;
+  return bn == 256 ? 0.84 : 0.66;
 }
 
 // Cost model: per-SM work of a tile / its efficiency, times the waves of

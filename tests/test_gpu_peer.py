@@ -282,7 +282,8 @@ def _subset_allreduce_worker(rank, world, port, q):
         shape = [2, world // 2]
         pm = PeerMesh(shape, rank, 0, 16)
         coord = (rank // shape[1], rank % shape[1])
-        M, Kt, N = 512, 1024, 256
+        # M / group size must be whole 128-row tiles for the fused scatter
+        M, Kt, N = 128 * world, 1024, 256
         for axes in ((0,), (1,), (0, 1)):
             members = pm.axis_group(axes)
             me, P = members.index(rank), len(members)
