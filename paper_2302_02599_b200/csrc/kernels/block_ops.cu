@@ -25,6 +25,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 
@@ -380,6 +381,19 @@ __device__ __forceinline__ uint32_t ldg_stream4(const void* p) {
 // No "memory" clobber: volatile asm keeps these stores in program order with
 // the volatile prefetch loads, while ordinary loads (gamma / beta, L1 hits)
 // may still be scheduled across them instead of serialising behind each store.
+__device__ __forceinline__ void stg16(void* p, const uint4& v);
+__device__ __forceinline__ void stg16_cs(void* p, const uint4& v) {  // streaming (evict-first)
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w));
+}
+// Output sinks of the row functions: 0 st.global, 1 st.global.cs
+// (evict-first), 2 the streamed kernel's shared-memory slab (stored to HBM
+// by a TMA bulk store).
+__device__ __forceinline__ void stg16(void* p, const uint4& v, int sink) {
+  if (sink == 2) *reinterpret_cast<uint4*>(p) = v;
+  else if (sink == 1) stg16_cs(p, v);
+  else stg16(p, v);
+}
 __device__ __forceinline__ void stg16(void* p, const uint4& v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w));
@@ -439,6 +453,219 @@ struct Raw<float> {
   }
 };
 
+// ---- per-row math, shared by the prefetching register kernels and the
+// TMA-streamed ones (identical arithmetic, so either engine's output is the
+// same bytes). A warp owns one row held as NV raw 16-byte vectors per lane.
+
+// softmax(alpha * x + fill * mask) of one row of width <= 32 * NV * V.
+template <typename T, int NV, bool kMask>
+__device__ __forceinline__ void softmax_row(const uint4 (&cur)[NV],
+                                            const typename Raw<T>::Mask (&mc)[NV], int lane,
+                                            int nv, float alpha, float fill, T* __restrict__ yrow,
+                                            int cs = 0) {
+  using R = Raw<T>;
+  constexpr int V = R::V;
+  float f[NV][V];
+  float m = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+    if (lane + 32 * j < nv) {
+      R::unpack(cur[j], f[j]);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if constexpr (kMask) f[j][k] = fmaf(alpha, f[j][k], fill * R::mask_at(mc[j], k));
+        else f[j][k] *= alpha;
+        m = fmaxf(m, f[j][k]);
+      }
+    }
+  m = warp_max(m);
+  const float ml = m * 1.4426950408889634f;
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+    if (lane + 32 * j < nv)
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        f[j][k] = ex2_ftz(fmaf(f[j][k], 1.4426950408889634f, -ml));
+        s += f[j][k];
+      }
+  const float inv = 1.f / warp_sum(s);
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i = lane + 32 * j;
+    if (i < nv) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) f[j][k] *= inv;
+      stg16(yrow + static_cast<int64_t>(i) * V, R::pack(f[j]), cs);
+    }
+  }
+}
+
+// Shared-memory slot of parameter element c in the lane-interleaved fp32
+// layout load_param<.., true> reads (V elements per 16-byte vector i; vector
+// i belongs to lane i % 32).
+template <int V>
+__device__ __forceinline__ int64_t gb_index(int64_t c) {
+  const int64_t i = c / V, k = c % V;
+  return (((i >> 5) * (V / 4) + k / 4) * 32 + (i & 31)) * 4 + (k & 3);
+}
+
+// gamma / beta of vector i: the bf16 / fp32 parameter in global memory
+// (kGB32 = false) or its fp32 copy staged in shared memory (kGB32 = true);
+// the same fp32 values either way.
+template <typename T, int V, bool kGB32>
+__device__ __forceinline__ void load_param(const void* p, int i, float (&f)[V]) {
+  if constexpr (kGB32) {
+    // staged lane-interleaved (gb_index): a warp's float4 loads are contiguous,
+    // so each LDS.128 is conflict-free
+    const float* q = static_cast<const float*>(p);
+#pragma unroll
+    for (int u = 0; u < V / 4; ++u) {
+      const float4 v =
+          *reinterpret_cast<const float4*>(q + ((((i >> 5) * (V / 4) + u) << 5) + (i & 31)) * 4);
+      f[4 * u] = v.x;
+      f[4 * u + 1] = v.y;
+      f[4 * u + 2] = v.z;
+      f[4 * u + 3] = v.w;
+    }
+  } else {
+    load_row<T, V>(static_cast<const T*>(p), i, f);
+  }
+}
+
+// layernorm of one row; two-pass mean / variance from the registers (the
+// same arithmetic as ln_bwd_row, so backward's recomputed statistics equal
+// forward's bit for bit). The row is unpacked to fp32 once and normalised
+// in FMA form, y = x * (rstd g) + (b - mean rstd g): three FP32 ops per
+// element where (x - mean) * rstd * g + b took four plus two re-unpacks --
+// the streamed kernel is issue-bound (ncu r02: issue slots 75% busy).
+template <typename T, int NV, bool kGB32, bool kKeepF32>
+__device__ __forceinline__ void ln_row(const uint4 (&cur)[NV], int lane, int nv, float inv_w,
+                                       float eps, const void* __restrict__ gamma,
+                                       const void* __restrict__ beta, T* __restrict__ yrow,
+                                       int cs = 0) {
+  using R = Raw<T>;
+  constexpr int V = R::V;
+  // kKeepF32: the row unpacked once and kept in fp32 registers (streamed
+  // kernel, registers to spare); else re-unpacked per pass (prefetch kernel,
+  // whose occupancy is its registers). Unpacking is exact: same bytes.
+  float keep[kKeepF32 ? NV : 1][V];
+  auto row = [&](int j, float (&f)[V]) {
+    if constexpr (kKeepF32) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) f[k] = keep[j][k];
+    } else {
+      R::unpack(cur[j], f);
+    }
+  };
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+    if (lane + 32 * j < nv) {
+      float f[V];
+      R::unpack(cur[j], f);
+      if constexpr (kKeepF32) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) keep[j][k] = f[k];
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) s += f[k];
+    }
+  const float mean = warp_sum(s) * inv_w;
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+    if (lane + 32 * j < nv) {
+      float f[V];
+      row(j, f);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float c = f[k] - mean;
+        q += c * c;
+      }
+    }
+  const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
+  const float nm = -mean;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i = lane + 32 * j;
+    if (i < nv) {
+      float f[V], g[V], b[V];
+      row(j, f);
+      if (gamma != nullptr) load_param<T, V, kGB32>(gamma, i, g);
+      if (beta != nullptr) load_param<T, V, kGB32>(beta, i, b);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float a = gamma != nullptr ? rstd * g[k] : rstd;
+        const float c = fmaf(nm, a, beta != nullptr ? b[k] : 0.f);
+        f[k] = fmaf(f[k], a, c);
+      }
+      stg16(yrow + static_cast<int64_t>(i) * V, R::pack(f), cs);
+    }
+  }
+}
+
+// layernorm backward of one row: dx and (lane 0) the row's (mean, rstd),
+// computed exactly as ln_row does.
+template <typename T, int NV, bool kGB32>
+__device__ __forceinline__ void ln_bwd_row(const uint4 (&cx)[NV], const uint4 (&cd)[NV], int lane,
+                                           int nv, float inv_w, float eps,
+                                           const void* __restrict__ gamma, T* __restrict__ dxrow,
+                                           float2* __restrict__ stat, int cs = 0) {
+  using R = Raw<T>;
+  constexpr int V = R::V;
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+    if (lane + 32 * j < nv) {
+      float f[V];
+      R::unpack(cx[j], f);
+#pragma unroll
+      for (int k = 0; k < V; ++k) s += f[k];
+    }
+  const float mean = warp_sum(s) * inv_w;
+  float q = 0.f, sa = 0.f, sax = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+    if (lane + 32 * j < nv) {
+      float f[V], d[V], g[V];
+      R::unpack(cx[j], f);
+      R::unpack(cd[j], d);
+      if (gamma != nullptr) load_param<T, V, kGB32>(gamma, lane + 32 * j, g);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float c = f[k] - mean;
+        const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
+        q += c * c;
+        sa += gd;
+        sax += gd * c;
+      }
+    }
+  const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
+  const float a = warp_sum(sa) * inv_w;
+  const float b = rstd * warp_sum(sax) * inv_w;  // mean(g.dy.xhat)
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i = lane + 32 * j;
+    if (i < nv) {
+      float f[V], d[V], g[V];
+      R::unpack(cx[j], f);
+      R::unpack(cd[j], d);
+      if (gamma != nullptr) load_param<T, V, kGB32>(gamma, i, g);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
+        f[k] = rstd * (gd - a - (f[k] - mean) * rstd * b);
+      }
+      stg16(dxrow + static_cast<int64_t>(i) * V, R::pack(f), cs);
+    }
+  }
+  if (lane == 0 && stat != nullptr) *stat = make_float2(mean, rstd);
+}
+
+// ---- prefetching register kernels: the NEXT row's loads issued before the
+// current row's reductions.
+
 // softmax(alpha * x + fill * mask) over rows of width <= 32 * NV * V.
 template <typename T, int NV, bool kMask>
 __global__ void __launch_bounds__(256) softmax_pipe_kernel(const T* __restrict__ x,
@@ -467,40 +694,7 @@ __global__ void __launch_bounds__(256) softmax_pipe_kernel(const T* __restrict__
   if (r < rows) load(r, cur, mc);
   for (; r < rows; r += stride) {
     if (r + stride < rows) load(r + stride, nxt, mn);
-    float f[NV][V];
-    float m = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (lane + 32 * j < nv) {
-        R::unpack(cur[j], f[j]);
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          if constexpr (kMask) f[j][k] = fmaf(alpha, f[j][k], fill * R::mask_at(mc[j], k));
-          else f[j][k] *= alpha;
-          m = fmaxf(m, f[j][k]);
-        }
-      }
-    m = warp_max(m);
-    const float ml = m * 1.4426950408889634f;
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (lane + 32 * j < nv)
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          f[j][k] = ex2_ftz(fmaf(f[j][k], 1.4426950408889634f, -ml));
-          s += f[j][k];
-        }
-    const float inv = 1.f / warp_sum(s);
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int i = lane + 32 * j;
-      if (i < nv) {
-#pragma unroll
-        for (int k = 0; k < V; ++k) f[j][k] *= inv;
-        stg16(y + r * width + static_cast<int64_t>(i) * V, R::pack(f[j]));
-      }
-    }
+    softmax_row<T, NV, kMask>(cur, mc, lane, nv, alpha, fill, y + r * width);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       cur[j] = nxt[j];
@@ -509,9 +703,7 @@ __global__ void __launch_bounds__(256) softmax_pipe_kernel(const T* __restrict__
   }
 }
 
-// layernorm forward, rows of width <= 32 * NV * V; two-pass mean / variance
-// from the registers (the same arithmetic as layernorm_backward's pipe kernel,
-// so backward's recomputed statistics equal forward's bit for bit).
+// layernorm forward, rows of width <= 32 * NV * V.
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) layernorm_pipe_kernel(
     const T* __restrict__ x, const T* __restrict__ gamma, const T* __restrict__ beta,
@@ -524,8 +716,6 @@ __global__ void __launch_bounds__(256) layernorm_pipe_kernel(
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / 32;
   int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
   uint4 cur[NV], nxt[NV];
-  typename R::Mask unused[NV];
-  (void)unused;
   auto load = [&](int64_t row, uint4 (&d)[NV]) {
 #pragma unroll
     for (int j = 0; j < NV; ++j)
@@ -534,53 +724,14 @@ __global__ void __launch_bounds__(256) layernorm_pipe_kernel(
   if (r < rows) load(r, cur);
   for (; r < rows; r += stride) {
     if (r + stride < rows) load(r + stride, nxt);
-    // the row stays packed; each pass unpacks it again (one ALU op per bf16)
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (lane + 32 * j < nv) {
-        float f[V];
-        R::unpack(cur[j], f);
-#pragma unroll
-        for (int k = 0; k < V; ++k) s += f[k];
-      }
-    const float mean = warp_sum(s) * inv_w;
-    float q = 0.f;
-#pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (lane + 32 * j < nv) {
-        float f[V];
-        R::unpack(cur[j], f);
-#pragma unroll
-        for (int k = 0; k < V; ++k) q += (f[k] - mean) * (f[k] - mean);
-      }
-    const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int i = lane + 32 * j;
-      if (i < nv) {
-        float f[V], g[V], b[V];
-        R::unpack(cur[j], f);
-        if (gamma != nullptr) load_row<T, V>(gamma, i, g);
-        if (beta != nullptr) load_row<T, V>(beta, i, b);
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          float v = (f[k] - mean) * rstd;
-          if (gamma != nullptr) v *= g[k];
-          if (beta != nullptr) v += b[k];
-          f[k] = v;
-        }
-        stg16(y + r * width + static_cast<int64_t>(i) * V, R::pack(f));
-      }
-    }
+    ln_row<T, NV, false, false>(cur, lane, nv, inv_w, eps, gamma, beta, y + r * width);
 #pragma unroll
     for (int j = 0; j < NV; ++j) cur[j] = nxt[j];
   }
 }
 
 // layernorm backward (dx and the per-row statistics for the parameter pass),
-// x and dy of the next row prefetched; mean / rstd computed exactly as the
-// forward pipe kernel does (two passes over the registers).
+// x and dy of the next row prefetched.
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) layernorm_bwd_pipe_kernel(
     const T* __restrict__ x, const T* __restrict__ gamma, const T* __restrict__ dy,
@@ -605,53 +756,8 @@ __global__ void __launch_bounds__(256) layernorm_bwd_pipe_kernel(
   if (r < rows) load(r, cx, cd);
   for (; r < rows; r += stride) {
     if (r + stride < rows) load(r + stride, nx, nd);
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (lane + 32 * j < nv) {
-        float f[V];
-        R::unpack(cx[j], f);
-#pragma unroll
-        for (int k = 0; k < V; ++k) s += f[k];
-      }
-    const float mean = warp_sum(s) * inv_w;
-    float q = 0.f, sa = 0.f, sax = 0.f;
-#pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (lane + 32 * j < nv) {
-        float f[V], d[V], g[V];
-        R::unpack(cx[j], f);
-        R::unpack(cd[j], d);
-        if (gamma != nullptr) load_row<T, V>(gamma, lane + 32 * j, g);
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const float c = f[k] - mean;
-          const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
-          q += c * c;
-          sa += gd;
-          sax += gd * c;
-        }
-      }
-    const float rstd = rsqrtf(warp_sum(q) * inv_w + eps);
-    const float a = warp_sum(sa) * inv_w;
-    const float b = rstd * warp_sum(sax) * inv_w;  // mean(g.dy.xhat)
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int i = lane + 32 * j;
-      if (i < nv) {
-        float f[V], d[V], g[V];
-        R::unpack(cx[j], f);
-        R::unpack(cd[j], d);
-        if (gamma != nullptr) load_row<T, V>(gamma, i, g);
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const float gd = gamma != nullptr ? g[k] * d[k] : d[k];
-          f[k] = rstd * (gd - a - (f[k] - mean) * rstd * b);
-        }
-        stg16(dx + r * width + static_cast<int64_t>(i) * V, R::pack(f));
-      }
-    }
-    if (lane == 0 && stats != nullptr) stats[r] = make_float2(mean, rstd);
+    ln_bwd_row<T, NV, false>(cx, cd, lane, nv, inv_w, eps, gamma, dx + r * width,
+                      stats != nullptr ? stats + r : nullptr);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       cx[j] = nx[j];
@@ -660,6 +766,243 @@ __global__ void __launch_bounds__(256) layernorm_bwd_pipe_kernel(
   }
 }
 
+// ---- TMA-streamed row kernels -------------------------------------------------
+// The register-prefetch kernels keep one row per warp in flight, so their
+// bytes in flight are capped by registers (occupancy): the layernorm pair
+// measured 0.74 / 0.72 of the HBM roofline with it (r02). Here the loads
+// leave the register file: a producer warp streams slabs of kRsRows
+// contiguous rows (every input of the row op: x, dy, the u8 mask) into a
+// ring of shared-memory stages with cp.async.bulk (one bulk copy per input
+// per slab, completion counted on the stage's mbarrier), and kRsRows
+// consumer warps each take one row of the slab from shared memory, free the
+// stage, and run the same per-row math, storing straight to HBM. Bytes in
+// flight per SM = resident CTAs x stages x slab bytes, independent of the
+// math's register footprint.
+constexpr int kRsRows = 8;            // consumer warps = rows per slab
+constexpr int kRsMaxStages = 8;
+constexpr int kRsBudget = 72 * 1024;  // stage ring per CTA: 3 CTAs per SM
+
+enum RowOp { kRowLn = 0, kRowSoftmax = 1, kRowMaskedSoftmax = 2, kRowLnBwd = 3 };
+
+struct RowStreamArgs {
+  const void* in0;      // x (layernorm, softmax) / x (layernorm backward)
+  const void* in1;      // dy (layernorm backward)
+  const uint8_t* mask;  // u8 mask (masked softmax)
+  const void* gamma;
+  const void* beta;
+  void* out;
+  float2* stats;
+  int64_t rows, width;
+  float eps, alpha, fill;
+  int stages;
+  uint32_t row0, row1, rowm;      // bytes per row of each input (0: absent)
+  uint32_t off1, offm, stage;     // offsets inside a stage, stage bytes
+  uint32_t params;                // bytes of fp32 gamma + beta staged before the ring
+  int policy;                     // bit 0: evict-first bulk loads; bit 1: streaming stores
+};
+
+__device__ __forceinline__ void rs_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void rs_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                        bool evict_first) {
+  if (evict_first) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+        "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "l"(pol)
+        : "memory");
+    return;
+  }
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+// kTS = false: consumers store their rows with st.global and free the stage
+// right after reading it. kTS = true: consumers write the result over their
+// input row in shared memory and a storer warp writes the slab back with one
+// cp.async.bulk store (TMA both ways, like the bulk copy engine); the stage
+// is freed once that store has read it.
+// Position in the stage ring (slot, mbarrier phase), advanced per slab
+// without integer division.
+struct RsRing {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++s == n) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+template <typename T, int NV, int kOp, int kMinBlocks, bool kTS>
+__global__ void __launch_bounds__(32 * (kRsRows + 1 + kTS), kMinBlocks)
+    row_stream_kernel(const __grid_constant__ RowStreamArgs a) {
+  using R = Raw<T>;
+  constexpr int V = R::V;
+  extern __shared__ __align__(128) uint8_t rs_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(rs_smem);
+  uint64_t* empty = full + kRsMaxStages;
+  uint64_t* done = empty + kRsMaxStages;  // kTS: consumers -> storer
+  // [barriers 256 B][fp32 gamma][fp32 beta][stage ring]
+  float* g32 = reinterpret_cast<float*>(rs_smem + 256);
+  float* b32 = g32 + (a.width / V + 31) / 32 * 32 * V;  // gb_index spans whole lane groups
+  uint8_t* data = rs_smem + 256 + a.params;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t slabs = (a.rows + kRsRows - 1) / kRsRows;
+  if constexpr (kOp == kRowLn || kOp == kRowLnBwd) {
+    for (int64_t c = threadIdx.x; c < a.width; c += blockDim.x) {
+      if (a.gamma != nullptr) g32[gb_index<V>(c)] = ld(static_cast<const T*>(a.gamma) + c);
+      if (a.beta != nullptr) b32[gb_index<V>(c)] = ld(static_cast<const T*>(a.beta) + c);
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&full[s])))
+                   : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&empty[s]))),
+                   "r"(kTS ? 1 : kRsRows)
+                   : "memory");
+      if constexpr (kTS)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&done[s]))),
+                     "r"(kRsRows)
+                     : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kRsRows) {  // producer
+    if (lane == 0) {
+      RsRing ring;
+      for (int64_t slab = blockIdx.x; slab < slabs; slab += gridDim.x, ring.next(a.stages)) {
+        const int s = ring.s;
+        rs_wait(&empty[s], ring.ph ^ 1);
+        const int64_t r0 = slab * kRsRows;
+        const int64_t left = a.rows - r0;
+        const uint32_t nr = static_cast<uint32_t>(left < kRsRows ? left : kRsRows);
+        uint8_t* st = data + static_cast<size_t>(s) * a.stage;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&full[s]))),
+                     "r"(nr * (a.row0 + a.row1 + a.rowm))
+                     : "memory");
+        const bool ef = a.policy & 1;
+        rs_bulk(st, static_cast<const uint8_t*>(a.in0) + r0 * a.row0, nr * a.row0, &full[s], ef);
+        if (a.row1)
+          rs_bulk(st + a.off1, static_cast<const uint8_t*>(a.in1) + r0 * a.row1, nr * a.row1,
+                  &full[s], ef);
+        if (a.rowm) rs_bulk(st + a.offm, a.mask + r0 * a.rowm, nr * a.rowm, &full[s], ef);
+      }
+    }
+    return;
+  }
+  if constexpr (kTS) {
+    if (warp == kRsRows + 1) {  // storer: slab s back to HBM, then free its stage
+      if (lane == 0) {
+        RsRing ring;
+        int prev = -1;
+        for (int64_t slab = blockIdx.x; slab < slabs; slab += gridDim.x, ring.next(a.stages)) {
+          const int s = ring.s;
+          rs_wait(&done[s], ring.ph);
+          const int64_t r0 = slab * kRsRows;
+          const int64_t left = a.rows - r0;
+          const uint32_t nr = static_cast<uint32_t>(left < kRsRows ? left : kRsRows);
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                           static_cast<uint8_t*>(a.out) + r0 * a.row0),
+                       "r"(static_cast<uint32_t>(
+                           __cvta_generic_to_shared(data + static_cast<size_t>(s) * a.stage))),
+                       "r"(nr * a.row0)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          // at most this slab's store still reading shared memory: the previous
+          // slab's stage is free
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          if (prev >= 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(&empty[prev])))
+                         : "memory");
+          prev = s;
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      }
+      return;
+    }
+  }
+  const int nv = static_cast<int>(a.width / V);
+  const float inv_w = 1.f / static_cast<float>(a.width);
+  RsRing ring;
+  for (int64_t slab = blockIdx.x; slab < slabs; slab += gridDim.x, ring.next(a.stages)) {
+    const int s = ring.s;
+    rs_wait(&full[s], ring.ph);
+    const int64_t r = slab * kRsRows + warp;
+    const bool live = r < a.rows;
+    uint8_t* st = data + static_cast<size_t>(s) * a.stage;
+    uint4 c0[NV], c1[NV];
+    typename R::Mask mc[NV];
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int i = lane + 32 * j;
+        if (i < nv) {
+          c0[j] = *reinterpret_cast<const uint4*>(st + warp * a.row0 + i * 16);
+          if constexpr (kOp == kRowLnBwd)
+            c1[j] = *reinterpret_cast<const uint4*>(st + a.off1 + warp * a.row1 + i * 16);
+          if constexpr (kOp == kRowMaskedSoftmax)
+            mc[j] = *reinterpret_cast<const typename R::Mask*>(st + a.offm + warp * a.rowm +
+                                                              i * sizeof(typename R::Mask));
+        }
+      }
+    }
+    if constexpr (!kTS) {
+      // the row is in registers: release the stage to the producer
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&empty[s])))
+                     : "memory");
+      if (!live) continue;
+    }
+    if (live) {
+      // kTS: the result overwrites this warp's input row in the stage
+      T* out = kTS ? reinterpret_cast<T*>(st + warp * a.row0) : static_cast<T*>(a.out) + r * a.width;
+      const int sink = kTS ? 2 : ((a.policy & 2) ? 1 : 0);
+      if constexpr (kOp == kRowLn) {
+        ln_row<T, NV, true, true>(c0, lane, nv, inv_w, a.eps, a.gamma != nullptr ? g32 : nullptr,
+                                  a.beta != nullptr ? b32 : nullptr, out, sink);
+      } else if constexpr (kOp == kRowLnBwd) {
+        ln_bwd_row<T, NV, true>(c0, c1, lane, nv, inv_w, a.eps,
+                                a.gamma != nullptr ? g32 : nullptr, out,
+                                a.stats != nullptr ? a.stats + r : nullptr, sink);
+      } else {
+        softmax_row<T, NV, kOp == kRowMaskedSoftmax>(c0, mc, lane, nv, a.alpha, a.fill, out,
+                                                     sink);
+      }
+    }
+    if constexpr (kTS) {
+      // generic-proxy writes -> visible to the bulk store (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&done[s])))
+                     : "memory");
+    }
+  }
+}
 // softmax backward, y and dy of the next row prefetched.
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) softmax_bwd_pipe_kernel(const T* __restrict__ y,
@@ -1043,6 +1386,127 @@ bool pipe_rows_enabled() {
   return on;
 }
 
+// Row engine per op (r02 measurements, 128 Ki rows x 1024 bf16, fraction of
+// the HBM copy peak, profiles/r02_block_ops_*.jsonl): layernorm 0.80 streamed
+// vs 0.73 register-prefetch, its backward 0.84 vs 0.71, masked softmax 0.87
+// vs 0.82 -- the streamed kernel wins where the row math's registers cap
+// the prefetch kernel's bytes in flight; plain softmax 0.80 vs 0.92 -- there
+// the prefetch kernel's occupancy suffices and it pays no barrier traffic.
+// APL_ROW_ENGINE=stream / pipe forces one engine for every op (A/B, tests).
+int row_engine_forced() {  // -1 policy, 0 pipe, 1 stream
+  static const int v = [] {
+    const char* e = std::getenv("APL_ROW_ENGINE");
+    if (e == nullptr) return -1;
+    if (std::strcmp(e, "pipe") == 0) return 0;
+    if (std::strcmp(e, "stream") == 0) return 1;
+    return -1;
+  }();
+  return v;
+}
+bool row_stream_enabled(bool plain_softmax = false) {
+  const int f = row_engine_forced();
+  return f < 0 ? !plain_softmax : f == 1;
+}
+
+constexpr uint32_t align128(uint32_t v) { return (v + 127u) & ~127u; }
+
+// One TMA-streamed row launch; cudaErrorNotSupported when the slab does not
+// fit two stages (the caller falls back to the register kernels).
+template <typename T, int NV, int kOp, bool kTS>
+cudaError_t launch_row_stream(RowStreamArgs a, cudaStream_t s) {
+  // layernorm keeps its row in fp32 registers: 2 CTAs per SM (<= 113 regs)
+  constexpr int kMin = (kTS || kOp == kRowLn || (kOp == kRowLnBwd && NV >= 4)) ? 2 : 3;
+  constexpr int kThreads = 32 * (kRsRows + 1 + kTS);
+  auto kern = row_stream_kernel<T, NV, kOp, kMin, kTS>;
+  a.off1 = align128(kRsRows * a.row0);
+  a.offm = align128(a.off1 + kRsRows * a.row1);
+  a.stage = align128(a.offm + kRsRows * a.rowm);
+  static const int budget = [] {  // APL_RS_BUDGET_KB: stage-ring bytes per CTA (probe)
+    const char* e = std::getenv("APL_RS_BUDGET_KB");
+    return e ? std::max(16, std::min(200, std::atoi(e))) * 1024 : kRsBudget;
+  }();
+  a.stages = std::min<int>(kRsMaxStages, budget / static_cast<int>(a.stage));
+  if (a.stages < 2) return cudaErrorNotSupported;
+  static const int policy = [] {  // APL_RS_POLICY: cache-policy probe bits (see RowStreamArgs)
+    const char* e = std::getenv("APL_RS_POLICY");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.policy = policy;
+  constexpr int kV = 16 / static_cast<int>(sizeof(T));
+  a.params = (kOp == kRowLn || kOp == kRowLnBwd)
+                 ? align128(static_cast<uint32_t>(2 * ((a.width / kV + 31) / 32 * 32 * kV) *
+                                                  sizeof(float)))
+                 : 0u;
+  const int smem = 256 + static_cast<int>(a.params) + a.stages * static_cast<int>(a.stage);
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> occ_of;
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  int occ;
+  {
+    std::lock_guard<std::mutex> hold(mu);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), smem);
+    auto it = occ_of.find(key);
+    if (it == occ_of.end()) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           std::min(227 * 1024, 256 + 8192 + std::max(budget, kRsBudget)));
+      int o = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem) !=
+              cudaSuccess ||
+          o < 1)
+        o = 1;
+      it = occ_of.emplace(key, o).first;
+    }
+    occ = it->second;
+  }
+  const int64_t slabs = (a.rows + kRsRows - 1) / kRsRows;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slabs, int64_t{sms} * occ)));
+  kern<<<grid, kThreads, smem, s>>>(a);
+  return cudaSuccess;
+}
+
+// Store path of the streamed kernel per op (r02, fraction of the HBM copy
+// peak): softmax / masked softmax write back with TMA bulk stores (0.92 /
+// 0.93 vs 0.79 / 0.89 with st.global); layernorm and its backward with
+// st.global (0.78 / 0.92 vs 0.73-0.74 / 0.89), whose longer row math holds a
+// TMA-store stage too long. APL_RS_STORE=tma / stg forces one (A/B, tests).
+bool row_stream_tma_store(int op) {
+  static const int forced = [] {
+    const char* e = std::getenv("APL_RS_STORE");
+    if (e == nullptr) return -1;
+    return std::strcmp(e, "stg") == 0 ? 0 : std::strcmp(e, "tma") == 0 ? 1 : -1;
+  }();
+  return forced >= 0 ? forced == 1 : (op == kRowSoftmax || op == kRowMaskedSoftmax);
+}
+
+template <typename T, int kOp>
+cudaError_t row_stream_nv(int nv, const RowStreamArgs& a, cudaStream_t s) {
+  if (row_stream_tma_store(kOp)) {
+    if (nv == 1) return launch_row_stream<T, 1, kOp, true>(a, s);
+    if (nv == 2) return launch_row_stream<T, 2, kOp, true>(a, s);
+    return launch_row_stream<T, 4, kOp, true>(a, s);
+  }
+  if (nv == 1) return launch_row_stream<T, 1, kOp, false>(a, s);
+  if (nv == 2) return launch_row_stream<T, 2, kOp, false>(a, s);
+  return launch_row_stream<T, 4, kOp, false>(a, s);
+}
+
+// Streams rows of <= 4 16-byte vectors per lane; the inputs must be 16-byte
+// aligned with 16-byte rows (the mask's rows too).
+template <typename T>
+cudaError_t row_stream(int op, int nv, const RowStreamArgs& a, cudaStream_t s) {
+  switch (op) {
+    case kRowLn: return row_stream_nv<T, kRowLn>(nv, a, s);
+    case kRowSoftmax: return row_stream_nv<T, kRowSoftmax>(nv, a, s);
+    case kRowMaskedSoftmax: return row_stream_nv<T, kRowMaskedSoftmax>(nv, a, s);
+    default: return row_stream_nv<T, kRowLnBwd>(nv, a, s);
+  }
+}
+
 struct SoftmaxPre {
   float alpha = 1.f;
   const uint8_t* mask = nullptr;
@@ -1071,6 +1535,26 @@ cudaError_t rowwise(bool softmax, const void* x, const void* g, const void* b, v
   auto G = static_cast<const T*>(g);
   auto B = static_cast<const T*>(b);
   const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;  // vectors each lane holds
+  if (per_lane >= 1 && per_lane <= 4 && row_stream_enabled(softmax && p.mask == nullptr) &&
+      (p.mask == nullptr || (width % 16 == 0 && aligned16(p.mask)))) {
+    const bool masked = p.mask != nullptr;
+    RowStreamArgs a{};
+    a.in0 = x;
+    a.mask = p.mask;
+    a.gamma = g;
+    a.beta = b;
+    a.out = y;
+    a.rows = rows;
+    a.width = width;
+    a.eps = eps;
+    a.alpha = p.alpha;
+    a.fill = p.fill;
+    a.row0 = static_cast<uint32_t>(width * sizeof(T));
+    a.rowm = masked ? static_cast<uint32_t>(width) : 0u;
+    const int op = !softmax ? kRowLn : masked ? kRowMaskedSoftmax : kRowSoftmax;
+    const int nv = per_lane == 1 ? 1 : per_lane == 2 ? 2 : 4;
+    if (row_stream<T>(op, nv, a, s) != cudaErrorNotSupported) return done();
+  }
   if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
     const bool masked = p.mask != nullptr;
     const int nv = per_lane == 1 ? 1 : per_lane == 2 ? 2 : 4;
@@ -1330,7 +1814,23 @@ cudaError_t layernorm_bwd_typed(const void* x, const void* gamma, const void* dy
   // 16-byte vectors keep its occupancy up; the r01 fp32-register variant
   // halved it and measured 0.54 of the roofline); longer rows stream.
   const int64_t per_lane = vec ? (width / V + 31) / 32 : 0;
-  if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
+  bool streamed = false;
+  if (per_lane >= 1 && per_lane <= 4 && row_stream_enabled()) {
+    RowStreamArgs a{};
+    a.in0 = x;
+    a.in1 = dy;
+    a.gamma = gamma;
+    a.out = dx;
+    a.stats = stats;
+    a.rows = rows;
+    a.width = width;
+    a.eps = eps;
+    a.row0 = a.row1 = static_cast<uint32_t>(width * sizeof(T));
+    const int nv = per_lane == 1 ? 1 : per_lane == 2 ? 2 : 4;
+    streamed = row_stream<T>(kRowLnBwd, nv, a, s) != cudaErrorNotSupported;
+  }
+  if (streamed) {
+  } else if (per_lane >= 1 && per_lane <= 4 && pipe_rows_enabled()) {
     if (per_lane == 1)
       layernorm_bwd_pipe_kernel<T, 1><<<pipe_grid(layernorm_bwd_pipe_kernel<T, 1>, rows), 256, 0,
                                         s>>>(X, G, D, O, stats, rows, width, eps);

@@ -6,6 +6,7 @@ against the measured copy peak in MEASURED_PEAKS.json.
     python tools/block_ops_bench.py
 """
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -73,7 +74,8 @@ def main():
     for name, fn, bytes_ in cases:
         ms = timed(fn)
         gbs = bytes_ / (ms * 1e-3) / 1e9
-        print(json.dumps({"kernel": name, "ms": round(ms, 4), "algorithmic_bytes": bytes_,
+        print(json.dumps({"kernel": name, "engine": os.environ.get("APL_ROW_ENGINE", "stream"),
+                          "ms": round(ms, 4), "algorithmic_bytes": bytes_,
                           "gbs": round(gbs, 1), "peak_gbs": pk, "frac": round(gbs / pk, 3)}),
               flush=True)
 
