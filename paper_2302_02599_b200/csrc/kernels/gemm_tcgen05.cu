@@ -134,6 +134,34 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// Whole-warp variants: every lane runs the issue loop (its state stays
+// warp-uniform, so the compiler keeps descriptors in uniform registers) and
+// one elected lane issues. The lane-0-only loop moved every descriptor
+// through an R2UR.BROADCAST / ELECT sequence per MMA: ~25 instructions per
+// MMA on one thread, which could not keep the N=128 tiles' 64-cycle MMAs
+// queued (r02 SASS / ncu: tensor pipe 42% active on the pair 256x128 tile).
+__device__ __forceinline__ void mma_bf16_elect(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_addr(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -207,14 +235,12 @@ constexpr int kEpiGeluSave = 3;  // GELU, and the pre-activation stored to aux (
 // 32 accumulator columns of one row: epilogue computed once, then stored to
 // each of `fan` outputs (the fused all-reduce writes every group member).
 // Vector path when the 32 columns are in bounds and 16-byte aligned.
-template <int kEpi, bool kOutF32>
-__device__ __forceinline__ void epi_store32(void* const* outs, int fan, int ldc, int M, int N,
-                                            int row, int col, const uint32_t (&r)[32],
-                                            const void* aux, int ldaux) {
+// The epilogue's arithmetic on 32 accumulator columns of one row, in place:
+// GELU backward against aux, the pre-activation saved to aux, GELU.
+template <int kEpi>
+__device__ __forceinline__ void epi_values32(float (&v)[32], int row, int col, int M, int N,
+                                             const void* aux, int ldaux) {
   if (row >= M || col >= N) return;
-  float v[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
   const bool full = col + 32 <= N;
   if constexpr (kEpi == kEpiDGelu) {
     const __nv_bfloat16* a =
@@ -261,6 +287,18 @@ __device__ __forceinline__ void epi_store32(void* const* outs, int fan, int ldc,
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
   }
+}
+
+template <int kEpi, bool kOutF32>
+__device__ __forceinline__ void epi_store32(void* const* outs, int fan, int ldc, int M, int N,
+                                            int row, int col, const uint32_t (&r)[32],
+                                            const void* aux, int ldaux) {
+  if (row >= M || col >= N) return;
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  epi_values32<kEpi>(v, row, col, M, N, aux, ldaux);
+  const bool full = col + 32 <= N;
   if constexpr (kOutF32) {
     for (int j = 0; j < fan; ++j) {
       float* dst = static_cast<float*>(outs[j]) + static_cast<size_t>(row) * ldc + col;
@@ -296,13 +334,58 @@ __device__ __forceinline__ void epi_store32(void* const* outs, int fan, int ldc,
   }
 }
 
+// ---- TMA-store epilogue ---------------------------------------------------
+// Each epilogue warp stages 32 rows x 128 bytes of output (64 bf16 / 32 fp32
+// columns) in its own 4 KiB of shared memory, 128B-swizzled (16-byte vector
+// q of row r at q ^ (r % 8): the warp's row-per-lane stores are bank-conflict
+// free), and one lane writes the box to every fan-out output with
+// cp.async.bulk.tensor stores (out-of-bounds rows / columns clipped by TMA).
+// The per-lane st.global epilogue scattered 32 rows per instruction, which
+// paced the small-K GEMMs (r02 ncu: the MMA pipe idled behind it).
+constexpr int kStageOut = 4096;                  // per epilogue warp
+constexpr int kStagingBytes = kEpiWarps * kStageOut;
+
+template <bool kOutF32>
+__device__ __forceinline__ void epi_stage32(uint8_t* stage, int lane, int piece,
+                                            const float (&v)[32]) {
+  uint8_t* row = stage + lane * 128;
+  if constexpr (kOutF32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(row + ((q ^ (lane & 7)) << 4)) =
+          make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t p[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
+        std::memcpy(&p[i], &h, 4);
+      }
+      *reinterpret_cast<uint4*>(row + (((4 * piece + q) ^ (lane & 7)) << 4)) =
+          make_uint4(p[0], p[1], p[2], p[3]);
+    }
+  }
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x,
+                                             int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_addr(src)), "r"(x), "r"(y)
+      : "memory");
+}
+
 template <int BN>
 struct Smem {
   static constexpr int kStageA = kBM * kBK * 2;
   static constexpr int kStageB = BN * kBK * 2;
   static constexpr int kStages = (BN >= 256) ? 4 : 6;
   static constexpr int kData = kStages * (kStageA + kStageB);
-  static constexpr int kBytes = kData + 1024 /*align slack*/ + 256 /*barriers*/;
+  // [stage ring][output staging, 1024-aligned][barriers]
+  static constexpr int kBytes = kData + kStagingBytes + 1024 /*align slack*/ + 256 /*barriers*/;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
 };
 
@@ -351,6 +434,14 @@ struct GemmArgs {
   int streamk;
   float* sk_ws;
   int* sk_flags;
+  // TMA-store epilogue: cmap[g * fan + j] maps output c[g * fan + j]
+  // (box 32 rows x 128 bytes, 128B swizzle); 0 = per-lane st.global stores
+  // (scatter_rows, unaligned outputs).
+  int tma_out;
+  // pair kernel: 4-CTA clusters multicasting A across two pairs (A maps with
+  // 64-row boxes)
+  int a_mc;
+  CUtensorMap cmap[kMaxBatch];
 };
 
 // Segments of the (tile, k-block) iteration space a CTA processes, in order.
@@ -394,7 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   uint8_t* tiles_a = base;
   uint8_t* tiles_b = base + S::kStages * S::kStageA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + S::kData);
+  uint8_t* staging = base + S::kData;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + S::kData + kStagingBytes);
   uint64_t* empty = full + S::kStages;
   uint64_t* acc_full = empty + S::kStages;  // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2;       // [2] epilogue -> MMA
@@ -470,8 +562,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // MMA issuer: the whole warp walks the schedule, one elected lane issues
+    {
       constexpr uint32_t idesc = instr_desc<BN, kBMN, kAMN>();
+      const uint64_t da0 = kAMN ? smem_desc_mn(tiles_a) : smem_desc(tiles_a);
+      const uint64_t db0 = kBMN ? smem_desc_mn(tiles_b) : smem_desc(tiles_b);
       int it = 0, local = 0;
       SegIter seg(args.streamk != 0, blockIdx.x, gridDim.x, tiles, KT);
       int t, k0, k1;
@@ -485,22 +580,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&full[s], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t da = kAMN ? smem_desc_mn(tiles_a + s * S::kStageA)
-                                   : smem_desc(tiles_a + s * S::kStageA);
-          const uint64_t db = kBMN ? smem_desc_mn(tiles_b + s * S::kStageB)
-                                   : smem_desc(tiles_b + s * S::kStageB);
+          // stage s's descriptors: base + s stages (address field in 16 B units)
+          const uint64_t da = da0 + uint64_t(s) * (S::kStageA >> 4);
+          const uint64_t db = db0 + uint64_t(s) * (S::kStageB >> 4);
           // K advance per instruction: K-major = 32 B inside the swizzle row;
           // MN-major = 16 rows of 128 B.
           constexpr uint64_t kAdvA = kAMN ? (16 * 128) >> 4 : 2;
           constexpr uint64_t kAdvB = kBMN ? (16 * 128) >> 4 : 2;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            mma_bf16(d, da + kAdvA * k, db + kAdvB * k, idesc,
-                     (kk > k0 || k > 0) ? 1u : 0u);
+            mma_bf16_elect(d, da + kAdvA * k, db + kAdvB * k, idesc,
+                           (kk > k0 || k > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
+          mma_commit_elect(&empty[s]);  // frees the slot once these MMAs have read it
         }
-        mma_commit(&acc_full[acc]);  // accumulator complete
+        mma_commit_elect(&acc_full[acc]);  // accumulator complete
       }
     }
   } else {
@@ -552,19 +646,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-#pragma unroll 1
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-        uint32_t r[32];
-        tmem_ld32(lane_addr + uint32_t(c), r);
-        if (partial) {
-          float4* w = reinterpret_cast<float4*>(args.sk_ws +
-                                                (static_cast<size_t>(blockIdx.x) * kBM + trow) * BN + c);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            w[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                               __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-          continue;
-        }
+      // head of a split tile: add the later CTAs' fp32 partials of columns [c, c+32)
+      auto add_parts = [&](uint32_t (&r)[32], int c) {
         for (int cc = c_first; cc <= c_last; ++cc) {
           if (seg.total * cc / gridDim.x == seg.total * (cc + 1) / gridDim.x) continue;
           const float4* w = reinterpret_cast<const float4*>(
@@ -578,8 +661,51 @@ __global__ void __launch_bounds__(kThreads, 1)
             r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + p.w);
           }
         }
+      };
+      if (args.tma_out && !partial) {
+        uint8_t* stage = staging + (warp - 2) * kStageOut;
+        constexpr int kCW = kOutF32 ? 32 : 64;  // columns per 128-byte staged row
+#pragma unroll 1
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += kCW) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();  // the previous box's store has read the staging
+#pragma unroll
+          for (int p = 0; p < kCW / 32; ++p) {
+            uint32_t r[32];
+            tmem_ld32(lane_addr + uint32_t(c + 32 * p), r);
+            add_parts(r, c + 32 * p);
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            epi_values32<kEpi>(v, row, n0 + c + 32 * p, rows, N, args.aux[g], args.ldaux);
+            epi_stage32<kOutF32>(stage, lane, p, v);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            for (int j = 0; j < fan; ++j)
+              tma_store_2d(&args.cmap[g * args.fan + j], stage, n0 + c, m0 + quarter * 32);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      } else {
+#pragma unroll 1
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_addr + uint32_t(c), r);
+        if (partial) {
+          float4* w = reinterpret_cast<float4*>(args.sk_ws +
+                                                (static_cast<size_t>(blockIdx.x) * kBM + trow) * BN + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            w[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                               __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          continue;
+        }
+        add_parts(r, c);
         epi_store32<kEpi, kOutF32>(outs, fan, ldc, rows, N, row, n0 + c, r, args.aux[g],
                                    args.ldaux);
+      }
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -600,6 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -641,7 +768,7 @@ struct Cfg {
   static constexpr int kStageB = (BN / 2) * kBK * 2;    // 8 / 16 KiB
   static constexpr int kStages = BN >= 256 ? 6 : 8;
   static constexpr int kData = kStages * (kStageA + kStageB);
-  static constexpr int kBytes = kData + 1024 + 256;
+  static constexpr int kBytes = kData + kStagingBytes + 1024 + 256;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
 };
 
@@ -677,6 +804,19 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// Multicast variant: the box lands at the same offset in every CTA of `mask`,
+// each destination's completion counted on its pair leader's barrier.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map,
+                                                    uint64_t* bar_local, int x, int y,
+                                                    uint16_t mask) {
+  const uint32_t bar = smem_addr(bar_local) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -688,11 +828,35 @@ __device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void commit_pair(uint64_t* bar_local) {
+__device__ __forceinline__ void mma_pair_elect(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void commit_pair_elect(uint64_t* bar_local, uint16_t mask) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n"
+      "}\n" ::"r"(smem_addr(bar_local)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void commit_pair(uint64_t* bar_local, uint16_t mask = 0b11) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_addr(bar_local)),
-      "h"(static_cast<uint16_t>(0b11))
+      "h"(mask)
       : "memory");
 }
 
@@ -724,8 +888,16 @@ __device__ __forceinline__ void wait_flag(const int* f) {
 // inside the tile) writes its fp32 partial -- each CTA its own 128 rows --
 // to sk_ws[its CTA] and raises sk_flags[its CTA]; the head CTA of the same
 // cluster rank adds them in cluster order (deterministic) and clears them.
-template <int BN, int kEpi, bool kOutF32, bool kBMN, bool kAMN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+//
+// kMC: a cluster of 4 = two CTA pairs on adjacent N tiles of the same 256
+// rows. Both pairs need the same A rows, so each CTA loads half of its 128
+// A rows and multicasts them to its counterpart in the other pair: L2 reads
+// per SM drop from (A 16 + B 8|16) to (A 8 + B 8|16) KiB per 64-deep K
+// block, the operand fill that paced the pair kernel. A stage is refilled
+// only when both pairs' MMAs have freed it (empty[] counts both leaders'
+// commits). Whole N-tile pairs only (host: even tile count, no stream-K).
+template <int BN, int kEpi, bool kOutF32, bool kBMN, bool kAMN, bool kMC>
+__global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ GemmArgs args) {
   using S = Cfg<BN>;
   const int M = args.M, N = args.N, K = args.K, ldc = args.ldc;
@@ -734,27 +906,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   uint8_t* tiles_a = base;
   uint8_t* tiles_b = base + S::kStages * S::kStageA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + S::kData);
+  uint8_t* staging = base + S::kData;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + S::kData + kStagingBytes);
   uint64_t* empty = full + S::kStages;
   uint64_t* acc_full = empty + S::kStages;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_rank();
+  constexpr int kCS = kMC ? 4 : 2;
+  const uint32_t crank = cluster_rank();
+  const uint32_t rank = crank & 1u;  // position in the CTA pair (0: MMA leader)
+  const int pid = static_cast<int>(crank >> 1);  // pair within a kMC cluster
+  const uint32_t pair_leader = crank & ~1u;
   const bool leader = rank == 0;
   const int kblocks = (K + kBK - 1) / kBK;
   const int n_tiles = (N + BN - 1) / BN;
-  const int per_problem = ((M + 2 * kBM - 1) / (2 * kBM)) * n_tiles;
+  const int n_units = kMC ? n_tiles / 2 : n_tiles;  // N tiles (pairs of them) per cluster tile
+  const int per_problem = ((M + 2 * kBM - 1) / (2 * kBM)) * n_units;
   const int tiles = per_problem * args.count;
-  const int cluster = blockIdx.x / 2, clusters = gridDim.x / 2;
+  const int cluster = blockIdx.x / kCS, clusters = gridDim.x / kCS;
+  auto ntile_of = [&](int lt) { return kMC ? (lt % n_units) * 2 + pid : lt % n_units; };
   const int KT = kblocks * args.reduce;
   const bool sk = args.streamk != 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 2);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kMC ? 2 : 1);  // kMC: both pair leaders' commits
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
@@ -779,14 +958,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t full_leader0 = map_to_rank(smem_addr(&full[0]), 0);
+      const uint32_t full_leader0 = map_to_rank(smem_addr(&full[0]), pair_leader);
+      const uint16_t a_mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
       int it = 0;
       SegIter seg(sk, cluster, clusters, tiles, KT);
       int t, k0, k1;
       while (seg.next(t, k0, k1)) {
         const int g = t / per_problem, lt = t % per_problem;
-        const int m0 = (lt / n_tiles) * 2 * kBM + static_cast<int>(rank) * kBM;
-        const int n0 = (lt % n_tiles) * BN + static_cast<int>(rank) * (BN / 2);
+        const int m0 = (lt / n_units) * 2 * kBM + static_cast<int>(rank) * kBM;
+        const int n0 = ntile_of(lt) * BN + static_cast<int>(rank) * (BN / 2);
         for (int kk = k0; kk < k1; ++kk, ++it) {
           const int kb = kk % kblocks;
           const CUtensorMap* map_a = &args.a[g * args.reduce + kk / kblocks];
@@ -795,7 +975,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
           if (leader) mbar_expect_tx(&full[s], 2 * (S::kStageA + S::kStageB));
-          if constexpr (kAMN) {  // A^T stored [K, M]: two [64 k][64 m] MN atoms
+          if constexpr (kMC) {  // this CTA's 64-row half of the A rows, to both pairs
+            if constexpr (kAMN)
+              tma_load_2d_pair_mc(tiles_a + s * S::kStageA + pid * 8192, map_a, &full[s],
+                                  m0 + pid * 64, kb * kBK, a_mask);
+            else
+              tma_load_2d_pair_mc(tiles_a + s * S::kStageA + pid * 8192, map_a, &full[s],
+                                  kb * kBK, m0 + pid * 64, a_mask);
+          } else if constexpr (kAMN) {  // A^T stored [K, M]: two [64 k][64 m] MN atoms
             tma_load_2d_pair(tiles_a + s * S::kStageA, map_a, &full[s], m0, kb * kBK);
             tma_load_2d_pair(tiles_a + s * S::kStageA + 8192, map_a, &full[s], m0 + 64, kb * kBK);
           } else {
@@ -814,8 +1001,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {  // whole warp walks the schedule, one elected lane issues
       constexpr uint32_t idesc = instr_desc_pair<BN, kBMN, kAMN>();
+      const uint64_t da0 = kAMN ? smem_desc_mn(tiles_a) : smem_desc(tiles_a);
+      const uint64_t db0 = kBMN ? smem_desc_mn(tiles_b) : smem_desc(tiles_b);
       int it = 0, local = 0;
       SegIter seg(sk, cluster, clusters, tiles, KT);
       int t, k0, k1;
@@ -828,32 +1017,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int s = it % S::kStages;
           mbar_wait(&full[s], (it / S::kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t da = kAMN ? smem_desc_mn(tiles_a + s * S::kStageA)
-                                   : smem_desc(tiles_a + s * S::kStageA);
-          const uint64_t db = kBMN ? smem_desc_mn(tiles_b + s * S::kStageB)
-                                   : smem_desc(tiles_b + s * S::kStageB);
+          const uint64_t da = da0 + uint64_t(s) * (S::kStageA >> 4);
+          const uint64_t db = db0 + uint64_t(s) * (S::kStageB >> 4);
           constexpr uint64_t kAdvA = kAMN ? (16 * 128) >> 4 : 2;
           constexpr uint64_t kAdvB = kBMN ? (16 * 128) >> 4 : 2;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            mma_pair(d, da + kAdvA * k, db + kAdvB * k, idesc, (kk > k0 || k > 0) ? 1u : 0u);
-          commit_pair(&empty[s]);
+            mma_pair_elect(d, da + kAdvA * k, db + kAdvB * k, idesc,
+                           (kk > k0 || k > 0) ? 1u : 0u);
+          commit_pair_elect(&empty[s], kMC ? 0b1111 : 0b11);  // kMC: the other pair's stage too
         }
-        commit_pair(&acc_full[acc]);
+        commit_pair_elect(&acc_full[acc], static_cast<uint16_t>(0b11u << (2 * pid)));
       }
     }
   } else {
     const int quarter = warp % 4;
     const int half = (warp - 2) / 4;
-    const uint32_t acc_empty_leader = map_to_rank(smem_addr(&acc_empty[0]), 0);
+    const uint32_t acc_empty_leader = map_to_rank(smem_addr(&acc_empty[0]), pair_leader);
     int local = 0;
     SegIter seg(sk, cluster, clusters, tiles, KT);
     int t, k0, k1;
     for (; seg.next(t, k0, k1); ++local) {
       const int acc = local & 1;
       const int g = t / per_problem, lt = t % per_problem;
-      const int m0 = (lt / n_tiles) * 2 * kBM + static_cast<int>(rank) * kBM;
-      const int n0 = (lt % n_tiles) * BN;
+      const int m0 = (lt / n_units) * 2 * kBM + static_cast<int>(rank) * kBM;
+      const int n0 = ntile_of(lt) * BN;
       void* const* const outs = args.c + g * args.fan;
       const int trow = quarter * 32 + lane;
       const int row = m0 + trow;
@@ -875,19 +1063,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-#pragma unroll 1
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-        uint32_t r[32];
-        tmem_ld32(lane_addr + uint32_t(c), r);
-        if (partial) {
-          float4* w = reinterpret_cast<float4*>(
-              args.sk_ws + (static_cast<size_t>(blockIdx.x) * kBM + trow) * BN + c);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            w[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                               __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-          continue;
-        }
+      auto add_parts = [&](uint32_t (&r)[32], int c) {
         for (int cc = c_first; cc <= c_last; ++cc) {
           if (seg.total * cc / clusters == seg.total * (cc + 1) / clusters) continue;
           const float4* w = reinterpret_cast<const float4*>(
@@ -901,8 +1077,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + p.w);
           }
         }
+      };
+      if (args.tma_out && !partial) {
+        uint8_t* stage = staging + (warp - 2) * kStageOut;
+        constexpr int kCW = kOutF32 ? 32 : 64;
+#pragma unroll 1
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += kCW) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int p = 0; p < kCW / 32; ++p) {
+            uint32_t r[32];
+            tmem_ld32(lane_addr + uint32_t(c + 32 * p), r);
+            add_parts(r, c + 32 * p);
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            epi_values32<kEpi>(v, row, n0 + c + 32 * p, M, N, args.aux[g], args.ldaux);
+            epi_stage32<kOutF32>(stage, lane, p, v);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            for (int j = 0; j < args.fan; ++j)
+              tma_store_2d(&args.cmap[g * args.fan + j], stage, n0 + c, m0 + quarter * 32);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      } else {
+#pragma unroll 1
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_addr + uint32_t(c), r);
+        if (partial) {
+          float4* w = reinterpret_cast<float4*>(
+              args.sk_ws + (static_cast<size_t>(blockIdx.x) * kBM + trow) * BN + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            w[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                               __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          continue;
+        }
+        add_parts(r, c);
         epi_store32<kEpi, kOutF32>(outs, args.fan, ldc, M, N, row, n0 + c, r, args.aux[g],
                                    args.ldaux);
+      }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -922,6 +1141,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -995,6 +1215,56 @@ bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int
   return r == CUDA_SUCCESS;
 }
 
+// Output map of the TMA-store epilogue: [rows][cols] of bf16 / fp32 with
+// leading dimension ld, box = 32 rows x 128 bytes, 128B swizzle.
+bool make_out_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, bool f32) {
+  EncodeFn enc = encode_fn();
+  if (enc == nullptr) return false;
+  const int elt = f32 ? 4 : 2;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * elt};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elt), 32};
+  const cuuint32_t elem[2] = {1, 1};
+  const CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                         2, const_cast<void*>(ptr), dims, strides, box, elem,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// APL_GEMM_MC=1: the 4-CTA multicast pair kernel. Off by default: measured
+// equal or slower than 2-CTA clusters on every config-5 shape and 8192^3
+// (profiles/r02_gemm_sweep_mc.jsonl) -- A operand reads are not the limiter.
+bool gemm_mc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_GEMM_MC");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// APL_GEMM_TMA_OUT=0: per-lane st.global epilogue (A/B).
+bool tma_out_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_GEMM_TMA_OUT");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Fill args.cmap for outputs c[0 .. n) when every one can take TMA stores.
+void attach_out_maps(GemmArgs& args, int n, bool out_f32) {
+  args.tma_out = 0;
+  if (!tma_out_enabled() || args.scatter_rows > 0) return;
+  const int elt = out_f32 ? 4 : 2;
+  if ((static_cast<int64_t>(args.ldc) * elt) % 16) return;
+  for (int i = 0; i < n; ++i)
+    if ((reinterpret_cast<uintptr_t>(args.c[i]) & 15) ||
+        !make_out_map(&args.cmap[i], args.c[i], args.M, args.N, args.ldc, out_f32))
+      return;
+  args.tma_out = 1;
+}
+
 template <int BN, int E, bool F, bool BMN, bool AMN = false>
 cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
   auto kernel = gemm_bf16_tcgen05<BN, E, F, BMN, AMN>;
@@ -1039,9 +1309,9 @@ cudaError_t dispatch(const GemmArgs& args, bool out_f32, int epi, bool a_km,
 }
 
 // 2-CTA pair kernel launch (cluster dims are compiled into the kernel).
-template <int BN, int E, bool F, bool BMN, bool AMN = false>
-cudaError_t launch_pair(const GemmArgs& args, cudaStream_t stream) {
-  auto kernel = pair::gemm_bf16_tcgen05_pair<BN, E, F, BMN, AMN>;
+template <int BN, int E, bool F, bool BMN, bool AMN, bool MC>
+cudaError_t launch_pair_t(const GemmArgs& args, cudaStream_t stream) {
+  auto kernel = pair::gemm_bf16_tcgen05_pair<BN, E, F, BMN, AMN, MC>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1055,12 +1325,35 @@ cudaError_t launch_pair(const GemmArgs& args, cudaStream_t stream) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
   }();
+  constexpr int kCS = MC ? 4 : 2;
+  // co-resident clusters: a persistent grid larger than this runs its last
+  // clusters as a second wave (4-CTA clusters do not tile every GPC)
+  static const int max_clusters = [&] {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kCS * (sms / kCS), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = pair::Cfg<BN>::kBytes;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = sms / kCS;
+    }
+    if (debug_on()) std::fprintf(stderr, "apl gemm: %d-CTA clusters co-resident: %d\n", kCS, n);
+    return std::min(n, sms / kCS);
+  }();
   const int tiles = ((args.N + BN - 1) / BN) *
-                    ((args.M + 2 * pair::kBM - 1) / (2 * pair::kBM)) * args.count;
-  const int clusters = args.streamk ? sms / 2 : std::min(tiles, sms / 2);
-  kernel<<<2 * clusters, kThreads, pair::Cfg<BN>::kBytes, stream>>>(args);
+                    ((args.M + 2 * pair::kBM - 1) / (2 * pair::kBM)) * args.count / (MC ? 2 : 1);
+  const int clusters = args.streamk ? max_clusters : std::min(tiles, max_clusters);
+  kernel<<<kCS * clusters, kThreads, pair::Cfg<BN>::kBytes, stream>>>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return why(cudaGetLastError(), "pair gemm launch");
+}
+
+// args.a_mc: A maps built with 64-row boxes for the multicast cluster kernel.
+template <int BN, int E, bool F, bool BMN, bool AMN = false>
+cudaError_t launch_pair(const GemmArgs& args, cudaStream_t stream) {
+  return args.a_mc ? launch_pair_t<BN, E, F, BMN, AMN, true>(args, stream)
+                   : launch_pair_t<BN, E, F, BMN, AMN, false>(args, stream);
 }
 
 template <int BN, bool BMN>
@@ -1152,13 +1445,14 @@ struct GemmPlan {
 };
 
 // Relative per-SM throughput of each tile shape, calibrated on 8192^3 where
-// wave quantisation is negligible (profiles/r02_gemm_sweep.jsonl: pair256
-// 1393, cta256 1171, pair128 954, cta128 923 TFLOP/s). Operand fill per MMA
-// cycle sets the order: the 256 x 256 pair tile needs 64 B/clk per SM, the
-// others 96-128 B/clk.
+// wave quantisation is negligible, with the TMA-store epilogue and the
+// whole-warp MMA issuer (profiles/r02_gemm_sweep_elect.jsonl: pair256
+// ~1430, cta256 1292, pair128 1063, cta128 932 TFLOP/s). Operand fill per
+// MMA cycle sets the order: the 256 x 256 pair tile needs 64 B/clk per SM,
+// the others 96-128 B/clk.
 double tile_eff(bool paired, int bn) {
-  if (paired) return bn == 256 ? 1.0 : 0.685;
-  return bn == 256 ? 0.84 : 0.66;
+  if (paired) return bn == 256 ? 1.0 : 0.74;
+  return bn == 256 ? 0.9 : 0.65;
 }
 
 // Cost model: per-SM work of a tile / its efficiency, times the waves of
@@ -1243,6 +1537,9 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
   // B box rows for the K-major layout: the pair kernel stages half of its
   // N tile per CTA.
   const int b_rows = paired ? bn / 2 : bn;
+  // whole-tile pair plans with an even N-tile count run as 4-CTA clusters
+  // that multicast A across the two pairs (APL_GEMM_MC=0: 2-CTA clusters)
+  const bool mc = paired && !plan.streamk && ((N + bn - 1) / bn) % 2 == 0 && gemm_mc_enabled();
   for (int first = 0; first < groups; first += per_launch) {
     GemmArgs args;
     std::memset(&args, 0, sizeof(args));
@@ -1260,12 +1557,14 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
       if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
         return why(cudaErrorInvalidValue, "operand base not 16-byte aligned (TMA)");
       const bool oka = a_km ? make_map(&args.a[i], a, K, M, lda, kBK, 64)
-                            : make_map(&args.a[i], a, M, K, lda, kBM);
+                            : make_map(&args.a[i], a, M, K, lda, mc ? kBM / 2 : kBM);
       const bool okb = b_kn ? make_map(&args.b[i], b, K, N, ldb, kBK, 64)
                             : make_map(&args.b[i], b, N, K, ldb, b_rows);
       if (!oka || !okb) return why(cudaErrorInvalidValue, "tensor map encode");
     }
     for (int i = 0; i < args.count * fan; ++i) args.c[i] = C[first * fan + i];
+    attach_out_maps(args, args.count * fan, out_f32);
+    args.a_mc = mc ? 1 : 0;
     if (epi >= kEpiDGelu)
       for (int i = 0; i < args.count; ++i) args.aux[i] = aux[first + i];
     if (plan.streamk && !streamk_attach(args, stream)) return cudaErrorMemoryAllocation;

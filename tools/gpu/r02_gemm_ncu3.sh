@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+APL_GEMM_PAIR=1 APL_GEMM_BN=128 timeout 300 ncu --set full --clock-control none -k regex:gemm_bf16 -s 3 -c 1 -o gpurun_out/ncu_pair128_fc2m python tools/gemm_case.py 2048 1024 4096 --iters 1 > gpurun_out/ncu_p1.log 2>&1
+ls -la gpurun_out; du -sh gpurun_out
