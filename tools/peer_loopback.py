@@ -30,6 +30,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--modes", default="fused,unfused",
+                    help="comma list of fused / unfused (each in its own process for A/B)")
+    ap.add_argument("--debug", action="store_true", help="synchronise and report after each warm-up exchange")
     args = ap.parse_args()
     P = args.ranks
     # one hardware queue per stream: two ranks' streams sharing a queue would
@@ -95,10 +98,13 @@ def main():
         row = {"case": name, "ranks": P, "tensor": list(shape), "conversion": f"{a}->{b}",
                "grid_cap": int(os.environ["APL_PULL_GRID_CAP"]),
                "bytes_pulled_per_rank": s.per_device_bytes(meta, geo) * (P - 1) // (1 if b == "RR" else P)}
-        for fused in (True, False):
+        for fused in [m == "fused" for m in args.modes.split(",")]:
             for _ in range(5):
                 epoch += 1
                 exchange(fused, epoch)
+                if args.debug:
+                    torch.cuda.synchronize()
+                    print(f"ok {name} fused={fused} epoch={epoch}", file=sys.stderr, flush=True)
             torch.cuda.synchronize()
             start = torch.cuda.Event(enable_timing=True)
             start.record(torch.cuda.current_stream())
@@ -116,9 +122,12 @@ def main():
             us = max(start.elapsed_time(ev) for ev in ends) / args.iters * 1e3
             row["fused_us" if fused else "unfused_us"] = round(us, 2)
         row["launches_per_rank_per_exchange"] = {"fused": 2, "unfused": 5}
-        row["identical_bytes"] = all(torch.equal(x, y) for x, y in zip(outs["fused"],
-                                                                       outs["unfused"]))
-        row["bus_gbs_per_rank_fused"] = round(row["bytes_pulled_per_rank"] / row["fused_us"] / 1e3, 1)
+        if "fused_us" in row and "unfused_us" in row:
+            row["identical_bytes"] = all(torch.equal(x, y) for x, y in zip(outs["fused"],
+                                                                           outs["unfused"]))
+        for m in ("fused", "unfused"):
+            if f"{m}_us" in row:
+                row[f"bus_gbs_per_rank_{m}"] = round(row["bytes_pulled_per_rank"] / row[f"{m}_us"] / 1e3, 1)
         print(json.dumps(row), flush=True)
     for h in meshes:
         lib.apl_mesh_destroy(h)
