@@ -479,6 +479,18 @@ int apl_softmax_ex(const void* x, void* y, int64_t rows, int64_t width, float al
 /* transpose perm [0, 2, 1]: x [batch, rows, cols] -> y [batch, cols, rows]. */
 int apl_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                   int elem_bytes, void* stream);
+/* any transpose: x row-major with extents shape[0..rank) (rank <= 8), y the
+ * row-major tensor with y dim d = x dim perm[d] (graph_ir.cpp:270-290).
+ * Out of place; bit-exact element moves (elem_bytes 1/2/4/8). */
+int apl_permute(const void* x, void* y, int rank, const int64_t* shape, const int64_t* perm,
+                int elem_bytes, void* stream);
+/* softmax over the middle dim of a row-major [outer, len, inner] tensor (the
+ * graph's softmax `axis` when it is not the last), and its backward from the
+ * output: dx = alpha * y * (dy - sum_axis(dy * y)). */
+int apl_softmax_axis(const void* x, void* y, int64_t outer, int64_t len, int64_t inner,
+                     int dtype, void* stream);
+int apl_softmax_axis_backward(const void* y, const void* dy, void* dx, int64_t outer,
+                              int64_t len, int64_t inner, float alpha, int dtype, void* stream);
 /* elementwise-unary y = alpha * x. */
 int apl_scale(const void* x, void* y, size_t count, float alpha, int dtype, void* stream);
 /* elementwise-binary y = a + alpha * b; b has a's dtype, or with b_mask != 0

@@ -522,12 +522,13 @@ class PlanExecutor {
     if (nd.kind == "reshape") {
       out.push_back({0, dy, required_spec(nd, 0)});
     } else if (nd.kind == "transpose") {
-      const size_t r = ls.size();
-      const int64_t rows = ls[r - 2], cols = ls[r - 1], batch = numel(ls) / (rows * cols);
+      // dx = dy permuted back: inverse permutation of the output's layout
+      std::vector<int64_t> inv(nd.perm.size());
+      for (size_t k = 0; k < nd.perm.size(); ++k) inv[static_cast<size_t>(nd.perm[k])] = static_cast<int64_t>(k);
       std::vector<const void*> dx;
       for (int d = 0; d < num_local_; ++d) {
         void* o = grad_buf(count * 2);
-        apl_detail::check(apl_transpose(dy.p[d], o, batch, rows, cols, 2, stream));
+        permute(dy.p[d], o, ls, inv, 2, stream);
         dx.push_back(o);
       }
       out.push_back({0, Grad{dx, 2}, required_spec(nd, 0)});
@@ -549,11 +550,13 @@ class PlanExecutor {
       }
     } else if (nd.kind == "softmax") {
       const auto& y = saved_.at(nd.id)[0];
-      const int64_t w = ls.back(), rows = numel(ls) / w;
+      const int64_t so = axis_outer(ls, nd.axis), sn = ls[axis_of(ls, nd.axis)],
+                    si = numel(ls) / (so * sn);
       std::vector<const void*> dx;
       for (int d = 0; d < num_local_; ++d) {
         void* o = grad_buf(count * 2);
-        apl_detail::check(apl_softmax_backward(y[d], dy.p[d], o, rows, w, 1.f, APL_BF16, stream));
+        apl_detail::check(
+            apl_softmax_axis_backward(y[d], dy.p[d], o, so, sn, si, 1.f, APL_BF16, stream));
         dx.push_back(o);
       }
       out.push_back({0, Grad{dx, 2}, required_spec(nd, 0)});
@@ -811,6 +814,34 @@ class PlanExecutor {
     return std::vector<ShardingSpec>(nd.inputs.size(), nd.spec);  // elementwise
   }
 
+  static size_t axis_of(const std::vector<int64_t>& shape, int64_t axis) {
+    const int64_t r = static_cast<int64_t>(shape.size());
+    return static_cast<size_t>(axis < 0 ? axis + r : axis);
+  }
+  // product of the extents before the softmax axis
+  static int64_t axis_outer(const std::vector<int64_t>& shape, int64_t axis) {
+    int64_t o = 1;
+    for (size_t k = 0; k < axis_of(shape, axis); ++k) o *= shape[k];
+    return o;
+  }
+  // any transpose of a local shard (graph_ir.cpp:270-290); the last-two swap
+  // takes the tiled 2-D transpose kernel
+  static void permute(const void* x, void* y, const std::vector<int64_t>& in_shape,
+                      const std::vector<int64_t>& perm, int elem_bytes, void* stream) {
+    const size_t r = perm.size();
+    bool last2 = r >= 2 && perm[r - 2] == static_cast<int64_t>(r - 1) &&
+                 perm[r - 1] == static_cast<int64_t>(r - 2);
+    for (size_t i = 0; last2 && i + 2 < r; ++i) last2 = perm[i] == static_cast<int64_t>(i);
+    if (last2) {
+      const int64_t rows = in_shape[r - 2], cols = in_shape[r - 1];
+      const int64_t batch = numel(in_shape) / std::max<int64_t>(1, rows * cols);
+      apl_detail::check(apl_transpose(x, y, batch, rows, cols, elem_bytes, stream));
+      return;
+    }
+    apl_detail::check(apl_permute(x, y, static_cast<int>(r), in_shape.data(), perm.data(),
+                                  elem_bytes, stream));
+  }
+
   void bind_unary(Node& nd) const {
     const Node& src = nodes_.at(nd.inputs.at(0));
     if (src.meta.dtype_bytes == 1) {
@@ -819,8 +850,13 @@ class PlanExecutor {
       nd.unary = Unary::kScale;
       const double k = static_cast<double>(nodes_.at(src.inputs.at(0)).meta.shape.back());
       nd.alpha = static_cast<float>(1.0 / std::sqrt(k));
+    } else if (src.kind == "matmul" || nd.id.find("gelu") != std::string::npos) {
+      nd.unary = Unary::kGelu;  // the MLP activation (fc1 -> act)
     } else {
-      nd.unary = Unary::kGelu;
+      // the graph does not name the function: refuse to guess (the Python
+      // executor takes an explicit unary= binding for such graphs)
+      throw SchemaError(nd.id + ": elementwise-unary consuming a " + src.kind +
+                        " node has no known function binding");
     }
   }
 
@@ -931,24 +967,15 @@ class PlanExecutor {
                                         ins.size() > 2 ? ins[2][d] : nullptr, out[d], rows, w,
                                         1e-5f, dt, stream));
     } else if (nd.kind == "softmax") {
-      if (nd.axis != -1 && nd.axis != static_cast<int64_t>(ls.size()) - 1)
-        throw SchemaError(nd.id + ": softmax over a non-last axis is not executable");
-      const int64_t w = ls.back(), rows = numel(ls) / w;
+      // the softmax axis is replicated under every strategy (intraop.cpp:368-384)
+      const int64_t o = axis_outer(ls, nd.axis), n = ls[axis_of(ls, nd.axis)],
+                    i = numel(ls) / (o * n);
       for (int d = 0; d < num_local_; ++d)
-        apl_detail::check(apl_softmax(ins[0][d], out[d], rows, w, dt, stream));
+        apl_detail::check(apl_softmax_axis(ins[0][d], out[d], o, n, i, dt, stream));
     } else if (nd.kind == "transpose") {
-      const size_t r = nd.perm.size();
-      for (size_t i = 0; i + 2 < r; ++i)
-        if (nd.perm[i] != static_cast<int64_t>(i))
-          throw SchemaError(nd.id + ": only last-two-dim transposes are executable");
-      if (r < 2 || nd.perm[r - 2] != static_cast<int64_t>(r - 1) ||
-          nd.perm[r - 1] != static_cast<int64_t>(r - 2))
-        throw SchemaError(nd.id + ": only last-two-dim transposes are executable");
       const auto is = local_shape(required_spec(nd, 0), nodes_.at(nd.inputs[0]).meta);
-      const int64_t rows = is[r - 2], cols = is[r - 1], batch = numel(is) / (rows * cols);
       for (int d = 0; d < num_local_; ++d)
-        apl_detail::check(
-            apl_transpose(ins[0][d], out[d], batch, rows, cols, nd.meta.dtype_bytes, stream));
+        permute(ins[0][d], out[d], is, nd.perm, nd.meta.dtype_bytes, stream);
     } else if (nd.kind == "elementwise-binary") {
       int a = 0, b = 1;
       if (nodes_.at(nd.inputs[0]).meta.dtype_bytes == 1) std::swap(a, b);

@@ -187,6 +187,13 @@ _SIGS = {
                                  C.c_void_p, C.c_float, C.c_int, C.c_void_p]),
     "apl_transpose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                 C.c_void_p]),
+    "apl_permute": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, P(C.c_int64), P(C.c_int64),
+                              C.c_int, C.c_void_p]),
+    "apl_softmax_axis": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                   C.c_int, C.c_void_p]),
+    "apl_softmax_axis_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                            C.c_int64, C.c_int64, C.c_float, C.c_int,
+                                            C.c_void_p]),
     "apl_scale": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_float, C.c_int, C.c_void_p]),
     "apl_add": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_float,
                           C.c_int, C.c_void_p]),

@@ -76,6 +76,42 @@ def transpose_last2(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
                                 x.element_size(), _stream_handle(stream)))
 
 
+def permute(x: torch.Tensor, y: torch.Tensor, perm, stream=None) -> None:
+    """y = x.permute(perm) materialised (row-major), any permutation of rank
+    <= 8: the graph's general transpose (apl_permute)."""
+    perm = [int(p) for p in perm]
+    if sorted(perm) != list(range(x.dim())) or list(y.shape) != [x.shape[p] for p in perm]:
+        raise ValueError(f"bad permutation {perm} for {tuple(x.shape)} -> {tuple(y.shape)}")
+    I64 = C.c_int64 * max(1, x.dim())
+    check(A.lib().apl_permute(_p(x), _p(y), x.dim(), I64(*x.shape), I64(*perm),
+                              x.element_size(), _stream_handle(stream)))
+
+
+def _axis_split(shape, axis):
+    axis = axis % len(shape)
+    outer = 1
+    for e in shape[:axis]:
+        outer *= e
+    inner = 1
+    for e in shape[axis + 1:]:
+        inner *= e
+    return outer, shape[axis], inner
+
+
+def softmax_axis(x: torch.Tensor, y: torch.Tensor, axis: int, stream=None) -> None:
+    """Softmax over any axis (the last one takes the row kernels)."""
+    o, n, i = _axis_split(tuple(x.shape), axis)
+    check(A.lib().apl_softmax_axis(_p(x), _p(y), o, n, i, _DTYPE_CODE[x.dtype],
+                                   _stream_handle(stream)))
+
+
+def softmax_axis_backward(y: torch.Tensor, dy: torch.Tensor, dx: torch.Tensor, axis: int,
+                          alpha: float = 1.0, stream=None) -> None:
+    o, n, i = _axis_split(tuple(y.shape), axis)
+    check(A.lib().apl_softmax_axis_backward(_p(y), _p(dy), _p(dx), o, n, i, alpha,
+                                            _DTYPE_CODE[y.dtype], _stream_handle(stream)))
+
+
 def scale(x: torch.Tensor, y: torch.Tensor, alpha: float, stream=None) -> None:
     check(A.lib().apl_scale(_p(x), _p(y), x.numel(), alpha, _DTYPE_CODE[x.dtype],
                             _stream_handle(stream)))

@@ -1133,6 +1133,64 @@ int apl_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t c
   });
 }
 
+int apl_permute(const void* x, void* y, int rank, const int64_t* shape, const int64_t* perm,
+                int elem_bytes, void* stream) {
+  return guarded([&] {
+    need(rank >= 1 && rank <= 8 && shape != nullptr && perm != nullptr, "rank must be 1..8");
+    bool seen[8] = {};
+    int64_t numel = 1;
+    for (int d = 0; d < rank; ++d) {
+      need(perm[d] >= 0 && perm[d] < rank && !seen[perm[d]], "perm is not a permutation");
+      seen[perm[d]] = true;
+      need(shape[d] >= 0, "negative extent");
+      numel *= shape[d];
+    }
+    need((x && y) || numel == 0, "null buffer");
+    need(x != y || numel == 0, "permute is out of place");
+    need(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8,
+         "elem_bytes must be 1, 2, 4 or 8");
+    apl::check_cuda(apl::launch_permute(x, y, rank, shape, perm, elem_bytes,
+                                        static_cast<cudaStream_t>(stream)),
+                    "permute launch");
+  });
+}
+
+int apl_softmax_axis(const void* x, void* y, int64_t outer, int64_t len, int64_t inner,
+                     int dtype, void* stream) {
+  return guarded([&] {
+    need(outer >= 0 && len > 0 && inner > 0, "bad extents");
+    need((x && y) || outer == 0, "null buffer");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    if (inner == 1) {
+      apl::check_cuda(apl::launch_softmax(x, y, outer, len, 1.f, nullptr, 0.f, dtype,
+                                          static_cast<cudaStream_t>(stream)),
+                      "softmax launch");
+      return;
+    }
+    apl::check_cuda(apl::launch_softmax_axis(x, y, outer, len, inner, dtype,
+                                             static_cast<cudaStream_t>(stream)),
+                    "softmax (axis) launch");
+  });
+}
+
+int apl_softmax_axis_backward(const void* y, const void* dy, void* dx, int64_t outer,
+                              int64_t len, int64_t inner, float alpha, int dtype, void* stream) {
+  return guarded([&] {
+    need(outer >= 0 && len > 0 && inner > 0, "bad extents");
+    need((y && dy && dx) || outer == 0, "null buffer");
+    need(dtype == APL_F32 || dtype == APL_BF16, "dtype must be f32 or bf16");
+    if (inner == 1) {
+      apl::check_cuda(apl::launch_softmax_backward(y, dy, dx, outer, len, alpha, dtype,
+                                                   static_cast<cudaStream_t>(stream)),
+                      "softmax backward launch");
+      return;
+    }
+    apl::check_cuda(apl::launch_softmax_axis_backward(y, dy, dx, outer, len, inner, alpha, dtype,
+                                                      static_cast<cudaStream_t>(stream)),
+                    "softmax (axis) backward launch");
+  });
+}
+
 int apl_scale(const void* x, void* y, size_t count, float alpha, int dtype, void* stream) {
   return guarded([&] {
     need((x && y) || count == 0, "null buffer");

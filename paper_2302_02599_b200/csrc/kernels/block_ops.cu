@@ -32,6 +32,7 @@
 namespace apl {
 
 extern std::atomic<uint64_t> g_launches;
+int sm_count();
 
 namespace {
 
@@ -1059,6 +1060,126 @@ __global__ void __launch_bounds__(256) softmax_bwd_pipe_kernel(const T* __restri
   }
 }
 
+
+// ---- general transpose (any permutation) and softmax over any axis ----------
+// The graph format's transpose carries an arbitrary `perm` and softmax an
+// `axis` (graph_ir.cpp:270-290); the block plans only use the last-two swap
+// and the last axis (the kernels above), these cover the rest.
+
+constexpr int kMaxPermDims = 8;
+struct PermArgs {
+  int rank;
+  int64_t out_shape[kMaxPermDims];   // output extents
+  int64_t in_stride[kMaxPermDims];   // input element stride of output dim d (x dim perm[d])
+  int64_t out_stride[kMaxPermDims];  // output element strides (row-major)
+};
+
+// perm[r-1] == r-1: the last dim stays innermost, so each output row is one
+// contiguous input row -- a warp copies it (16-byte vectors when aligned).
+template <typename W>
+__global__ void __launch_bounds__(256) permute_rows_kernel(const W* __restrict__ x,
+                                                           W* __restrict__ y, int64_t rows,
+                                                           int64_t row_words,
+                                                           const __grid_constant__ PermArgs a) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * blockDim.x / 32;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += warps) {
+    int64_t rem = r, in_off = 0;  // a.in_stride in W words
+    for (int d = a.rank - 2; d >= 0; --d) {  // output coordinates of row r, minor first
+      const int64_t c = rem % a.out_shape[d];
+      rem /= a.out_shape[d];
+      in_off += c * a.in_stride[d];
+    }
+    const W* from = x + in_off;
+    W* to = y + r * row_words;
+    for (int64_t i = lane; i < row_words; i += 32) to[i] = from[i];
+  }
+}
+
+// General case: the input's last dim (contiguous in x) and input dim q =
+// perm[r-1] (contiguous in y) form a 32 x 32 shared-memory tile, so reads
+// are coalesced along x's last dim and writes along y's; every other dim
+// is a batch index. a.in_stride / a.out_stride here are indexed by INPUT dim.
+template <typename E>
+__global__ void __launch_bounds__(256) permute_tile_kernel(const E* __restrict__ x,
+                                                           E* __restrict__ y, int q, int last,
+                                                           int64_t nq, int64_t nl, int64_t batch,
+                                                           const __grid_constant__ PermArgs a) {
+  __shared__ E tile[32][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+  const int64_t tiles_l = (nl + 31) / 32, tiles_q = (nq + 31) / 32;
+  for (int64_t t = blockIdx.x; t < batch * tiles_q * tiles_l; t += gridDim.x) {
+    int64_t b = t / (tiles_q * tiles_l);
+    const int64_t tt = t % (tiles_q * tiles_l);
+    const int64_t q0 = (tt / tiles_l) * 32, l0 = (tt % tiles_l) * 32;
+    // batch index over the input dims other than q and last, minor first
+    int64_t in_base = 0, out_base = 0;
+    for (int d = a.rank - 1; d >= 0; --d) {
+      if (d == q || d == last) continue;
+      const int64_t c = b % a.out_shape[d];  // out_shape holds INPUT extents here
+      b /= a.out_shape[d];
+      in_base += c * a.in_stride[d];
+      out_base += c * a.out_stride[d];
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+      const int64_t qi = q0 + i, li = l0 + tx;
+      if (qi < nq && li < nl) tile[i][tx] = x[in_base + qi * a.in_stride[q] + li];
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+      const int64_t li = l0 + i, qi = q0 + tx;
+      if (qi < nq && li < nl) y[out_base + li * a.out_stride[last] + qi] = tile[tx][i];
+    }
+  }
+}
+
+// softmax over the middle dim of [outer, len, inner] (inner > 1): a thread per
+// (outer, inner) column, consecutive threads on consecutive inner indices so
+// every pass is coalesced; one online max/sum pass, one normalising pass.
+template <typename T>
+__global__ void __launch_bounds__(256) softmax_axis_kernel(const T* __restrict__ x,
+                                                           T* __restrict__ y, int64_t outer,
+                                                           int64_t len, int64_t inner) {
+  const int64_t cols = outer * inner;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cols;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t o = c / inner, i = c % inner;
+    const T* xc = x + o * len * inner + i;
+    T* yc = y + o * len * inner + i;
+    float m = -INFINITY, s = 0.f;
+    for (int64_t k = 0; k < len; ++k) {
+      const float v = ld(xc + k * inner);
+      const float nm = fmaxf(m, v);
+      s = s * __expf(m - nm) + __expf(v - nm);
+      m = nm;
+    }
+    const float inv = 1.f / s;
+    for (int64_t k = 0; k < len; ++k) st(yc + k * inner, __expf(ld(xc + k * inner) - m) * inv);
+  }
+}
+
+// its backward from the output: dx = alpha * y * (dy - sum_k dy * y)
+template <typename T>
+__global__ void __launch_bounds__(256) softmax_axis_bwd_kernel(const T* __restrict__ y,
+                                                               const T* __restrict__ dy,
+                                                               T* __restrict__ dx, int64_t outer,
+                                                               int64_t len, int64_t inner,
+                                                               float alpha) {
+  const int64_t cols = outer * inner;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cols;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t base = (c / inner) * len * inner + c % inner;
+    float s = 0.f;
+    for (int64_t k = 0; k < len; ++k) s += ld(y + base + k * inner) * ld(dy + base + k * inner);
+    for (int64_t k = 0; k < len; ++k) {
+      const int64_t o = base + k * inner;
+      st(dx + o, alpha * ld(y + o) * (ld(dy + o) - s));
+    }
+  }
+}
+
 // ---- backward ---------------------------------------------------------------
 // layernorm: dx = rstd * (g.dy - mean(g.dy) - xhat * mean(g.dy.xhat)), warp per
 // row: one pass for the four row sums (mean / rstd recomputed from x, kept per
@@ -1715,6 +1836,87 @@ cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, 
   if (dtype == 1)
     return rowwise<__nv_bfloat16>(true, x, nullptr, nullptr, y, rows, width, 0.f, s, p);
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_permute(const void* x, void* y, int rank, const int64_t* shape,
+                           const int64_t* perm, int elem_bytes, cudaStream_t s) {
+  int64_t numel = 1;
+  for (int d = 0; d < rank; ++d) numel *= shape[d];
+  if (numel == 0) return cudaSuccess;
+  int64_t in_stride[kMaxPermDims];  // row-major element strides of x
+  in_stride[rank - 1] = 1;
+  for (int d = rank - 2; d >= 0; --d) in_stride[d] = in_stride[d + 1] * shape[d + 1];
+  PermArgs a{};
+  a.rank = rank;
+  const int last = rank - 1;
+  if (perm[last] == last) {  // rows stay contiguous: a row copy
+    for (int d = 0; d < rank; ++d) {
+      a.out_shape[d] = shape[perm[d]];
+      a.in_stride[d] = in_stride[perm[d]];
+    }
+    const int64_t row_bytes = shape[last] * elem_bytes, rows = numel / shape[last];
+    const bool v16 = row_bytes % 16 == 0 && aligned16(x) && aligned16(y);
+    const int w = v16 ? 16 : elem_bytes;
+    for (int d = 0; d < rank; ++d) a.in_stride[d] = a.in_stride[d] * elem_bytes / w;
+    const int grid = grid_for(rows * 32);
+    switch (w) {
+      case 16: permute_rows_kernel<uint4><<<grid, 256, 0, s>>>(static_cast<const uint4*>(x), static_cast<uint4*>(y), rows, row_bytes / 16, a); break;
+      case 8: permute_rows_kernel<uint64_t><<<grid, 256, 0, s>>>(static_cast<const uint64_t*>(x), static_cast<uint64_t*>(y), rows, row_bytes / 8, a); break;
+      case 4: permute_rows_kernel<uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(x), static_cast<uint32_t*>(y), rows, row_bytes / 4, a); break;
+      case 2: permute_rows_kernel<uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x), static_cast<uint16_t*>(y), rows, row_bytes / 2, a); break;
+      default: permute_rows_kernel<uint8_t><<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(x), static_cast<uint8_t*>(y), rows, row_bytes, a); break;
+    }
+    return done();
+  }
+  // tile case: strides indexed by INPUT dim; out_shape carries input extents
+  int64_t out_dim_stride[kMaxPermDims];  // row-major strides of y
+  out_dim_stride[rank - 1] = 1;
+  for (int d = rank - 2; d >= 0; --d) out_dim_stride[d] = out_dim_stride[d + 1] * shape[perm[d + 1]];
+  for (int d = 0; d < rank; ++d) {
+    a.out_shape[d] = shape[d];
+    a.in_stride[d] = in_stride[d];
+  }
+  for (int d = 0; d < rank; ++d) a.out_stride[perm[d]] = out_dim_stride[d];
+  const int q = static_cast<int>(perm[last]);
+  const int64_t nq = shape[q], nl = shape[last], batch = numel / (nq * nl);
+  const int64_t tiles = batch * ((nq + 31) / 32) * ((nl + 31) / 32);
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t{sm_count()} * 16));
+  switch (elem_bytes) {
+    case 1: permute_tile_kernel<uint8_t><<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(x), static_cast<uint8_t*>(y), q, last, nq, nl, batch, a); break;
+    case 2: permute_tile_kernel<uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x), static_cast<uint16_t*>(y), q, last, nq, nl, batch, a); break;
+    case 4: permute_tile_kernel<uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(x), static_cast<uint32_t*>(y), q, last, nq, nl, batch, a); break;
+    default: permute_tile_kernel<uint64_t><<<grid, 256, 0, s>>>(static_cast<const uint64_t*>(x), static_cast<uint64_t*>(y), q, last, nq, nl, batch, a); break;
+  }
+  return done();
+}
+
+cudaError_t launch_softmax_axis(const void* x, void* y, int64_t outer, int64_t len, int64_t inner,
+                                int dtype, cudaStream_t s) {
+  if (outer * len * inner == 0) return cudaSuccess;
+  const int grid = grid_for(outer * inner);
+  if (dtype == 0)
+    softmax_axis_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x),
+                                                    static_cast<float*>(y), outer, len, inner);
+  else
+    softmax_axis_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), outer, len, inner);
+  return done();
+}
+
+cudaError_t launch_softmax_axis_backward(const void* y, const void* dy, void* dx, int64_t outer,
+                                         int64_t len, int64_t inner, float alpha, int dtype,
+                                         cudaStream_t s) {
+  if (outer * len * inner == 0) return cudaSuccess;
+  const int grid = grid_for(outer * inner);
+  if (dtype == 0)
+    softmax_axis_bwd_kernel<float><<<grid, 256, 0, s>>>(
+        static_cast<const float*>(y), static_cast<const float*>(dy), static_cast<float*>(dx),
+        outer, len, inner, alpha);
+  else
+    softmax_axis_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(y), static_cast<const __nv_bfloat16*>(dy),
+        static_cast<__nv_bfloat16*>(dx), outer, len, inner, alpha);
+  return done();
 }
 
 cudaError_t launch_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,

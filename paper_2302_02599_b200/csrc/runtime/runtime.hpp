@@ -82,6 +82,15 @@ cudaError_t launch_layernorm(const void* x, const void* gamma, const void* beta,
                              int64_t rows, int64_t width, float eps, int dtype, cudaStream_t s);
 cudaError_t launch_softmax(const void* x, void* y, int64_t rows, int64_t width, float alpha,
                            const void* mask, float fill, int dtype, cudaStream_t s);
+// any permutation of a row-major tensor of rank <= 8 (y dim d = x dim perm[d])
+cudaError_t launch_permute(const void* x, void* y, int rank, const int64_t* shape,
+                           const int64_t* perm, int elem_bytes, cudaStream_t s);
+// softmax over the middle dim of [outer, len, inner], and its backward
+cudaError_t launch_softmax_axis(const void* x, void* y, int64_t outer, int64_t len, int64_t inner,
+                                int dtype, cudaStream_t s);
+cudaError_t launch_softmax_axis_backward(const void* y, const void* dy, void* dx, int64_t outer,
+                                         int64_t len, int64_t inner, float alpha, int dtype,
+                                         cudaStream_t s);
 cudaError_t launch_transpose(const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                              int elem_bytes, cudaStream_t s);
 cudaError_t launch_scale(const void* x, void* y, size_t count, float alpha, int dtype,

@@ -33,8 +33,9 @@ and executes the forward pass on a `runtime.Mesh` (simulated or distributed):
 The graph format names the elementwise-unary function only by node id (the
 reference plans it as an opaque elementwise op), so the executor binds:
 a uint8 operand -> logical not (the block's `mask2`); an id containing
-"scale" behind a batched matmul -> x / sqrt(k) (attention scaling); anything
-else -> exact-erf GELU. A binary op with a uint8 operand adds it as an
+"scale" behind a batched matmul -> x / sqrt(k) (attention scaling); a
+matmul output (the MLP activation) or an id containing "gelu" -> exact-erf
+GELU; any other unary node is rejected (ValueError) unless `unary=` binds it. A binary op with a uint8 operand adds it as an
 additive mask (a - 1e4 * m); otherwise it is a + b (residuals). `unary=`
 overrides the binding per node.
 
@@ -196,7 +197,12 @@ class PlanExecutor:
         if "scale" in nid and prod["kind"] == "batched-matmul":
             k = self.shapes[prod["inputs"][0][0]][0][-1]
             return ("scale", 1.0 / float(k) ** 0.5)
-        return ("gelu",)
+        if prod["kind"] == "matmul" or "gelu" in nid.lower():
+            return ("gelu",)  # the MLP activation (fc1 -> act)
+        raise ValueError(
+            f"{nid}: the graph does not name this elementwise-unary function (it consumes a "
+            f"{prod['kind']} node); pass unary={{{nid!r}: ('gelu',) | ('scale', alpha) | "
+            f"('not',)}} to bind it")
 
     def _attention_chains(self) -> dict:
         """softmax id -> (softmax, scale node, binary node, scores id, mask id,
@@ -447,17 +453,19 @@ class PlanExecutor:
                 B.layernorm(x, gg, bb, o, stream=stream)
         elif kind == "softmax":
             axis = n.get("attrs", {}).get("axis", -1)
-            if axis not in (-1, len(local) - 1):
-                raise NotImplementedError("softmax over a non-last axis")
             for x, o in zip(ins[0], outs):
-                B.softmax(x, o, stream=stream)
+                if axis in (-1, len(local) - 1):
+                    B.softmax(x, o, stream=stream)
+                else:  # the strategy keeps the softmax axis whole on every device
+                    B.softmax_axis(x, o, axis, stream=stream)
         elif kind == "transpose":
             perm = list(n["attrs"]["perm"])
             r = len(perm)
-            if perm != list(range(r - 2)) + [r - 1, r - 2]:
-                raise NotImplementedError(f"transpose perm {perm}")
             for x, o in zip(ins[0], outs):
-                B.transpose_last2(x, o, stream=stream)
+                if perm == list(range(r - 2)) + [r - 1, r - 2]:
+                    B.transpose_last2(x, o, stream=stream)
+                else:
+                    B.permute(x, o, perm, stream=stream)
         elif kind == "elementwise-binary":
             a, b = ins
             if a[0].dtype == torch.uint8:
@@ -757,10 +765,15 @@ class PlanExecutor:
             shape = self.required_spec(nid, 0).local_shape(self._meta(ins[0]), self.geo)
             out.append((0, [g.view(shape) for g in dy]))
         elif kind == "transpose":
-            dx = [self._empty(g.shape[:-2] + (g.shape[-1], g.shape[-2]), g.dtype, g.device)
-                  for g in dy]
+            perm = list(n["attrs"]["perm"])
+            r = len(perm)
+            inv = [perm.index(d) for d in range(r)]  # dx = dy permuted back
+            dx = [self._empty(tuple(g.shape[i] for i in inv), g.dtype, g.device) for g in dy]
             for g, o in zip(dy, dx):
-                B.transpose_last2(g, o, stream=stream)
+                if perm == list(range(r - 2)) + [r - 1, r - 2]:
+                    B.transpose_last2(g, o, stream=stream)
+                else:
+                    B.permute(g, o, inv, stream=stream)
             out.append((0, dx))
         elif kind == "elementwise-unary":
             op = self.unary_op(nid)
@@ -778,8 +791,12 @@ class PlanExecutor:
         elif kind == "softmax":
             y = self._saved[nid]
             dx = like(dy)
+            axis = n.get("attrs", {}).get("axis", -1)
             for yy, g, o in zip(y, dy, dx):
-                B.softmax_backward(yy, g, o, stream=stream)
+                if axis in (-1, yy.dim() - 1):
+                    B.softmax_backward(yy, g, o, stream=stream)
+                else:
+                    B.softmax_axis_backward(yy, g, o, axis, stream=stream)
             out.append((0, dx))
         elif kind == "layernorm":
             x, *aff = self._saved[nid]

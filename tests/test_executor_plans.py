@@ -62,3 +62,26 @@ def test_block_plans_decode_and_match_communication(path):
     for rw in plan.get("reshape_rewrites", []):
         nid = rw["node"]
         assert list(ex.spec[nid].local_shape(ex._meta(nid), ex.geo)) == rw["new_target_shape"]
+
+
+def test_unnamed_unary_is_rejected_unless_bound():
+    """The graph format does not name elementwise-unary functions; a unary
+    node the executor cannot identify (here one renamed to hide the
+    attention-scale role) is refused instead of silently becoming GELU, and
+    an explicit unary= binding executes it."""
+    graph = json.loads((PLANS / "gpt_block_fixture_graph.json").read_text())
+    plan = json.loads((PLANS / "gpt_block_fixture_mesh4_unlimited.json").read_text())
+    ren = {"scaled": "mystery"}
+    for n in graph["nodes"]:
+        n["id"] = ren.get(n["id"], n["id"])
+        n["inputs"] = [[ren.get(a, a), i] for a, i in n["inputs"]]
+    plan["nodes"] = {ren.get(k, k): v for k, v in plan["nodes"].items()}
+    for c in plan.get("inserted_comm_nodes", []):
+        for key in ("producer", "consumer"):
+            if c.get(key) in ren:
+                c[key] = ren[c[key]]
+    with pytest.raises(ValueError, match="mystery"):  # rejected up front
+        PlanExecutor(_GeoOnly(plan["mesh"]["shape"]), graph, plan)
+    ex2 = PlanExecutor(_GeoOnly(plan["mesh"]["shape"]), graph, plan,
+                       unary={"mystery": ("scale", 0.125)})
+    assert ex2.unary_op("mystery") == ("scale", 0.125)
