@@ -380,11 +380,20 @@ int env_int(const char* name, int dflt) {
 // Strided tables: U=4 @ 4 CTAs/SM as well (r01 short-row probe: 0.92 vs
 // 0.85 for U=8 @ 3 on 256 B rows at 512 MiB, ahead at every size measured,
 // profiles/r01_short_row_probe.jsonl); U=8 @ 3 stays selectable (variant 3).
+// Fan-out tables (r02 knob sweep, profiles/r02_copy_variant_probe.jsonl,
+// and the every-pair sweep, r02_pairs_*.jsonl): U=16 @ 1 CTA/SM only wins
+// for wide fan-outs of contiguous source runs (config 2's S0R->RR 0.91 vs
+// 0.87; S1R->RR on 2x4 0.93 vs 0.89). Narrow fan-outs (2-way: a target
+// replicated over one mesh axis of 2) and strided sources went from
+// 0.65-0.76 with it to 0.87-0.98 with U=8 @ 2 CTAs/SM, which keeps twice
+// the loads in flight per SM.
 int copy_variant(int max_outer, int max_fan, int64_t write_bytes) {
   static int forced = env_int("APL_COPY_VARIANT", -1);
   if (forced >= 0) return forced;
-  if (max_fan > 1) return write_bytes / max_fan < (int64_t{8} << 20) ? 1 : 2;
-  (void)max_outer;
+  if (max_fan > 1) {
+    if (write_bytes / max_fan < (int64_t{8} << 20)) return 1;
+    return max_fan >= 4 && max_outer == 0 ? 2 : 0;
+  }
   return 1;
 }
 
