@@ -85,6 +85,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Elected-lane forms for the whole-warp TMA producer (warp-uniform operands,
+// one lane issues; see mma_bf16_elect).
+__device__ __forceinline__ void mbar_expect_tx_e(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_e(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                              int x, int y) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n}\n" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
 // K-major, 128B-swizzled operand tile: rows of 128 B, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t smem_desc(const void* tile) {
   const uint64_t addr = smem_addr(tile);
@@ -527,36 +546,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int KT = kblocks * args.reduce;
   if (warp == 0) {
-    if (lane == 0) {
+    // TMA producer: the whole warp walks the schedule (warp-uniform state,
+    // no per-K-block division: the input slice r and its block kb advance
+    // incrementally), one elected lane issues
+    {
       int it = 0;  // ring position across tiles
       SegIter seg(args.streamk != 0, blockIdx.x, gridDim.x, tiles, KT);
       int t, k0, k1;
       while (seg.next(t, k0, k1)) {
         const int g = t / per_problem, lt = t % per_problem;
         const int m0 = (lt / n_tiles) * kBM, n0 = (lt % n_tiles) * BN;
+        int r = k0 / kblocks, kb = k0 - r * kblocks;
         for (int kk = k0; kk < k1; ++kk, ++it) {
-          const int kb = kk % kblocks;
-          const CUtensorMap* map_a = &args.a[g * args.reduce + kk / kblocks];
-          const CUtensorMap* map_b = &args.b[g * args.reduce + kk / kblocks];
+          const CUtensorMap* map_a = &args.a[g * args.reduce + r];
+          const CUtensorMap* map_b = &args.b[g * args.reduce + r];
           const int s = it % S::kStages;
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
-          mbar_expect_tx(&full[s], S::kStageA + S::kStageB);
+          mbar_expect_tx_e(&full[s], S::kStageA + S::kStageB);
           if constexpr (kAMN) {
             // two boxes of [64 k][64 m], one MN swizzle atom column each
-            tma_load_2d(tiles_a + s * S::kStageA, map_a, &full[s], m0, kb * kBK);
-            tma_load_2d(tiles_a + s * S::kStageA + 8192, map_a, &full[s], m0 + 64, kb * kBK);
+            tma_load_2d_e(tiles_a + s * S::kStageA, map_a, &full[s], m0, kb * kBK);
+            tma_load_2d_e(tiles_a + s * S::kStageA + 8192, map_a, &full[s], m0 + 64, kb * kBK);
           } else {
-            tma_load_2d(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
+            tma_load_2d_e(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
           }
           if constexpr (kBMN) {
             // BN/64 boxes of [64 k][64 n], one MN swizzle atom column each
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(tiles_b + s * S::kStageB + j * 8192, map_b, &full[s], n0 + j * 64,
-                          kb * kBK);
+              tma_load_2d_e(tiles_b + s * S::kStageB + j * 8192, map_b, &full[s], n0 + j * 64,
+                            kb * kBK);
           } else {
-            tma_load_2d(tiles_b + s * S::kStageB, map_b, &full[s], kb * kBK, n0);
+            tma_load_2d_e(tiles_b + s * S::kStageB, map_b, &full[s], kb * kBK, n0);
+          }
+          if (++kb == kblocks) {
+            kb = 0;
+            ++r;
           }
         }
       }
@@ -804,6 +830,35 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// Elected-lane forms for the whole-warp pair producer.
+__device__ __forceinline__ void tma_load_2d_pair_e(void* dst, const CUtensorMap* map,
+                                                   uint64_t* bar_local, int x, int y) {
+  const uint32_t bar = smem_addr(bar_local) & 0xFEFFFFFFu;  // peer bit -> rank 0
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n}\n" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair_mc_e(void* dst, const CUtensorMap* map,
+                                                      uint64_t* bar_local, int x, int y,
+                                                      uint16_t mask) {
+  const uint32_t bar = smem_addr(bar_local) & 0xFEFFFFFFu;
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;\n}\n" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void remote_arrive_e(uint32_t cluster_addr) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e mbarrier.arrive.shared::cluster.b64 _, [%0];\n}\n" ::"r"(cluster_addr)
+      : "memory");
+}
+
 // Multicast variant: the box lands at the same offset in every CTA of `mask`,
 // each destination's completion counted on its pair leader's barrier.
 __device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map,
@@ -957,7 +1012,8 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    // TMA producer: whole warp, incremental K position, one elected lane issues
+    {
       const uint32_t full_leader0 = map_to_rank(smem_addr(&full[0]), pair_leader);
       const uint16_t a_mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
       int it = 0;
@@ -967,36 +1023,41 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
         const int g = t / per_problem, lt = t % per_problem;
         const int m0 = (lt / n_units) * 2 * kBM + static_cast<int>(rank) * kBM;
         const int n0 = ntile_of(lt) * BN + static_cast<int>(rank) * (BN / 2);
+        int r = k0 / kblocks, kb = k0 - r * kblocks;
         for (int kk = k0; kk < k1; ++kk, ++it) {
-          const int kb = kk % kblocks;
-          const CUtensorMap* map_a = &args.a[g * args.reduce + kk / kblocks];
-          const CUtensorMap* map_b = &args.b[g * args.reduce + kk / kblocks];
+          const CUtensorMap* map_a = &args.a[g * args.reduce + r];
+          const CUtensorMap* map_b = &args.b[g * args.reduce + r];
           const int s = it % S::kStages;
           const uint32_t phase = (it / S::kStages) & 1;
           mbar_wait(&empty[s], phase ^ 1);
-          if (leader) mbar_expect_tx(&full[s], 2 * (S::kStageA + S::kStageB));
+          if (leader) mbar_expect_tx_e(&full[s], 2 * (S::kStageA + S::kStageB));
           if constexpr (kMC) {  // this CTA's 64-row half of the A rows, to both pairs
             if constexpr (kAMN)
-              tma_load_2d_pair_mc(tiles_a + s * S::kStageA + pid * 8192, map_a, &full[s],
-                                  m0 + pid * 64, kb * kBK, a_mask);
+              tma_load_2d_pair_mc_e(tiles_a + s * S::kStageA + pid * 8192, map_a, &full[s],
+                                    m0 + pid * 64, kb * kBK, a_mask);
             else
-              tma_load_2d_pair_mc(tiles_a + s * S::kStageA + pid * 8192, map_a, &full[s],
-                                  kb * kBK, m0 + pid * 64, a_mask);
+              tma_load_2d_pair_mc_e(tiles_a + s * S::kStageA + pid * 8192, map_a, &full[s],
+                                    kb * kBK, m0 + pid * 64, a_mask);
           } else if constexpr (kAMN) {  // A^T stored [K, M]: two [64 k][64 m] MN atoms
-            tma_load_2d_pair(tiles_a + s * S::kStageA, map_a, &full[s], m0, kb * kBK);
-            tma_load_2d_pair(tiles_a + s * S::kStageA + 8192, map_a, &full[s], m0 + 64, kb * kBK);
+            tma_load_2d_pair_e(tiles_a + s * S::kStageA, map_a, &full[s], m0, kb * kBK);
+            tma_load_2d_pair_e(tiles_a + s * S::kStageA + 8192, map_a, &full[s], m0 + 64,
+                               kb * kBK);
           } else {
-            tma_load_2d_pair(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
+            tma_load_2d_pair_e(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
           }
           if constexpr (kBMN) {
 #pragma unroll
             for (int j = 0; j < (BN / 2) / 64; ++j)
-              tma_load_2d_pair(tiles_b + s * S::kStageB + j * 8192, map_b, &full[s], n0 + j * 64,
-                               kb * kBK);
+              tma_load_2d_pair_e(tiles_b + s * S::kStageB + j * 8192, map_b, &full[s],
+                                 n0 + j * 64, kb * kBK);
           } else {
-            tma_load_2d_pair(tiles_b + s * S::kStageB, map_b, &full[s], kb * kBK, n0);
+            tma_load_2d_pair_e(tiles_b + s * S::kStageB, map_b, &full[s], kb * kBK, n0);
           }
-          if (!leader) remote_arrive(full_leader0 + s * 8);
+          if (!leader) remote_arrive_e(full_leader0 + s * 8);
+          if (++kb == kblocks) {
+            kb = 0;
+            ++r;
+          }
         }
       }
     }
@@ -1446,13 +1507,13 @@ struct GemmPlan {
 
 // Relative per-SM throughput of each tile shape, calibrated on 8192^3 where
 // wave quantisation is negligible, with the TMA-store epilogue and the
-// whole-warp MMA issuer (profiles/r02_gemm_sweep_elect.jsonl: pair256
-// ~1430, cta256 1292, pair128 1063, cta128 932 TFLOP/s). Operand fill per
-// MMA cycle sets the order: the 256 x 256 pair tile needs 64 B/clk per SM,
-// the others 96-128 B/clk.
+// whole-warp MMA issuer and TMA producer (profiles/r02_gemm_sweep_prod.jsonl:
+// pair256 1471, pair128 1196, cta256 1176, cta128 903 TFLOP/s). Operand
+// fill per MMA cycle sets the order: the 256 x 256 pair tile needs 64 B/clk
+// per SM, the others 96-128 B/clk.
 double tile_eff(bool paired, int bn) {
-  if (paired) return bn == 256 ? 1.0 : 0.74;
-  return bn == 256 ? 0.9 : 0.65;
+  if (paired) return bn == 256 ? 1.0 : 0.81;
+  return bn == 256 ? 0.8 : 0.62;
 }
 
 // Cost model: per-SM work of a tile / its efficiency, times the waves of
