@@ -273,6 +273,20 @@ typedef struct {
 int apl_run_pull_sync(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
                       const apl_meta* meta, const void* const* peer_in, void* out,
                       const apl_peer_sync* sync, void* stream);
+/* The same exchange as a PUSH (remote stores instead of remote loads): this
+ * rank stores every piece it sends straight into the receivers' outputs.
+ * peer_out[q] = rank q's output mapped here (exported memory), peer_out[rank]
+ * = the local output; in = this rank's source (local). One launch: CTA 0
+ * stores `epoch` into slot `rank` of every peer (this rank's output may be
+ * overwritten), every CTA waits until the ranks it writes to announced
+ * `epoch`, the stores run, and after a system-scope fence the last CTA
+ * stores `epoch` into slot P + rank of every peer (done writing). The
+ * receiver waits for done of its senders (apl_exchange_peers' `senders`,
+ * apl_peer_flags_wait on slots P + s) before reading its output; the source
+ * is never read remotely, so no wait is needed before overwriting it. */
+int apl_run_push_sync(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                      const apl_meta* meta, const void* in, void* const* peer_out,
+                      const apl_peer_sync* sync, void* stream);
 /* Peers of this rank in a src -> tgt peer exchange: the ranks it reads from
  * (senders) and the ranks that read its source (readers); arrays of
  * num_devices entries (either may be NULL to count only). */

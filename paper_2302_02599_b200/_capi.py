@@ -113,6 +113,8 @@ _SIGS = {
                                C.c_void_p]),
     "apl_run_pull_sync": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_void_p),
                                     C.c_void_p, P(PeerSyncC), C.c_void_p]),
+    "apl_run_push_sync": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), C.c_void_p,
+                                    P(C.c_void_p), P(PeerSyncC), C.c_void_p]),
     "apl_exchange_peers": (C.c_int, [C.c_void_p, P(Spec), P(Spec), P(Meta), P(C.c_int32),
                                      P(C.c_int), P(C.c_int32), P(C.c_int)]),
     "apl_mesh_info": (C.c_int, [C.c_void_p, P(C.c_int), P(C.c_int), P(C.c_int), P(C.c_int)]),

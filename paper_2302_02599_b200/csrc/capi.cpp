@@ -528,6 +528,18 @@ int apl_run_pull_sync(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
   });
 }
 
+int apl_run_push_sync(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
+                      const apl_meta* meta, const void* in, void* const* peer_out,
+                      const apl_peer_sync* sync, void* stream) {
+  return guarded([&] {
+    need(mesh && in && peer_out && sync, "null argument");
+    apl::PeerSyncArgs a{sync->peer_flags, sync->local_flags, sync->counter, sync->epoch,
+                        static_cast<uint64_t>(sync->timeout_ms) * 1000000ull};
+    apl::run_push_sync(mesh->impl, to_spec(src), to_spec(tgt), to_meta(meta), in, peer_out, a,
+                       static_cast<cudaStream_t>(stream));
+  });
+}
+
 int apl_exchange_peers(apl_mesh* mesh, const apl_spec* src, const apl_spec* tgt,
                        const apl_meta* meta, int32_t* senders, int* n_senders, int32_t* readers,
                        int* n_readers) {

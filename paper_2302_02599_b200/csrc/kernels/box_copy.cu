@@ -337,7 +337,8 @@ __global__ void __launch_bounds__(256, MINB)
     __syncthreads();  // every load of this CTA has returned (its stores consumed them)
     __shared__ unsigned int last;
     if (t == 0) {
-      __threadfence();
+      if (sync.mode & PeerSync::kPush) __threadfence_system();  // remote stores visible
+      else __threadfence();
       last = atomicAdd(sync.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
     }
     __syncthreads();
@@ -382,17 +383,19 @@ int env_int(const char* name, int dflt) {
 // profiles/r01_short_row_probe.jsonl); U=8 @ 3 stays selectable (variant 3).
 // Fan-out tables (r02 knob sweep, profiles/r02_copy_variant_probe.jsonl,
 // and the every-pair sweep, r02_pairs_*.jsonl): U=16 @ 1 CTA/SM only wins
-// for wide fan-outs of contiguous source runs (config 2's S0R->RR 0.91 vs
-// 0.87; S1R->RR on 2x4 0.93 vs 0.89). Narrow fan-outs (2-way: a target
-// replicated over one mesh axis of 2) and strided sources went from
-// 0.65-0.76 with it to 0.87-0.98 with U=8 @ 2 CTAs/SM, which keeps twice
-// the loads in flight per SM.
+// for wide (>= 4-way) fan-outs (config 2's S0R->RR 0.91 vs 0.87; S1R->RR
+// on 2x4 0.93 vs 0.89; the 8-way S0S1->RR of strided 4 KiB runs 0.90 vs
+// 0.87). Narrow fan-outs (2-way: a target replicated over one mesh axis of
+// 2, or a 4x-replicated source feeding 8 receivers) went from 0.65-0.76
+// with it to 0.87-0.98 with U=8 @ 2 CTAs/SM, which keeps twice the loads
+// in flight per SM.
 int copy_variant(int max_outer, int max_fan, int64_t write_bytes) {
   static int forced = env_int("APL_COPY_VARIANT", -1);
   if (forced >= 0) return forced;
+  (void)max_outer;
   if (max_fan > 1) {
     if (write_bytes / max_fan < (int64_t{8} << 20)) return 1;
-    return max_fan >= 4 && max_outer == 0 ? 2 : 0;
+    return max_fan >= 4 ? 2 : 0;
   }
   return 1;
 }

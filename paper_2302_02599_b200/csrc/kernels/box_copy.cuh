@@ -83,7 +83,9 @@ struct PtrTable {
 // written", slot P + p = "rank p finished reading its sources".
 constexpr int kPeerMaxRanks = 64;
 struct PeerSync {
-  enum : int { kAnnounce = 1, kDone = 2 };
+  // kPush: the table writes into peers' outputs (remote stores), so every
+  // CTA fences at system scope before the last one announces done.
+  enum : int { kAnnounce = 1, kDone = 2, kPush = 4 };
   uint32_t* remote[kPeerMaxRanks];   // every peer's flag array (mapped here)
   const uint32_t* local;             // this rank's flag array
   unsigned int* counter;             // zeroed device counter (last-CTA election)

@@ -36,6 +36,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <unordered_map>
 #include <tuple>
 
 namespace apl {
@@ -1256,10 +1257,51 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+// Encoded tensor maps by (pointer, extents, leading dim, box, dtype): a
+// training loop reuses its buffers, so most launches skip the driver's
+// encode (the host cost that dominated eager small GEMMs). Bounded: cleared
+// when it outgrows kMapCache entries.
+constexpr size_t kMapCache = 512;
+struct MapKey {
+  uintptr_t ptr;
+  int64_t rows, cols, ld;
+  int box_rows, box_cols, f32;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld &&
+           box_rows == o.box_rows && box_cols == o.box_cols && f32 == o.f32;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<uintptr_t>()(k.ptr);
+    for (int64_t v : {k.rows, k.cols, k.ld, int64_t{k.box_rows}, int64_t{k.box_cols},
+                      int64_t{k.f32}})
+      h = h * 1000003u ^ std::hash<int64_t>()(v);
+    return h;
+  }
+};
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+bool cached_map(const MapKey& k, CUtensorMap* map) {
+  std::lock_guard<std::mutex> hold(g_map_mu);
+  auto it = g_maps.find(k);
+  if (it == g_maps.end()) return false;
+  *map = it->second;
+  return true;
+}
+void remember_map(const MapKey& k, const CUtensorMap& map) {
+  std::lock_guard<std::mutex> hold(g_map_mu);
+  if (g_maps.size() >= kMapCache) g_maps.clear();
+  g_maps.emplace(k, map);
+}
+
 // 2-D bf16 tensor map, 128B swizzle, box = [box_rows][box_cols] (box_cols
 // x 2 B = one 128-byte swizzle row).
 bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int box_rows,
               int box_cols = kBK) {
+  const MapKey key{reinterpret_cast<uintptr_t>(ptr), rows, cols, ld, box_rows, box_cols, 0};
+  if (cached_map(key, map)) return true;
   EncodeFn enc = encode_fn();
   if (enc == nullptr) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -1273,12 +1315,15 @@ bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int
   if (r != CUDA_SUCCESS && debug_on())
     std::fprintf(stderr, "apl gemm: cuTensorMapEncodeTiled(%p, %d x %d, ld %d, box %d x %d) = %d\n",
                  ptr, rows, cols, ld, box_rows, box_cols, static_cast<int>(r));
+  if (r == CUDA_SUCCESS) remember_map(key, *map);
   return r == CUDA_SUCCESS;
 }
 
 // Output map of the TMA-store epilogue: [rows][cols] of bf16 / fp32 with
 // leading dimension ld, box = 32 rows x 128 bytes, 128B swizzle.
 bool make_out_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, bool f32) {
+  const MapKey key{reinterpret_cast<uintptr_t>(ptr), rows, cols, ld, 32, -1, f32 ? 1 : 0};
+  if (cached_map(key, map)) return true;
   EncodeFn enc = encode_fn();
   if (enc == nullptr) return false;
   const int elt = f32 ? 4 : 2;
@@ -1290,6 +1335,7 @@ bool make_out_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld,
                          2, const_cast<void*>(ptr), dims, strides, box, elem,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS) remember_map(key, *map);
   return r == CUDA_SUCCESS;
 }
 

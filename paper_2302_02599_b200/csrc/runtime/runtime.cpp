@@ -450,7 +450,7 @@ void run_copies(const CompiledCopies& c, const PtrTable& ptrs, cudaStream_t stre
 
 Mesh::~Mesh() {
   for (auto& [key, ex] : exchanges) {
-    for (auto* m : {&ex->copies, &ex->pre, &ex->post, &ex->pull})
+    for (auto* m : {&ex->copies, &ex->pre, &ex->post, &ex->pull, &ex->push})
       for (auto& [v, c] : *m) free_copies(c);
   }
   for (auto& [ptr, owned] : peer_buffers)
@@ -555,6 +555,28 @@ std::shared_ptr<Exchange> get_exchange(Mesh& mesh, const autoplan::ShardingSpec&
       }
     }
     merge_splits(ex->host_pre);
+    // Push form: the pieces the pull form's receivers take from this rank
+    // (the same sender choice, so pull and push move identical bytes).
+    // Receivers taking the identical box at the same offset (replicated
+    // targets) share one fan-out descriptor: the source is read once.
+    std::map<std::vector<int64_t>, size_t> group;
+    for (int64_t q = 0; q < mesh.geo.num_devices(); ++q)
+      for (const Piece& p : pieces_for_receiver(src, tgt, mesh.geo, meta, q)) {
+        if (p.sender != me) continue;
+        std::vector<int64_t> key(p.src_lo);
+        key.insert(key.end(), p.dst_lo.begin(), p.dst_lo.end());
+        key.insert(key.end(), p.ext.begin(), p.ext.end());
+        auto it = group.find(key);
+        if (it != group.end() && ex->host_push[it->second].ndst < CopyDesc::kMaxFan) {
+          CopyDesc& c = ex->host_push[it->second];
+          c.extra_dst[c.ndst - 1] = static_cast<int>(q);
+          ++c.ndst;
+          continue;
+        }
+        group[key] = ex->host_push.size();
+        ex->host_push.push_back(make_copy(0, ls, p.src_lo, static_cast<int>(q), lt, p.dst_lo,
+                                          p.ext, eb));
+      }
   }
   std::lock_guard<std::mutex> hold(mesh.mu);
   ex->label = key;
@@ -845,6 +867,53 @@ void run_pull_sync(Mesh& mesh, const autoplan::ShardingSpec& src,
   check_cuda(launch_box_pull_sync(c.table, c.begins.data(), c.ntasks, c.total_units, c.vec,
                                   c.max_outer, t, y, stream),
              "fused peer exchange launch");
+}
+
+void run_push_sync(Mesh& mesh, const autoplan::ShardingSpec& src,
+                   const autoplan::ShardingSpec& tgt, const autoplan::TensorMeta& meta,
+                   const void* in, void* const* peer_out, const PeerSyncArgs& sync,
+                   cudaStream_t stream) {
+  if (!mesh.distributed) throw RuntimeError(APL_ERR_ARG, "peer push needs a distributed mesh");
+  if (!src.valid_for(meta, mesh.geo) || !tgt.valid_for(meta, mesh.geo))
+    throw RuntimeError(APL_ERR_SHAPE, "spec is not valid for the tensor/mesh");
+  const int64_t p = mesh.geo.num_devices();
+  if (p > kCopyMaxPtrs || p > kPeerMaxRanks)
+    throw RuntimeError(APL_ERR_ARG, "mesh too large for one push launch");
+  if (sync.flags == nullptr || sync.local_flags == nullptr || sync.counter == nullptr)
+    throw RuntimeError(APL_ERR_ARG, "null flag arrays / counter");
+  DeviceGuard guard(mesh.device);
+  auto ex = get_exchange(mesh, src, tgt, meta);
+  NvtxRange range(ex->label.c_str());
+  PtrTable t{};
+  int align = std::min(natural_vec(ex->host_push), ptr_align(in));
+  t.src[0] = static_cast<const char*>(in);
+  for (int64_t i = 0; i < p; ++i) {
+    t.dst[i] = static_cast<char*>(peer_out[i]);
+    align = std::min(align, ptr_align(peer_out[i]));
+  }
+  PeerSync y{};
+  for (int64_t q = 0; q < p; ++q) {
+    if (q == mesh.rank) continue;
+    y.remote[y.n_remote++] = static_cast<uint32_t*>(sync.flags[q]);
+  }
+  // the receivers of this rank's pieces must have entered this epoch (their
+  // previous output is consumed) before it is overwritten
+  for (int r : ex->pull_readers) y.wait_slot[y.n_wait++] = r;
+  y.local = static_cast<const uint32_t*>(sync.local_flags);
+  y.counter = static_cast<unsigned int*>(sync.counter);
+  y.ready_slot = mesh.rank;
+  y.done_slot = static_cast<int32_t>(p) + mesh.rank;
+  y.mode = PeerSync::kAnnounce | PeerSync::kDone | PeerSync::kPush;
+  y.epoch = sync.epoch;
+  y.timeout_ns = sync.timeout_ns;
+  std::lock_guard<std::mutex> hold(mesh.mu);
+  auto it = ex->push.find(align);
+  if (it == ex->push.end())
+    it = ex->push.emplace(align, compile_copies(ex->host_push, align, false)).first;
+  const CompiledCopies& c = it->second;
+  check_cuda(launch_box_pull_sync(c.table, c.begins.data(), c.ntasks, c.total_units, c.vec,
+                                  c.max_outer, t, y, stream),
+             "peer push launch");
 }
 
 namespace {

@@ -179,7 +179,9 @@ struct Exchange {
                                       // piece straight from the senders' shards
   std::vector<int> pull_senders;      // peer mode: ranks this rank reads from (not itself)
   std::vector<int> pull_readers;      // peer mode: ranks that read this rank's source
-  std::map<int, CompiledCopies> copies, pre, post, pull;  // keyed by vector width
+  std::vector<CopyDesc> host_push;    // peer push mode: every piece this rank sends, stored
+                                      // straight into the receivers' outputs (dst id = rank)
+  std::map<int, CompiledCopies> copies, pre, post, pull, push;  // keyed by vector width
   struct Xfer {
     int peer;
     bool direct;  // straight from `in` / into `out` (contiguous box)
@@ -285,6 +287,17 @@ struct PeerSyncArgs {
 void run_pull_sync(Mesh& mesh, const autoplan::ShardingSpec& src,
                    const autoplan::ShardingSpec& tgt, const autoplan::TensorMeta& meta,
                    const void* const* peer_in, void* out, const PeerSyncArgs& sync,
+                   cudaStream_t stream);
+// Peer push: this rank stores every piece it sends straight into the
+// receivers' (peer-mapped, exported) outputs -- peer_out[q] = rank q's output
+// mapped here, peer_out[rank] = the local output -- in ONE launch that
+// announces `epoch` (this rank's output may now be overwritten), acquires the
+// announcements of the ranks it writes to, stores, and marks done (slot
+// P + rank) at every peer after a system-scope fence. The receiver waits for
+// done of its senders (apl_peer_flags_wait) before reading its output.
+void run_push_sync(Mesh& mesh, const autoplan::ShardingSpec& src,
+                   const autoplan::ShardingSpec& tgt, const autoplan::TensorMeta& meta,
+                   const void* in, void* const* peer_out, const PeerSyncArgs& sync,
                    cudaStream_t stream);
 
 size_t path_workspace(Mesh& mesh, const autoplan::ShardingSpec& src,

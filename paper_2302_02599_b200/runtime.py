@@ -533,6 +533,47 @@ class PeerMesh:
         self._last_readers = None
         return e
 
+    def push_output(self, nbytes: int):
+        """The exported output buffer push exchanges of this size write into:
+        (this rank's uint8 tensor, [rank q's buffer mapped here for every q]).
+        Collective on the first use of a size (shared_buffer)."""
+        key = -(-max(nbytes, 16) // 256) * 256
+        bufs = self.__dict__.setdefault("_push_bufs", {})
+        if key not in bufs:
+            local, ptrs = self.shared_buffer(key)
+            bufs[key] = (local, ptrs, (C.c_void_p * len(ptrs))(*ptrs))
+        return bufs[key]
+
+    def push_async(self, src: ShardingSpec, tgt: ShardingSpec, meta: TensorMeta,
+                   x: torch.Tensor, stream=None) -> torch.Tensor:
+        """The exchange as a PUSH (apl_run_push_sync): ONE kernel stores every
+        piece of this rank's source `x` (any local tensor) straight into the
+        receivers' exported outputs, after they announced this epoch, and
+        marks done at every peer after a system-scope fence; then this rank
+        waits (stream-ordered) for done of the ranks that write to it.
+        Returns this rank's output: a view of the push buffer, valid in
+        stream order until the next push of the same size. The source is
+        never read remotely, so it may be overwritten right after."""
+        if x.numel() * x.element_size() < src.per_device_bytes(meta, self.geo):
+            raise ValueError("source smaller than the shard")
+        nbytes = tgt.per_device_bytes(meta, self.geo)
+        local, _, table = self.push_output(nbytes)
+        self.epoch += 1
+        e, P = self.epoch, self.geo.num_devices()
+        sh = _stream_handle(stream)
+        senders, _ = self.exchange_peers(src, tgt, meta)
+        sync = A.PeerSyncC(self._all_flags, self.flags.data_ptr(), self._counter.data_ptr(), e,
+                           self.timeout_ms)
+        check(A.lib().apl_run_push_sync(self._h, C.byref(src.c()), C.byref(tgt.c()),
+                                        C.byref(meta.c()), C.c_void_p(x.data_ptr()), table,
+                                        C.byref(sync), sh))
+        if senders:
+            slots = (C.c_int32 * len(senders))(*[P + q for q in senders])
+            check(A.lib().apl_peer_flags_wait(C.c_void_p(self.flags.data_ptr()), slots,
+                                              len(senders), e, self.timeout_ms, sh))
+        self._last_readers = []  # nobody reads this rank's source remotely
+        return local[:nbytes]
+
     def shared_buffer(self, nbytes: int):
         """Collective: allocate and export a device buffer on every rank and
         map every peer's. Returns (this rank's buffer as a uint8 tensor,

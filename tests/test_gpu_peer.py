@@ -337,3 +337,75 @@ def test_fused_gemm_allreduce_over_axis_subsets(cuda, world):
             if r[1] == axes:
                 by_group.setdefault(r[4], set()).add(r[5])
         assert all(len(v) == 1 for v in by_group.values()), (axes, by_group)
+
+
+def _push_worker(rank, world, port, cases, q):
+    """Push exchanges (remote stores into the receivers' exported outputs),
+    synchronised only on the device, several epochs back to back with a
+    different source each epoch; every output checked against the oracle."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from oracle import data as O
+    from paper_2302_02599_b200 import ShardingSpec, TensorMeta
+    from paper_2302_02599_b200.runtime import PeerMesh
+
+    dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}
+    npdt = {1: np.uint8, 2: np.int16, 4: np.int32}
+    try:
+        for mesh_shape, shape, eb, a, b in cases:
+            mr = len(mesh_shape)
+            meta = TensorMeta(shape, eb)
+            pm = PeerMesh(mesh_shape, rank, 0, 16)
+            s, t = ShardingSpec.parse(a, mr), ShardingSpec.parse(b, mr)
+            pm.push_output(t.per_device_bytes(meta, pm.geo))  # collective allocation
+            srcs, wants = [], []
+            for e in range(EPOCHS):
+                g = O.fill_global(shape, eb, seed=2000 + e)
+                srcs.append(torch.from_numpy(O.local(g, O.parse_spec(a, mr), mesh_shape, rank)
+                                             .view(npdt[eb])).cuda())
+                wants.append(O.local(g, O.parse_spec(b, mr), mesh_shape, rank))
+            torch.cuda.synchronize()
+            dist.barrier()  # setup only
+            outs = []
+            for e in range(EPOCHS):
+                out = pm.push_async(s, t, meta, srcs[e])
+                outs.append(out.view(dt[eb]).clone())  # consume before the next epoch
+            torch.cuda.synchronize()
+            for e in range(EPOCHS):
+                q.put((rank, a, b, e, outs[e].cpu().numpy().tobytes() == wants[e].tobytes()))
+            dist.barrier()
+            pm.close()
+            dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+PUSH_CASES = {
+    4: EPOCH_CASES[4] + [([2, 2], (512, 256), 2, "RR", "S01R"), ([4], (64, 32), 2, "RS0", "S0R")],
+    8: EPOCH_CASES[8] + [([8], (2048, 256), 2, "S0R", "RR"), ([2, 4], (512, 512), 2, "S0S1", "RS01")],
+}
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_peer_push_exchange_epochs(cuda, world):
+    """apl_run_push_sync: the push form of the peer exchange (remote stores,
+    fan-out descriptors for replicated targets) against the oracle."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_push_worker, args=(r, world, port, PUSH_CASES[world], q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    res = []
+    while not q.empty():
+        res.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert len(res) == world * len(PUSH_CASES[world]) * EPOCHS
+    assert all(ok for *_, ok in res), [r for r in res if not r[-1]]

@@ -126,20 +126,29 @@ def main():
         c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
         flops = 2.0 * m * n * k
         iters = 3 if quick else 20
-        ms = time_fn(lambda: gemm(a, bt, out=c), iters)
-        ms_g = time_fn(lambda: gemm(a, bt, out=c, gelu=True), iters)
+        # device time: CUDA-graph replays (best of 5), both sides alike -- the
+        # per-call host cost (tensor-map encoding, ctypes; torch's dispatch)
+        # is reported separately as the eager figures
         b_kn = bt.t().contiguous()
-        ms_kn = time_fn(lambda: gemm(a, b_kn, out=c, b_layout="kn"), iters)
-        ms_cublas = time_fn(lambda: torch.matmul(a, bt.t(), out=c), iters)
+        fns = {"ours": lambda: gemm(a, bt, out=c),
+               "gelu": lambda: gemm(a, bt, out=c, gelu=True),
+               "kn": lambda: gemm(a, b_kn, out=c, b_layout="kn"),
+               "cublas": lambda: torch.matmul(a, bt.t(), out=c)}
+        dev = {k: min(graph_time(f) for _ in range(2)) for k, f in fns.items()}
+        eager = {k: time_fn(fns[k], iters) for k in ("ours", "cublas")}
         ref = (a.float() @ bt.float().t())
         err = ((gemm(a, bt).float() - ref).abs().max() / ref.abs().max()).item()
+        tf = lambda ms: round(flops / ms / 1e9, 1)  # noqa: E731
         out["rows"].append({
             "shape": name, "m": m, "n": n, "k": k,
-            "ours_ms": round(ms, 4), "ours_tflops": round(flops / ms / 1e9, 1),
-            "ours_gelu_tflops": round(flops / ms_g / 1e9, 1),
-            "ours_b_kn_tflops": round(flops / ms_kn / 1e9, 1),
-            "cublas_ms": round(ms_cublas, 4), "cublas_tflops": round(flops / ms_cublas / 1e9, 1),
-            "frac_of_peak": round(flops / ms / 1e9 / out["peak_tflops"], 3),
+            "ours_ms": round(dev["ours"], 4), "ours_tflops": tf(dev["ours"]),
+            "ours_gelu_tflops": tf(dev["gelu"]), "ours_b_kn_tflops": tf(dev["kn"]),
+            "cublas_ms": round(dev["cublas"], 4), "cublas_tflops": tf(dev["cublas"]),
+            "ours_vs_cublas": round(dev["cublas"] / dev["ours"], 3),
+            "ours_eager_tflops": tf(eager["ours"]), "cublas_eager_tflops": tf(eager["cublas"]),
+            "frac_of_peak": round(flops / dev["ours"] / 1e9 / out["peak_tflops"], 3),
+            "timing": "device: CUDA-graph replay of 20 back-to-back calls, best of 5 x 2; eager: "
+                      "20 launches from Python",
             "max_rel_err": err})
     print(json.dumps(out))
 

@@ -86,13 +86,15 @@ def main():
         for _ in range(3):
             conv(ins, outs, stream=stream)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.iters):
-            conv(ins, outs, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms_ = e0.elapsed_time(e1) / args.iters
+        ms_ = 1e30
+        for _ in range(2):  # best of two rounds: a sporadic stall on the box is not the kernel
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.iters):
+                conv(ins, outs, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_ = min(ms_, e0.elapsed_time(e1) / args.iters)
         conv.close()
         row = {"src": a, "tgt": b, "ref_steps": len(path.steps), "us": round(ms_ * 1e3, 2),
                "hbm_bytes": nbytes, "frac": round(nbytes / (ms_ * 1e-3) / 1e9 / peak, 4)}
