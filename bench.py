@@ -240,9 +240,19 @@ def run_ours_peer(args):
     torch.cuda.synchronize()
     dist.barrier()
 
+    push = args.transport == "push"
+
+    def xchg(c):
+        """One exchange of the peer transport: the fused pull (default) or the
+        push form (remote stores into the receivers' exported outputs)."""
+        if push:
+            return pm.push_async(s, c["tgt"], meta, src, stream=stream)
+        pm.exchange_async(s, c["tgt"], meta, c["out"], stream=stream)
+        return c["out"]
+
     def step():
         for c in convs:
-            pm.exchange_async(s, c["tgt"], meta, c["out"], stream=stream)
+            xchg(c)
 
     for _ in range(args.warmup):
         step()
@@ -258,7 +268,7 @@ def run_ours_peer(args):
         for _ in range(args.steps):
             for c in convs:
                 evs[k][0].record(stream)
-                pm.exchange_async(s, c["tgt"], meta, c["out"], stream=stream)
+                xchg(c)
                 evs[k][1].record(stream)
                 k += 1
         t1.record(stream)
@@ -275,7 +285,7 @@ def run_ours_peer(args):
     step_bus = sum(c["bus"] for c in convs)  # per rank (every rank receives the same)
     value = step_bus / (ms_per_step * 1e-3) / 1e9
     dom = max(convs, key=lambda c: per_ms[c["name"]])
-    roof = nvlink_roofline(f"box_copy pull kernel over peer pointers ({dom['name']})",
+    roof = nvlink_roofline(f"box_copy {'push' if push else 'pull'} kernel over peer pointers ({dom['name']})",
                            dom["bus"], per_ms[dom["name"]], gpus_shared)
     # e2e through the public API with host buffers: H2D of this rank's source
     # shard (after the readers of the last epoch finished), both exchanges,
@@ -289,8 +299,7 @@ def run_ours_peer(args):
         pm.wait_readers(stream=stream)
         src.copy_(host_in, non_blocking=True)
         for c, h in zip(convs, host_out):
-            pm.exchange_async(s, c["tgt"], meta, c["out"], stream=stream)
-            h.copy_(c["out"], non_blocking=True)
+            h.copy_(xchg(c).view(c["out"].dtype).view(c["out"].shape), non_blocking=True)
 
     for _ in range(2):
         e2e_step()
@@ -317,11 +326,13 @@ def run_ours_peer(args):
         "data": "synthetic (random bf16 bit patterns, torch.random_ on device)",
         "aggregate_bus_gbs": round(value * ws, 1), "bus_bytes_per_rank_per_step": int(step_bus),
         "config": {"workload": "configs[1]: mesh of N, S0R->RR all-gather + S0R->RS0 all-to-all",
-                   "tensor": list(shape), "mesh": [ws], "transport": "peer",
+                   "tensor": list(shape), "mesh": [ws], "transport": "push" if push else "peer",
                    "gpus_shared": gpus_shared,
-                   "mode": "one process per GPU, fused pull kernel over peer memory, "
-                           "device-side epoch flags",
-                   "path": "collapsed exchange (one pull kernel per rank)",
+                   "mode": ("one process per GPU, push kernel (remote stores) over peer memory, "
+                            "device-side epoch flags" if push else
+                            "one process per GPU, fused pull kernel over peer memory, "
+                            "device-side epoch flags"),
+                   "path": "collapsed exchange (one %s kernel per rank)" % ("push" if push else "pull"),
                    "l2": "per-GPU shard 128 MiB > L2", "parallelism": f"mesh[{ws}]"},
         "per_conversion_ms": {k: round(v_, 4) for k, v_ in per_ms.items()},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e,
@@ -1009,9 +1020,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs 3/4 mesh sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
-                    help="N > 1: fused peer-memory pull (default) or NCCL per mesh-axis "
-                         "communicator + pack/unpack kernels")
+    ap.add_argument("--transport", default="peer", choices=["peer", "push", "nccl"],
+                    help="N > 1: fused peer-memory pull (default), peer-memory push (remote "
+                         "stores), or NCCL per mesh-axis communicator + pack/unpack kernels")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     ws = dist_env()[0]
@@ -1022,7 +1033,7 @@ def main():
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn(args))
-    if ws > 1 and args.transport == "peer":
+    if ws > 1 and args.transport in ("peer", "push"):
         if not run_ours_peer(args):
             run_ours(args)
     else:
