@@ -406,8 +406,10 @@ int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, i
                   int64_t lda, int64_t ldb, int64_t ldc, int b_layout, int out_dtype,
                   int epilogue, void* stream);
 /* Force parts of every later GEMM's launch plan (-1 = automatic): pair != 0
- * the 2-CTA kernel (256-row tiles), bn the N tile (128 / 256), streamk != 0
- * the stream-K schedule. For A/B measurements; results do not change. */
+ * the 2-CTA kernel (256-row tiles), bn the N tile (128 / 256), streamk 1 the
+ * stream-K schedule, 2..4 aligned split-K by that factor (each unit one K
+ * slice of one tile). For A/B measurements; results do not change beyond
+ * fp32 summation order. */
 int apl_gemm_force_plan(int pair, int bn, int streamk);
 
 /* Grouped GEMM, one persistent launch: `groups` output problems, each the

@@ -945,8 +945,9 @@ int apl_matmul_strategies(const apl_mesh_desc* mesh, const apl_meta* a_meta,
 int apl_gemm_force_plan(int pair, int bn, int streamk) {
   return guarded([&] {
     need(pair >= -1 && pair <= 1 && (bn == -1 || bn == 128 || bn == 256) && streamk >= -1 &&
-             streamk <= 1,
-         "pair / streamk in {-1, 0, 1}, bn in {-1, 128, 256}");
+             streamk <= 4,
+         "pair in {-1, 0, 1}, bn in {-1, 128, 256}, streamk in {-1, 0, 1} or an aligned "
+         "split-K factor 2..4");
     apl::gemm_force_plan(pair, bn, streamk);
   });
 }

@@ -458,6 +458,7 @@ struct GemmArgs {
   // (box 32 rows x 128 bytes, 128B swizzle); 0 = per-lane st.global stores
   // (scatter_rows, unaligned outputs).
   int tma_out;
+  int sk_units;  // > 0: stream-K grid of exactly this many CTAs / clusters (aligned split-K)
   // pair kernel: 4-CTA clusters multicasting A across two pairs (A maps with
   // 64-row boxes)
   int a_mc;
@@ -1389,7 +1390,8 @@ cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
     return n > 0 ? n : 148;
   }();
   const int tiles = ((args.N + BN - 1) / BN) * ((args.M + kBM - 1) / kBM) * args.count;
-  const int grid = args.streamk ? sms : (tiles < sms ? tiles : sms);
+  const int grid = args.streamk ? (args.sk_units > 0 ? args.sk_units : sms)
+                                 : (tiles < sms ? tiles : sms);
   kernel<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return why(cudaGetLastError(), "gemm launch");
@@ -1450,7 +1452,9 @@ cudaError_t launch_pair_t(const GemmArgs& args, cudaStream_t stream) {
   }();
   const int tiles = ((args.N + BN - 1) / BN) *
                     ((args.M + 2 * pair::kBM - 1) / (2 * pair::kBM)) * args.count / (MC ? 2 : 1);
-  const int clusters = args.streamk ? max_clusters : std::min(tiles, max_clusters);
+  const int clusters = args.streamk ? (args.sk_units > 0 ? std::min(args.sk_units, max_clusters)
+                                                         : max_clusters)
+                                     : std::min(tiles, max_clusters);
   kernel<<<kCS * clusters, kThreads, pair::Cfg<BN>::kBytes, stream>>>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return why(cudaGetLastError(), "pair gemm launch");
@@ -1549,6 +1553,8 @@ struct GemmPlan {
   bool paired;   // CTA-pair (cta_group::2) kernel, 256-row tiles
   int bn;        // N tile: 128 or 256
   bool streamk;  // stream-K over (tile, k-block) instead of whole tiles
+  int split = 0; // > 1: aligned split-K -- stream-K over exactly tiles x split units, so
+                 // every unit is one K slice of one tile (one segment, one fixup)
 };
 
 // Relative per-SM throughput of each tile shape, calibrated on 8192^3 where
@@ -1562,10 +1568,31 @@ double tile_eff(bool paired, int bn) {
   return bn == 256 ? 0.8 : 0.62;
 }
 
+// APL_GEMM_SPLITK=<s>: force aligned split-K s (probe); APL_GEMM_SPLIT_AUTO=1
+// lets the cost model pick it (off: the per-lane fp32 partial exchange made
+// every split slower than whole tiles, profiles/r02_gemm_sweep_split.jsonl).
+int split_forced() {
+  static const int v = [] {
+    const char* e = std::getenv("APL_GEMM_SPLITK");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+bool split_auto() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_GEMM_SPLIT_AUTO");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // Cost model: per-SM work of a tile / its efficiency, times the waves of
 // tiles over the resident units (clusters for pairs, CTAs otherwise);
-// stream-K spreads the k-blocks evenly and pays ~8% for the fixup.
-// APL_GEMM_PAIR=0/1, APL_GEMM_BN=128/256, APL_GEMM_STREAMK=0/1 force parts.
+// stream-K spreads the k-blocks evenly and pays ~8% for the fixup; aligned
+// split-K s runs tiles x s one-segment units (one wave at most) and pays
+// ~10% for its fixup (fp32 partial tiles through L2).
+// APL_GEMM_PAIR=0/1, APL_GEMM_BN=128/256, APL_GEMM_STREAMK=0/1 force parts;
+// apl_gemm_force_plan's streamk >= 2 forces aligned split-K.
 GemmPlan plan_gemm(int M, int N, int K, int count, bool sk_allowed, bool pair_allowed) {
   static const int e_pair = [] {
     const char* e = std::getenv("APL_GEMM_PAIR");
@@ -1604,6 +1631,17 @@ GemmPlan plan_gemm(int M, int N, int K, int count, bool sk_allowed, bool pair_al
         if (cost < best_cost) {
           best_cost = cost;
           best = GemmPlan{paired != 0, bn, sk != 0};
+        }
+      }
+      // aligned split-K: only when the whole tiles leave units idle
+      const int fs = o_sk >= 2 ? o_sk : split_forced();
+      for (int split : {2, 4}) {
+        if (!sk_allowed || kb % split || kb / split < 4 || tiles * split > units) continue;
+        if (fs >= 2 ? split != fs : (f_sk >= 0 || fs == 0 || !split_auto())) continue;
+        const double cost = 1.1 * work / split;
+        if (cost < best_cost || fs >= 2) {
+          best_cost = cost;
+          best = GemmPlan{paired != 0, bn, true, split};
         }
       }
     }
@@ -1675,6 +1713,11 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
     if (epi >= kEpiDGelu)
       for (int i = 0; i < args.count; ++i) args.aux[i] = aux[first + i];
     if (plan.streamk && !streamk_attach(args, stream)) return cudaErrorMemoryAllocation;
+    if (plan.split > 1) {
+      const int64_t tm = paired ? 256 : 128;
+      args.sk_units = static_cast<int>(((M + tm - 1) / tm) * ((N + bn - 1) / bn) *
+                                       args.count * plan.split);
+    }
     cudaError_t e;
     if (paired && bn == 256)
       e = b_kn ? dispatch_pair<256, true>(args, out_f32, epi, a_km, stream)

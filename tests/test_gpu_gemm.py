@@ -211,9 +211,10 @@ def test_megatron_mlp_on_mesh8(cuda):
 
 
 # Every launch plan (1-CTA / CTA-pair kernel x N tile 128 / 256 x whole
-# tiles / stream-K, forced through apl_gemm_force_plan) on shapes that
-# under-fill the SMs, ragged tails and both B layouts.
-PLANS = [(p, bn, sk) for p in (0, 1) for bn in (128, 256) for sk in (0, 1)]
+# tiles / stream-K / aligned split-K 2 and 4, forced through
+# apl_gemm_force_plan) on shapes that under-fill the SMs, ragged tails and
+# both B layouts. A split the shape cannot take falls back to a whole-tile plan.
+PLANS = [(p, bn, sk) for p in (0, 1) for bn in (128, 256) for sk in (0, 1, 2, 4)]
 
 
 @pytest.fixture

@@ -83,8 +83,10 @@ def sweep():
 
     lib = A.lib()
     pk = peak()
-    plans = [("auto", -1, -1, -1)] + [(f"{'pair' if p else 'cta'}{bn}{'-sk' if sk else ''}", p, bn, sk)
-                                      for p in (0, 1) for bn in (128, 256) for sk in (0, 1)]
+    plans = [("auto", -1, -1, -1)] + [
+        (f"{'pair' if p else 'cta'}{bn}{'' if not sk else '-sk' if sk == 1 else f'-split{sk}'}",
+         p, bn, sk)
+        for p in (0, 1) for bn in (128, 256) for sk in (0, 1, 2, 4)]
     rounds = 3
     for name, m, n, k in SHAPES:
         a = torch.randn(m, k, device="cuda").bfloat16()
