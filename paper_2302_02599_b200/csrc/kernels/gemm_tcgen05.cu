@@ -398,6 +398,60 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
       : "memory");
 }
 
+// ---- stream-K / split-K fixup through TMA -------------------------------------
+// The fp32 partial tiles live in sk_ws, viewed by args.skmap as
+// [CTAs x 128 rows][BN cols] (32 x 32 fp32 boxes, 128B swizzle). A partial
+// CTA's warp stages its 32 rows x 32 columns and bulk-stores them; the head
+// TMA-loads each later CTA's box into the same staging and adds it from
+// shared memory. The per-lane float4 form scattered 32 rows per instruction
+// (~8k L2 requests per CTA each way) and made every split slower than whole
+// tiles (profiles/r02_gemm_sweep_split.jsonl).
+__device__ __forceinline__ void sk_store_chunk(const CUtensorMap* map, uint8_t* stage, int lane,
+                                               const uint32_t (&r)[32], int col, int row) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  epi_stage32<true>(stage, lane, 0, v);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map, stage, col, row);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+// every partial box written and visible (generic and async proxies) before
+// the CTA's flag is released
+__device__ __forceinline__ void sk_store_done(int lane) {
+  if (lane == 0)
+    asm volatile("cp.async.bulk.wait_group 0;\n\tfence.proxy.async.global;" ::: "memory");
+  __syncwarp();
+}
+// head: r += the 32 x 32 fp32 box of a partial tile at (col, row); the
+// staging must be free (no bulk store still reading it)
+__device__ __forceinline__ void sk_add_chunk(const CUtensorMap* map, uint8_t* stage,
+                                             uint64_t* bar, uint32_t& phase, int lane,
+                                             uint32_t (&r)[32], int col, int row) {
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_expect_tx(bar, 32 * 128);
+    tma_load_2d(stage, map, bar, col, row);
+  }
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+  const uint8_t* rowp = stage + lane * 128;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 p = *reinterpret_cast<const float4*>(rowp + ((q ^ (lane & 7)) << 4));
+    r[4 * q] = __float_as_uint(__uint_as_float(r[4 * q]) + p.x);
+    r[4 * q + 1] = __float_as_uint(__uint_as_float(r[4 * q + 1]) + p.y);
+    r[4 * q + 2] = __float_as_uint(__uint_as_float(r[4 * q + 2]) + p.z);
+    r[4 * q + 3] = __float_as_uint(__uint_as_float(r[4 * q + 3]) + p.w);
+  }
+  __syncwarp();  // every lane read the box before the next load overwrites it
+}
+
 template <int BN>
 struct Smem {
   static constexpr int kStageA = kBM * kBK * 2;
@@ -458,6 +512,8 @@ struct GemmArgs {
   // (box 32 rows x 128 bytes, 128B swizzle); 0 = per-lane st.global stores
   // (scatter_rows, unaligned outputs).
   int tma_out;
+  int sk_tma;             // stream-K fixup through args.skmap (TMA) instead of per-lane
+  CUtensorMap skmap;      // fp32 view of sk_ws: [CTAs x 128][BN]
   int sk_units;  // > 0: stream-K grid of exactly this many CTAs / clusters (aligned split-K)
   // pair kernel: 4-CTA clusters multicasting A across two pairs (A maps with
   // 64-row boxes)
@@ -512,6 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = empty + S::kStages;  // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2;       // [2] epilogue -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* pbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kEpiWarps] stream-K loads
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -529,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], kEpiWarps);  // one arrive per epilogue warp
     }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&pbar[w], 1);  // stream-K box loads
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int g = 0; g < args.count * args.reduce; ++g) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.a[g])) : "memory");
@@ -630,6 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp % 4;          // TMEM lanes this warp may access
     const int half = (warp - 2) / 4;       // which half of the tile's columns
     int local = 0;
+    uint32_t pphase = 0;  // this warp's stream-K box-load barrier phase
     SegIter seg(args.streamk != 0, blockIdx.x, gridDim.x, tiles, KT);
     int t, k0, k1;
     for (; seg.next(t, k0, k1); ++local) {
@@ -674,6 +733,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+      // head of a split tile, per-lane form: partial of CTA cc, columns [c, c+32)
+      auto add_one = [&](uint32_t (&r)[32], int c, int cc) {
+        const float4* w = reinterpret_cast<const float4*>(
+            args.sk_ws + (static_cast<size_t>(cc) * kBM + trow) * BN + c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 p = w[i];
+          r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + p.x);
+          r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + p.y);
+          r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + p.z);
+          r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + p.w);
+        }
+      };
       // head of a split tile: add the later CTAs' fp32 partials of columns [c, c+32)
       auto add_parts = [&](uint32_t (&r)[32], int c) {
         for (int cc = c_first; cc <= c_last; ++cc) {
@@ -690,21 +762,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       };
-      if (args.tma_out && !partial) {
-        uint8_t* stage = staging + (warp - 2) * kStageOut;
+      uint8_t* stage = staging + (warp - 2) * kStageOut;
+      if (partial && args.sk_tma) {  // raw accumulator to this CTA's partial tile
+#pragma unroll 1
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+          uint32_t r[32];
+          tmem_ld32(lane_addr + uint32_t(c), r);
+          sk_store_chunk(&args.skmap, stage, lane, r, c, static_cast<int>(blockIdx.x) * kBM + quarter * 32);
+        }
+        sk_store_done(lane);
+      } else if (args.tma_out && !partial) {
         constexpr int kCW = kOutF32 ? 32 : 64;  // columns per 128-byte staged row
 #pragma unroll 1
         for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += kCW) {
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();  // the previous box's store has read the staging
+          uint32_t r[kCW / 32][32];
+#pragma unroll
+          for (int p = 0; p < kCW / 32; ++p) tmem_ld32(lane_addr + uint32_t(c + 32 * p), r[p]);
+          if (head) {  // add the later CTAs' partials, in CTA order (deterministic)
+            for (int cc = c_first; cc <= c_last; ++cc) {
+              if (seg.total * cc / gridDim.x == seg.total * (cc + 1) / gridDim.x) continue;
+#pragma unroll
+              for (int p = 0; p < kCW / 32; ++p) {
+                if (args.sk_tma)
+                  sk_add_chunk(&args.skmap, stage, &pbar[warp - 2], pphase, lane, r[p],
+                               c + 32 * p, cc * kBM + quarter * 32);
+                else
+                  add_one(r[p], c + 32 * p, cc);
+              }
+            }
+          }
 #pragma unroll
           for (int p = 0; p < kCW / 32; ++p) {
-            uint32_t r[32];
-            tmem_ld32(lane_addr + uint32_t(c + 32 * p), r);
-            add_parts(r, c + 32 * p);
             float v[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[p][i]);
             epi_values32<kEpi>(v, row, n0 + c + 32 * p, rows, N, args.aux[g], args.ldaux);
             epi_stage32<kOutF32>(stage, lane, p, v);
           }
@@ -969,6 +1062,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
   uint64_t* acc_full = empty + S::kStages;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* pbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kEpiWarps] stream-K loads
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   constexpr int kCS = kMC ? 4 : 2;
@@ -996,6 +1090,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 2 * kEpiWarps);  // epilogue warps of both CTAs
     }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&pbar[w], 1);  // stream-K box loads
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int g = 0; g < args.count * args.reduce; ++g) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.a[g])) : "memory");
@@ -1098,6 +1193,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
     const int half = (warp - 2) / 4;
     const uint32_t acc_empty_leader = map_to_rank(smem_addr(&acc_empty[0]), pair_leader);
     int local = 0;
+    uint32_t pphase = 0;  // this warp's stream-K box-load barrier phase
     SegIter seg(sk, cluster, clusters, tiles, KT);
     int t, k0, k1;
     for (; seg.next(t, k0, k1); ++local) {
@@ -1126,6 +1222,18 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+      auto add_one = [&](uint32_t (&r)[32], int c, int cc) {
+        const float4* w = reinterpret_cast<const float4*>(
+            args.sk_ws + (static_cast<size_t>(2 * cc + rank) * kBM + trow) * BN + c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 p = w[i];
+          r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + p.x);
+          r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + p.y);
+          r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + p.z);
+          r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + p.w);
+        }
+      };
       auto add_parts = [&](uint32_t (&r)[32], int c) {
         for (int cc = c_first; cc <= c_last; ++cc) {
           if (seg.total * cc / clusters == seg.total * (cc + 1) / clusters) continue;
@@ -1141,21 +1249,42 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           }
         }
       };
-      if (args.tma_out && !partial) {
-        uint8_t* stage = staging + (warp - 2) * kStageOut;
+      uint8_t* stage = staging + (warp - 2) * kStageOut;
+      if (partial && args.sk_tma) {  // raw accumulator to this CTA's partial tile
+#pragma unroll 1
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+          uint32_t r[32];
+          tmem_ld32(lane_addr + uint32_t(c), r);
+          sk_store_chunk(&args.skmap, stage, lane, r, c, static_cast<int>(blockIdx.x) * kBM + quarter * 32);
+        }
+        sk_store_done(lane);
+      } else if (args.tma_out && !partial) {
         constexpr int kCW = kOutF32 ? 32 : 64;
 #pragma unroll 1
         for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += kCW) {
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
+          uint32_t r[kCW / 32][32];
+#pragma unroll
+          for (int p = 0; p < kCW / 32; ++p) tmem_ld32(lane_addr + uint32_t(c + 32 * p), r[p]);
+          if (head) {  // add the later CTAs' partials, in CTA order (deterministic)
+            for (int cc = c_first; cc <= c_last; ++cc) {
+              if (seg.total * cc / clusters == seg.total * (cc + 1) / clusters) continue;
+#pragma unroll
+              for (int p = 0; p < kCW / 32; ++p) {
+                if (args.sk_tma)
+                  sk_add_chunk(&args.skmap, stage, &pbar[warp - 2], pphase, lane, r[p],
+                               c + 32 * p, (2 * cc + static_cast<int>(rank)) * kBM + quarter * 32);
+                else
+                  add_one(r[p], c + 32 * p, cc);
+              }
+            }
+          }
 #pragma unroll
           for (int p = 0; p < kCW / 32; ++p) {
-            uint32_t r[32];
-            tmem_ld32(lane_addr + uint32_t(c + 32 * p), r);
-            add_parts(r, c + 32 * p);
             float v[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[p][i]);
             epi_values32<kEpi>(v, row, n0 + c + 32 * p, M, N, args.aux[g], args.ldaux);
             epi_stage32<kOutF32>(stage, lane, p, v);
           }
@@ -1529,7 +1658,9 @@ int sm_count_cached() {
 
 // Stream-K workspace: one fp32 128 x 256 partial tile and one flag per CTA,
 // kept per stream (partial tiles of one launch are consumed within it).
-bool streamk_attach(GemmArgs& args, cudaStream_t stream) {
+bool make_out_map(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, bool f32);
+
+bool streamk_attach(GemmArgs& args, cudaStream_t stream, int bn) {
   const int sms = sm_count_cached();
   static std::mutex mu;
   static std::map<cudaStream_t, StreamKWs> pool;
@@ -1545,6 +1676,8 @@ bool streamk_attach(GemmArgs& args, cudaStream_t stream) {
   args.streamk = 1;
   args.sk_ws = w.ws;
   args.sk_flags = w.flags;
+  // partial tiles as [CTAs x 128 rows][bn fp32 columns] for the TMA fixup
+  args.sk_tma = make_out_map(&args.skmap, w.ws, sms * kBM, bn, bn, true) ? 1 : 0;
   return true;
 }
 
@@ -1712,7 +1845,7 @@ cudaError_t gemm_bf16_grouped(const void* const* A, const void* const* B, void* 
     args.a_mc = mc ? 1 : 0;
     if (epi >= kEpiDGelu)
       for (int i = 0; i < args.count; ++i) args.aux[i] = aux[first + i];
-    if (plan.streamk && !streamk_attach(args, stream)) return cudaErrorMemoryAllocation;
+    if (plan.streamk && !streamk_attach(args, stream, bn)) return cudaErrorMemoryAllocation;
     if (plan.split > 1) {
       const int64_t tm = paired ? 256 : 128;
       args.sk_units = static_cast<int>(((M + tm - 1) / tm) * ((N + bn - 1) / bn) *
