@@ -5,9 +5,14 @@
 // node's plan spec, runs the forward pass and writes device 0's output
 // replica to <dir>/out.bin. With "train" it runs forward + backward against
 // <dir>/dy.bin and writes every parameter gradient to <dir>/grad_<id>.bin.
+// Distributed mode (env APL_TEST_RANK, APL_TEST_IDFILE = a 128-byte NCCL
+// unique id): this process is one rank of the mesh on the NCCL transport
+// (MeshRuntime::Distributed), feeds only its own shards and writes its
+// output replica / gradient shards as out_r<rank>.bin / grad_<id>_r<rank>.bin.
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -35,7 +40,16 @@ int main(int argc, char** argv) {
   const bool train = argc == 6 && std::string(argv[5]) == "train";
   const std::string dir = argv[4];
   const DeviceMesh mesh = DeviceMesh::uniform(parse_mesh_shape(argv[3]));
-  MeshRuntime rt = MeshRuntime::Simulated(mesh, 0);
+  const char* rank_env = std::getenv("APL_TEST_RANK");
+  const bool dist = rank_env != nullptr;
+  const int64_t my_rank = dist ? std::atoll(rank_env) : 0;
+  std::string nccl_id;
+  if (dist) nccl_id = slurp(std::getenv("APL_TEST_IDFILE"));
+  MeshRuntime rt = dist ? MeshRuntime::Distributed(
+                              mesh, static_cast<int>(my_rank),
+                              reinterpret_cast<const uint8_t*>(nccl_id.data()), 0)
+                        : MeshRuntime::Simulated(mesh, 0);
+  const std::string sfx = dist ? "_r" + std::to_string(my_rank) : "";
   PlanExecutor ex(rt, mesh, slurp(argv[1]), slurp(argv[2]));
   std::map<std::string, std::vector<const void*>> feeds;
   std::vector<void*> owned;
@@ -46,7 +60,7 @@ int main(int argc, char** argv) {
     const size_t rank = m.shape.size();
     const int64_t eb = m.dtype_bytes;
     std::vector<const void*> shards;
-    for (int64_t d = 0; d < mesh.num_devices(); ++d) {
+    for (int64_t d = dist ? my_rank : 0; d < (dist ? my_rank + 1 : mesh.num_devices()); ++d) {
       const auto c = mesh.coord_of(d);
       std::vector<int64_t> blk(rank, 0), loc(rank);
       int64_t total = 1;
@@ -89,7 +103,7 @@ int main(int argc, char** argv) {
   std::vector<void*> dys;
   if (train) {  // <dir>/dy.bin: the output gradient (global bf16), replicated
     const std::string dy = slurp(dir + "/dy.bin");
-    for (int64_t d = 0; d < mesh.num_devices(); ++d) {
+    for (int64_t d = 0; d < (dist ? 1 : mesh.num_devices()); ++d) {
       void* p = nullptr;
       cudaMalloc(&p, dy.size());
       cudaMemcpy(p, dy.data(), dy.size(), cudaMemcpyHostToDevice);
@@ -109,13 +123,14 @@ int main(int argc, char** argv) {
     std::fprintf(stderr, "copy-back failed\n");
     return 1;
   }
-  std::ofstream(dir + "/out.bin", std::ios::binary).write(host.data(), static_cast<long>(bytes));
+  std::ofstream(dir + "/out" + sfx + ".bin", std::ios::binary)
+      .write(host.data(), static_cast<long>(bytes));
   for (auto& [id, shards] : grads) {  // grad_<id>.bin: fp32 shards in device order
     const TensorMeta& m = ex.meta(id);
     TensorMeta m4 = m;
     m4.dtype_bytes = 4;
     const size_t sb = static_cast<size_t>(ex.spec(id).per_device_bytes(m4, mesh));
-    std::ofstream f(dir + "/grad_" + id + ".bin", std::ios::binary);
+    std::ofstream f(dir + "/grad_" + id + sfx + ".bin", std::ios::binary);
     std::vector<char> h(sb);
     for (void* p : shards) {
       cudaMemcpy(h.data(), p, sb, cudaMemcpyDeviceToHost);
@@ -124,6 +139,10 @@ int main(int argc, char** argv) {
   }
   for (void* p : dys) cudaFree(p);
   for (void* p : owned) cudaFree(p);
-  std::cout << "plan executed on " << mesh.num_devices() << " simulated devices\n";
+  if (dist)
+    std::cout << "plan executed as rank " << my_rank << " of " << mesh.num_devices()
+              << " over NCCL\n";
+  else
+    std::cout << "plan executed on " << mesh.num_devices() << " simulated devices\n";
   return 0;
 }
