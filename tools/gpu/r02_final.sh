@@ -12,4 +12,6 @@ timeout 600 python tools/mlp_bench.py > gpurun_out/mlp_bench_final.jsonl 2>&1
 timeout 600 python tools/block_bench.py > gpurun_out/block_bench_final.jsonl 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu > gpurun_out/bench_ncu_final.log 2>&1
 timeout 900 python tools/ncu_traffic.py > gpurun_out/ncu_traffic_final.log 2>&1
-echo ALLDONE
+
+timeout 900 ncu --set full --clock-control none -k regex:"box_copy|bulk_copy" -s 6 -c 2 --csv --page details python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu > gpurun_out/ncu_bench_details.csv 2> gpurun_out/ncu_bench_details.err
+echo ALLDONE2
