@@ -42,14 +42,18 @@ def test_memcheck_gemm(cuda):
     _run("memcheck", "gemm")
 
 
-def test_memcheck_block_ops(cuda):
-    _run("memcheck", "block")
+@pytest.mark.parametrize("engine", ["policy", "stream", "pipe"])
+def test_memcheck_block_ops(cuda, engine):
+    """every row op on each row engine (stream: TMA slabs, TMA-store
+    write-back for the softmaxes)"""
+    _run("memcheck", "block", {} if engine == "policy" else {"APL_ROW_ENGINE": engine})
 
 
 def test_memcheck_peer_exchange(cuda):
     _run("memcheck", "peer", {"CUDA_DEVICE_MAX_CONNECTIONS": "32"})
 
 
-@pytest.mark.parametrize("case,env", [("block", {}), ("copies", {"APL_COPY_ENGINE": "bulk"})])
+@pytest.mark.parametrize("case,env", [("block", {}), ("block", {"APL_ROW_ENGINE": "stream"}),
+                                      ("copies", {"APL_COPY_ENGINE": "bulk"})])
 def test_racecheck_shared_memory(cuda, case, env):
     _run("racecheck", case, env)

@@ -124,6 +124,20 @@ def block():
     B.softmax(s, p)
     assert (p.float() - torch.softmax(s.float(), -1)).abs().max().item() < 1e-2
     B.masked_softmax(s, p, alpha=0.125)
+    m = (torch.rand(4, 50, 64, device="cuda") < 0.3).to(torch.uint8)  # streamed + TMA stores
+    B.masked_softmax(s, p, 0.125, m, -1e4)
+    ref = torch.softmax(0.125 * s.float() - 1e4 * m.float(), -1)
+    assert (p.float() - ref).abs().max().item() < 1e-2
+    # general transpose (row-copy and tile kernels) and softmax over a middle axis
+    for perm in ((1, 0, 2), (2, 0, 1)):
+        q = torch.empty(tuple(s.shape[i] for i in perm), device="cuda").bfloat16()
+        B.permute(s, q, perm)
+        assert torch.equal(q, s.permute(perm))
+    sa = torch.empty_like(s)
+    B.softmax_axis(s, sa, 1)
+    assert (sa.float() - torch.softmax(s.float(), 1)).abs().max().item() < 1e-2
+    dsa = torch.empty_like(s)
+    B.softmax_axis_backward(sa, torch.randn_like(s), dsa, 1)
     ds = torch.empty_like(s)
     B.softmax_backward(p, torch.randn_like(s), ds, alpha=0.125)
     t = torch.empty(4, 64, 50, device="cuda").bfloat16()
