@@ -194,6 +194,21 @@ def peer():
         torch.cuda.synchronize()
         for o, w in zip(outs, want):
             assert o.cpu().numpy().tobytes() == w.tobytes(), (a, b)
+        # the push form: remote stores into every rank's output
+        pouts = [torch.full(t.local_shape(meta, geo), -1, dtype=torch.int16, device="cuda")
+                 for _ in range(P)]
+        ptable = (C.c_void_p * P)(*[x.data_ptr() for x in pouts])
+        torch.cuda.synchronize()
+        epoch += 1
+        for r in range(P):
+            sync = A.PeerSyncC(all_flags, flags[r].data_ptr(), counters[r].data_ptr(), epoch,
+                               30000)
+            check(lib.apl_run_push_sync(meshes[r], C.byref(s.c()), C.byref(t.c()),
+                                        C.byref(meta.c()), C.c_void_p(srcs[r].data_ptr()), ptable,
+                                        C.byref(sync), C.c_void_p(streams[r].cuda_stream)))
+        torch.cuda.synchronize()
+        for o, w in zip(pouts, want):
+            assert o.cpu().numpy().tobytes() == w.tobytes(), ("push", a, b)
     for h in meshes:
         lib.apl_mesh_destroy(h)
 
