@@ -115,6 +115,12 @@ class PlanExecutor:
     # elementwise-unary binding per node id: ("gelu",) | ("scale", alpha) | ("not",)
     unary: dict | None = None
     comm: list = field(default_factory=list)
+    # honour the plan's activation-checkpoint schedule (ckpt.cpp: Rotor
+    # decisions per chain stage): stages decided store_boundary / recompute
+    # drop what backward needs after the first forward pass and re-run from
+    # their block's boundary inputs when backward reaches them. False: store
+    # everything (same bytes, more memory).
+    checkpoint: bool = True
     _saved: dict = None
 
     def __post_init__(self):
@@ -150,6 +156,7 @@ class PlanExecutor:
                 self._consumers.setdefault(src, []).append((n["id"], slot))
         self._paths = {}
         self._convs = {}
+        self._block_of, self._blocks = self._checkpoint_blocks()
         self._attn = self._attention_chains()
         self._attn_members = {m for ch in self._attn.values() for m in ch[1:3]}
 
@@ -237,12 +244,37 @@ class PlanExecutor:
             out[sm] = (sm, u, b, x, m, self.unary_op(u)[1])
         return out
 
+    def _checkpoint_blocks(self):
+        """node id -> recompute block index, and block -> member ids in graph
+        order, from plan["schedule"] (block_index: maximal runs of stages
+        decided store_boundary / recompute, ckpt.cpp; -1 = stored in full)
+        and plan["stages"] (each stage's member nodes)."""
+        sched, stages = self.plan.get("schedule"), self.plan.get("stages")
+        if not self.checkpoint or not sched or not stages:
+            return {}, {}
+        block_of = {}
+        for st in stages:
+            b = sched["block_index"][st["index"]]
+            if b >= 0:
+                for m in st["members"]:
+                    block_of[m] = b
+        order = [n["id"] for n in self.graph["nodes"]]
+        blocks = {}
+        for nid in order:
+            if nid in block_of:
+                blocks.setdefault(block_of[nid], []).append(nid)
+        return block_of, blocks
+
     def _fusable_gelu(self, mm: str):
-        """The GELU node fused into matmul `mm`'s epilogue, if any."""
+        """The GELU node fused into matmul `mm`'s epilogue, if any (never
+        across a checkpoint-block boundary: a recomputed GELU re-reads its
+        producer's output)."""
         cons = self._consumers.get(mm, [])
         if len(cons) != 1 or mm in self.partial or self.nodes[mm]["kind"] != "matmul":
             return None
         gid, _ = cons[0]
+        if self._block_of.get(mm) != self._block_of.get(gid):
+            return None
         g = self.nodes[gid]
         if (g["kind"] == "elementwise-unary" and self.spec[gid] == self.spec[mm]
                 and self.unary_op(gid) == ("gelu",)):
@@ -329,21 +361,28 @@ class PlanExecutor:
         conv(shards, outs, stream=stream)
         return outs
 
-    def forward(self, feeds: dict, stream=None, train: bool = False) -> list:
+    def forward(self, feeds: dict, stream=None, train: bool = False, _only=None,
+                _values=None) -> list:
         """feeds: global tensors for every placeholder and parameter, or
         already-sharded lists (node id -> list of local shards).
         train=True keeps what backward() needs: every matmul's operands in
         the layouts its strategy consumed them, and every GELU's input (the
-        fused GELU's epilogue then also stores its pre-activation)."""
+        fused GELU's epilogue then also stores its pre-activation) -- except
+        for the stages the plan's checkpoint schedule recomputes, whose state
+        is dropped after the pass and rebuilt by backward (_only / _values:
+        that recompute: only these nodes, from these boundary values)."""
         from .runtime import gelu
 
-        values, converted, fused = {}, {}, set()
-        self._saved = {} if train else None
-        begin = getattr(self.mesh, "begin_step", None)
-        if begin is not None:  # recycle a per-step allocator (peer runtime heap)
-            begin(stream)
+        values, converted, fused = dict(_values or {}), {}, set()
+        if _only is None:
+            self._saved = {} if train else None
+            begin = getattr(self.mesh, "begin_step", None)
+            if begin is not None:  # recycle a per-step allocator (peer runtime heap)
+                begin(stream)
         for n in self.graph["nodes"]:
             nid, kind = n["id"], n["kind"]
+            if _only is not None and nid not in _only:
+                continue
             if kind in ("placeholder", "parameter"):
                 v = feeds[nid]
                 values[nid] = v if isinstance(v, list) else self.shard(nid, v)
@@ -428,7 +467,28 @@ class PlanExecutor:
                         self._saved[nid] = values[nid]
             else:
                 raise NotImplementedError(kind)
+        if _only is not None:
+            return None
+        if train and self._blocks:
+            # checkpointed stages: keep each block's boundary inputs, drop the
+            # backward state of its members (rebuilt by _recompute_block)
+            self._ckpt_values = {}
+            for members in self._blocks.values():
+                inside = set(members)
+                for m in members:
+                    for src, _ in self.nodes[m]["inputs"]:
+                        if src not in inside:
+                            self._ckpt_values[src] = values[src]
+                    self._saved.pop(m, None)
+            self._recomputed = set()
         return values[self.graph["output"]]
+
+    def _recompute_block(self, b: int, stream) -> None:
+        """Re-run checkpoint block b's forward from its boundary values,
+        keeping what backward needs (the schedule's second f_all pass)."""
+        self.forward(None, stream=stream, train=True, _only=set(self._blocks[b]),
+                     _values=self._ckpt_values)
+        self._recomputed.add(b)
 
     def _block_node(self, n: dict, ins: list, stream) -> list:
         """One transformer-block node on every local shard (module docstring)."""
@@ -698,15 +758,22 @@ class PlanExecutor:
             k = self.nodes[nid]["kind"]
             return k not in ("placeholder", "parameter") or k in kinds
 
+        def ensure(nid):  # a checkpointed node's backward state, recomputed on demand
+            b = self._block_of.get(nid)
+            if b is not None and b not in self._recomputed:
+                self._recompute_block(b, stream)
+
         for n in reversed(self.graph["nodes"]):
             nid, kind = n["id"], n["kind"]
             if nid in done or nid not in grads:
                 continue
             dy = grads[nid]
+            ensure(nid)
             if kind == "matmul":
                 st = self.strategy[nid]
                 a_saved, b_saved = self._saved[nid]
                 a_src, b_src = n["inputs"][0][0], n["inputs"][1][0]
+                ensure(a_src)  # a GELU feeding A: its saved input decides the fusion
                 a_meta, b_meta = self._meta(a_src), self._meta(b_src)
                 # GELU producing A in A's layout: its backward rides the dA epilogue.
                 aux, a_target = None, a_src

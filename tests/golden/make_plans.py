@@ -155,7 +155,7 @@ def main():
     out.mkdir(exist_ok=True)
     (out / "gpt2_mlp_graph.json").write_text(json.dumps(g, indent=1))
     for mesh in ([8], [2, 4], [2, 2, 2]):
-        for budget_mib in (0, 96, 192):
+        for budget_mib in (0, 88, 96, 192):  # 88: Rotor checkpoints fc1/gelu
             budget = (budget_mib << 20) if budget_mib else (1 << 40)
             name = f"gpt2_mlp_mesh{'x'.join(map(str, mesh))}_{budget_mib or 'unlimited'}"
             try:
@@ -170,7 +170,8 @@ def main():
     fixture = json.loads(Path("/root/reference/proj/tests/fixtures/gpt_block.json").read_text())
     blocks = {"fixture": (fixture, ([2, 2], [4], [2, 4], [8]), (0,)),
               "b8s1024": (block_graph(), ([8], [2, 4], [2, 2, 2]), (0,)),
-              "b4s1024": (block_graph(b=4), ([8], [2, 4], [2, 2, 2]), (0,)),
+              # 100 MiB on [8]: the attention stage is checkpointed (store_boundary)
+              "b4s1024": (block_graph(b=4), ([8], [2, 4], [2, 2, 2]), (0, 100)),
               "b1s4096": (block_graph(b=1, s=4096), ([8], [2, 4], [2, 2, 2]), (0,))}
     for tag, (g, meshes, budgets) in blocks.items():
         (out / f"gpt_block_{tag}_graph.json").write_text(json.dumps(g, indent=1))

@@ -85,3 +85,33 @@ def test_unnamed_unary_is_rejected_unless_bound():
     ex2 = PlanExecutor(_GeoOnly(plan["mesh"]["shape"]), graph, plan,
                        unary={"mystery": ("scale", 0.125)})
     assert ex2.unary_op("mystery") == ("scale", 0.125)
+
+
+@pytest.mark.parametrize("path", ["gpt2_mlp_mesh8_88.json", "gpt2_mlp_mesh2x4_88.json",
+                                  "gpt_block_b4s1024_mesh8_100.json"])
+def test_checkpoint_blocks_follow_the_schedule(path):
+    """Recompute blocks (executor._checkpoint_blocks) are exactly the stages
+    the reference schedule marks with a block index (ckpt.cpp decisions
+    store_boundary / recompute), members in graph order; checkpoint=False
+    (or a store_all schedule) has none."""
+    plan = json.loads((PLANS / path).read_text())
+    tag = path.split("_mesh")[0]
+    graph = GRAPH if tag == "gpt2_mlp" else json.loads((PLANS / f"{tag}_graph.json").read_text())
+    ex = PlanExecutor(_GeoOnly(plan["mesh"]["shape"]), graph, plan)
+    sched = plan["schedule"]
+    want = {}
+    for st in plan["stages"]:
+        b = sched["block_index"][st["index"]]
+        if b >= 0:
+            want.setdefault(b, set()).update(st["members"])
+    assert want and {b: set(m) for b, m in ex._blocks.items()} == want
+    order = [n["id"] for n in graph["nodes"]]
+    for ms in ex._blocks.values():
+        assert ms == sorted(ms, key=order.index)
+    if tag == "gpt2_mlp":
+        assert set(ex._blocks[0]) == {"fc1", "gelu"}
+        assert ex._fusable_gelu("fc1") == "gelu"  # same block: still fused
+    assert not PlanExecutor(_GeoOnly(plan["mesh"]["shape"]), graph, plan,
+                            checkpoint=False)._blocks
+    store_all = json.loads((PLANS / "gpt2_mlp_mesh8_unlimited.json").read_text())
+    assert not PlanExecutor(_GeoOnly([8]), GRAPH, store_all)._blocks
