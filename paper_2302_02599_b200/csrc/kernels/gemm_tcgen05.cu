@@ -452,6 +452,18 @@ __device__ __forceinline__ void sk_add_chunk(const CUtensorMap* map, uint8_t* st
   __syncwarp();  // every lane read the box before the next load overwrites it
 }
 
+// Programmatic dependent launch: everything above this point (barrier init,
+// TMEM allocation, tensor-map prefetch) overlaps the previous kernel's tail;
+// no global memory is touched before the wait, which returns once the
+// prerequisite grid has completed and its writes are visible. The dependents
+// are released at once: the grid is persistent, so every CTA is resident by
+// the time all have executed this. Both are no-ops without the launch
+// attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <int BN>
 struct Smem {
   static constexpr int kStageA = kBM * kBK * 2;
@@ -603,6 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_enter();
 
   const int KT = kblocks * args.reduce;
   if (warp == 0) {
@@ -1107,6 +1120,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
   cluster_sync();  // barriers initialised in both CTAs before any remote use
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_enter();
 
   if (warp == 0) {
     // TMA producer: whole warp, incremental K position, one elected lane issues
@@ -1489,6 +1503,32 @@ bool tma_out_enabled() {
   return on;
 }
 
+// APL_GEMM_PDL=0: launch without the programmatic-serialization attribute
+// (the kernel's griddepcontrol instructions are then no-ops).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_GEMM_PDL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <typename Kernel>
+cudaError_t launch_gemm_kernel(Kernel kernel, int grid, int smem, cudaStream_t stream,
+                               const GemmArgs& args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args);
+}
+
 // Fill args.cmap for outputs c[0 .. n) when every one can take TMA stores.
 void attach_out_maps(GemmArgs& args, int n, bool out_f32) {
   args.tma_out = 0;
@@ -1521,9 +1561,9 @@ cudaError_t launch_gemm(const GemmArgs& args, cudaStream_t stream) {
   const int tiles = ((args.N + BN - 1) / BN) * ((args.M + kBM - 1) / kBM) * args.count;
   const int grid = args.streamk ? (args.sk_units > 0 ? args.sk_units : sms)
                                  : (tiles < sms ? tiles : sms);
-  kernel<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(args);
+  cudaError_t e = launch_gemm_kernel(kernel, grid, Smem<BN>::kBytes, stream, args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return why(cudaGetLastError(), "gemm launch");
+  return why(e, "gemm launch");
 }
 
 template <int BN, bool BMN>
@@ -1584,9 +1624,9 @@ cudaError_t launch_pair_t(const GemmArgs& args, cudaStream_t stream) {
   const int clusters = args.streamk ? (args.sk_units > 0 ? std::min(args.sk_units, max_clusters)
                                                          : max_clusters)
                                      : std::min(tiles, max_clusters);
-  kernel<<<kCS * clusters, kThreads, pair::Cfg<BN>::kBytes, stream>>>(args);
+  cudaError_t e = launch_gemm_kernel(kernel, kCS * clusters, pair::Cfg<BN>::kBytes, stream, args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return why(cudaGetLastError(), "pair gemm launch");
+  return why(e, "pair gemm launch");
 }
 
 // args.a_mc: A maps built with 64-row boxes for the multicast cluster kernel.
