@@ -3,6 +3,7 @@ torch.matmul (cuBLAS) and the measured bf16 peak; prints one JSON object.
 
     python tools/gemm_bench.py [--quick]
     python tools/gemm_bench.py --sweep     # every launch plan per shape (JSON lines)
+    python tools/gemm_bench.py --sweep --gelu --only "fc1"   # GELU epilogue, shape filter
 
 --sweep forces each plan (apl_gemm_force_plan: 1-CTA / CTA-pair kernel,
 N tile 128 / 256, whole tiles / stream-K) on every shape and prints one line
@@ -88,7 +89,11 @@ def sweep():
          p, bn, sk)
         for p in (0, 1) for bn in (128, 256) for sk in (0, 1, 2, 4)]
     rounds = 3
+    use_gelu = "--gelu" in sys.argv
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else ""
     for name, m, n, k in SHAPES:
+        if only not in name:
+            continue
         a = torch.randn(m, k, device="cuda").bfloat16()
         bt = torch.randn(n, k, device="cuda").bfloat16()
         c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
@@ -100,7 +105,8 @@ def sweep():
                                  graph_time(lambda: torch.matmul(a, bt.t(), out=c)))
             for pname, p, bn, sk in plans:
                 assert lib.apl_gemm_force_plan(p, bn, sk) == 0
-                best[pname] = min(best.get(pname, 1e30), graph_time(lambda: gemm(a, bt, out=c)))
+                best[pname] = min(best.get(pname, 1e30),
+                                  graph_time(lambda: gemm(a, bt, out=c, gelu=use_gelu)))
         for pname, p, bn, sk in [("cublas", 0, 0, 0)] + plans:
             err = None
             if pname != "cublas":
@@ -109,6 +115,7 @@ def sweep():
                 err = ((out - ref).abs().max() / ref.abs().max()).item()
             ms = best[pname]
             print(json.dumps({"shape": name, "m": m, "n": n, "k": k, "plan": pname,
+                              "epilogue": "gelu" if use_gelu and pname != "cublas" else "none",
                               "ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1),
                               "frac_of_peak": round(flops / ms / 1e9 / pk, 3),
                               "vs_cublas": round(best["cublas"] / ms, 3), "max_rel_err": err}),
