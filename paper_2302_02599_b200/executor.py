@@ -252,6 +252,11 @@ class PlanExecutor:
         sched, stages = self.plan.get("schedule"), self.plan.get("stages")
         if not self.checkpoint or not sched or not stages:
             return {}, {}
+        if getattr(self.mesh, "empty", None) is not None:
+            # a per-step bump allocator (the peer runtime's symmetric heap)
+            # frees nothing before the next step: dropping saved state would
+            # save no memory and the recompute would take more heap
+            return {}, {}
         block_of = {}
         for st in stages:
             b = sched["block_index"][st["index"]]

@@ -115,3 +115,16 @@ def test_checkpoint_blocks_follow_the_schedule(path):
                             checkpoint=False)._blocks
     store_all = json.loads((PLANS / "gpt2_mlp_mesh8_unlimited.json").read_text())
     assert not PlanExecutor(_GeoOnly([8]), GRAPH, store_all)._blocks
+
+
+def test_checkpoint_off_on_bump_allocator_meshes():
+    """A mesh with its own per-step allocator (the peer runtime's symmetric
+    heap) frees nothing mid-step, so the executor stores everything there."""
+    plan = json.loads((PLANS / "gpt2_mlp_mesh8_88.json").read_text())
+
+    class _HeapMesh(_GeoOnly):
+        def empty(self, shape, dtype):  # pragma: no cover - never called here
+            raise AssertionError
+
+    assert PlanExecutor(_GeoOnly([8]), GRAPH, plan)._blocks
+    assert not PlanExecutor(_HeapMesh([8]), GRAPH, plan)._blocks
