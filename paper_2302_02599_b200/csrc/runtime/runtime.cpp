@@ -170,6 +170,45 @@ bool tile_auto_enabled() {
   return on;
 }
 
+// APL_TILE_AUTO=0: never pick the tiles automatically (not even by the
+// deep-box rule below).
+bool tile_rule_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("APL_TILE_AUTO");
+    return e == nullptr || std::string(e) != "0";
+  }();
+  return on;
+}
+
+// The deep-box rule: tables whose bytes mostly sit in descriptors with two
+// or more outer dims left after merging and short runs. The LDG kernel
+// resolves every 16-byte chunk through one FastDiv per level (~157
+// instructions per chunk at NO = 2 against ~117 at NO = 1, ncu), and on
+// these boxes it stalls at 0.65-0.69 of the copy peak where the tensor
+// tiles move a whole box per TMA instruction. Every-pair sweep of the
+// rank-3 2x2x2 mesh, tiles vs LDG (profiles/r02_pairs_222_r3_*.jsonl):
+//   129-256 B runs: tiles ahead on 1,530 of 1,557 such pairs, +13% mean;
+//   65-128 B runs: ahead only when the source rows are dense and the
+//     destination is strided (strided 128 B reads: -14% worst);
+//   <= 64 B runs: no rule (strided 64 B writes on tiles lose up to 35%).
+bool deep_short_box(const CopyDesc& d) {
+  if (d.nouter < 2) return false;
+  const int64_t inner = d.nouter - 1;  // ext/stride index of the innermost outer dim
+  if (d.run_bytes > 128 && d.run_bytes <= 256) return true;
+  return d.run_bytes > 64 && d.run_bytes <= 128 && d.src_stride[inner] == d.run_bytes &&
+         d.dst_stride[inner] != d.run_bytes;
+}
+
+bool deep_short_boxes(const std::vector<CopyDesc>& descs) {
+  int64_t deep = 0, all = 0;
+  for (const CopyDesc& d : descs) {
+    const int64_t b = d.bytes();
+    all += b;
+    if (deep_short_box(d)) deep += b;
+  }
+  return all > 0 && 2 * deep >= all;
+}
+
 }  // namespace
 
 int64_t copy_read_bytes(const std::vector<CopyDesc>& descs) {
@@ -330,7 +369,7 @@ bool tile_eligible(const std::vector<CopyDesc>& descs, int vec) {
   // ramp) loses to the LDG kernel's small-launch variant (16 MiB 256 B-run
   // all-to-all: 8.3 vs 13.8 us; profiles/r01_crossover.jsonl)
   if (forced != 2 && copy_read_bytes(descs) < kTileMinBytes) return false;
-  return forced == 2 || tile_auto_enabled();
+  return forced == 2 || tile_auto_enabled() || (tile_rule_enabled() && deep_short_boxes(descs));
 }
 
 CompiledCopies compile_copies(const std::vector<CopyDesc>& descs, int vec, bool bulk, bool tile) {
