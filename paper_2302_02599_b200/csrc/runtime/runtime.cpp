@@ -156,7 +156,8 @@ constexpr int64_t kSmallCopyBytes = int64_t{8} << 20;   // below: LDG small-laun
 constexpr int64_t kFanRingMaxBytes = int64_t{64} << 20;  // fan-out gathers on the ring below
 constexpr int64_t kTileMinBytes = int64_t{64} << 20;     // TMA tensor tiles from (when on)
 
-// The tile engine's place in the automatic policy: off unless APL_TILE_AUTO=1.
+// The tile engine's place in the automatic policy: the deep-box rule below
+// (r02), or every eligible table with APL_TILE_AUTO=1.
 // r01 short-row probe (profiles/r01_short_row_probe.jsonl): for strided rows
 // of 64 B - 1 KiB the LDG kernel at U=4 @ 4 CTAs/SM matches the tensor tiles
 // at 128 MiB (0.84 vs 0.85) and beats them from 512 MiB (0.92 vs 0.88 at
