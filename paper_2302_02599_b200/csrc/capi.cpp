@@ -952,6 +952,10 @@ int apl_gemm_force_plan(int pair, int bn, int streamk) {
   });
 }
 
+int apl_gemm_trace(void* buf) {
+  return guarded([&] { apl::gemm_trace(buf); });
+}
+
 int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                   int64_t lda, int64_t ldb, int64_t ldc, int b_layout, int out_dtype,
                   int epilogue, void* stream) {

@@ -625,8 +625,24 @@ struct GemmArgs {
   // pair kernel: 4-CTA clusters multicasting A across two pairs (A maps with
   // 64-row boxes)
   int a_mc;
+  // diagnostics (apl_gemm_trace): per-CTA timestamps of the kernel's phases,
+  // kTraceSlots per CTA; nullptr in normal runs
+  unsigned long long* trace;
   CUtensorMap cmap[kMaxBatch];
 };
+
+constexpr int kTraceSlots = 16;
+// slot 0: %globaltimer at entry; 1..: clock64 at entry, after the prologue,
+// after griddepcontrol.wait, first TMA issued, first stage landed (MMA
+// issuer), last accumulator committed, last accumulator drained by epilogue
+// warp 0, its last store issued, its bulk stores done, teardown start, exit
+__device__ __forceinline__ void trace_mark(unsigned long long* trace, int slot) {
+  if (trace != nullptr) {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    trace[blockIdx.x * kTraceSlots + slot] = static_cast<unsigned long long>(c);
+  }
+}
 
 // Segments of the (tile, k-block) iteration space a CTA processes, in order.
 struct SegIter {
@@ -1158,6 +1174,12 @@ template <int BN, int kEpi, bool kOutF32, bool kBMN, bool kAMN, bool kMC>
 __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ GemmArgs args) {
   using S = Cfg<BN>;
+  if (args.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    args.trace[blockIdx.x * kTraceSlots] = g;
+    trace_mark(args.trace, 1);
+  }
   const int M = args.M, N = args.N, K = args.K, ldc = args.ldc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -1215,7 +1237,9 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
   cluster_sync();  // barriers initialised in both CTAs before any remote use
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) trace_mark(args.trace, 2);
   pdl_enter();
+  if (threadIdx.x == 0) trace_mark(args.trace, 3);
 
   if (warp == 0) {
     // TMA producer: whole warp, incremental K position, one elected lane issues
@@ -1235,8 +1259,11 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           const CUtensorMap* map_b = &args.b[g * args.reduce + r];
           const int s = it % S::kStages;
           const uint32_t phase = (it / S::kStages) & 1;
+          if (it == 0 && lane == 0) trace_mark(args.trace, 12);
           mbar_wait(&empty[s], phase ^ 1);
+          if (it == 0 && lane == 0) trace_mark(args.trace, 13);
           if (leader) mbar_expect_tx_e(&full[s], 2 * (S::kStageA + S::kStageB));
+          if (it == 0 && lane == 0) trace_mark(args.trace, 14);
           if constexpr (kMC) {  // this CTA's 64-row half of the A rows, to both pairs
             if constexpr (kAMN)
               tma_load_2d_pair_mc_e(tiles_a + s * S::kStageA + pid * 8192, map_a, &full[s],
@@ -1251,6 +1278,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           } else {
             tma_load_2d_pair_e(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
           }
+          if (it == 0 && lane == 0) trace_mark(args.trace, 15);
           if constexpr (kBMN) {
 #pragma unroll
             for (int j = 0; j < (BN / 2) / 64; ++j)
@@ -1260,6 +1288,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
             tma_load_2d_pair_e(tiles_b + s * S::kStageB, map_b, &full[s], kb * kBK, n0);
           }
           if (!leader) remote_arrive_e(full_leader0 + s * 8);
+          if (it == 0 && lane == 0) trace_mark(args.trace, 4);
           if (++kb == kblocks) {
             kb = 0;
             ++r;
@@ -1284,6 +1313,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           const int s = it % S::kStages;
           mbar_wait(&full[s], (it / S::kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (it == 0 && lane == 0) trace_mark(args.trace, 5);
           const uint64_t da = da0 + uint64_t(s) * (S::kStageA >> 4);
           const uint64_t db = db0 + uint64_t(s) * (S::kStageB >> 4);
           constexpr uint64_t kAdvA = kAMN ? (16 * 128) >> 4 : 2;
@@ -1295,6 +1325,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           commit_pair_elect(&empty[s], kMC ? 0b1111 : 0b11);  // kMC: the other pair's stage too
         }
         commit_pair_elect(&acc_full[acc], static_cast<uint16_t>(0b11u << (2 * pid)));
+        if (lane == 0) trace_mark(args.trace, 6);
       }
     }
   } else {
@@ -1330,6 +1361,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
       }
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (warp == 2 && lane == 0) trace_mark(args.trace, 7);
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
       auto add_one = [&](uint32_t (&r)[32], int c, int cc) {
         const float4* w = reinterpret_cast<const float4*>(
@@ -1403,6 +1435,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
             for (int j = 0; j < args.fan; ++j)
               tma_store_2d(&args.cmap[g * args.fan + j], stage, n0 + c, m0 + quarter * 32);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (warp == 2) trace_mark(args.trace, 8);
           }
         }
       } else {
@@ -1443,20 +1476,26 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (warp == 2 && lane == 0) trace_mark(args.trace, 9);
   }
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (threadIdx.x == 0) trace_mark(args.trace, 10);
   cluster_sync();  // peer done with our barriers / TMEM before teardown
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(S::kTmemCols));
+    if (lane == 0) trace_mark(args.trace, 11);
   }
 }
 
 }  // namespace pair
 
 // ---- host side ---------------------------------------------------------------
+
+// apl_gemm_trace's buffer (nullptr: off).
+std::atomic<unsigned long long*> g_trace{nullptr};
 
 // APL_DEBUG=1: say which step of a GEMM launch failed (stderr).
 bool debug_on() {
@@ -1719,7 +1758,15 @@ cudaError_t launch_pair_t(const GemmArgs& args, cudaStream_t stream) {
   const int clusters = args.streamk ? (args.sk_units > 0 ? std::min(args.sk_units, max_clusters)
                                                          : max_clusters)
                                      : std::min(tiles, max_clusters);
-  cudaError_t e = launch_gemm_kernel(kernel, kCS * clusters, pair::Cfg<BN>::kBytes, stream, args);
+  unsigned long long* tr = g_trace.load();
+  cudaError_t e;
+  if (tr != nullptr) {
+    GemmArgs traced = args;
+    traced.trace = tr;
+    e = launch_gemm_kernel(kernel, kCS * clusters, pair::Cfg<BN>::kBytes, stream, traced);
+  } else {
+    e = launch_gemm_kernel(kernel, kCS * clusters, pair::Cfg<BN>::kBytes, stream, args);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return why(e, "pair gemm launch");
 }
@@ -2061,6 +2108,10 @@ cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K
 
 // Force parts of the GEMM plan (-1: automatic): the CTA pair kernel, the N
 // tile, stream-K. For A/B measurements (tools/gemm_bench.py --sweep).
+// Diagnostics: CTA-pair GEMM launches record per-CTA phase timestamps into
+// `buf` (kTraceSlots u64 per CTA; nullptr turns it off).
+void gemm_trace(void* buf) { g_trace.store(static_cast<unsigned long long*>(buf)); }
+
 void gemm_force_plan(int pair, int bn, int streamk) {
   g_force_pair.store(pair);
   g_force_bn.store(bn);
