@@ -1234,7 +1234,11 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster_sync();  // barriers initialised in both CTAs before any remote use
+  // barriers initialised in both CTAs before any remote use: the
+  // fence.mbarrier_init.release.cluster above already publishes them, so the
+  // arrive is relaxed (no MEMBAR.GPU / ERRBAR drain in the prologue)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) trace_mark(args.trace, 2);
@@ -1259,11 +1263,8 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           const CUtensorMap* map_b = &args.b[g * args.reduce + r];
           const int s = it % S::kStages;
           const uint32_t phase = (it / S::kStages) & 1;
-          if (it == 0 && lane == 0) trace_mark(args.trace, 12);
           mbar_wait(&empty[s], phase ^ 1);
-          if (it == 0 && lane == 0) trace_mark(args.trace, 13);
           if (leader) mbar_expect_tx_e(&full[s], 2 * (S::kStageA + S::kStageB));
-          if (it == 0 && lane == 0) trace_mark(args.trace, 14);
           if constexpr (kMC) {  // this CTA's 64-row half of the A rows, to both pairs
             if constexpr (kAMN)
               tma_load_2d_pair_mc_e(tiles_a + s * S::kStageA + pid * 8192, map_a, &full[s],
@@ -1278,7 +1279,6 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           } else {
             tma_load_2d_pair_e(tiles_a + s * S::kStageA, map_a, &full[s], kb * kBK, m0);
           }
-          if (it == 0 && lane == 0) trace_mark(args.trace, 15);
           if constexpr (kBMN) {
 #pragma unroll
             for (int j = 0; j < (BN / 2) / 64; ++j)
@@ -1288,7 +1288,6 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
             tma_load_2d_pair_e(tiles_b + s * S::kStageB, map_b, &full[s], kb * kBK, n0);
           }
           if (!leader) remote_arrive_e(full_leader0 + s * 8);
-          if (it == 0 && lane == 0) trace_mark(args.trace, 4);
           if (++kb == kblocks) {
             kb = 0;
             ++r;
@@ -1313,7 +1312,6 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           const int s = it % S::kStages;
           mbar_wait(&full[s], (it / S::kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (it == 0 && lane == 0) trace_mark(args.trace, 5);
           const uint64_t da = da0 + uint64_t(s) * (S::kStageA >> 4);
           const uint64_t db = db0 + uint64_t(s) * (S::kStageB >> 4);
           constexpr uint64_t kAdvA = kAMN ? (16 * 128) >> 4 : 2;

@@ -22,8 +22,7 @@ from paper_2302_02599_b200.runtime import gemm  # noqa: E402
 
 SLOTS = ["entry", "prologue_done", "pdl_wait_done", "first_tma_issued", "first_stage_landed",
          "last_acc_committed", "last_acc_drained", "last_store_issued", "stores_done",
-         "teardown", "exit", "producer_before_empty_wait", "producer_after_empty_wait",
-         "producer_after_expect_tx", "producer_after_a_load"]
+         "teardown", "exit"]
 
 
 def main():
