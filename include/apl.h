@@ -413,13 +413,15 @@ int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, i
 int apl_gemm_force_plan(int pair, int bn, int streamk);
 
 /* Diagnostics: CTA-pair GEMM launches write per-CTA phase timestamps into the
- * device buffer `buf` (16 u64 per CTA: slot 0 %globaltimer at entry, slots
- * 1-11 %clock64 at entry, after the prologue, after griddepcontrol.wait, first
- * TMA issued, first stage landed, last accumulator committed, last accumulator
- * drained, last store issued, bulk stores done, teardown, exit; slots the CTA
- * does not reach stay as they were). NULL turns it off. Not for production
- * launches: every traced launch copies the argument block once more. */
-int apl_gemm_trace(void* buf);
+ * device buffer `buf` of `bytes` bytes (16 u64 per CTA: slot 0 %globaltimer at
+ * entry; slots 1, 2, 3, 6-11 %clock64 at entry, after the prologue, after
+ * griddepcontrol.wait, last accumulator committed, last accumulator drained,
+ * last store issued, bulk stores done, teardown, exit; nothing is stamped
+ * inside the K loop). A launch with more CTAs than `bytes` holds runs
+ * untraced. NULL turns it off. Not for production launches: every traced
+ * launch copies the argument block once more. APL_ERR_ARG when `bytes` is
+ * below one CTA's 128. */
+int apl_gemm_trace(void* buf, size_t bytes);
 
 /* Grouped GEMM, one persistent launch: `groups` output problems, each the
  * sum over `reduce` inputs C_g = epi(sum_r A[g*reduce+r] . B[g*reduce+r]),

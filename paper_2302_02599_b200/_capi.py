@@ -141,7 +141,7 @@ _SIGS = {
     "apl_matmul_strategies": (C.c_int, [P(MeshDesc), P(Meta), P(Meta), C.c_int, C.c_double,
                                         P(StrategyInfoC), C.c_int, P(C.c_int)]),
     "apl_gemm_force_plan": (C.c_int, [C.c_int, C.c_int, C.c_int]),
-    "apl_gemm_trace": (C.c_int, [C.c_void_p]),
+    "apl_gemm_trace": (C.c_int, [C.c_void_p, C.c_size_t]),
     "apl_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                 C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
                                 C.c_int, C.c_void_p]),

@@ -952,8 +952,11 @@ int apl_gemm_force_plan(int pair, int bn, int streamk) {
   });
 }
 
-int apl_gemm_trace(void* buf) {
-  return guarded([&] { apl::gemm_trace(buf); });
+int apl_gemm_trace(void* buf, size_t bytes) {
+  return guarded([&] {
+    need(buf == nullptr || bytes >= 16 * sizeof(uint64_t), "trace buffer smaller than one CTA's slots");
+    apl::gemm_trace(buf, bytes);
+  });
 }
 
 int apl_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,

@@ -628,6 +628,7 @@ struct GemmArgs {
   // diagnostics (apl_gemm_trace): per-CTA timestamps of the kernel's phases,
   // kTraceSlots per CTA; nullptr in normal runs
   unsigned long long* trace;
+  int trace_ctas;  // CTAs the trace buffer holds (kTraceSlots u64 each)
   CUtensorMap cmap[kMaxBatch];
 };
 
@@ -637,7 +638,7 @@ constexpr int kTraceSlots = 16;
 // issuer), last accumulator committed, last accumulator drained by epilogue
 // warp 0, its last store issued, its bulk stores done, teardown start, exit
 __device__ __forceinline__ void trace_mark(unsigned long long* trace, int slot) {
-  if (trace != nullptr) {
+  if (trace != nullptr) {  // launches only trace when the buffer covers the grid
     long long c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
     trace[blockIdx.x * kTraceSlots + slot] = static_cast<unsigned long long>(c);
@@ -1494,6 +1495,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
 
 // apl_gemm_trace's buffer (nullptr: off).
 std::atomic<unsigned long long*> g_trace{nullptr};
+std::atomic<int> g_trace_ctas{0};
 
 // APL_DEBUG=1: say which step of a GEMM launch failed (stderr).
 bool debug_on() {
@@ -1758,9 +1760,10 @@ cudaError_t launch_pair_t(const GemmArgs& args, cudaStream_t stream) {
                                      : std::min(tiles, max_clusters);
   unsigned long long* tr = g_trace.load();
   cudaError_t e;
-  if (tr != nullptr) {
+  if (tr != nullptr && kCS * clusters <= g_trace_ctas.load()) {
     GemmArgs traced = args;
     traced.trace = tr;
+    traced.trace_ctas = g_trace_ctas.load();
     e = launch_gemm_kernel(kernel, kCS * clusters, pair::Cfg<BN>::kBytes, stream, traced);
   } else {
     e = launch_gemm_kernel(kernel, kCS * clusters, pair::Cfg<BN>::kBytes, stream, args);
@@ -2107,8 +2110,12 @@ cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K
 // Force parts of the GEMM plan (-1: automatic): the CTA pair kernel, the N
 // tile, stream-K. For A/B measurements (tools/gemm_bench.py --sweep).
 // Diagnostics: CTA-pair GEMM launches record per-CTA phase timestamps into
-// `buf` (kTraceSlots u64 per CTA; nullptr turns it off).
-void gemm_trace(void* buf) { g_trace.store(static_cast<unsigned long long*>(buf)); }
+// `buf` (kTraceSlots u64 per CTA; nullptr turns it off). A launch whose grid
+// has more CTAs than `bytes` holds runs untraced.
+void gemm_trace(void* buf, size_t bytes) {
+  g_trace_ctas.store(buf ? static_cast<int>(bytes / (kTraceSlots * sizeof(unsigned long long))) : 0);
+  g_trace.store(static_cast<unsigned long long*>(buf));
+}
 
 void gemm_force_plan(int pair, int bn, int streamk) {
   g_force_pair.store(pair);

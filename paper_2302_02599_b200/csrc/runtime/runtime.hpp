@@ -112,7 +112,7 @@ cudaError_t launch_embedding_backward_block(const int64_t* const* ids, const voi
                                             int dtype, cudaStream_t s);
 cudaError_t launch_mask_not(const void* x, void* y, size_t count, cudaStream_t s);
 void gemm_force_plan(int pair, int bn, int streamk);
-void gemm_trace(void* buf);
+void gemm_trace(void* buf, size_t bytes);
 cudaError_t gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                       int ldb, int ldc, bool b_kn, bool out_f32, bool gelu, cudaStream_t stream);
 cudaError_t gemm_bf16_batched(const void* const* A, const void* const* B, void* const* C,

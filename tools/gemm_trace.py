@@ -41,10 +41,10 @@ def main():
         gemm(a, bt, out=c)
     torch.cuda.synchronize()
     buf = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
-    assert lib.apl_gemm_trace(buf.data_ptr()) == 0
+    assert lib.apl_gemm_trace(buf.data_ptr(), buf.numel() * 8) == 0
     gemm(a, bt, out=c)
     torch.cuda.synchronize()
-    lib.apl_gemm_trace(None)
+    lib.apl_gemm_trace(None, 0)
     lib.apl_gemm_force_plan(-1, -1, -1)
     t = buf.view(148, 16).cpu().tolist()
     ctas = [r for r in t if r[1] != 0]
