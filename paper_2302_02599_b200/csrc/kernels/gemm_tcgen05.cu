@@ -1295,6 +1295,13 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
           }
         }
       }
+      // drain: the issuer's stage-release commits land in this CTA's empty
+      // barriers (both CTAs of the pair, and the other pair's with kMC); wait
+      // for the last ones so none is in flight at teardown
+      for (int j = 0; j < S::kStages && j < it; ++j) {
+        const int i2 = it - 1 - j;
+        mbar_wait(&empty[i2 % S::kStages], (i2 / S::kStages) & 1);
+      }
     }
   } else if (warp == 1) {
     if (leader) {  // whole warp walks the schedule, one elected lane issues
@@ -1331,6 +1338,15 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
     const int quarter = warp % 4;
     const int half = (warp - 2) / 4;
     const uint32_t acc_empty_leader = map_to_rank(smem_addr(&acc_empty[0]), pair_leader);
+    // accumulator-release arrivals for this cluster's last two tiles are never
+    // waited on (the MMA issuer waits on tile l-2's before tile l); skipping
+    // them leaves no remote arrive in flight at teardown
+    int ntiles = 0;
+    {
+      SegIter cnt(sk, cluster, clusters, tiles, KT);
+      int a0, a1, a2;
+      while (cnt.next(a0, a1, a2)) ++ntiles;
+    }
     int local = 0;
     uint32_t pphase = 0;  // this warp's stream-K box-load barrier phase
     SegIter seg(sk, cluster, clusters, tiles, KT);
@@ -1458,7 +1474,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) remote_arrive(acc_empty_leader + acc * 8);
+      if (lane == 0 && local + 2 < ntiles) remote_arrive(acc_empty_leader + acc * 8);
       if (partial || head) {
         // all 8 epilogue warps of this CTA finished writing / reading
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
@@ -1480,7 +1496,13 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if (threadIdx.x == 0) trace_mark(args.trace, 10);
-  cluster_sync();  // peer done with our barriers / TMEM before teardown
+  // peer done with our barriers / TMEM before teardown. Relaxed: no remote
+  // operation on shared memory is in flight here (every full-barrier arrive
+  // and stage commit was waited on, the unconsumed accumulator-release
+  // arrivals are skipped), and a release arrive costs MEMBAR.GPU + ERRBAR
+  // (0.5 us per launch, tools/gemm_k_slope.py)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
