@@ -1254,6 +1254,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
       int it = 0;
       SegIter seg(sk, cluster, clusters, tiles, KT);
       int t, k0, k1;
+      if (lane == 0) trace_mark(args.trace, 4);  // producer about to enter its loop
       while (seg.next(t, k0, k1)) {
         const int g = t / per_problem, lt = t % per_problem;
         const int m0 = (lt / n_units) * 2 * kBM + static_cast<int>(rank) * kBM;
@@ -1311,6 +1312,7 @@ __global__ void __cluster_dims__(kMC ? 4 : 2, 1, 1) __launch_bounds__(kThreads, 
       int it = 0, local = 0;
       SegIter seg(sk, cluster, clusters, tiles, KT);
       int t, k0, k1;
+      if (lane == 0) trace_mark(args.trace, 5);  // issuer about to enter its loop
       for (; seg.next(t, k0, k1); ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);

@@ -20,7 +20,7 @@ import torch  # noqa: E402
 from paper_2302_02599_b200 import _capi as A  # noqa: E402
 from paper_2302_02599_b200.runtime import gemm  # noqa: E402
 
-SLOTS = ["entry", "prologue_done", "pdl_wait_done", "first_tma_issued", "first_stage_landed",
+SLOTS = ["entry", "prologue_done", "pdl_wait_done", "producer_loop_entry", "issuer_loop_entry",
          "last_acc_committed", "last_acc_drained", "last_store_issued", "stores_done",
          "teardown", "exit"]
 
