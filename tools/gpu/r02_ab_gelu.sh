@@ -1,3 +1,5 @@
+# Same-box A/B of two builds of libapl.so: ab/libapl_old.so and ab/libapl_new.so
+# (built locally from the two source versions; ab/ is not tracked).
 mkdir -p gpurun_out
 for round in 1 2; do
   for v in old new; do
